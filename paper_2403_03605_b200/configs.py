@@ -1,0 +1,141 @@
+"""Scenario definitions for the PD fine-step path.
+
+Each scenario is a plain dict in the reference's own config vocabulary
+(``[section] key = value``, reference: proj/include/perimts/config.hpp:18-177,
+keys and defaults from proj/include/perimts/scenario.hpp:90-258).  The same
+dict drives three consumers:
+
+* ``render_cfg`` -- text for the reference's ``load_scenario`` (the oracle
+  harness ``oracle/_ref/ref_driver`` and the bench's reference arm);
+* ``paper_2403_03605_b200.scenario.build`` -- the native C++ setup behind the
+  C-ABI (structured mesh, geometry, traction bands, lumped mass, loads);
+* the tests, which pick small members for parity.
+
+BASELINE-only extensions that the reference cannot express (constant
+micromodulus c = 9E/(pi h delta^3) or 18K/(pi delta^4), per-bond s0 factor)
+live under the ``ext`` key and are never rendered into reference configs.
+"""
+from __future__ import annotations
+
+import copy
+import math
+
+# Material shared by BASELINE configs 1-5 (BASELINE.json configs[0]).
+_E = 72e9
+_RHO = 2440.0
+_G0 = 3.8
+
+
+def _plate2d(nx: int, ny: int, dx: float, *, E: float, rho: float, delta_factor: float,
+             l_factor: float, s_crit: float, dt: float, steps: int, m: int = 1,
+             notch=(-0.001, 0.02, 0.05, 0.02), traction: float = 12e6) -> dict:
+    lx, ly = nx * dx, ny * dx
+    return {
+        "mesh": {"kind": "generated", "dim": 2, "bounds": [0.0, 0.0, lx, ly], "spacing": dx,
+                 "notch1": list(notch) if notch else None},
+        "material": {"E": E, "nu": 0.3333333333333333, "rho": rho,
+                     "formulation": "plane_stress"},
+        "pd": {"delta_factor": delta_factor, "l_factor": l_factor, "s_crit": s_crit},
+        "load": {
+            "traction1": [-0.01, ly - 1e-7, lx + 0.01, ly + 1e-7, 0.0, traction],
+            "traction2": [-0.01, -1e-7, lx + 0.01, 1e-7, 0.0, -traction],
+        },
+        "time": {"dt_pd": dt, "m": m, "total_time": dt * m * round(steps / m),
+                 "gamma_pd": 0.5, "beta_pd": 0.0},
+        "run": {"mode": "pure_pd"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+
+
+def s0_2d(E: float, G0: float, delta: float) -> float:
+    """BASELINE cfg1: s0 = sqrt(4 pi G0 / (9 E delta))."""
+    return math.sqrt(4.0 * math.pi * G0 / (9.0 * E * delta))
+
+
+def s0_3d(E: float, nu: float, G0: float, delta: float) -> float:
+    """BASELINE cfg4: s0 = sqrt(5 G0 / (9 K delta)), K = E / (3 (1 - 2 nu))."""
+    K = E / (3.0 * (1.0 - 2.0 * nu))
+    return math.sqrt(5.0 * G0 / (9.0 * K * delta))
+
+
+def scenarios() -> dict:
+    s = {}
+    # Reference-native twin of BASELINE cfg1 (SURVEY.md 8(c) fixture 1):
+    # the shipped branching plate (coarse) run in pure-PD mode.
+    s["bp_coarse"] = _plate2d(200, 80, 5e-4, E=65e9, rho=2235.0, delta_factor=3.03,
+                              l_factor=10.0, s_crit=0.002689, dt=1e-8, steps=6000, m=10)
+    # BASELINE cfg1 analog in the reference's own form (SURVEY.md 8(c) fixture 2):
+    # exponential micromodulus with l = delta, s_crit = s0 from G0.
+    d1 = 3.015 * 5e-4
+    s["cfg1"] = _plate2d(200, 80, 5e-4, E=_E, rho=_RHO, delta_factor=3.015, l_factor=1.0,
+                         s_crit=2.211e-4, dt=2.5e-8, steps=1000)
+    # BASELINE cfg1 with its own constant micromodulus (extension, restatement only).
+    s["cfg1_const"] = copy.deepcopy(s["cfg1"])
+    s["cfg1_const"]["ext"] = {"micromodulus": "constant",
+                              "c": 9.0 * _E / (math.pi * 1e-3 * d1 ** 3), "h": 1e-3}
+    # BASELINE cfg3: 2000 x 800 at 0.05 mm, per-bond s0 factor U[0.95, 1.05].
+    d3 = 3.015 * 5e-5
+    s["cfg3"] = _plate2d(2000, 800, 5e-5, E=_E, rho=_RHO, delta_factor=3.015, l_factor=1.0,
+                         s_crit=round(s0_2d(_E, _G0, d3), 7), dt=5e-9, steps=1000)
+    s["cfg3"]["ext"] = {"micromodulus": "constant",
+                        "c": 9.0 * _E / (math.pi * 1e-3 * d3 ** 3), "h": 1e-3,
+                        "s_crit_spread": 0.05, "seed": 0x5eed5 + 3}
+    # Reference-native analog of cfg3 (exponential kernel, scalar s_crit): the
+    # form the reference arm and the deterministic path run at full size.
+    s["cfg3_native"] = copy.deepcopy(s["cfg3"])
+    s["cfg3_native"]["ext"] = {}
+    # Miniature notched plate of the reference's driver test
+    # (proj/tests/test_driver.cpp:296-333), horizontal tension.
+    mini = _plate2d(40, 16, 1e-3, E=72e9, rho=2235.0, delta_factor=3.03, l_factor=10.0,
+                    s_crit=0.0004, dt=5e-8, steps=80, notch=(0.02, 0.016, 0.02, 0.010))
+    mini["load"] = {"traction1": [-1e-9, -1.0, 1e-9, 1.0, -16e6, 0.0],
+                    "traction2": [0.0399, -1.0, 0.0401, 1.0, 16e6, 0.0]}
+    s["mini"] = mini
+    # Small 3D hex8 block (probe on 20x20x10): tension on top/bottom.
+    d3d = 3.015 * 5e-4
+    blk = {
+        "mesh": {"kind": "generated", "dim": 3, "bounds": [0, 0, 0, 0.005, 0.005, 0.004],
+                 "spacing": 5e-4, "notch1": None},
+        "material": {"E": _E, "nu": 0.25, "rho": _RHO, "formulation": "three_d"},
+        "pd": {"delta_factor": 3.015, "l_factor": 1.0,
+               "s_crit": round(s0_3d(_E, 0.25, _G0, d3d), 7)},
+        "load": {"traction1": [-1, -1, 0.004 - 1e-7, 1, 1, 0.004 + 1e-7, 0, 0, 12e6],
+                 "traction2": [-1, -1, -1e-7, 1, 1, 1e-7, 0, 0, -12e6]},
+        "time": {"dt_pd": 2e-8, "m": 1, "total_time": 2e-8 * 100, "gamma_pd": 0.5,
+                 "beta_pd": 0.0},
+        "run": {"mode": "pure_pd"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+    s["block3d"] = blk
+    return s
+
+
+def get(name: str, **over) -> dict:
+    sc = copy.deepcopy(scenarios()[name])
+    for k, v in over.items():
+        sec, key = k.split(".", 1)
+        sc[sec][key] = v
+    return sc
+
+
+def n_steps(sc: dict) -> int:
+    return int(round(sc["time"]["total_time"] / sc["time"]["dt_pd"]))
+
+
+def render_cfg(sc: dict) -> str:
+    """Reference config text (proj/include/perimts/config.hpp format)."""
+    out = []
+    for sec in ("mesh", "material", "pd", "load", "time", "run", "output"):
+        out.append(f"[{sec}]")
+        for k, v in sc[sec].items():
+            if v is None:
+                continue
+            if isinstance(v, (list, tuple)):
+                v = " ".join(repr(float(x)) for x in v)
+            elif isinstance(v, float):
+                v = repr(v)
+            out.append(f"{k} = {v}")
+        out.append("")
+    return "\n".join(out)
