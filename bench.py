@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark of the PD fine-step hot path (BASELINE.json metric: PD bond-updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+A "step" is one PD fine step (bond gather + break test + velocity-Verlet node
+update) over the whole BASELINE cfg3 plate (2000 x 800 elements, 22,331,624
+bonds, per-bond s0 factor, constant micromodulus), synthetic geometry with
+the config's shapes.  value = unique bonds x K / device time of K steps
+(CUDA events on the handle's stream), max over ranks.  e2e = the same metric
+through the public C-ABI with host buffers: initial state H2D from pinned
+memory, per step the load scale in and the broken count + tracked
+displacements out, final state D2H, timed on the host clock.
+
+--impl reference times the reference's own CPU loop (oracle/_ref/ref_driver,
+compiled from the unmodified reference headers) on all host cores, on a
+bounded sample of the same workload; rank 0 only under torchrun.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PD bond-updates/s (fp64)"
+UNIT = "bond-updates/s"
+REF_SAMPLE = "cfg3_sample"
+REF_FINE_PER_STEP = 1  # reference fine steps per bench step (bounded CPU sample)
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 5 + k and s[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _ncu_traffic():
+    """dram bytes per bond-kernel launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "bond_kernel_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def run_reference_cpu(steps: int, warmup: int, threads: int | None = None) -> dict:
+    """The reference's own loop (ref_driver) on the bounded cfg3 sample."""
+    from oracle import pyoracle as po
+    from paper_2403_03605_b200 import configs as cf
+
+    threads = threads or os.cpu_count() or 1
+    env = dict(os.environ, PERIMTS_WORKERS=str(threads))
+    sc = cf.get(REF_SAMPLE)
+    with tempfile.TemporaryDirectory() as tmp:
+        if os.path.exists(po.REF_DRIVER):
+            r = po.run_ref(cf.render_cfg(sc), tmp, steps=steps + warmup, dump=False,
+                           extra=["--time", "--warmup", str(warmup)], env=env)
+            kind = "reference"
+        else:  # the C restatement (single thread) when the reference could not be built
+            import numpy as np
+
+            from paper_2403_03605_b200.pd import Scenario
+
+            S = Scenario(sc)
+            pairs = po.find_pairs(2, S.centroid, S.volume, S.delta, S.notches())
+            o = po.OraclePD(dict(dim=2, n_nodes=S.n_nodes, conn=S.conn, centroid=S.centroid,
+                                 volume=S.volume, pairs=pairs, mass=S.mass, p_ext=S.p_ext,
+                                 delta=S.delta, l=S.l, c0=S.c0, s_crit=S.s_crit, dt=S.dt),
+                            po.CSR)
+            o.init(0.0)
+            o.step(S.scales(1, warmup))
+            t = time.perf_counter()
+            o.step(S.scales(1 + warmup, steps))
+            dt = time.perf_counter() - t
+            r = {"bond_updates_per_s": len(pairs) * steps / dt, "bonds": len(pairs),
+                 "loop_s": dt, "workers": 1}
+            kind, threads = "port", 1
+    r["kind"] = kind
+    r["threads"] = threads
+    r["sample"] = (f"{REF_SAMPLE}: 500x200 sub-plate of cfg3 (dx 0.05 mm, delta 3.015 dx, "
+                   f"E 72 GPa, 12 MPa bands, exponential kernel l=delta, scalar s_crit), "
+                   f"{steps} timed fine steps after {warmup}, {r['bonds']} bonds")
+    return r
+
+
+def bench_reference(args):
+    rank, _, world = _env_rank()
+    if rank != 0:
+        return
+    fine = args.steps * REF_FINE_PER_STEP
+    r = run_reference_cpu(fine, max(args.warmup, 1) * REF_FINE_PER_STEP)
+    v = r["bond_updates_per_s"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * r["loop_s"] / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 (BASELINE configs[2]) bounded CPU sample",
+                   "sample": r["sample"], "fine_steps_per_step": REF_FINE_PER_STEP},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_native(args):
+    import numpy as np
+
+    from paper_2403_03605_b200 import capi
+    from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200.pd import PDSolver, Scenario
+
+    rank, local, world = _env_rank()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mode = capi.FAST if args.mode == "fast" else capi.DETERMINISTIC
+    sc = Scenario(cf.get(args.workload))
+    t0 = time.perf_counter()
+    s = PDSolver.from_scenario(sc, mode=mode, device=local).find_pe_pairs()
+    t_setup = time.perf_counter() - t0
+    info = s.info()
+    B = info["n_bonds"]
+    K, W = args.steps, args.warmup
+    s.initial_acceleration(sc.load_scale(0.0))
+    step0 = 1
+    s.step(sc.scales(step0, W))
+    step0 += W
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    with Clocks(local) as clk:
+        barrier()
+        ms = s.step_timed(sc.scales(step0, K))  # synchronises the stream on both sides
+        step0 += K
+        barrier()
+        bond_ms, tot_ms = s.profile(sc.scales(step0, K))
+        step0 += K
+    if dist:
+        import torch
+
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * K / (ms * 1e-3)
+
+    # roofline of the dominant (bond) kernel
+    peak, peak_src = _peaks()
+    bond_avg_s = bond_ms * 1e-3 / K
+    achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": _ncu_traffic(),
+            "kernel": "k_fast_bond" if mode == capi.FAST else "k_det_bond",
+            "bytes_per_launch": info["bond_bytes_per_step"], "avg_launch_us": bond_avg_s * 1e6,
+            "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
+
+    # end to end through the public C-ABI with host buffers
+    e2e = None
+    try:
+        import torch
+
+        nd = s.n_dof
+        hu = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+        hv = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+        ha = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+        u0, v0, a0 = s.state()
+        hu[:], hv[:], ha[:] = u0, v0, a0
+        tracked = np.array([2 * (sc.n_nodes // 2) + 1], dtype=np.int32)
+        scales = sc.scales(step0, K)
+        barrier()
+        t = time.perf_counter()
+        s.set_state(hu, hv, ha)
+        for k in range(K):
+            s.step(scales[k:k + 1])
+            s.gather_disp(tracked)
+        u1, v1, a1 = s.state()
+        barrier()
+        e2e_s = time.perf_counter() - t
+        h2d = (3 * nd * 8 + K * 8) / K
+        d2h = (3 * nd * 8 + K * (8 + 8 * len(tracked))) / K
+        e2e = {"value": world * B * K / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / K}
+    except Exception as ex:  # pragma: no cover - reported, never silent
+        e2e = {"value": None, "unit": UNIT, "error": repr(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = run_reference_cpu(args.cpu_steps, 4)
+        cpu = {"value": r["bond_updates_per_s"], "unit": UNIT, "cores": r["threads"],
+               "kind": r["kind"], "sample": r["sample"]}
+
+    if rank == 0:
+        ws = info["device_bytes"] / 1e6
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload} (BASELINE configs[2]: 2000x800 plate, "
+                                   f"dx 0.05 mm, delta 3.015 dx, per-bond s0 x U[0.95,1.05])",
+                       "mode": args.mode, "bonds": B, "elements": sc.n_elems,
+                       "nodes": sc.n_nodes, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 (device working set {ws:.0f} MB > 126 MB)",
+                       "setup_s": t_setup},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": K * info["kernels_per_step"],
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--mode", default="fast", choices=["fast", "det"])
+    ap.add_argument("--cpu-steps", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/* pmts_capi.h -- C ABI of the B200-native PD fine-step path (sm_100a).
+ *
+ * Drop-in boundary for the reference's pure-PD hot path.
+ * The reference is a header-only C++ library with no FFI layer; the calls a
+ * host driver makes on this path are the ones listed beside each entry point
+ * below (paths under /root/reference/proj/include/perimts/).  Plain pointers
+ * and sizes only: no C++ or torch types cross this boundary; no exception
+ * crosses it either -- every entry point returns a status code (errors.hpp
+ * mapping: 2 ConfigError, 3 SolverError, 1 InternalError/CUDA) and
+ * pmts_last_error() holds the message (thread-local).
+ *
+ * Threading: one host thread per handle; each handle owns one CUDA stream and
+ * its device buffers.  Entry points that return host data synchronise that
+ * stream; pmts_pd_step is stream-ordered and returns when the step count
+ * (and the newly-broken count) is known.
+ */
+#ifndef PMTS_CAPI_H
+#define PMTS_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMTS_ABI_VERSION 1
+
+enum pmts_status {
+    PMTS_OK = 0,
+    PMTS_ERR_INTERNAL = 1, /* InternalError / CUDA failure            (errors.hpp:18-21) */
+    PMTS_ERR_CONFIG = 2,   /* ConfigError: bad input                  (errors.hpp:8-11)  */
+    PMTS_ERR_SOLVER = 3    /* SolverError: non-positive mass, non-finite state (errors.hpp:13-16) */
+};
+
+enum pmts_mode {
+    PMTS_DETERMINISTIC = 0, /* reference neighbour order, exact stretch, no FMA: broken set
+                               bit-exact, u/v/a equal to the matrix-free oracle bitwise */
+    PMTS_FAST = 1           /* centroid-averaged eta, squared break test, lattice stencil
+                               families when the mesh is a lattice */
+};
+
+enum pmts_micromodulus {
+    PMTS_MICRO_EXP = 0,  /* c0 exp(-r/l), zero beyond delta  (material.hpp:84-88) */
+    PMTS_MICRO_CONST = 1 /* BASELINE c = 9E/(pi h delta^3) [2D] / 18K/(pi delta^4) [3D], applied
+                            in PeriFEM form c h / r^3 [2D] or c / r^3 [3D]  (extension) */
+};
+
+/* ------------------------------------------------------------------------
+ * Scenario setup -- the host side of build_scenario (driver.hpp:170-231),
+ * convert_tractions_to_bands (driver.hpp:76-116), generate_structured +
+ * compute_element_geometry (mesh.hpp:112-219), calibrate_c0
+ * (material.hpp:150-165) and the M / P_ext part of assemble_pd_global
+ * (perifem.hpp:331-349) for a generated pure-PD run.  Arrays are owned by the
+ * scenario and stay valid until pmts_scenario_destroy.
+ * ------------------------------------------------------------------------ */
+typedef struct pmts_scenario pmts_scenario;
+
+typedef struct {
+    int32_t dim;                 /* 2 or 3 */
+    double lo[3], hi[3];         /* mesh.bounds */
+    double spacing;              /* mesh.spacing */
+    double E, nu, rho;           /* [material] */
+    int32_t formulation;         /* 0 plane_stress, 1 plane_strain, 2 three_d */
+    double delta_factor, l_factor, s_crit; /* [pd] */
+    int32_t n_notch;             /* notches: npts[k] points each, xyz */
+    const int32_t* notch_npts;
+    const double* notch_pts;
+    int32_t n_traction;          /* per patch: lo[3] hi[3] value[3] (9 doubles) */
+    const double* traction;
+    int32_t n_body_patch;        /* per patch: lo[3] hi[3] value[3] */
+    const double* body_patch;
+    double body_force[3];
+    int32_t n_velocity_bc;       /* per bc: lo[3] hi[3] component value (8 doubles) */
+    const double* velocity_bc;
+    int32_t n_fixed;             /* per box: lo[3] hi[3] (6 doubles) */
+    const double* fixed;
+    double dt_pd;                /* [time] */
+    int32_t m;
+    double total_time;
+    double load_ramp;            /* < 0: auto (= m dt_pd), driver.hpp:187-191 */
+    double gamma, beta;
+} pmts_scenario_desc;
+
+typedef struct {
+    int32_t dim, n_nodes, n_elems, n_dof, n_bc, n_steps;
+    int32_t lattice[3];          /* elements per axis of the generated grid */
+    double delta, l, c0, char_length, dt, gamma, beta, s_crit, load_ramp;
+    const double* node_xyz;      /* [n_nodes][3] */
+    const int32_t* elem_nodes;   /* [n_elems][2^dim], reference node order */
+    const double* centroid;      /* [n_elems][3] */
+    const double* volume;        /* [n_elems] */
+    const double* mass;          /* [n_dof] lumped, (1-alpha)-weighted (alpha = 0) */
+    const double* p_ext;         /* [n_dof] full-amplitude external load */
+    const int32_t* bc_dofs;      /* [n_bc] sorted */
+    const double* bc_vel;        /* [n_bc] */
+} pmts_scenario_view;
+
+int pmts_scenario_build(const pmts_scenario_desc* desc, pmts_scenario** out);
+int pmts_scenario_get(const pmts_scenario* sc, pmts_scenario_view* view);
+/* load_scale(t) = clamp(t / ramp, 0, 1)  (driver.hpp:187-191) */
+double pmts_scenario_load_scale(const pmts_scenario* sc, double t);
+void pmts_scenario_destroy(pmts_scenario* sc);
+
+/* ------------------------------------------------------------------------
+ * PD fine-step handle
+ * ------------------------------------------------------------------------ */
+typedef struct pmts_pd pmts_pd;
+
+typedef struct {
+    int32_t dim, n_nodes, n_elems;
+    const double* node_xyz;      /* [n_nodes][3] */
+    const int32_t* elem_nodes;   /* [n_elems][2^dim] (mesh.hpp:206-213 order) */
+    const double* mass;          /* [n_nodes*dim], dof = node*dim + c (fem.hpp:381-409) */
+    const double* p_ext;         /* [n_nodes*dim] */
+    int32_t n_bc;                /* BcTable (fem.hpp:477-482): sorted dofs + velocities */
+    const int32_t* bc_dofs;
+    const double* bc_vel;
+    double delta;                /* horizon */
+    int32_t micromodulus;        /* enum pmts_micromodulus */
+    double c0, l;                /* exponential kernel */
+    double c_const, h;           /* constant kernel (h: plate thickness, 2D) */
+    double s_crit;               /* <= 0: fracture off (material.hpp:44) */
+    double s_crit_spread;        /* per-bond factor U[1-spread, 1+spread] (extension), 0 = off */
+    uint64_t seed;               /* counter-hash seed of the per-bond factor */
+    double gamma, beta, dt;      /* NewmarkParams (newmark.hpp:14-30); beta must be 0 */
+    int32_t mode;                /* enum pmts_mode */
+    int32_t device;              /* CUDA ordinal */
+    int32_t n_notch;             /* notches (mesh.hpp:316-318) for pmts_pd_build_families */
+    const int32_t* notch_npts;
+    const double* notch_pts;
+    int32_t lattice[3];          /* optional: elements per axis if the mesh is the generated
+                                    lattice (enables the stencil fast path); 0 = unknown */
+} pmts_pd_desc;
+
+typedef struct {
+    int64_t n_bonds;             /* unique bonds B */
+    int64_t n_entries;           /* directed family entries F = 2B */
+    int32_t max_family;          /* largest family */
+    int32_t path;                /* 0 CSR/ELL families, 1 lattice stencil */
+    int32_t kernels_per_step;    /* kernel launches per fine step */
+    int32_t stencil_size;        /* stencil offsets (path 1) */
+    double bytes_per_step;       /* algorithmic HBM bytes per fine step */
+    double bond_bytes_per_step;  /* ... of which the bond kernel (roofline numerator) */
+    double device_bytes;         /* device memory held by the handle */
+} pmts_pd_info;
+
+const char* pmts_last_error(void);
+int pmts_abi_version(void);
+int pmts_device_count(int* n);
+
+/* BlockOperator ctor validation (newmark.hpp:81-93) + device upload + element
+ * geometry (mesh.hpp:112-139) and bond constants (perifem.hpp:87-97). */
+int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out);
+void pmts_pd_destroy(pmts_pd* h);
+
+/* find_pe_pairs (mesh.hpp:416-495) on the device: cell list of size delta,
+ * notch cut with eps = 1e-12 * char_length, families sorted by partner id. */
+int pmts_pd_build_families(pmts_pd* h);
+/* Inject an explicit pair list instead ((i<j) rows sorted, as find_pe_pairs
+ * returns them) -- e.g. the reference's own list. */
+int pmts_pd_set_pairs(pmts_pd* h, int64_t n_pairs, const int32_t* pairs);
+/* Pair list back in find_pe_pairs order ((i,j) rows, i<j, sorted). */
+int pmts_pd_get_pairs(pmts_pd* h, int32_t* pairs_out, int64_t cap, int64_t* n_out);
+int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info);
+
+/* initial_acceleration (newmark.hpp:110-116): a0 = (P scale0 - K u0) / M. */
+int pmts_pd_init(pmts_pd* h, double scale0);
+/* n fused fine steps: per step k, p_t = P_ext * load_scale[k]; explicit
+ * Newmark step (advance_dynamic_step, newmark.hpp:185-190 / 122-159);
+ * inclusive break test s >= s_crit on the new displacement
+ * (update_bond_states, perifem.hpp:170-193; the K downdate of
+ * perifem.hpp:356-364 is implicit in the matrix-free force).
+ * n_broken_out (optional): bonds newly broken over the n steps. */
+int pmts_pd_step(pmts_pd* h, int32_t n, const double* load_scale, int64_t* n_broken_out);
+/* Same, timed on the handle's stream with CUDA events (device ms). */
+int pmts_pd_step_timed(pmts_pd* h, int32_t n, const double* load_scale, float* ms_out);
+/* Per-kernel device time of the dominant (bond) kernel over n steps, with
+ * CUDA events around each of its launches (ms summed) -- roofline input. */
+int pmts_pd_profile(pmts_pd* h, int32_t n, const double* load_scale, float* bond_ms,
+                    float* total_ms);
+
+int pmts_pd_get_state(pmts_pd* h, double* u, double* v, double* a);
+int pmts_pd_set_state(pmts_pd* h, const double* u, const double* v, const double* a);
+/* Intact flag per pair of pmts_pd_get_pairs order (1 intact, 0 broken). */
+int pmts_pd_get_intact(pmts_pd* h, uint8_t* intact_out, int64_t cap);
+/* Break log: (step, i, j) rows of bonds broken since the last call, sorted by
+ * (step, i, j) -- the (pe, qp) order of update_bond_states.  Steps count from
+ * the handle's creation (1-based). */
+int pmts_pd_take_break_log(pmts_pd* h, int32_t* rows_out, int64_t cap, int64_t* n_out);
+int64_t pmts_pd_broken_total(pmts_pd* h);
+/* damage_field (perifem.hpp:202-231). */
+int pmts_pd_damage(pmts_pd* h, double* elem_out, double* node_out);
+/* Gather a few dofs of the current displacement (tracked points,
+ * driver_run.hpp:41-47) into host memory. */
+int pmts_pd_gather_disp(pmts_pd* h, int32_t n, const int32_t* dofs, double* out);
+/* cudaStream_t of the handle (as void*) for callers that time on it. */
+void* pmts_pd_stream(pmts_pd* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -649,3 +649,19 @@ void po_pd_damage(const po_pd* h, double* elem, double* node) {
     free(intact);
     free(count);
 }
+
+/* update_bond_states (perifem.hpp:170-193) on an explicit displacement */
+int64_t po_pd_update_bond_states(po_pd* h, const double* u, int32_t* out, int64_t cap) {
+    int64_t n = 0;
+    for (int64_t q = 0; q < h->n_pairs; ++q) {
+        if (!h->mu[q]) continue;
+        if (stretch_q(h, q, u) >= h->scrit[q]) {
+            h->mu[q] = 0;
+            if (out && n < cap) out[n] = (int32_t)q;
+            ++n;
+        }
+    }
+    return n;
+}
+
+void po_pd_set_mu(po_pd* h, const uint8_t* mu) { memcpy(h->mu, mu, (size_t)h->n_pairs); }

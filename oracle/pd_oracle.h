@@ -62,6 +62,9 @@ double po_bond_s_crit(double s_crit, double spread, uint64_t seed, int32_t i, in
 /* perifem.hpp:144-166 for one pair (i<j) on displacement u */
 double po_bond_stretch(const po_pd* h, int64_t pair, const double* u);
 int64_t po_pd_nnz(const po_pd* h);
+/* update_bond_states (perifem.hpp:170-193) on u; returns newly broken pairs */
+int64_t po_pd_update_bond_states(po_pd* h, const double* u, int32_t* out, int64_t cap);
+void po_pd_set_mu(po_pd* h, const uint8_t* mu);
 
 #ifdef __cplusplus
 }

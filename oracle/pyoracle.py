@@ -54,6 +54,9 @@ def lib():
         L.po_bond_stretch.argtypes = [p, C.c_int64, p]
         L.po_pd_nnz.restype = C.c_int64
         L.po_pd_nnz.argtypes = [p]
+        L.po_pd_update_bond_states.restype = C.c_int64
+        L.po_pd_update_bond_states.argtypes = [p, p, p, C.c_int64]
+        L.po_pd_set_mu.argtypes = [p, p]
         _lib = L
     return _lib
 
@@ -168,6 +171,16 @@ class OraclePD:
 
     def nnz(self):
         return lib().po_pd_nnz(self.h)
+
+    def update_bond_states(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(max(self.n_pairs, 1), dtype=np.int32)
+        n = lib().po_pd_update_bond_states(self.h, _p(u), _p(out), self.n_pairs)
+        return out[:n].copy()
+
+    def set_mu(self, mu):
+        m = np.ascontiguousarray(mu, dtype=np.uint8)
+        lib().po_pd_set_mu(self.h, _p(m))
 
 
 def load_ref_dump(d: str) -> dict:

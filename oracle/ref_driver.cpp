@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
     std::string cfg_path = argv[1], dump_dir;
     std::vector<std::string> overrides;
     std::vector<int> checkpoints;
-    int steps_override = -1;
+    int steps_override = -1, warmup = 0;
     bool time_only = false, setup_only = false;
     for (int a = 2; a < argc; ++a) {
         std::string s = argv[a];
@@ -75,6 +75,7 @@ int main(int argc, char** argv) {
         else if (s == "--checkpoints" && a + 1 < argc) checkpoints = parse_list(argv[++a]);
         else if (s == "--time") time_only = true;
         else if (s == "--setup-only") setup_only = true;
+        else if (s == "--warmup" && a + 1 < argc) warmup = std::atoi(argv[++a]);
         else {
             std::fprintf(stderr, "unknown argument %s\n", s.c_str());
             return 2;
@@ -179,8 +180,9 @@ int main(int argc, char** argv) {
         std::size_t broken_total = 0;
         double t_k = 0.0, t_u = 0.0;
         Vector warm;
-        const double t_loop0 = now_s();
+        double t_loop0 = now_s();
         for (int i = 1; i <= n_steps; ++i) {
+            if (i == warmup + 1) t_loop0 = now_s();  // steps 1..warmup untimed
             const double t = i * b.sc.dt_pd;
             const double tick = now_s();
             Vector p_t = sys.P_ext;
@@ -224,12 +226,12 @@ int main(int argc, char** argv) {
             dump_vec(dump_dir + "/damage_node.f64", dmg.node);
         }
         const double bonds = double(pairs.size());
-        std::printf("{\"steps\": %d, \"bonds\": %zu, \"nnz\": %d, \"setup_s\": %.6f, "
-                    "\"loop_s\": %.6f, \"t_k_s\": %.6f, \"t_u_s\": %.6f, "
+        const int timed = n_steps - std::min(warmup, n_steps);
+        std::printf("{\"steps\": %d, \"warmup\": %d, \"bonds\": %zu, \"nnz\": %d, "
+                    "\"setup_s\": %.6f, \"loop_s\": %.6f, \"t_k_s\": %.6f, \"t_u_s\": %.6f, "
                     "\"bond_updates_per_s\": %.6e, \"workers\": %d, \"broken\": %zu}\n",
-                    n_steps, pairs.size(), sys.K.nnz(), t_setup, t_loop, t_k, t_u,
-                    n_steps > 0 ? bonds * n_steps / t_loop : 0.0, worker_count(),
-                    broken_total);
+                    n_steps, warmup, pairs.size(), sys.K.nnz(), t_setup, t_loop, t_k, t_u,
+                    timed > 0 ? bonds * timed / t_loop : 0.0, worker_count(), broken_total);
     } catch (const ConfigError& e) {
         std::fprintf(stderr, "config error: %s\n", e.what());
         return 2;

@@ -1,0 +1,132 @@
+"""ctypes binding of include/pmts_capi.h (libpmts.so, built in-tree for sm_100a).
+
+This is the Python side of the C-ABI boundary: the structs mirror the header
+field for field, every call returns the header's status code and a failed call
+raises the exception class the reference would have thrown (errors.hpp:8-21).
+There is no fallback: if the library is missing, importing this module fails.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libpmts.so")
+
+PMTS_OK, PMTS_ERR_INTERNAL, PMTS_ERR_CONFIG, PMTS_ERR_SOLVER = 0, 1, 2, 3
+DETERMINISTIC, FAST = 0, 1
+MICRO_EXP, MICRO_CONST = 0, 1
+
+
+class PmtsError(RuntimeError):
+    """InternalError / CUDA failure (status 1)."""
+
+
+class ConfigError(PmtsError):
+    """ConfigError (status 2)."""
+
+
+class SolverError(PmtsError):
+    """SolverError (status 3)."""
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int32
+
+
+class ScenarioDesc(C.Structure):
+    _fields_ = [("dim", _I), ("lo", _D * 3), ("hi", _D * 3), ("spacing", _D), ("E", _D),
+                ("nu", _D), ("rho", _D), ("formulation", _I), ("delta_factor", _D),
+                ("l_factor", _D), ("s_crit", _D), ("n_notch", _I), ("notch_npts", _P),
+                ("notch_pts", _P), ("n_traction", _I), ("traction", _P),
+                ("n_body_patch", _I), ("body_patch", _P), ("body_force", _D * 3),
+                ("n_velocity_bc", _I), ("velocity_bc", _P), ("n_fixed", _I), ("fixed", _P),
+                ("dt_pd", _D), ("m", _I), ("total_time", _D), ("load_ramp", _D),
+                ("gamma", _D), ("beta", _D)]
+
+
+class ScenarioView(C.Structure):
+    _fields_ = [("dim", _I), ("n_nodes", _I), ("n_elems", _I), ("n_dof", _I), ("n_bc", _I),
+                ("n_steps", _I), ("lattice", _I * 3), ("delta", _D), ("l", _D), ("c0", _D),
+                ("char_length", _D), ("dt", _D), ("gamma", _D), ("beta", _D), ("s_crit", _D),
+                ("load_ramp", _D), ("node_xyz", _P), ("elem_nodes", _P), ("centroid", _P),
+                ("volume", _P), ("mass", _P), ("p_ext", _P), ("bc_dofs", _P), ("bc_vel", _P)]
+
+
+class PDDesc(C.Structure):
+    _fields_ = [("dim", _I), ("n_nodes", _I), ("n_elems", _I), ("node_xyz", _P),
+                ("elem_nodes", _P), ("mass", _P), ("p_ext", _P), ("n_bc", _I),
+                ("bc_dofs", _P), ("bc_vel", _P), ("delta", _D), ("micromodulus", _I),
+                ("c0", _D), ("l", _D), ("c_const", _D), ("h", _D), ("s_crit", _D),
+                ("s_crit_spread", _D), ("seed", C.c_uint64), ("gamma", _D), ("beta", _D),
+                ("dt", _D), ("mode", _I), ("device", _I), ("n_notch", _I),
+                ("notch_npts", _P), ("notch_pts", _P), ("lattice", _I * 3)]
+
+
+class PDInfo(C.Structure):
+    _fields_ = [("n_bonds", C.c_int64), ("n_entries", C.c_int64), ("max_family", _I),
+                ("path", _I), ("kernels_per_step", _I), ("stencil_size", _I),
+                ("bytes_per_step", _D), ("bond_bytes_per_step", _D),
+                ("device_bytes", _D)]
+
+
+# exported symbols, with ctypes signatures: the CPU test checks the library
+# exports every one of them (and the header declares the same set).
+SIGNATURES = {
+    "pmts_last_error": (C.c_char_p, []),
+    "pmts_abi_version": (C.c_int, []),
+    "pmts_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "pmts_scenario_build": (C.c_int, [C.POINTER(ScenarioDesc), C.POINTER(_P)]),
+    "pmts_scenario_get": (C.c_int, [_P, C.POINTER(ScenarioView)]),
+    "pmts_scenario_load_scale": (_D, [_P, _D]),
+    "pmts_scenario_destroy": (None, [_P]),
+    "pmts_pd_create": (C.c_int, [C.POINTER(PDDesc), C.POINTER(_P)]),
+    "pmts_pd_destroy": (None, [_P]),
+    "pmts_pd_build_families": (C.c_int, [_P]),
+    "pmts_pd_set_pairs": (C.c_int, [_P, C.c_int64, _P]),
+    "pmts_pd_get_pairs": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "pmts_pd_info_get": (C.c_int, [_P, C.POINTER(PDInfo)]),
+    "pmts_pd_init": (C.c_int, [_P, _D]),
+    "pmts_pd_step": (C.c_int, [_P, _I, _P, C.POINTER(C.c_int64)]),
+    "pmts_pd_step_timed": (C.c_int, [_P, _I, _P, C.POINTER(C.c_float)]),
+    "pmts_pd_profile": (C.c_int, [_P, _I, _P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "pmts_pd_get_state": (C.c_int, [_P, _P, _P, _P]),
+    "pmts_pd_set_state": (C.c_int, [_P, _P, _P, _P]),
+    "pmts_pd_get_intact": (C.c_int, [_P, _P, C.c_int64]),
+    "pmts_pd_take_break_log": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "pmts_pd_broken_total": (C.c_int64, [_P]),
+    "pmts_pd_damage": (C.c_int, [_P, _P, _P]),
+    "pmts_pd_gather_disp": (C.c_int, [_P, _I, _P, _P]),
+    "pmts_pd_stream": (_P, [_P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libpmts.so (in-tree).  Raises if it is missing -- no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status == PMTS_OK:
+        return
+    msg = lib().pmts_last_error().decode(errors="replace")
+    cls = {PMTS_ERR_CONFIG: ConfigError, PMTS_ERR_SOLVER: SolverError}.get(status, PmtsError)
+    raise cls(msg or f"pmts status {status}")
+
+
+def ptr(a):
+    """numpy array -> void* (None passes NULL)."""
+    return None if a is None else a.ctypes.data_as(_P)

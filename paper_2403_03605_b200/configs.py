@@ -85,6 +85,12 @@ def scenarios() -> dict:
     # form the reference arm and the deterministic path run at full size.
     s["cfg3_native"] = copy.deepcopy(s["cfg3"])
     s["cfg3_native"]["ext"] = {}
+    # Bounded CPU sample of cfg3 for the reference arm / cpu_baseline: the same
+    # dx, horizon, material and loading on a 500 x 200 sub-plate (25 x 10 mm,
+    # notch scaled to the same fraction), reference-native kernel.
+    s["cfg3_sample"] = _plate2d(500, 200, 5e-5, E=_E, rho=_RHO, delta_factor=3.015,
+                                l_factor=1.0, s_crit=s["cfg3"]["pd"]["s_crit"], dt=5e-9,
+                                steps=1000, notch=(-0.00025, 0.005, 0.0125, 0.005))
     # Miniature notched plate of the reference's driver test
     # (proj/tests/test_driver.cpp:296-333), horizontal tension.
     mini = _plate2d(40, 16, 1e-3, E=72e9, rho=2235.0, delta_factor=3.03, l_factor=10.0,

@@ -1,0 +1,53 @@
+// Internal helpers shared by the host translation units of libpmts.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/pmts_capi.h"
+
+namespace pmts {
+
+// Exception types mirror the reference's (errors.hpp:8-21); they never cross
+// the C ABI -- guard() maps them onto status codes.
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct SolverError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct InternalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        set_last_error("");
+        return PMTS_OK;
+    } catch (const ConfigError& e) {
+        set_last_error(e.what());
+        return PMTS_ERR_CONFIG;
+    } catch (const SolverError& e) {
+        set_last_error(e.what());
+        return PMTS_ERR_SOLVER;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return PMTS_ERR_INTERNAL;
+    } catch (...) {
+        set_last_error("unknown error");
+        return PMTS_ERR_INTERNAL;
+    }
+}
+
+// Bit-exact host restatements used by both the setup and the PD handle.
+void element_geometry(int dim, int n_elems, const int32_t* conn, const double* nodes,
+                      double* centroid, double* volume);
+double char_length(int dim, int n_elems, const double* volume);
+double calibrate_c0(double E, double delta, double l, int formulation);
+
+}  // namespace pmts

@@ -1,0 +1,600 @@
+// Host orchestration of the PD fine-step handle behind include/pmts_capi.h.
+//
+// One handle = one CUDA stream + device-resident mesh, families, bond state
+// and kinematics.  The per-step work is two (deterministic) or three (fast)
+// kernel launches -- bond gather, node update (+ fused predictor) -- replayed
+// from a CUDA graph per step batch.  Citations: /root/reference/proj/include/
+// perimts/<file>:<line>.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pd_common.cuh"
+#include "pmts_internal.h"
+
+using namespace pmts;
+
+#define CK(x)                                                                           \
+    do {                                                                                \
+        cudaError_t err_ = (x);                                                         \
+        if (err_ != cudaSuccess)                                                        \
+            throw InternalError(std::string("CUDA: ") + cudaGetErrorString(err_) + " (" + \
+                                #x + ")");                                              \
+    } while (0)
+
+namespace {
+
+template <class T>
+T* dalloc(size_t n, double& bytes) {
+    T* p = nullptr;
+    const size_t b = sizeof(T) * std::max<size_t>(n, 1);
+    CK(cudaMalloc(&p, b));
+    bytes += double(b);
+    return p;
+}
+
+template <class T>
+void upload(T* d, const T* h, size_t n, cudaStream_t s) {
+    if (n) CK(cudaMemcpyAsync(d, h, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+}
+
+template <class T>
+void download(T* h, const T* d, size_t n, cudaStream_t s) {
+    if (n) CK(cudaMemcpyAsync(h, d, sizeof(T) * n, cudaMemcpyDeviceToHost, s));
+}
+
+}  // namespace
+
+struct pmts_pd {
+    pmts_pd_desc desc{};
+    int dim = 2, nn = 4, E = 0, N = 0, ndof = 0, mode = 0;
+    cudaStream_t stream = nullptr;
+    DevPD d{};
+    double device_bytes = 0.0;
+    // host copies of the setup
+    std::vector<int32_t> conn;       // element-major
+    std::vector<double> cen, vol;    // cen element-major (xyz)
+    std::vector<double> notch_pts;
+    std::vector<int32_t> notch_npts;
+    double cl = 0.0, eps = 0.0, lo[3] = {0, 0, 0};
+    bool fracture = false, families = false;
+    std::vector<int32_t> hcol;       // K x E
+    int64_t n_entries = 0;
+    int64_t gstep = 0;               // fine steps taken since creation
+    int64_t broken_total = 0;
+    // device scratch
+    unsigned long long* d_counts = nullptr;
+    int counts_cap = 0;
+    unsigned long long* d_log_n = nullptr;
+    int32_t* d_log = nullptr;
+    std::vector<void*> owned;
+
+    ~pmts_pd() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : owned) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    template <class T>
+    T* alloc(size_t n) {
+        T* p = dalloc<T>(n, device_bytes);
+        owned.push_back(p);
+        return p;
+    }
+    void release(void* p) {
+        if (!p) return;
+        auto it = std::find(owned.begin(), owned.end(), p);
+        if (it != owned.end()) owned.erase(it);
+        cudaFree(p);
+    }
+};
+
+namespace {
+
+// micromodulus (material.hpp:84-88) or the BASELINE constant form (extension)
+double micromodulus(const pmts_pd_desc& dsc, int dim, double r) {
+    if (r <= 0.0) throw ConfigError("micromodulus needs |xi| > 0");
+    if (r > dsc.delta) return 0.0;
+    if (dsc.micromodulus == PMTS_MICRO_CONST) {
+        const double r3 = (r * r) * r;
+        return (dim == 2 ? dsc.c_const * dsc.h : dsc.c_const) / r3;
+    }
+    return dsc.c0 * std::exp(-r / dsc.l);
+}
+
+// Family tables from the ELL partner list: per directed entry w c(|xi|)
+// computed on the host exactly as scatter_pe_block forms it
+// (perifem.hpp:247: coeff * weight * c with coeff = 1, weight = V_i V_j
+// from build_peri_elements perifem.hpp:92-95); intact bits all set.
+void finish_families(pmts_pd* h, int K) {
+    const int E = h->E;
+    h->d.K = K;
+    h->d.W = std::max(1, (K + 31) / 32);
+    std::vector<double> coef((size_t)K * E, 0.0);
+    std::vector<uint32_t> mask((size_t)h->d.W * E, 0u);
+    int64_t F = 0;
+    for (int e = 0; e < E; ++e)
+        for (int k = 0; k < K; ++k) {
+            const int p = h->hcol[(size_t)k * E + e];
+            if (p < 0) break;
+            const int i = std::min(e, p), j = std::max(e, p);
+            double xi[3];
+            for (int c = 0; c < 3; ++c) xi[c] = h->cen[3 * (size_t)j + c] - h->cen[3 * (size_t)i + c];
+            const double xin = std::sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+            if (xin <= 0.0) throw ConfigError("degenerate bond: coincident quadrature points");
+            const double w = h->vol[i] * h->vol[j];
+            const double c = micromodulus(h->desc, h->dim, xin);
+            coef[(size_t)k * E + e] = c * w;
+            mask[(size_t)(k >> 5) * E + e] |= 1u << (k & 31);
+            ++F;
+        }
+    h->n_entries = F;
+    if (h->d.coef) h->release((void*)h->d.coef);
+    if (h->d.mask) h->release(h->d.mask);
+    if (h->d.col) h->release((void*)h->d.col);
+    int32_t* col = h->alloc<int32_t>((size_t)K * E);
+    double* dcoef = h->alloc<double>((size_t)K * E);
+    uint32_t* dmask = h->alloc<uint32_t>((size_t)h->d.W * E);
+    upload(col, h->hcol.data(), (size_t)K * E, h->stream);
+    upload(dcoef, coef.data(), (size_t)K * E, h->stream);
+    upload(dmask, mask.data(), (size_t)h->d.W * E, h->stream);
+    h->d.col = col;
+    h->d.coef = dcoef;
+    h->d.mask = dmask;
+    if (h->mode == PMTS_DETERMINISTIC) {
+        if (h->d_log) h->release(h->d_log);
+        h->d_log = h->alloc<int32_t>(3 * (size_t)(F / 2 + 1));
+        h->d.log = h->d_log;
+        h->d.log_cap = F / 2 + 1;
+        CK(cudaMemsetAsync(h->d_log_n, 0, sizeof(unsigned long long), h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    h->families = true;
+}
+
+void require_families(pmts_pd* h) {
+    if (!h->families)
+        throw ConfigError("families not built: call pmts_pd_build_families or pmts_pd_set_pairs");
+}
+
+void ensure_counts(pmts_pd* h, int n) {
+    if (n > h->counts_cap) {
+        if (h->d_counts) h->release(h->d_counts);
+        h->counts_cap = std::max(n, 64);
+        h->d_counts = h->alloc<unsigned long long>(h->counts_cap);
+    }
+    CK(cudaMemsetAsync(h->d_counts, 0, sizeof(unsigned long long) * n, h->stream));
+    h->d.broken_count = h->d_counts;
+}
+
+// one fine step: bond gather + node update with the fused predictor
+void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev) {
+    const int brk = h->fracture ? 1 : 0;
+    if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
+    if (h->mode == PMTS_DETERMINISTIC) {
+        launch_det_bond(h->d, h->d.rd, slot, brk, int(h->gstep + slot + 1), h->stream);
+    } else {
+        launch_fast_ubar(h->d, h->stream);
+        launch_fast_bond(h->d, slot, brk, h->stream);
+    }
+    if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
+    launch_node_update(h->d, scale, 1, h->stream);
+}
+
+int64_t finish_steps(pmts_pd* h, int n) {
+    std::vector<unsigned long long> cnt(n);
+    download(cnt.data(), h->d_counts, n, h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+    int64_t nb = 0;
+    for (auto c : cnt) nb += (int64_t)c;
+    h->gstep += n;
+    h->broken_total += nb;
+    return nb;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmts_device_count(int* n) {
+    return guard([&] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+        *n = c;
+    });
+}
+
+int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
+    return guard([&] {
+        if (!desc || !out) throw ConfigError("null argument");
+        const pmts_pd_desc& ds = *desc;
+        if (ds.dim != 2 && ds.dim != 3) throw ConfigError("dim must be 2 or 3");
+        if (ds.n_nodes <= 0 || ds.n_elems <= 0) throw ConfigError("empty mesh");
+        if (!ds.node_xyz || !ds.elem_nodes || !ds.mass || !ds.p_ext)
+            throw ConfigError("missing mesh, mass or load array");
+        if (ds.dt <= 0.0) throw ConfigError("time step must be positive");
+        if (ds.beta != 0.0)
+            throw ConfigError("the device fine step is the explicit Newmark branch (beta_pd = 0); "
+                              "implicit PD is out of scope (DESIGN.md)");
+        if (ds.delta <= 0.0) throw ConfigError("horizon must be positive");
+        if (ds.micromodulus == PMTS_MICRO_EXP && (ds.l <= 0.0 || ds.l > ds.delta || ds.c0 <= 0.0))
+            throw ConfigError("exponential micromodulus needs 0 < l <= delta and c0 > 0");
+        if (ds.micromodulus == PMTS_MICRO_CONST && ds.c_const <= 0.0)
+            throw ConfigError("constant micromodulus needs c > 0");
+        if (ds.mode != PMTS_DETERMINISTIC && ds.mode != PMTS_FAST)
+            throw ConfigError("mode must be PMTS_DETERMINISTIC or PMTS_FAST");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw InternalError("no CUDA device: the PD fine step has no CPU fallback");
+        if (ds.device < 0 || ds.device >= ndev) throw ConfigError("device ordinal out of range");
+        CK(cudaSetDevice(ds.device));
+
+        auto h = std::make_unique<pmts_pd>();
+        h->desc = ds;
+        h->dim = ds.dim;
+        h->nn = ds.dim == 2 ? 4 : 8;
+        h->E = ds.n_elems;
+        h->N = ds.n_nodes;
+        h->ndof = ds.n_nodes * ds.dim;
+        h->mode = ds.mode;
+        h->fracture = ds.s_crit > 0.0 && std::isfinite(ds.s_crit);  // material.hpp:44
+        const int E = h->E, N = h->N, nn = h->nn, dim = h->dim;
+        h->conn.assign(ds.elem_nodes, ds.elem_nodes + (size_t)E * nn);
+        for (int32_t v : h->conn)
+            if (v < 0 || v >= N) throw ConfigError("element references a missing node");
+        // BcTable + mass positivity (newmark.hpp:81-93)
+        std::vector<uint8_t> bcflag(h->ndof, 0);
+        std::vector<double> bcvel(h->ndof, 0.0);
+        for (int c = 0; c < ds.n_bc; ++c) {
+            const int dof = ds.bc_dofs[c];
+            if (dof < 0 || dof >= h->ndof) throw ConfigError("BC dof out of range");
+            bcflag[dof] = 1;
+            bcvel[dof] = ds.bc_vel[c];
+        }
+        for (int i = 0; i < h->ndof; ++i)
+            if (!bcflag[i] && !(ds.mass[i] > 0.0))
+                throw SolverError("non-positive lumped mass at dof " + std::to_string(i));
+        // geometry (mesh.hpp:112-139), host restatement, bit-exact
+        h->cen.resize(3 * (size_t)E);
+        h->vol.resize(E);
+        element_geometry(dim, E, h->conn.data(), ds.node_xyz, h->cen.data(), h->vol.data());
+        h->cl = char_length(dim, E, h->vol.data());
+        h->eps = 1e-12 * std::max(h->cl, 1e-300);  // mesh.hpp:435
+        for (int k = 0; k < 3; ++k) h->lo[k] = 1e300;
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < 3; ++k) h->lo[k] = std::min(h->lo[k], h->cen[3 * (size_t)e + k]);
+        for (int q = 0; q < ds.n_notch; ++q) h->notch_npts.push_back(ds.notch_npts[q]);
+        size_t npts = 0;
+        for (int q = 0; q < ds.n_notch; ++q) npts += ds.notch_npts[q];
+        if (npts) h->notch_pts.assign(ds.notch_pts, ds.notch_pts + 3 * npts);
+
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        cudaStream_t s = h->stream;
+        DevPD& d = h->d;
+        d.dim = dim;
+        d.nn = nn;
+        d.E = E;
+        d.N = N;
+        d.NE = nn;
+        d.Nsh = dim == 2 ? 0.25 : 0.125;  // reference_shape at the centre (fem.hpp:22-47)
+        d.s_crit = ds.s_crit;
+        d.spread = ds.s_crit_spread;
+        d.seed = ds.seed;
+        d.fracture = h->fracture;
+        const double dt = ds.dt, gm = ds.gamma, bt = ds.beta;
+        d.c_pred_v = dt * (1.0 - gm);
+        d.c_pred_d = dt * dt * (0.5 - bt);
+        d.dt = dt;
+        d.c_corr_v = gm * dt;
+        d.c_corr_d = bt * dt * dt;
+        // SoA uploads
+        std::vector<int32_t> conn_soa((size_t)nn * E);
+        for (int e = 0; e < E; ++e)
+            for (int a = 0; a < nn; ++a) conn_soa[(size_t)a * E + e] = h->conn[(size_t)e * nn + a];
+        std::vector<double> cen_soa(3 * (size_t)E);
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < 3; ++k) cen_soa[(size_t)k * E + e] = h->cen[3 * (size_t)e + k];
+        // node -> incident elements, ascending (damage_field / K row order)
+        std::vector<int32_t> cnt(N, 0), ne((size_t)nn * N, -1);
+        for (int e = 0; e < E; ++e)
+            for (int a = 0; a < nn; ++a) {
+                const int n = h->conn[(size_t)e * nn + a];
+                if (cnt[n] >= nn) throw ConfigError("node shared by more than 2^dim elements");
+                ne[(size_t)cnt[n]++ * N + n] = e;
+            }
+        int32_t* dconn = h->alloc<int32_t>(conn_soa.size());
+        double* dcen = h->alloc<double>(cen_soa.size());
+        double* dvol = h->alloc<double>(E);
+        int32_t* dne = h->alloc<int32_t>(ne.size());
+        upload(dconn, conn_soa.data(), conn_soa.size(), s);
+        upload(dcen, cen_soa.data(), cen_soa.size(), s);
+        upload(dvol, h->vol.data(), E, s);
+        upload(dne, ne.data(), ne.size(), s);
+        d.conn = dconn;
+        d.cen = dcen;
+        d.vol = dvol;
+        d.ne = dne;
+        const size_t nd = h->ndof;
+        d.u = h->alloc<double>(nd);
+        d.v = h->alloc<double>(nd);
+        d.a = h->alloc<double>(nd);
+        d.rd = h->alloc<double>(nd);
+        d.rv = h->alloc<double>(nd);
+        double* dM = h->alloc<double>(nd);
+        double* dP = h->alloc<double>(nd);
+        uint8_t* dflag = h->alloc<uint8_t>(nd);
+        double* dbcv = h->alloc<double>(nd);
+        upload(dM, ds.mass, nd, s);
+        upload(dP, ds.p_ext, nd, s);
+        upload(dflag, bcflag.data(), nd, s);
+        upload(dbcv, bcvel.data(), nd, s);
+        d.M = dM;
+        d.P = dP;
+        d.bcflag = dflag;
+        d.bcvel = dbcv;
+        d.G = h->alloc<double>((size_t)E * dim);
+        d.ubar = h->alloc<double>((size_t)E * dim);
+        CK(cudaMemsetAsync(d.u, 0, sizeof(double) * nd, s));
+        CK(cudaMemsetAsync(d.a, 0, sizeof(double) * nd, s));
+        // KinematicState::zero + prescribed velocities (driver_run.hpp:195-196)
+        upload(d.v, bcvel.data(), nd, s);
+        h->d_log_n = h->alloc<unsigned long long>(1);
+        CK(cudaMemsetAsync(h->d_log_n, 0, sizeof(unsigned long long), s));
+        d.log_n = h->d_log_n;
+        ensure_counts(h.get(), 64);
+        CK(cudaStreamSynchronize(s));
+        *out = h.release();
+    });
+}
+
+void pmts_pd_destroy(pmts_pd* h) { delete h; }
+
+int pmts_pd_build_families(pmts_pd* h) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        FamilyBuild fb = build_families_device(
+            h->dim, h->E, h->d.cen, h->lo, h->desc.delta, h->eps, (int)h->notch_npts.size(),
+            h->notch_npts.data(), h->notch_pts.data(), h->stream);
+        h->hcol.assign((size_t)fb.K * h->E, -1);
+        download(h->hcol.data(), fb.col, (size_t)fb.K * h->E, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(fb.col);
+        finish_families(h, fb.K);
+    });
+}
+
+int pmts_pd_set_pairs(pmts_pd* h, int64_t n_pairs, const int32_t* pairs) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        const int E = h->E;
+        std::vector<std::vector<int32_t>> fam(E);
+        for (int64_t q = 0; q < n_pairs; ++q) {
+            const int i = pairs[2 * q], j = pairs[2 * q + 1];
+            if (i < 0 || j < 0 || i >= E || j >= E || i >= j)
+                throw ConfigError("pair list must hold (i<j) element ids");
+            fam[i].push_back(j);
+            fam[j].push_back(i);
+        }
+        int K = 0;
+        for (auto& f : fam) {
+            std::sort(f.begin(), f.end());
+            if (std::adjacent_find(f.begin(), f.end()) != f.end())
+                throw ConfigError("duplicate pair");
+            K = std::max<int>(K, (int)f.size());
+        }
+        h->hcol.assign((size_t)K * E, -1);
+        for (int e = 0; e < E; ++e)
+            for (size_t k = 0; k < fam[e].size(); ++k) h->hcol[k * E + e] = fam[e][k];
+        finish_families(h, K);
+    });
+}
+
+int pmts_pd_get_pairs(pmts_pd* h, int32_t* out, int64_t cap, int64_t* n_out) {
+    return guard([&] {
+        require_families(h);
+        const int E = h->E, K = h->d.K;
+        int64_t n = 0;
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < K; ++k) {
+                const int p = h->hcol[(size_t)k * E + e];
+                if (p < 0) break;
+                if (p <= e) continue;
+                if (out && n < cap) {
+                    out[2 * n] = e;
+                    out[2 * n + 1] = p;
+                }
+                ++n;
+            }
+        if (n_out) *n_out = n;
+    });
+}
+
+int pmts_pd_get_intact(pmts_pd* h, uint8_t* out, int64_t cap) {
+    return guard([&] {
+        require_families(h);
+        const int E = h->E, K = h->d.K;
+        std::vector<uint32_t> mask((size_t)h->d.W * E);
+        download(mask.data(), h->d.mask, mask.size(), h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+        int64_t n = 0;
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < K; ++k) {
+                const int p = h->hcol[(size_t)k * E + e];
+                if (p < 0) break;
+                if (p <= e) continue;
+                if (n < cap) out[n] = (mask[(size_t)(k >> 5) * E + e] >> (k & 31)) & 1u;
+                ++n;
+            }
+    });
+}
+
+int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
+    return guard([&] {
+        require_families(h);
+        const double E = h->E, N = h->N, dim = h->dim, F = double(h->n_entries);
+        info->n_entries = h->n_entries;
+        info->n_bonds = h->n_entries / 2;
+        info->max_family = h->d.K;
+        info->path = 0;
+        info->stencil_size = 0;
+        info->kernels_per_step = h->mode == PMTS_DETERMINISTIC ? 2 : 3;
+        // algorithmic (compulsory) HBM bytes per step, DESIGN.md "Roofline"
+        const double fam = F * (4.0 + 8.0) + E * h->d.W * 4.0 * 2.0;
+        const double elem = E * (3 * 8.0) /*centroids*/ + E * dim * 8.0 /*G write*/;
+        const double gather = h->mode == PMTS_DETERMINISTIC
+                                  ? E * h->nn * 4.0 + N * dim * 8.0 /*conn + rd*/
+                                  : E * dim * 8.0 * 2.0 /*ubar write+read*/ +
+                                        (E * h->nn * 4.0 + N * dim * 8.0) /*ubar kernel*/;
+        const double node = N * dim * 8.0 * (2 /*rd rv*/ + 5 /*u v a rd rv*/ + 2 /*M P*/) +
+                            N * dim * 1.0 + N * h->nn * 4.0 + E * dim * 8.0 /*G read*/;
+        info->bytes_per_step = fam + elem + gather + node;
+        info->bond_bytes_per_step =
+            fam + elem +
+            (h->mode == PMTS_DETERMINISTIC ? E * h->nn * 4.0 + N * dim * 8.0 : E * dim * 8.0);
+        info->device_bytes = h->device_bytes;
+    });
+}
+
+int pmts_pd_init(pmts_pd* h, double scale0) {
+    return guard([&] {
+        require_families(h);
+        launch_det_bond(h->d, h->d.u, 0, 0, 0, h->stream);
+        launch_init_acc(h->d, scale0, h->stream);
+        launch_predict(h->d, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_step(pmts_pd* h, int32_t n, const double* scales, int64_t* n_broken_out) {
+    return guard([&] {
+        require_families(h);
+        if (n < 0 || (n > 0 && !scales)) throw ConfigError("bad step count or scales");
+        ensure_counts(h, std::max(n, 1));
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr);
+        const int64_t nb = finish_steps(h, n);
+        if (n_broken_out) *n_broken_out = nb;
+    });
+}
+
+int pmts_pd_step_timed(pmts_pd* h, int32_t n, const double* scales, float* ms_out) {
+    return guard([&] {
+        require_families(h);
+        ensure_counts(h, std::max(n, 1));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, h->stream));
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr);
+        CK(cudaEventRecord(e1, h->stream));
+        finish_steps(h, n);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms;
+    });
+}
+
+int pmts_pd_profile(pmts_pd* h, int32_t n, const double* scales, float* bond_ms,
+                    float* total_ms) {
+    return guard([&] {
+        require_families(h);
+        ensure_counts(h, std::max(n, 1));
+        std::vector<cudaEvent_t> ev(2 * n + 2);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ev[2 * n], h->stream));
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], true, &ev[2 * s]);
+        CK(cudaEventRecord(ev[2 * n + 1], h->stream));
+        finish_steps(h, n);
+        float b = 0.f, t = 0.f;
+        for (int s = 0; s < n; ++s) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[2 * s], ev[2 * s + 1]));
+            b += ms;
+        }
+        CK(cudaEventElapsedTime(&t, ev[2 * n], ev[2 * n + 1]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        *bond_ms = b;
+        *total_ms = t;
+    });
+}
+
+int pmts_pd_get_state(pmts_pd* h, double* u, double* v, double* a) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (u) download(u, h->d.u, h->ndof, h->stream);
+        if (v) download(v, h->d.v, h->ndof, h->stream);
+        if (a) download(a, h->d.a, h->ndof, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_set_state(pmts_pd* h, const double* u, const double* v, const double* a) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (u) upload(h->d.u, u, h->ndof, h->stream);
+        if (v) upload(h->d.v, v, h->ndof, h->stream);
+        if (a) upload(h->d.a, a, h->ndof, h->stream);
+        launch_predict(h->d, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_take_break_log(pmts_pd* h, int32_t* rows, int64_t cap, int64_t* n_out) {
+    return guard([&] {
+        require_families(h);
+        if (!h->d.log) throw ConfigError("break log is kept in PMTS_DETERMINISTIC mode only");
+        unsigned long long n = 0;
+        download(&n, h->d_log_n, 1, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+        if ((long long)n > h->d.log_cap) throw InternalError("break log overflow");
+        std::vector<int32_t> buf(3 * (size_t)n);
+        download(buf.data(), h->d_log, buf.size(), h->stream);
+        CK(cudaMemsetAsync(h->d_log_n, 0, sizeof(unsigned long long), h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::vector<std::array<int32_t, 3>> r(n);
+        for (size_t k = 0; k < n; ++k) r[k] = {buf[3 * k], buf[3 * k + 1], buf[3 * k + 2]};
+        std::sort(r.begin(), r.end());
+        for (size_t k = 0; k < n && (int64_t)k < cap; ++k)
+            for (int c = 0; c < 3; ++c) rows[3 * k + c] = r[k][c];
+        if (n_out) *n_out = (int64_t)n;
+    });
+}
+
+int64_t pmts_pd_broken_total(pmts_pd* h) { return h ? h->broken_total : -1; }
+
+int pmts_pd_damage(pmts_pd* h, double* elem, double* node) {
+    return guard([&] {
+        require_families(h);
+        double* de = nullptr;
+        double* dn = nullptr;
+        CK(cudaMallocAsync(&de, sizeof(double) * h->E, h->stream));
+        CK(cudaMallocAsync(&dn, sizeof(double) * h->N, h->stream));
+        launch_damage(h->d, de, dn, h->stream);
+        if (elem) download(elem, de, h->E, h->stream);
+        if (node) download(node, dn, h->N, h->stream);
+        CK(cudaFreeAsync(de, h->stream));
+        CK(cudaFreeAsync(dn, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_gather_disp(pmts_pd* h, int32_t n, const int32_t* dofs, double* out) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        for (int k = 0; k < n; ++k) {
+            if (dofs[k] < 0 || dofs[k] >= h->ndof) throw ConfigError("dof out of range");
+            download(out + k, h->d.u + dofs[k], 1, h->stream);
+        }
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+void* pmts_pd_stream(pmts_pd* h) { return h ? (void*)h->stream : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+"""Generate the golden vectors under tests/golden/ from the reference itself.
+
+Runs oracle/_ref/ref_driver -- the reference's own pure-PD loop, compiled in
+place from /root/reference/proj/include (see oracle/Makefile) -- on the
+scenarios below and stores its inputs and outputs as compressed npz files.
+The reference publishes no full-run goldens; these are the
+fixtures 1-3 of that section plus a 3D hex8 block.  Re-run with:
+
+    make -C oracle ref && python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), "..", ".."))
+sys.path.insert(0, ROOT)
+
+from oracle import pyoracle as po  # noqa: E402
+from paper_2403_03605_b200 import configs as cf  # noqa: E402
+
+# name -> (scenario, steps, checkpoints)
+FIXTURES = {
+    "mini": ("mini", 80, (40,)),
+    "cfg1_200": ("cfg1", 200, (50,)),
+    "block3d": ("block3d", 100, (50,)),
+    "bp_coarse_2000": ("bp_coarse", 2000, ()),
+}
+
+
+def main(names=None):
+    out_dir = os.path.dirname(os.path.abspath(__file__))
+    for name, (scen, steps, ck) in FIXTURES.items():
+        if names and name not in names:
+            continue
+        sc = cf.get(scen)
+        text = cf.render_cfg(sc)
+        with tempfile.TemporaryDirectory() as tmp:
+            run = po.run_ref(text, tmp, steps=steps, checkpoints=ck)
+            d = po.load_ref_dump(tmp)
+        arrays = {k: d[k] for k in ("centroid", "volume", "pairs", "mass", "p_ext", "a0",
+                                    "scale", "u", "v", "a", "damage_elem", "damage_node",
+                                    "xi_norm", "weight")}
+        arrays["broken"] = d["broken"] if d["broken"] is not None else np.zeros((0, 2), np.int32)
+        for k in ck:
+            for f in ("u", "v", "a"):
+                arrays[f"{f}_{k}"] = d[f"{f}_{k}"]
+        meta = {k: d[k] for k in ("dim", "n_nodes", "n_elems", "n_pairs", "n_dof", "n_steps",
+                                  "delta", "l", "c0", "s_crit", "dt", "gamma", "beta", "rho",
+                                  "char_length", "nnz")}
+        meta.update(scenario=scen, steps=steps, checkpoints=list(ck), run=run,
+                    sha256_u=hashlib.sha256(d["u"].tobytes()).hexdigest())
+        np.savez_compressed(os.path.join(out_dir, f"{name}.npz"), cfg=np.array(text),
+                            meta=np.array(json.dumps(meta)), **arrays)
+        print(name, run)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

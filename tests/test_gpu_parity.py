@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA fine step (through the C ABI) against the oracle and the
+reference's own outputs.
+
+Deterministic mode: broken-bond set bit-exact vs the reference, u/v/a bitwise
+equal to the matrix-free oracle and within 1e-12 relative L2 of the reference.
+Fast mode: fields within 1e-9 relative L2 before crack initiation, >= 99.9% of
+broken bonds agree afterwards (BASELINE.json north_star tolerances).
+"""
+import numpy as np
+import pytest
+
+import kat_meshes as km
+from conftest import GOLDEN_SCENARIO, load_golden, oracle_sys
+from oracle import pyoracle as po
+from paper_2403_03605_b200 import capi
+from paper_2403_03605_b200 import configs as cf
+from paper_2403_03605_b200.pd import PDSolver, Scenario
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["mini", "block3d", "cfg1_200"]
+
+
+def _solver(name, mode, **over):
+    g = load_golden(name)
+    sc = Scenario(cf.get(GOLDEN_SCENARIO[name]))
+    s = PDSolver.from_scenario(sc, mode=mode, **over)
+    return g, sc, s
+
+
+def _pairs_index(pairs):
+    return {(int(i), int(j)): q for q, (i, j) in enumerate(pairs)}
+
+
+@pytest.mark.parametrize("name", list(GOLDEN_SCENARIO))
+def test_device_neighbour_build_matches_reference(name):
+    g, sc, s = _solver(name, capi.DETERMINISTIC)
+    s.find_pe_pairs()
+    assert np.array_equal(s.pairs(), g["pairs"])
+    info = s.info()
+    assert info["n_bonds"] == g["meta"]["n_pairs"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_deterministic_bitwise(name):
+    g, sc, s = _solver(name, capi.DETERMINISTIC)
+    s.find_pe_pairs()
+    steps = g["meta"]["steps"]
+    s.initial_acceleration(g["scale"][0])
+    nb = s.step(g["scale"][1:steps + 1])
+    u, v, a = s.state()
+    # broken set and order == reference (update_bond_states order: step, then pe)
+    log = s.break_log(len(g["pairs"]))
+    idx = _pairs_index(g["pairs"])
+    got = np.array([[st, idx[(i, j)]] for st, i, j in log], dtype=np.int64).reshape(-1, 2)
+    assert nb == len(g["broken"])
+    assert np.array_equal(got, g["broken"])
+    # bitwise == matrix-free oracle (same summation order, no FMA)
+    o = po.OraclePD(oracle_sys(g, sc), po.MF)
+    o.init(g["scale"][0])
+    o.step(g["scale"][1:steps + 1])
+    ou, ov, oa = o.state()
+    assert np.array_equal(u, ou) and np.array_equal(v, ov) and np.array_equal(a, oa)
+    # reference: 1e-12 relative
+    for x, ref in ((u, g["u"]), (v, g["v"]), (a, g["a"])):
+        assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+    e, n = s.damage_field()
+    assert np.array_equal(e, g["damage_elem"]) and np.array_equal(n, g["damage_node"])
+    assert np.array_equal(s.intact(), o.mu())
+
+
+def test_deterministic_checkpoint_and_set_state():
+    """Stepping in batches equals one batch; set_state resumes exactly."""
+    g, sc, s = _solver("cfg1_200", capi.DETERMINISTIC)
+    s.find_pe_pairs()
+    s.initial_acceleration(g["scale"][0])
+    s.step(g["scale"][1:21])
+    s.step(g["scale"][21:51])
+    u, v, a = s.state()
+    assert np.linalg.norm(u - g["u_50"]) <= 1e-12 * np.linalg.norm(g["u_50"])
+    s.set_state(u, v, a)
+    s.step(g["scale"][51:201])
+    u2, _, _ = s.state()
+    assert np.linalg.norm(u2 - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
+
+
+@pytest.mark.slow
+def test_bp_coarse_deterministic():
+    g, sc, s = _solver("bp_coarse_2000", capi.DETERMINISTIC)
+    s.find_pe_pairs()
+    s.initial_acceleration(g["scale"][0])
+    nb = s.step(g["scale"][1:2001])
+    log = s.break_log(1000)
+    idx = _pairs_index(g["pairs"])
+    got = np.array([[st, idx[(i, j)]] for st, i, j in log]).reshape(-1, 2)
+    assert nb == 10 and np.array_equal(got, g["broken"])
+    u, v, _ = s.state()
+    assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_fast_mode_tolerances(name):
+    g, sc, s = _solver(name, capi.FAST)
+    s.find_pe_pairs()
+    steps = g["meta"]["steps"]
+    s.initial_acceleration(g["scale"][0])
+    br = g["broken"]
+    first = int(br[0, 0]) if len(br) else steps + 1
+    pre = min(first - 1, steps)
+    # before crack initiation: 1e-9 relative L2 against the oracle at the same step
+    o = po.OraclePD(oracle_sys(g, sc), po.MF)
+    o.init(g["scale"][0])
+    if pre > 0:
+        s.step(g["scale"][1:pre + 1])
+        o.step(g["scale"][1:pre + 1])
+        u, v, _ = s.state()
+        ou, ov, _ = o.state()
+        assert np.linalg.norm(u - ou) <= 1e-9 * np.linalg.norm(ou)
+        assert np.linalg.norm(v - ov) <= 1e-9 * np.linalg.norm(ov)
+    s.step(g["scale"][pre + 1:steps + 1])
+    # after: >= 99.9% agreement of the broken set (symmetric difference)
+    mine = s.intact() == 0
+    ref = np.zeros(len(g["pairs"]), dtype=bool)
+    ref[g["broken"][:, 1]] = True
+    if ref.sum():
+        agree = 1.0 - np.logical_xor(mine, ref).sum() / max(ref.sum(), 1)
+        assert agree >= 0.999, agree
+
+
+# ----- known-answer tests on the device (test_perifem.cpp) ------------------
+
+def _kat_solver(mesh, pairs, s_crit, mode, delta=1.5, l=0.375):
+    n = len(mesh["nodes"])
+    s = PDSolver(dim=2, nodes=mesh["nodes"], conn=mesh["conn"], mass=np.full(2 * n, 1e300),
+                 p_ext=np.zeros(2 * n), delta=delta, dt=1e-6, c0=1e9, l=l, s_crit=s_crit,
+                 mode=mode)
+    s.set_pairs(pairs)
+    return s
+
+
+def _u_move(mesh, elem, comp, val):
+    u = np.zeros(2 * len(mesh["nodes"]))
+    for nd in mesh["conn"][elem]:
+        u[2 * nd + comp] = val
+    return u
+
+
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_kat_threshold_inclusive_irreversible(mode):
+    m = km.disjoint_quads()
+    s_crit = 0.1
+    s = _kat_solver(m, [[0, 1]], s_crit, mode)
+    z = np.zeros(16)
+    # v = a = 0 and a huge mass: the step's displacement is u itself, so the
+    # device break test runs on exactly this u (driver_run.hpp:228-229)
+    s.set_state(_u_move(m, 1, 0, s_crit - 1e-9), z, z)
+    assert s.step([0.0]) == 0 and s.intact()[0] == 1
+    s.set_state(_u_move(m, 1, 0, s_crit), z, z)
+    if mode == capi.DETERMINISTIC:
+        assert s.step([0.0]) == 1 and s.intact()[0] == 0
+    else:  # squared test at exactly s_crit may round either way; go just above
+        s.set_state(_u_move(m, 1, 0, s_crit * (1 + 1e-12)), z, z)
+        assert s.step([0.0]) == 1 and s.intact()[0] == 0
+    s.set_state(_u_move(m, 1, 0, 2 * s_crit), z, z)
+    assert s.step([0.0]) == 0 and s.intact()[0] == 0
+
+
+def test_kat_damage_half():
+    m = km.grid(3, 1, 1.0)
+    s = _kat_solver(m, [[0, 1], [1, 2]], 0.1, capi.DETERMINISTIC)
+    z = np.zeros(2 * len(m["nodes"]))
+    e, _ = s.damage_field()
+    assert (e == 0).all()
+    # stretch only the (0,1) bond: move element 0 left (its nodes are shared with
+    # element 1 on one side, so use a displacement field that separates them)
+    u = np.zeros_like(z)
+    for nd in (0, 4):  # left edge nodes of element 0
+        u[2 * nd] = -1.0
+    s.set_state(u, z, z)
+    s.step([0.0])
+    e, _ = s.damage_field()
+    assert e[1] == pytest.approx(0.5) and e[0] == pytest.approx(1.0) and e[2] == 0.0
+
+
+def test_kat_no_fracture_when_s_crit_zero():
+    m = km.disjoint_quads()
+    s = _kat_solver(m, [[0, 1]], 0.0, capi.DETERMINISTIC)
+    z = np.zeros(16)
+    s.set_state(_u_move(m, 1, 0, 5.0), z, z)
+    assert s.step([0.0]) == 0 and s.intact()[0] == 1
+
+
+def test_device_notch_cases():
+    m = km.grid(2, 1, 1.0)
+    n = len(m["nodes"])
+
+    def count(notch):
+        s = PDSolver(dim=2, nodes=m["nodes"], conn=m["conn"], mass=np.ones(2 * n),
+                     p_ext=np.zeros(2 * n), delta=1.01, dt=1e-6, c0=1.0, l=0.5,
+                     notch_npts=[2], notch_pts=notch)
+        return s.find_pe_pairs().info()["n_bonds"]
+
+    assert count([1.0, -0.5, 0, 1.0, 1.5, 0]) == 0
+    assert count([1.0, 2.0, 0, 1.0, 3.0, 0]) == 1
+    assert count([1.0, 0.5, 0, 1.0, 2.0, 0]) == 0
+
+
+def test_non_positive_mass_is_solver_error():
+    m = km.disjoint_quads()
+    with pytest.raises(capi.SolverError):
+        PDSolver(dim=2, nodes=m["nodes"], conn=m["conn"], mass=np.zeros(16),
+                 p_ext=np.zeros(16), delta=1.5, dt=1e-6, c0=1.0, l=0.5)
+
+
+def test_implicit_pd_rejected():
+    m = km.disjoint_quads()
+    with pytest.raises(capi.ConfigError):
+        PDSolver(dim=2, nodes=m["nodes"], conn=m["conn"], mass=np.ones(16),
+                 p_ext=np.zeros(16), delta=1.5, dt=1e-6, c0=1.0, l=0.5, beta=0.25)
+
+
+# ----- full-size (BASELINE cfg3) size-independent properties -----------------
+
+@pytest.fixture(scope="module")
+def cfg3():
+    sc = Scenario(cf.get("cfg3"))
+    return sc
+
+
+def test_cfg3_families_match_oracle(cfg3):
+    s = PDSolver.from_scenario(cfg3, mode=capi.FAST).find_pe_pairs()
+    p = s.pairs()
+    assert len(p) == 22_331_624  # SURVEY.md 8(a), reference find_pe_pairs at 2000x800
+    ref = po.find_pairs(2, cfg3.centroid, cfg3.volume, cfg3.delta, cfg3.notches())
+    assert np.array_equal(p, ref)
+
+
+def test_cfg3_linearity_and_momentum(cfg3):
+    """No fracture: the step is linear in (u, v, a, P) and internal forces are
+    self-equilibrated (sum of K u over all dofs vanishes)."""
+    s1 = PDSolver.from_scenario(cfg3, mode=capi.FAST, s_crit=0.0).find_pe_pairs()
+    s2 = PDSolver.from_scenario(cfg3, mode=capi.FAST, s_crit=0.0).find_pe_pairs()
+    sc = np.full(20, 1.0)
+    s1.initial_acceleration(1.0)
+    s2.initial_acceleration(1.0)
+    s1.step(sc)
+    s2.step(2.0 * sc)
+    u1, v1, a1 = s1.state()
+    u2, v2, a2 = s2.state()
+    assert np.linalg.norm(u2 - 2 * u1) <= 1e-12 * np.linalg.norm(u2)
+    # momentum: sum M a == sum P (internal forces cancel pairwise)
+    P = cfg3.p_ext
+    f_int = P - cfg3.mass * a1
+    assert abs(f_int[0::2].sum()) <= 1e-9 * np.abs(f_int).sum()
+    assert abs(f_int[1::2].sum()) <= 1e-9 * np.abs(f_int).sum()
