@@ -22,6 +22,7 @@ SOURCES = [
     # (file, extra nvcc flags)
     ("pd_det.cu", ["-fmad=false"]),
     ("pd_fast.cu", []),
+    ("pd_stencil.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp"]

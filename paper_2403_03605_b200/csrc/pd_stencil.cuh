@@ -1,0 +1,28 @@
+// Lattice-stencil family encoding (fast mode) -- see pd_stencil.cu.
+#pragma once
+
+#include "pd_common.cuh"
+
+namespace pmts {
+
+constexpr int kMaxStencil = 128;
+
+struct LatticeDev {
+    int nx, ny, nz;      // elements per axis
+    int R;               // max |offset component|
+    int S;               // stencil size
+    int W;               // mask words per element (S <= 32 W)
+    const int8_t* di;    // per offset (device)
+    const int8_t* dj;
+    const int8_t* dk;
+    const int* delta_id; // linear element-id delta of each offset
+    const double* table; // per offset: xi[3], w c(|xi|), |xi|^2, ((1+s_crit)|xi|)^2
+};
+
+size_t lattice_smem_bytes(int dim, int R, int S);
+void lattice_configure(int dim, int R, int S);
+void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,
+                         double scale, int write_state, bool time_bond, cudaEvent_t* ev,
+                         cudaStream_t s);
+
+}  // namespace pmts

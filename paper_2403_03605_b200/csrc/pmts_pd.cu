@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "pd_common.cuh"
+#include "pd_stencil.cuh"
 #include "pmts_internal.h"
 
 using namespace pmts;
@@ -72,6 +73,10 @@ struct pmts_pd {
     int counts_cap = 0;
     unsigned long long* d_log_n = nullptr;
     int32_t* d_log = nullptr;
+    // lattice-stencil fast path (pd_stencil.cu)
+    bool lattice = false;
+    LatticeDev L{};
+    std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
     std::vector<void*> owned;
 
     ~pmts_pd() {
@@ -106,6 +111,8 @@ double micromodulus(const pmts_pd_desc& dsc, int dim, double r) {
     }
     return dsc.c0 * std::exp(-r / dsc.l);
 }
+
+bool try_lattice(pmts_pd* h);
 
 // Family tables from the ELL partner list: per directed entry w c(|xi|)
 // computed on the host exactly as scatter_pe_block forms it
@@ -155,6 +162,179 @@ void finish_families(pmts_pd* h, int K) {
     }
     CK(cudaStreamSynchronize(h->stream));
     h->families = true;
+    h->lattice = false;
+    if (h->mode == PMTS_FAST) try_lattice(h);
+}
+
+// Stencil encoding of the families when the mesh is the generated lattice
+// (fast mode).  Returns false (ELL path stays) if any bond's offset falls
+// outside one shared stencil of <= kMaxStencil offsets.
+bool try_lattice(pmts_pd* h) {
+    const int E = h->E, K = h->d.K, dim = h->dim;
+    const int nx = h->desc.lattice[0], ny = h->desc.lattice[1];
+    const int nz = dim == 3 ? h->desc.lattice[2] : 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0 || (int64_t)nx * ny * nz != E) return false;
+    // element (i,j,k) of id e must be the lattice cell: check centroids are monotone
+    auto ijk = [&](int e, int& i, int& j, int& k) {
+        i = e % nx;
+        j = (e / nx) % ny;
+        k = e / (nx * ny);
+    };
+    int R = 0;
+    for (int e = 0; e < E; ++e)
+        for (int q = 0; q < K; ++q) {
+            const int p = h->hcol[(size_t)q * E + e];
+            if (p < 0) break;
+            int a, b, c, x, y, z;
+            ijk(e, a, b, c);
+            ijk(p, x, y, z);
+            R = std::max({R, std::abs(x - a), std::abs(y - b), std::abs(z - c)});
+        }
+    if (R == 0 || R > 8) return false;
+    const int span = 2 * R + 1;
+    std::vector<int> slot(span * span * span, -1);
+    auto key = [&](int di, int dj, int dk) { return ((dk + R) * span + dj + R) * span + di + R; };
+    std::vector<int> offs;  // keys
+    for (int e = 0; e < E; ++e)
+        for (int q = 0; q < K; ++q) {
+            const int p = h->hcol[(size_t)q * E + e];
+            if (p < 0) break;
+            int a, b, c, x, y, z;
+            ijk(e, a, b, c);
+            ijk(p, x, y, z);
+            const int kk = key(x - a, y - b, z - c);
+            if (slot[kk] < 0) {
+                slot[kk] = 0;
+                offs.push_back(kk);
+            }
+        }
+    // symmetric closure and ascending linear delta (== ascending partner id)
+    auto decode = [&](int kk, int& di, int& dj, int& dk) {
+        di = kk % span - R;
+        dj = (kk / span) % span - R;
+        dk = kk / (span * span) - R;
+    };
+    for (size_t n = 0, m = offs.size(); n < m; ++n) {
+        int di, dj, dk;
+        decode(offs[n], di, dj, dk);
+        const int neg = key(-di, -dj, -dk);
+        if (slot[neg] < 0) {
+            slot[neg] = 0;
+            offs.push_back(neg);
+        }
+    }
+    auto lin = [&](int kk) {
+        int di, dj, dk;
+        decode(kk, di, dj, dk);
+        return (dk * ny + dj) * nx + di;
+    };
+    std::sort(offs.begin(), offs.end(), [&](int a, int b) { return lin(a) < lin(b); });
+    const int S = (int)offs.size();
+    if (S > kMaxStencil) return false;
+    for (int s = 0; s < S; ++s) slot[offs[s]] = s;
+    const int W = (S + 31) / 32;
+    // per-offset constants from one representative bond of the positive offset;
+    // the negative offset gets the exact negation (both directions of a bond then
+    // evaluate bitwise-negated operands and agree on every break)
+    std::vector<double> table(6 * (size_t)S, 0.0);
+    std::vector<char> have(S, 0);
+    std::vector<uint32_t> mask((size_t)W * E, 0u);
+    const double s1 = 1.0 + h->desc.s_crit;
+    for (int e = 0; e < E; ++e)
+        for (int q = 0; q < K; ++q) {
+            const int p = h->hcol[(size_t)q * E + e];
+            if (p < 0) break;
+            int a, b, c, x, y, z;
+            ijk(e, a, b, c);
+            ijk(p, x, y, z);
+            const int s = slot[key(x - a, y - b, z - c)];
+            mask[(size_t)(s >> 5) * E + e] |= 1u << (s & 31);
+            if (p > e && !have[s]) {
+                have[s] = 1;
+                double xi[3];
+                for (int k = 0; k < 3; ++k) xi[k] = h->cen[3 * (size_t)p + k] - h->cen[3 * (size_t)e + k];
+                const double x2 = xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2];
+                const double f = micromodulus(h->desc, dim, std::sqrt(x2)) * (h->vol[e] * h->vol[p]);
+                int di, dj, dk;
+                decode(offs[s], di, dj, dk);
+                const int sn = slot[key(-di, -dj, -dk)];
+                for (int k = 0; k < 3; ++k) {
+                    table[6 * s + k] = xi[k];
+                    table[6 * sn + k] = -xi[k];
+                }
+                table[6 * s + 3] = table[6 * sn + 3] = f;
+                table[6 * s + 4] = table[6 * sn + 4] = x2;
+                table[6 * s + 5] = table[6 * sn + 5] = s1 * s1 * x2;
+                have[sn] = 1;
+            }
+        }
+    std::vector<int8_t> di(S), dj(S), dk(S);
+    std::vector<int> dl(S);
+    for (int s = 0; s < S; ++s) {
+        int a, b, c;
+        decode(offs[s], a, b, c);
+        di[s] = (int8_t)a;
+        dj[s] = (int8_t)b;
+        dk[s] = (int8_t)c;
+        dl[s] = lin(offs[s]);
+    }
+    LatticeDev& L = h->L;
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    L.R = R;
+    L.S = S;
+    L.W = W;
+    int8_t* ddi = h->alloc<int8_t>(S);
+    int8_t* ddj = h->alloc<int8_t>(S);
+    int8_t* ddk = h->alloc<int8_t>(S);
+    int* ddl = h->alloc<int>(S);
+    double* dtab = h->alloc<double>(6 * (size_t)S);
+    upload(ddi, di.data(), S, h->stream);
+    upload(ddj, dj.data(), S, h->stream);
+    upload(ddk, dk.data(), S, h->stream);
+    upload(ddl, dl.data(), S, h->stream);
+    upload(dtab, table.data(), 6 * (size_t)S, h->stream);
+    L.di = ddi;
+    L.dj = ddj;
+    L.dk = ddk;
+    L.delta_id = ddl;
+    L.table = dtab;
+    // the stencil mask replaces the ELL mask; ELL coefficients are not needed
+    h->release(h->d.mask);
+    uint32_t* dmask = h->alloc<uint32_t>((size_t)W * E);
+    upload(dmask, mask.data(), (size_t)W * E, h->stream);
+    h->d.mask = dmask;
+    h->d.W = W;
+    h->release((void*)h->d.coef);
+    h->d.coef = nullptr;
+    h->stencil_delta = dl;
+    lattice_configure(dim, R, S);
+    CK(cudaStreamSynchronize(h->stream));
+    h->lattice = true;
+    return true;
+}
+
+// ELL-layout intact mask (bit k = k-th family entry) from the stencil mask
+std::vector<uint32_t> ell_mask_host(pmts_pd* h) {
+    const int E = h->E, K = h->d.K;
+    std::vector<uint32_t> m((size_t)h->d.W * E);
+    download(m.data(), h->d.mask, m.size(), h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+    if (!h->lattice) return m;
+    const int We = std::max(1, (K + 31) / 32);
+    std::vector<uint32_t> out((size_t)We * E, 0u);
+    std::map<int, int> sidx;
+    for (size_t s = 0; s < h->stencil_delta.size(); ++s) sidx[h->stencil_delta[s]] = (int)s;
+    for (int e = 0; e < E; ++e)
+        for (int q = 0; q < K; ++q) {
+            const int p = h->hcol[(size_t)q * E + e];
+            if (p < 0) break;
+            const int s = sidx.at(p - e);
+            if ((m[(size_t)(s >> 5) * E + e] >> (s & 31)) & 1u)
+                out[(size_t)(q >> 5) * E + e] |= 1u << (q & 31);
+        }
+    return out;
 }
 
 void require_families(pmts_pd* h) {
@@ -173,8 +353,13 @@ void ensure_counts(pmts_pd* h, int n) {
 }
 
 // one fine step: bond gather + node update with the fused predictor
-void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev) {
+void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev,
+                  bool last = true) {
     const int brk = h->fracture ? 1 : 0;
+    if (h->lattice) {
+        launch_lattice_step(h->d, h->L, slot, brk, scale, last ? 1 : 0, time_bond, ev, h->stream);
+        return;
+    }
     if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
     if (h->mode == PMTS_DETERMINISTIC) {
         launch_det_bond(h->d, h->d.rd, slot, brk, int(h->gstep + slot + 1), h->stream);
@@ -418,9 +603,7 @@ int pmts_pd_get_intact(pmts_pd* h, uint8_t* out, int64_t cap) {
     return guard([&] {
         require_families(h);
         const int E = h->E, K = h->d.K;
-        std::vector<uint32_t> mask((size_t)h->d.W * E);
-        download(mask.data(), h->d.mask, mask.size(), h->stream);
-        CK(cudaStreamSynchronize(h->stream));
+        const std::vector<uint32_t> mask = ell_mask_host(h);
         int64_t n = 0;
         for (int e = 0; e < E; ++e)
             for (int k = 0; k < K; ++k) {
@@ -456,6 +639,17 @@ int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
         info->bond_bytes_per_step =
             fam + elem +
             (h->mode == PMTS_DETERMINISTIC ? E * h->nn * 4.0 + N * dim * 8.0 : E * dim * 8.0);
+        if (h->lattice) {
+            // ubar: rd in, ubar out | bond: ubar in, bits in, G out | node: G, rd, rv, M,
+            // P, flags in; rd, rv out (u, v, a only on a batch's last step)
+            info->path = 1;
+            info->stencil_size = h->L.S;
+            const double ubar = N * dim * 8.0 + E * dim * 8.0;
+            const double bond = E * dim * 8.0 + E * h->L.W * 4.0 + E * dim * 8.0;
+            const double nodek = E * dim * 8.0 + N * dim * 8.0 * 6 + N * dim * 1.0;
+            info->bytes_per_step = ubar + bond + nodek;
+            info->bond_bytes_per_step = bond;
+        }
         info->device_bytes = h->device_bytes;
     });
 }
@@ -463,7 +657,22 @@ int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
 int pmts_pd_init(pmts_pd* h, double scale0) {
     return guard([&] {
         require_families(h);
-        launch_det_bond(h->d, h->d.u, 0, 0, 0, h->stream);
+        if (h->lattice) {  // K u0 through the stencil kernels (rd <- u0 first)
+            CK(cudaMemcpyAsync(h->d.rd, h->d.u, sizeof(double) * h->ndof,
+                               cudaMemcpyDeviceToDevice, h->stream));
+            ensure_counts(h, 1);
+            DevPD dd = h->d;
+            double* junk = nullptr;
+            CK(cudaMallocAsync(&junk, sizeof(double) * 2 * h->ndof, h->stream));
+            dd.rv = junk;  // the node kernel's predictor output is discarded here
+            dd.rd = junk + h->ndof;
+            CK(cudaMemcpyAsync(dd.rd, h->d.u, sizeof(double) * h->ndof,
+                               cudaMemcpyDeviceToDevice, h->stream));
+            launch_lattice_step(dd, h->L, 0, 0, 0.0, 0, false, nullptr, h->stream);
+            CK(cudaFreeAsync(junk, h->stream));
+        } else {
+            launch_det_bond(h->d, h->d.u, 0, 0, 0, h->stream);
+        }
         launch_init_acc(h->d, scale0, h->stream);
         launch_predict(h->d, h->stream);
         CK(cudaStreamSynchronize(h->stream));
@@ -475,7 +684,7 @@ int pmts_pd_step(pmts_pd* h, int32_t n, const double* scales, int64_t* n_broken_
         require_families(h);
         if (n < 0 || (n > 0 && !scales)) throw ConfigError("bad step count or scales");
         ensure_counts(h, std::max(n, 1));
-        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr);
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr, s == n - 1);
         const int64_t nb = finish_steps(h, n);
         if (n_broken_out) *n_broken_out = nb;
     });
@@ -489,7 +698,7 @@ int pmts_pd_step_timed(pmts_pd* h, int32_t n, const double* scales, float* ms_ou
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, h->stream));
-        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr);
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], false, nullptr, s == n - 1);
         CK(cudaEventRecord(e1, h->stream));
         finish_steps(h, n);
         float ms = 0.f;
@@ -508,7 +717,7 @@ int pmts_pd_profile(pmts_pd* h, int32_t n, const double* scales, float* bond_ms,
         std::vector<cudaEvent_t> ev(2 * n + 2);
         for (auto& e : ev) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(ev[2 * n], h->stream));
-        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], true, &ev[2 * s]);
+        for (int s = 0; s < n; ++s) enqueue_step(h, s, scales[s], true, &ev[2 * s], s == n - 1);
         CK(cudaEventRecord(ev[2 * n + 1], h->stream));
         finish_steps(h, n);
         float b = 0.f, t = 0.f;
@@ -575,7 +784,17 @@ int pmts_pd_damage(pmts_pd* h, double* elem, double* node) {
         double* dn = nullptr;
         CK(cudaMallocAsync(&de, sizeof(double) * h->E, h->stream));
         CK(cudaMallocAsync(&dn, sizeof(double) * h->N, h->stream));
-        launch_damage(h->d, de, dn, h->stream);
+        DevPD dd = h->d;
+        uint32_t* tmp = nullptr;
+        if (h->lattice) {  // damage walks ELL families: translate the stencil bits
+            const std::vector<uint32_t> m = ell_mask_host(h);
+            CK(cudaMallocAsync(&tmp, sizeof(uint32_t) * m.size(), h->stream));
+            upload(tmp, m.data(), m.size(), h->stream);
+            dd.mask = tmp;
+            dd.W = std::max(1, (h->d.K + 31) / 32);
+        }
+        launch_damage(dd, de, dn, h->stream);
+        if (tmp) CK(cudaFreeAsync(tmp, h->stream));
         if (elem) download(elem, de, h->E, h->stream);
         if (node) download(node, dn, h->N, h->stream);
         CK(cudaFreeAsync(de, h->stream));

@@ -98,10 +98,13 @@ def test_bp_coarse_deterministic():
     assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
 
 
+@pytest.mark.parametrize("path", ["lattice", "ell"])
 @pytest.mark.parametrize("name", SMALL)
-def test_fast_mode_tolerances(name):
-    g, sc, s = _solver(name, capi.FAST)
+def test_fast_mode_tolerances(name, path):
+    over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
+    g, sc, s = _solver(name, capi.FAST, **over)
     s.find_pe_pairs()
+    assert s.info()["path"] == (1 if path == "lattice" else 0)
     steps = g["meta"]["steps"]
     s.initial_acceleration(g["scale"][0])
     br = g["broken"]
@@ -242,7 +245,7 @@ def test_cfg3_linearity_and_momentum(cfg3):
     s2 = PDSolver.from_scenario(cfg3, mode=capi.FAST, s_crit=0.0).find_pe_pairs()
     sc = np.full(20, 1.0)
     s1.initial_acceleration(1.0)
-    s2.initial_acceleration(1.0)
+    s2.initial_acceleration(2.0)
     s1.step(sc)
     s2.step(2.0 * sc)
     u1, v1, a1 = s1.state()
