@@ -4,19 +4,22 @@
 // element's family is a subset of one global offset stencil: partner =
 // e + (di, dj, dk).  The family then needs no per-bond storage at all -- one
 // bit per stencil offset per element ("active" = in the family and intact),
-// and per-offset constants (xi, w c(|xi|), |xi|^2) shared by all elements.
-// Compared with ELL families this drops the 12 B per directed entry (partner
-// id + coefficient) that dominated HBM traffic; what remains per element is
-// the centroid displacement, the bit mask and the element force.
+// and per-offset constants (xi, w c(|xi|), thresholds) shared by all
+// elements.  Compared with ELL families this drops the 12 B per directed
+// entry (partner id + coefficient) that dominated HBM traffic.
 //
-// Per fine step (3 launches):
-//   k_lat_ubar   ubar_e = N sum_a rd(node_a)                 (perifem.hpp:149-157)
-//   k_lat_bond   CTA tile of elements + stencil apron of ubar staged in shared
-//                memory; per active offset: eta = ubar_p - ubar_e,
-//                G_e -= w c (xi.eta) xi, squared break test (one-way bits)
-//   k_lat_node   K u at the nodes from the <= 2^d incident G_e, explicit
-//                Newmark update (newmark.hpp:125-157) + next predictor
-//                (newmark.hpp:61-69); u, v, a written on the batch's last step
+// Per fine step:
+//   2D: k_lat_bond<2> (ubar from a shared-memory node tile, fused) + k_lat_node
+//   3D: k_lat_ubar<3> + k_lat_bond<3> + k_lat_node
+//   ubar_e = N sum_a rd(node_a)                                  perifem.hpp:149-157
+//   per active offset: eta = ubar_p - ubar_e;  G_e -= w c (xi.eta) xi;
+//     break iff 2 xi.eta + |eta|^2 >= (2 s + s^2) |xi|^2   (== |xi+eta|^2 >=
+//     ((1+s)|xi|)^2, the squared form of perifem.hpp:158-165, 183)
+//   node: K u = N sum G_e (<= 2^d incident elements); explicit Newmark update
+//     (newmark.hpp:125-157) + next predictor (newmark.hpp:61-69); u, v, a are
+//     materialised on the last step of a batch only.
+// The per-bond s0 factor (counter hash) is evaluated only for the rare bonds
+// whose stretch already exceeds the smallest possible threshold.
 #include <stdexcept>
 #include <string>
 
@@ -57,81 +60,151 @@ __global__ void __launch_bounds__(256) k_lat_ubar(DevPD d, LatticeDev L) {
     for (int c = 0; c < DIM; ++c) d.ubar[(size_t)e * DIM + c] = d.Nsh * s[c];
 }
 
-template <int DIM, int TX, int TY, int TZ>
+// Stencil table row (8 doubles, 16 B aligned pairs):
+//   0 xi0  1 xi1  2 f = w c(|xi|)  3 cthr = (2 s + s^2)|xi|^2  4 xi2
+//   5 cthr_lo (smallest threshold under the per-bond factor)  6 |xi|^2  7 pad
+constexpr int kRow = 8;
+
+template <int DIM, int TX, int TY, int TZ, int EPT>
+struct BondTile {
+    static constexpr int NT = TX * TY * TZ;          // threads
+    static constexpr int EY = DIM == 2 ? TY * EPT : TY;  // tile extent (elements)
+    static constexpr int EZ = DIM == 2 ? 1 : TZ * EPT;
+};
+
+// shared bytes for a tile (host + device agree)
+template <int DIM, int TX, int TY, int TZ, int EPT>
+__host__ __device__ inline size_t bond_smem(int R, int S) {
+    using T = BondTile<DIM, TX, TY, TZ, EPT>;
+    const size_t ax = TX + 2 * R, ay = T::EY + 2 * R, az = DIM == 3 ? T::EZ + 2 * R : 1;
+    size_t b = sizeof(double) * DIM * ax * ay * az;                 // ubar apron
+    if (DIM == 2) b += sizeof(double) * 2 * (ax + 1) * (ay + 1);     // node tile (fused ubar)
+    b += sizeof(double) * kRow * S + sizeof(int2) * S;              // stencil table
+    return b;
+}
+
+template <int DIM, int TX, int TY, int TZ, int EPT>
 __global__ void __launch_bounds__(TX* TY* TZ)
 k_lat_bond(DevPD d, LatticeDev L, int step, int do_break) {
-    extern __shared__ double smem[];
-    constexpr int NT = TX * TY * TZ;
+    using T = BondTile<DIM, TX, TY, TZ, EPT>;
+    extern __shared__ __align__(16) double smem[];
     const int R = L.R;
-    const int AX = TX + 2 * R, AY = TY + 2 * R, AZ = DIM == 3 ? TZ + 2 * R : 1;
+    const int AX = TX + 2 * R, AY = T::EY + 2 * R, AZ = DIM == 3 ? T::EZ + 2 * R : 1;
     const int napron = AX * AY * AZ;
-    // shared layout: ubar apron tile (SoA per component), then the stencil table
-    double* ub = smem;                                  // DIM * napron
-    double* tab = smem + (size_t)DIM * napron;          // S * 6: xi[3], f, x2, thr
-    int* toff = reinterpret_cast<int*>(tab + 6 * L.S);  // S * 2: tile offset, id delta
+    double* ub = smem;  // 2D: double2 per apron cell; 3D: SoA per component
+    double* nodes = smem + DIM * napron;
+    double* tab = nodes + (DIM == 2 ? 2 * (AX + 1) * (AY + 1) : 0);
+    int2* toff = reinterpret_cast<int2*>(tab + kRow * L.S);
     const int tid = threadIdx.x;
-    for (int q = tid; q < L.S; q += NT) {
-        for (int c = 0; c < 6; ++c) tab[6 * q + c] = L.table[6 * q + c];
-        toff[2 * q] = (L.dk[q] * AY + L.dj[q]) * AX + L.di[q];
-        toff[2 * q + 1] = L.delta_id[q];
-    }
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY, k0 = blockIdx.z * TZ;
-    for (int q = tid; q < napron; q += NT) {
-        const int ax = q % AX, r = q / AX;
-        const int ay = r % AY, az = r / AY;
-        const int gi = i0 + ax - R, gj = j0 + ay - R, gk = DIM == 3 ? k0 + az - R : 0;
-        const bool in = gi >= 0 && gj >= 0 && gk >= 0 && gi < L.nx && gj < L.ny && gk < L.nz;
-        const size_t ge = ((size_t)gk * L.ny + gj) * L.nx + gi;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * T::EY, k0 = blockIdx.z * T::EZ;
+    for (int q = tid; q < L.S; q += T::NT) {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) ub[c * napron + q] = in ? d.ubar[ge * DIM + c] : 0.0;
+        for (int c = 0; c < kRow; ++c) tab[kRow * q + c] = L.table[kRow * q + c];
+        toff[q] = make_int2((L.dk[q] * AY + L.dj[q]) * AX + L.di[q], L.delta_id[q]);
+    }
+    if constexpr (DIM == 2) {
+        // node tile (AX+1) x (AY+1), then ubar of every apron element from it
+        const int NX = L.nx + 1, NY = L.ny + 1, BX = AX + 1, BY = AY + 1;
+        const double2* rd2 = reinterpret_cast<const double2*>(d.rd);
+        double2* nt = reinterpret_cast<double2*>(nodes);
+        for (int q = tid; q < BX * BY; q += T::NT) {
+            const int bx = q % BX, by = q / BX;
+            const int gi = i0 - R + bx, gj = j0 - R + by;
+            double2 v = make_double2(0.0, 0.0);
+            if (gi >= 0 && gj >= 0 && gi < NX && gj < NY) v = rd2[(size_t)gj * NX + gi];
+            nt[q] = v;
+        }
+        __syncthreads();
+        double2* u2 = reinterpret_cast<double2*>(ub);
+        for (int q = tid; q < napron; q += T::NT) {
+            const int ax = q % AX, ay = q / AX;
+            const double2 a = nt[ay * BX + ax], b = nt[ay * BX + ax + 1];
+            const double2 c = nt[(ay + 1) * BX + ax + 1], e = nt[(ay + 1) * BX + ax];
+            u2[q] = make_double2(d.Nsh * (((a.x + b.x) + c.x) + e.x),
+                                 d.Nsh * (((a.y + b.y) + c.y) + e.y));
+        }
+    } else {
+        for (int q = tid; q < napron; q += T::NT) {
+            const int ax = q % AX, r = q / AX;
+            const int ay = r % AY, az = r / AY;
+            const int gi = i0 + ax - R, gj = j0 + ay - R, gk = k0 + az - R;
+            const bool in = gi >= 0 && gj >= 0 && gk >= 0 && gi < L.nx && gj < L.ny && gk < L.nz;
+            const size_t ge = ((size_t)gk * L.ny + gj) * L.nx + gi;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) ub[c * napron + q] = in ? d.ubar[ge * DIM + c] : 0.0;
+        }
     }
     __syncthreads();
+
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
-    const int gi = i0 + tx, gj = j0 + ty, gk = k0 + tz;
     unsigned long long nb = 0;
-    if (gi < L.nx && gj < L.ny && gk < L.nz) {
-        const int e = (gk * L.ny + gj) * L.nx + gi;
-        const int q0 = ((DIM == 3 ? tz + R : 0) * AY + ty + R) * AX + tx + R;
-        double ue[DIM], G[DIM];
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            ue[c] = ub[c * napron + q0];
-            G[c] = 0.0;
+    for (int r = 0; r < EPT; ++r) {
+        const int ly = DIM == 2 ? ty + r * TY : ty;
+        const int lz = DIM == 2 ? 0 : tz + r * TZ;
+        const int gi = i0 + tx, gj = j0 + ly, gk = k0 + lz;
+        if (gi >= L.nx || gj >= L.ny || gk >= L.nz) continue;
+        const int e = (gk * L.ny + gj) * L.nx + gi;
+        const int q0 = ((DIM == 3 ? lz + R : 0) * AY + ly + R) * AX + tx + R;
+        double ue[DIM], G[DIM];
+        if constexpr (DIM == 2) {
+            const double2 v = reinterpret_cast<const double2*>(ub)[q0];
+            ue[0] = v.x;
+            ue[1] = v.y;
+        } else {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) ue[c] = ub[c * napron + q0];
         }
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) G[c] = 0.0;
         for (int w = 0; w < L.W; ++w) {
-            uint32_t m = d.mask[(size_t)w * d.E + e];
-            const uint32_t m0 = m;
-            uint32_t live = m;
+            const uint32_t m0 = d.mask[(size_t)w * d.E + e];
+            uint32_t m = m0, live = m0;
             while (live) {
                 const int b = __ffs(live) - 1;
                 live &= live - 1;
                 const int s = 32 * w + b;
-                const double* t = tab + 6 * s;
-                const int q = q0 + toff[2 * s];
-                double dot = 0.0, l2 = 0.0;
-                double xi[DIM];
+                const double* t = tab + kRow * s;
+                const int2 of = toff[s];
+                double xi[DIM], eta[DIM];
+                if constexpr (DIM == 2) {
+                    const double2 x01 = *reinterpret_cast<const double2*>(t);
+                    xi[0] = x01.x;
+                    xi[1] = x01.y;
+                    const double2 up = reinterpret_cast<const double2*>(ub)[q0 + of.x];
+                    eta[0] = up.x - ue[0];
+                    eta[1] = up.y - ue[1];
+                } else {
 #pragma unroll
-                for (int c = 0; c < DIM; ++c) {
-                    xi[c] = t[c];
-                    const double eta = ub[c * napron + q] - ue[c];
-                    dot = fma(xi[c], eta, dot);
-                    const double y = xi[c] + eta;
-                    l2 = fma(y, y, l2);
+                    for (int c = 0; c < DIM; ++c) {
+                        xi[c] = t[c == 2 ? 4 : c];
+                        eta[c] = ub[c * napron + q0 + of.x] - ue[c];
+                    }
                 }
-                const double fd = t[3] * dot;
+                double dot = xi[0] * eta[0], e2 = eta[0] * eta[0];
+#pragma unroll
+                for (int c = 1; c < DIM; ++c) {
+                    dot = fma(xi[c], eta[c], dot);
+                    e2 = fma(eta[c], eta[c], e2);
+                }
+                const double2 fc = *reinterpret_cast<const double2*>(t + 2);  // f, cthr
+                const double fd = fc.x * dot;
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) G[c] = fma(-fd, xi[c], G[c]);
                 if (do_break) {
-                    double thr = t[5];
-                    if (d.spread != 0.0) {
-                        const int p = e + toff[2 * s + 1];
-                        const double s1 = 1.0 + bond_s_crit(d.s_crit, d.spread, d.seed,
-                                                            e < p ? e : p, e < p ? p : e);
-                        thr = s1 * s1 * t[4];
-                    }
-                    if (l2 >= thr) {
-                        m &= ~(1u << b);
-                        if (toff[2 * s + 1] > 0) ++nb;
+                    const double lhs = fma(2.0, dot, e2);
+                    if (lhs >= t[5]) {  // >= the smallest threshold any bond can have
+                        double thr = fc.y;  // (2 s + s^2) |xi|^2 with the scalar s_crit
+                        if (d.spread != 0.0) {
+                            const int p = e + of.y;
+                            const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
+                                                          e < p ? e : p, e < p ? p : e);
+                            thr = fma(sb, sb, 2.0 * sb) * t[6];
+                        }
+                        if (lhs >= thr) {
+                            m &= ~(1u << b);
+                            if (of.y > 0) ++nb;
+                        }
                     }
                 }
             }
@@ -141,13 +214,13 @@ k_lat_bond(DevPD d, LatticeDev L, int step, int do_break) {
         for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
     }
     if (do_break) {
-        __shared__ unsigned long long part[NT / 32];
+        __shared__ unsigned long long part[T::NT / 32];
         for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
         if ((tid & 31) == 0) part[tid >> 5] = nb;
         __syncthreads();
         if (tid == 0) {
             unsigned long long t = 0;
-            for (int w = 0; w < NT / 32; ++w) t += part[w];
+            for (int w = 0; w < T::NT / 32; ++w) t += part[w];
             if (t) atomicAdd(d.broken_count + step, t);
         }
     }
@@ -164,7 +237,6 @@ k_lat_node(DevPD d, LatticeDev L, double scale, int write_state) {
     double Ku[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
-    // incident elements (i-1|i, j-1|j, k-1|k), ascending id
 #pragma unroll
     for (int dz = (DIM == 3 ? -1 : 0); dz <= 0; ++dz)
 #pragma unroll
@@ -177,11 +249,15 @@ k_lat_node(DevPD d, LatticeDev L, double scale, int write_state) {
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) Ku[c] += d.G[e * DIM + c];
             }
+    // node flags: bit c = dof c constrained, bit 3 = carries external load
+    const uint8_t fl = L.nflag[n];
+    const double im = L.inv_mass[n];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
         const size_t q = (size_t)n * DIM + c;
-        const bool bc = d.bcflag[q] != 0;
-        const double acc = bc ? 0.0 : (d.P[q] * scale - d.Nsh * Ku[c]) / d.M[q];
+        const bool bc = (fl >> c) & 1;
+        const double p = (fl & 8) ? d.P[q] * scale : 0.0;
+        const double acc = bc ? 0.0 : (p - d.Nsh * Ku[c]) * im;
         double vel = d.rv[q] + d.c_corr_v * acc;
         const double dis = d.rd[q] + d.c_corr_d * acc;
         if (bc) vel = d.bcvel[q];
@@ -195,31 +271,32 @@ k_lat_node(DevPD d, LatticeDev L, double scale, int write_state) {
     }
 }
 
+// tile shapes
+#define BOND2 2, 32, 8, 1, 2
+#define BOND3 3, 16, 4, 4, 2
+
 size_t lattice_smem_bytes(int dim, int R, int S) {
-    const int TX = dim == 2 ? 32 : 16, TY = dim == 2 ? 8 : 4, TZ = dim == 2 ? 1 : 4;
-    const size_t napron =
-        (size_t)(TX + 2 * R) * (TY + 2 * R) * (dim == 3 ? TZ + 2 * R : 1);
-    return sizeof(double) * (dim * napron + 6 * (size_t)S) + sizeof(int) * 2 * (size_t)S;
+    return dim == 2 ? bond_smem<BOND2>(R, S) : bond_smem<BOND3>(R, S);
 }
 
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,
                          double scale, int write_state, bool time_bond, cudaEvent_t* ev,
                          cudaStream_t s) {
-    const int eb = (d.E + 255) / 256;
     const int nb = (d.N + 255) / 256;
     const size_t smem = lattice_smem_bytes(d.dim, L.R, L.S);
     if (d.dim == 2) {
-        k_lat_ubar<2><<<eb, 256, 0, s>>>(d, L);
+        using T = BondTile<BOND2>;
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[0], s));
-        dim3 grid((L.nx + 31) / 32, (L.ny + 7) / 8, 1);
-        k_lat_bond<2, 32, 8, 1><<<grid, 256, smem, s>>>(d, L, step, do_break);
+        dim3 grid((L.nx + 31) / 32, (L.ny + T::EY - 1) / T::EY, 1);
+        k_lat_bond<BOND2><<<grid, T::NT, smem, s>>>(d, L, step, do_break);
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[1], s));
         k_lat_node<2><<<nb, 256, 0, s>>>(d, L, scale, write_state);
     } else {
-        k_lat_ubar<3><<<eb, 256, 0, s>>>(d, L);
+        using T = BondTile<BOND3>;
+        k_lat_ubar<3><<<(d.E + 255) / 256, 256, 0, s>>>(d, L);
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[0], s));
-        dim3 grid((L.nx + 15) / 16, (L.ny + 3) / 4, (L.nz + 3) / 4);
-        k_lat_bond<3, 16, 4, 4><<<grid, 256, smem, s>>>(d, L, step, do_break);
+        dim3 grid((L.nx + 15) / 16, (L.ny + 3) / 4, (L.nz + T::EZ - 1) / T::EZ);
+        k_lat_bond<BOND3><<<grid, T::NT, smem, s>>>(d, L, step, do_break);
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[1], s));
         k_lat_node<3><<<nb, 256, 0, s>>>(d, L, scale, write_state);
     }
@@ -229,10 +306,10 @@ void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_b
 void lattice_configure(int dim, int R, int S) {
     const int bytes = (int)lattice_smem_bytes(dim, R, S);
     if (dim == 2)
-        PMTS_CUDA_S(cudaFuncSetAttribute(k_lat_bond<2, 32, 8, 1>,
+        PMTS_CUDA_S(cudaFuncSetAttribute(k_lat_bond<BOND2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     else
-        PMTS_CUDA_S(cudaFuncSetAttribute(k_lat_bond<3, 16, 4, 4>,
+        PMTS_CUDA_S(cudaFuncSetAttribute(k_lat_bond<BOND3>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 

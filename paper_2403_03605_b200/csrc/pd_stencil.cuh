@@ -16,8 +16,12 @@ struct LatticeDev {
     const int8_t* dj;
     const int8_t* dk;
     const int* delta_id; // linear element-id delta of each offset
-    const double* table; // per offset: xi[3], w c(|xi|), |xi|^2, ((1+s_crit)|xi|)^2
+    const double* table; // per offset, 8 doubles (layout in pd_stencil.cu)
+    const uint8_t* nflag;     // per node: bit c = dof c constrained, bit 3 = loaded
+    const double* inv_mass;   // per node: 1 / M (lumped mass is per node)
 };
+
+constexpr int kTableRow = 8;
 
 size_t lattice_smem_bytes(int dim, int R, int S);
 void lattice_configure(int dim, int R, int S);

@@ -77,6 +77,8 @@ struct pmts_pd {
     bool lattice = false;
     LatticeDev L{};
     std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
+    std::vector<double> hM, hP;      // host copies (per dof)
+    std::vector<uint8_t> hbc;        // per dof: constrained
     std::vector<void*> owned;
 
     ~pmts_pd() {
@@ -236,10 +238,10 @@ bool try_lattice(pmts_pd* h) {
     // per-offset constants from one representative bond of the positive offset;
     // the negative offset gets the exact negation (both directions of a bond then
     // evaluate bitwise-negated operands and agree on every break)
-    std::vector<double> table(6 * (size_t)S, 0.0);
+    std::vector<double> table(kTableRow * (size_t)S, 0.0);
     std::vector<char> have(S, 0);
     std::vector<uint32_t> mask((size_t)W * E, 0u);
-    const double s1 = 1.0 + h->desc.s_crit;
+    const double s0 = h->desc.s_crit, sl = s0 * (1.0 - h->desc.s_crit_spread);
     for (int e = 0; e < E; ++e)
         for (int q = 0; q < K; ++q) {
             const int p = h->hcol[(size_t)q * E + e];
@@ -258,13 +260,21 @@ bool try_lattice(pmts_pd* h) {
                 int di, dj, dk;
                 decode(offs[s], di, dj, dk);
                 const int sn = slot[key(-di, -dj, -dk)];
+                const double cthr = (2.0 * s0 + s0 * s0) * x2;
+                const double clo = h->desc.s_crit_spread != 0.0
+                                       ? (2.0 * sl + sl * sl) * x2 * (1.0 - 1e-12)
+                                       : cthr;
+                const int xs[3] = {0, 1, 4};
                 for (int k = 0; k < 3; ++k) {
-                    table[6 * s + k] = xi[k];
-                    table[6 * sn + k] = -xi[k];
+                    table[kTableRow * s + xs[k]] = xi[k];
+                    table[kTableRow * sn + xs[k]] = -xi[k];
                 }
-                table[6 * s + 3] = table[6 * sn + 3] = f;
-                table[6 * s + 4] = table[6 * sn + 4] = x2;
-                table[6 * s + 5] = table[6 * sn + 5] = s1 * s1 * x2;
+                for (int r : {s, sn}) {
+                    table[kTableRow * r + 2] = f;
+                    table[kTableRow * r + 3] = cthr;
+                    table[kTableRow * r + 5] = clo;
+                    table[kTableRow * r + 6] = x2;
+                }
                 have[sn] = 1;
             }
         }
@@ -289,12 +299,32 @@ bool try_lattice(pmts_pd* h) {
     int8_t* ddj = h->alloc<int8_t>(S);
     int8_t* ddk = h->alloc<int8_t>(S);
     int* ddl = h->alloc<int>(S);
-    double* dtab = h->alloc<double>(6 * (size_t)S);
+    double* dtab = h->alloc<double>(kTableRow * (size_t)S);
     upload(ddi, di.data(), S, h->stream);
     upload(ddj, dj.data(), S, h->stream);
     upload(ddk, dk.data(), S, h->stream);
     upload(ddl, dl.data(), S, h->stream);
-    upload(dtab, table.data(), 6 * (size_t)S, h->stream);
+    upload(dtab, table.data(), kTableRow * (size_t)S, h->stream);
+    // per-node flags and inverse lumped mass (the lumped mass is one value per node)
+    std::vector<uint8_t> nflag(h->N, 0);
+    std::vector<double> im(h->N, 0.0);
+    for (int n = 0; n < h->N; ++n) {
+        uint8_t f = 0;
+        for (int c = 0; c < dim; ++c) {
+            const size_t q = (size_t)n * dim + c;
+            if (h->hbc[q]) f |= uint8_t(1u << c);
+            if (h->hP[q] != 0.0) f |= 8u;
+            if (!h->hbc[q] && h->hM[q] != h->hM[(size_t)n * dim]) return false;
+        }
+        nflag[n] = f;
+        im[n] = 1.0 / h->hM[(size_t)n * dim];
+    }
+    uint8_t* dnf = h->alloc<uint8_t>(h->N);
+    double* dim_ = h->alloc<double>(h->N);
+    upload(dnf, nflag.data(), h->N, h->stream);
+    upload(dim_, im.data(), h->N, h->stream);
+    L.nflag = dnf;
+    L.inv_mass = dim_;
     L.di = ddi;
     L.dj = ddj;
     L.dk = ddk;
@@ -444,6 +474,9 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         for (int i = 0; i < h->ndof; ++i)
             if (!bcflag[i] && !(ds.mass[i] > 0.0))
                 throw SolverError("non-positive lumped mass at dof " + std::to_string(i));
+        h->hM.assign(ds.mass, ds.mass + h->ndof);
+        h->hP.assign(ds.p_ext, ds.p_ext + h->ndof);
+        h->hbc = bcflag;
         // geometry (mesh.hpp:112-139), host restatement, bit-exact
         h->cen.resize(3 * (size_t)E);
         h->vol.resize(E);
