@@ -23,6 +23,7 @@ SOURCES = [
     ("pd_det.cu", ["-fmad=false"]),
     ("pd_fast.cu", []),
     ("pd_stencil.cu", []),
+    ("pd_stencil_fused.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp"]

@@ -23,6 +23,30 @@ struct LatticeDev {
 
 constexpr int kTableRow = 8;
 
+// Fused single-kernel 2D step (pd_stencil_fused.cu) for the stencil sizes it is
+// instantiated for; per-offset constants travel in the kernel's parameter space.
+constexpr int kFusedS = 28;  // delta in [3, sqrt(10)) dx: the paper's / BASELINE's 3.015 dx
+constexpr int kFusedR = 3;
+constexpr int kFusedTX = 31, kFusedTY = 15;  // own elements; force region 32 x 16
+constexpr int kFusedAX = kFusedTX + 1 + 2 * kFusedR;
+struct Stencil2D {
+    double xi0[kFusedS], xi1[kFusedS], f[kFusedS], cthr[kFusedS], clo[kFusedS], x2[kFusedS];
+    int aoff[kFusedS];  // partner offset inside the shared ubar apron (dj * AX + di)
+    int did[kFusedS];   // partner element-id delta
+};
+
+struct FusedBufs {
+    const double* rd_in;
+    double* rd_out;
+    const uint32_t* mask_in;
+    uint32_t* mask_out;
+};
+
+void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
+                         const FusedBufs& b, int step, int do_break, double scale,
+                         int write_state, cudaStream_t s);
+void fused2d_configure();
+
 size_t lattice_smem_bytes(int dim, int R, int S);
 void lattice_configure(int dim, int R, int S);
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -77,6 +78,10 @@ struct pmts_pd {
     bool lattice = false;
     LatticeDev L{};
     std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
+    bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu)
+    Stencil2D st2{};
+    double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
+    uint32_t* mask_alt = nullptr;
     std::vector<double> hM, hP;      // host copies (per dof)
     std::vector<uint8_t> hbc;        // per dof: constrained
     std::vector<void*> owned;
@@ -340,6 +345,26 @@ bool try_lattice(pmts_pd* h) {
     h->d.coef = nullptr;
     h->stencil_delta = dl;
     lattice_configure(dim, R, S);
+    h->fused = false;
+    if (dim == 2 && S == kFusedS && R == kFusedR && !std::getenv("PMTS_NO_FUSED")) {
+        Stencil2D& st = h->st2;
+        for (int s = 0; s < S; ++s) {
+            const double* t = table.data() + kTableRow * (size_t)s;
+            st.xi0[s] = t[0];
+            st.xi1[s] = t[1];
+            st.f[s] = t[2];
+            st.cthr[s] = t[3];
+            st.clo[s] = t[5];
+            st.x2[s] = t[6];
+            st.aoff[s] = dj[s] * kFusedAX + di[s];
+            st.did[s] = dl[s];
+        }
+        if (!h->rd_alt) h->rd_alt = h->alloc<double>(h->ndof);
+        if (h->mask_alt) h->release(h->mask_alt);
+        h->mask_alt = h->alloc<uint32_t>((size_t)E);
+        fused2d_configure();
+        h->fused = true;
+    }
     CK(cudaStreamSynchronize(h->stream));
     h->lattice = true;
     return true;
@@ -386,6 +411,15 @@ void ensure_counts(pmts_pd* h, int n) {
 void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev,
                   bool last = true) {
     const int brk = h->fracture ? 1 : 0;
+    if (h->fused) {
+        FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
+        if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
+        launch_fused2d_step(h->d, h->L, h->st2, b, slot, brk, scale, last ? 1 : 0, h->stream);
+        if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
+        std::swap(h->d.rd, h->rd_alt);
+        std::swap(h->d.mask, h->mask_alt);
+        return;
+    }
     if (h->lattice) {
         launch_lattice_step(h->d, h->L, slot, brk, scale, last ? 1 : 0, time_bond, ev, h->stream);
         return;
@@ -682,6 +716,13 @@ int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
             const double nodek = E * dim * 8.0 + N * dim * 8.0 * 6 + N * dim * 1.0;
             info->bytes_per_step = ubar + bond + nodek;
             info->bond_bytes_per_step = bond;
+            if (h->fused) {
+                // rd in + out, rv in + out, 1/M, node flags, mask in + out
+                info->kernels_per_step = 1;
+                info->path = 2;
+                info->bytes_per_step = N * dim * 8.0 * 4 + N * 8.0 + N * 1.0 + E * 4.0 * 2;
+                info->bond_bytes_per_step = info->bytes_per_step;
+            }
         }
         info->device_bytes = h->device_bytes;
     });
