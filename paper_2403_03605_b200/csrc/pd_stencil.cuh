@@ -30,7 +30,9 @@ constexpr int kFusedR = 3;
 constexpr int kFusedTX = 31, kFusedTY = 15;  // own elements; force region 32 x 16
 constexpr int kFusedAX = kFusedTX + 1 + 2 * kFusedR;
 struct Stencil2D {
-    double xi0[kFusedS], xi1[kFusedS], f[kFusedS], cthr[kFusedS], clo[kFusedS], x2[kFusedS];
+    double xi0[kFusedS], xi1[kFusedS];    // representative xi of the offset
+    double fx0[kFusedS], fx1[kFusedS];    // w c(|xi|) xi
+    double cthr[kFusedS], clo[kFusedS], x2[kFusedS];
     int aoff[kFusedS];  // partner offset inside the shared ubar apron (dj * AX + di)
     int did[kFusedS];   // partner element-id delta
 };

@@ -7,11 +7,14 @@
 // bond forces of the 32 x 16 elements whose G the owned nodes need (its own
 // block plus one ring of neighbours, recomputed -- ~10% extra arithmetic
 // instead of a grid-wide dependency), and finishes with the Verlet update of
-// the owned nodes.  Nothing per-element ever goes to HBM except one mask word;
-// the per-offset constants live in the kernel's parameter space (constant
-// bank operands of the fp64 instructions).  Displacement and mask are
-// ping-ponged across steps so neighbouring CTAs never observe a half-updated
-// step.  Reference semantics as in pd_stencil.cu.
+// the owned nodes.  Nothing per-element goes to HBM except one mask word.
+//
+// Work split: 4 warps; lane = column of the 32-wide force region, warp w owns
+// rows 4w..4w+3, so every per-offset constant (kernel parameter space) is
+// fetched once per thread and used for 4 elements, and each shared-memory
+// load of a warp touches 32 consecutive apron cells.  Displacement and mask
+// are ping-ponged across steps so neighbouring CTAs never observe a
+// half-updated step.  Reference semantics as in pd_stencil.cu.
 #include <stdexcept>
 #include <string>
 
@@ -22,18 +25,19 @@ namespace pmts {
 namespace {
 
 constexpr int TX = kFusedTX, TY = kFusedTY, R = kFusedR;
-constexpr int GX = TX + 1, GY = TY + 1;       // force region (elements)
+constexpr int GX = TX + 1, GY = TY + 1;          // force region (elements)
 constexpr int AX = GX + 2 * R, AY = GY + 2 * R;  // ubar apron (elements)
 constexpr int BX = AX + 1, BY = AY + 1;          // node apron
-constexpr int NT = 256;
-static_assert(GX * GY == 2 * NT, "force region = 2 elements per thread");
+constexpr int NT = 128;
+constexpr int EPT = GY / (NT / 32);              // elements per thread (rows per warp)
+static_assert(GX == 32 && EPT * (NT / 32) == GY, "lane = column, warp = EPT rows");
 static_assert(AX == kFusedAX, "apron width");
 
 constexpr size_t kSmem = sizeof(double2) * (BX * BY + AX * AY + GX * GY);
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 4)
+__global__ void __launch_bounds__(NT, 6)
 k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs bf, int step,
           int do_break, double scale, int write_state) {
     extern __shared__ __align__(16) double2 sm2[];
@@ -43,7 +47,6 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
     const int tid = threadIdx.x;
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-    // node apron: nodes [i0-1-R, i0-1-R+BX) x [j0-1-R, ...)
     const double2* rd2 = reinterpret_cast<const double2*>(bf.rd_in);
     for (int q = tid; q < BX * BY; q += NT) {
         const int bx = q % BX, by = q / BX;
@@ -60,52 +63,65 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
         ub[q] = make_double2(d.Nsh * (((a.x + b.x) + c.x) + e.x),
                              d.Nsh * (((a.y + b.y) + c.y) + e.y));
     }
+
+    // per-thread elements: column gx = lane, rows gy = EPT*warp + r
+    const int gx = tid & 31, gy0 = (tid >> 5) * EPT;
+    const int ei = i0 - 1 + gx;
+    int e[EPT];
+    uint32_t m0[EPT], m[EPT];
+    double2 ue[EPT];
+    double G0[EPT], G1[EPT];
+    const int q0 = (gy0 + R) * AX + gx + R;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        const int ej = j0 - 1 + gy0 + r;
+        const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
+        e[r] = in ? ej * nx + ei : -1;
+        m0[r] = in ? bf.mask_in[e[r]] : 0u;
+        m[r] = m0[r];
+        G0[r] = 0.0;
+        G1[r] = 0.0;
+    }
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) ue[r] = ub[q0 + r * AX];
 
     unsigned long long nb = 0;
-#pragma unroll 1
-    for (int r = 0; r < 2; ++r) {
-        const int g = tid + r * NT;
-        const int gx = g % GX, gy = g / GX;
-        const int ei = i0 - 1 + gx, ej = j0 - 1 + gy;
-        double G0 = 0.0, G1 = 0.0;
-        if (ei >= 0 && ej >= 0 && ei < nx && ej < ny) {
-            const int e = ej * nx + ei;
-            const bool own = gx >= 1 && gy >= 1;
-            const int q0 = (gy + R) * AX + gx + R;
-            const double2 ue = ub[q0];
-            const uint32_t m0 = bf.mask_in[e];
-            uint32_t m = m0;
 #pragma unroll
-            for (int k = 0; k < kFusedS; ++k) {
-                if (m0 & (1u << k)) {
-                    const double2 up = ub[q0 + st.aoff[k]];
-                    const double e0 = up.x - ue.x, e1 = up.y - ue.y;
-                    const double dot = fma(st.xi1[k], e1, st.xi0[k] * e0);
-                    const double fd = st.f[k] * dot;
-                    G0 = fma(-fd, st.xi0[k], G0);
-                    G1 = fma(-fd, st.xi1[k], G1);
-                    if (do_break) {
-                        const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
-                        if (lhs >= st.clo[k]) {
-                            double thr = st.cthr[k];
-                            if (d.spread != 0.0) {
-                                const int p = e + st.did[k];
-                                const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
-                                                              e < p ? e : p, e < p ? p : e);
-                                thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
-                            }
-                            if (lhs >= thr) {
-                                m &= ~(1u << k);
-                                if (own && st.did[k] > 0) ++nb;
-                            }
-                        }
+    for (int k = 0; k < kFusedS; ++k) {
+        const double xi0 = st.xi0[k], xi1 = st.xi1[k];
+        const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
+        const double2* up_base = ub + q0 + st.aoff[k];
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+            if (!(m0[r] & (1u << k))) continue;
+            const double2 up = up_base[r * AX];
+            const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+            const double dot = fma(xi1, e1, xi0 * e0);
+            G0[r] = fma(-dot, fx0, G0[r]);
+            G1[r] = fma(-dot, fx1, G1[r]);
+            if (do_break) {
+                const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
+                if (lhs >= clo) {  // >= the smallest threshold any bond of the offset has
+                    double thr = st.cthr[k];
+                    if (d.spread != 0.0) {
+                        const int p = e[r] + st.did[k];
+                        const int lo = e[r] < p ? e[r] : p, hi = e[r] < p ? p : e[r];
+                        const double sb = bond_s_crit(d.s_crit, d.spread, d.seed, lo, hi);
+                        thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
+                    }
+                    if (lhs >= thr) {
+                        m[r] &= ~(1u << k);
+                        if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0) ++nb;
                     }
                 }
             }
-            if (own) bf.mask_out[e] = m;
         }
-        gt[g] = make_double2(G0, G1);
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        if (e[r] >= 0 && gx >= 1 && gy0 + r >= 1) bf.mask_out[e[r]] = m[r];
+        gt[(gy0 + r) * GX + gx] = make_double2(G0[r], G1[r]);
     }
     __syncthreads();
 
@@ -122,9 +138,9 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
         const size_t n = (size_t)nj * NX + ni;
         // incident elements (ni-1|ni, nj-1|nj) sit at force-region (lx|lx+1, ly|ly+1)
         const double2 a = gt[ly * GX + lx], b = gt[ly * GX + lx + 1];
-        const double2 c = gt[(ly + 1) * GX + lx], e = gt[(ly + 1) * GX + lx + 1];
-        const double k0 = d.Nsh * ((a.x + b.x) + (c.x + e.x));
-        const double k1 = d.Nsh * ((a.y + b.y) + (c.y + e.y));
+        const double2 c = gt[(ly + 1) * GX + lx], f = gt[(ly + 1) * GX + lx + 1];
+        const double k0 = d.Nsh * ((a.x + b.x) + (c.x + f.x));
+        const double k1 = d.Nsh * ((a.y + b.y) + (c.y + f.y));
         const uint8_t fl = L.nflag[n];
         const double im = L.inv_mass[n];
         double2 p = make_double2(0.0, 0.0);

@@ -352,7 +352,8 @@ bool try_lattice(pmts_pd* h) {
             const double* t = table.data() + kTableRow * (size_t)s;
             st.xi0[s] = t[0];
             st.xi1[s] = t[1];
-            st.f[s] = t[2];
+            st.fx0[s] = t[2] * t[0];
+            st.fx1[s] = t[2] * t[1];
             st.cthr[s] = t[3];
             st.clo[s] = t[5];
             st.x2[s] = t[6];

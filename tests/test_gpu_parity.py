@@ -104,7 +104,7 @@ def test_fast_mode_tolerances(name, path):
     over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
     g, sc, s = _solver(name, capi.FAST, **over)
     s.find_pe_pairs()
-    assert s.info()["path"] == (1 if path == "lattice" else 0)
+    assert s.info()["path"] in ((1, 2) if path == "lattice" else (0,))
     steps = g["meta"]["steps"]
     s.initial_acceleration(g["scale"][0])
     br = g["broken"]
