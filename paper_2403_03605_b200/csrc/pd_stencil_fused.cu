@@ -37,9 +37,10 @@ constexpr size_t kSmem = sizeof(double2) * (BX * BY + AX * AY + GX * GY);
 
 }  // namespace
 
+template <bool DO_BREAK>
 __global__ void __launch_bounds__(NT, 6)
 k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs bf, int step,
-          int do_break, double scale, int write_state) {
+          double scale, int write_state) {
     extern __shared__ __align__(16) double2 sm2[];
     double2* nt = sm2;                 // BX * BY node apron
     double2* ub = nt + BX * BY;        // AX * AY element apron
@@ -86,7 +87,11 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
 #pragma unroll
     for (int r = 0; r < EPT; ++r) ue[r] = ub[q0 + r * AX];
 
-    unsigned long long nb = 0;
+    // pass 1, branch-free: forces of all active bonds, and a candidate bit for
+    // every bond whose stretch reaches the smallest threshold of its offset
+    uint32_t cand[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) cand[r] = 0u;
 #pragma unroll
     for (int k = 0; k < kFusedS; ++k) {
         const double xi0 = st.xi0[k], xi1 = st.xi1[k];
@@ -94,26 +99,42 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
         const double2* up_base = ub + q0 + st.aoff[k];
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
-            if (!(m0[r] & (1u << k))) continue;
+            const bool act = (m0[r] >> k) & 1u;
             const double2 up = up_base[r * AX];
             const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
             const double dot = fma(xi1, e1, xi0 * e0);
-            G0[r] = fma(-dot, fx0, G0[r]);
-            G1[r] = fma(-dot, fx1, G1[r]);
-            if (do_break) {
+            const double dm = act ? dot : 0.0;
+            G0[r] = fma(-dm, fx0, G0[r]);
+            G1[r] = fma(-dm, fx1, G1[r]);
+            if (DO_BREAK) {
                 const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
-                if (lhs >= clo) {  // >= the smallest threshold any bond of the offset has
-                    double thr = st.cthr[k];
-                    if (d.spread != 0.0) {
-                        const int p = e[r] + st.did[k];
-                        const int lo = e[r] < p ? e[r] : p, hi = e[r] < p ? p : e[r];
-                        const double sb = bond_s_crit(d.s_crit, d.spread, d.seed, lo, hi);
-                        thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
-                    }
-                    if (lhs >= thr) {
-                        m[r] &= ~(1u << k);
-                        if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0) ++nb;
-                    }
+                cand[r] |= (act && lhs >= clo) ? (1u << k) : 0u;
+            }
+        }
+    }
+    // pass 2 (rare): exact per-bond thresholds for the candidates
+    unsigned long long nb = 0;
+    if (DO_BREAK) {
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+            uint32_t c = cand[r];
+            while (c) {
+                const int k = __ffs(c) - 1;
+                c &= c - 1;
+                const double2 up = ub[q0 + r * AX + st.aoff[k]];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(st.xi1[k], e1, st.xi0[k] * e0);
+                const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
+                double thr = st.cthr[k];
+                if (d.spread != 0.0) {
+                    const int p = e[r] + st.did[k];
+                    const int lo = e[r] < p ? e[r] : p, hi = e[r] < p ? p : e[r];
+                    const double sb = bond_s_crit(d.s_crit, d.spread, d.seed, lo, hi);
+                    thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
+                }
+                if (lhs >= thr) {
+                    m[r] &= ~(1u << k);
+                    if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0) ++nb;
                 }
             }
         }
@@ -168,7 +189,7 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
         rdo[n] = make_double2(u0 + d.dt * v0 + d.c_pred_d * a0, u1 + d.dt * v1 + d.c_pred_d * a1);
     }
 
-    if (do_break) {
+    if (DO_BREAK) {
         __shared__ unsigned long long part[NT / 32];
         for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
         if ((tid & 31) == 0) part[tid >> 5] = nb;
@@ -182,16 +203,20 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
 }
 
 void fused2d_configure() {
-    cudaError_t e = cudaFuncSetAttribute(k_fused2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmem);
-    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    for (auto fn : {k_fused2d<true>, k_fused2d<false>}) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+        if (e != cudaSuccess)
+            throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    }
 }
 
 void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                          const FusedBufs& b, int step, int do_break, double scale,
                          int write_state, cudaStream_t s) {
     dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, 1);
-    k_fused2d<<<grid, NT, kSmem, s>>>(d, L, st, b, step, do_break, scale, write_state);
+    if (do_break) k_fused2d<true><<<grid, NT, kSmem, s>>>(d, L, st, b, step, scale, write_state);
+    else k_fused2d<false><<<grid, NT, kSmem, s>>>(d, L, st, b, step, scale, write_state);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
