@@ -87,37 +87,58 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
 #pragma unroll
     for (int r = 0; r < EPT; ++r) ue[r] = ub[q0 + r * AX];
 
-    // pass 1, branch-free: forces of all active bonds, and a candidate bit for
-    // every bond whose stretch reaches the smallest threshold of its offset
-    uint32_t cand[EPT];
+    // pass 1, branch-free: forces of all active bonds, and one flag per element
+    // if any active bond reaches the smallest threshold of its offset.  Warps
+    // whose elements all carry the full intact stencil (the interior, nearly
+    // always) skip the per-bond activity selects.
+    bool anyc[EPT];
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) cand[r] = 0u;
+    for (int r = 0; r < EPT; ++r) anyc[r] = false;
+    constexpr uint32_t kFull = (1u << kFusedS) - 1u;
+    bool full = true;
 #pragma unroll
-    for (int k = 0; k < kFusedS; ++k) {
-        const double xi0 = st.xi0[k], xi1 = st.xi1[k];
-        const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
-        const double2* up_base = ub + q0 + st.aoff[k];
+    for (int r = 0; r < EPT; ++r) full = full && m0[r] == kFull;
+    if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
-        for (int r = 0; r < EPT; ++r) {
-            const bool act = (m0[r] >> k) & 1u;
-            const double2 up = up_base[r * AX];
-            const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
-            const double dot = fma(xi1, e1, xi0 * e0);
-            const double dm = act ? dot : 0.0;
-            G0[r] = fma(-dm, fx0, G0[r]);
-            G1[r] = fma(-dm, fx1, G1[r]);
-            if (DO_BREAK) {
-                const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
-                cand[r] |= (act && lhs >= clo) ? (1u << k) : 0u;
+        for (int k = 0; k < kFusedS; ++k) {
+            const double xi0 = st.xi0[k], xi1 = st.xi1[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
+            const double2* up_base = ub + q0 + st.aoff[k];
+#pragma unroll
+            for (int r = 0; r < EPT; ++r) {
+                const double2 up = up_base[r * AX];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(xi1, e1, xi0 * e0);
+                G0[r] = fma(-dot, fx0, G0[r]);
+                G1[r] = fma(-dot, fx1, G1[r]);
+                if (DO_BREAK) anyc[r] |= fma(2.0, dot, fma(e1, e1, e0 * e0)) >= clo;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kFusedS; ++k) {
+            const double xi0 = st.xi0[k], xi1 = st.xi1[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
+            const double2* up_base = ub + q0 + st.aoff[k];
+#pragma unroll
+            for (int r = 0; r < EPT; ++r) {
+                const bool act = (m0[r] >> k) & 1u;
+                const double2 up = up_base[r * AX];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(xi1, e1, xi0 * e0);
+                const double dm = act ? dot : 0.0;
+                G0[r] = fma(-dm, fx0, G0[r]);
+                G1[r] = fma(-dm, fx1, G1[r]);
+                if (DO_BREAK) anyc[r] |= act && fma(2.0, dot, fma(e1, e1, e0 * e0)) >= clo;
             }
         }
     }
-    // pass 2 (rare): exact per-bond thresholds for the candidates
+    // pass 2 (rare): exact per-bond thresholds for the flagged elements
     unsigned long long nb = 0;
     if (DO_BREAK) {
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
-            uint32_t c = cand[r];
+            uint32_t c = anyc[r] ? m0[r] : 0u;
             while (c) {
                 const int k = __ffs(c) - 1;
                 c &= c - 1;
