@@ -35,6 +35,7 @@ METRIC = "PD bond-updates/s (fp64)"
 UNIT = "bond-updates/s"
 REF_SAMPLE = "cfg3_sample"
 REF_FINE_PER_STEP = 1  # reference fine steps per bench step (bounded CPU sample)
+FP64_PEAK_TFLOPS = 37.0  # nominal B200 FP64 (vector); MEASURED_PEAKS.json has no fp64 figure
 
 
 def _env_rank():
@@ -98,12 +99,12 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic():
-    """dram bytes per bond-kernel launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "bond_kernel_traffic.json")
+def _ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
     return None
 
 
@@ -219,11 +220,19 @@ def bench_native(args):
     peak, peak_src = _peaks()
     bond_avg_s = bond_ms * 1e-3 / K
     achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
+    kname = {2: "k_fused2d", 1: "k_lat_bond"}.get(
+        info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": _ncu_traffic(),
-            "kernel": "k_fast_bond" if mode == capi.FAST else "k_det_bond",
-            "bytes_per_launch": info["bond_bytes_per_step"], "avg_launch_us": bond_avg_s * 1e6,
+            "frac": achieved / peak, "traffic": _ncu_traffic(kname),
+            "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],
+            "avg_launch_us": bond_avg_s * 1e6,
             "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
+    # the bond work is fp64-arithmetic heavy: 14 flops per directed entry in fast
+    # mode (eta 2, xi.eta 3, force 4, |eta|^2 3, test 2) = 28 per unique bond
+    flops = 28.0 * B / bond_avg_s / 1e12
+    roof_fp64 = {"bound": "fp64", "achieved": flops, "peak": FP64_PEAK_TFLOPS,
+                 "unit": "TFLOP/s", "frac": flops / FP64_PEAK_TFLOPS,
+                 "flops_per_bond": 28, "peak_source": "nominal B200 FP64 (no measured fp64 peak)"}
 
     # end to end through the public C-ABI with host buffers
     e2e = None
@@ -273,6 +282,7 @@ def bench_native(args):
                        "l2": f"inputs larger than L2 (device working set {ws:.0f} MB > 126 MB)",
                        "setup_s": t_setup},
             "roofline": roof,
+            "roofline_fp64": roof_fp64,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": K * info["kernels_per_step"],
