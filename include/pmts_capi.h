@@ -130,6 +130,12 @@ typedef struct {
     const double* notch_pts;
     int32_t lattice[3];          /* optional: elements per axis if the mesh is the generated
                                     lattice (enables the stencil fast path); 0 = unknown */
+    /* --- slab decomposition (multi-GPU); all zero for a single domain --- */
+    int64_t global_id_offset;    /* global id of local element 0 (per-bond hash uses global ids) */
+    int32_t owned_elems[2];      /* local element range this rank owns (broken counts); 0,0 = all */
+    double lattice_h;            /* > 0: stencil constants from the nominal lattice (xi = offset*h,
+                                    w = lattice_vol^2) so every rank's table is identical */
+    double lattice_vol;
 } pmts_pd_desc;
 
 typedef struct {
@@ -195,6 +201,27 @@ int pmts_pd_damage(pmts_pd* h, double* elem_out, double* node_out);
 int pmts_pd_gather_disp(pmts_pd* h, int32_t n, const int32_t* dofs, double* out);
 /* cudaStream_t of the handle (as void*) for callers that time on it. */
 void* pmts_pd_stream(pmts_pd* h);
+
+/* ------------------------------------------------------------------------
+ * Slab decomposition.  A rank's handle holds its slab plus a
+ * halo of whole node rows (2D) / layers (3D); after every fine step the
+ * predictor displacement of the boundary node rows goes to the neighbours.
+ * Node ranges are contiguous local node ids.
+ * ------------------------------------------------------------------------ */
+/* host <-> device copy of the predictor displacement rd of nodes [first, first+n)
+ * (host-mediated exchange; also the single-GPU emulation of several ranks) */
+int pmts_pd_get_rows(pmts_pd* h, int32_t first_node, int32_t n_nodes, double* out);
+int pmts_pd_set_rows(pmts_pd* h, int32_t first_node, int32_t n_nodes, const double* in);
+/* NCCL (loaded at run time): unique id of a new clique (128 bytes) */
+int pmts_nccl_unique_id(void* id_out);
+/* join the clique; then each fine step ends with ncclSend/ncclRecv of the halo rows
+ * to/from the lower (peer_lo) and upper (peer_hi) neighbour, -1 = none */
+int pmts_pd_comm_init(pmts_pd* h, const void* id, int32_t nranks, int32_t rank);
+int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t recv_lo_first,
+                     int32_t n_lo, int32_t peer_hi, int32_t send_hi_first,
+                     int32_t recv_hi_first, int32_t n_hi);
+/* sum of an int64 over the clique (broken counts at output cadence) */
+int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value);
 
 #ifdef __cplusplus
 }

@@ -38,6 +38,7 @@ struct po_pd {
     double* G;
     double delta, l, c0, c_const, h, s_crit, spread, gamma, beta, dt, N;
     uint64_t seed;
+    int64_t goff;
 };
 
 /* ------------------------------------------------------------------ */
@@ -410,6 +411,7 @@ po_pd* po_pd_create(int dim, int n_nodes, int n_elems, const int32_t* conn, cons
     h->kind = (int)iprm[0];
     h->seed = (uint64_t)iprm[1];
     h->variant = (int)iprm[2];
+    h->goff = iprm[3]; /* global id of local element 0 (slab tests) */
     const size_t nd = (size_t)h->n_dof;
     h->conn = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_elems * h->nn);
     memcpy(h->conn, conn, sizeof(int32_t) * (size_t)n_elems * h->nn);
@@ -448,7 +450,8 @@ po_pd* po_pd_create(int dim, int n_nodes, int n_elems, const int32_t* conn, cons
         h->xin[q] = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
         h->w[q] = vol[i] * vol[j];
         h->coef[q] = po_micromodulus(h, h->xin[q]);
-        h->scrit[q] = po_bond_s_crit(h->s_crit, h->spread, h->seed, i, j);
+        h->scrit[q] = po_bond_s_crit(h->s_crit, h->spread, h->seed, (int32_t)(i + h->goff),
+                                     (int32_t)(j + h->goff));
         h->mu[q] = 1;
     }
     h->u = (double*)calloc(nd, sizeof(double));

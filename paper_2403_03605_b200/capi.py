@@ -61,7 +61,9 @@ class PDDesc(C.Structure):
                 ("c0", _D), ("l", _D), ("c_const", _D), ("h", _D), ("s_crit", _D),
                 ("s_crit_spread", _D), ("seed", C.c_uint64), ("gamma", _D), ("beta", _D),
                 ("dt", _D), ("mode", _I), ("device", _I), ("n_notch", _I),
-                ("notch_npts", _P), ("notch_pts", _P), ("lattice", _I * 3)]
+                ("notch_npts", _P), ("notch_pts", _P), ("lattice", _I * 3),
+                ("global_id_offset", C.c_int64), ("owned_elems", _I * 2),
+                ("lattice_h", _D), ("lattice_vol", _D)]
 
 
 class PDInfo(C.Structure):
@@ -99,6 +101,12 @@ SIGNATURES = {
     "pmts_pd_damage": (C.c_int, [_P, _P, _P]),
     "pmts_pd_gather_disp": (C.c_int, [_P, _I, _P, _P]),
     "pmts_pd_stream": (_P, [_P]),
+    "pmts_pd_get_rows": (C.c_int, [_P, _I, _I, _P]),
+    "pmts_pd_set_rows": (C.c_int, [_P, _I, _I, _P]),
+    "pmts_nccl_unique_id": (C.c_int, [_P]),
+    "pmts_pd_comm_init": (C.c_int, [_P, _P, _I, _I]),
+    "pmts_pd_set_halo": (C.c_int, [_P, _I, _I, _I, _I, _I, _I, _I, _I]),
+    "pmts_pd_allreduce_sum": (C.c_int, [_P, C.POINTER(C.c_int64)]),
 }
 
 _lib = None

@@ -118,6 +118,27 @@ def scenarios() -> dict:
     return s
 
 
+def stacked(name: str, n: int) -> dict:
+    """Weak-scaling variant of a 2D plate scenario: n copies of its height stacked
+    (same dx, material, loads on the new top/bottom, notch at the new mid-height)."""
+    sc = get(name)
+    if n == 1:
+        return sc
+    m = sc["mesh"]
+    if m["dim"] != 2:
+        raise ValueError("stacked() is defined for the 2D plates")
+    x0, y0, x1, y1 = m["bounds"]
+    ly = (y1 - y0) * n
+    m["bounds"] = [x0, y0, x1, y0 + ly]
+    if m.get("notch1"):
+        a, b, c, d = m["notch1"]
+        mid = y0 + 0.5 * ly
+        m["notch1"] = [a, mid, c, mid]
+    t = sc["load"]["traction1"]
+    sc["load"]["traction1"] = [t[0], y0 + ly - 1e-7, t[2], y0 + ly + 1e-7, t[4], t[5]]
+    return sc
+
+
 def get(name: str, **over) -> dict:
     sc = copy.deepcopy(scenarios()[name])
     for k, v in over.items():

@@ -38,6 +38,8 @@ struct DevPD {
     double s_crit, spread;
     uint64_t seed;
     int fracture;
+    long long goff;      // global id of local element 0 (slab decomposition)
+    int own_lo, own_hi;  // owned local element range (broken counts, break log)
     // Newmark coefficients, each rounded exactly as the reference's expression
     double c_pred_v;  // dt*(1-gamma)              newmark.hpp:65
     double c_pred_d;  // (dt*dt)*(0.5-beta)        newmark.hpp:66
@@ -60,7 +62,8 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 // Per-bond critical stretch, BASELINE cfg3 extension: factor
 // U[1-spread, 1+spread] from a counter hash of (min id, max id, seed).
 // Explicit _rn intrinsics: never contracted, bitwise equal to the oracle.
-__device__ inline double bond_s_crit(double s_crit, double spread, uint64_t seed, int i, int j) {
+__device__ inline double bond_s_crit(double s_crit, double spread, uint64_t seed, long long i,
+                                     long long j) {
     if (spread == 0.0) return s_crit;
     const uint64_t key = ((uint64_t)(uint32_t)i << 32) | (uint64_t)(uint32_t)j;
     const uint64_t hv = splitmix64(seed ^ splitmix64(key));

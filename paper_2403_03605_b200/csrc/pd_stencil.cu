@@ -198,12 +198,13 @@ k_lat_bond(DevPD d, LatticeDev L, int step, int do_break) {
                         if (d.spread != 0.0) {
                             const int p = e + of.y;
                             const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
-                                                          e < p ? e : p, e < p ? p : e);
+                                                          (e < p ? e : p) + d.goff,
+                                                          (e < p ? p : e) + d.goff);
                             thr = fma(sb, sb, 2.0 * sb) * t[6];
                         }
                         if (lhs >= thr) {
                             m &= ~(1u << b);
-                            if (of.y > 0) ++nb;
+                            if (of.y > 0 && e >= d.own_lo && e < d.own_hi) ++nb;
                         }
                     }
                 }

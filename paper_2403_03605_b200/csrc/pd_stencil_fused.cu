@@ -150,12 +150,15 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
                 if (d.spread != 0.0) {
                     const int p = e[r] + st.did[k];
                     const int lo = e[r] < p ? e[r] : p, hi = e[r] < p ? p : e[r];
-                    const double sb = bond_s_crit(d.s_crit, d.spread, d.seed, lo, hi);
+                    const double sb =
+                        bond_s_crit(d.s_crit, d.spread, d.seed, lo + d.goff, hi + d.goff);
                     thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
                 }
                 if (lhs >= thr) {
                     m[r] &= ~(1u << k);
-                    if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0) ++nb;
+                    if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0 && e[r] >= d.own_lo &&
+                        e[r] < d.own_hi)
+                        ++nb;
                 }
             }
         }

@@ -15,6 +15,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "pd_common.cuh"
 #include "pd_stencil.cuh"
 #include "pmts_internal.h"
@@ -82,6 +85,10 @@ struct pmts_pd {
     Stencil2D st2{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
     uint32_t* mask_alt = nullptr;
+    // slab decomposition: NCCL clique + halo rows (node ranges, local ids)
+    void* comm = nullptr;            // ncclComm_t
+    int peer_lo = -1, peer_hi = -1;
+    int send_lo = 0, recv_lo = 0, n_lo = 0, send_hi = 0, recv_hi = 0, n_hi = 0;
     std::vector<double> hM, hP;      // host copies (per dof)
     std::vector<uint8_t> hbc;        // per dof: constrained
     std::vector<void*> owned;
@@ -120,6 +127,77 @@ double micromodulus(const pmts_pd_desc& dsc, int dim, double r) {
 }
 
 bool try_lattice(pmts_pd* h);
+
+// ---- NCCL, resolved at run time (libpmts loads without it; the halo exchange
+// of the slab decomposition is the only user).  Types follow nccl.h 2.x.
+struct NcclApi {
+    void* lib = nullptr;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclGetErrorString) err = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.lib) {
+        // the process may already hold torch's bundled NCCL; reuse whatever is loaded
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            api.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (api.lib) break;
+        }
+        if (!api.lib) throw InternalError("NCCL not found (dlopen libnccl.so.2)");
+        auto sym = [&](const char* n) {
+            void* p = dlsym(api.lib, n);
+            if (!p) throw InternalError(std::string("NCCL symbol missing: ") + n);
+            return p;
+        };
+        api.get_unique_id = (decltype(api.get_unique_id))sym("ncclGetUniqueId");
+        api.comm_init_rank = (decltype(api.comm_init_rank))sym("ncclCommInitRank");
+        api.send = (decltype(api.send))sym("ncclSend");
+        api.recv = (decltype(api.recv))sym("ncclRecv");
+        api.group_start = (decltype(api.group_start))sym("ncclGroupStart");
+        api.group_end = (decltype(api.group_end))sym("ncclGroupEnd");
+        api.all_reduce = (decltype(api.all_reduce))sym("ncclAllReduce");
+        api.comm_destroy = (decltype(api.comm_destroy))sym("ncclCommDestroy");
+        api.err = (decltype(api.err))sym("ncclGetErrorString");
+    }
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw InternalError(std::string("NCCL ") + what + ": " + nccl().err(r));
+}
+
+constexpr ncclDataType_t kNcclFloat64 = ncclFloat64;
+
+// halo exchange of the predictor displacement after a fine step
+void exchange_halo(pmts_pd* h) {
+    if (!h->comm || (h->peer_lo < 0 && h->peer_hi < 0)) return;
+    NcclApi& a = nccl();
+    const int dim = h->dim;
+    double* rd = h->d.rd;
+    nccl_check(a.group_start(), "group");
+    if (h->peer_lo >= 0) {
+        nccl_check(a.send(rd + (size_t)h->send_lo * dim, (size_t)h->n_lo * dim, kNcclFloat64,
+                          h->peer_lo, (ncclComm_t)h->comm, h->stream), "send");
+        nccl_check(a.recv(rd + (size_t)h->recv_lo * dim, (size_t)h->n_lo * dim, kNcclFloat64,
+                          h->peer_lo, (ncclComm_t)h->comm, h->stream), "recv");
+    }
+    if (h->peer_hi >= 0) {
+        nccl_check(a.send(rd + (size_t)h->send_hi * dim, (size_t)h->n_hi * dim, kNcclFloat64,
+                          h->peer_hi, (ncclComm_t)h->comm, h->stream), "send");
+        nccl_check(a.recv(rd + (size_t)h->recv_hi * dim, (size_t)h->n_hi * dim, kNcclFloat64,
+                          h->peer_hi, (ncclComm_t)h->comm, h->stream), "recv");
+    }
+    nccl_check(a.group_end(), "group");
+}
 
 // Family tables from the ELL partner list: per directed entry w c(|xi|)
 // computed on the host exactly as scatter_pe_block forms it
@@ -258,12 +336,24 @@ bool try_lattice(pmts_pd* h) {
             mask[(size_t)(s >> 5) * E + e] |= 1u << (s & 31);
             if (p > e && !have[s]) {
                 have[s] = 1;
-                double xi[3];
-                for (int k = 0; k < 3; ++k) xi[k] = h->cen[3 * (size_t)p + k] - h->cen[3 * (size_t)e + k];
-                const double x2 = xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2];
-                const double f = micromodulus(h->desc, dim, std::sqrt(x2)) * (h->vol[e] * h->vol[p]);
                 int di, dj, dk;
                 decode(offs[s], di, dj, dk);
+                double xi[3];
+                double wv = h->vol[e] * h->vol[p];
+                if (h->desc.lattice_h > 0.0) {
+                    // nominal lattice constants: identical on every rank of a slab
+                    // decomposition (the representative bond is not)
+                    const double hh = h->desc.lattice_h;
+                    xi[0] = di * hh;
+                    xi[1] = dj * hh;
+                    xi[2] = dk * hh;
+                    wv = h->desc.lattice_vol * h->desc.lattice_vol;
+                } else {
+                    for (int k = 0; k < 3; ++k)
+                        xi[k] = h->cen[3 * (size_t)p + k] - h->cen[3 * (size_t)e + k];
+                }
+                const double x2 = xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2];
+                const double f = micromodulus(h->desc, dim, std::sqrt(x2)) * wv;
                 const int sn = slot[key(-di, -dj, -dk)];
                 const double cthr = (2.0 * s0 + s0 * s0) * x2;
                 const double clo = h->desc.s_crit_spread != 0.0
@@ -419,10 +509,12 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
         if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
         std::swap(h->d.rd, h->rd_alt);
         std::swap(h->d.mask, h->mask_alt);
+        exchange_halo(h);
         return;
     }
     if (h->lattice) {
         launch_lattice_step(h->d, h->L, slot, brk, scale, last ? 1 : 0, time_bond, ev, h->stream);
+        exchange_halo(h);
         return;
     }
     if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
@@ -434,6 +526,7 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
     }
     if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
     launch_node_update(h->d, scale, 1, h->stream);
+    exchange_halo(h);
 }
 
 int64_t finish_steps(pmts_pd* h, int n) {
@@ -539,6 +632,16 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         d.spread = ds.s_crit_spread;
         d.seed = ds.seed;
         d.fracture = h->fracture;
+        d.goff = ds.global_id_offset;
+        d.own_lo = 0;
+        d.own_hi = E;
+        if (ds.owned_elems[0] != 0 || ds.owned_elems[1] != 0) {
+            if (ds.owned_elems[0] < 0 || ds.owned_elems[1] > E ||
+                ds.owned_elems[0] > ds.owned_elems[1])
+                throw ConfigError("owned element range out of bounds");
+            d.own_lo = ds.owned_elems[0];
+            d.own_hi = ds.owned_elems[1];
+        }
         const double dt = ds.dt, gm = ds.gamma, bt = ds.beta;
         d.c_pred_v = dt * (1.0 - gm);
         d.c_pred_d = dt * dt * (0.5 - bt);
@@ -605,7 +708,14 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
     });
 }
 
-void pmts_pd_destroy(pmts_pd* h) { delete h; }
+void pmts_pd_destroy(pmts_pd* h) {
+    if (h && h->comm) {
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        nccl().comm_destroy((ncclComm_t)h->comm);
+        h->comm = nullptr;
+    }
+    delete h;
+}
 
 int pmts_pd_build_families(pmts_pd* h) {
     return guard([&] {
@@ -750,6 +860,7 @@ int pmts_pd_init(pmts_pd* h, double scale0) {
         }
         launch_init_acc(h->d, scale0, h->stream);
         launch_predict(h->d, h->stream);
+        exchange_halo(h);
         CK(cudaStreamSynchronize(h->stream));
     });
 }
@@ -825,6 +936,7 @@ int pmts_pd_set_state(pmts_pd* h, const double* u, const double* v, const double
         if (v) upload(h->d.v, v, h->ndof, h->stream);
         if (a) upload(h->d.a, a, h->ndof, h->stream);
         launch_predict(h->d, h->stream);
+        exchange_halo(h);
         CK(cudaStreamSynchronize(h->stream));
     });
 }
@@ -890,5 +1002,79 @@ int pmts_pd_gather_disp(pmts_pd* h, int32_t n, const int32_t* dofs, double* out)
 }
 
 void* pmts_pd_stream(pmts_pd* h) { return h ? (void*)h->stream : nullptr; }
+
+int pmts_pd_get_rows(pmts_pd* h, int32_t first, int32_t n, double* out) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (first < 0 || n < 0 || first + n > h->N) throw ConfigError("node range out of bounds");
+        download(out, h->d.rd + (size_t)first * h->dim, (size_t)n * h->dim, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_set_rows(pmts_pd* h, int32_t first, int32_t n, const double* in) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (first < 0 || n < 0 || first + n > h->N) throw ConfigError("node range out of bounds");
+        upload(h->d.rd + (size_t)first * h->dim, in, (size_t)n * h->dim, h->stream);
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_nccl_unique_id(void* id_out) {
+    return guard([&] {
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "get unique id");
+        std::memcpy(id_out, &id, sizeof(id));
+    });
+}
+
+int pmts_pd_comm_init(pmts_pd* h, const void* id, int32_t nranks, int32_t rank) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ConfigError("bad rank / size");
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        CK(cudaSetDevice(h->desc.device));
+        ncclComm_t c = nullptr;
+        nccl_check(nccl().comm_init_rank(&c, nranks, uid, rank), "comm init");
+        h->comm = c;
+    });
+}
+
+int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t recv_lo_first,
+                     int32_t n_lo, int32_t peer_hi, int32_t send_hi_first,
+                     int32_t recv_hi_first, int32_t n_hi) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        auto ok = [&](int f, int n) { return f >= 0 && n >= 0 && f + n <= h->N; };
+        if ((peer_lo >= 0 && (!ok(send_lo_first, n_lo) || !ok(recv_lo_first, n_lo))) ||
+            (peer_hi >= 0 && (!ok(send_hi_first, n_hi) || !ok(recv_hi_first, n_hi))))
+            throw ConfigError("halo node range out of bounds");
+        h->peer_lo = peer_lo;
+        h->send_lo = send_lo_first;
+        h->recv_lo = recv_lo_first;
+        h->n_lo = n_lo;
+        h->peer_hi = peer_hi;
+        h->send_hi = send_hi_first;
+        h->recv_hi = recv_hi_first;
+        h->n_hi = n_hi;
+    });
+}
+
+int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (!h->comm) return;
+        int64_t* d = nullptr;
+        CK(cudaMallocAsync(&d, sizeof(int64_t), h->stream));
+        upload(d, value, 1, h->stream);
+        nccl_check(nccl().all_reduce(d, d, 1, ncclInt64, ncclSum, (ncclComm_t)h->comm, h->stream),
+                   "allreduce");
+        download(value, d, 1, h->stream);
+        CK(cudaFreeAsync(d, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
 
 }  // extern "C"

@@ -155,7 +155,8 @@ class PDSolver:
     def __init__(self, *, dim, nodes, conn, mass, p_ext, delta, dt, bc_dofs=None, bc_vel=None,
                  micromodulus=capi.MICRO_EXP, c0=0.0, l=1.0, c_const=0.0, h=1.0, s_crit=0.0,
                  s_crit_spread=0.0, seed=0, gamma=0.5, beta=0.0, mode=capi.DETERMINISTIC,
-                 device=0, notch_npts=None, notch_pts=None, lattice=(0, 0, 0)):
+                 device=0, notch_npts=None, notch_pts=None, lattice=(0, 0, 0),
+                 global_id_offset=0, owned_elems=(0, 0), lattice_h=0.0, lattice_vol=0.0):
         self.dim = dim
         self._nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
         self._conn = np.ascontiguousarray(conn, dtype=np.int32)
@@ -183,6 +184,9 @@ class PDSolver:
         d.n_notch, d.notch_npts, d.notch_pts = n_notch, ptr(self._npts), ptr(self._pts)
         for k in range(3):
             d.lattice[k] = lattice[k]
+        d.global_id_offset = int(global_id_offset)
+        d.owned_elems[0], d.owned_elems[1] = int(owned_elems[0]), int(owned_elems[1])
+        d.lattice_h, d.lattice_vol = float(lattice_h), float(lattice_vol)
         self.n_nodes, self.n_elems = d.n_nodes, d.n_elems
         self.n_dof = self.n_nodes * dim
         self.mode = mode
@@ -204,10 +208,19 @@ class PDSolver:
             kw.update(micromodulus=capi.MICRO_CONST, c_const=ext["c"], h=ext.get("h", 1.0))
         if ext.get("s_crit_spread"):
             kw.update(s_crit_spread=ext["s_crit_spread"], seed=int(ext.get("seed", 0)))
+        if any(sc.lattice):  # nominal stencil constants: same table as any slab run
+            kw.update(lattice_h=float(sc.nodes[1, 0] - sc.nodes[0, 0]),
+                      lattice_vol=float(sc.volume[0]))
         kw.update(over)
         s = cls(**kw)
         s.scenario = sc
         return s
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().pmts_nccl_unique_id(buf))
+        return buf.raw
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -297,6 +310,29 @@ class PDSolver:
         out = np.zeros(len(d))
         check(lib().pmts_pd_gather_disp(self.h, len(d), ptr(d), ptr(out)))
         return out
+
+    # -- slab decomposition ---------------------------------------------------
+    def get_rows(self, first, n) -> np.ndarray:
+        out = np.zeros(n * self.dim)
+        check(lib().pmts_pd_get_rows(self.h, first, n, ptr(out)))
+        return out
+
+    def set_rows(self, first, n, vals):
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        check(lib().pmts_pd_set_rows(self.h, first, n, ptr(v)))
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(uid, 128)
+        check(lib().pmts_pd_comm_init(self.h, buf, nranks, rank))
+
+    def set_halo(self, peer_lo, send_lo, recv_lo, n_lo, peer_hi, send_hi, recv_hi, n_hi):
+        check(lib().pmts_pd_set_halo(self.h, peer_lo, send_lo, recv_lo, n_lo, peer_hi,
+                                     send_hi, recv_hi, n_hi))
+
+    def allreduce_sum(self, v: int) -> int:
+        x = C.c_int64(v)
+        check(lib().pmts_pd_allreduce_sum(self.h, C.byref(x)))
+        return x.value
 
     # -- run_built's pure-PD loop ------------------------------------------
     def run(self, n_steps=None, batch=100):
