@@ -24,6 +24,7 @@ SOURCES = [
     ("pd_fast.cu", []),
     ("pd_stencil.cu", []),
     ("pd_stencil_fused.cu", []),
+    ("pd_strip2d.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp"]

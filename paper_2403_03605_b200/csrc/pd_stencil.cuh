@@ -49,6 +49,18 @@ void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& s
                          int write_state, cudaStream_t s);
 void fused2d_configure();
 
+// Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
+// positive offsets, in that kernel's order.
+struct StripStencil {
+    double xi0[14], xi1[14], fx0[14], fx1[14], clo[14], cthr[14], x2[14];
+    long long did[14];
+};
+int strip2d_pos_offset(int k, int* di, int* dj);  // returns the offset's stencil index
+void strip2d_configure();
+void launch_strip2d_step(const DevPD& d, const LatticeDev& L, const StripStencil& st,
+                         const FusedBufs& b, int step, int do_break, double scale,
+                         int write_state, int H, cudaStream_t s);
+
 size_t lattice_smem_bytes(int dim, int R, int S);
 void lattice_configure(int dim, int R, int S);
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,

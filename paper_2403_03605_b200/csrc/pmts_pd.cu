@@ -81,8 +81,11 @@ struct pmts_pd {
     bool lattice = false;
     LatticeDev L{};
     std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
-    bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu)
+    bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu / pd_strip2d.cu)
+    bool strip = false;              // ... the row-streaming bond-symmetric variant
+    int strip_h = 16;                // node rows per strip segment
     Stencil2D st2{};
+    StripStencil sst{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
     uint32_t* mask_alt = nullptr;
     // slab decomposition: NCCL clique + halo rows (node ranges, local ids)
@@ -455,6 +458,29 @@ bool try_lattice(pmts_pd* h) {
         h->mask_alt = h->alloc<uint32_t>((size_t)E);
         fused2d_configure();
         h->fused = true;
+        // row-streaming variant: constants of the 14 positive offsets
+        h->strip = !std::getenv("PMTS_FUSED_TILE");
+        if (h->strip) {
+            for (int k = 0; k < 14; ++k) {
+                int pdi = 0, pdj = 0;
+                const int s = strip2d_pos_offset(k, &pdi, &pdj);
+                if (di[s] != pdi || dj[s] != pdj) {
+                    h->strip = false;  // host stencil order differs: keep the tile kernel
+                    break;
+                }
+                const double* t = table.data() + kTableRow * (size_t)s;
+                h->sst.xi0[k] = t[0];
+                h->sst.xi1[k] = t[1];
+                h->sst.fx0[k] = t[2] * t[0];
+                h->sst.fx1[k] = t[2] * t[1];
+                h->sst.cthr[k] = t[3];
+                h->sst.clo[k] = t[5];
+                h->sst.x2[k] = t[6];
+                h->sst.did[k] = dl[s];
+            }
+            if (const char* e = std::getenv("PMTS_STRIP_H")) h->strip_h = std::max(8, std::atoi(e));
+            if (h->strip) strip2d_configure();
+        }
     }
     CK(cudaStreamSynchronize(h->stream));
     h->lattice = true;
@@ -505,7 +531,11 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
-        launch_fused2d_step(h->d, h->L, h->st2, b, slot, brk, scale, last ? 1 : 0, h->stream);
+        if (h->strip)
+            launch_strip2d_step(h->d, h->L, h->sst, b, slot, brk, scale, last ? 1 : 0,
+                                h->strip_h, h->stream);
+        else
+            launch_fused2d_step(h->d, h->L, h->st2, b, slot, brk, scale, last ? 1 : 0, h->stream);
         if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
         std::swap(h->d.rd, h->rd_alt);
         std::swap(h->d.mask, h->mask_alt);

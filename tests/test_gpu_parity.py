@@ -98,9 +98,12 @@ def test_bp_coarse_deterministic():
     assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
 
 
-@pytest.mark.parametrize("path", ["lattice", "ell"])
+@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "ell"])
 @pytest.mark.parametrize("name", SMALL)
-def test_fast_mode_tolerances(name, path):
+def test_fast_mode_tolerances(name, path, monkeypatch):
+    if path == "lattice-tile":  # the one-shot tile kernel instead of the row-streaming one
+        monkeypatch.setenv("PMTS_FUSED_TILE", "1")
+        path = "lattice"
     over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
     g, sc, s = _solver(name, capi.FAST, **over)
     s.find_pe_pairs()
