@@ -25,6 +25,7 @@ SOURCES = [
     ("pd_stencil.cu", []),
     ("pd_stencil_fused.cu", []),
     ("pd_strip2d.cu", []),
+    ("pd_tma2d.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp"]

@@ -1,6 +1,8 @@
 // Lattice-stencil family encoding (fast mode) -- see pd_stencil.cu.
 #pragma once
 
+#include <cuda.h>
+
 #include "pd_common.cuh"
 
 namespace pmts {
@@ -48,6 +50,22 @@ void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& s
                          const FusedBufs& b, int step, int do_break, double scale,
                          int write_state, cudaStream_t s);
 void fused2d_configure();
+
+// TMA-pipelined persistent variant (pd_tma2d.cu): tensor maps of the current
+// predictor displacement (as [NY][2NX] doubles), rv and the packed {1/M, flags}.
+struct TmaMaps {
+    CUtensorMap rd, rv, aux;
+};
+int tma2d_tile_x();
+int tma2d_tile_y();
+int tma2d_apron_box_x();
+int tma2d_apron_box_y();
+int tma2d_in_box_x();
+int tma2d_in_box_y();
+void tma2d_configure();
+void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
+                       const TmaMaps& maps, const FusedBufs& b, int step, int do_break,
+                       double scale, int write_state, cudaStream_t s);
 
 // Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
 // positive offsets, in that kernel's order.

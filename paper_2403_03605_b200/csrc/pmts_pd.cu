@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <dlfcn.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include "pd_common.cuh"
@@ -83,7 +84,11 @@ struct pmts_pd {
     std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
     bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu / pd_strip2d.cu)
     bool strip = false;              // ... the row-streaming bond-symmetric variant
+    bool tma = false;                // ... the TMA-pipelined persistent variant
     int strip_h = 16;                // node rows per strip segment
+    TmaMaps tmaps[2]{};              // tensor maps with rd = buffer 0 / buffer 1
+    double* rd_buf[2] = {nullptr, nullptr};
+    double* d_aux = nullptr;         // per node {1/M, flags} (TMA path)
     Stencil2D st2{};
     StripStencil sst{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
@@ -252,6 +257,38 @@ void finish_families(pmts_pd* h, int K) {
     h->families = true;
     h->lattice = false;
     if (h->mode == PMTS_FAST) try_lattice(h);
+}
+
+// TMA tensor maps for the persistent 2D kernel: rd (both ping-pong buffers),
+// rv, and the packed {1/M, flags}, all viewed as [NY][2 NX] doubles.
+void build_tma_maps(pmts_pd* h) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            throw InternalError("cuTensorMapEncodeTiled unavailable");
+        encode = (PFN_cuTensorMapEncodeTiled)fn;
+    }
+    const int NX = h->L.nx + 1, NY = h->L.ny + 1;
+    auto make = [&](CUtensorMap* m, void* base, int bx, int by) {
+        const cuuint64_t dims[2] = {(cuuint64_t)2 * NX, (cuuint64_t)NY};
+        const cuuint64_t strides[1] = {(cuuint64_t)2 * NX * sizeof(double)};
+        const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw InternalError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    };
+    for (int b = 0; b < 2; ++b) {
+        make(&h->tmaps[b].rd, h->rd_buf[b], tma2d_apron_box_x(), tma2d_apron_box_y());
+        make(&h->tmaps[b].rv, h->d.rv, tma2d_in_box_x(), tma2d_in_box_y());
+        make(&h->tmaps[b].aux, h->d_aux, tma2d_in_box_x(), tma2d_in_box_y());
+    }
 }
 
 // Stencil encoding of the families when the mesh is the generated lattice
@@ -458,8 +495,24 @@ bool try_lattice(pmts_pd* h) {
         h->mask_alt = h->alloc<uint32_t>((size_t)E);
         fused2d_configure();
         h->fused = true;
-        // row-streaming variant: constants of the 14 positive offsets
-        h->strip = !std::getenv("PMTS_FUSED_TILE");
+        // kernel variant: PMTS_FUSED_KERNEL = tma (default) | tile | strip
+        const char* kv = std::getenv("PMTS_FUSED_KERNEL");
+        const std::string kvs = kv ? kv : (std::getenv("PMTS_FUSED_TILE") ? "tile" : "tma");
+        h->strip = kvs == "strip";
+        h->tma = kvs == "tma";
+        if (h->tma) {
+            std::vector<double> aux(2 * (size_t)h->N);
+            for (int n = 0; n < h->N; ++n) {
+                aux[2 * (size_t)n] = im[n];
+                aux[2 * (size_t)n + 1] = (double)nflag[n];
+            }
+            if (!h->d_aux) h->d_aux = h->alloc<double>(2 * (size_t)h->N);
+            upload(h->d_aux, aux.data(), aux.size(), h->stream);
+            h->rd_buf[0] = h->d.rd;
+            h->rd_buf[1] = h->rd_alt;
+            build_tma_maps(h);
+            tma2d_configure();
+        }
         if (h->strip) {
             for (int k = 0; k < 14; ++k) {
                 int pdi = 0, pdj = 0;
@@ -531,7 +584,10 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
-        if (h->strip)
+        if (h->tma)
+            launch_tma2d_step(h->d, h->L, h->st2, h->tmaps[h->d.rd == h->rd_buf[0] ? 0 : 1], b,
+                              slot, brk, scale, last ? 1 : 0, h->stream);
+        else if (h->strip)
             launch_strip2d_step(h->d, h->L, h->sst, b, slot, brk, scale, last ? 1 : 0,
                                 h->strip_h, h->stream);
         else

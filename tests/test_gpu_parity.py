@@ -98,11 +98,11 @@ def test_bp_coarse_deterministic():
     assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
 
 
-@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "ell"])
+@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "lattice-strip", "ell"])
 @pytest.mark.parametrize("name", SMALL)
 def test_fast_mode_tolerances(name, path, monkeypatch):
-    if path == "lattice-tile":  # the one-shot tile kernel instead of the row-streaming one
-        monkeypatch.setenv("PMTS_FUSED_TILE", "1")
+    if path.startswith("lattice-"):  # the other fused 2D kernel variants (default: tma)
+        monkeypatch.setenv("PMTS_FUSED_KERNEL", path.split("-")[1])
         path = "lattice"
     over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
     g, sc, s = _solver(name, capi.FAST, **over)
