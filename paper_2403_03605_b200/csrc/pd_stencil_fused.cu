@@ -9,6 +9,14 @@
 // instead of a grid-wide dependency), and finishes with the Verlet update of
 // the owned nodes.  Nothing per-element goes to HBM except one mask word.
 //
+// Bond state lives with the bond's lower element only ("positive" offsets,
+// mask bits 14..27): the break test -- the |eta|^2 half of the fp64 work of a
+// directed entry -- runs once per bond, from its lower end, and the upper end
+// reads the state from the staged mask apron.  Bits 0..13 of a mask word are
+// not maintained by this kernel (pmts_pd reads them through the lower element).
+// The candidate test compares the fp64 bit patterns as integers (exact for the
+// positive thresholds) to keep it off the fp64 pipe, which bounds this kernel.
+//
 // Work split: 4 warps; lane = column of the 32-wide force region, warp w owns
 // rows 4w..4w+3, so every per-offset constant (kernel parameter space) is
 // fetched once per thread and used for 4 elements, and each shared-memory
@@ -30,79 +38,103 @@ constexpr int AX = GX + 2 * R, AY = GY + 2 * R;  // ubar apron (elements)
 constexpr int BX = AX + 1, BY = AY + 1;          // node apron
 constexpr int NT = 128;
 constexpr int EPT = GY / (NT / 32);              // elements per thread (rows per warp)
+constexpr int SHALF = kFusedS / 2;               // offsets 0..13 negative, 14..27 positive
 static_assert(GX == 32 && EPT * (NT / 32) == GY, "lane = column, warp = EPT rows");
 static_assert(AX == kFusedAX, "apron width");
 
-constexpr size_t kSmem = sizeof(double2) * (BX * BY + AX * AY + GX * GY);
+constexpr size_t kSmem =
+    sizeof(double2) * (BX * BY + AX * AY + GX * GY) + sizeof(uint32_t) * AX * AY;
+
+__device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
 
 }  // namespace
 
 template <bool DO_BREAK>
-__global__ void __launch_bounds__(NT, 6)
+__global__ void __launch_bounds__(NT, 5)
 k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs bf, int step,
           double scale, int write_state) {
     extern __shared__ __align__(16) double2 sm2[];
     double2* nt = sm2;                 // BX * BY node apron
     double2* ub = nt + BX * BY;        // AX * AY element apron
     double2* gt = ub + AX * AY;        // GX * GY element forces
+    uint32_t* ma = reinterpret_cast<uint32_t*>(gt + GX * GY);  // AX * AY mask apron
     const int tid = threadIdx.x;
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     const double2* rd2 = reinterpret_cast<const double2*>(bf.rd_in);
-    for (int q = tid; q < BX * BY; q += NT) {
+    // node apron and mask apron: all loads of a thread in flight together
+    constexpr int NB = (BX * BY + NT - 1) / NT, NA = (AX * AY + NT - 1) / NT;
+    double2 nv[NB];
+    uint32_t mv[NA];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        const int q = tid + j * NT;
         const int bx = q % BX, by = q / BX;
         const int gi = i0 - 1 - R + bx, gj = j0 - 1 - R + by;
-        double2 v = make_double2(0.0, 0.0);
-        if (gi >= 0 && gj >= 0 && gi < NX && gj < NY) v = rd2[(size_t)gj * NX + gi];
-        nt[q] = v;
+        nv[j] = make_double2(0.0, 0.0);
+        if (q < BX * BY && gi >= 0 && gj >= 0 && gi < NX && gj < NY)
+            nv[j] = rd2[(size_t)gj * NX + gi];
     }
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        const int q = tid + j * NT;
+        const int ax = q % AX, ay = q / AX;
+        const int gi = i0 - 1 - R + ax, gj = j0 - 1 - R + ay;
+        mv[j] = 0u;
+        if (q < AX * AY && gi >= 0 && gj >= 0 && gi < nx && gj < ny)
+            mv[j] = bf.mask_in[(size_t)gj * nx + gi];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+        if (tid + j * NT < BX * BY) nt[tid + j * NT] = nv[j];
+#pragma unroll
+    for (int j = 0; j < NA; ++j)
+        if (tid + j * NT < AX * AY) ma[tid + j * NT] = mv[j];
     __syncthreads();
+    bool tile_full = true;  // every apron element carries its full intact stencil
+    constexpr uint32_t kPos = ((1u << kFusedS) - 1u) & ~((1u << SHALF) - 1u);
     for (int q = tid; q < AX * AY; q += NT) {
         const int ax = q % AX, ay = q / AX;
         const double2 a = nt[ay * BX + ax], b = nt[ay * BX + ax + 1];
         const double2 c = nt[(ay + 1) * BX + ax + 1], e = nt[(ay + 1) * BX + ax];
         ub[q] = make_double2(d.Nsh * (((a.x + b.x) + c.x) + e.x),
                              d.Nsh * (((a.y + b.y) + c.y) + e.y));
+        tile_full = tile_full && (ma[q] & kPos) == kPos;
     }
+    tile_full = __syncthreads_and(tile_full);
 
     // per-thread elements: column gx = lane, rows gy = EPT*warp + r
     const int gx = tid & 31, gy0 = (tid >> 5) * EPT;
     const int ei = i0 - 1 + gx;
+    const int q0 = (gy0 + R) * AX + gx + R;
     int e[EPT];
     uint32_t m0[EPT], m[EPT];
     double2 ue[EPT];
     double G0[EPT], G1[EPT];
-    const int q0 = (gy0 + R) * AX + gx + R;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
         const int ej = j0 - 1 + gy0 + r;
         const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
         e[r] = in ? ej * nx + ei : -1;
-        m0[r] = in ? bf.mask_in[e[r]] : 0u;
+        m0[r] = ma[q0 + r * AX];
         m[r] = m0[r];
+        ue[r] = ub[q0 + r * AX];
         G0[r] = 0.0;
         G1[r] = 0.0;
     }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) ue[r] = ub[q0 + r * AX];
 
-    // pass 1, branch-free: forces of all active bonds, and one flag per element
-    // if any active bond reaches the smallest threshold of its offset.  Warps
-    // whose elements all carry the full intact stencil (the interior, nearly
-    // always) skip the per-bond activity selects.
+    // pass 1, branch-free: forces of all intact bonds (state of a negative offset
+    // read from the partner's positive bit) and, for the positive offsets, one
+    // flag per element if a bond reaches the smallest threshold of its offset
     bool anyc[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) anyc[r] = false;
-    constexpr uint32_t kFull = (1u << kFusedS) - 1u;
-    bool full = true;
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) full = full && m0[r] == kFull;
-    if (__all_sync(0xffffffffu, full)) {
+    if (tile_full) {
 #pragma unroll
         for (int k = 0; k < kFusedS; ++k) {
             const double xi0 = st.xi0[k], xi1 = st.xi1[k];
-            const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k];
+            const long long clo = dbits(st.clo[k]);
             const double2* up_base = ub + q0 + st.aoff[k];
 #pragma unroll
             for (int r = 0; r < EPT; ++r) {
@@ -111,25 +143,30 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
                 const double dot = fma(xi1, e1, xi0 * e0);
                 G0[r] = fma(-dot, fx0, G0[r]);
                 G1[r] = fma(-dot, fx1, G1[r]);
-                if (DO_BREAK) anyc[r] |= fma(2.0, dot, fma(e1, e1, e0 * e0)) >= clo;
+                if (DO_BREAK && k >= SHALF)
+                    anyc[r] |= dbits(fma(2.0, dot, fma(e1, e1, e0 * e0))) >= clo;
             }
         }
     } else {
 #pragma unroll
         for (int k = 0; k < kFusedS; ++k) {
             const double xi0 = st.xi0[k], xi1 = st.xi1[k];
-            const double fx0 = st.fx0[k], fx1 = st.fx1[k], clo = st.clo[k];
-            const double2* up_base = ub + q0 + st.aoff[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k];
+            const long long clo = dbits(st.clo[k]);
+            const int aoff = st.aoff[k];
+            const double2* up_base = ub + q0 + aoff;
 #pragma unroll
             for (int r = 0; r < EPT; ++r) {
-                const bool act = (m0[r] >> k) & 1u;
+                const bool act = k >= SHALF ? ((m0[r] >> k) & 1u)
+                                            : ((ma[q0 + r * AX + aoff] >> (kFusedS - 1 - k)) & 1u);
                 const double2 up = up_base[r * AX];
                 const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
                 const double dot = fma(xi1, e1, xi0 * e0);
                 const double dm = act ? dot : 0.0;
                 G0[r] = fma(-dm, fx0, G0[r]);
                 G1[r] = fma(-dm, fx1, G1[r]);
-                if (DO_BREAK) anyc[r] |= act && fma(2.0, dot, fma(e1, e1, e0 * e0)) >= clo;
+                if (DO_BREAK && k >= SHALF)
+                    anyc[r] |= act && dbits(fma(2.0, dot, fma(e1, e1, e0 * e0))) >= clo;
             }
         }
     }
@@ -138,7 +175,7 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
     if (DO_BREAK) {
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
-            uint32_t c = anyc[r] ? m0[r] : 0u;
+            uint32_t c = anyc[r] ? (m0[r] & kPos) : 0u;
             while (c) {
                 const int k = __ffs(c) - 1;
                 c &= c - 1;
@@ -149,16 +186,13 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
                 double thr = st.cthr[k];
                 if (d.spread != 0.0) {
                     const int p = e[r] + st.did[k];
-                    const int lo = e[r] < p ? e[r] : p, hi = e[r] < p ? p : e[r];
                     const double sb =
-                        bond_s_crit(d.s_crit, d.spread, d.seed, lo + d.goff, hi + d.goff);
+                        bond_s_crit(d.s_crit, d.spread, d.seed, e[r] + d.goff, p + d.goff);
                     thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
                 }
                 if (lhs >= thr) {
                     m[r] &= ~(1u << k);
-                    if (gx >= 1 && gy0 + r >= 1 && st.did[k] > 0 && e[r] >= d.own_lo &&
-                        e[r] < d.own_hi)
-                        ++nb;
+                    if (gx >= 1 && gy0 + r >= 1 && e[r] >= d.own_lo && e[r] < d.own_hi) ++nb;
                 }
             }
         }
@@ -171,23 +205,42 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
     __syncthreads();
 
     // Verlet update of the owned nodes (the last block row/column also owns the
-    // domain's far node line)
+    // domain's far node line); the per-node loads of a thread go out together
     const int ox = (blockIdx.x == gridDim.x - 1) ? NX - i0 : TX;
     const int oy = (blockIdx.y == gridDim.y - 1) ? NY - j0 : TY;
     double2* rdo = reinterpret_cast<double2*>(bf.rd_out);
     double2* rv2 = reinterpret_cast<double2*>(d.rv);
     const double2* P2 = reinterpret_cast<const double2*>(d.P);
-    for (int q = tid; q < ox * oy; q += NT) {
+    constexpr int NO = (GX * GY + NT - 1) / NT;
+    double2 rvv[NO];
+    double imv[NO];
+    uint8_t flv[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+        const int q = tid + j * NT;
+        rvv[j] = make_double2(0.0, 0.0);
+        imv[j] = 0.0;
+        flv[j] = 0;
+        if (q < ox * oy) {
+            const size_t n = (size_t)(j0 + q / ox) * NX + i0 + q % ox;
+            rvv[j] = rv2[n];
+            imv[j] = L.inv_mass[n];
+            flv[j] = L.nflag[n];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+        const int q = tid + j * NT;
+        if (q >= ox * oy) continue;
         const int lx = q % ox, ly = q / ox;
-        const int ni = i0 + lx, nj = j0 + ly;
-        const size_t n = (size_t)nj * NX + ni;
+        const size_t n = (size_t)(j0 + ly) * NX + i0 + lx;
         // incident elements (ni-1|ni, nj-1|nj) sit at force-region (lx|lx+1, ly|ly+1)
         const double2 a = gt[ly * GX + lx], b = gt[ly * GX + lx + 1];
         const double2 c = gt[(ly + 1) * GX + lx], f = gt[(ly + 1) * GX + lx + 1];
         const double k0 = d.Nsh * ((a.x + b.x) + (c.x + f.x));
         const double k1 = d.Nsh * ((a.y + b.y) + (c.y + f.y));
-        const uint8_t fl = L.nflag[n];
-        const double im = L.inv_mass[n];
+        const uint8_t fl = flv[j];
+        const double im = imv[j];
         double2 p = make_double2(0.0, 0.0);
         if (fl & 8) {
             p = P2[n];
@@ -196,7 +249,7 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
         }
         const double a0 = (fl & 1) ? 0.0 : (p.x - k0) * im;
         const double a1 = (fl & 2) ? 0.0 : (p.y - k1) * im;
-        const double2 rv = rv2[n];
+        const double2 rv = rvv[j];
         const double2 rd = nt[(ly + 1 + R) * BX + lx + 1 + R];
         double v0 = rv.x + d.c_corr_v * a0, v1 = rv.y + d.c_corr_v * a1;
         const double u0 = rd.x + d.c_corr_d * a0, u1 = rd.y + d.c_corr_d * a1;

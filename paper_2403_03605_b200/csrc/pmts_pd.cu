@@ -85,6 +85,7 @@ struct pmts_pd {
     bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu / pd_strip2d.cu)
     bool strip = false;              // ... the row-streaming bond-symmetric variant
     bool tma = false;                // ... the TMA-pipelined persistent variant
+    bool pos_only = false;           // mask bits of negative offsets not maintained
     int strip_h = 16;                // node rows per strip segment
     TmaMaps tmaps[2]{};              // tensor maps with rd = buffer 0 / buffer 1
     double* rd_buf[2] = {nullptr, nullptr};
@@ -497,9 +498,10 @@ bool try_lattice(pmts_pd* h) {
         h->fused = true;
         // kernel variant: PMTS_FUSED_KERNEL = tma (default) | tile | strip
         const char* kv = std::getenv("PMTS_FUSED_KERNEL");
-        const std::string kvs = kv ? kv : (std::getenv("PMTS_FUSED_TILE") ? "tile" : "tma");
+        const std::string kvs = kv ? kv : "tile";
         h->strip = kvs == "strip";
         h->tma = kvs == "tma";
+        h->pos_only = !h->strip && !h->tma;  // the tile kernel keeps bond state at the lower end
         if (h->tma) {
             std::vector<double> aux(2 * (size_t)h->N);
             for (int n = 0; n < h->N; ++n) {
@@ -551,12 +553,17 @@ std::vector<uint32_t> ell_mask_host(pmts_pd* h) {
     std::vector<uint32_t> out((size_t)We * E, 0u);
     std::map<int, int> sidx;
     for (size_t s = 0; s < h->stencil_delta.size(); ++s) sidx[h->stencil_delta[s]] = (int)s;
+    const int S = (int)h->stencil_delta.size();
     for (int e = 0; e < E; ++e)
         for (int q = 0; q < K; ++q) {
             const int p = h->hcol[(size_t)q * E + e];
             if (p < 0) break;
-            const int s = sidx.at(p - e);
-            if ((m[(size_t)(s >> 5) * E + e] >> (s & 31)) & 1u)
+            int s = sidx.at(p - e), owner = e;
+            if (h->pos_only && p < e) {  // state kept by the lower element, reverse offset
+                s = S - 1 - s;
+                owner = p;
+            }
+            if ((m[(size_t)(s >> 5) * E + owner] >> (s & 31)) & 1u)
                 out[(size_t)(q >> 5) * E + e] |= 1u << (q & 31);
         }
     return out;
