@@ -120,21 +120,23 @@ k_fused2d(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st, FusedBufs
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int x = lane + 32 * h;
-        if (x < AX) {
-            const int y0 = URB * warp;
-            double2 lo = make_double2(0.0, 0.0);
-            if (y0 < AY) {
-                const double2 a = nt[y0 * BX + x], b = nt[y0 * BX + x + 1];
-                lo = make_double2(a.x + b.x, a.y + b.y);
+        const int y0 = URB * warp;
+        if (x < AX && y0 < AY) {
+            // all node pairs of the band first (independent shared loads in flight),
+            // then the sums; rows past the apron read the (zero-padded) top node row
+            double2 hs[URB + 1];
+#pragma unroll
+            for (int i = 0; i <= URB; ++i) {
+                const int y = min(y0 + i, BY - 1);
+                const double2 a = nt[y * BX + x], b = nt[y * BX + x + 1];
+                hs[i] = make_double2(a.x + b.x, a.y + b.y);
             }
 #pragma unroll
             for (int i = 0; i < URB; ++i) {
                 const int y = y0 + i;
                 if (y < AY) {
-                    const double2 a = nt[(y + 1) * BX + x], b = nt[(y + 1) * BX + x + 1];
-                    const double2 hi = make_double2(a.x + b.x, a.y + b.y);
-                    ub[y * AX + x] = make_double2(d.Nsh * (lo.x + hi.x), d.Nsh * (lo.y + hi.y));
-                    lo = hi;
+                    ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
+                                                  d.Nsh * (hs[i].y + hs[i + 1].y));
                     tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
                 }
             }
