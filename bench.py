@@ -274,13 +274,14 @@ def bench_native(args):
         hu[:], hv[:], ha[:] = u0, v0, a0
         tracked = np.array([2 * (s.n_nodes // 2) + 1], dtype=np.int32)
         scales = sc.scales(step0, K)
+        trk = torch.empty((1, len(tracked)), dtype=torch.float64, pin_memory=True).numpy()
+        nbk = torch.empty(1, dtype=torch.int64, pin_memory=True).numpy()
         barrier()
         t = time.perf_counter()
         s.set_state(hu, hv, ha)
-        for k in range(K):
-            s.step(scales[k:k + 1])
-            s.gather_disp(tracked)
-        u1, v1, a1 = s.state()
+        for k in range(K):  # per step: scale in; tracked displacement + broken count out
+            s.step_tracked(scales[k:k + 1], tracked, trk, nbk)
+        s.get_state_into(hu, hv, ha)
         e2e_s = time.perf_counter() - t
         if dist:
             te = torch.tensor([e2e_s], dtype=torch.float64)

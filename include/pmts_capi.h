@@ -178,7 +178,13 @@ int pmts_pd_init(pmts_pd* h, double scale0);
  * perifem.hpp:356-364 is implicit in the matrix-free force).
  * n_broken_out (optional): bonds newly broken over the n steps. */
 int pmts_pd_step(pmts_pd* h, int32_t n, const double* load_scale, int64_t* n_broken_out);
-/* Same, timed on the handle's stream with CUDA events (device ms). */
+/* n fine steps that also report, per step, the displacement of n_tracked dofs
+ * (the tracked points run_built records every step, driver_run.hpp:204-208,241)
+ * into tracked_out[n][n_tracked] and the bonds broken in that step into
+ * broken_out[n] -- one device->host copy and one synchronisation per call. */
+int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* load_scale, int32_t n_tracked,
+                         const int32_t* dofs, double* tracked_out, int64_t* broken_out);
+/* Same as pmts_pd_step, timed on the handle's stream with CUDA events (device ms). */
 int pmts_pd_step_timed(pmts_pd* h, int32_t n, const double* load_scale, float* ms_out);
 /* Per-kernel device time of the dominant (bond) kernel over n steps, with
  * CUDA events around each of its launches (ms summed) -- roofline input. */

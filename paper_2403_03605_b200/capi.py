@@ -92,6 +92,7 @@ SIGNATURES = {
     "pmts_pd_init": (C.c_int, [_P, _D]),
     "pmts_pd_step": (C.c_int, [_P, _I, _P, C.POINTER(C.c_int64)]),
     "pmts_pd_step_timed": (C.c_int, [_P, _I, _P, C.POINTER(C.c_float)]),
+    "pmts_pd_step_tracked": (C.c_int, [_P, _I, _P, _I, _P, _P, _P]),
     "pmts_pd_profile": (C.c_int, [_P, _I, _P, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "pmts_pd_get_state": (C.c_int, [_P, _P, _P, _P]),
     "pmts_pd_set_state": (C.c_int, [_P, _P, _P, _P]),

@@ -285,6 +285,17 @@ void launch_damage(const DevPD& d, double* elem, double* node, cudaStream_t s) {
     PMTS_CUDA(cudaFreeAsync(has, s));
 }
 
+__global__ void k_gather(const double* src, const int32_t* idx, int n, double* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+void launch_gather(const double* src, const int32_t* idx, int n, double* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    k_gather<<<(n + 127) / 128, 128, 0, s>>>(src, idx, n, dst);
+    PMTS_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------------------
 // Neighbour build: find_pe_pairs (mesh.hpp:416-495) as a device cell list.
 // Same cell function (cells of size delta from the minimum centroid), same

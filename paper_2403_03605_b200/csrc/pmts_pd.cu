@@ -969,6 +969,45 @@ int pmts_pd_step(pmts_pd* h, int32_t n, const double* scales, int64_t* n_broken_
     });
 }
 
+int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_tracked,
+                         const int32_t* dofs, double* tracked_out, int64_t* broken_out) {
+    return guard([&] {
+        require_families(h);
+        if (n < 0 || (n > 0 && !scales) || n_tracked < 0) throw ConfigError("bad arguments");
+        for (int j = 0; j < n_tracked; ++j)
+            if (dofs[j] < 0 || dofs[j] >= h->ndof) throw ConfigError("tracked dof out of range");
+        ensure_counts(h, std::max(n, 1));
+        // device staging: dofs, then per-step tracked values, counts alongside
+        const size_t bytes = sizeof(int32_t) * n_tracked + sizeof(double) * (size_t)n * n_tracked;
+        char* buf = nullptr;
+        if (bytes) CK(cudaMallocAsync(&buf, bytes, h->stream));
+        int32_t* didx = reinterpret_cast<int32_t*>(buf);
+        double* dtrk = reinterpret_cast<double*>(buf + ((sizeof(int32_t) * n_tracked + 7) & ~7));
+        if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
+        for (int s = 0; s < n; ++s) {
+            // u of step s: the fused kernel's displacement is the step's predictor
+            // (beta = 0), i.e. the rd buffer it consumed; the other paths write u
+            const bool every = !h->fused;
+            enqueue_step(h, s, scales[s], false, nullptr, every || s == n - 1);
+            const double* src = h->fused ? h->rd_alt : h->d.u;
+            launch_gather(src, didx, n_tracked, dtrk + (size_t)s * n_tracked, h->stream);
+        }
+        std::vector<unsigned long long> cnt(std::max(n, 1));
+        if (n_tracked && n)
+            download(tracked_out, dtrk, (size_t)n * n_tracked, h->stream);
+        download(cnt.data(), h->d_counts, n, h->stream);
+        if (buf) CK(cudaFreeAsync(buf, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        int64_t nb = 0;
+        for (int s = 0; s < n; ++s) {
+            nb += (int64_t)cnt[s];
+            if (broken_out) broken_out[s] = (int64_t)cnt[s];
+        }
+        h->gstep += n;
+        h->broken_total += nb;
+    });
+}
+
 int pmts_pd_step_timed(pmts_pd* h, int32_t n, const double* scales, float* ms_out) {
     return guard([&] {
         require_families(h);

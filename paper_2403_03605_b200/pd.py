@@ -259,6 +259,18 @@ class PDSolver:
         check(lib().pmts_pd_step(self.h, len(s), ptr(s), C.byref(nb)))
         return nb.value
 
+    def step_tracked(self, scales, dofs, out=None, broken=None):
+        """Steps + per-step tracked displacements and broken counts (one sync)."""
+        s = np.ascontiguousarray(scales, dtype=np.float64)
+        d = np.ascontiguousarray(dofs, dtype=np.int32)
+        if out is None:
+            out = np.zeros((len(s), len(d)))
+        if broken is None:
+            broken = np.zeros(len(s), dtype=np.int64)
+        check(lib().pmts_pd_step_tracked(self.h, len(s), ptr(s), len(d), ptr(d), ptr(out),
+                                         ptr(broken)))
+        return out, broken
+
     def step_timed(self, scales) -> float:
         s = np.ascontiguousarray(scales, dtype=np.float64)
         ms = C.c_float()
@@ -276,6 +288,10 @@ class PDSolver:
         u, v, a = (np.zeros(self.n_dof) for _ in range(3))
         check(lib().pmts_pd_get_state(self.h, ptr(u), ptr(v), ptr(a)))
         return u, v, a
+
+    def get_state_into(self, u, v, a):
+        """get_state into caller-owned (e.g. pinned) float64 buffers."""
+        check(lib().pmts_pd_get_state(self.h, ptr(u), ptr(v), ptr(a)))
 
     def set_state(self, u=None, v=None, a=None):
         arrs = [None if x is None else np.ascontiguousarray(x, dtype=np.float64) for x in (u, v, a)]

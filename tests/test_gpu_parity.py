@@ -133,6 +133,30 @@ def test_fast_mode_tolerances(name, path, monkeypatch):
         assert agree >= 0.999, agree
 
 
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_step_tracked_reports_every_step(mode):
+    """pmts_pd_step_tracked: per-step tracked displacements and broken counts equal
+    single-step stepping (and, deterministic, the oracle's u at every step)."""
+    g, sc, s = _solver("mini", mode)
+    _, _, s2 = _solver("mini", mode)
+    s.find_pe_pairs()
+    s2.find_pe_pairs()
+    steps = 40
+    dofs = np.array([1, 2 * (sc.n_nodes // 2), 2 * sc.n_nodes - 1], dtype=np.int32)
+    s.initial_acceleration(g["scale"][0])
+    s2.initial_acceleration(g["scale"][0])
+    trk, nb = s.step_tracked(g["scale"][1:steps + 1], dofs)
+    ref_nb = []
+    for i in range(steps):
+        ref_nb.append(s2.step(g["scale"][i + 1:i + 2]))
+        u, _, _ = s2.state()
+        assert np.array_equal(trk[i], u[dofs])
+    assert list(nb) == ref_nb
+    u1, v1, a1 = s.state()
+    u2, v2, a2 = s2.state()
+    assert np.array_equal(u1, u2) and np.array_equal(v1, v2) and np.array_equal(a1, a2)
+
+
 # ----- known-answer tests on the device (test_perifem.cpp) ------------------
 
 def _kat_solver(mesh, pairs, s_crit, mode, delta=1.5, l=0.375):
