@@ -978,11 +978,12 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
             if (dofs[j] < 0 || dofs[j] >= h->ndof) throw ConfigError("tracked dof out of range");
         ensure_counts(h, std::max(n, 1));
         // device staging: dofs, then per-step tracked values, counts alongside
-        const size_t bytes = sizeof(int32_t) * n_tracked + sizeof(double) * (size_t)n * n_tracked;
+        const size_t idx_bytes = (sizeof(int32_t) * n_tracked + 7) & ~size_t(7);
+        const size_t bytes = idx_bytes + sizeof(double) * (size_t)n * n_tracked;
         char* buf = nullptr;
         if (bytes) CK(cudaMallocAsync(&buf, bytes, h->stream));
         int32_t* didx = reinterpret_cast<int32_t*>(buf);
-        double* dtrk = reinterpret_cast<double*>(buf + ((sizeof(int32_t) * n_tracked + 7) & ~7));
+        double* dtrk = reinterpret_cast<double*>(buf + idx_bytes);
         if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
         for (int s = 0; s < n; ++s) {
             // u of step s: the fused kernel's displacement is the step's predictor
