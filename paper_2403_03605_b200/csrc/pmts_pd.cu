@@ -98,12 +98,18 @@ struct pmts_pd {
     void* comm = nullptr;            // ncclComm_t
     int peer_lo = -1, peer_hi = -1;
     int send_lo = 0, recv_lo = 0, n_lo = 0, send_hi = 0, recv_hi = 0, n_hi = 0;
+    unsigned long long* h_counts = nullptr;  // pinned
+    int h_counts_cap = 0;
+    char* trk_buf = nullptr;         // pmts_pd_step_tracked staging
+    size_t trk_cap = 0;
+    std::vector<int32_t> trk_dofs;
     std::vector<double> hM, hP;      // host copies (per dof)
     std::vector<uint8_t> hbc;        // per dof: constrained
     std::vector<void*> owned;
 
     ~pmts_pd() {
         if (stream) cudaStreamSynchronize(stream);
+        if (h_counts) cudaFreeHost(h_counts);
         for (void* p : owned) cudaFree(p);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -622,12 +628,22 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
     exchange_halo(h);
 }
 
+// pinned host mirror of the per-step broken counts (async D2H, no staging copy)
+unsigned long long* pinned_counts(pmts_pd* h, int n) {
+    if (n > h->h_counts_cap) {
+        if (h->h_counts) cudaFreeHost(h->h_counts);
+        h->h_counts_cap = std::max(n, 64);
+        CK(cudaMallocHost(&h->h_counts, sizeof(unsigned long long) * h->h_counts_cap));
+    }
+    return h->h_counts;
+}
+
 int64_t finish_steps(pmts_pd* h, int n) {
-    std::vector<unsigned long long> cnt(n);
-    download(cnt.data(), h->d_counts, n, h->stream);
+    unsigned long long* cnt = pinned_counts(h, std::max(n, 1));
+    download(cnt, h->d_counts, n, h->stream);
     CK(cudaStreamSynchronize(h->stream));
     int64_t nb = 0;
-    for (auto c : cnt) nb += (int64_t)c;
+    for (int s = 0; s < n; ++s) nb += (int64_t)cnt[s];
     h->gstep += n;
     h->broken_total += nb;
     return nb;
@@ -977,14 +993,22 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
         for (int j = 0; j < n_tracked; ++j)
             if (dofs[j] < 0 || dofs[j] >= h->ndof) throw ConfigError("tracked dof out of range");
         ensure_counts(h, std::max(n, 1));
-        // device staging: dofs, then per-step tracked values, counts alongside
+        // device staging (kept across calls): dofs, then per-step tracked values
         const size_t idx_bytes = (sizeof(int32_t) * n_tracked + 7) & ~size_t(7);
         const size_t bytes = idx_bytes + sizeof(double) * (size_t)n * n_tracked;
-        char* buf = nullptr;
-        if (bytes) CK(cudaMallocAsync(&buf, bytes, h->stream));
-        int32_t* didx = reinterpret_cast<int32_t*>(buf);
-        double* dtrk = reinterpret_cast<double*>(buf + idx_bytes);
-        if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
+        if (bytes > h->trk_cap) {
+            if (h->trk_buf) h->release(h->trk_buf);
+            h->trk_cap = std::max<size_t>(bytes, 4096);
+            h->trk_buf = h->alloc<char>(h->trk_cap);
+            h->trk_dofs.clear();
+        }
+        int32_t* didx = reinterpret_cast<int32_t*>(h->trk_buf);
+        double* dtrk = reinterpret_cast<double*>(h->trk_buf + idx_bytes);
+        if (h->trk_dofs.size() != (size_t)n_tracked ||
+            !std::equal(h->trk_dofs.begin(), h->trk_dofs.end(), dofs)) {
+            h->trk_dofs.assign(dofs, dofs + n_tracked);
+            if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
+        }
         for (int s = 0; s < n; ++s) {
             // u of step s: the fused kernel's displacement is the step's predictor
             // (beta = 0), i.e. the rd buffer it consumed; the other paths write u
@@ -993,11 +1017,10 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
             const double* src = h->fused ? h->rd_alt : h->d.u;
             launch_gather(src, didx, n_tracked, dtrk + (size_t)s * n_tracked, h->stream);
         }
-        std::vector<unsigned long long> cnt(std::max(n, 1));
+        unsigned long long* cnt = pinned_counts(h, n);
         if (n_tracked && n)
             download(tracked_out, dtrk, (size_t)n * n_tracked, h->stream);
-        download(cnt.data(), h->d_counts, n, h->stream);
-        if (buf) CK(cudaFreeAsync(buf, h->stream));
+        download(cnt, h->d_counts, n, h->stream);
         CK(cudaStreamSynchronize(h->stream));
         int64_t nb = 0;
         for (int s = 0; s < n; ++s) {
