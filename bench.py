@@ -36,6 +36,14 @@ UNIT = "bond-updates/s"
 REF_SAMPLE = "cfg3_sample"
 REF_FINE_PER_STEP = 1  # reference fine steps per bench step (bounded CPU sample)
 FP64_PEAK_TFLOPS = 37.0  # nominal B200 FP64 (vector); MEASURED_PEAKS.json has no fp64 figure
+WORKLOADS = {
+    "cfg3": "cfg3 (BASELINE configs[2]: 2000x800 plate, dx 0.05 mm, delta 3.015 dx, "
+            "per-bond s0 x U[0.95,1.05], constant micromodulus)",
+    "cfg1": "cfg1 analog (BASELINE configs[0]: 200x80 plate, dx 0.5 mm, reference-native "
+            "exponential kernel l = delta)",
+    "cfg4": "cfg4 (BASELINE configs[3]: 3D 200x200x50 hex8 block, dx 0.5 mm, delta 3.015 dx, "
+            "constant micromodulus, 20 m/s +-5% impact patch)",
+}
 
 
 def _env_rank():
@@ -219,6 +227,10 @@ def bench_native(args):
     if world == 1 and not args.force_slabs:
         B = info["n_bonds"]
     K, W = args.steps, args.warmup
+    v0 = sc.initial_velocity()  # cfg4's impact patch (extension); zero for the plates
+    if v0.any() and world == 1 and not args.force_slabs:
+        z = np.zeros(s.n_dof)
+        s.set_state(z, v0, z)
     s.initial_acceleration(sc.load_scale(0.0))
     step0 = 1
     s.step(sc.scales(step0, W))
@@ -308,8 +320,7 @@ def bench_native(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": (f"{args.workload} (BASELINE configs[2]: 2000x800 plate, "
-                                    f"dx 0.05 mm, delta 3.015 dx, per-bond s0 x U[0.95,1.05])"
+            "config": {"workload": (WORKLOADS.get(args.workload, args.workload)
                                     + ("" if world == 1 else
                                        f"; weak scaling: {world} cfg3 slabs stacked into a "
                                        f"2000x{800 * world} plate, one slab per GPU")),

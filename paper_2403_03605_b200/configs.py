@@ -115,6 +115,36 @@ def scenarios() -> dict:
         "ext": {},
     }
     s["block3d"] = blk
+    # BASELINE cfg4: 3D impact block 200 x 200 x 50 at 0.5 mm (2.0M hexes), constant
+    # micromodulus c = 18K/(pi delta^4), s0 = sqrt(5 G0/(9 K delta)), 20 m/s +-5% seeded
+    # initial velocity on a 10 x 10 mm patch of the top face (extension: the reference
+    # has no initial-velocity hook), dt = 20 ns, 500 steps.
+    K4 = _E / (3.0 * (1.0 - 2.0 * 0.25))
+    c4 = {
+        "mesh": {"kind": "generated", "dim": 3, "bounds": [0, 0, 0, 0.1, 0.1, 0.025],
+                 "spacing": 5e-4, "notch1": None},
+        "material": {"E": _E, "nu": 0.25, "rho": _RHO, "formulation": "three_d"},
+        "pd": {"delta_factor": 3.015, "l_factor": 1.0,
+               "s_crit": round(s0_3d(_E, 0.25, _G0, d3d), 7)},
+        "load": {},
+        "time": {"dt_pd": 2e-8, "m": 1, "total_time": 2e-8 * 500, "gamma_pd": 0.5,
+                 "beta_pd": 0.0},
+        "run": {"mode": "pure_pd"},
+        "output": {"interval": 0.0},
+        "ext": {"micromodulus": "constant", "c": 18.0 * K4 / (math.pi * d3d ** 4),
+                "initial_velocity": {"lo": [0.045, 0.045, 0.025 - 1e-7],
+                                     "hi": [0.055, 0.055, 0.025 + 1e-7],
+                                     "comp": 2, "value": -20.0, "spread": 0.05,
+                                     "seed": 0x5eed5 + 4}},
+    }
+    s["cfg4"] = c4
+    # small 3D twin of cfg4 for tests (same physics, 20 x 20 x 10)
+    c4s = copy.deepcopy(c4)
+    c4s["mesh"]["bounds"] = [0, 0, 0, 0.01, 0.01, 0.005]
+    c4s["ext"]["initial_velocity"].update(lo=[0.003, 0.003, 0.005 - 1e-7],
+                                          hi=[0.007, 0.007, 0.005 + 1e-7])
+    c4s["time"]["total_time"] = 2e-8 * 100
+    s["cfg4_small"] = c4s
     return s
 
 

@@ -39,6 +39,25 @@ def _box3(v, dim, nvals):
     return lo + hi, vals
 
 
+def _splitmix64(x: int) -> int:
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def _hash_factor(i: int, j: int, seed: int, spread: float) -> float:
+    """U[1 - spread, 1 + spread] from the counter hash of (i, j, seed) -- the same
+    construction as the per-bond s0 factor (pd_common.cuh bond_s_crit)."""
+    if spread == 0.0:
+        return 1.0
+    key = ((i & 0xFFFFFFFF) << 32) | (j & 0xFFFFFFFF)
+    h = _splitmix64(seed ^ _splitmix64(key))
+    u = (h >> 11) * 2.0 ** -53
+    return (1.0 - spread) + (2.0 * spread) * u
+
+
 class Scenario:
     """build_scenario for a generated pure-PD run (host C++ setup in libpmts)."""
 
@@ -140,6 +159,24 @@ class Scenario:
     def scales(self, first_step: int, n: int) -> np.ndarray:
         """load_scale(i dt) for i = first_step .. first_step + n - 1 (driver_run.hpp:220)."""
         return np.array([self.load_scale(i * self.dt) for i in range(first_step, first_step + n)])
+
+    def initial_velocity(self) -> np.ndarray:
+        """BASELINE cfg4 extension: seeded velocity on a face patch (the reference has no
+        initial-velocity hook; its velocity BCs are re-imposed every step).  Per node in
+        the box: value * U[1 - spread, 1 + spread] from the same counter hash as the
+        per-bond s0 factor, keyed by (node id, component, seed)."""
+        v = np.zeros(self.n_dof)
+        iv = self.cfg.get("ext", {}).get("initial_velocity")
+        if not iv:
+            return v
+        lo, hi = np.array(iv["lo"]), np.array(iv["hi"])
+        d = self.dim
+        inside = np.all((self.nodes[:, :d] >= lo[:d]) & (self.nodes[:, :d] <= hi[:d]), axis=1)
+        ids = np.nonzero(inside)[0]
+        spread, seed = float(iv.get("spread", 0.0)), int(iv.get("seed", 0))
+        fac = np.array([_hash_factor(int(n), int(iv["comp"]), seed, spread) for n in ids])
+        v[ids * d + int(iv["comp"])] = float(iv["value"]) * fac
+        return v
 
     def notches(self):
         out, k = [], 0
@@ -355,6 +392,10 @@ class PDSolver:
         """driver_run.hpp:199-245 (minus file output): returns per-step broken counts."""
         sc = self.scenario
         n_steps = sc.n_steps if n_steps is None else n_steps
+        v0 = sc.initial_velocity()
+        if v0.any():
+            z = np.zeros(self.n_dof)
+            self.set_state(z, v0, z)
         self.initial_acceleration(sc.load_scale(0.0))
         broken = []
         i = 1
