@@ -26,6 +26,7 @@ SOURCES = [
     ("pd_stencil_fused.cu", []),
     ("pd_strip2d.cu", []),
     ("pd_tma2d.cu", []),
+    ("pd_lat3.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp"]

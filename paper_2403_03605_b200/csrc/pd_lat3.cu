@@ -1,0 +1,239 @@
+// 3D lattice bond kernel for the 122-offset stencil (delta in [3, sqrt(10)) dx,
+// BASELINE cfg4/cfg5's 3.015 dx), fast mode, nominal lattice constants.
+//
+// On the nominal lattice xi = h (di, dj, dk) with small compile-time integers,
+// and w c(|xi|) depends on |xi|^2 only (8 classes: 1,2,3,4,5,6,8,9 h^2).  The
+// 122 offsets are expanded at compile time (template recursion), so every
+// offset's partner address is an immediate shared-memory offset, the xi.eta
+// product is a handful of adds / small-integer multiplies, and the per-offset
+// constants collapse to 8 class values held in uniform registers -- no table
+// loads, no bit-scan loop (the generic stencil kernel spent ~46 instructions per
+// directed entry; this one ~20).
+//
+//   eta   = ubar_p - ubar_e
+//   G_e  -= (w c h^2) (o . eta) o                      (o = integer offset, xi = h o)
+//   test  2 h (o . eta) + |eta|^2 >= (2 s + s^2) h^2 |o|^2 -- the squared break test
+// CTA tile 16 x 4 x 4 elements + a 3-element ubar apron staged in shared memory
+// (SoA), one element per thread.  Reference semantics as in pd_stencil.cu.
+#include <stdexcept>
+#include <string>
+
+#include "pd_stencil.cuh"
+
+namespace pmts {
+
+namespace {
+
+constexpr int TX = 16, TY = 4, TZ = 4, R = 3;
+constexpr int AX = TX + 2 * R, AY = TY + 2 * R, AZ = TZ + 2 * R;
+constexpr int NA = AX * AY * AZ;
+constexpr int NT = TX * TY * TZ;
+constexpr int S3 = 122;
+
+struct Off3 {
+    int di[S3], dj[S3], dk[S3];
+};
+__host__ __device__ constexpr Off3 make_off3() {
+    Off3 o{};
+    int n = 0;
+    for (int k = -3; k <= 3; ++k)
+        for (int j = -3; j <= 3; ++j)
+            for (int i = -3; i <= 3; ++i) {
+                const int d2 = i * i + j * j + k * k;
+                if (d2 == 0 || d2 > 9) continue;
+                o.di[n] = i;
+                o.dj[n] = j;
+                o.dk[n] = k;
+                ++n;
+            }
+    return o;
+}
+// |o|^2 -> class index (|o|^2 = 7 does not occur on the integer lattice)
+__host__ __device__ constexpr int cls_of(int d2) {
+    return d2 <= 6 ? d2 - 1 : d2 == 8 ? 6 : 7;
+}
+
+template <int K>
+struct Ofs {
+    static constexpr Off3 o = make_off3();
+    static constexpr int di = o.di[K], dj = o.dj[K], dk = o.dk[K];
+    static constexpr int d2 = di * di + dj * dj + dk * dk;
+    static constexpr int cls = cls_of(d2);
+    static constexpr int aoff = (dk * AY + dj) * AX + di;
+};
+
+// c * e for a small compile-time integer c (exact for |c| <= 3 as adds)
+template <int C>
+__device__ __forceinline__ double imul(double e) {
+    if constexpr (C == 0) return 0.0;
+    else if constexpr (C == 1) return e;
+    else if constexpr (C == -1) return -e;
+    else if constexpr (C == 2) return e + e;
+    else if constexpr (C == -2) return -(e + e);
+    else return (double)C * e;
+}
+// acc + c * e
+template <int C>
+__device__ __forceinline__ double iaxpy(double acc, double e) {
+    if constexpr (C == 0) return acc;
+    else if constexpr (C == 1) return acc + e;
+    else if constexpr (C == -1) return acc - e;
+    else return fma((double)C, e, acc);
+}
+
+struct Ctx {
+    const double* ux;
+    const double* uy;
+    const double* uz;
+    int q0;
+    double ex, ey, ez;
+    uint32_t m[4];
+    double gx, gy, gz;
+    bool anyc;
+};
+
+template <int K, bool DO_BREAK>
+__device__ __forceinline__ void bond(Ctx& c, const Stencil3D& st) {
+    using O = Ofs<K>;
+    const int q = c.q0 + O::aoff;
+    const double e0 = c.ux[q] - c.ex, e1 = c.uy[q] - c.ey, e2 = c.uz[q] - c.ez;
+    double dot = imul<O::di>(e0);
+    dot = iaxpy<O::dj>(dot, e1);
+    dot = iaxpy<O::dk>(dot, e2);
+    const bool act = (c.m[K >> 5] >> (K & 31)) & 1u;
+    const double t = act ? dot * st.c[O::cls] : 0.0;
+    c.gx = iaxpy<-O::di>(c.gx, t);
+    c.gy = iaxpy<-O::dj>(c.gy, t);
+    c.gz = iaxpy<-O::dk>(c.gz, t);
+    if (DO_BREAK) {
+        const double lhs = fma(st.h2, dot, fma(e2, e2, fma(e1, e1, e0 * e0)));
+        c.anyc |= act && __double_as_longlong(lhs) >= st.clo[O::cls];
+    }
+}
+
+template <int K, bool DO_BREAK>
+struct Unroll {
+    static __device__ __forceinline__ void run(Ctx& c, const Stencil3D& st) {
+        bond<K, DO_BREAK>(c, st);
+        Unroll<K + 1, DO_BREAK>::run(c, st);
+    }
+};
+template <bool DO_BREAK>
+struct Unroll<S3, DO_BREAK> {
+    static __device__ __forceinline__ void run(Ctx&, const Stencil3D&) {}
+};
+
+}  // namespace
+
+bool lat3_offsets_match(const int8_t* di, const int8_t* dj, const int8_t* dk, int S) {
+    if (S != S3) return false;
+    constexpr Off3 o = make_off3();
+    for (int s = 0; s < S3; ++s)
+        if (di[s] != o.di[s] || dj[s] != o.dj[s] || dk[s] != o.dk[s]) return false;
+    return true;
+}
+int lat3_class_of(int d2) { return cls_of(d2); }
+
+template <bool DO_BREAK>
+__global__ void __launch_bounds__(NT, 3)
+k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int step) {
+    extern __shared__ double sm3[];
+    double* ux = sm3;
+    double* uy = sm3 + NA;
+    double* uz = sm3 + 2 * NA;
+    const int tid = threadIdx.x;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY, k0 = blockIdx.z * TZ;
+    for (int q = tid; q < NA; q += NT) {
+        const int ax = q % AX, r = q / AX;
+        const int ay = r % AY, az = r / AY;
+        const int gi = i0 + ax - R, gj = j0 + ay - R, gk = k0 + az - R;
+        const bool in = gi >= 0 && gj >= 0 && gk >= 0 && gi < L.nx && gj < L.ny && gk < L.nz;
+        const size_t ge = ((size_t)gk * L.ny + gj) * L.nx + gi;
+        ux[q] = in ? d.ubar[ge * 3] : 0.0;
+        uy[q] = in ? d.ubar[ge * 3 + 1] : 0.0;
+        uz[q] = in ? d.ubar[ge * 3 + 2] : 0.0;
+    }
+    __syncthreads();
+    const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
+    const int gi = i0 + tx, gj = j0 + ty, gk = k0 + tz;
+    unsigned long long nb = 0;
+    if (gi < L.nx && gj < L.ny && gk < L.nz) {
+        const int e = (gk * L.ny + gj) * L.nx + gi;
+        Ctx c;
+        c.ux = ux;
+        c.uy = uy;
+        c.uz = uz;
+        c.q0 = ((tz + R) * AY + ty + R) * AX + tx + R;
+        c.ex = ux[c.q0];
+        c.ey = uy[c.q0];
+        c.ez = uz[c.q0];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c.m[w] = d.mask[(size_t)w * d.E + e];
+        c.gx = c.gy = c.gz = 0.0;
+        c.anyc = false;
+        Unroll<0, DO_BREAK>::run(c, st);
+        if (DO_BREAK && c.anyc) {  // rare: exact per-bond thresholds (generic table)
+            uint32_t mw[4] = {c.m[0], c.m[1], c.m[2], c.m[3]};
+            for (int w = 0; w < 4; ++w) {
+                uint32_t live = c.m[w];
+                while (live) {
+                    const int b = __ffs(live) - 1;
+                    live &= live - 1;
+                    const int s = 32 * w + b;
+                    const int a = (L.dk[s] * AY + L.dj[s]) * AX + L.di[s];
+                    const double e0 = ux[c.q0 + a] - c.ex, e1 = uy[c.q0 + a] - c.ey,
+                                 e2 = uz[c.q0 + a] - c.ez;
+                    const double dot = fma((double)L.dk[s], e2,
+                                           fma((double)L.dj[s], e1, (double)L.di[s] * e0));
+                    const double lhs = fma(st.h2, dot, fma(e2, e2, fma(e1, e1, e0 * e0)));
+                    const int d2 = L.di[s] * L.di[s] + L.dj[s] * L.dj[s] + L.dk[s] * L.dk[s];
+                    const int p = e + L.delta_id[s];
+                    double thr = __longlong_as_double(st.cthr[cls_of(d2)]);
+                    if (d.spread != 0.0) {
+                        const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
+                                                      (e < p ? e : p) + d.goff,
+                                                      (e < p ? p : e) + d.goff);
+                        thr = fma(sb, sb, 2.0 * sb) * st.hh * d2;
+                    }
+                    if (lhs >= thr) {
+                        mw[w] &= ~(1u << b);
+                        if (p > e && e >= d.own_lo && e < d.own_hi) ++nb;
+                    }
+                }
+                if (mw[w] != c.m[w]) d.mask[(size_t)w * d.E + e] = mw[w];
+            }
+        }
+        d.G[(size_t)e * 3] = c.gx;
+        d.G[(size_t)e * 3 + 1] = c.gy;
+        d.G[(size_t)e * 3 + 2] = c.gz;
+    }
+    if (DO_BREAK) {
+        __shared__ unsigned long long part[NT / 32];
+        for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+        if ((tid & 31) == 0) part[tid >> 5] = nb;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < NT / 32; ++w) t += part[w];
+            if (t) atomicAdd(d.broken_count + step, t);
+        }
+    }
+}
+
+void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
+                      int do_break, cudaStream_t s) {
+    dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
+    constexpr size_t smem = sizeof(double) * 3 * NA;
+    static bool configured = false;
+    if (!configured) {
+        for (auto fn : {k_lat3_bond<true>, k_lat3_bond<false>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    if (do_break) k_lat3_bond<true><<<grid, NT, smem, s>>>(d, L, st, step);
+    else k_lat3_bond<false><<<grid, NT, smem, s>>>(d, L, st, step);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+}  // namespace pmts

@@ -282,8 +282,17 @@ size_t lattice_smem_bytes(int dim, int R, int S) {
 
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,
                          double scale, int write_state, bool time_bond, cudaEvent_t* ev,
-                         cudaStream_t s) {
+                         cudaStream_t s, const Stencil3D* st3) {
     const int nb = (d.N + 255) / 256;
+    if (d.dim == 3 && st3) {  // the specialised 122-offset kernel (pd_lat3.cu)
+        k_lat_ubar<3><<<(d.E + 255) / 256, 256, 0, s>>>(d, L);
+        if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[0], s));
+        launch_lat3_bond(d, L, *st3, step, do_break, s);
+        if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[1], s));
+        k_lat_node<3><<<nb, 256, 0, s>>>(d, L, scale, write_state);
+        PMTS_CUDA_S(cudaGetLastError());
+        return;
+    }
     const size_t smem = lattice_smem_bytes(d.dim, L.R, L.S);
     if (d.dim == 2) {
         using T = BondTile<BOND2>;

@@ -67,6 +67,20 @@ void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const TmaMaps& maps, const FusedBufs& b, int step, int do_break,
                        double scale, int write_state, cudaStream_t s);
 
+// 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class
+// (1,2,3,4,5,6,8,9): c = w c(h|o|) h^2, and the bit patterns of the smallest /
+// scalar thresholds (2 s + s^2) h^2 |o|^2.
+struct Stencil3D {
+    double c[8];
+    long long clo[8], cthr[8];
+    double h2;  // 2 h
+    double hh;  // h^2
+};
+bool lat3_offsets_match(const int8_t* di, const int8_t* dj, const int8_t* dk, int S);
+int lat3_class_of(int d2);
+void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
+                      int do_break, cudaStream_t s);
+
 // Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
 // positive offsets, in that kernel's order.
 struct StripStencil {
@@ -81,8 +95,9 @@ void launch_strip2d_step(const DevPD& d, const LatticeDev& L, const StripStencil
 
 size_t lattice_smem_bytes(int dim, int R, int S);
 void lattice_configure(int dim, int R, int S);
+struct Stencil3D;
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,
                          double scale, int write_state, bool time_bond, cudaEvent_t* ev,
-                         cudaStream_t s);
+                         cudaStream_t s, const Stencil3D* st3 = nullptr);
 
 }  // namespace pmts

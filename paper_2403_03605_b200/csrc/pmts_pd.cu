@@ -92,6 +92,8 @@ struct pmts_pd {
     double* d_aux = nullptr;         // per node {1/M, flags} (TMA path)
     Stencil2D st2{};
     StripStencil sst{};
+    bool lat3 = false;               // 3D 122-offset nominal-lattice bond kernel
+    Stencil3D st3{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
     uint32_t* mask_alt = nullptr;
     // slab decomposition: NCCL clique + halo rows (node ranges, local ids)
@@ -482,6 +484,33 @@ bool try_lattice(pmts_pd* h) {
     h->d.coef = nullptr;
     h->stencil_delta = dl;
     lattice_configure(dim, R, S);
+    // 3D, 122 offsets, nominal constants: class-constant table for pd_lat3.cu
+    h->lat3 = false;
+    if (dim == 3 && h->desc.lattice_h > 0.0 && lat3_offsets_match(di.data(), dj.data(), dk.data(), S) &&
+        !std::getenv("PMTS_NO_LAT3")) {
+        const double hh = h->desc.lattice_h;
+        bool ok = true, seen[8] = {false, false, false, false, false, false, false, false};
+        for (int s = 0; s < S && ok; ++s) {
+            const int d2 = di[s] * di[s] + dj[s] * dj[s] + dk[s] * dk[s];
+            const int cl = lat3_class_of(d2);
+            const double* t = table.data() + kTableRow * (size_t)s;
+            const double c = t[2] * (hh * hh);
+            long long clo, cth;
+            std::memcpy(&clo, &t[5], 8);
+            std::memcpy(&cth, &t[3], 8);
+            if (!seen[cl]) {
+                h->st3.c[cl] = c;
+                h->st3.clo[cl] = clo;
+                h->st3.cthr[cl] = cth;
+                seen[cl] = true;
+            } else {
+                ok = h->st3.c[cl] == c && h->st3.clo[cl] == clo && h->st3.cthr[cl] == cth;
+            }
+        }
+        h->st3.h2 = 2.0 * hh;
+        h->st3.hh = hh * hh;
+        h->lat3 = ok;
+    }
     h->fused = false;
     if (dim == 2 && S == kFusedS && R == kFusedR && !std::getenv("PMTS_NO_FUSED")) {
         Stencil2D& st = h->st2;
@@ -612,7 +641,8 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
         return;
     }
     if (h->lattice) {
-        launch_lattice_step(h->d, h->L, slot, brk, scale, last ? 1 : 0, time_bond, ev, h->stream);
+        launch_lattice_step(h->d, h->L, slot, brk, scale, last ? 1 : 0, time_bond, ev, h->stream,
+                            h->lat3 ? &h->st3 : nullptr);
         exchange_halo(h);
         return;
     }
@@ -962,7 +992,8 @@ int pmts_pd_init(pmts_pd* h, double scale0) {
             dd.rd = junk + h->ndof;
             CK(cudaMemcpyAsync(dd.rd, h->d.u, sizeof(double) * h->ndof,
                                cudaMemcpyDeviceToDevice, h->stream));
-            launch_lattice_step(dd, h->L, 0, 0, 0.0, 0, false, nullptr, h->stream);
+            launch_lattice_step(dd, h->L, 0, 0, 0.0, 0, false, nullptr, h->stream,
+                                h->lat3 ? &h->st3 : nullptr);
             CK(cudaFreeAsync(junk, h->stream));
         } else {
             launch_det_bond(h->d, h->d.u, 0, 0, 0, h->stream);
