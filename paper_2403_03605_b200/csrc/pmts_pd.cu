@@ -503,8 +503,8 @@ bool try_lattice(pmts_pd* h) {
                 h->st3.clo[cl] = clo;
                 h->st3.cthr[cl] = cth;
                 seen[cl] = true;
-            } else {
-                ok = h->st3.c[cl] == c && h->st3.clo[cl] == clo && h->st3.cthr[cl] == cth;
+            } else {  // same |o|^2: equal up to the rounding order of |xi|^2 (fast mode)
+                ok = std::abs(h->st3.c[cl] - c) <= 1e-14 * std::abs(c);
             }
         }
         h->st3.h2 = 2.0 * hh;
