@@ -228,7 +228,10 @@ def bench_native(args):
         B = info["n_bonds"]
     K, W = args.steps, args.warmup
     v0 = sc.initial_velocity()  # cfg4's impact patch (extension); zero for the plates
-    if v0.any() and world == 1 and not args.force_slabs:
+    if v0.any():
+        if world > 1 or args.force_slabs:  # this slab's nodes (halo included)
+            n0 = slab.node_first * sc.dim
+            v0 = v0[n0:n0 + s.n_dof]
         z = np.zeros(s.n_dof)
         s.set_state(z, v0, z)
     s.initial_acceleration(sc.load_scale(0.0))

@@ -155,8 +155,16 @@ def stacked(name: str, n: int) -> dict:
     if n == 1:
         return sc
     m = sc["mesh"]
-    if m["dim"] != 2:
-        raise ValueError("stacked() is defined for the 2D plates")
+    if m["dim"] == 3:  # 3D blocks stack along z (the slab axis); the impact patch stays on top
+        b = list(m["bounds"])
+        lz = (b[5] - b[2]) * n
+        b[5] = b[2] + lz
+        m["bounds"] = b
+        iv = sc["ext"].get("initial_velocity")
+        if iv:
+            iv["lo"][2] = b[5] - 1e-7
+            iv["hi"][2] = b[5] + 1e-7
+        return sc
     x0, y0, x1, y1 = m["bounds"]
     ly = (y1 - y0) * n
     m["bounds"] = [x0, y0, x1, y0 + ly]

@@ -16,8 +16,14 @@ pytestmark = pytest.mark.gpu
 def _run_slabs(sc, nranks, mode, steps):
     hs = [slabs.solver_for_slab(sc, slabs.make_slab(sc.lattice, sc.dim, r, nranks), mode)
           for r in range(nranks)]
+    v0 = sc.initial_velocity()
+    d = sc.dim
     for h in hs:
         h.find_pe_pairs()
+        if v0.any():
+            n0, n1 = h.slab.node_first, h.slab.node_first + h.slab.n_nodes
+            z = np.zeros(h.n_dof)
+            h.set_state(z, v0[n0 * d:n1 * d], z)
         h.initial_acceleration(sc.load_scale(0.0))
 
     def exchange():
@@ -41,10 +47,15 @@ def _run_slabs(sc, nranks, mode, steps):
 
 
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
-@pytest.mark.parametrize("name,nranks,steps", [("mini", 3, 80), ("cfg1", 4, 120)])
+@pytest.mark.parametrize("name,nranks,steps", [("mini", 3, 80), ("cfg1", 4, 120),
+                                               ("cfg4_small", 2, 60)])
 def test_slabs_equal_single_domain(mode, name, nranks, steps):
     sc = Scenario(cf.get(name))
     one = PDSolver.from_scenario(sc, mode=mode).find_pe_pairs()
+    v0 = sc.initial_velocity()
+    if v0.any():
+        z = np.zeros(sc.n_dof)
+        one.set_state(z, v0, z)
     one.initial_acceleration(sc.load_scale(0.0))
     nb1 = one.step([sc.load_scale(i * sc.dt) for i in range(1, steps + 1)])
     u, v, a = one.state()
