@@ -26,6 +26,7 @@ SOURCES = [
     ("pd_stencil_fused.cu", []),
     ("pd_strip2d.cu", []),
     ("pd_tma2d.cu", []),
+    ("pd_tile9.cu", []),
     ("pd_lat3.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
 ]

@@ -37,6 +37,7 @@ struct Stencil2D {
     double cthr[kFusedS], clo[kFusedS], x2[kFusedS];
     int aoff[kFusedS];  // partner offset inside the shared ubar apron (dj * AX + di)
     int did[kFusedS];   // partner element-id delta
+    int moff[kFusedS];  // partner offset inside the TMA mask box (dj * 40 + di; pd_tile9.cu)
 };
 
 struct FusedBufs {
@@ -65,6 +66,19 @@ int tma2d_in_box_y();
 void tma2d_configure();
 void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const TmaMaps& maps, const FusedBufs& b, int step, int do_break,
+                       double scale, int write_state, cudaStream_t s);
+
+// One-shot TMA-staged variant (pd_tile9.cu): tensor maps of the current rd
+// ([NY][2 NX] doubles), the current mask ([ny][nx] u32), rv and {1/M | flags}
+// ([NY][NXP] doubles, NXP even, flags in the three low mantissa bits).
+struct Tile9Maps {
+    CUtensorMap rd, mask, rv, im;
+};
+void tile9_boxes(int* rd_x, int* rd_y, int* ma_x, int* ma_y, int* rv_x, int* rv_y, int* im_x,
+                 int* im_y);
+int tile9_configure();  // returns resident CTAs per SM
+void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
+                       const Tile9Maps& maps, const FusedBufs& b, int step, int do_break,
                        double scale, int write_state, cudaStream_t s);
 
 // 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class

@@ -1,0 +1,344 @@
+// One-shot fused 2D fine step with TMA staging (tile v9), 28-offset stencil,
+// fast mode.  Arithmetic is the tile kernel's (pd_stencil_fused.cu: 31 x 31
+// owned elements, 32 x 32 force region, bond state at the lower end, integer
+// candidate compare); what changes is how the CTA gets its inputs:
+//
+//   * at launch one thread issues four cp.async.bulk.tensor loads completing on
+//     two mbarriers -- the node apron of the predictor displacement and the
+//     mask apron (needed first), and the owned nodes' rv and {1/M, flags}
+//     (needed last, so their latency hides behind the ubar and force passes).
+//     Out-of-domain parts of a box are zero-filled by the TMA unit, exactly the
+//     zeros the tile kernel writes with bounds-checked loads; no thread spends
+//     instructions on load addresses or bounds (the tile kernel's ncu source
+//     page put ~25 % of the stall samples on its staging phase and ~27 % on the
+//     node-update loads);
+//   * G aliases the ubar apron after the force pass, and the node flags ride
+//     in the three low mantissa bits of 1/M (relative change <= 2^-49, far
+//     below the fast-mode tolerance), so the whole CTA fits in 76.7 KB and
+//     three CTAs (24 warps) stay resident per SM.
+//
+// Requirements (checked by the host): nx % 4 == 0 (the mask rows must be a
+// multiple of 16 bytes for the tensor map).  Reference semantics as in
+// pd_stencil.cu.
+#include <stdexcept>
+#include <string>
+
+#include "pd_stencil.cuh"
+
+namespace pmts {
+
+namespace {
+
+constexpr int TX = 31, TY = 31, R = kFusedR;
+constexpr int GX = TX + 1, GY = TY + 1;          // force region (elements), 32 x 32
+constexpr int AX = GX + 2 * R, AY = GY + 2 * R;  // ubar apron (elements), 38 x 38
+constexpr int BX = AX + 1, BY = AY + 1;          // node apron, 39 x 39
+constexpr int MX = 40, MY = GY + R;              // mask box: the rows the force pass reads
+constexpr int IX = 32;                           // {1/M, flags} box row (16-byte multiple)
+constexpr int NW = 8, NT = 32 * NW;
+constexpr int EPT = GY / NW;
+constexpr int SHALF = kFusedS / 2;
+constexpr int URB = (AY + NW - 1) / NW;
+static_assert(GX == 32 && EPT * NW == GY, "lane = column, warp = EPT rows");
+static_assert(AX == kFusedAX, "Stencil2D apron offsets assume this width");
+
+constexpr int rup(int x, int a) { return (x + a - 1) / a * a; }
+constexpr int kNtBytes = BX * BY * 16;
+constexpr int kMaBytes = MX * MY * 4;
+constexpr int kRvBytes = TX * TY * 16;
+constexpr int kImBytes = IX * TY * 8;
+constexpr int kOffNt = 0;
+constexpr int kOffMa = rup(kOffNt + kNtBytes, 128);
+constexpr int kOffRv = rup(kOffMa + kMaBytes, 128);
+constexpr int kOffIm = rup(kOffRv + kRvBytes, 128);
+constexpr int kOffUb = rup(kOffIm + kImBytes, 16);
+constexpr int kOffBar = rup(kOffUb + AX * AY * 16, 8);
+constexpr int kOffPart = kOffBar + 16;
+constexpr int kSmem = kOffPart + 8 * NW;
+static_assert(GX * GY * 16 <= AX * AY * 16, "G fits in the ubar apron");
+static_assert(kSmem + 1024 <= 233472 / 3, "three CTAs per SM");
+
+__device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+                 "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(phase));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(b))
+        : "memory");
+}
+
+}  // namespace
+
+template <bool DO_BREAK>
+__global__ void __launch_bounds__(NT, 3)
+k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
+        const __grid_constant__ Tile9Maps maps, FusedBufs bf, int step, double scale,
+        int write_state) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const double2* nt = reinterpret_cast<const double2*>(sm + kOffNt);
+    const uint32_t* ma = reinterpret_cast<const uint32_t*>(sm + kOffMa);
+    const double2* rvs = reinterpret_cast<const double2*>(sm + kOffRv);
+    const double* ims = reinterpret_cast<const double*>(sm + kOffIm);
+    double2* ub = reinterpret_cast<double2*>(sm + kOffUb);
+    double2* gt = ub;  // G aliases the ubar apron once the force pass is done
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
+    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm + kOffPart);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    const int ax0 = i0 - 1 - R, ay0 = j0 - 1 - R;
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(sm) & 127u) __trap();  // TMA destinations need 128-byte alignment
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        mbar_expect_tx(&bar[0], kNtBytes + kMaBytes);
+        tma_load_2d(sm + kOffNt, &maps.rd, 2 * ax0, ay0, &bar[0]);
+        tma_load_2d(sm + kOffMa, &maps.mask, ax0, ay0, &bar[0]);
+        mbar_expect_tx(&bar[1], kRvBytes + kImBytes);
+        tma_load_2d(sm + kOffRv, &maps.rv, 2 * i0, j0, &bar[1]);
+        tma_load_2d(sm + kOffIm, &maps.im, i0, j0, &bar[1]);
+    }
+    __syncthreads();
+    mbar_wait(&bar[0], 0);
+
+    // (2) ubar of the apron (column walk with carried node-pair sums); the
+    //     positive-stencil completeness of every mask the force pass reads
+    constexpr uint32_t kPos = ((1u << kFusedS) - 1u) & ~((1u << SHALF) - 1u);
+    bool tile_full = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int x = lane + 32 * h;
+        const int y0 = URB * warp;
+        if (x < AX && y0 < AY) {
+            double2 hs[URB + 1];
+#pragma unroll
+            for (int i = 0; i <= URB; ++i) {
+                const int y = min(y0 + i, BY - 1);
+                const double2 a = nt[y * BX + x], b = nt[y * BX + x + 1];
+                hs[i] = make_double2(a.x + b.x, a.y + b.y);
+            }
+#pragma unroll
+            for (int i = 0; i < URB; ++i) {
+                const int y = y0 + i;
+                if (y < AY) {
+                    ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
+                                                  d.Nsh * (hs[i].y + hs[i + 1].y));
+                    if (y < MY) tile_full = tile_full && (ma[y * MX + x] & kPos) == kPos;
+                }
+            }
+        }
+    }
+    tile_full = __syncthreads_and(tile_full);
+
+    // (3) forces of the 32 x 32 region: column = lane, rows EPT*warp + r
+    const int gx = lane, gy0 = warp * EPT;
+    const int ei = i0 - 1 + gx;
+    const int q0 = (gy0 + R) * AX + gx + R;
+    const int qm = (gy0 + R) * MX + gx + R;
+    int e[EPT];
+    uint32_t m0[EPT], m[EPT];
+    double2 ue[EPT];
+    double G0[EPT], G1[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        const int ej = j0 - 1 + gy0 + r;
+        const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
+        e[r] = in ? ej * nx + ei : -1;
+        m0[r] = ma[qm + r * MX];
+        m[r] = m0[r];
+        ue[r] = ub[q0 + r * AX];
+        G0[r] = 0.0;
+        G1[r] = 0.0;
+    }
+    bool anyc[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) anyc[r] = false;
+    if (tile_full) {
+#pragma unroll
+        for (int k = 0; k < kFusedS; ++k) {
+            const double xi0 = st.xi0[k], xi1 = st.xi1[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k];
+            const long long clo = dbits(st.clo[k]);
+            const double2* up_base = ub + q0 + st.aoff[k];
+#pragma unroll
+            for (int r = 0; r < EPT; ++r) {
+                const double2 up = up_base[r * AX];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(xi1, e1, xi0 * e0);
+                G0[r] = fma(-dot, fx0, G0[r]);
+                G1[r] = fma(-dot, fx1, G1[r]);
+                if (DO_BREAK && k >= SHALF)
+                    anyc[r] |= dbits(fma(2.0, dot, fma(e1, e1, e0 * e0))) >= clo;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kFusedS; ++k) {
+            const double xi0 = st.xi0[k], xi1 = st.xi1[k];
+            const double fx0 = st.fx0[k], fx1 = st.fx1[k];
+            const long long clo = dbits(st.clo[k]);
+            const double2* up_base = ub + q0 + st.aoff[k];
+            const int moff = st.moff[k];
+#pragma unroll
+            for (int r = 0; r < EPT; ++r) {
+                const bool act = k >= SHALF ? ((m0[r] >> k) & 1u)
+                                            : ((ma[qm + r * MX + moff] >> (kFusedS - 1 - k)) & 1u);
+                const double2 up = up_base[r * AX];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(xi1, e1, xi0 * e0);
+                const double dm = act ? dot : 0.0;
+                G0[r] = fma(-dm, fx0, G0[r]);
+                G1[r] = fma(-dm, fx1, G1[r]);
+                if (DO_BREAK && k >= SHALF)
+                    anyc[r] |= act && dbits(fma(2.0, dot, fma(e1, e1, e0 * e0))) >= clo;
+            }
+        }
+    }
+    unsigned long long nb = 0;
+    if (DO_BREAK) {  // rare: exact per-bond thresholds for the flagged elements
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+            uint32_t c = anyc[r] ? (m0[r] & kPos) : 0u;
+            while (c) {
+                const int k = __ffs(c) - 1;
+                c &= c - 1;
+                const double2 up = ub[q0 + r * AX + st.aoff[k]];
+                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double dot = fma(st.xi1[k], e1, st.xi0[k] * e0);
+                const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
+                double thr = st.cthr[k];
+                if (d.spread != 0.0) {
+                    const int p = e[r] + st.did[k];
+                    const double sb =
+                        bond_s_crit(d.s_crit, d.spread, d.seed, e[r] + d.goff, p + d.goff);
+                    thr = fma(sb, sb, 2.0 * sb) * st.x2[k];
+                }
+                if (lhs >= thr) {
+                    m[r] &= ~(1u << k);
+                    if (gx >= 1 && gy0 + r >= 1 && e[r] >= d.own_lo && e[r] < d.own_hi) ++nb;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r)
+        if (e[r] >= 0 && gx >= 1 && gy0 + r >= 1) bf.mask_out[e[r]] = m[r];
+    __syncthreads();  // every read of ub is done: G may overwrite it
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) gt[(gy0 + r) * GX + gx] = make_double2(G0[r], G1[r]);
+    mbar_wait(&bar[1], 0);
+    __syncthreads();
+
+    // (4) Verlet update of the owned nodes: column i0 + lane, rows j0 + 4*warp + r.
+    //     The grid has floor(n/31) + 1 blocks per axis, so the last block owns at
+    //     most 31 node columns / rows including the domain's far node line.
+    const int ox = (blockIdx.x == gridDim.x - 1) ? NX - i0 : TX;
+    const int oy = (blockIdx.y == gridDim.y - 1) ? NY - j0 : TY;
+    double2* rdo = reinterpret_cast<double2*>(bf.rd_out);
+    double2* rv2 = reinterpret_cast<double2*>(d.rv);
+    const double2* P2 = reinterpret_cast<const double2*>(d.P);
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        const int lx = lane, ly = gy0 + r;
+        if (lx >= ox || ly >= oy) continue;
+        const size_t n = (size_t)(j0 + ly) * NX + i0 + lx;
+        const double2 a = gt[ly * GX + lx], b = gt[ly * GX + lx + 1];
+        const double2 c = gt[(ly + 1) * GX + lx], f = gt[(ly + 1) * GX + lx + 1];
+        const double k0 = d.Nsh * ((a.x + b.x) + (c.x + f.x));
+        const double k1 = d.Nsh * ((a.y + b.y) + (c.y + f.y));
+        const double im = ims[ly * IX + lx];
+        const int fl = (int)(dbits(im) & 7);  // 1: x constrained, 2: y constrained, 4: loaded
+        double2 p = make_double2(0.0, 0.0);
+        if (fl & 4) {
+            p = P2[n];
+            p.x *= scale;
+            p.y *= scale;
+        }
+        const double a0 = (fl & 1) ? 0.0 : (p.x - k0) * im;
+        const double a1 = (fl & 2) ? 0.0 : (p.y - k1) * im;
+        const double2 rv = rvs[ly * TX + lx];
+        const double2 rd = nt[(ly + 1 + R) * BX + lx + 1 + R];
+        double v0 = rv.x + d.c_corr_v * a0, v1 = rv.y + d.c_corr_v * a1;
+        const double u0 = rd.x + d.c_corr_d * a0, u1 = rd.y + d.c_corr_d * a1;
+        if (fl & 3) {
+            if (fl & 1) v0 = d.bcvel[2 * n];
+            if (fl & 2) v1 = d.bcvel[2 * n + 1];
+        }
+        if (write_state) {
+            reinterpret_cast<double2*>(d.a)[n] = make_double2(a0, a1);
+            reinterpret_cast<double2*>(d.v)[n] = make_double2(v0, v1);
+            reinterpret_cast<double2*>(d.u)[n] = make_double2(u0, u1);
+        }
+        rv2[n] = make_double2(v0 + d.c_pred_v * a0, v1 + d.c_pred_v * a1);
+        rdo[n] = make_double2(u0 + d.dt * v0 + d.c_pred_d * a0, u1 + d.dt * v1 + d.c_pred_d * a1);
+    }
+
+    if (DO_BREAK) {
+        for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+        if (lane == 0) part[warp] = nb;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < NW; ++w) t += part[w];
+            if (t) atomicAdd(d.broken_count + step, t);
+        }
+    }
+}
+
+void tile9_boxes(int* rd_x, int* rd_y, int* ma_x, int* ma_y, int* rv_x, int* rv_y, int* im_x,
+                 int* im_y) {
+    *rd_x = 2 * BX;
+    *rd_y = BY;
+    *ma_x = MX;
+    *ma_y = MY;
+    *rv_x = 2 * TX;
+    *rv_y = TY;
+    *im_x = IX;
+    *im_y = TY;
+}
+
+int tile9_configure() {
+    for (auto fn : {k_tile9<true>, k_tile9<false>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e != cudaSuccess)
+            throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true>, NT, kSmem);
+    return occ;
+}
+
+void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
+                       const Tile9Maps& maps, const FusedBufs& b, int step, int do_break,
+                       double scale, int write_state, cudaStream_t s) {
+    dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
+    if (do_break) k_tile9<true><<<grid, NT, kSmem, s>>>(d, L, st, maps, b, step, scale, write_state);
+    else k_tile9<false><<<grid, NT, kSmem, s>>>(d, L, st, maps, b, step, scale, write_state);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+}  // namespace pmts

@@ -90,6 +90,11 @@ struct pmts_pd {
     TmaMaps tmaps[2]{};              // tensor maps with rd = buffer 0 / buffer 1
     double* rd_buf[2] = {nullptr, nullptr};
     double* d_aux = nullptr;         // per node {1/M, flags} (TMA path)
+    bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
+    int tile9_occ = 0;               // its resident CTAs per SM
+    CUtensorMap t9_rd[2]{}, t9_mask[2]{}, t9_rv{}, t9_im{};
+    uint32_t* mask_buf[2] = {nullptr, nullptr};
+    double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
     Stencil2D st2{};
     StripStencil sst{};
     bool lat3 = false;               // 3D 122-offset nominal-lattice bond kernel
@@ -300,6 +305,51 @@ void build_tma_maps(pmts_pd* h) {
     }
 }
 
+// TMA tensor maps of the tile9 kernel: rd and mask of both ping-pong buffers,
+// rv and {1/M | flags}.  Box sizes come from pd_tile9.cu.
+void build_tile9_maps(pmts_pd* h) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            throw InternalError("cuTensorMapEncodeTiled unavailable");
+        encode = (PFN_cuTensorMapEncodeTiled)fn;
+    }
+    const int nx = h->L.nx, ny = h->L.ny, NX = nx + 1, NY = ny + 1, NXP = (NX + 1) & ~1;
+    int rdx, rdy, max_, may, rvx, rvy, imx, imy;
+    tile9_boxes(&rdx, &rdy, &max_, &may, &rvx, &rvy, &imx, &imy);
+    auto make = [&](CUtensorMap* m, CUtensorMapDataType ty, size_t esz, void* base, int w,
+                    int rows, int bx, int by) {
+        const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)rows};
+        const cuuint64_t strides[1] = {(cuuint64_t)w * esz};
+        const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(m, ty, 2, base, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw InternalError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    };
+    for (int b = 0; b < 2; ++b) {
+        make(&h->t9_rd[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->rd_buf[b], 2 * NX, NY, rdx, rdy);
+        make(&h->t9_mask[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, h->mask_buf[b], nx, ny, max_, may);
+    }
+    make(&h->t9_rv, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->d.rv, 2 * NX, NY, rvx, rvy);
+    make(&h->t9_im, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->d_imf, NXP, NY, imx, imy);
+}
+
+Tile9Maps tile9_maps(const pmts_pd* h) {
+    Tile9Maps m;
+    m.rd = h->t9_rd[h->d.rd == h->rd_buf[0] ? 0 : 1];
+    m.mask = h->t9_mask[h->d.mask == h->mask_buf[0] ? 0 : 1];
+    m.rv = h->t9_rv;
+    m.im = h->t9_im;
+    return m;
+}
+
 // Stencil encoding of the families when the mesh is the generated lattice
 // (fast mode).  Returns false (ELL path stays) if any bond's offset falls
 // outside one shared stencil of <= kMaxStencil offsets.
@@ -462,6 +512,16 @@ bool try_lattice(pmts_pd* h) {
         }
         nflag[n] = f;
         im[n] = 1.0 / h->hM[(size_t)n * dim];
+        if (dim == 2) {
+            // 2D: every lattice kernel uses 1/M with the node flags (1 x, 2 y
+            // constrained, 4 loaded) in its three low mantissa bits -- the form the
+            // TMA-staged tile kernel reads -- so all 2D variants stay bitwise equal
+            // (relative change of 1/M <= 2^-49, far inside the fast-mode tolerance)
+            uint64_t b;
+            std::memcpy(&b, &im[n], 8);
+            b = (b & ~uint64_t(7)) | (f & 3u) | ((f & 8u) ? 4u : 0u);
+            std::memcpy(&im[n], &b, 8);
+        }
     }
     uint8_t* dnf = h->alloc<uint8_t>(h->N);
     double* dim_ = h->alloc<double>(h->N);
@@ -524,6 +584,7 @@ bool try_lattice(pmts_pd* h) {
             st.clo[s] = t[5];
             st.x2[s] = t[6];
             st.aoff[s] = dj[s] * kFusedAX + di[s];
+            st.moff[s] = dj[s] * 40 + di[s];
             st.did[s] = dl[s];
         }
         if (!h->rd_alt) h->rd_alt = h->alloc<double>(h->ndof);
@@ -531,12 +592,31 @@ bool try_lattice(pmts_pd* h) {
         h->mask_alt = h->alloc<uint32_t>((size_t)E);
         fused2d_configure();
         h->fused = true;
-        // kernel variant: PMTS_FUSED_KERNEL = tma (default) | tile | strip
+        // kernel variant: PMTS_FUSED_KERNEL = tile9 (default) | tile | tma | strip
         const char* kv = std::getenv("PMTS_FUSED_KERNEL");
-        const std::string kvs = kv ? kv : "tile";
+        const std::string kvs = kv ? kv : "tile9";
         h->strip = kvs == "strip";
         h->tma = kvs == "tma";
-        h->pos_only = !h->strip && !h->tma;  // the tile kernel keeps bond state at the lower end
+        h->tile9 = kvs == "tile9" && h->L.nx % 4 == 0;  // mask rows: 16-byte multiple
+        h->pos_only = !h->strip && !h->tma;  // the tile kernels keep bond state at the lower end
+        if (h->tile9) {
+            // {1/M | flags}: flags (1 x, 2 y constrained, 4 loaded) in the low mantissa bits
+            const int NX = h->L.nx + 1, NY = h->L.ny + 1, NXP = (NX + 1) & ~1;
+            std::vector<double> imf((size_t)NXP * NY, 0.0);
+            for (int j = 0; j < NY; ++j)
+                for (int i = 0; i < NX; ++i) {
+                    imf[(size_t)j * NXP + i] = im[j * NX + i];  // flags already encoded
+                }
+            if (h->d_imf) h->release(h->d_imf);
+            h->d_imf = h->alloc<double>(imf.size());
+            upload(h->d_imf, imf.data(), imf.size(), h->stream);
+            h->rd_buf[0] = h->d.rd;
+            h->rd_buf[1] = h->rd_alt;
+            h->mask_buf[0] = h->d.mask;
+            h->mask_buf[1] = h->mask_alt;
+            build_tile9_maps(h);
+            h->tile9_occ = tile9_configure();
+        }
         if (h->tma) {
             std::vector<double> aux(2 * (size_t)h->N);
             for (int n = 0; n < h->N; ++n) {
@@ -626,7 +706,10 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
-        if (h->tma)
+        if (h->tile9)
+            launch_tile9_step(h->d, h->L, h->st2, tile9_maps(h), b, slot, brk, scale,
+                              last ? 1 : 0, h->stream);
+        else if (h->tma)
             launch_tma2d_step(h->d, h->L, h->st2, h->tmaps[h->d.rd == h->rd_buf[0] ? 0 : 1], b,
                               slot, brk, scale, last ? 1 : 0, h->stream);
         else if (h->strip)

@@ -98,10 +98,11 @@ def test_bp_coarse_deterministic():
     assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
 
 
-@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "lattice-strip", "ell"])
+@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "lattice-tma", "lattice-strip",
+                                  "ell"])
 @pytest.mark.parametrize("name", SMALL)
 def test_fast_mode_tolerances(name, path, monkeypatch):
-    if path.startswith("lattice-"):  # the other fused 2D kernel variants (default: tma)
+    if path.startswith("lattice-"):  # the other fused 2D kernel variants (default: tile9)
         monkeypatch.setenv("PMTS_FUSED_KERNEL", path.split("-")[1])
         path = "lattice"
     over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
@@ -131,6 +132,40 @@ def test_fast_mode_tolerances(name, path, monkeypatch):
     if ref.sum():
         agree = 1.0 - np.logical_xor(mine, ref).sum() / max(ref.sum(), 1)
         assert agree >= 0.999, agree
+
+
+def _plate(nx, ny):
+    """The mini notched plate (horizontal tension) resized to nx x ny elements."""
+    sc = cf.get("mini")
+    dx = sc["mesh"]["spacing"]
+    lx, ly = nx * dx, ny * dx
+    sc["mesh"]["bounds"] = [0.0, 0.0, lx, ly]
+    sc["mesh"]["notch1"] = [0.5 * lx, 0.5 * ly, 0.5 * lx, 0.25 * ly]
+    sc["load"]["traction2"] = [lx - 1e-4, -1.0, lx + 1e-4, 1.0, 16e6, 0.0]
+    return Scenario(sc)
+
+
+@pytest.mark.parametrize("nx,ny", [(40, 16), (124, 62), (32, 31), (64, 93), (60, 35), (42, 20)])
+def test_tile9_bitwise_equals_tile(nx, ny, monkeypatch):
+    """The TMA-staged tile kernel (default) and the bounds-checked tile kernel run
+    the same arithmetic: u, v, a and every bond state agree bit for bit, on
+    lattices that are multiples of the 31 x 31 tile, smaller than one tile, and
+    ragged -- the TMA zero-fill must reproduce the bounds checks exactly."""
+    sc = _plate(nx, ny)
+    out = {}
+    for kv in ("tile9", "tile"):
+        monkeypatch.setenv("PMTS_FUSED_KERNEL", kv)
+        s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+        assert s.info()["path"] == 2
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = s.step([sc.load_scale(i * sc.dt) for i in range(1, 121)])
+        out[kv] = (nb, *s.state(), s.intact())
+    a, b = out["tile9"], out["tile"]
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
+    if (nx, ny) == (40, 16):
+        assert a[0] > 0  # the notched mini plate cracks within 120 steps
 
 
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
