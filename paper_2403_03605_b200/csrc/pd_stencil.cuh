@@ -37,7 +37,6 @@ struct Stencil2D {
     double cthr[kFusedS], clo[kFusedS], x2[kFusedS];
     int aoff[kFusedS];  // partner offset inside the shared ubar apron (dj * AX + di)
     int did[kFusedS];   // partner element-id delta
-    int moff[kFusedS];  // partner offset inside the TMA mask box (dj * 40 + di; pd_tile9.cu)
 };
 
 struct FusedBufs {
@@ -69,13 +68,12 @@ void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        double scale, int write_state, cudaStream_t s);
 
 // One-shot TMA-staged variant (pd_tile9.cu): tensor maps of the current rd
-// ([NY][2 NX] doubles), the current mask ([ny][nx] u32), rv and {1/M | flags}
-// ([NY][NXP] doubles, NXP even, flags in the three low mantissa bits).
+// ([NY][2 NX] doubles), rv, and {1/M | flags} ([NY][NXP] doubles, NXP even,
+// flags in the three low mantissa bits).
 struct Tile9Maps {
-    CUtensorMap rd, mask, rv, im;
+    CUtensorMap rd, rv, im;
 };
-void tile9_boxes(int* rd_x, int* rd_y, int* ma_x, int* ma_y, int* rv_x, int* rv_y, int* im_x,
-                 int* im_y);
+void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y);
 int tile9_configure();  // returns resident CTAs per SM
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const Tile9Maps& maps, const FusedBufs& b, int step, int do_break,

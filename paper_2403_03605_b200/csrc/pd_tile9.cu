@@ -1,25 +1,30 @@
 // One-shot fused 2D fine step with TMA staging (tile v9), 28-offset stencil,
 // fast mode.  Arithmetic is the tile kernel's (pd_stencil_fused.cu: 31 x 31
 // owned elements, 32 x 32 force region, bond state at the lower end, integer
-// candidate compare); what changes is how the CTA gets its inputs:
+// candidate compare) -- the two kernels are bitwise equal -- what changes is
+// how the CTA gets its inputs:
 //
-//   * at launch one thread issues four cp.async.bulk.tensor loads completing on
-//     two mbarriers -- the node apron of the predictor displacement and the
-//     mask apron (needed first), and the owned nodes' rv and {1/M, flags}
-//     (needed last, so their latency hides behind the ubar and force passes).
-//     Out-of-domain parts of a box are zero-filled by the TMA unit, exactly the
-//     zeros the tile kernel writes with bounds-checked loads; no thread spends
-//     instructions on load addresses or bounds (the tile kernel's ncu source
-//     page put ~25 % of the stall samples on its staging phase and ~27 % on the
-//     node-update loads);
+//   * at launch one thread issues three cp.async.bulk.tensor loads completing
+//     on two mbarriers -- the node apron of the predictor displacement (needed
+//     first), and the owned nodes' rv and {1/M, flags} (needed last, so their
+//     latency hides behind the ubar and force passes).  Out-of-domain parts of
+//     a box are zero-filled by the TMA unit, exactly the zeros the tile kernel
+//     writes with bounds-checked loads (the tile kernel's ncu source page put
+//     ~25 % of the stall samples on its staging phase and ~27 % on the
+//     node-update loads).  The bond-state apron goes through 4-byte cp.async
+//     with zero fill: a TMA box row must start 16-byte aligned in global
+//     memory, which the mask apron (start column i0 - 4) is not, and the
+//     aligned superset box would not leave room for three CTAs per SM;
 //   * G aliases the ubar apron after the force pass, and the node flags ride
-//     in the three low mantissa bits of 1/M (relative change <= 2^-49, far
-//     below the fast-mode tolerance), so the whole CTA fits in 76.7 KB and
-//     three CTAs (24 warps) stay resident per SM.
+//     in the three low mantissa bits of 1/M (pmts_pd.cu encodes them for every
+//     2D lattice kernel), so the CTA fits in 76.3 KB and three CTAs (24 warps)
+//     stay resident per SM.
 //
-// Requirements (checked by the host): nx % 4 == 0 (the mask rows must be a
-// multiple of 16 bytes for the tensor map).  Reference semantics as in
-// pd_stencil.cu.
+// TMA rules this layout honours (measured: violations fault with "illegal
+// instruction" / "misaligned address"): 128-byte aligned shared destinations,
+// 16-byte aligned global row starts (so the {1/M, flags} box starts at the
+// even column i0 & ~1 of rows padded to an even length).  Reference semantics
+// as in pd_stencil.cu.
 #include <stdexcept>
 #include <string>
 
@@ -33,8 +38,8 @@ constexpr int TX = 31, TY = 31, R = kFusedR;
 constexpr int GX = TX + 1, GY = TY + 1;          // force region (elements), 32 x 32
 constexpr int AX = GX + 2 * R, AY = GY + 2 * R;  // ubar apron (elements), 38 x 38
 constexpr int BX = AX + 1, BY = AY + 1;          // node apron, 39 x 39
-constexpr int MX = 40, MY = GY + R;              // mask box: the rows the force pass reads
-constexpr int IX = 32;                           // {1/M, flags} box row (16-byte multiple)
+constexpr int MY = GY + R;                       // bond-state apron rows the force pass reads
+constexpr int IX = 32;                           // {1/M, flags} box row (from an even column)
 constexpr int NW = 8, NT = 32 * NW;
 constexpr int EPT = GY / NW;
 constexpr int SHALF = kFusedS / 2;
@@ -44,18 +49,18 @@ static_assert(AX == kFusedAX, "Stencil2D apron offsets assume this width");
 
 constexpr int rup(int x, int a) { return (x + a - 1) / a * a; }
 constexpr int kNtBytes = BX * BY * 16;
-constexpr int kMaBytes = MX * MY * 4;
 constexpr int kRvBytes = TX * TY * 16;
 constexpr int kImBytes = IX * TY * 8;
-constexpr int kOffNt = 0;
-constexpr int kOffMa = rup(kOffNt + kNtBytes, 128);
-constexpr int kOffRv = rup(kOffMa + kMaBytes, 128);
-constexpr int kOffIm = rup(kOffRv + kRvBytes, 128);
-constexpr int kOffUb = rup(kOffIm + kImBytes, 16);
+// TMA destinations (128-byte aligned) first, ordered to minimise padding
+constexpr int kOffIm = 0;
+constexpr int kOffNt = rup(kOffIm + kImBytes, 128);
+constexpr int kOffRv = rup(kOffNt + kNtBytes, 128);
+constexpr int kOffMa = rup(kOffRv + kRvBytes, 16);  // AX x MY bond-state words
+constexpr int kOffUb = rup(kOffMa + AX * MY * 4, 16);
 constexpr int kOffBar = rup(kOffUb + AX * AY * 16, 8);
-constexpr int kOffPart = kOffBar + 16;
-constexpr int kSmem = kOffPart + 8 * NW;
-static_assert(GX * GY * 16 <= AX * AY * 16, "G fits in the ubar apron");
+constexpr int kOffPart = kOffUb + GX * GY * 16;  // in the ubar apron's tail, after G
+constexpr int kSmem = kOffBar + 16 + 128;        // + realignment slack of the dynamic base
+static_assert(GX * GY * 16 + 8 * NW <= AX * AY * 16, "G and the partial counts fit in ub");
 static_assert(kSmem + 1024 <= 233472 / 3, "three CTAs per SM");
 
 __device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
@@ -87,6 +92,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(b))
         : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
 
 }  // namespace
 
@@ -95,9 +105,11 @@ __global__ void __launch_bounds__(NT, 3)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const __grid_constant__ Tile9Maps maps, FusedBufs bf, int step, double scale,
         int write_state) {
-    extern __shared__ __align__(1024) unsigned char sm[];
+    extern __shared__ __align__(16) unsigned char smraw[];
+    // the dynamic base is only guaranteed 16-byte aligned: realign for TMA
+    unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
     const double2* nt = reinterpret_cast<const double2*>(sm + kOffNt);
-    const uint32_t* ma = reinterpret_cast<const uint32_t*>(sm + kOffMa);
+    uint32_t* ma = reinterpret_cast<uint32_t*>(sm + kOffMa);
     const double2* rvs = reinterpret_cast<const double2*>(sm + kOffRv);
     const double* ims = reinterpret_cast<const double*>(sm + kOffIm);
     double2* ub = reinterpret_cast<double2*>(sm + kOffUb);
@@ -108,19 +120,33 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
     const int ax0 = i0 - 1 - R, ay0 = j0 - 1 - R;
+    const int ie = i0 & ~1;  // {1/M, flags} box start: 16-byte aligned global row start
 
+    // (1) staging: TMA for the node apron and the node-update inputs; 4-byte
+    //     cp.async (zero-filled outside the domain) for the bond-state apron
     if (threadIdx.x == 0) {
-        if (smem_u32(sm) & 127u) __trap();  // TMA destinations need 128-byte alignment
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-        mbar_expect_tx(&bar[0], kNtBytes + kMaBytes);
+        mbar_expect_tx(&bar[0], kNtBytes);
         tma_load_2d(sm + kOffNt, &maps.rd, 2 * ax0, ay0, &bar[0]);
-        tma_load_2d(sm + kOffMa, &maps.mask, ax0, ay0, &bar[0]);
         mbar_expect_tx(&bar[1], kRvBytes + kImBytes);
         tma_load_2d(sm + kOffRv, &maps.rv, 2 * i0, j0, &bar[1]);
-        tma_load_2d(sm + kOffIm, &maps.im, i0, j0, &bar[1]);
+        tma_load_2d(sm + kOffIm, &maps.im, ie, j0, &bar[1]);
     }
+    for (int y = warp; y < MY; y += NW) {
+        const int gj = ay0 + y;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = lane + 32 * h, gi = ax0 + x;
+            if (x < AX) {
+                const bool in = gi >= 0 && gj >= 0 && gi < nx && gj < ny;
+                cp_async4(ma + y * AX + x, bf.mask_in + (in ? (size_t)gj * nx + gi : 0), in);
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     mbar_wait(&bar[0], 0);
 
@@ -146,7 +172,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                 if (y < AY) {
                     ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
                                                   d.Nsh * (hs[i].y + hs[i + 1].y));
-                    if (y < MY) tile_full = tile_full && (ma[y * MX + x] & kPos) == kPos;
+                    if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
                 }
             }
         }
@@ -157,7 +183,6 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     const int gx = lane, gy0 = warp * EPT;
     const int ei = i0 - 1 + gx;
     const int q0 = (gy0 + R) * AX + gx + R;
-    const int qm = (gy0 + R) * MX + gx + R;
     int e[EPT];
     uint32_t m0[EPT], m[EPT];
     double2 ue[EPT];
@@ -167,7 +192,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const int ej = j0 - 1 + gy0 + r;
         const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
         e[r] = in ? ej * nx + ei : -1;
-        m0[r] = ma[qm + r * MX];
+        m0[r] = ma[q0 + r * AX];
         m[r] = m0[r];
         ue[r] = ub[q0 + r * AX];
         G0[r] = 0.0;
@@ -200,12 +225,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             const double xi0 = st.xi0[k], xi1 = st.xi1[k];
             const double fx0 = st.fx0[k], fx1 = st.fx1[k];
             const long long clo = dbits(st.clo[k]);
-            const double2* up_base = ub + q0 + st.aoff[k];
-            const int moff = st.moff[k];
+            const int aoff = st.aoff[k];
+            const double2* up_base = ub + q0 + aoff;
 #pragma unroll
             for (int r = 0; r < EPT; ++r) {
                 const bool act = k >= SHALF ? ((m0[r] >> k) & 1u)
-                                            : ((ma[qm + r * MX + moff] >> (kFusedS - 1 - k)) & 1u);
+                                            : ((ma[q0 + r * AX + aoff] >> (kFusedS - 1 - k)) & 1u);
                 const double2 up = up_base[r * AX];
                 const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
                 const double dot = fma(xi1, e1, xi0 * e0);
@@ -269,7 +294,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const double2 c = gt[(ly + 1) * GX + lx], f = gt[(ly + 1) * GX + lx + 1];
         const double k0 = d.Nsh * ((a.x + b.x) + (c.x + f.x));
         const double k1 = d.Nsh * ((a.y + b.y) + (c.y + f.y));
-        const double im = ims[ly * IX + lx];
+        const double im = ims[ly * IX + lx + (i0 - ie)];
         const int fl = (int)(dbits(im) & 7);  // 1: x constrained, 2: y constrained, 4: loaded
         double2 p = make_double2(0.0, 0.0);
         if (fl & 4) {
@@ -308,12 +333,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
 }
 
-void tile9_boxes(int* rd_x, int* rd_y, int* ma_x, int* ma_y, int* rv_x, int* rv_y, int* im_x,
-                 int* im_y) {
+void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y) {
     *rd_x = 2 * BX;
     *rd_y = BY;
-    *ma_x = MX;
-    *ma_y = MY;
     *rv_x = 2 * TX;
     *rv_y = TY;
     *im_x = IX;

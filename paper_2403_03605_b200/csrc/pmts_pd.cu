@@ -5,6 +5,7 @@
 // kernel launches -- bond gather, node update (+ fused predictor) -- replayed
 // from a CUDA graph per step batch.  Citations: /root/reference/proj/include/
 // perimts/<file>:<line>.
+#include <cstdio>
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -92,8 +93,7 @@ struct pmts_pd {
     double* d_aux = nullptr;         // per node {1/M, flags} (TMA path)
     bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
     int tile9_occ = 0;               // its resident CTAs per SM
-    CUtensorMap t9_rd[2]{}, t9_mask[2]{}, t9_rv{}, t9_im{};
-    uint32_t* mask_buf[2] = {nullptr, nullptr};
+    CUtensorMap t9_rd[2]{}, t9_rv{}, t9_im{};
     double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
     Stencil2D st2{};
     StripStencil sst{};
@@ -305,8 +305,8 @@ void build_tma_maps(pmts_pd* h) {
     }
 }
 
-// TMA tensor maps of the tile9 kernel: rd and mask of both ping-pong buffers,
-// rv and {1/M | flags}.  Box sizes come from pd_tile9.cu.
+// TMA tensor maps of the tile9 kernel: rd of both ping-pong buffers, rv and
+// {1/M | flags}.  Box sizes come from pd_tile9.cu.
 void build_tile9_maps(pmts_pd* h) {
     static PFN_cuTensorMapEncodeTiled encode = nullptr;
     if (!encode) {
@@ -318,8 +318,8 @@ void build_tile9_maps(pmts_pd* h) {
         encode = (PFN_cuTensorMapEncodeTiled)fn;
     }
     const int nx = h->L.nx, ny = h->L.ny, NX = nx + 1, NY = ny + 1, NXP = (NX + 1) & ~1;
-    int rdx, rdy, max_, may, rvx, rvy, imx, imy;
-    tile9_boxes(&rdx, &rdy, &max_, &may, &rvx, &rvy, &imx, &imy);
+    int rdx, rdy, rvx, rvy, imx, imy;
+    tile9_boxes(&rdx, &rdy, &rvx, &rvy, &imx, &imy);
     auto make = [&](CUtensorMap* m, CUtensorMapDataType ty, size_t esz, void* base, int w,
                     int rows, int bx, int by) {
         const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)rows};
@@ -335,7 +335,6 @@ void build_tile9_maps(pmts_pd* h) {
     };
     for (int b = 0; b < 2; ++b) {
         make(&h->t9_rd[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->rd_buf[b], 2 * NX, NY, rdx, rdy);
-        make(&h->t9_mask[b], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, h->mask_buf[b], nx, ny, max_, may);
     }
     make(&h->t9_rv, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->d.rv, 2 * NX, NY, rvx, rvy);
     make(&h->t9_im, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->d_imf, NXP, NY, imx, imy);
@@ -344,7 +343,6 @@ void build_tile9_maps(pmts_pd* h) {
 Tile9Maps tile9_maps(const pmts_pd* h) {
     Tile9Maps m;
     m.rd = h->t9_rd[h->d.rd == h->rd_buf[0] ? 0 : 1];
-    m.mask = h->t9_mask[h->d.mask == h->mask_buf[0] ? 0 : 1];
     m.rv = h->t9_rv;
     m.im = h->t9_im;
     return m;
@@ -584,7 +582,6 @@ bool try_lattice(pmts_pd* h) {
             st.clo[s] = t[5];
             st.x2[s] = t[6];
             st.aoff[s] = dj[s] * kFusedAX + di[s];
-            st.moff[s] = dj[s] * 40 + di[s];
             st.did[s] = dl[s];
         }
         if (!h->rd_alt) h->rd_alt = h->alloc<double>(h->ndof);
@@ -597,7 +594,7 @@ bool try_lattice(pmts_pd* h) {
         const std::string kvs = kv ? kv : "tile9";
         h->strip = kvs == "strip";
         h->tma = kvs == "tma";
-        h->tile9 = kvs == "tile9" && h->L.nx % 4 == 0;  // mask rows: 16-byte multiple
+        h->tile9 = kvs == "tile9";
         h->pos_only = !h->strip && !h->tma;  // the tile kernels keep bond state at the lower end
         if (h->tile9) {
             // {1/M | flags}: flags (1 x, 2 y constrained, 4 loaded) in the low mantissa bits
@@ -612,8 +609,6 @@ bool try_lattice(pmts_pd* h) {
             upload(h->d_imf, imf.data(), imf.size(), h->stream);
             h->rd_buf[0] = h->d.rd;
             h->rd_buf[1] = h->rd_alt;
-            h->mask_buf[0] = h->d.mask;
-            h->mask_buf[1] = h->mask_alt;
             build_tile9_maps(h);
             h->tile9_occ = tile9_configure();
         }

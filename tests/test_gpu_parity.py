@@ -145,7 +145,7 @@ def _plate(nx, ny):
     return Scenario(sc)
 
 
-@pytest.mark.parametrize("nx,ny", [(40, 16), (124, 62), (32, 31), (64, 93), (60, 35), (42, 20)])
+@pytest.mark.parametrize("nx,ny", [(40, 16), (124, 62), (32, 31), (64, 93), (60, 35), (42, 20), (33, 65)])
 def test_tile9_bitwise_equals_tile(nx, ny, monkeypatch):
     """The TMA-staged tile kernel (default) and the bounds-checked tile kernel run
     the same arithmetic: u, v, a and every bond state agree bit for bit, on
