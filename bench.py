@@ -262,8 +262,9 @@ def bench_native(args):
     peak, peak_src = _peaks()
     bond_avg_s = bond_ms * 1e-3 / K
     achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
-    kname = {2: "k_fused2d", 1: "k_lat_bond"}.get(
-        info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
+    fused = {"tile9": "k_tile9", "tile": "k_fused2d", "tma": "k_tma2d", "strip": "k_strip2d"}
+    kname = {2: fused.get(os.environ.get("PMTS_FUSED_KERNEL", "tile9"), "k_tile9"),
+             1: "k_lat_bond"}.get(info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": _ncu_traffic(kname),
             "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],

@@ -74,10 +74,24 @@ struct Tile9Maps {
     CUtensorMap rd, rv, im;
 };
 void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y);
+// Pair-symmetric force constants of the 14 positive offsets of the 28-offset
+// stencil on the nominal lattice (xi = h o), in pd_tile9.cu's pair order
+// (1,0) (2,0) (3,0) (0,1) (0,2) (0,3) (1,1) (-1,1) (2,2) (-2,2) (2,1) (-2,1)
+// (1,2) (-1,2): G += fa t e_x + fb t e_y with t = o . (eta_o + eta_-o) (axis
+// pairs: fa = F A^2 with t = s_x, resp. fb = F B^2), F = -w c(h|o|) h^2; cl = bit
+// pattern of the smallest threshold of the offset's class, lowered by 1e-12.
+struct PairStencil2D {
+    double fa[14], fb[14];
+    long long cl[14];
+    int off[14];   // apron offset of o (dj * 38 + di)
+    int pbit[14];  // mask bit of the positive offset o
+    double h2;    // 2 h
+};
+int tile9_pair_offset(int k, int* a, int* b);
 int tile9_configure();  // returns resident CTAs per SM
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
-                       const Tile9Maps& maps, const FusedBufs& b, int step, int do_break,
-                       double scale, int write_state, cudaStream_t s);
+                       const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
+                       int step, int do_break, double scale, int write_state, cudaStream_t s);
 
 // 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class
 // (1,2,3,4,5,6,8,9): c = w c(h|o|) h^2, and the bit patterns of the smallest /

@@ -98,13 +98,94 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid
                  : "memory");
 }
 
+constexpr int kPairA[14] = {1, 2, 3, 0, 0, 0, 1, -1, 2, -2, 2, -2, 1, -1};
+constexpr int kPairB[14] = {0, 0, 0, 1, 2, 3, 1, 1, 2, 2, 1, 1, 2, 2};
+
+// One opposite-offset pair (o, -o) of every element of the thread: the two
+// directed entries share xi xi^T, so their forces combine into one term of
+// s = eta_o + eta_-o (G_e = -w c h^2 sum (o.s) o); the bond to e + o (state kept
+// here, at its lower end) also gets the candidate break test.  Tiles with a
+// broken or absent bond in reach take the MASKED instance, which is bitwise the
+// same arithmetic for intact pairs -- so results do not depend on how the
+// domain is cut into tiles or slabs.  The products
+// with the integer offset components are compile-time (adds / small-constant
+// multiplies); the apron offset itself comes from the parameter block, which
+// keeps ptxas from hoisting all 112 loads of a thread to the top (immediate
+// offsets did, and spilled).
+template <bool DO_BREAK, bool MASKED, int K>
+__device__ __forceinline__ void pair_term(const double2* ubq, const uint32_t* maq,
+                                          const double2 (&ue)[EPT], const uint32_t (&m0)[EPT],
+                                          double (&G0)[EPT], double (&G1)[EPT],
+                                          bool (&anyc)[EPT], const PairStencil2D& ps) {
+    constexpr int A = kPairA[K], B = kPairB[K];
+    const int off = ps.off[K];
+    const double2* pp = ubq + off;
+    const double2* pm = ubq - off;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        const double2 up = pp[r * AX];
+        const double2 um = pm[r * AX];
+        double ep0 = up.x - ue[r].x, ep1 = up.y - ue[r].y;
+        double em0 = um.x - ue[r].x, em1 = um.y - ue[r].y;
+        bool actp = true;
+        if (MASKED) {
+            // bond e -> e+o lives at e, bond e-o -> e at e-o, both under the bit of +o;
+            // a broken (or absent) bond contributes an exact zero, so a pair with both
+            // bonds intact rounds exactly as on the unmasked path
+            const int bit = ps.pbit[K];
+            actp = (m0[r] >> bit) & 1u;
+            const bool actm = (maq[r * AX - off] >> bit) & 1u;
+            em0 = actm ? em0 : 0.0;
+            em1 = actm ? em1 : 0.0;
+        }
+        const double fp0 = MASKED && !actp ? 0.0 : ep0, fp1 = MASKED && !actp ? 0.0 : ep1;
+        double tp;
+        if (B == 0) {
+            const double s0 = fp0 + em0;
+            G0[r] = fma(ps.fa[K], s0, G0[r]);
+            tp = A * ep0;
+        } else if (A == 0) {
+            const double s1 = fp1 + em1;
+            G1[r] = fma(ps.fb[K], s1, G1[r]);
+            tp = B * ep1;
+        } else {
+            const double s0 = fp0 + em0, s1 = fp1 + em1;
+            const double t = fma((double)A, s0, B * s1);
+            G0[r] = fma(ps.fa[K], t, G0[r]);
+            G1[r] = fma(ps.fb[K], t, G1[r]);
+            tp = fma((double)A, ep0, B * ep1);
+        }
+        if (DO_BREAK)
+            anyc[r] |= actp && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
+    }
+}
+
+template <bool DO_BREAK, bool MASKED, int K>
+__device__ __forceinline__ void pair_terms(const double2* ubq, const uint32_t* maq,
+                                           const double2 (&ue)[EPT], const uint32_t (&m0)[EPT],
+                                           double (&G0)[EPT], double (&G1)[EPT],
+                                           bool (&anyc)[EPT], const PairStencil2D& ps) {
+    if constexpr (K < 14) {
+        pair_term<DO_BREAK, MASKED, K>(ubq, maq, ue, m0, G0, G1, anyc, ps);
+        pair_terms<DO_BREAK, MASKED, K + 1>(ubq, maq, ue, m0, G0, G1, anyc, ps);
+    }
+}
+
 }  // namespace
 
-template <bool DO_BREAK>
+int tile9_pair_offset(int k, int* a, int* b) {
+    static const int A[14] = {1, 2, 3, 0, 0, 0, 1, -1, 2, -2, 2, -2, 1, -1};
+    static const int B[14] = {0, 0, 0, 1, 2, 3, 1, 1, 2, 2, 1, 1, 2, 2};
+    *a = A[k];
+    *b = B[k];
+    return 14;
+}
+
+template <bool DO_BREAK, bool PAIRS>
 __global__ void __launch_bounds__(NT, 3)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
-        const __grid_constant__ Tile9Maps maps, FusedBufs bf, int step, double scale,
-        int write_state) {
+        const __grid_constant__ PairStencil2D ps, const __grid_constant__ Tile9Maps maps,
+        FusedBufs bf, int step, double scale, int write_state) {
     extern __shared__ __align__(16) unsigned char smraw[];
     // the dynamic base is only guaranteed 16-byte aligned: realign for TMA
     unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
@@ -183,17 +264,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     const int gx = lane, gy0 = warp * EPT;
     const int ei = i0 - 1 + gx;
     const int q0 = (gy0 + R) * AX + gx + R;
-    int e[EPT];
-    uint32_t m0[EPT], m[EPT];
+    // only ue, G and the candidate flags stay live through the force pass (the
+    // element ids and bond-state words are re-derived afterwards: registers)
     double2 ue[EPT];
     double G0[EPT], G1[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-        const int ej = j0 - 1 + gy0 + r;
-        const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
-        e[r] = in ? ej * nx + ei : -1;
-        m0[r] = ma[q0 + r * AX];
-        m[r] = m0[r];
         ue[r] = ub[q0 + r * AX];
         G0[r] = 0.0;
         G1[r] = 0.0;
@@ -201,7 +277,15 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     bool anyc[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) anyc[r] = false;
-    if (tile_full) {
+    if (PAIRS && tile_full) {
+        const uint32_t none[EPT] = {};
+        pair_terms<DO_BREAK, false, 0>(ub + q0, ma + q0, ue, none, G0, G1, anyc, ps);
+    } else if (PAIRS) {
+        uint32_t m0[EPT];
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) m0[r] = ma[q0 + r * AX];
+        pair_terms<DO_BREAK, true, 0>(ub + q0, ma + q0, ue, m0, G0, G1, anyc, ps);
+    } else if (tile_full) {
 #pragma unroll
         for (int k = 0; k < kFusedS; ++k) {
             const double xi0 = st.xi0[k], xi1 = st.xi1[k];
@@ -220,6 +304,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             }
         }
     } else {
+        uint32_t m0[EPT];
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) m0[r] = ma[q0 + r * AX];
 #pragma unroll
         for (int k = 0; k < kFusedS; ++k) {
             const double xi0 = st.xi0[k], xi1 = st.xi1[k];
@@ -241,6 +328,16 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                     anyc[r] |= act && dbits(fma(2.0, dot, fma(e1, e1, e0 * e0))) >= clo;
             }
         }
+    }
+    int e[EPT];
+    uint32_t m0[EPT], m[EPT];
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        const int ej = j0 - 1 + gy0 + r;
+        const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
+        e[r] = in ? ej * nx + ei : -1;
+        m0[r] = ma[q0 + r * AX];
+        m[r] = m0[r];
     }
     unsigned long long nb = 0;
     if (DO_BREAK) {  // rare: exact per-bond thresholds for the flagged elements
@@ -343,22 +440,34 @@ void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_
 }
 
 int tile9_configure() {
-    for (auto fn : {k_tile9<true>, k_tile9<false>}) {
+    for (auto fn : {k_tile9<true, false>, k_tile9<false, false>, k_tile9<true, true>,
+                    k_tile9<false, true>}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         if (e != cudaSuccess)
             throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true>, NT, kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true, true>, NT, kSmem);
     return occ;
 }
 
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
-                       const Tile9Maps& maps, const FusedBufs& b, int step, int do_break,
-                       double scale, int write_state, cudaStream_t s) {
+                       const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
+                       int step, int do_break, double scale, int write_state, cudaStream_t s) {
     dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
-    if (do_break) k_tile9<true><<<grid, NT, kSmem, s>>>(d, L, st, maps, b, step, scale, write_state);
-    else k_tile9<false><<<grid, NT, kSmem, s>>>(d, L, st, maps, b, step, scale, write_state);
+    const PairStencil2D none{};
+    const PairStencil2D& p = ps ? *ps : none;
+    if (ps) {
+        if (do_break)
+            k_tile9<true, true><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
+        else
+            k_tile9<false, true><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
+    } else {
+        if (do_break)
+            k_tile9<true, false><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
+        else
+            k_tile9<false, false><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }

@@ -94,6 +94,8 @@ struct pmts_pd {
     bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
     int tile9_occ = 0;               // its resident CTAs per SM
     CUtensorMap t9_rd[2]{}, t9_rv{}, t9_im{};
+    bool pairs = false;              // tile9 with the pair-symmetric compile-time stencil
+    PairStencil2D pst{};
     double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
     Stencil2D st2{};
     StripStencil sst{};
@@ -611,6 +613,30 @@ bool try_lattice(pmts_pd* h) {
             h->rd_buf[1] = h->rd_alt;
             build_tile9_maps(h);
             h->tile9_occ = tile9_configure();
+            // pair-symmetric force on the nominal lattice (PMTS_NO_PAIRS=1 keeps the
+            // tile kernel's per-offset arithmetic, bitwise equal to pd_stencil_fused.cu)
+            h->pairs = h->desc.lattice_h > 0.0 && !std::getenv("PMTS_NO_PAIRS");
+            const double hh = h->desc.lattice_h;
+            for (int k = 0; k < 14 && h->pairs; ++k) {
+                int A = 0, B = 0;
+                tile9_pair_offset(k, &A, &B);
+                int s = -1;
+                for (int q = 0; q < S; ++q)
+                    if (di[q] == A && dj[q] == B) s = q;
+                if (s < 0) {
+                    h->pairs = false;
+                    break;
+                }
+                const double* t = table.data() + kTableRow * (size_t)s;
+                const double F = -t[2] * (hh * hh);
+                h->pst.fa[k] = B == 0 ? F * (A * A) : F * A;
+                h->pst.fb[k] = A == 0 ? F * (B * B) : F * B;
+                const double clo = t[5] * (1.0 - 1e-12);
+                std::memcpy(&h->pst.cl[k], &clo, 8);
+                h->pst.off[k] = B * kFusedAX + A;
+                h->pst.pbit[k] = s;
+            }
+            h->pst.h2 = 2.0 * hh;
         }
         if (h->tma) {
             std::vector<double> aux(2 * (size_t)h->N);
@@ -702,8 +728,8 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
         if (h->tile9)
-            launch_tile9_step(h->d, h->L, h->st2, tile9_maps(h), b, slot, brk, scale,
-                              last ? 1 : 0, h->stream);
+            launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
+                              slot, brk, scale, last ? 1 : 0, h->stream);
         else if (h->tma)
             launch_tma2d_step(h->d, h->L, h->st2, h->tmaps[h->d.rd == h->rd_buf[0] ? 0 : 1], b,
                               slot, brk, scale, last ? 1 : 0, h->stream);

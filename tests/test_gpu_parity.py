@@ -98,11 +98,14 @@ def test_bp_coarse_deterministic():
     assert np.linalg.norm(u - g["u"]) <= 1e-12 * np.linalg.norm(g["u"])
 
 
-@pytest.mark.parametrize("path", ["lattice", "lattice-tile", "lattice-tma", "lattice-strip",
-                                  "ell"])
+@pytest.mark.parametrize("path", ["lattice", "lattice-nopairs", "lattice-tile", "lattice-tma",
+                                  "lattice-strip", "ell"])
 @pytest.mark.parametrize("name", SMALL)
 def test_fast_mode_tolerances(name, path, monkeypatch):
-    if path.startswith("lattice-"):  # the other fused 2D kernel variants (default: tile9)
+    if path == "lattice-nopairs":  # tile9 with per-offset (not pair-symmetric) sums
+        monkeypatch.setenv("PMTS_NO_PAIRS", "1")
+        path = "lattice"
+    elif path.startswith("lattice-"):  # the other fused 2D kernel variants (default: tile9)
         monkeypatch.setenv("PMTS_FUSED_KERNEL", path.split("-")[1])
         path = "lattice"
     over = {} if path == "lattice" else {"lattice": (0, 0, 0)}
@@ -153,6 +156,7 @@ def test_tile9_bitwise_equals_tile(nx, ny, monkeypatch):
     ragged -- the TMA zero-fill must reproduce the bounds checks exactly."""
     sc = _plate(nx, ny)
     out = {}
+    monkeypatch.setenv("PMTS_NO_PAIRS", "1")  # tile9 with the tile kernel's per-offset sums
     for kv in ("tile9", "tile"):
         monkeypatch.setenv("PMTS_FUSED_KERNEL", kv)
         s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
@@ -166,6 +170,28 @@ def test_tile9_bitwise_equals_tile(nx, ny, monkeypatch):
         assert np.array_equal(x, y)
     if (nx, ny) == (40, 16):
         assert a[0] > 0  # the notched mini plate cracks within 120 steps
+
+
+@pytest.mark.parametrize("nx,ny", [(40, 16), (124, 62), (64, 93)])
+def test_tile9_pairs_close_to_per_offset(nx, ny, monkeypatch):
+    """The pair-symmetric force (default) regroups the same terms: fields within
+    1e-12 relative L2 of the per-offset sums and the same broken bonds."""
+    sc = _plate(nx, ny)
+    out = {}
+    for pairs in (True, False):
+        if pairs:
+            monkeypatch.delenv("PMTS_NO_PAIRS", raising=False)
+        else:
+            monkeypatch.setenv("PMTS_NO_PAIRS", "1")
+        s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = s.step([sc.load_scale(i * sc.dt) for i in range(1, 121)])
+        out[pairs] = (nb, *s.state(), s.intact())
+    a, b = out[True], out[False]
+    assert a[0] == b[0]
+    assert np.array_equal(a[4], b[4])
+    for x, y in zip(a[1:4], b[1:4]):
+        assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
 
 
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
