@@ -181,7 +181,10 @@ int pmts_pd_step(pmts_pd* h, int32_t n, const double* load_scale, int64_t* n_bro
 /* n fine steps that also report, per step, the displacement of n_tracked dofs
  * (the tracked points run_built records every step, driver_run.hpp:204-208,241)
  * into tracked_out[n][n_tracked] and the bonds broken in that step into
- * broken_out[n] -- one device->host copy and one synchronisation per call. */
+ * broken_out[n].  Per step, asynchronously on the handle's stream: the step's
+ * load scale host->device (pinned staging), the step, and the step's tracked
+ * row and broken count device->host; one synchronisation per call.  Pass
+ * pinned (page-locked) tracked_out for the copies to overlap the steps. */
 int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* load_scale, int32_t n_tracked,
                          const int32_t* dofs, double* tracked_out, int64_t* broken_out);
 /* Same as pmts_pd_step, timed on the handle's stream with CUDA events (device ms). */

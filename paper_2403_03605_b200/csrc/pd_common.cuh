@@ -80,6 +80,9 @@ void launch_predict(const DevPD& d, cudaStream_t s);
 void launch_init_acc(const DevPD& d, double scale, cudaStream_t s);
 void launch_damage(const DevPD& d, double* elem, double* node, cudaStream_t s);
 void launch_gather(const double* src, const int32_t* idx, int n, double* dst, cudaStream_t s);
+void launch_track(const double* src, const int32_t* idx, int n, double* trk_host,
+                  const unsigned long long* cnt_dev, unsigned long long* cnt_host,
+                  const double* scl_host_next, double* scl_dev_next, cudaStream_t s);
 // launchers (pd_fast.cu)
 void launch_fast_ubar(const DevPD& d, cudaStream_t s);
 void launch_fast_bond(const DevPD& d, int step, int do_break, cudaStream_t s);

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Deterministic-mode kernels, neighbour build and node update (sm_100a).
 //
 // This translation unit is compiled with -fmad=false: every fp64 expression
@@ -293,6 +294,30 @@ __global__ void k_gather(const double* src, const int32_t* idx, int n, double* d
 void launch_gather(const double* src, const int32_t* idx, int n, double* dst, cudaStream_t s) {
     if (n <= 0) return;
     k_gather<<<(n + 127) / 128, 128, 0, s>>>(src, idx, n, dst);
+    PMTS_CUDA(cudaGetLastError());
+}
+
+// Per-step reporting for pmts_pd_step_tracked, one tiny launch: the step's
+// tracked displacements and broken count written straight into mapped pinned
+// host memory (the device->host transfer of the step's result, no copy op),
+// and the next step's load scale read from mapped pinned host memory into
+// device memory (its host->device transfer).
+__global__ void k_track(const double* src, const int32_t* idx, int n, double* trk_host,
+                        const unsigned long long* cnt_dev, unsigned long long* cnt_host,
+                        const double* scl_host_next, double* scl_dev_next) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) trk_host[i] = src[idx[i]];
+    if (i == 0) {
+        *cnt_host = *cnt_dev;
+        if (scl_dev_next) *scl_dev_next = *scl_host_next;
+    }
+}
+
+void launch_track(const double* src, const int32_t* idx, int n, double* trk_host,
+                  const unsigned long long* cnt_dev, unsigned long long* cnt_host,
+                  const double* scl_host_next, double* scl_dev_next, cudaStream_t s) {
+    k_track<<<(std::max(n, 1) + 127) / 128, 128, 0, s>>>(src, idx, n, trk_host, cnt_dev, cnt_host,
+                                                       scl_host_next, scl_dev_next);
     PMTS_CUDA(cudaGetLastError());
 }
 

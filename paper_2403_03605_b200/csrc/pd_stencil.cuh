@@ -44,6 +44,7 @@ struct FusedBufs {
     double* rd_out;
     const uint32_t* mask_in;
     uint32_t* mask_out;
+    const double* scale_dev = nullptr;  // tile9: per-step load scales copied H2D (or null)
 };
 
 void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,

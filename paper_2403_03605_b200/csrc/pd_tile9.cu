@@ -395,9 +395,10 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const int fl = (int)(dbits(im) & 7);  // 1: x constrained, 2: y constrained, 4: loaded
         double2 p = make_double2(0.0, 0.0);
         if (fl & 4) {
+            const double sc = bf.scale_dev ? bf.scale_dev[step] : scale;
             p = P2[n];
-            p.x *= scale;
-            p.y *= scale;
+            p.x *= sc;
+            p.y *= sc;
         }
         const double a0 = (fl & 1) ? 0.0 : (p.x - k0) * im;
         const double a1 = (fl & 2) ? 0.0 : (p.y - k1) * im;

@@ -108,6 +108,8 @@ struct pmts_pd {
     int peer_lo = -1, peer_hi = -1;
     int send_lo = 0, recv_lo = 0, n_lo = 0, send_hi = 0, recv_hi = 0, n_hi = 0;
     unsigned long long* h_counts = nullptr;  // pinned
+    void* h_map = nullptr;                   // mapped pinned staging (step_tracked)
+    size_t h_map_cap = 0;
     int h_counts_cap = 0;
     char* trk_buf = nullptr;         // pmts_pd_step_tracked staging
     size_t trk_cap = 0;
@@ -119,6 +121,7 @@ struct pmts_pd {
     ~pmts_pd() {
         if (stream) cudaStreamSynchronize(stream);
         if (h_counts) cudaFreeHost(h_counts);
+        if (h_map) cudaFreeHost(h_map);
         for (void* p : owned) cudaFree(p);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -722,10 +725,10 @@ void ensure_counts(pmts_pd* h, int n) {
 
 // one fine step: bond gather + node update with the fused predictor
 void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev,
-                  bool last = true) {
+                  bool last = true, const double* scale_dev = nullptr) {
     const int brk = h->fracture ? 1 : 0;
     if (h->fused) {
-        FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt};
+        FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt, scale_dev};
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
         if (h->tile9)
             launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
@@ -1128,9 +1131,10 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
         for (int j = 0; j < n_tracked; ++j)
             if (dofs[j] < 0 || dofs[j] >= h->ndof) throw ConfigError("tracked dof out of range");
         ensure_counts(h, std::max(n, 1));
-        // device staging (kept across calls): dofs, then per-step tracked values
+        // device staging (kept across calls): tracked dofs, per-step scales
         const size_t idx_bytes = (sizeof(int32_t) * n_tracked + 7) & ~size_t(7);
-        const size_t bytes = idx_bytes + sizeof(double) * (size_t)n * n_tracked;
+        const size_t scl_bytes = sizeof(double) * (size_t)std::max(n, 1);
+        const size_t bytes = idx_bytes + scl_bytes;
         if (bytes > h->trk_cap) {
             if (h->trk_buf) h->release(h->trk_buf);
             h->trk_cap = std::max<size_t>(bytes, 4096);
@@ -1138,25 +1142,50 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
             h->trk_dofs.clear();
         }
         int32_t* didx = reinterpret_cast<int32_t*>(h->trk_buf);
-        double* dtrk = reinterpret_cast<double*>(h->trk_buf + idx_bytes);
+        double* dscl = reinterpret_cast<double*>(h->trk_buf + idx_bytes);
+        // mapped pinned staging: per-step scales (read by the device), tracked rows
+        // and broken counts (written by the device)
+        const size_t need = sizeof(double) * ((size_t)n * (1 + n_tracked)) +
+                            sizeof(unsigned long long) * (size_t)n;
+        if (need > h->h_map_cap) {
+            if (h->h_map) cudaFreeHost(h->h_map);
+            h->h_map_cap = std::max<size_t>(need, 4096);
+            CK(cudaHostAlloc(&h->h_map, h->h_map_cap, cudaHostAllocMapped));
+        }
+        double* h_scl = reinterpret_cast<double*>(h->h_map);
+        double* h_trk = h_scl + n;
+        unsigned long long* h_cnt = reinterpret_cast<unsigned long long*>(h_trk + (size_t)n * n_tracked);
+        void* dmap = nullptr;
+        CK(cudaHostGetDevicePointer(&dmap, h->h_map, 0));
+        double* m_scl = reinterpret_cast<double*>(dmap);
+        double* m_trk = m_scl + n;
+        unsigned long long* m_cnt = reinterpret_cast<unsigned long long*>(m_trk + (size_t)n * n_tracked);
+        std::copy(scales, scales + n, h_scl);
         if (h->trk_dofs.size() != (size_t)n_tracked ||
             !std::equal(h->trk_dofs.begin(), h->trk_dofs.end(), dofs)) {
             h->trk_dofs.assign(dofs, dofs + n_tracked);
             if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
         }
+        // per step, all asynchronous on the handle's stream (one synchronisation at
+        // the end): the step (the tile9 kernel reads its load scale from device
+        // memory), then one tiny launch that writes the step's tracked row and
+        // broken count into mapped pinned host memory and moves the next step's
+        // scale from mapped pinned host memory to the device
+        if (n > 0) upload(dscl, h_scl, 1, h->stream);
         for (int s = 0; s < n; ++s) {
             // u of step s: the fused kernel's displacement is the step's predictor
             // (beta = 0), i.e. the rd buffer it consumed; the other paths write u
             const bool every = !h->fused;
-            enqueue_step(h, s, scales[s], false, nullptr, every || s == n - 1);
+            enqueue_step(h, s, scales[s], false, nullptr, every || s == n - 1,
+                         h->tile9 ? dscl : nullptr);
             const double* src = h->fused ? h->rd_alt : h->d.u;
-            launch_gather(src, didx, n_tracked, dtrk + (size_t)s * n_tracked, h->stream);
+            launch_track(src, didx, n_tracked, m_trk + (size_t)s * n_tracked, h->d_counts + s,
+                         m_cnt + s, s + 1 < n ? m_scl + s + 1 : nullptr,
+                         s + 1 < n ? dscl + s + 1 : nullptr, h->stream);
         }
-        unsigned long long* cnt = pinned_counts(h, n);
-        if (n_tracked && n)
-            download(tracked_out, dtrk, (size_t)n * n_tracked, h->stream);
-        download(cnt, h->d_counts, n, h->stream);
         CK(cudaStreamSynchronize(h->stream));
+        if (n_tracked && n) std::copy(h_trk, h_trk + (size_t)n * n_tracked, tracked_out);
+        const unsigned long long* cnt = h_cnt;
         int64_t nb = 0;
         for (int s = 0; s < n; ++s) {
             nb += (int64_t)cnt[s];
