@@ -232,6 +232,84 @@ int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t
 /* sum of an int64 over the clique (broken counts at output cadence) */
 int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value);
 
+/* ------------------------------------------------------------------------
+ * Coupled multi-time-step (Arlequin) integrator -- SURVEY.md 8(f) row 1.
+ * The reference's coupled run: build_scenario's coupled part
+ * (driver.hpp:211-222), assemble_global (fem.hpp:421-474), find_pe_pairs over
+ * the PD-active elements (mesh.hpp:416-495), assemble_pd_global with (1-alpha)
+ * weights (perifem.hpp:276-351), build_coupling_map (coupling.hpp:72-105) and
+ * CoupledIntegrator (mts.hpp:79-535).  FE and PD states, the unit responses
+ * and the Lagrange multipliers live on the device; the dense interface factor
+ * (n_lambda <= 400, or run.interface = dense) is solved on the host exactly as
+ * DenseLu does (linalg.hpp:368-412).  Explicit PD substeps only (beta_pd = 0,
+ * the BASELINE configs); the FE side may be explicit or implicit (PCG).
+ * ------------------------------------------------------------------------ */
+typedef struct pmts_mts pmts_mts;
+
+typedef struct {
+    const pmts_scenario_desc* scenario; /* mesh, material, [pd], loads, [time]; its
+                                           gamma/beta are the PD Newmark parameters.
+                                           Tractions stay surface loads (no bands). */
+    int32_t n_pd_box;            /* [region] pd_box<k>: lo[3] hi[3] per box */
+    const double* pd_boxes;
+    double overlap_width_factor; /* region.overlap_width_factor */
+    int32_t weight_kind;         /* 0 constant, 1 linear, 2 cubic (coupling.hpp:14-21) */
+    double gamma_fe, beta_fe;    /* time.gamma_fe / beta_fe */
+    int32_t interface_mode;      /* 0 auto, 1 dense, 2 matrix_free (mts.hpp:27) */
+    int32_t enforce_continuity;  /* run.enforce_continuity */
+    int32_t track_energy;        /* output.energy */
+    int32_t device;              /* CUDA ordinal */
+} pmts_mts_desc;
+
+typedef struct {
+    int32_t dim, n_nodes, n_elems, fe_n_dof, pd_n_dof, n_lambda, dense, m, n_macro;
+    int32_t fe_nnz, fe_n_bc, pd_n_bc, n_pd_elems;
+    int64_t n_pairs;
+    double dt_pd, delta, c0, l, char_length, load_ramp;
+    const int32_t* labels;       /* per element: 0 FE_only, 1 PD_only, 2 Overlap */
+    const double* alpha;         /* per element blend weight */
+    const int32_t* fe_node_dof;  /* per node: first FE dof or -1 */
+    const int32_t* pd_node_dof;
+    const int32_t* fe_k_rowptr;  /* FE stiffness, CSR (from_triplets order) */
+    const int32_t* fe_k_col;
+    const double* fe_k_val;
+    const double* fe_mass;
+    const double* fe_p_ext;
+    const double* pd_mass;
+    const double* pd_p_ext;
+    const int32_t* fe_bc_dofs;
+    const double* fe_bc_vel;
+    const int32_t* pd_bc_dofs;
+    const double* pd_bc_vel;
+    const int32_t* cpl_fe_dof;   /* coupling rows (node, component) ascending */
+    const int32_t* cpl_pd_dof;
+    const int32_t* pairs;        /* [n_pairs][2] global element ids, find_pe_pairs order */
+    const double* pe_weight;     /* [n_pairs] 1 - alpha at the bond midpoint */
+} pmts_mts_view;
+
+typedef struct {                 /* MacroReport (mts.hpp:41-63) */
+    double t_kinematic, t_update, t_lambda, t_unit;
+    double quad_fe, quad_pd, lambda_fe, lambda_pd;
+    double continuity;
+    int32_t newly_broken, interface_iterations;
+} pmts_mts_report;
+
+int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out);
+int pmts_mts_view_get(const pmts_mts* h, pmts_mts_view* view);
+/* CoupledIntegrator::initialize_accelerations (mts.hpp:133-140) */
+int pmts_mts_init(pmts_mts* h);
+/* n macro steps (mts.hpp:244-306); reports (optional) receives n records */
+int pmts_mts_macro_step(pmts_mts* h, int32_t n, pmts_mts_report* reports);
+/* device time of n macro steps (CUDA events around the whole sequence, host
+ * orchestration and host-side interface solves included) */
+int pmts_mts_macro_step_timed(pmts_mts* h, int32_t n, float* ms_out);
+/* which: 0 FE, 1 PD; (u, v, a) in that subdomain's dof order (nullable) */
+int pmts_mts_get_state(pmts_mts* h, int32_t which, double* u, double* v, double* a);
+int pmts_mts_get_lambda(pmts_mts* h, double* lambda_out);
+/* per pair (pmts_mts_view.pairs order): 1 intact, 0 broken */
+int pmts_mts_get_intact(pmts_mts* h, uint8_t* out);
+void pmts_mts_destroy(pmts_mts* h);
+
 #ifdef __cplusplus
 }
 #endif

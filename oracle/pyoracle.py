@@ -245,3 +245,61 @@ def run_ref(cfg_text: str, workdir: str, steps=None, dump=True, checkpoints=(), 
     r = subprocess.run(cmd, check=True, capture_output=True, text=True, env=env)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     return json.loads(line)
+
+
+REF_MTS_DRIVER = os.path.join(os.path.dirname(REF_DRIVER), "ref_mts_driver")
+
+_MTS_FILES = {
+    "labels": np.int32, "alpha": np.float64, "fe_node_dof": np.int32, "pd_node_dof": np.int32,
+    "fe_k_rowptr": np.int32, "fe_k_col": np.int32, "fe_k_val": np.float64,
+    "fe_mass": np.float64, "fe_p_ext": np.float64, "pd_k_rowptr": np.int32,
+    "pd_k_col": np.int32, "pd_k_val": np.float64, "pd_mass": np.float64, "pd_p_ext": np.float64,
+    "pairs": np.int32, "pe_weight": np.float64, "fe_bc_dofs": np.int32, "fe_bc_vel": np.float64,
+    "pd_bc_dofs": np.int32, "pd_bc_vel": np.float64, "fe_dof": np.int32, "pd_dof": np.int32,
+    "scale": np.float64, "lambda": np.float64, "broken": np.int32, "continuity": np.float64,
+    "energy": np.float64, "iterations": np.int32,
+}
+
+
+def run_ref_mts(cfg_text: str, workdir: str, steps=None, dump=True, checkpoints=(), extra=(),
+                env=None) -> dict:
+    """Run oracle/_ref/ref_mts_driver (the reference's own coupled loop)."""
+    import json
+    os.makedirs(workdir, exist_ok=True)
+    cfg = os.path.join(workdir, "scenario.cfg")
+    with open(cfg, "w") as f:
+        f.write(cfg_text)
+    cmd = [REF_MTS_DRIVER, cfg]
+    if steps is not None:
+        cmd += ["--steps", str(steps)]
+    if dump:
+        cmd += ["--dump", workdir]
+    if checkpoints:
+        cmd += ["--checkpoints", ",".join(str(c) for c in checkpoints)]
+    cmd += list(extra)
+    r = subprocess.run(cmd, check=True, capture_output=True, text=True, env=env)
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    return json.loads(line)
+
+
+def load_ref_mts_dump(d: str) -> dict:
+    """Arrays written by ref_mts_driver --dump (see oracle/ref_mts_driver.cpp)."""
+    out = {}
+    for name, dt in _MTS_FILES.items():
+        p = os.path.join(d, name + (".i32" if dt == np.int32 else ".f64"))
+        if os.path.exists(p):
+            out[name] = np.fromfile(p, dtype=dt)
+    out["pairs"] = out["pairs"].reshape(-1, 2)
+    out["broken"] = out["broken"].reshape(-1, 2)
+    out["energy"] = out["energy"].reshape(-1, 4)
+    for f in os.listdir(d):
+        if f.endswith(".f64") and f.split("_")[0] in ("fe", "pd", "fe0", "pd0", "lambda"):
+            key = f[:-4]
+            if key not in out:
+                out[key] = np.fromfile(os.path.join(d, f), dtype=np.float64)
+    with open(os.path.join(d, "meta.txt")) as fh:
+        for line in fh:
+            k, v = line.split()
+            out[k] = float(v) if "." in v or "e" in v else int(v)
+    return out
+

@@ -29,8 +29,10 @@ SOURCES = [
     ("pd_tile9.cu", []),
     ("pd_lat3.cu", []),
     ("pmts_pd.cu", ["-fmad=false"]),
+    ("pd_mts.cu", ["-fmad=false"]),
+    ("pmts_mts.cu", ["-fmad=false"]),
 ]
-HOST_SOURCES = ["pmts_setup.cpp"]
+HOST_SOURCES = ["pmts_setup.cpp", "pmts_mts_setup.cpp"]
 
 
 def _newer(target, deps):

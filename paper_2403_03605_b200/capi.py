@@ -75,6 +75,32 @@ class PDInfo(C.Structure):
 
 # exported symbols, with ctypes signatures: the CPU test checks the library
 # exports every one of them (and the header declares the same set).
+class MtsDesc(C.Structure):
+    _fields_ = [("scenario", C.POINTER(ScenarioDesc)), ("n_pd_box", _I), ("pd_boxes", _P),
+                ("overlap_width_factor", _D), ("weight_kind", _I), ("gamma_fe", _D),
+                ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
+                ("track_energy", _I), ("device", _I)]
+
+
+class MtsView(C.Structure):
+    _fields_ = [("dim", _I), ("n_nodes", _I), ("n_elems", _I), ("fe_n_dof", _I),
+                ("pd_n_dof", _I), ("n_lambda", _I), ("dense", _I), ("m", _I), ("n_macro", _I),
+                ("fe_nnz", _I), ("fe_n_bc", _I), ("pd_n_bc", _I), ("n_pd_elems", _I),
+                ("n_pairs", C.c_int64), ("dt_pd", _D), ("delta", _D), ("c0", _D), ("l", _D),
+                ("char_length", _D), ("load_ramp", _D), ("labels", _P), ("alpha", _P),
+                ("fe_node_dof", _P), ("pd_node_dof", _P), ("fe_k_rowptr", _P), ("fe_k_col", _P),
+                ("fe_k_val", _P), ("fe_mass", _P), ("fe_p_ext", _P), ("pd_mass", _P),
+                ("pd_p_ext", _P), ("fe_bc_dofs", _P), ("fe_bc_vel", _P), ("pd_bc_dofs", _P),
+                ("pd_bc_vel", _P), ("cpl_fe_dof", _P), ("cpl_pd_dof", _P), ("pairs", _P),
+                ("pe_weight", _P)]
+
+
+class MtsReport(C.Structure):
+    _fields_ = [("t_kinematic", _D), ("t_update", _D), ("t_lambda", _D), ("t_unit", _D),
+                ("quad_fe", _D), ("quad_pd", _D), ("lambda_fe", _D), ("lambda_pd", _D),
+                ("continuity", _D), ("newly_broken", _I), ("interface_iterations", _I)]
+
+
 SIGNATURES = {
     "pmts_last_error": (C.c_char_p, []),
     "pmts_abi_version": (C.c_int, []),
@@ -108,6 +134,15 @@ SIGNATURES = {
     "pmts_pd_comm_init": (C.c_int, [_P, _P, _I, _I]),
     "pmts_pd_set_halo": (C.c_int, [_P, _I, _I, _I, _I, _I, _I, _I, _I]),
     "pmts_pd_allreduce_sum": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "pmts_mts_create": (C.c_int, [C.POINTER(MtsDesc), C.POINTER(_P)]),
+    "pmts_mts_view_get": (C.c_int, [_P, C.POINTER(MtsView)]),
+    "pmts_mts_init": (C.c_int, [_P]),
+    "pmts_mts_macro_step": (C.c_int, [_P, _I, _P]),
+    "pmts_mts_macro_step_timed": (C.c_int, [_P, _I, C.POINTER(C.c_float)]),
+    "pmts_mts_get_state": (C.c_int, [_P, _I, _P, _P, _P]),
+    "pmts_mts_get_lambda": (C.c_int, [_P, _P]),
+    "pmts_mts_get_intact": (C.c_int, [_P, _P]),
+    "pmts_mts_destroy": (None, [_P]),
 }
 
 _lib = None

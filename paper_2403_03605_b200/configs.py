@@ -145,6 +145,42 @@ def scenarios() -> dict:
                                           hi=[0.007, 0.007, 0.005 + 1e-7])
     c4s["time"]["total_time"] = 2e-8 * 100
     s["cfg4_small"] = c4s
+
+    # --- coupled MTS --------------------------------
+    # Miniature coupled strip: 30 x 10 elements at 1 mm, PD box = middle third
+    # (full height, so no interior corners -- SURVEY F6), overlap one element,
+    # traction on the right (FE) face, left face fixed.  Explicit FE (beta_fe =
+    # 0, stable at 1 mm / 40 ns) and a dense interface (n_lambda <= 400).
+    mts = {
+        "mesh": {"kind": "generated", "dim": 2, "bounds": [0.0, 0.0, 0.03, 0.01],
+                 "spacing": 1e-3, "notch1": None},
+        "material": {"E": 65e9, "nu": 0.3333333333333333, "rho": 2235.0,
+                     "formulation": "plane_stress"},
+        "pd": {"delta_factor": 2.2, "l_factor": 8.0, "s_crit": 0.0},
+        "region": {"pd_box1": [0.01, 0.0, 0.02, 0.01], "overlap_width_factor": 1.0,
+                   "weight_kind": "cubic"},
+        "load": {"traction1": [0.03 - 1e-7, -0.001, 0.03 + 1e-7, 0.011, 40e6, 0.0],
+                 "fixed1": [-1e-7, -0.001, 1e-7, 0.011]},
+        "time": {"dt_pd": 2e-8, "m": 2, "total_time": 2e-8 * 2 * 40, "gamma_fe": 0.5,
+                 "beta_fe": 0.0, "gamma_pd": 0.5, "beta_pd": 0.0},
+        "run": {"mode": "coupled_mts", "interface": "auto"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+    s["mts_mini"] = mts
+    # implicit FE (Newmark beta 1/4: PCG solves), m = 4
+    mi = copy.deepcopy(mts)
+    mi["time"].update(beta_fe=0.25, m=4, total_time=2e-8 * 4 * 20)
+    s["mts_mini_implicit"] = mi
+    # fracture in the PD core: notch-free tension with a low critical stretch
+    mf = copy.deepcopy(mts)
+    mf["pd"]["s_crit"] = 2.5e-4
+    mf["time"].update(total_time=2e-8 * 2 * 60)
+    s["mts_mini_frac"] = mf
+    # matrix-free interface (forced), implicit FE
+    mm = copy.deepcopy(mi)
+    mm["run"]["interface"] = "matrix_free"
+    s["mts_mini_mfree"] = mm
     return s
 
 
@@ -192,7 +228,9 @@ def n_steps(sc: dict) -> int:
 def render_cfg(sc: dict) -> str:
     """Reference config text (proj/include/perimts/config.hpp format)."""
     out = []
-    for sec in ("mesh", "material", "pd", "load", "time", "run", "output"):
+    for sec in ("mesh", "material", "pd", "region", "load", "time", "run", "output"):
+        if sec not in sc:
+            continue
         out.append(f"[{sec}]")
         for k, v in sc[sec].items():
             if v is None:

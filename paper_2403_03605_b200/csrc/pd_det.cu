@@ -235,6 +235,29 @@ __global__ void k_init_acc(DevPD d, double scale) {
     }
 }
 
+// (K x)_n = sum over incident elements (ascending) of N G_e -- the node half
+// of the matrix-free K^PD x after k_det_bond(x); used by the MTS integrator
+template <int DIM>
+__global__ void k_node_force(DevPD d, double* __restrict__ kx) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= d.N) return;
+    double Ku[DIM];
+    for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
+    for (int q = 0; q < d.NE; ++q) {
+        const int e = d.ne[(size_t)q * d.N + n];
+        if (e < 0) break;
+        for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
+    }
+    for (int c = 0; c < DIM; ++c) kx[(size_t)n * DIM + c] = Ku[c];
+}
+
+void launch_node_force(const DevPD& d, double* kx, cudaStream_t s) {
+    const int blocks = (d.N + kThreads - 1) / kThreads;
+    if (d.dim == 2) k_node_force<2><<<blocks, kThreads, 0, s>>>(d, kx);
+    else k_node_force<3><<<blocks, kThreads, 0, s>>>(d, kx);
+    PMTS_CUDA(cudaGetLastError());
+}
+
 void launch_init_acc(const DevPD& d, double scale, cudaStream_t s) {
     const int blocks = (d.N + kThreads - 1) / kThreads;
     if (d.dim == 2) k_init_acc<2><<<blocks, kThreads, 0, s>>>(d, scale);

@@ -1,0 +1,46 @@
+// Launchers of the MTS integrator kernels (pd_mts.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pmts {
+namespace mtsk {
+
+void csr_spmv(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+              double* y, cudaStream_t s);
+void predict(int n, const double* u, const double* v, const double* a, double* rd, double* rv,
+             double dt, double cpv, double cpd, cudaStream_t s);
+// ra (nullable) is scaled by ra_scale; homog: constrained velocities 0 instead of bcvel
+void explicit_solve(int n, const double* ra, double ra_scale, const double* kd, const double* M,
+                    const uint8_t* cf, const double* rv, const double* rd, double gdt, double bdt2,
+                    const double* bcvel, int homog, double* u, double* v, double* a,
+                    cudaStream_t s);
+void rhs(int n, const double* ra, double ra_scale, const double* kd, const uint8_t* cf, double* b,
+         cudaStream_t s);
+void apply_a(int n, const double* x, const double* kx, const double* M, const uint8_t* cf,
+             double bdt2, double* y, cudaStream_t s);
+void finish(int n, const double* acc, const double* rv, const double* rd, double gdt, double bdt2,
+            const uint8_t* cf, const double* bcvel, int homog, double* u, double* v, double* a,
+            cudaStream_t s);
+void zero_constrained(int n, const uint8_t* cf, double* x, cudaStream_t s);
+void init_acc(int n, const double* p, const double* ku, const double* M, const uint8_t* cf,
+              double* a, cudaStream_t s);
+void scatter_add(int n, const int32_t* idx, const double* vals, double* dst, cudaStream_t s);
+void gather(int n, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+void scale(int n, const double* x, double sc, double* y, cudaStream_t s);
+void add(int n, const double* x, double* y, cudaStream_t s);  // y += x
+void add_states(int n, const double* a0, const double* a1, const double* a2, const double* b0,
+                const double* b1, const double* b2, double* o0, double* o1, double* o2,
+                cudaStream_t s);
+void cg_update(int n, const double* alpha_dev, const double* p, const double* ap, double* x,
+               double* r, cudaStream_t s);
+void precond(int n, const double* r, const double* jac, double* z, cudaStream_t s);
+void xpby(int n, const double* z, const double* beta_dev, double* p, cudaStream_t s);
+int dot_partials();
+void dot(int n, const double* x, const double* y, double* part, double* out, cudaStream_t s);
+void ratio(const double* num, const double* den, double* out, cudaStream_t s);
+void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream_t s);
+
+}  // namespace mtsk
+}  // namespace pmts

@@ -49,5 +49,10 @@ void element_geometry(int dim, int n_elems, const int32_t* conn, const double* n
                       double* centroid, double* volume);
 double char_length(int dim, int n_elems, const double* volume);
 double calibrate_c0(double E, double delta, double l, int formulation);
+// reference_shape gradients / values (fem.hpp:22-47) and the Jacobian
+// determinant of shape_and_gradients (fem.hpp:51-79); nodes are xyz triples
+void corner_gradient(int dim, const double* xi, int a, double* g);
+double shape_value(int dim, const double* xi, int a);
+double jacobian_det(int dim, const int32_t* en, const double* nodes, const double* xi);
 
 }  // namespace pmts

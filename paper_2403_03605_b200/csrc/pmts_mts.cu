@@ -1,0 +1,1060 @@
+// Coupled multi-time-step (Arlequin) integrator on the device -- SURVEY.md
+// 8(f) row 1, behind pmts_mts_* (include/pmts_capi.h).
+//
+// A restatement of the reference's CoupledIntegrator (mts.hpp:79-535) with
+// every FE / PD state, unit response and multiplier vector resident in HBM:
+//   * FE operator: the alpha-weighted stiffness in CSR, assembled on the host
+//     exactly as the reference (pmts_mts_setup.cpp), applied in the
+//     reference's row order (pd_mts.cu); implicit FE solves are the
+//     reference's Jacobi-PCG (linalg.hpp:243-296) with device reductions;
+//   * PD operator: the matrix-free K^PD x of the deterministic kernels
+//     (pd_det.cu) over the PD-active elements, per-pair (1 - alpha) weights in
+//     the bond coefficients, the live bond mask and the unit-response snapshot
+//     (k_sync_, mts.hpp:98) as two bit masks; the bond test of each free PD
+//     substep is fused into that substep's force pass (beta_pd = 0: the tested
+//     displacement is the force's predictor, mts.hpp:159-177);
+//   * interface: dense H = H_FE + G_PD vel(Y_PD) factored on the host with the
+//     reference's DenseLu (linalg.hpp:368-412), or the matrix-free CG on the
+//     device (apply_h_pd = m linear PD substeps per iteration, mts.hpp:184-215,
+//     410-420).
+// The summation order of K x differs from the reference's CSR (matrix-free PD,
+// device CG reductions), so parity is to rounding (tests/test_gpu_mts.py), the
+// setup arrays bitwise (tests/test_mts_setup.py).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "pd_common.cuh"
+#include "pd_mts.cuh"
+#include "pmts_mts_setup.h"
+
+namespace pmts {
+DevPD pd_internal_dev(pmts_pd* h);
+cudaStream_t pd_internal_stream(pmts_pd* h);
+void pd_internal_pair_weights(pmts_pd* h, const double* w);
+}  // namespace pmts
+
+using namespace pmts;
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw InternalError(std::string("CUDA: ") + cudaGetErrorString(e) + " (" + what + ")");
+}
+#define CKM(x) ck((x), #x)
+
+void check_pd(int status) {
+    if (status == PMTS_OK) return;
+    const std::string msg = pmts_last_error();
+    if (status == PMTS_ERR_CONFIG) throw ConfigError(msg);
+    if (status == PMTS_ERR_SOLVER) throw SolverError(msg);
+    throw InternalError(msg);
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+// DenseLu (linalg.hpp:368-412), host: the interface factor
+struct HostLu {
+    std::vector<double> lu;
+    std::vector<int> perm;
+    int n = 0;
+    void factor(std::vector<double> a, int nn) {
+        n = nn;
+        lu = std::move(a);
+        double amax = 0.0;
+        for (double v : lu) amax = std::max(amax, std::abs(v));
+        perm.resize(n);
+        for (int i = 0; i < n; ++i) perm[i] = i;
+        for (int k = 0; k < n; ++k) {
+            int piv = k;
+            double best = std::abs(lu[(size_t)k * n + k]);
+            for (int i = k + 1; i < n; ++i) {
+                const double v = std::abs(lu[(size_t)i * n + k]);
+                if (v > best) {
+                    best = v;
+                    piv = i;
+                }
+            }
+            if (best <= 1e-14 * std::max(amax, 1e-300))
+                throw SolverError("singular interface system: coincident or disconnected overlap");
+            if (piv != k) {
+                std::swap(perm[k], perm[piv]);
+                for (int j = 0; j < n; ++j) std::swap(lu[(size_t)k * n + j], lu[(size_t)piv * n + j]);
+            }
+            const double inv = 1.0 / lu[(size_t)k * n + k];
+            for (int i = k + 1; i < n; ++i) {
+                const double f = lu[(size_t)i * n + k] * inv;
+                lu[(size_t)i * n + k] = f;
+                if (f == 0.0) continue;
+                for (int j = k + 1; j < n; ++j) lu[(size_t)i * n + j] -= f * lu[(size_t)k * n + j];
+            }
+        }
+    }
+    std::vector<double> solve(const std::vector<double>& b) const {
+        std::vector<double> x(n);
+        for (int i = 0; i < n; ++i) x[i] = b[perm[i]];
+        for (int i = 1; i < n; ++i) {
+            double s = x[i];
+            for (int j = 0; j < i; ++j) s -= lu[(size_t)i * n + j] * x[j];
+            x[i] = s;
+        }
+        for (int ii = n; ii-- > 0;) {
+            double s = x[ii];
+            for (int j = ii + 1; j < n; ++j) s -= lu[(size_t)ii * n + j] * x[j];
+            x[ii] = s / lu[(size_t)ii * n + ii];
+        }
+        return x;
+    }
+};
+
+struct DState {
+    double *u = nullptr, *v = nullptr, *a = nullptr;
+};
+
+// Newmark coefficients rounded as the reference's expressions
+struct Nm {
+    double gamma = 0.5, beta = 0.0, dt = 0.0;
+    double cpv = 0, cpd = 0, gdt = 0, bdt2 = 0;
+    void set(double g, double b, double d) {
+        gamma = g;
+        beta = b;
+        dt = d;
+        cpv = dt * (1.0 - gamma);          // newmark.hpp:65
+        cpd = dt * dt * (0.5 - beta);      // newmark.hpp:66
+        gdt = gamma * dt;                  // newmark.hpp:153
+        bdt2 = beta * dt * dt;             // newmark.hpp:141,154
+    }
+    bool explicit_scheme() const { return beta == 0.0; }
+};
+
+}  // namespace
+
+struct pmts_mts {
+    MtsSystem s;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    pmts_pd* pd = nullptr;
+    DevPD pdv{};
+    std::vector<int32_t> pairs;  // global ids
+    std::vector<double> pe_weight;
+    int nf = 0, np = 0, nl = 0, npe = 0, m = 1;
+    Nm fe_nm, pd_nm;
+    int iface_mode = 0;
+    bool enforce_continuity = true, track_energy = true, fracture = false;
+    double continuity_tol = 1e-8, cg_tol = 1e-10, interface_cg_tol = 1e-11;
+    int fe_cg_max = 100;
+    std::vector<void*> owned;
+    // device: FE
+    int32_t *fe_rp = nullptr, *fe_ci = nullptr;
+    double *fe_v = nullptr, *fe_M = nullptr, *fe_P = nullptr, *fe_bcv = nullptr, *fe_jac = nullptr;
+    uint8_t* fe_cf = nullptr;
+    // device: PD
+    double *pd_M = nullptr, *pd_P = nullptr, *pd_bcv = nullptr;
+    uint8_t* pd_cf = nullptr;
+    uint32_t *mask_live = nullptr, *mask_sync = nullptr;
+    size_t mask_words = 0;
+    unsigned long long* d_counts = nullptr;  // per substep slot
+    int counts_cap = 0;
+    // device: coupling
+    int32_t *cfe = nullptr, *cpd = nullptr;
+    // device: states and scratch
+    DState ufe, upd, vfe, vpd, wst, yst, fe_prev;
+    double *rd = nullptr, *rv = nullptr, *ra = nullptr, *kd = nullptr;     // size max(nf, np)
+    double *cg_b = nullptr, *cg_x = nullptr, *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr,
+           *cg_ap = nullptr, *cg_kx = nullptr;                             // size max(nf, nl)
+    double *part = nullptr, *scal = nullptr;                               // reductions
+    double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
+    double* hfe_d = nullptr;                                               // nl x nl
+    double *warm_fe_free = nullptr, *warm_fe_link = nullptr;
+    bool warm_free_ok = false, warm_link_ok = false;
+    // host interface state
+    std::vector<double> lambda_prev, lambda, g_p_fe, h_fe, h;
+    HostLu lu;
+    bool h_valid = false, unit_stale = false, use_dense = true;
+    double t = 0.0;
+    std::vector<std::vector<double>> gp_free, gp_link;
+    std::vector<double> fe_prev_gvel;
+    int64_t broken_total = 0;
+
+    ~pmts_mts() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : owned) cudaFree(p);
+        if (pd) pmts_pd_destroy(pd);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    template <class T>
+    T* alloc(size_t n) {
+        T* p = nullptr;
+        CKM(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+        owned.push_back(p);
+        return p;
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v) {
+        T* p = alloc<T>(v.size());
+        if (!v.empty()) CKM(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, stream));
+        return p;
+    }
+    DState state(int n) {
+        DState st{alloc<double>(n), alloc<double>(n), alloc<double>(n)};
+        zero(st, n);
+        return st;
+    }
+    void zero(const DState& st, int n) {
+        CKM(cudaMemsetAsync(st.u, 0, sizeof(double) * n, stream));
+        CKM(cudaMemsetAsync(st.v, 0, sizeof(double) * n, stream));
+        CKM(cudaMemsetAsync(st.a, 0, sizeof(double) * n, stream));
+    }
+    void copy(const DState& dst, const DState& src, int n) {
+        CKM(cudaMemcpyAsync(dst.u, src.u, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+        CKM(cudaMemcpyAsync(dst.v, src.v, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+        CKM(cudaMemcpyAsync(dst.a, src.a, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+    }
+    std::vector<double> to_host(const double* d, int n) {
+        std::vector<double> h(n);
+        if (n) CKM(cudaMemcpyAsync(h.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        return h;
+    }
+    void to_dev(double* d, const std::vector<double>& h) {
+        if (!h.empty()) CKM(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, stream));
+    }
+    double scalar(const double* d) {
+        double v = 0.0;
+        CKM(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        return v;
+    }
+
+    double load_scale(double tt) const {
+        const double ramp = s.ramp;
+        if (ramp <= 0.0) return 1.0;
+        return std::clamp(tt / ramp, 0.0, 1.0);
+    }
+    double dt_fe() const { return m * s.dt_pd; }
+
+    // ---- operators ----
+    void fe_K(const double* x, double* y) { mtsk::csr_spmv(nf, fe_rp, fe_ci, fe_v, x, y, stream); }
+    // K^PD x with the given bond mask; do_break: the inclusive stretch test on x
+    // updates that mask (count into slot)
+    void pd_K(const double* x, double* y, uint32_t* mask, bool do_break, int slot) {
+        DevPD d = pdv;
+        d.mask = mask;
+        d.log = nullptr;
+        d.broken_count = d_counts;
+        launch_det_bond(d, x, slot, do_break ? 1 : 0, 0, stream);
+        launch_node_force(d, y, stream);
+    }
+
+    // reference cg_solve (linalg.hpp:243-296) on the device; A applied by op(x, y)
+    template <class Op>
+    int cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac) {
+        double* r = cg_r;
+        double* z = cg_z;
+        double* p = cg_p;
+        double* ap = cg_ap;
+        double* s_bb = scal + 0;
+        double* s_rz = scal + 1;
+        double* s_rr = scal + 2;
+        double* s_pap = scal + 3;
+        double* s_alpha = scal + 4;
+        double* s_rzn = scal + 5;
+        double* s_beta = scal + 6;
+        mtsk::dot(n, b, b, part, s_bb, stream);
+        const double bnorm = std::sqrt(scalar(s_bb));
+        if (bnorm == 0.0) {
+            CKM(cudaMemsetAsync(x, 0, sizeof(double) * n, stream));
+            return 0;
+        }
+        op(x, ap);
+        sub(n, b, ap, r);  // r = b - A x
+        mtsk::precond(n, r, jac, z, stream);
+        CKM(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+        mtsk::dot(n, r, z, part, s_rz, stream);
+        mtsk::dot(n, r, r, part, s_rr, stream);
+        double rnorm = std::sqrt(scalar(s_rr));
+        int it = 0;
+        while (rnorm / bnorm > tol) {
+            if (it >= max_iter)
+                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
+                                  " iterations, residual " + std::to_string(rnorm / bnorm));
+            op(p, ap);
+            mtsk::dot(n, p, ap, part, s_pap, stream);
+            const double pap = scalar(s_pap);
+            if (pap <= 0.0)
+                throw SolverError("cg: operator not positive definite (p'Ap = " +
+                                  std::to_string(pap) + ")");
+            mtsk::ratio(s_rz, s_pap, s_alpha, stream);
+            mtsk::cg_update(n, s_alpha, p, ap, x, r, stream);
+            mtsk::precond(n, r, jac, z, stream);
+            mtsk::dot(n, r, z, part, s_rzn, stream);
+            mtsk::ratio(s_rzn, s_rz, s_beta, stream);
+            mtsk::xpby(n, z, s_beta, p, stream);
+            CKM(cudaMemcpyAsync(s_rz, s_rzn, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+            mtsk::dot(n, r, r, part, s_rr, stream);
+            rnorm = std::sqrt(scalar(s_rr));
+            ++it;
+        }
+        return it;
+    }
+    void sub(int n, const double* b, const double* ap, double* r) {
+        // r = b - ap, elementwise, exactly as the reference's r[i] = b[i] - ap[i]
+        mtsk::rhs(n, b, 1.0, ap, zero_flags(n), r, stream);
+    }
+    uint8_t* zf = nullptr;
+    int zf_n = 0;
+    const uint8_t* zero_flags(int n) {
+        if (n > zf_n) {
+            zf = alloc<uint8_t>(n);
+            CKM(cudaMemsetAsync(zf, 0, n, stream));
+            zf_n = n;
+        }
+        return zf;
+    }
+
+    // BlockOperator::solve (newmark.hpp:122-159) for the FE subdomain.  rhs.a =
+    // ra * ra_scale (ra nullable); rv, rd the predictor rows.
+    void fe_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
+                  double* warm, bool* warm_ok, bool homog, const DState& out) {
+        fe_K(rdp, kd);
+        if (fe_nm.explicit_scheme()) {
+            mtsk::explicit_solve(nf, ra, ra_scale, kd, fe_M, fe_cf, rvp, rdp, fe_nm.gdt, fe_nm.bdt2,
+                                 fe_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
+            return;
+        }
+        mtsk::rhs(nf, ra, ra_scale, kd, fe_cf, cg_b, stream);
+        if (warm && warm_ok && *warm_ok) {
+            CKM(cudaMemcpyAsync(cg_x, warm, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
+            mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
+        } else {
+            CKM(cudaMemsetAsync(cg_x, 0, sizeof(double) * nf, stream));
+        }
+        const double bdt2 = fe_nm.bdt2;
+        cg(nf,
+           [&](const double* x, double* y) {
+               fe_K(x, cg_kx);
+               mtsk::apply_a(nf, x, cg_kx, fe_M, fe_cf, bdt2, y, stream);
+           },
+           cg_b, cg_x, cg_tol, fe_cg_max, fe_jac);
+        mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
+        if (warm) {
+            CKM(cudaMemcpyAsync(warm, cg_x, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
+            if (warm_ok) *warm_ok = true;
+        }
+        mtsk::finish(nf, cg_x, rvp, rdp, fe_nm.gdt, fe_nm.bdt2, fe_cf, fe_bcv, homog ? 1 : 0, out.u,
+                     out.v, out.a, stream);
+    }
+    // explicit PD solve (beta_pd = 0); the bond test on rd when do_break
+    void pd_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
+                  uint32_t* mask, bool do_break, int slot, bool homog, const DState& out) {
+        pd_K(rdp, kd, mask, do_break, slot);
+        mtsk::explicit_solve(np, ra, ra_scale, kd, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
+                             pd_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
+    }
+
+    // ---- coupling (coupling.hpp:46-68) ----
+    std::vector<double> gather_fe(const double* x) {
+        mtsk::gather(nl, cfe, x, gvec, stream);
+        return to_host(gvec, nl);
+    }
+    std::vector<double> gather_pd(const double* x) {
+        mtsk::gather(nl, cpd, x, gvec, stream);
+        return to_host(gvec, nl);
+    }
+    // dst[cpl[r]] += vals[r] (host vals, uploaded)
+    void add_gt(const int32_t* cpl, const std::vector<double>& vals, double* dst) {
+        to_dev(lam_tmp, vals);
+        mtsk::scatter_add(nl, cpl, lam_tmp, dst, stream);
+    }
+    void zero_vec(double* x, int n) { CKM(cudaMemsetAsync(x, 0, sizeof(double) * n, stream)); }
+
+    // ---- unit responses (mts.hpp:389-445) ----
+    void unit_fe_column(int k, const DState& y) {
+        // M_block Y = -G^T e_k, homogeneous, no warm start
+        zero_vec(ra, nf);
+        zero_vec(rv, nf);
+        zero_vec(rd, nf);
+        const double m1 = -1.0;
+        CKM(cudaMemcpyAsync(ra + s.cpl_fe[k], &m1, sizeof(double), cudaMemcpyHostToDevice, stream));
+        CKM(cudaStreamSynchronize(stream));
+        fe_solve(ra, 1.0, rv, rd, nullptr, nullptr, true, y);
+    }
+    void unit_pd_column(int k, const DState& y) {
+        zero(y, np);
+        for (int j = 1; j <= m; ++j) {
+            mtsk::predict(np, y.u, y.v, y.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+            zero_vec(ra, np);
+            const double val = double(j) / m;
+            CKM(cudaMemcpyAsync(ra + s.cpl_pd[k], &val, sizeof(double), cudaMemcpyHostToDevice, stream));
+            CKM(cudaStreamSynchronize(stream));
+            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, y);
+        }
+    }
+    void build_h_fe() {
+        h_fe.assign((size_t)nl * nl, 0.0);
+        for (int k = 0; k < nl; ++k) {
+            unit_fe_column(k, yst);
+            const std::vector<double> g = gather_fe(yst.v);
+            for (int r = 0; r < nl; ++r) h_fe[(size_t)r * nl + k] = -g[r];
+        }
+        if (!use_dense || iface_mode == 2) {
+            hfe_d = alloc<double>((size_t)nl * nl);
+            to_dev(hfe_d, h_fe);
+        }
+    }
+    void refresh_dense_interface() {
+        h = h_fe;
+        for (int k = 0; k < nl; ++k) {
+            unit_pd_column(k, yst);
+            const std::vector<double> g = gather_pd(yst.v);
+            for (int r = 0; r < nl; ++r) h[(size_t)r * nl + k] += g[r];
+        }
+        lu.factor(h, nl);
+        h_valid = true;
+    }
+    // G_PD vel(Y_PD_m) w without materialising Y (mts.hpp:410-420), device in/out
+    void apply_h_pd(const double* w_dev, double* out_dev) {
+        zero(yst, np);
+        for (int j = 1; j <= m; ++j) {
+            mtsk::predict(np, yst.u, yst.v, yst.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+            zero_vec(ra, np);
+            mtsk::scale(nl, w_dev, double(j) / m, lam_tmp, stream);
+            mtsk::scatter_add(nl, cpd, lam_tmp, ra, stream);
+            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, yst);
+        }
+        mtsk::gather(nl, cpd, yst.v, out_dev, stream);
+    }
+
+    // ---- the macro step (mts.hpp:133-306) ----
+    std::vector<double> s_vector(int j) const {
+        const double w = double(j) / m;
+        std::vector<double> sv(nl);
+        const double bracket = load_scale(t + j * s.dt_pd) - (1.0 - w) * load_scale(t) -
+                               w * load_scale(t + dt_fe());
+        for (int r = 0; r < nl; ++r) sv[r] = (1.0 - w) * lambda_prev[r] + bracket * g_p_fe[r];
+        return sv;
+    }
+    static std::vector<double> scaled(const std::vector<double>& v, double f) {
+        std::vector<double> o = v;
+        for (double& x : o) x *= f;
+        return o;
+    }
+
+    void initialize_accelerations() {
+        // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
+        mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
+        add_gt(cfe, scaled(lambda_prev, -1.0), ra);
+        fe_K(ufe.u, kd);
+        mtsk::init_acc(nf, ra, kd, fe_M, fe_cf, ufe.a, stream);
+        mtsk::scale(np, pd_P, load_scale(t), ra, stream);
+        add_gt(cpd, lambda_prev, ra);
+        pd_K(upd.u, kd, mask_live, false, 0);
+        mtsk::init_acc(np, ra, kd, pd_M, pd_cf, upd.a, stream);
+        CKM(cudaStreamSynchronize(stream));
+    }
+
+    std::vector<double> interface_solve(int* iterations) {
+        std::vector<double> rhs = gather_fe(vfe.v);
+        const std::vector<double> gp = gather_pd(vpd.v);
+        for (int r = 0; r < nl; ++r) rhs[r] -= gp[r];
+        if (use_dense) {
+            if (!h_valid) throw InternalError("interface solve with stale unit response");
+            *iterations = 0;
+            return lu.solve(rhs);
+        }
+        // matrix-free CG (no preconditioner), warm start lambda_prev
+        to_dev(lam_d, lambda_prev);
+        double* b = alloc_iface_b();
+        to_dev(b, rhs);
+        try {
+            const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
+            *iterations = cg(nl,
+                             [&](const double* in, double* out) {
+                                 mtsk::dense_matvec(nl, hfe_d, in, out, stream);
+                                 apply_h_pd(in, iface_tmp);
+                                 mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
+                             },
+                             b, lam_d, interface_cg_tol, max_iter, nullptr);
+        } catch (const SolverError&) {
+            use_dense = true;
+            h_valid = false;
+            refresh_dense_interface();
+            *iterations = 0;
+            return lu.solve(rhs);
+        }
+        return to_host(lam_d, nl);
+    }
+    double* iface_b = nullptr;
+    double* iface_tmp = nullptr;
+    double* alloc_iface_b() {
+        if (!iface_b) {
+            iface_b = alloc<double>(nl);
+            iface_tmp = alloc<double>(nl);
+        }
+        return iface_b;
+    }
+
+    pmts_mts_report macro_step();
+};
+
+namespace {
+
+// FE side BlockOperator diagonal (refresh_diagonal, newmark.hpp:99-104)
+std::vector<double> jacobi_diag(const MtsSystem& s, double bdt2) {
+    std::vector<double> d(s.fe_n_dof, 0.0);
+    if (bdt2 != 0.0)
+        for (int i = 0; i < s.fe_n_dof; ++i)
+            for (int p = s.fe_rowptr[i]; p < s.fe_rowptr[i + 1]; ++p)
+                if (s.fe_col[p] == i) {
+                    d[i] = s.fe_val[p];
+                    break;
+                }
+    for (int i = 0; i < s.fe_n_dof; ++i) d[i] = s.fe_mass[i] + bdt2 * d[i];
+    return d;
+}
+
+}  // namespace
+
+pmts_mts_report pmts_mts::macro_step() {
+    pmts_mts_report rep{};
+    // snapshot_previous (mts.hpp:507-510)
+    CKM(cudaMemcpyAsync(fe_prev.a, ufe.a, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
+    fe_prev_gvel = gather_fe(ufe.v);
+    // unit-response upkeep (mts.hpp:249-260)
+    {
+        const double t0 = now_s();
+        if (unit_stale) {
+            CKM(cudaMemcpyAsync(mask_sync, mask_live, sizeof(uint32_t) * mask_words,
+                                cudaMemcpyDeviceToDevice, stream));
+            h_valid = false;
+            unit_stale = false;
+            if (use_dense) refresh_dense_interface();
+        }
+        CKM(cudaStreamSynchronize(stream));
+        rep.t_unit = now_s() - t0;
+    }
+    if (counts_cap < m + 1) {
+        d_counts = alloc<unsigned long long>(m + 1);
+        counts_cap = m + 1;
+    }
+    CKM(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * (m + 1), stream));
+    // free FE solve (mts.hpp:143-147)
+    const double tk0 = now_s();
+    mtsk::predict(nf, ufe.u, ufe.v, ufe.a, rd, rv, fe_nm.dt, fe_nm.cpv, fe_nm.cpd, stream);
+    fe_solve(fe_P, load_scale(t + dt_fe()), rv, rd, warm_fe_free, &warm_free_ok, false, vfe);
+    CKM(cudaStreamSynchronize(stream));
+    const double fe_seconds = now_s() - tk0;
+    // free PD solve, m substeps with the known multiplier load S_j (mts.hpp:152-180)
+    const double tp0 = now_s();
+    gp_free.assign(m + 1, std::vector<double>(nl, 0.0));
+    gp_free[0] = gather_pd(upd.v);
+    copy(vpd, upd, np);
+    for (int j = 1; j <= m; ++j) {
+        mtsk::predict(np, vpd.u, vpd.v, vpd.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+        mtsk::scale(np, pd_P, load_scale(t + j * s.dt_pd), ra, stream);
+        add_gt(cpd, s_vector(j), ra);
+        pd_solve(ra, 1.0, rv, rd, mask_live, fracture, j, false, vpd);
+        gp_free[j] = gather_pd(vpd.v);
+    }
+    CKM(cudaStreamSynchronize(stream));
+    const double pd_seconds = now_s() - tp0;
+    rep.t_kinematic = std::max(fe_seconds, pd_seconds);
+    // interface solve + recombination (mts.hpp:184-241)
+    const double tl0 = now_s();
+    int iters = 0;
+    lambda = interface_solve(&iters);
+    rep.interface_iterations = iters;
+    {  // FE correction: M_block W = -G^T lambda
+        zero_vec(ra, nf);
+        zero_vec(rv, nf);
+        zero_vec(rd, nf);
+        add_gt(cfe, scaled(lambda, -1.0), ra);
+        fe_solve(ra, 1.0, rv, rd, warm_fe_link, &warm_link_ok, true, wst);
+        mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst.u, wst.v, wst.a, ufe.u, ufe.v, ufe.a, stream);
+    }
+    {  // PD correction: m substeps under the ramped multiplier load, on k_sync
+        zero(wst, np);
+        gp_link.assign(m + 1, std::vector<double>(nl, 0.0));
+        for (int j = 1; j <= m; ++j) {
+            mtsk::predict(np, wst.u, wst.v, wst.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+            zero_vec(ra, np);
+            add_gt(cpd, scaled(lambda, double(j) / m), ra);
+            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, wst);
+            gp_link[j] = gather_pd(wst.v);
+        }
+        mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
+    }
+    CKM(cudaStreamSynchronize(stream));
+    rep.t_lambda = now_s() - tl0;
+    // bonds broken in the free substeps, then the post-recombination audit
+    const double tu0 = now_s();
+    if (fracture) {
+        pd_K(upd.u, kd, mask_live, true, 0);  // slot 0: the audit
+        std::vector<unsigned long long> cnt(m + 1);
+        CKM(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(unsigned long long) * (m + 1),
+                            cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        long long nb = 0;
+        for (auto c : cnt) nb += (long long)c;
+        if (nb > 0) unit_stale = true;
+        rep.newly_broken = (int32_t)nb;
+        broken_total += nb;
+    }
+    rep.t_update = now_s() - tu0;
+    // energy record (mts.hpp:447-504)
+    if (track_energy) {
+        if (fe_nm.gamma != 0.5) {
+            double* da = cg_kx;  // scratch, nf
+            mtsk::rhs(nf, ufe.a, 1.0, fe_prev.a, zero_flags(nf), da, stream);  // da = acc - prev
+            const std::vector<double> dah = to_host(da, nf);
+            fe_K(da, cg_ap);
+            const std::vector<double> ka = to_host(cg_ap, nf);
+            double quad = 0.0;
+            const double f = fe_nm.dt * fe_nm.dt * (fe_nm.beta - fe_nm.gamma / 2.0);
+            for (int i = 0; i < nf; ++i) quad += dah[i] * (s.fe_mass[i] * dah[i] + f * ka[i]);
+            rep.quad_fe = -(fe_nm.gamma - 0.5) * quad;
+        }
+        {
+            const std::vector<double> gf_m = gather_fe(ufe.v);
+            double sum = 0.0;
+            for (int r = 0; r < nl; ++r)
+                sum += (gf_m[r] - fe_prev_gvel[r]) * (lambda[r] - lambda_prev[r]);
+            rep.lambda_fe = sum / dt_fe();
+        }
+        {
+            double sum = 0.0;
+            for (int j = 1; j <= m; ++j) {
+                const std::vector<double> sj = s_vector(j), sjm = s_vector(j - 1);
+                for (int r = 0; r < nl; ++r) {
+                    const double vel_j = gp_free[j][r] + gp_link[j][r];
+                    const double vel_jm = gp_free[j - 1][r] + (j > 1 ? gp_link[j - 1][r] : 0.0);
+                    const double lam_j = sj[r] + (double(j) / m) * lambda[r];
+                    const double lam_jm = sjm[r] + (double(j - 1) / m) * lambda[r];
+                    sum += (vel_j - vel_jm) * (lam_j - lam_jm);
+                }
+            }
+            rep.lambda_pd = -sum / s.dt_pd;
+        }
+    }
+    // continuity residual (mts.hpp:309-317)
+    {
+        const std::vector<double> gf = gather_fe(ufe.v), gp = gather_pd(upd.v);
+        double resid = 0.0;
+        for (int r = 0; r < nl; ++r) resid = std::max(resid, std::abs(gf[r] - gp[r]));
+        const std::vector<double> vf = to_host(ufe.v, nf), vp = to_host(upd.v, np);
+        double nf_inf = 0.0, np_inf = 0.0;
+        for (double x : vf) nf_inf = std::max(nf_inf, std::abs(x));
+        for (double x : vp) np_inf = std::max(np_inf, std::abs(x));
+        rep.continuity = resid / std::max(1.0, std::max(nf_inf, np_inf));
+        if (enforce_continuity && rep.continuity > continuity_tol)
+            throw SolverError("velocity continuity violated: residual " +
+                              std::to_string(rep.continuity) + " at t=" +
+                              std::to_string(t + dt_fe()));
+    }
+    lambda_prev = lambda;
+    t += dt_fe();
+    return rep;
+}
+
+namespace {
+
+void build_host(pmts_mts& h, const pmts_mts_desc& d) {
+    const pmts_scenario_desc& sd = *d.scenario;
+    MtsSystem& s = h.s;
+    // mesh + geometry + material: the pure-PD scenario builder's generator
+    pmts_scenario* sc = nullptr;
+    {
+        // build a scenario without loads (tractions stay surface loads here)
+        pmts_scenario_desc g = sd;
+        g.n_traction = 0;
+        g.n_body_patch = 0;
+        g.n_velocity_bc = 0;
+        g.n_fixed = 0;
+        check_pd(pmts_scenario_build(&g, &sc));
+    }
+    pmts_scenario_view v{};
+    pmts_scenario_get(sc, &v);
+    s.dim = v.dim;
+    for (int k = 0; k < 3; ++k) s.n[k] = v.lattice[k];
+    s.nodes.assign(v.node_xyz, v.node_xyz + 3 * (size_t)v.n_nodes);
+    const int nn = v.dim == 2 ? 4 : 8;
+    s.conn.assign(v.elem_nodes, v.elem_nodes + (size_t)nn * v.n_elems);
+    s.centroid.assign(v.centroid, v.centroid + 3 * (size_t)v.n_elems);
+    s.volume.assign(v.volume, v.volume + v.n_elems);
+    s.cl = v.char_length;
+    s.delta = v.delta;
+    s.l = v.l;
+    s.c0 = v.c0;
+    s.s_crit = sd.s_crit;
+    s.ramp = v.load_ramp;
+    pmts_scenario_destroy(sc);
+    s.E = sd.E;
+    s.nu = sd.nu;
+    s.rho = sd.rho;
+    s.formulation = sd.formulation;
+    for (int p = 0; p < sd.n_traction; ++p) {
+        MtsTraction t;
+        for (int k = 0; k < 3; ++k) {
+            t.box.lo[k] = sd.traction[9 * p + k];
+            t.box.hi[k] = sd.traction[9 * p + 3 + k];
+            t.value[k] = sd.traction[9 * p + 6 + k];
+        }
+        s.tractions.push_back(t);
+    }
+    for (int p = 0; p < sd.n_body_patch; ++p) {
+        MtsTraction t;
+        for (int k = 0; k < 3; ++k) {
+            t.box.lo[k] = sd.body_patch[9 * p + k];
+            t.box.hi[k] = sd.body_patch[9 * p + 3 + k];
+            t.value[k] = sd.body_patch[9 * p + 6 + k];
+        }
+        s.body_patches.push_back(t);
+    }
+    for (int k = 0; k < 3; ++k) s.body_force[k] = sd.body_force[k];
+    for (int b = 0; b < sd.n_velocity_bc; ++b) {
+        MtsKinematic kb;
+        for (int k = 0; k < 3; ++k) {
+            kb.box.lo[k] = sd.velocity_bc[8 * b + k];
+            kb.box.hi[k] = sd.velocity_bc[8 * b + 3 + k];
+        }
+        kb.comp = int(sd.velocity_bc[8 * b + 6]);
+        kb.vel = sd.velocity_bc[8 * b + 7];
+        if (kb.comp < 0 || kb.comp >= s.dim) throw ConfigError("velocity_bc component out of range");
+        s.kinematic.push_back(kb);
+    }
+    for (int b = 0; b < sd.n_fixed; ++b) {
+        MtsKinematic kb;
+        for (int k = 0; k < 3; ++k) {
+            kb.box.lo[k] = sd.fixed[6 * b + k];
+            kb.box.hi[k] = sd.fixed[6 * b + 3 + k];
+        }
+        kb.fix_all = true;
+        s.kinematic.push_back(kb);
+    }
+    for (int b = 0; b < d.n_pd_box; ++b) {
+        MtsBox box;
+        for (int k = 0; k < 3; ++k) {
+            box.lo[k] = d.pd_boxes[6 * b + k];
+            box.hi[k] = d.pd_boxes[6 * b + 3 + k];
+        }
+        s.pd_boxes.push_back(box);
+    }
+    s.overlap_width_factor = d.overlap_width_factor;
+    s.weight_kind = d.weight_kind;
+    s.dt_pd = sd.dt_pd;
+    s.m = sd.m;
+    if (s.m < 1) throw ConfigError("time.m must be >= 1");
+    const double steps = sd.total_time / (s.m * s.dt_pd);
+    if (std::abs(steps - std::round(steps)) > 1e-6)
+        throw ConfigError("time.total_time must be a multiple of m * dt_pd");
+    s.n_macro = int(std::llround(sd.total_time / (s.m * s.dt_pd)));
+    s.fe_gamma = d.gamma_fe;
+    s.fe_beta = d.beta_fe;
+    s.pd_gamma = sd.gamma;
+    s.pd_beta = sd.beta;
+    build_mts_system(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
+    return guard([&] {
+        if (!desc || !desc->scenario || !out) throw ConfigError("null argument");
+        auto h = std::make_unique<pmts_mts>();
+        build_host(*h, *desc);
+        MtsSystem& s = h->s;
+        if (s.pd_beta != 0.0)
+            throw ConfigError("coupled PD substeps are explicit only (beta_pd = 0)");
+        h->device = desc->device;
+        h->nl = int(s.cpl_fe.size());
+        h->m = s.m;
+        h->iface_mode = desc->interface_mode;
+        // interface mode (mts.hpp:111-114); the PD side is explicit
+        h->use_dense = h->iface_mode == 1 || (h->iface_mode == 0 && h->nl <= 400);
+        if (h->device < 0) {  // host-only: the assembled systems (view), no integrator
+            *out = h.release();
+            return;
+        }
+        CKM(cudaSetDevice(h->device));
+        CKM(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->nf = s.fe_n_dof;
+        h->np = s.pd_n_dof;
+        h->nl = int(s.cpl_fe.size());
+        h->m = s.m;
+        h->fe_nm.set(s.fe_gamma, s.fe_beta, s.m * s.dt_pd);
+        h->pd_nm.set(s.pd_gamma, s.pd_beta, s.dt_pd);
+        h->iface_mode = desc->interface_mode;
+        h->enforce_continuity = desc->enforce_continuity != 0;
+        h->track_energy = desc->track_energy != 0;
+        h->fracture = s.s_crit > 0.0;
+        if (h->track_energy && s.pd_gamma != 0.5)
+            throw ConfigError("energy tracking of the PD quadratic term needs gamma_pd = 1/2");
+        h->fe_cg_max = std::max(100, int(40 * std::sqrt(double(h->nf))));
+
+        // ---- PD subdomain handle: compact nodes / elements of the PD-active set ----
+        const int dim = s.dim, nn = dim == 2 ? 4 : 8;
+        const int NPn = int(s.pd_active_nodes.size());
+        std::vector<int> compact(s.nodes.size() / 3, -1);
+        for (int k = 0; k < NPn; ++k) compact[s.pd_active_nodes[k]] = k;
+        std::vector<double> pxyz(3 * (size_t)NPn);
+        for (int k = 0; k < NPn; ++k)
+            for (int c = 0; c < 3; ++c) pxyz[3 * (size_t)k + c] = s.nodes[3 * (size_t)s.pd_active_nodes[k] + c];
+        std::vector<int32_t> pconn;
+        for (int e : s.pd_active)
+            for (int a = 0; a < nn; ++a) pconn.push_back(compact[s.conn[(size_t)e * nn + a]]);
+        pmts_pd_desc pdd{};
+        pdd.dim = dim;
+        pdd.n_nodes = NPn;
+        pdd.n_elems = int(s.pd_active.size());
+        pdd.node_xyz = pxyz.data();
+        pdd.elem_nodes = pconn.data();
+        pdd.mass = s.pd_mass.data();
+        pdd.p_ext = s.pd_p_ext.data();
+        pdd.n_bc = int(s.pd_bc_dofs.size());
+        pdd.bc_dofs = s.pd_bc_dofs.data();
+        pdd.bc_vel = s.pd_bc_vel.data();
+        pdd.delta = s.delta;
+        pdd.micromodulus = PMTS_MICRO_EXP;
+        pdd.c0 = s.c0;
+        pdd.l = s.l;
+        pdd.s_crit = s.s_crit;
+        pdd.gamma = s.pd_gamma;
+        pdd.beta = 0.0;
+        pdd.dt = s.dt_pd;
+        pdd.mode = PMTS_DETERMINISTIC;
+        pdd.device = h->device;
+        pdd.n_notch = desc->scenario->n_notch;
+        pdd.notch_npts = desc->scenario->notch_npts;
+        pdd.notch_pts = desc->scenario->notch_pts;
+        check_pd(pmts_pd_create(&pdd, &h->pd));
+        check_pd(pmts_pd_build_families(h->pd));
+        int64_t npairs = 0;
+        check_pd(pmts_pd_get_pairs(h->pd, nullptr, 0, &npairs));
+        std::vector<int32_t> cp(2 * (size_t)npairs);
+        check_pd(pmts_pd_get_pairs(h->pd, cp.data(), npairs, &npairs));
+        h->npe = int(npairs);
+        h->pairs.resize(cp.size());
+        h->pe_weight.resize(npairs);
+        for (int64_t p = 0; p < npairs; ++p) {
+            const int gi = s.pd_active[cp[2 * p]], gj = s.pd_active[cp[2 * p + 1]];
+            h->pairs[2 * p] = gi;
+            h->pairs[2 * p + 1] = gj;
+            double mid[3];
+            for (int k = 0; k < 3; ++k)
+                mid[k] = 0.5 * (s.centroid[3 * (size_t)gi + k] + s.centroid[3 * (size_t)gj + k]);
+            const double w = 1.0 - mts_alpha_at(s, mid);  // perifem.hpp:320-326
+            if (w < 0.0) throw InternalError("negative PD weight at a bond midpoint");
+            h->pe_weight[p] = w;
+        }
+        pd_internal_pair_weights(h->pd, h->pe_weight.data());
+        h->pdv = pd_internal_dev(h->pd);
+        h->mask_live = h->pdv.mask;
+        h->mask_words = (size_t)h->pdv.W * h->pdv.E;
+        h->mask_sync = h->alloc<uint32_t>(h->mask_words);
+        CKM(cudaMemcpy(h->mask_sync, h->mask_live, sizeof(uint32_t) * h->mask_words,
+                       cudaMemcpyDeviceToDevice));
+
+        // ---- device arrays ----
+        auto flags = [](int n, const std::vector<int32_t>& bc, const std::vector<double>& vel,
+                        std::vector<uint8_t>& cf, std::vector<double>& bv) {
+            cf.assign(n, 0);
+            bv.assign(n, 0.0);
+            for (size_t c = 0; c < bc.size(); ++c) {
+                cf[bc[c]] = 1;
+                bv[bc[c]] = vel[c];
+            }
+        };
+        std::vector<uint8_t> cf;
+        std::vector<double> bv;
+        h->fe_rp = h->upload(s.fe_rowptr);
+        h->fe_ci = h->upload(s.fe_col);
+        h->fe_v = h->upload(s.fe_val);
+        h->fe_M = h->upload(s.fe_mass);
+        h->fe_P = h->upload(s.fe_p_ext);
+        flags(h->nf, s.fe_bc_dofs, s.fe_bc_vel, cf, bv);
+        h->fe_cf = h->upload(cf);
+        h->fe_bcv = h->upload(bv);
+        h->fe_jac = h->upload(jacobi_diag(s, h->fe_nm.bdt2));
+        h->pd_M = h->upload(s.pd_mass);
+        h->pd_P = h->upload(s.pd_p_ext);
+        flags(h->np, s.pd_bc_dofs, s.pd_bc_vel, cf, bv);
+        h->pd_cf = h->upload(cf);
+        h->pd_bcv = h->upload(bv);
+        h->cfe = h->upload(s.cpl_fe);
+        h->cpd = h->upload(s.cpl_pd);
+        const int nmax = std::max({h->nf, h->np, h->nl});
+        h->ufe = h->state(h->nf);
+        h->vfe = h->state(h->nf);
+        h->fe_prev = h->state(h->nf);
+        h->upd = h->state(h->np);
+        h->vpd = h->state(h->np);
+        h->wst = h->state(nmax);
+        h->yst = h->state(nmax);
+        h->rd = h->alloc<double>(nmax);
+        h->rv = h->alloc<double>(nmax);
+        h->ra = h->alloc<double>(nmax);
+        h->kd = h->alloc<double>(nmax);
+        for (double** p : {&h->cg_b, &h->cg_x, &h->cg_r, &h->cg_z, &h->cg_p, &h->cg_ap, &h->cg_kx})
+            *p = h->alloc<double>(nmax);
+        h->part = h->alloc<double>(mtsk::dot_partials());
+        h->scal = h->alloc<double>(16);
+        h->lam_d = h->alloc<double>(h->nl);
+        h->lam_tmp = h->alloc<double>(h->nl);
+        h->gvec = h->alloc<double>(h->nl);
+        h->warm_fe_free = h->alloc<double>(h->nf);
+        h->warm_fe_link = h->alloc<double>(h->nf);
+        h->d_counts = h->alloc<unsigned long long>(h->m + 1);
+        h->counts_cap = h->m + 1;
+        h->lambda_prev.assign(h->nl, 0.0);
+        h->lambda.assign(h->nl, 0.0);
+        // BC velocities on the initial states (mts.hpp:107-108)
+        {
+            std::vector<double> z(h->nf, 0.0);
+            for (size_t c = 0; c < s.fe_bc_dofs.size(); ++c) z[s.fe_bc_dofs[c]] = s.fe_bc_vel[c];
+            h->to_dev(h->ufe.v, z);
+            std::vector<double> zp(h->np, 0.0);
+            for (size_t c = 0; c < s.pd_bc_dofs.size(); ++c) zp[s.pd_bc_dofs[c]] = s.pd_bc_vel[c];
+            h->to_dev(h->upd.v, zp);
+        }
+        // g_p_fe = G_FE P_ext (mts.hpp:110)
+        h->g_p_fe.resize(h->nl);
+        for (int r = 0; r < h->nl; ++r) h->g_p_fe[r] = s.fe_p_ext[s.cpl_fe[r]];
+        CKM(cudaStreamSynchronize(h->stream));
+        h->build_h_fe();
+        if (h->use_dense) h->refresh_dense_interface();
+        CKM(cudaStreamSynchronize(h->stream));
+        *out = h.release();
+    });
+}
+
+int pmts_mts_view_get(const pmts_mts* h, pmts_mts_view* v) {
+    return guard([&] {
+        if (!h || !v) throw ConfigError("null argument");
+        const MtsSystem& s = h->s;
+        *v = pmts_mts_view{};
+        v->dim = s.dim;
+        v->n_nodes = int32_t(s.nodes.size() / 3);
+        v->n_elems = int32_t(s.volume.size());
+        v->fe_n_dof = s.fe_n_dof;
+        v->pd_n_dof = s.pd_n_dof;
+        v->n_lambda = h->nl;
+        v->dense = h->use_dense ? 1 : 0;
+        v->m = s.m;
+        v->n_macro = s.n_macro;
+        v->fe_nnz = int32_t(s.fe_val.size());
+        v->fe_n_bc = int32_t(s.fe_bc_dofs.size());
+        v->pd_n_bc = int32_t(s.pd_bc_dofs.size());
+        v->n_pd_elems = int32_t(s.pd_active.size());
+        v->n_pairs = h->npe;
+        v->dt_pd = s.dt_pd;
+        v->delta = s.delta;
+        v->c0 = s.c0;
+        v->l = s.l;
+        v->char_length = s.cl;
+        v->load_ramp = s.ramp;
+        static thread_local std::vector<int32_t> labels;
+        labels.assign(s.label.begin(), s.label.end());
+        v->labels = labels.data();
+        v->alpha = s.alpha.data();
+        v->fe_node_dof = s.fe_node_dof.data();
+        v->pd_node_dof = s.pd_node_dof.data();
+        v->fe_k_rowptr = s.fe_rowptr.data();
+        v->fe_k_col = s.fe_col.data();
+        v->fe_k_val = s.fe_val.data();
+        v->fe_mass = s.fe_mass.data();
+        v->fe_p_ext = s.fe_p_ext.data();
+        v->pd_mass = s.pd_mass.data();
+        v->pd_p_ext = s.pd_p_ext.data();
+        v->fe_bc_dofs = s.fe_bc_dofs.data();
+        v->fe_bc_vel = s.fe_bc_vel.data();
+        v->pd_bc_dofs = s.pd_bc_dofs.data();
+        v->pd_bc_vel = s.pd_bc_vel.data();
+        v->cpl_fe_dof = s.cpl_fe.data();
+        v->cpl_pd_dof = s.cpl_pd.data();
+        v->pairs = h->pairs.data();
+        v->pe_weight = h->pe_weight.data();
+    });
+}
+
+int pmts_mts_init(pmts_mts* h) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        CKM(cudaSetDevice(h->device));
+        h->initialize_accelerations();
+    });
+}
+
+int pmts_mts_macro_step(pmts_mts* h, int32_t n, pmts_mts_report* reports) {
+    return guard([&] {
+        if (!h || n < 0) throw ConfigError("bad arguments");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        CKM(cudaSetDevice(h->device));
+        for (int i = 0; i < n; ++i) {
+            const pmts_mts_report r = h->macro_step();
+            if (reports) reports[i] = r;
+        }
+    });
+}
+
+int pmts_mts_macro_step_timed(pmts_mts* h, int32_t n, float* ms_out) {
+    return guard([&] {
+        if (!h || n < 0) throw ConfigError("bad arguments");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        CKM(cudaSetDevice(h->device));
+        cudaEvent_t e0, e1;
+        CKM(cudaEventCreate(&e0));
+        CKM(cudaEventCreate(&e1));
+        CKM(cudaStreamSynchronize(h->stream));
+        CKM(cudaEventRecord(e0, h->stream));
+        for (int i = 0; i < n; ++i) h->macro_step();
+        CKM(cudaEventRecord(e1, h->stream));
+        CKM(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CKM(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (ms_out) *ms_out = ms;
+    });
+}
+
+int pmts_mts_get_state(pmts_mts* h, int32_t which, double* u, double* v, double* a) {
+    return guard([&] {
+        if (!h || (which != 0 && which != 1)) throw ConfigError("bad arguments");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        const DState& st = which == 0 ? h->ufe : h->upd;
+        const int n = which == 0 ? h->nf : h->np;
+        if (u) CKM(cudaMemcpyAsync(u, st.u, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+        if (v) CKM(cudaMemcpyAsync(v, st.v, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+        if (a) CKM(cudaMemcpyAsync(a, st.a, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+        CKM(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_mts_get_lambda(pmts_mts* h, double* out) {
+    return guard([&] {
+        if (!h || !out) throw ConfigError("bad arguments");
+        std::copy(h->lambda_prev.begin(), h->lambda_prev.end(), out);
+    });
+}
+
+int pmts_mts_get_intact(pmts_mts* h, uint8_t* out) {
+    return guard([&] {
+        if (!h || !out) throw ConfigError("bad arguments");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        check_pd(pmts_pd_get_intact(h->pd, out, h->npe));
+    });
+}
+
+void pmts_mts_destroy(pmts_mts* h) { delete h; }
+
+}  // extern "C"

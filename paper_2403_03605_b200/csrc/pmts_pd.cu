@@ -1003,6 +1003,55 @@ int pmts_pd_set_pairs(pmts_pd* h, int64_t n_pairs, const int32_t* pairs) {
     });
 }
 
+}  // extern "C"
+
+namespace pmts {
+// ---- internal (libpmts only): the MTS integrator (pmts_mts.cu) drives the
+// deterministic kernels of a PD handle on its own state vectors ----
+DevPD pd_internal_dev(pmts_pd* h) { return h->d; }
+cudaStream_t pd_internal_stream(pmts_pd* h) { return h->stream; }
+// coefficients of the directed entries from per-pair weights (pairs in
+// pmts_pd_get_pairs order): coef = (w_pair * V_i V_j) * c(|xi|), the
+// reference's f = coeff * qp.weight * micromodulus (perifem.hpp:247)
+void pd_internal_pair_weights(pmts_pd* h, const double* w) {
+    require_families(h);
+    const int E = h->E, K = h->d.K;
+    std::vector<int64_t> first(E + 1, 0);
+    for (int e = 0; e < E; ++e) {
+        int64_t c = 0;
+        for (int k = 0; k < K; ++k) {
+            const int p = h->hcol[(size_t)k * E + e];
+            if (p < 0) break;
+            if (p > e) ++c;
+        }
+        first[e + 1] = first[e] + c;
+    }
+    std::vector<double> coef((size_t)K * E, 0.0);
+    for (int e = 0; e < E; ++e)
+        for (int k = 0; k < K; ++k) {
+            const int p = h->hcol[(size_t)k * E + e];
+            if (p < 0) break;
+            const int i = std::min(e, p), j = std::max(e, p);
+            // rank of j among i's upper partners (ascending ELL)
+            int64_t idx = first[i];
+            for (int q = 0; q < K; ++q) {
+                const int pq = h->hcol[(size_t)q * E + i];
+                if (pq < 0 || pq >= j) break;
+                if (pq > i) ++idx;
+            }
+            double xi[3];
+            for (int c = 0; c < 3; ++c) xi[c] = h->cen[3 * (size_t)j + c] - h->cen[3 * (size_t)i + c];
+            const double xin = std::sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+            const double wv = w[idx] * (h->vol[i] * h->vol[j]);
+            coef[(size_t)k * E + e] = wv * micromodulus(h->desc, h->dim, xin);
+        }
+    upload(const_cast<double*>(h->d.coef), coef.data(), coef.size(), h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+}
+}  // namespace pmts
+
+extern "C" {
+
 int pmts_pd_get_pairs(pmts_pd* h, int32_t* out, int64_t cap, int64_t* n_out) {
     return guard([&] {
         require_families(h);

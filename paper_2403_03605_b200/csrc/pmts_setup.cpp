@@ -20,7 +20,7 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 // corner_gradient (mesh.hpp:74-89) == reference_shape gradients (fem.hpp:22-47)
-static void corner_gradient(int dim, const double* xi, int a, double* g) {
+void corner_gradient(int dim, const double* xi, int a, double* g) {
     if (dim == 2) {
         static const double sx[4] = {-1, 1, 1, -1};
         static const double sy[4] = {-1, -1, 1, 1};
@@ -37,7 +37,7 @@ static void corner_gradient(int dim, const double* xi, int a, double* g) {
     }
 }
 
-static double shape_value(int dim, const double* xi, int a) {
+double shape_value(int dim, const double* xi, int a) {
     if (dim == 2) {
         static const double sx[4] = {-1, 1, 1, -1};
         static const double sy[4] = {-1, -1, 1, 1};
@@ -50,7 +50,7 @@ static double shape_value(int dim, const double* xi, int a) {
 }
 
 // jacobian_det (mesh.hpp:91-105) == shape_and_gradients' detJ (fem.hpp:51-79)
-static double jacobian_det(int dim, const int32_t* en, const double* nodes, const double* xi) {
+double jacobian_det(int dim, const int32_t* en, const double* nodes, const double* xi) {
     double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     double g[3];
     const int nn = dim == 2 ? 4 : 8;

@@ -1,0 +1,126 @@
+"""Coupled multi-time-step (Arlequin PD + FE) integrator -- the Python side of
+pmts_mts_* (include/pmts_capi.h), SURVEY.md 8(f) row 1.
+
+Mirrors the reference's coupled run (driver_run.hpp:247-295 ->
+CoupledIntegrator, mts.hpp:79-535): build the scenario, initialize the
+accelerations, then macro steps of one FE step and m PD substeps glued by
+Lagrange multipliers on the overlap.  The integrator runs on the device;
+device=-1 builds only the host-assembled systems (for setup parity checks).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import capi
+from .capi import check, lib, ptr
+from .pd import scenario_desc
+
+WEIGHT_KIND = {"constant": 0, "linear": 1, "cubic": 2}
+INTERFACE = {"auto": 0, "dense": 1, "matrix_free": 2}
+
+
+def _arr(p, ctype, n, shape=None):
+    if n == 0 or not p:
+        return np.zeros(0 if shape is None else shape, dtype=np.dtype(ctype))
+    a = np.ctypeslib.as_array(C.cast(p, C.POINTER(ctype)), shape=(n,)).copy()
+    return a.reshape(shape) if shape else a
+
+
+class MtsSolver:
+    """One coupled run (reference config vocabulary: [region], time.m, gamma_fe,
+    beta_fe, run.interface, ...)."""
+
+    def __init__(self, sc: dict, device: int = 0):
+        self.cfg = sc
+        self._keep = []
+        sd = scenario_desc(sc, self._keep)
+        self._sd = sd
+        reg, tm, run = sc["region"], sc["time"], sc.get("run", {})
+        dim = int(sc["mesh"]["dim"])
+        boxes = []
+        for k, v in sorted(reg.items()):
+            if k.startswith("pd_box"):
+                lo = [v[i] if i < dim else 0.0 for i in range(3)]
+                hi = [v[dim + i] if i < dim else 0.0 for i in range(3)]
+                boxes.append(lo + hi)
+        self._boxes = np.array(boxes or [[0.0] * 6], dtype=np.float64)
+        d = capi.MtsDesc()
+        d.scenario = C.pointer(sd)
+        d.n_pd_box, d.pd_boxes = len(boxes), ptr(self._boxes)
+        d.overlap_width_factor = reg.get("overlap_width_factor", 3.0)
+        d.weight_kind = WEIGHT_KIND[reg.get("weight_kind", "cubic")]
+        d.gamma_fe, d.beta_fe = tm.get("gamma_fe", 0.5), tm.get("beta_fe", 0.25)
+        d.interface_mode = INTERFACE[run.get("interface", "auto")]
+        d.enforce_continuity = 1 if run.get("enforce_continuity", True) else 0
+        d.track_energy = 1 if sc.get("output", {}).get("energy", True) else 0
+        d.device = device
+        h = C.c_void_p()
+        check(lib().pmts_mts_create(C.byref(d), C.byref(h)))
+        self.h = h
+        v = capi.MtsView()
+        check(lib().pmts_mts_view_get(h, C.byref(v)))
+        self.view = v
+        self.dim, self.n_nodes, self.n_elems = v.dim, v.n_nodes, v.n_elems
+        self.fe_n_dof, self.pd_n_dof, self.n_lambda = v.fe_n_dof, v.pd_n_dof, v.n_lambda
+        self.dense, self.m, self.n_macro = bool(v.dense), v.m, v.n_macro
+        self.dt_pd = v.dt_pd
+        self.dt_fe = v.m * v.dt_pd
+        self.n_pairs = v.n_pairs
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().pmts_mts_destroy(h)
+            self.h = None
+
+    # -- assembled systems (host) -------------------------------------------
+    def system(self) -> dict:
+        v, i32, f64 = self.view, C.c_int32, C.c_double
+        nf, npd, E, N = v.fe_n_dof, v.pd_n_dof, v.n_elems, v.n_nodes
+        return {
+            "labels": _arr(v.labels, i32, E), "alpha": _arr(v.alpha, f64, E),
+            "fe_node_dof": _arr(v.fe_node_dof, i32, N), "pd_node_dof": _arr(v.pd_node_dof, i32, N),
+            "fe_k_rowptr": _arr(v.fe_k_rowptr, i32, nf + 1), "fe_k_col": _arr(v.fe_k_col, i32, v.fe_nnz),
+            "fe_k_val": _arr(v.fe_k_val, f64, v.fe_nnz),
+            "fe_mass": _arr(v.fe_mass, f64, nf), "fe_p_ext": _arr(v.fe_p_ext, f64, nf),
+            "pd_mass": _arr(v.pd_mass, f64, npd), "pd_p_ext": _arr(v.pd_p_ext, f64, npd),
+            "fe_bc_dofs": _arr(v.fe_bc_dofs, i32, v.fe_n_bc), "fe_bc_vel": _arr(v.fe_bc_vel, f64, v.fe_n_bc),
+            "pd_bc_dofs": _arr(v.pd_bc_dofs, i32, v.pd_n_bc), "pd_bc_vel": _arr(v.pd_bc_vel, f64, v.pd_n_bc),
+            "fe_dof": _arr(v.cpl_fe_dof, i32, v.n_lambda), "pd_dof": _arr(v.cpl_pd_dof, i32, v.n_lambda),
+            "pairs": _arr(v.pairs, i32, 2 * v.n_pairs, (v.n_pairs, 2)),
+            "pe_weight": _arr(v.pe_weight, f64, v.n_pairs),
+            "delta": v.delta, "c0": v.c0, "l": v.l, "char_length": v.char_length,
+            "load_ramp": v.load_ramp,
+        }
+
+    # -- integration --------------------------------------------------------
+    def initialize(self):
+        check(lib().pmts_mts_init(self.h))
+
+    def macro_step(self, n: int = 1) -> list[dict]:
+        reps = (capi.MtsReport * max(n, 1))()
+        check(lib().pmts_mts_macro_step(self.h, n, reps))
+        return [{f: getattr(r, f) for f, _ in capi.MtsReport._fields_} for r in reps[:n]]
+
+    def macro_step_timed(self, n: int) -> float:
+        ms = C.c_float()
+        check(lib().pmts_mts_macro_step_timed(self.h, n, C.byref(ms)))
+        return ms.value
+
+    def state(self, which: str):
+        n = self.fe_n_dof if which == "fe" else self.pd_n_dof
+        u, v, a = np.empty(n), np.empty(n), np.empty(n)
+        check(lib().pmts_mts_get_state(self.h, 0 if which == "fe" else 1, ptr(u), ptr(v), ptr(a)))
+        return u, v, a
+
+    def lam(self):
+        out = np.empty(self.n_lambda)
+        check(lib().pmts_mts_get_lambda(self.h, ptr(out)))
+        return out
+
+    def intact(self):
+        out = np.empty(self.n_pairs, dtype=np.uint8)
+        check(lib().pmts_mts_get_intact(self.h, ptr(out)))
+        return out

@@ -58,67 +58,76 @@ def _hash_factor(i: int, j: int, seed: int, spread: float) -> float:
     return (1.0 - spread) + (2.0 * spread) * u
 
 
+def scenario_desc(sc: dict, keep: list) -> "capi.ScenarioDesc":
+    """pmts_scenario_desc of a scenario dict (reference config vocabulary); the
+    arrays it points into are appended to keep (the caller holds them)."""
+    m, mat, pdc, load, tm = sc["mesh"], sc["material"], sc["pd"], sc.get("load", {}), sc["time"]
+    dim = int(m["dim"])
+    d = capi.ScenarioDesc()
+    d.dim = dim
+    b = m["bounds"]
+    for k in range(3):
+        d.lo[k] = b[k] if k < dim else 0.0
+        d.hi[k] = b[dim + k] if k < dim else 0.0
+    d.spacing = m["spacing"]
+    d.E, d.nu, d.rho = mat["E"], mat["nu"], mat["rho"]
+    d.formulation = _FORMULATION[mat["formulation"]]
+    d.delta_factor, d.l_factor = pdc["delta_factor"], pdc["l_factor"]
+    d.s_crit = pdc.get("s_crit", 0.0)
+    notches = [v for k, v in sorted(m.items()) if k.startswith("notch") and v]
+    npts, pts = [], []
+    for v in notches:
+        if len(v) == 4:
+            npts.append(2)
+            pts += [v[0], v[1], 0.0, v[2], v[3], 0.0]
+        else:
+            npts.append(len(v) // 3)
+            pts += list(v)
+    notch_npts = np.array(npts or [0], dtype=np.int32)
+    notch_pts = np.array(pts or [0.0], dtype=np.float64)
+    d.n_notch = len(npts)
+    d.notch_npts, d.notch_pts = ptr(notch_npts), ptr(notch_pts)
+    trac, bodyp, vel, fixed = [], [], [], []
+    for k, v in sorted(load.items()):
+        if k.startswith("traction"):
+            bx, val = _box3(v, dim, dim)
+            trac.append(bx + val + [0.0] * (3 - dim))
+        elif k.startswith("body_patch"):
+            bx, val = _box3(v, dim, dim)
+            bodyp.append(bx + val + [0.0] * (3 - dim))
+        elif k.startswith("velocity_bc"):
+            bx, val = _box3(v, dim, 2)
+            vel.append(bx + val)
+        elif k.startswith("fixed"):
+            bx, _ = _box3(v, dim, 0)
+            fixed.append(bx)
+    trac_a = np.array(trac or [[0.0] * 9], dtype=np.float64)
+    bodyp_a = np.array(bodyp or [[0.0] * 9], dtype=np.float64)
+    vel_a = np.array(vel or [[0.0] * 8], dtype=np.float64)
+    fixed_a = np.array(fixed or [[0.0] * 6], dtype=np.float64)
+    d.n_traction, d.traction = len(trac), ptr(trac_a)
+    d.n_body_patch, d.body_patch = len(bodyp), ptr(bodyp_a)
+    bf = load.get("body_force", [0.0] * dim)
+    for k in range(3):
+        d.body_force[k] = bf[k] if k < dim else 0.0
+    d.n_velocity_bc, d.velocity_bc = len(vel), ptr(vel_a)
+    d.n_fixed, d.fixed = len(fixed), ptr(fixed_a)
+    d.dt_pd, d.m, d.total_time = tm["dt_pd"], int(tm.get("m", 1)), tm["total_time"]
+    ramp = load.get("load_ramp", "auto")
+    d.load_ramp = -1.0 if ramp in (None, "auto") else float(ramp)
+    d.gamma, d.beta = tm.get("gamma_pd", 0.5), tm.get("beta_pd", 0.0)
+    keep += [notch_npts, notch_pts, trac_a, bodyp_a, vel_a, fixed_a]
+    return d
+
+
 class Scenario:
     """build_scenario for a generated pure-PD run (host C++ setup in libpmts)."""
 
     def __init__(self, sc: dict):
         self.cfg = sc
-        m, mat, pdc, load, tm = sc["mesh"], sc["material"], sc["pd"], sc.get("load", {}), sc["time"]
-        dim = int(m["dim"])
-        d = capi.ScenarioDesc()
-        d.dim = dim
-        b = m["bounds"]
-        for k in range(3):
-            d.lo[k] = b[k] if k < dim else 0.0
-            d.hi[k] = b[dim + k] if k < dim else 0.0
-        d.spacing = m["spacing"]
-        d.E, d.nu, d.rho = mat["E"], mat["nu"], mat["rho"]
-        d.formulation = _FORMULATION[mat["formulation"]]
-        d.delta_factor, d.l_factor = pdc["delta_factor"], pdc["l_factor"]
-        d.s_crit = pdc.get("s_crit", 0.0)
         self._keep = []
-        notches = [v for k, v in sorted(m.items()) if k.startswith("notch") and v]
-        npts, pts = [], []
-        for v in notches:
-            if len(v) == 4:
-                npts.append(2)
-                pts += [v[0], v[1], 0.0, v[2], v[3], 0.0]
-            else:
-                npts.append(len(v) // 3)
-                pts += list(v)
-        self.notch_npts = np.array(npts or [0], dtype=np.int32)
-        self.notch_pts = np.array(pts or [0.0], dtype=np.float64)
-        d.n_notch = len(npts)
-        d.notch_npts, d.notch_pts = ptr(self.notch_npts), ptr(self.notch_pts)
-        trac, bodyp, vel, fixed = [], [], [], []
-        for k, v in sorted(load.items()):
-            if k.startswith("traction"):
-                bx, val = _box3(v, dim, dim)
-                trac.append(bx + val + [0.0] * (3 - dim))
-            elif k.startswith("body_patch"):
-                bx, val = _box3(v, dim, dim)
-                bodyp.append(bx + val + [0.0] * (3 - dim))
-            elif k.startswith("velocity_bc"):
-                bx, val = _box3(v, dim, 2)
-                vel.append(bx + val)
-            elif k.startswith("fixed"):
-                bx, _ = _box3(v, dim, 0)
-                fixed.append(bx)
-        self.trac = np.array(trac or [[0.0] * 9], dtype=np.float64)
-        self.bodyp = np.array(bodyp or [[0.0] * 9], dtype=np.float64)
-        self.vel = np.array(vel or [[0.0] * 8], dtype=np.float64)
-        self.fixed = np.array(fixed or [[0.0] * 6], dtype=np.float64)
-        d.n_traction, d.traction = len(trac), ptr(self.trac)
-        d.n_body_patch, d.body_patch = len(bodyp), ptr(self.bodyp)
-        bf = load.get("body_force", [0.0] * dim)
-        for k in range(3):
-            d.body_force[k] = bf[k] if k < dim else 0.0
-        d.n_velocity_bc, d.velocity_bc = len(vel), ptr(self.vel)
-        d.n_fixed, d.fixed = len(fixed), ptr(self.fixed)
-        d.dt_pd, d.m, d.total_time = tm["dt_pd"], int(tm.get("m", 1)), tm["total_time"]
-        ramp = load.get("load_ramp", "auto")
-        d.load_ramp = -1.0 if ramp in (None, "auto") else float(ramp)
-        d.gamma, d.beta = tm.get("gamma_pd", 0.5), tm.get("beta_pd", 0.0)
+        d = scenario_desc(sc, self._keep)
+        self.notch_npts, self.notch_pts = self._keep[0], self._keep[1]
         h = C.c_void_p()
         check(lib().pmts_scenario_build(C.byref(d), C.byref(h)))
         self.h = h

@@ -24,6 +24,14 @@ sys.path.insert(0, ROOT)
 from oracle import pyoracle as po  # noqa: E402
 from paper_2403_03605_b200 import configs as cf  # noqa: E402
 
+# coupled MTS fixtures (oracle/_ref/ref_mts_driver): name -> (scenario, macro steps, checkpoints)
+MTS_FIXTURES = {
+    "mts_mini": ("mts_mini", 40, (10,)),
+    "mts_mini_implicit": ("mts_mini_implicit", 20, (5,)),
+    "mts_mini_frac": ("mts_mini_frac", 60, (30,)),
+    "mts_mini_mfree": ("mts_mini_mfree", 20, (5,)),
+}
+
 # name -> (scenario, steps, checkpoints)
 FIXTURES = {
     "mini": ("mini", 80, (40,)),
@@ -60,5 +68,23 @@ def main(names=None):
         print(name, run)
 
 
+def main_mts(names=None):
+    out_dir = os.path.dirname(os.path.abspath(__file__))
+    for name, (scen, steps, ck) in MTS_FIXTURES.items():
+        if names and name not in names:
+            continue
+        text = cf.render_cfg(cf.get(scen))
+        with tempfile.TemporaryDirectory() as tmp:
+            run = po.run_ref_mts(text, tmp, steps=steps, checkpoints=ck)
+            d = po.load_ref_mts_dump(tmp)
+        arrays = {k: v for k, v in d.items() if isinstance(v, np.ndarray)}
+        meta = {k: v for k, v in d.items() if not isinstance(v, np.ndarray)}
+        meta.update(scenario=scen, steps=steps, checkpoints=list(ck), run=run)
+        np.savez_compressed(os.path.join(out_dir, f"{name}.npz"), cfg=np.array(text),
+                            meta=np.array(json.dumps(meta)), **arrays)
+        print(name, run)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:])
+    main([a for a in sys.argv[1:] if not a.startswith("mts")] or None)
+    main_mts([a for a in sys.argv[1:] if a.startswith("mts")] or None)
