@@ -156,6 +156,73 @@ def run_reference_cpu(steps: int, warmup: int, threads: int | None = None) -> di
     return r
 
 
+MTS_METRIC = "coupled MTS coarse steps/s"
+MTS_UNIT = "coarse steps/s"
+
+
+def run_reference_mts(name: str, steps: int, warmup: int, threads: int | None = None) -> dict:
+    """The reference's own coupled loop (ref_mts_driver) on a bounded sample."""
+    from oracle import pyoracle as po
+    from paper_2403_03605_b200 import configs as cf
+
+    threads = threads or os.cpu_count() or 1
+    env = dict(os.environ, PERIMTS_WORKERS=str(threads))
+    if not os.path.exists(po.REF_MTS_DRIVER):
+        return {"unavailable": "oracle/_ref/ref_mts_driver not built"}
+    with tempfile.TemporaryDirectory() as tmp:
+        r = po.run_ref_mts(cf.render_cfg(cf.get(name)), tmp, steps=steps + warmup, dump=False,
+                           extra=["--time", "--warmup", str(warmup)], env=env)
+    r["threads"] = threads
+    return r
+
+
+def bench_mts(steps: int, warmup: int, with_cpu: bool) -> dict:
+    """Coupled MTS on BASELINE cfg2's conforming analog: device
+    time of K macro steps (CUDA events around the whole sequence, host-side
+    orchestration and interface solves inside), plus the same at 0.5 mm next to
+    the reference's own coupled loop on that sample."""
+    from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200.mts import MtsSolver
+
+    out = {"metric": MTS_METRIC, "unit": MTS_UNIT, "higher_is_better": True}
+    res = {}
+    for name in ("cfg2", "cfg2_0p5"):
+        t0 = time.perf_counter()
+        s = MtsSolver(cf.get(name))
+        setup = time.perf_counter() - t0
+        s.initialize()
+        s.macro_step(warmup)
+        ms = s.macro_step_timed(steps)
+        reps = s.macro_step(1)
+        res[name] = {"value": steps / (ms * 1e-3), "ms_per_step": ms / steps, "setup_s": setup,
+                     "n_lambda": s.n_lambda, "fe_dof": s.fe_n_dof, "pd_dof": s.pd_n_dof,
+                     "dense_interface": s.dense,
+                     "interface_iterations": reps[0]["interface_iterations"]}
+        del s
+    out.update(value=res["cfg2"]["value"], ms_per_step=res["cfg2"]["ms_per_step"],
+               steps=steps, warmup=warmup,
+               config={"workload": "cfg2 conforming analog (BASELINE configs[1]; SURVEY App. A): "
+                                   "100x40 mm plate, PD band 100x20 mm, FE elsewhere, both "
+                                   "0.25 mm, 2 mm linear gluing zones, implicit FE (PCG), "
+                                   "explicit PD, m=10, dt_pd 10 ns",
+                       **{k: v for k, v in res["cfg2"].items() if k not in ("value", "ms_per_step")}},
+               at_0p5mm=res["cfg2_0p5"])
+    if with_cpu:
+        r = run_reference_mts("cfg2_0p5", 3, 1)
+        if "unavailable" in r:
+            out["cpu_baseline"] = r
+        else:
+            out["cpu_baseline"] = {
+                "value": r["macro_steps_per_s"], "unit": MTS_UNIT, "cores": r["threads"],
+                "kind": "reference",
+                "sample": "cfg2 analog at 0.5 mm (n_lambda 4020), 3 timed macro steps after 1 "
+                          f"(setup {r['setup_s']:.1f} s); compare with at_0p5mm.value",
+                "ratio_at_0p5mm": res["cfg2_0p5"]["value"] / r["macro_steps_per_s"]}
+    out["reference_published"] = ("SURVEY.md 3.2/6: the reference at 0.25 mm takes 541.5 s of "
+                                  "setup and ~8.8 s per macro step on 8 cores")
+    return out
+
+
 def bench_reference(args):
     rank, _, world = _env_rank()
     if rank != 0:
@@ -345,6 +412,11 @@ def bench_native(args):
             "gpu_launches": K * info["kernels_per_step"],
             "clocks": clk.summary(),
         }
+        if world == 1 and not args.no_mts:
+            try:
+                line["coupled_mts"] = bench_mts(args.mts_steps, 3, not args.no_cpu_baseline)
+            except Exception as ex:  # pragma: no cover - reported, never silent
+                line["coupled_mts"] = {"metric": MTS_METRIC, "error": repr(ex)}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -360,11 +432,37 @@ def main():
     ap.add_argument("--mode", default="fast", choices=["fast", "det"])
     ap.add_argument("--cpu-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mts", action="store_true",
+                    help="skip the coupled MTS (cfg2) section of the line")
+    ap.add_argument("--mts-steps", type=int, default=20)
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the multi-GPU slab path (NCCL clique) even with one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload == "cfg2":  # the coupled MTS metric as its own line
+        rank, _, _ = _env_rank()
+        if rank != 0:
+            return
+        if args.impl == "reference":
+            r = run_reference_mts("cfg2_0p5", args.steps, args.warmup)
+            v = r.get("macro_steps_per_s")
+            line = {"impl": "reference", "metric": MTS_METRIC, "value": v, "unit": MTS_UNIT,
+                    "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": 1e3 / v if v else None, "higher_is_better": True,
+                    "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                    "config": {"workload": "cfg2 analog at 0.5 mm (bounded CPU sample; the "
+                                           "0.25 mm setup alone takes ~9 min on the CPU)"},
+                    "cpu_baseline": {"value": v, "unit": MTS_UNIT, "cores": r.get("threads"),
+                                     "kind": "reference", "sample": "cfg2 analog at 0.5 mm"},
+                    "e2e": {"value": v, "unit": MTS_UNIT, "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+        else:
+            out = bench_mts(args.steps, args.warmup, not args.no_cpu_baseline)
+            line = {"n_gpus": 1, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic", "gpu_launches": None, **out}
+        print(json.dumps(line), flush=True)
+        return
     if args.impl == "reference":
         bench_reference(args)
     else:

@@ -181,6 +181,30 @@ def scenarios() -> dict:
     mm = copy.deepcopy(mi)
     mm["run"]["interface"] = "matrix_free"
     s["mts_mini_mfree"] = mm
+    # BASELINE cfg2, conforming analog: the cfg1 plate and
+    # material, PD band 100 x 20 mm in the middle, FE elsewhere -- both at 0.25 mm
+    # (the reference cannot couple a non-matching 1 mm FE mesh), 2 mm gluing zones
+    # with a linear weight, implicit FE (100 ns is beyond the explicit limit at
+    # 0.25 mm), m = 10, 12 MPa traction on the top / bottom (FE) faces.
+    for tag, dx in (("cfg2", 2.5e-4), ("cfg2_0p5", 5e-4)):
+        dl = 3.015 * dx
+        c2 = {
+            "mesh": {"kind": "generated", "dim": 2, "bounds": [0.0, 0.0, 0.1, 0.04],
+                     "spacing": dx, "notch1": [-0.001, 0.02, 0.05, 0.02]},
+            "material": {"E": _E, "nu": 0.3333333333333333, "rho": _RHO,
+                         "formulation": "plane_stress"},
+            "pd": {"delta_factor": 3.015, "l_factor": 1.0, "s_crit": round(s0_2d(_E, _G0, dl), 7)},
+            "region": {"pd_box1": [0.0, 0.01, 0.1, 0.03],
+                       "overlap_width_factor": round(2e-3 / dx), "weight_kind": "linear"},
+            "load": {"traction1": [-0.01, 0.04 - 1e-7, 0.11, 0.04 + 1e-7, 0.0, 12e6],
+                     "traction2": [-0.01, -1e-7, 0.11, 1e-7, 0.0, -12e6]},
+            "time": {"dt_pd": 1e-8, "m": 10, "total_time": 1e-7 * 200, "gamma_fe": 0.5,
+                     "beta_fe": 0.25, "gamma_pd": 0.5, "beta_pd": 0.0},
+            "run": {"mode": "coupled_mts", "interface": "auto"},
+            "output": {"interval": 0.0},
+            "ext": {},
+        }
+        s[tag] = c2
     return s
 
 
