@@ -192,6 +192,18 @@ __global__ void k_sum_partials(int nb, const double* part, double* out) {
 // CG scalars on the device: alpha = rz / pap, beta = rz_new / rz
 __global__ void k_ratio(const double* num, const double* den, double* out) { *out = *num / *den; }
 
+// y = A x, CSR, one warp per row (long rows: the interface's H_FE)
+__global__ void k_csr_warp(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ x,
+                           double* __restrict__ y) {
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= n) return;
+    double s = 0.0;
+    for (int p = rp[row] + lane; p < rp[row + 1]; p += 32) s += v[p] * x[ci[p]];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) y[row] = s;
+}
+
 __global__ void k_dense_matvec(int n, const double* A, const double* x, double* y) {
     // y = A x for a row-major n x n matrix (the interface's H_FE), one warp per row
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -295,6 +307,11 @@ void dot(int n, const double* x, const double* y, double* part, double* out, cud
 void ratio(const double* num, const double* den, double* out, cudaStream_t s) {
     k_ratio<<<1, 1, 0, s>>>(num, den, out);
     check("ratio");
+}
+void csr_spmv_warp(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                   double* y, cudaStream_t s) {
+    k_csr_warp<<<(n * 32 + kT - 1) / kT, kT, 0, s>>>(n, rp, ci, v, x, y);
+    check("csr_warp");
 }
 void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream_t s) {
     k_dense_matvec<<<(n * 32 + kT - 1) / kT, kT, 0, s>>>(n, A, x, y);

@@ -41,6 +41,8 @@ int dot_partials();
 void dot(int n, const double* x, const double* y, double* part, double* out, cudaStream_t s);
 void ratio(const double* num, const double* den, double* out, cudaStream_t s);
 void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream_t s);
+void csr_spmv_warp(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                   double* y, cudaStream_t s);
 
 }  // namespace mtsk
 }  // namespace pmts

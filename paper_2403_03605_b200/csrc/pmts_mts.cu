@@ -171,7 +171,10 @@ struct pmts_mts {
            *cg_ap = nullptr, *cg_kx = nullptr;                             // size max(nf, nl)
     double *part = nullptr, *scal = nullptr;                               // reductions
     double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
-    double* hfe_d = nullptr;                                               // nl x nl
+    int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
+    double* hfe_v = nullptr;
+    int64_t hfe_nnz = 0;
+    double *sv_d = nullptr, *gp_free_d = nullptr, *gp_link_d = nullptr;    // m or m+1 rows of nl
     double *warm_fe_free = nullptr, *warm_fe_link = nullptr;
     bool warm_free_ok = false, warm_link_ok = false;
     // host interface state
@@ -185,6 +188,9 @@ struct pmts_mts {
 
     ~pmts_mts() {
         if (stream) cudaStreamSynchronize(stream);
+        for (auto& g : cg_graph)
+            if (g) cudaGraphExecDestroy(g);
+        if (h_pin) cudaFreeHost(h_pin);
         for (void* p : owned) cudaFree(p);
         if (pd) pmts_pd_destroy(pd);
         if (stream) cudaStreamDestroy(stream);
@@ -255,7 +261,8 @@ struct pmts_mts {
 
     // reference cg_solve (linalg.hpp:243-296) on the device; A applied by op(x, y)
     template <class Op>
-    int cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac) {
+    int cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac,
+           int graph_id) {
         double* r = cg_r;
         double* z = cg_z;
         double* p = cg_p;
@@ -280,17 +287,11 @@ struct pmts_mts {
         mtsk::dot(n, r, z, part, s_rz, stream);
         mtsk::dot(n, r, r, part, s_rr, stream);
         double rnorm = std::sqrt(scalar(s_rr));
-        int it = 0;
-        while (rnorm / bnorm > tol) {
-            if (it >= max_iter)
-                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
-                                  " iterations, residual " + std::to_string(rnorm / bnorm));
+        // the iteration body (same arithmetic as the reference's loop) as one CUDA
+        // graph over fixed buffers: one launch and one 16-byte readback per iteration
+        auto body = [&] {
             op(p, ap);
             mtsk::dot(n, p, ap, part, s_pap, stream);
-            const double pap = scalar(s_pap);
-            if (pap <= 0.0)
-                throw SolverError("cg: operator not positive definite (p'Ap = " +
-                                  std::to_string(pap) + ")");
             mtsk::ratio(s_rz, s_pap, s_alpha, stream);
             mtsk::cg_update(n, s_alpha, p, ap, x, r, stream);
             mtsk::precond(n, r, jac, z, stream);
@@ -299,11 +300,41 @@ struct pmts_mts {
             mtsk::xpby(n, z, s_beta, p, stream);
             CKM(cudaMemcpyAsync(s_rz, s_rzn, sizeof(double), cudaMemcpyDeviceToDevice, stream));
             mtsk::dot(n, r, r, part, s_rr, stream);
-            rnorm = std::sqrt(scalar(s_rr));
+        };
+        cudaGraphExec_t& ge = cg_graph[graph_id];
+        if (ge && cg_graph_x[graph_id] != x) {  // x is baked into the graph
+            cudaGraphExecDestroy(ge);
+            ge = nullptr;
+        }
+        if (!ge) {
+            cudaGraph_t g;
+            CKM(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            body();
+            CKM(cudaStreamEndCapture(stream, &g));
+            CKM(cudaGraphInstantiate(&ge, g, 0));
+            cudaGraphDestroy(g);
+            cg_graph_x[graph_id] = x;
+        }
+        int it = 0;
+        while (rnorm / bnorm > tol) {
+            if (it >= max_iter)
+                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
+                                  " iterations, residual " + std::to_string(rnorm / bnorm));
+            CKM(cudaGraphLaunch(ge, stream));
+            CKM(cudaMemcpyAsync(h_pin, scal + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+            CKM(cudaStreamSynchronize(stream));
+            const double pap = h_pin[1];
+            if (pap <= 0.0)
+                throw SolverError("cg: operator not positive definite (p'Ap = " +
+                                  std::to_string(pap) + ")");
+            rnorm = std::sqrt(h_pin[0]);
             ++it;
         }
         return it;
     }
+    cudaGraphExec_t cg_graph[2] = {nullptr, nullptr};
+    const double* cg_graph_x[2] = {nullptr, nullptr};
+    double* h_pin = nullptr;  // pinned: (rr, pap) of the last iteration
     void sub(int n, const double* b, const double* ap, double* r) {
         // r = b - ap, elementwise, exactly as the reference's r[i] = b[i] - ap[i]
         mtsk::rhs(n, b, 1.0, ap, zero_flags(n), r, stream);
@@ -342,7 +373,7 @@ struct pmts_mts {
                fe_K(x, cg_kx);
                mtsk::apply_a(nf, x, cg_kx, fe_M, fe_cf, bdt2, y, stream);
            },
-           cg_b, cg_x, cg_tol, fe_cg_max, fe_jac);
+           cg_b, cg_x, cg_tol, fe_cg_max, fe_jac, 0);
         mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
         if (warm) {
             CKM(cudaMemcpyAsync(warm, cg_x, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
@@ -405,8 +436,25 @@ struct pmts_mts {
             for (int r = 0; r < nl; ++r) h_fe[(size_t)r * nl + k] = -g[r];
         }
         if (!use_dense || iface_mode == 2) {
-            hfe_d = alloc<double>((size_t)nl * nl);
-            to_dev(hfe_d, h_fe);
+            // H_FE is exactly sparse: each unit column is a CG solve from one overlap
+            // dof, whose support grows by one stiffness neighbourhood per iteration, and
+            // disconnected FE parts never couple -- keep the nonzeros (lossless) in CSR
+            std::vector<int32_t> rp(nl + 1, 0), ci;
+            std::vector<double> vv;
+            for (int r = 0; r < nl; ++r) {
+                for (int k = 0; k < nl; ++k) {
+                    const double x = h_fe[(size_t)r * nl + k];
+                    if (x != 0.0) {
+                        ci.push_back(k);
+                        vv.push_back(x);
+                    }
+                }
+                rp[r + 1] = int32_t(ci.size());
+            }
+            hfe_nnz = int64_t(vv.size());
+            hfe_rp = upload(rp);
+            hfe_ci = upload(ci);
+            hfe_v = upload(vv);
         }
     }
     void refresh_dense_interface() {
@@ -477,11 +525,11 @@ struct pmts_mts {
             const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
             *iterations = cg(nl,
                              [&](const double* in, double* out) {
-                                 mtsk::dense_matvec(nl, hfe_d, in, out, stream);
+                                 mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
                                  apply_h_pd(in, iface_tmp);
                                  mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
                              },
-                             b, lam_d, interface_cg_tol, max_iter, nullptr);
+                             b, lam_d, interface_cg_tol, max_iter, nullptr, 1);
         } catch (const SolverError&) {
             use_dense = true;
             h_valid = false;
@@ -553,15 +601,23 @@ pmts_mts_report pmts_mts::macro_step() {
     const double fe_seconds = now_s() - tk0;
     // free PD solve, m substeps with the known multiplier load S_j (mts.hpp:152-180)
     const double tp0 = now_s();
-    gp_free.assign(m + 1, std::vector<double>(nl, 0.0));
-    gp_free[0] = gather_pd(upd.v);
+    // the substep multiplier loads S_j are known up front: one upload
+    {
+        std::vector<double> sv((size_t)m * nl);
+        for (int j = 1; j <= m; ++j) {
+            const std::vector<double> sj = s_vector(j);
+            std::copy(sj.begin(), sj.end(), sv.begin() + (size_t)(j - 1) * nl);
+        }
+        to_dev(sv_d, sv);
+    }
+    mtsk::gather(nl, cpd, upd.v, gp_free_d, stream);
     copy(vpd, upd, np);
     for (int j = 1; j <= m; ++j) {
         mtsk::predict(np, vpd.u, vpd.v, vpd.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
         mtsk::scale(np, pd_P, load_scale(t + j * s.dt_pd), ra, stream);
-        add_gt(cpd, s_vector(j), ra);
+        mtsk::scatter_add(nl, cpd, sv_d + (size_t)(j - 1) * nl, ra, stream);
         pd_solve(ra, 1.0, rv, rd, mask_live, fracture, j, false, vpd);
-        gp_free[j] = gather_pd(vpd.v);
+        mtsk::gather(nl, cpd, vpd.v, gp_free_d + (size_t)j * nl, stream);
     }
     CKM(cudaStreamSynchronize(stream));
     const double pd_seconds = now_s() - tp0;
@@ -581,18 +637,30 @@ pmts_mts_report pmts_mts::macro_step() {
     }
     {  // PD correction: m substeps under the ramped multiplier load, on k_sync
         zero(wst, np);
-        gp_link.assign(m + 1, std::vector<double>(nl, 0.0));
+        to_dev(lam_d, lambda);
+        zero_vec(gp_link_d, nl);
         for (int j = 1; j <= m; ++j) {
             mtsk::predict(np, wst.u, wst.v, wst.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
             zero_vec(ra, np);
-            add_gt(cpd, scaled(lambda, double(j) / m), ra);
+            mtsk::scale(nl, lam_d, double(j) / m, lam_tmp, stream);  // scaled(lambda, j/m)
+            mtsk::scatter_add(nl, cpd, lam_tmp, ra, stream);
             pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, wst);
-            gp_link[j] = gather_pd(wst.v);
+            mtsk::gather(nl, cpd, wst.v, gp_link_d + (size_t)j * nl, stream);
         }
         mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
     }
     CKM(cudaStreamSynchronize(stream));
     rep.t_lambda = now_s() - tl0;
+    if (track_energy) {
+        const std::vector<double> gf = to_host(gp_free_d, (m + 1) * nl);
+        const std::vector<double> gl = to_host(gp_link_d, (m + 1) * nl);
+        gp_free.assign(m + 1, std::vector<double>(nl));
+        gp_link.assign(m + 1, std::vector<double>(nl));
+        for (int j = 0; j <= m; ++j) {
+            std::copy(gf.begin() + (size_t)j * nl, gf.begin() + (size_t)(j + 1) * nl, gp_free[j].begin());
+            std::copy(gl.begin() + (size_t)j * nl, gl.begin() + (size_t)(j + 1) * nl, gp_link[j].begin());
+        }
+    }
     // bonds broken in the free substeps, then the post-recombination audit
     const double tu0 = now_s();
     if (fracture) {
@@ -906,10 +974,14 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         for (double** p : {&h->cg_b, &h->cg_x, &h->cg_r, &h->cg_z, &h->cg_p, &h->cg_ap, &h->cg_kx})
             *p = h->alloc<double>(nmax);
         h->part = h->alloc<double>(mtsk::dot_partials());
+        CKM(cudaMallocHost(&h->h_pin, 4 * sizeof(double)));
         h->scal = h->alloc<double>(16);
         h->lam_d = h->alloc<double>(h->nl);
         h->lam_tmp = h->alloc<double>(h->nl);
         h->gvec = h->alloc<double>(h->nl);
+        h->sv_d = h->alloc<double>((size_t)h->m * h->nl);
+        h->gp_free_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
+        h->gp_link_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
         h->warm_fe_free = h->alloc<double>(h->nf);
         h->warm_fe_link = h->alloc<double>(h->nf);
         h->d_counts = h->alloc<unsigned long long>(h->m + 1);
