@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "pd_common.cuh"
 #include "pd_mts.cuh"
 
 namespace pmts {
@@ -215,7 +216,243 @@ __global__ void k_dense_matvec(int n, const double* A, const double* x, double* 
     if (lane == 0) y[warp] = s;
 }
 
+// K^PD x for the MTS substeps, one warp per element, lanes over the family
+// (32 entries per round): the deterministic kernel's per-entry arithmetic
+// (pd_det.cu k_det_bond: eta from node displacements in the (i<j) orientation,
+// exact stretch, inclusive test) with a warp-tree sum instead of the ascending
+// serial sum -- small PD subdomains are latency-bound at one thread per element.
+template <int DIM>
+__global__ void __launch_bounds__(kT) k_pd_force_warp(DevPD d, const double* __restrict__ x,
+                                                      uint32_t* __restrict__ mask, int do_break,
+                                                      unsigned long long* cnt) {
+    constexpr int NN = DIM == 2 ? 4 : 8;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (e >= d.E) return;
+    const int E = d.E;
+    double qe[NN][DIM];
+    for (int a = 0; a < NN; ++a) {
+        const int node = d.conn[a * E + e];
+        for (int c = 0; c < DIM; ++c) qe[a][c] = d.Nsh * x[(size_t)node * DIM + c];
+    }
+    double Se[DIM];
+    for (int c = 0; c < DIM; ++c) {
+        double sacc = 0.0;
+        for (int a = 0; a < NN; ++a) sacc = sacc + qe[a][c];
+        Se[c] = sacc;
+    }
+    const double ce[3] = {d.cen[e], d.cen[E + e], d.cen[2 * E + e]};
+    double G[DIM];
+    for (int c = 0; c < DIM; ++c) G[c] = 0.0;
+    unsigned nb = 0;
+    for (int k0 = 0; k0 < d.K; k0 += 32) {
+        const int k = k0 + lane;
+        const int p = k < d.K ? d.col[(size_t)k * E + e] : -1;
+        const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
+        const bool on = p >= 0 && ((word >> lane) & 1u);
+        bool brk = false;
+        if (on) {
+            double eta[DIM], xi[3];
+            const double cp[3] = {d.cen[p], d.cen[E + p], d.cen[2 * E + p]};
+            double qp[NN][DIM];
+            for (int a = 0; a < NN; ++a) {
+                const int node = d.conn[a * E + p];
+                for (int c = 0; c < DIM; ++c) qp[a][c] = d.Nsh * x[(size_t)node * DIM + c];
+            }
+            if (e < p) {
+                for (int c = 0; c < DIM; ++c) {
+                    double sacc = 0.0;
+                    for (int a = 0; a < NN; ++a) sacc = sacc + qp[a][c];
+                    for (int a = 0; a < NN; ++a) sacc = sacc - qe[a][c];
+                    eta[c] = sacc;
+                }
+                for (int c = 0; c < 3; ++c) xi[c] = cp[c] - ce[c];
+            } else {
+                for (int c = 0; c < DIM; ++c) {
+                    double sacc = Se[c];
+                    for (int a = 0; a < NN; ++a) sacc = sacc - qp[a][c];
+                    eta[c] = sacc;
+                }
+                for (int c = 0; c < 3; ++c) xi[c] = ce[c] - cp[c];
+            }
+            double dot = xi[0] * eta[0] + xi[1] * eta[1];
+            if constexpr (DIM == 3) dot = dot + xi[2] * eta[2];
+            const double t = d.coef[(size_t)k * E + e] * dot;
+            if (e > p) {
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] + t * xi[c];
+            } else {
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+            }
+            if (do_break) {
+                const double xin = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+                double len2 = 0.0;
+                for (int c = 0; c < DIM; ++c) {
+                    const double v = xi[c] + eta[c];
+                    len2 = len2 + v * v;
+                }
+                const double len = sqrt(len2);
+                const double sv = len <= 0.0 ? -1.0 : (len - xin) / xin;
+                brk = sv >= d.s_crit;
+                if (brk && e < p) ++nb;
+            }
+        }
+        if (do_break) {
+            const unsigned bal = __ballot_sync(0xffffffffu, brk);
+            if (lane == 0 && bal) mask[(size_t)(k0 >> 5) * E + e] = word & ~bal;
+        }
+    }
+    for (int c = 0; c < DIM; ++c)
+        for (int o = 16; o > 0; o >>= 1) G[c] += __shfl_down_sync(0xffffffffu, G[c], o);
+    if (lane == 0)
+        for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
+    if (do_break) {
+        for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+        if (lane == 0 && nb) atomicAdd(cnt, (unsigned long long)nb);
+    }
+}
+
+// Linear K^PD x for the homogeneous substeps (unit responses, link and
+// interface solves -- no bond test): eta = ubar_p - ubar_e from per-element
+// centroid displacements, G_e = -sum coef (xi.eta) xi with xi = c_p - c_e.
+// The same operator as the deterministic form (sum_a N u_a = ubar exactly in
+// real arithmetic), one partner load of 16 bytes instead of 2^dim nodes.
+template <int DIM>
+__global__ void k_pd_ubar(DevPD d, const double* __restrict__ x, double* __restrict__ ub) {
+    constexpr int NN = DIM == 2 ? 4 : 8;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= d.E) return;
+    double s[DIM];
+    for (int c = 0; c < DIM; ++c) s[c] = 0.0;
+    for (int a = 0; a < NN; ++a) {
+        const int node = d.conn[a * d.E + e];
+        for (int c = 0; c < DIM; ++c) s[c] = s[c] + d.Nsh * x[(size_t)node * DIM + c];
+    }
+    for (int c = 0; c < DIM; ++c) ub[(size_t)e * DIM + c] = s[c];
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) k_pd_force_lin(DevPD d, const double* __restrict__ ub,
+                                                     const uint32_t* __restrict__ mask) {
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (e >= d.E) return;
+    const int E = d.E;
+    double ue[DIM], G[DIM];
+    for (int c = 0; c < DIM; ++c) {
+        ue[c] = ub[(size_t)e * DIM + c];
+        G[c] = 0.0;
+    }
+    const double ce[3] = {d.cen[e], d.cen[E + e], d.cen[2 * E + e]};
+    for (int k0 = 0; k0 < d.K; k0 += 32) {
+        const int k = k0 + lane;
+        const int p = k < d.K ? d.col[(size_t)k * E + e] : -1;
+        const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
+        if (p >= 0 && ((word >> lane) & 1u)) {
+            double xi[DIM], dot = 0.0;
+            for (int c = 0; c < DIM; ++c) {
+                xi[c] = d.cen[(size_t)c * E + p] - ce[c];
+                dot = dot + xi[c] * (ub[(size_t)p * DIM + c] - ue[c]);
+            }
+            const double t = d.coef[(size_t)k * E + e] * dot;
+            for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+        }
+    }
+    for (int c = 0; c < DIM; ++c)
+        for (int o = 16; o > 0; o >>= 1) G[c] += __shfl_down_sync(0xffffffffu, G[c], o);
+    if (lane == 0)
+        for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
+}
+
+// (K x)_n from the incident elements' G, fused with the explicit block solve
+// of the node's dofs (newmark.hpp:122-131, 150-158)
+template <int DIM>
+__global__ void k_pd_node_explicit(DevPD d, const double* ra, double ra_scale, const double* M,
+                                   const uint8_t* cf, const double* rv, const double* rd,
+                                   double gdt, double bdt2, const double* bcvel, int homog,
+                                   double* u, double* v, double* a) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= d.N) return;
+    double Ku[DIM];
+    for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
+    for (int q = 0; q < d.NE; ++q) {
+        const int e = d.ne[(size_t)q * d.N + n];
+        if (e < 0) break;
+        for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
+    }
+    for (int c = 0; c < DIM; ++c) {
+        const size_t i = (size_t)n * DIM + c;
+        const bool cc = cf[i] != 0;
+        const double rai = ra ? ra[i] * ra_scale : 0.0;
+        const double b = cc ? 0.0 : rai - Ku[c];
+        const double acc = cc ? 0.0 : b / M[i];
+        double vel = rv[i] + gdt * acc;
+        const double dis = rd[i] + bdt2 * acc;
+        if (cc) vel = homog ? 0.0 : bcvel[i];
+        a[i] = acc;
+        v[i] = vel;
+        u[i] = dis;
+    }
+}
+
+// predictor + load vector of one homogeneous substep: ra = 0, then the
+// multiplier rows (one launch: rows are distinct dofs, and the zeroing of a
+// row's dof is ordered before its add within the thread that owns it)
+__global__ void k_pd_pre(int n, const double* u, const double* v, const double* a, double* rd,
+                         double* rv, double* ra, double dt, double cpv, double cpd) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rv[i] = v[i] + cpv * a[i];
+    rd[i] = u[i] + dt * v[i] + cpd * a[i];
+    ra[i] = 0.0;
+}
+
+__global__ void k_scatter_scaled(int n, const int32_t* idx, const double* w, double f, double* dst) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) dst[idx[r]] += w[r] * f;
+}
+
 }  // namespace
+
+void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
+                   unsigned long long* cnt, cudaStream_t s) {
+    const int b = (int)(((long long)d.E * 32 + kT - 1) / kT);
+    if (d.dim == 2) k_pd_force_warp<2><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
+    else k_pd_force_warp<3><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
+    check("pd_force_warp");
+}
+void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double* ubar,
+                  cudaStream_t s) {
+    if (d.dim == 2) {
+        k_pd_ubar<2><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+        k_pd_force_lin<2><<<(int)(((long long)d.E * 32 + kT - 1) / kT), kT, 0, s>>>(d, ubar, mask);
+    } else {
+        k_pd_ubar<3><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+        k_pd_force_lin<3><<<(int)(((long long)d.E * 32 + kT - 1) / kT), kT, 0, s>>>(d, ubar, mask);
+    }
+    check("pd_force_lin");
+}
+void pd_node_explicit(const DevPD& d, const double* ra, double ra_scale, const double* M,
+                      const uint8_t* cf, const double* rv, const double* rd, double gdt,
+                      double bdt2, const double* bcvel, int homog, double* u, double* v,
+                      double* a, cudaStream_t s) {
+    const int b = (d.N + kT - 1) / kT;
+    if (d.dim == 2)
+        k_pd_node_explicit<2><<<b, kT, 0, s>>>(d, ra, ra_scale, M, cf, rv, rd, gdt, bdt2, bcvel,
+                                               homog, u, v, a);
+    else
+        k_pd_node_explicit<3><<<b, kT, 0, s>>>(d, ra, ra_scale, M, cf, rv, rd, gdt, bdt2, bcvel,
+                                               homog, u, v, a);
+    check("pd_node_explicit");
+}
+void pd_pre(int n, const double* u, const double* v, const double* a, double* rd, double* rv,
+            double* ra, double dt, double cpv, double cpd, cudaStream_t s) {
+    k_pd_pre<<<blocks(n), kT, 0, s>>>(n, u, v, a, rd, rv, ra, dt, cpv, cpd);
+    check("pd_pre");
+}
+void scatter_scaled(int n, const int32_t* idx, const double* w, double f, double* dst,
+                    cudaStream_t s) {
+    if (n <= 0) return;
+    k_scatter_scaled<<<blocks(n), kT, 0, s>>>(n, idx, w, f, dst);
+    check("scatter_scaled");
+}
 
 void csr_spmv(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
               double* y, cudaStream_t s) {

@@ -5,7 +5,25 @@
 #include <cuda_runtime.h>
 
 namespace pmts {
+struct DevPD;
 namespace mtsk {
+
+// PD substep kernels of the integrator: warp-per-element K^PD x (optional bond
+// test into mask / cnt), node sum fused with the explicit solve, the predictor
+// fused with zeroing the load, and scaled multiplier rows.
+void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
+                   unsigned long long* cnt, cudaStream_t s);
+// linear (no bond test) K^PD x via centroid displacements; ubar: E x dim scratch
+void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double* ubar,
+                  cudaStream_t s);
+void pd_node_explicit(const DevPD& d, const double* ra, double ra_scale, const double* M,
+                      const uint8_t* cf, const double* rv, const double* rd, double gdt,
+                      double bdt2, const double* bcvel, int homog, double* u, double* v,
+                      double* a, cudaStream_t s);
+void pd_pre(int n, const double* u, const double* v, const double* a, double* rd, double* rv,
+            double* ra, double dt, double cpv, double cpd, cudaStream_t s);
+void scatter_scaled(int n, const int32_t* idx, const double* w, double f, double* dst,
+                    cudaStream_t s);
 
 void csr_spmv(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
               double* y, cudaStream_t s);

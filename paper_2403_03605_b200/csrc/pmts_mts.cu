@@ -175,6 +175,7 @@ struct pmts_mts {
     double* hfe_v = nullptr;
     int64_t hfe_nnz = 0;
     double *sv_d = nullptr, *gp_free_d = nullptr, *gp_link_d = nullptr;    // m or m+1 rows of nl
+    double* pd_ubar = nullptr;                                             // E_pd x dim
     double *warm_fe_free = nullptr, *warm_fe_link = nullptr;
     bool warm_free_ok = false, warm_link_ok = false;
     // host interface state
@@ -251,12 +252,8 @@ struct pmts_mts {
     // K^PD x with the given bond mask; do_break: the inclusive stretch test on x
     // updates that mask (count into slot)
     void pd_K(const double* x, double* y, uint32_t* mask, bool do_break, int slot) {
-        DevPD d = pdv;
-        d.mask = mask;
-        d.log = nullptr;
-        d.broken_count = d_counts;
-        launch_det_bond(d, x, slot, do_break ? 1 : 0, 0, stream);
-        launch_node_force(d, y, stream);
+        mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream);
+        launch_node_force(pdv, y, stream);
     }
 
     // reference cg_solve (linalg.hpp:243-296) on the device; A applied by op(x, y)
@@ -385,9 +382,12 @@ struct pmts_mts {
     // explicit PD solve (beta_pd = 0); the bond test on rd when do_break
     void pd_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
                   uint32_t* mask, bool do_break, int slot, bool homog, const DState& out) {
-        pd_K(rdp, kd, mask, do_break, slot);
-        mtsk::explicit_solve(np, ra, ra_scale, kd, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
-                             pd_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
+        if (do_break || !homog)  // free substeps: the deterministic per-entry arithmetic
+            mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream);
+        else  // homogeneous linear substeps (unit, link, interface): centroid form
+            mtsk::pd_force_lin(pdv, rdp, mask, pd_ubar, stream);
+        mtsk::pd_node_explicit(pdv, ra, ra_scale, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
+                               pd_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
     }
 
     // ---- coupling (coupling.hpp:46-68) ----
@@ -471,10 +471,8 @@ struct pmts_mts {
     void apply_h_pd(const double* w_dev, double* out_dev) {
         zero(yst, np);
         for (int j = 1; j <= m; ++j) {
-            mtsk::predict(np, yst.u, yst.v, yst.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
-            zero_vec(ra, np);
-            mtsk::scale(nl, w_dev, double(j) / m, lam_tmp, stream);
-            mtsk::scatter_add(nl, cpd, lam_tmp, ra, stream);
+            mtsk::pd_pre(np, yst.u, yst.v, yst.a, rd, rv, ra, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+            mtsk::scatter_scaled(nl, cpd, w_dev, double(j) / m, ra, stream);  // scaled(w, j/m)
             pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, yst);
         }
         mtsk::gather(nl, cpd, yst.v, out_dev, stream);
@@ -640,10 +638,8 @@ pmts_mts_report pmts_mts::macro_step() {
         to_dev(lam_d, lambda);
         zero_vec(gp_link_d, nl);
         for (int j = 1; j <= m; ++j) {
-            mtsk::predict(np, wst.u, wst.v, wst.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
-            zero_vec(ra, np);
-            mtsk::scale(nl, lam_d, double(j) / m, lam_tmp, stream);  // scaled(lambda, j/m)
-            mtsk::scatter_add(nl, cpd, lam_tmp, ra, stream);
+            mtsk::pd_pre(np, wst.u, wst.v, wst.a, rd, rv, ra, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+            mtsk::scatter_scaled(nl, cpd, lam_d, double(j) / m, ra, stream);  // scaled(lambda, j/m)
             pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, wst);
             mtsk::gather(nl, cpd, wst.v, gp_link_d + (size_t)j * nl, stream);
         }
@@ -980,6 +976,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->lam_tmp = h->alloc<double>(h->nl);
         h->gvec = h->alloc<double>(h->nl);
         h->sv_d = h->alloc<double>((size_t)h->m * h->nl);
+        h->pd_ubar = h->alloc<double>((size_t)h->pdv.E * dim);
         h->gp_free_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
         h->gp_link_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
         h->warm_fe_free = h->alloc<double>(h->nf);
