@@ -392,6 +392,45 @@ __global__ void k_pd_node_explicit(DevPD d, const double* ra, double ra_scale, c
     }
 }
 
+// node phase of one homogeneous linear substep, fused: (K x)_n from the
+// incident G (none on substep 1, which starts from rest), the multiplier load
+// rhs.a = G_PD^T (w j/m) read through the dof's coupling row, the explicit
+// solve, the predictor of the next substep (in place), and the gather of the
+// coupling-row velocities into out (when non-null)
+template <int DIM>
+__global__ void k_pd_node_lin(DevPD d, int with_force, const double* w, const int32_t* row_of,
+                              double f, const double* M, const uint8_t* cf, double gdt, double bdt2,
+                              double dt, double cpv, double cpd, double* u, double* v, double* a,
+                              double* rd, double* rv, double* out) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= d.N) return;
+    double Ku[DIM];
+    for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
+    if (with_force)
+        for (int q = 0; q < d.NE; ++q) {
+            const int e = d.ne[(size_t)q * d.N + n];
+            if (e < 0) break;
+            for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
+        }
+    for (int c = 0; c < DIM; ++c) {
+        const size_t i = (size_t)n * DIM + c;
+        const bool cc = cf[i] != 0;
+        const int r = row_of[i];
+        const double rai = r >= 0 ? 0.0 + w[r] * f : 0.0;  // assign(0) + scaled(w, j/m)
+        const double b = cc ? 0.0 : rai - Ku[c];
+        const double acc = cc ? 0.0 : b / M[i];
+        double vel = rv[i] + gdt * acc;
+        const double dis = rd[i] + bdt2 * acc;
+        if (cc) vel = 0.0;  // homogeneous
+        a[i] = acc;
+        v[i] = vel;
+        u[i] = dis;
+        rv[i] = vel + cpv * acc;
+        rd[i] = dis + dt * vel + cpd * acc;
+        if (out && r >= 0) out[r] = vel;
+    }
+}
+
 // predictor + load vector of one homogeneous substep: ra = 0, then the
 // multiplier rows (one launch: rows are distinct dofs, and the zeroing of a
 // row's dof is ordered before its add within the thread that owns it)
@@ -441,6 +480,19 @@ void pd_node_explicit(const DevPD& d, const double* ra, double ra_scale, const d
         k_pd_node_explicit<3><<<b, kT, 0, s>>>(d, ra, ra_scale, M, cf, rv, rd, gdt, bdt2, bcvel,
                                                homog, u, v, a);
     check("pd_node_explicit");
+}
+void pd_node_lin(const DevPD& d, int with_force, const double* w, const int32_t* row_of, double f,
+                 const double* M, const uint8_t* cf, double gdt, double bdt2, double dt, double cpv,
+                 double cpd, double* u, double* v, double* a, double* rd, double* rv, double* out,
+                 cudaStream_t s) {
+    const int b = (d.N + kT - 1) / kT;
+    if (d.dim == 2)
+        k_pd_node_lin<2><<<b, kT, 0, s>>>(d, with_force, w, row_of, f, M, cf, gdt, bdt2, dt, cpv,
+                                          cpd, u, v, a, rd, rv, out);
+    else
+        k_pd_node_lin<3><<<b, kT, 0, s>>>(d, with_force, w, row_of, f, M, cf, gdt, bdt2, dt, cpv,
+                                          cpd, u, v, a, rd, rv, out);
+    check("pd_node_lin");
 }
 void pd_pre(int n, const double* u, const double* v, const double* a, double* rd, double* rv,
             double* ra, double dt, double cpv, double cpd, cudaStream_t s) {

@@ -20,6 +20,10 @@ void pd_node_explicit(const DevPD& d, const double* ra, double ra_scale, const d
                       const uint8_t* cf, const double* rv, const double* rd, double gdt,
                       double bdt2, const double* bcvel, int homog, double* u, double* v,
                       double* a, cudaStream_t s);
+void pd_node_lin(const DevPD& d, int with_force, const double* w, const int32_t* row_of, double f,
+                 const double* M, const uint8_t* cf, double gdt, double bdt2, double dt, double cpv,
+                 double cpd, double* u, double* v, double* a, double* rd, double* rv, double* out,
+                 cudaStream_t s);
 void pd_pre(int n, const double* u, const double* v, const double* a, double* rd, double* rv,
             double* ra, double dt, double cpv, double cpd, cudaStream_t s);
 void scatter_scaled(int n, const int32_t* idx, const double* w, double f, double* dst,

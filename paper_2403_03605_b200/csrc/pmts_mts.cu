@@ -176,6 +176,7 @@ struct pmts_mts {
     int64_t hfe_nnz = 0;
     double *sv_d = nullptr, *gp_free_d = nullptr, *gp_link_d = nullptr;    // m or m+1 rows of nl
     double* pd_ubar = nullptr;                                             // E_pd x dim
+    int32_t* row_of = nullptr;                                             // PD dof -> coupling row
     double *warm_fe_free = nullptr, *warm_fe_link = nullptr;
     bool warm_free_ok = false, warm_link_ok = false;
     // host interface state
@@ -418,14 +419,26 @@ struct pmts_mts {
         fe_solve(ra, 1.0, rv, rd, nullptr, nullptr, true, y);
     }
     void unit_pd_column(int k, const DState& y) {
-        zero(y, np);
+        // w = e_k: the ramped unit load at pd_dof[k] (mts.hpp:398-407)
+        zero_vec(lam_tmp, nl);
+        const double one = 1.0;
+        CKM(cudaMemcpyAsync(lam_tmp + k, &one, sizeof(double), cudaMemcpyHostToDevice, stream));
+        CKM(cudaStreamSynchronize(stream));
+        lin_substeps(lam_tmp, nullptr, nullptr, y);
+    }
+    // the m homogeneous linear substeps on k_sync (mts.hpp:230-238, 398-418):
+    // y_0 = 0; per substep the centroid-form force (skipped on the first, from
+    // rest) and one fused node kernel.  out_last: G_PD vel(y_m); out_rows: row j
+    // = G_PD vel(y_j), j = 1..m
+    void lin_substeps(const double* w_dev, double* out_last, double* out_rows, const DState& y) {
+        zero_vec(rd, np);
+        zero_vec(rv, np);
         for (int j = 1; j <= m; ++j) {
-            mtsk::predict(np, y.u, y.v, y.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
-            zero_vec(ra, np);
-            const double val = double(j) / m;
-            CKM(cudaMemcpyAsync(ra + s.cpl_pd[k], &val, sizeof(double), cudaMemcpyHostToDevice, stream));
-            CKM(cudaStreamSynchronize(stream));
-            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, y);
+            if (j > 1) mtsk::pd_force_lin(pdv, rd, mask_sync, pd_ubar, stream);
+            double* out = out_rows ? out_rows + (size_t)j * nl : (j == m ? out_last : nullptr);
+            mtsk::pd_node_lin(pdv, j > 1 ? 1 : 0, w_dev, row_of, double(j) / m, pd_M, pd_cf,
+                              pd_nm.gdt, pd_nm.bdt2, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, y.u, y.v, y.a,
+                              rd, rv, out, stream);
         }
     }
     void build_h_fe() {
@@ -469,13 +482,7 @@ struct pmts_mts {
     }
     // G_PD vel(Y_PD_m) w without materialising Y (mts.hpp:410-420), device in/out
     void apply_h_pd(const double* w_dev, double* out_dev) {
-        zero(yst, np);
-        for (int j = 1; j <= m; ++j) {
-            mtsk::pd_pre(np, yst.u, yst.v, yst.a, rd, rv, ra, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
-            mtsk::scatter_scaled(nl, cpd, w_dev, double(j) / m, ra, stream);  // scaled(w, j/m)
-            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, yst);
-        }
-        mtsk::gather(nl, cpd, yst.v, out_dev, stream);
+        lin_substeps(w_dev, out_dev, nullptr, yst);
     }
 
     // ---- the macro step (mts.hpp:133-306) ----
@@ -634,15 +641,9 @@ pmts_mts_report pmts_mts::macro_step() {
         mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst.u, wst.v, wst.a, ufe.u, ufe.v, ufe.a, stream);
     }
     {  // PD correction: m substeps under the ramped multiplier load, on k_sync
-        zero(wst, np);
         to_dev(lam_d, lambda);
         zero_vec(gp_link_d, nl);
-        for (int j = 1; j <= m; ++j) {
-            mtsk::pd_pre(np, wst.u, wst.v, wst.a, rd, rv, ra, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
-            mtsk::scatter_scaled(nl, cpd, lam_d, double(j) / m, ra, stream);  // scaled(lambda, j/m)
-            pd_solve(ra, 1.0, rv, rd, mask_sync, false, 0, true, wst);
-            mtsk::gather(nl, cpd, wst.v, gp_link_d + (size_t)j * nl, stream);
-        }
+        lin_substeps(lam_d, nullptr, gp_link_d, wst);
         mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
     }
     CKM(cudaStreamSynchronize(stream));
@@ -977,6 +978,11 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->gvec = h->alloc<double>(h->nl);
         h->sv_d = h->alloc<double>((size_t)h->m * h->nl);
         h->pd_ubar = h->alloc<double>((size_t)h->pdv.E * dim);
+        {
+            std::vector<int32_t> ro(h->np, -1);
+            for (int r = 0; r < h->nl; ++r) ro[s.cpl_pd[r]] = r;
+            h->row_of = h->upload(ro);
+        }
         h->gp_free_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
         h->gp_link_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
         h->warm_fe_free = h->alloc<double>(h->nf);
