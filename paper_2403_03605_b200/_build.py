@@ -54,7 +54,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(o)
         if force or _newer(o, [s] + headers):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
-                         "-Xcompiler", "-fPIC,-ffp-contract=off", *extra, "-c", s, "-o", o])
+                         "-Xcompiler", "-fPIC,-ffp-contract=off", *extra,
+                         *os.environ.get("PMTS_NVCC_FLAGS", "").split(), "-c", s, "-o", o])
     for src in HOST_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OUT, "obj", src + ".o")

@@ -181,6 +181,26 @@ def scenarios() -> dict:
     mm = copy.deepcopy(mi)
     mm["run"]["interface"] = "matrix_free"
     s["mts_mini_mfree"] = mm
+    # 3D coupled bar (hex8): 12 x 4 x 4 elements at 1 mm, PD box the middle third,
+    # tension on the +x face, -x face fixed, implicit FE
+    m3 = {
+        "mesh": {"kind": "generated", "dim": 3, "bounds": [0, 0, 0, 0.012, 0.004, 0.004],
+                 "spacing": 1e-3, "notch1": None},
+        "material": {"E": 65e9, "nu": 0.25, "rho": 2235.0, "formulation": "three_d"},
+        "pd": {"delta_factor": 2.2, "l_factor": 8.0, "s_crit": 0.0},
+        "region": {"pd_box1": [0.004, 0.0, 0.0, 0.008, 0.004, 0.004],
+                   "overlap_width_factor": 1.0, "weight_kind": "linear"},
+        "load": {"traction1": [0.012 - 1e-7, -0.001, -0.001, 0.012 + 1e-7, 0.005, 0.005,
+                               30e6, 0.0, 0.0],
+                 "fixed1": [-1e-7, -0.001, -0.001, 1e-7, 0.005, 0.005]},
+        "time": {"dt_pd": 2e-8, "m": 2, "total_time": 2e-8 * 2 * 15, "gamma_fe": 0.5,
+                 "beta_fe": 0.25, "gamma_pd": 0.5, "beta_pd": 0.0},
+        "run": {"mode": "coupled_mts", "interface": "auto"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+    s["mts_bar3d"] = m3
+
     # BASELINE cfg2, conforming analog: the cfg1 plate and
     # material, PD band 100 x 20 mm in the middle, FE elsewhere -- both at 0.25 mm
     # (the reference cannot couple a non-matching 1 mm FE mesh), 2 mm gluing zones

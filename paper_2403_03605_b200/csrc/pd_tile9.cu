@@ -40,7 +40,11 @@ constexpr int AX = GX + 2 * R, AY = GY + 2 * R;  // ubar apron (elements), 38 x 
 constexpr int BX = AX + 1, BY = AY + 1;          // node apron, 39 x 39
 constexpr int MY = GY + R;                       // bond-state apron rows the force pass reads
 constexpr int IX = 32;                           // {1/M, flags} box row (from an even column)
-constexpr int NW = 8, NT = 32 * NW;
+#ifndef PMTS_T9_NW
+#define PMTS_T9_NW 8
+#endif
+constexpr int NW = PMTS_T9_NW, NT = 32 * NW;  // 8 warps x 4 rows (3 CTAs/SM) or 16 x 2 (2 CTAs/SM)
+constexpr int kMinBlocks = NW == 8 ? 3 : 2;
 constexpr int EPT = GY / NW;
 constexpr int SHALF = kFusedS / 2;
 constexpr int URB = (AY + NW - 1) / NW;
@@ -182,7 +186,7 @@ int tile9_pair_offset(int k, int* a, int* b) {
 }
 
 template <bool DO_BREAK, bool PAIRS>
-__global__ void __launch_bounds__(NT, 3)
+__global__ void __launch_bounds__(NT, kMinBlocks)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const __grid_constant__ PairStencil2D ps, const __grid_constant__ Tile9Maps maps,
         FusedBufs bf, int step, double scale, int write_state) {

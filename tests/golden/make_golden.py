@@ -30,6 +30,7 @@ MTS_FIXTURES = {
     "mts_mini_implicit": ("mts_mini_implicit", 20, (5,)),
     "mts_mini_frac": ("mts_mini_frac", 60, (30,)),
     "mts_mini_mfree": ("mts_mini_mfree", 20, (5,)),
+    "mts_bar3d": ("mts_bar3d", 15, (5,)),
 }
 
 # name -> (scenario, steps, checkpoints)

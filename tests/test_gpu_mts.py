@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 # rounding-only; implicit FE (PCG 1e-10) and the matrix-free interface CG (1e-11)
 # carry their solver tolerances
 CASES = [("mts_mini", 1e-11), ("mts_mini_implicit", 1e-8), ("mts_mini_frac", 1e-9),
-         ("mts_mini_mfree", 1e-8)]
+         ("mts_mini_mfree", 1e-8), ("mts_bar3d", 1e-8)]
 
 
 def _rel(x, r):

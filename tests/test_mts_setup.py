@@ -11,7 +11,7 @@ from conftest import load_golden
 from paper_2403_03605_b200 import configs as cf
 from paper_2403_03605_b200.mts import MtsSolver
 
-FIXTURES = ["mts_mini", "mts_mini_implicit", "mts_mini_frac", "mts_mini_mfree"]
+FIXTURES = ["mts_mini", "mts_mini_implicit", "mts_mini_frac", "mts_mini_mfree", "mts_bar3d"]
 KEYS = ["labels", "alpha", "fe_node_dof", "pd_node_dof", "fe_k_rowptr", "fe_k_col", "fe_k_val",
         "fe_mass", "fe_p_ext", "pd_mass", "pd_p_ext", "fe_bc_dofs", "fe_bc_vel", "pd_bc_dofs",
         "pd_bc_vel", "fe_dof", "pd_dof"]
