@@ -102,8 +102,10 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid
                  : "memory");
 }
 
-constexpr int kPairA[14] = {1, 2, 3, 0, 0, 0, 1, -1, 2, -2, 2, -2, 1, -1};
-constexpr int kPairB[14] = {0, 0, 0, 1, 2, 3, 1, 1, 2, 2, 1, 1, 2, 2};
+// pair order = the column groups of the register-blocked full-tile path
+// (|A| = 0, 1, 2, 3); the masked path accumulates in the same order
+constexpr int kPairA[14] = {0, 0, 0, 1, 1, -1, 1, -1, 2, 2, -2, 2, -2, 3};
+constexpr int kPairB[14] = {1, 2, 3, 0, 1, 1, 2, 2, 0, 1, 1, 2, 2, 0};
 
 // One opposite-offset pair (o, -o) of every element of the thread: the two
 // directed entries share xi xi^T, so their forces combine into one term of
@@ -116,52 +118,118 @@ constexpr int kPairB[14] = {0, 0, 0, 1, 2, 3, 1, 1, 2, 2, 1, 1, 2, 2};
 // multiplies); the apron offset itself comes from the parameter block, which
 // keeps ptxas from hoisting all 112 loads of a thread to the top (immediate
 // offsets did, and spilled).
+// the arithmetic of one pair of one element (shared by every path, so they
+// round identically)
+template <bool DO_BREAK, bool MASKED, int K>
+__device__ __forceinline__ void pair_math(double2 up, double2 um, double2 ue, bool actp, bool actm,
+                                          double& G0, double& G1, bool& anyc,
+                                          const PairStencil2D& ps) {
+    constexpr int A = kPairA[K], B = kPairB[K];
+    const double ep0 = up.x - ue.x, ep1 = up.y - ue.y;
+    double em0 = um.x - ue.x, em1 = um.y - ue.y;
+    if (MASKED) {
+        em0 = actm ? em0 : 0.0;
+        em1 = actm ? em1 : 0.0;
+    }
+    const double fp0 = MASKED && !actp ? 0.0 : ep0, fp1 = MASKED && !actp ? 0.0 : ep1;
+    double tp;
+    if (B == 0) {
+        const double s0 = fp0 + em0;
+        G0 = fma(ps.fa[K], s0, G0);
+        tp = A * ep0;
+    } else if (A == 0) {
+        const double s1 = fp1 + em1;
+        G1 = fma(ps.fb[K], s1, G1);
+        tp = B * ep1;
+    } else {
+        const double s0 = fp0 + em0, s1 = fp1 + em1;
+        const double t = fma((double)A, s0, B * s1);
+        G0 = fma(ps.fa[K], t, G0);
+        G1 = fma(ps.fb[K], t, G1);
+        tp = fma((double)A, ep0, B * ep1);
+    }
+    if (DO_BREAK)
+        anyc |= (!MASKED || actp) && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
+}
+
 template <bool DO_BREAK, bool MASKED, int K>
 __device__ __forceinline__ void pair_term(const double2* ubq, const uint32_t* maq,
                                           const double2 (&ue)[EPT], const uint32_t (&m0)[EPT],
                                           double (&G0)[EPT], double (&G1)[EPT],
                                           bool (&anyc)[EPT], const PairStencil2D& ps) {
-    constexpr int A = kPairA[K], B = kPairB[K];
     const int off = ps.off[K];
     const double2* pp = ubq + off;
     const double2* pm = ubq - off;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
-        const double2 up = pp[r * AX];
-        const double2 um = pm[r * AX];
-        double ep0 = up.x - ue[r].x, ep1 = up.y - ue[r].y;
-        double em0 = um.x - ue[r].x, em1 = um.y - ue[r].y;
-        bool actp = true;
+        bool actp = true, actm = true;
         if (MASKED) {
             // bond e -> e+o lives at e, bond e-o -> e at e-o, both under the bit of +o;
             // a broken (or absent) bond contributes an exact zero, so a pair with both
             // bonds intact rounds exactly as on the unmasked path
             const int bit = ps.pbit[K];
             actp = (m0[r] >> bit) & 1u;
-            const bool actm = (maq[r * AX - off] >> bit) & 1u;
-            em0 = actm ? em0 : 0.0;
-            em1 = actm ? em1 : 0.0;
+            actm = (maq[r * AX - off] >> bit) & 1u;
         }
-        const double fp0 = MASKED && !actp ? 0.0 : ep0, fp1 = MASKED && !actp ? 0.0 : ep1;
-        double tp;
-        if (B == 0) {
-            const double s0 = fp0 + em0;
-            G0[r] = fma(ps.fa[K], s0, G0[r]);
-            tp = A * ep0;
-        } else if (A == 0) {
-            const double s1 = fp1 + em1;
-            G1[r] = fma(ps.fb[K], s1, G1[r]);
-            tp = B * ep1;
-        } else {
-            const double s0 = fp0 + em0, s1 = fp1 + em1;
-            const double t = fma((double)A, s0, B * s1);
-            G0[r] = fma(ps.fa[K], t, G0[r]);
-            G1[r] = fma(ps.fb[K], t, G1[r]);
-            tp = fma((double)A, ep0, B * ep1);
-        }
-        if (DO_BREAK)
-            anyc[r] |= actp && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
+        pair_math<DO_BREAK, MASKED, K>(pp[r * AX], pm[r * AX], ue[r], actp, actm, G0[r], G1[r],
+                                       anyc[r], ps);
     }
+}
+
+// full tiles, register-blocked by column group: the 4 rows of column x need,
+// for the pairs of one |A| group, the cells of columns x +- A at rows -3..6
+// (A = 0), -2..5 (|A| = 1, 2, loaded per half of the rows to stay within 80
+// registers) or 0..3 (|A| = 3): 62 shared loads per thread instead of 112 --
+// the shared-memory pipe was the limiter (ncu: 67 % of peak)
+template <bool DO_BREAK>
+__device__ __forceinline__ void pairs_blocked(const double2* ubq, const double2 (&ue)[EPT],
+                                              double (&G0)[EPT], double (&G1)[EPT],
+                                              bool (&anyc)[EPT], const PairStencil2D& ps) {
+    static_assert(EPT == 4, "blocked path assumes 4 rows per thread");
+    {  // A = 0: (0,1) (0,2) (0,3)
+        double2 c[10];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) c[i] = (i >= 3 && i < 7) ? ue[i - 3] : ubq[(i - 3) * AX];
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+            pair_math<DO_BREAK, false, 0>(c[r + 4], c[r + 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+            pair_math<DO_BREAK, false, 1>(c[r + 5], c[r + 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+            pair_math<DO_BREAK, false, 2>(c[r + 6], c[r], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+        }
+    }
+#pragma unroll
+    for (int g = 1; g <= 2; ++g) {    // |A| = 1: pairs 3..7, |A| = 2: pairs 8..12
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {  // rows 2 half .. 2 half + 1: cells rows -2..3 (+2 half)
+            double2 p[6], m[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                p[i] = ubq[(i - 2 + 2 * half) * AX + g];
+                m[i] = ubq[(i - 2 + 2 * half) * AX - g];
+            }
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int r = 2 * half + rr, q = rr + 2;
+                if (g == 1) {
+                    pair_math<DO_BREAK, false, 3>(p[q], m[q], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 4>(p[q + 1], m[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 5>(m[q + 1], p[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 6>(p[q + 2], m[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 7>(m[q + 2], p[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                } else {
+                    pair_math<DO_BREAK, false, 8>(p[q], m[q], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 9>(p[q + 1], m[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 10>(m[q + 1], p[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 11>(p[q + 2], m[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    pair_math<DO_BREAK, false, 12>(m[q + 2], p[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < EPT; ++r)  // |A| = 3: (3,0)
+        pair_math<DO_BREAK, false, 13>(ubq[r * AX + 3], ubq[r * AX - 3], ue[r], true, true, G0[r],
+                                       G1[r], anyc[r], ps);
 }
 
 template <bool DO_BREAK, bool MASKED, int K>
@@ -178,8 +246,8 @@ __device__ __forceinline__ void pair_terms(const double2* ubq, const uint32_t* m
 }  // namespace
 
 int tile9_pair_offset(int k, int* a, int* b) {
-    static const int A[14] = {1, 2, 3, 0, 0, 0, 1, -1, 2, -2, 2, -2, 1, -1};
-    static const int B[14] = {0, 0, 0, 1, 2, 3, 1, 1, 2, 2, 1, 1, 2, 2};
+    static const int A[14] = {0, 0, 0, 1, 1, -1, 1, -1, 2, 2, -2, 2, -2, 3};
+    static const int B[14] = {1, 2, 3, 0, 1, 1, 2, 2, 0, 1, 1, 2, 2, 0};
     *a = A[k];
     *b = B[k];
     return 14;
@@ -282,8 +350,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
 #pragma unroll
     for (int r = 0; r < EPT; ++r) anyc[r] = false;
     if (PAIRS && tile_full) {
-        const uint32_t none[EPT] = {};
-        pair_terms<DO_BREAK, false, 0>(ub + q0, ma + q0, ue, none, G0, G1, anyc, ps);
+        pairs_blocked<DO_BREAK>(ub + q0, ue, G0, G1, anyc, ps);
     } else if (PAIRS) {
         uint32_t m0[EPT];
 #pragma unroll
