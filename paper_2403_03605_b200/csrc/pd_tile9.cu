@@ -65,6 +65,7 @@ constexpr int kOffBar = rup(kOffUb + AX * AY * 16, 8);
 constexpr int kOffPart = kOffUb + GX * GY * 16;  // in the ubar apron's tail, after G
 constexpr int kSmem = kOffBar + 16 + 128;        // + realignment slack of the dynamic base
 static_assert(GX * GY * 16 + 8 * NW <= AX * AY * 16, "G and the partial counts fit in ub");
+static_assert(TY < GY, "a band's last force row is never an owned node row");
 static_assert(kSmem + 1024 <= 233472 / 3, "three CTAs per SM");
 
 __device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
@@ -439,9 +440,17 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
 #pragma unroll
     for (int r = 0; r < EPT; ++r)
         if (e[r] >= 0 && gx >= 1 && gy0 + r >= 1) bf.mask_out[e[r]] = m[r];
-    __syncthreads();  // every read of ub is done: G may overwrite it
+    // the node update needs, per node, (G(x,y) + G(x+1,y)) + (G(x,y+1) + G(x+1,y+1)):
+    // the horizontal pair sums come from the neighbour lane, the vertical partner
+    // row from this thread's next row -- except for a band's last row, whose
+    // partner is the next warp's first row (the only G that goes through smem)
+    double2 hsum[EPT];
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) gt[(gy0 + r) * GX + gx] = make_double2(G0[r], G1[r]);
+    for (int r = 0; r < EPT; ++r)
+        hsum[r] = make_double2(G0[r] + __shfl_down_sync(0xffffffffu, G0[r], 1),
+                               G1[r] + __shfl_down_sync(0xffffffffu, G1[r], 1));
+    __syncthreads();  // every read of ub is done: the band rows may overwrite it
+    if (warp > 0) gt[(warp - 1) * GX + lane] = hsum[0];
     mbar_wait(&bar[1], 0);
     __syncthreads();
 
@@ -458,10 +467,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const int lx = lane, ly = gy0 + r;
         if (lx >= ox || ly >= oy) continue;
         const size_t n = (size_t)(j0 + ly) * NX + i0 + lx;
-        const double2 a = gt[ly * GX + lx], b = gt[ly * GX + lx + 1];
-        const double2 c = gt[(ly + 1) * GX + lx], f = gt[(ly + 1) * GX + lx + 1];
-        const double k0 = d.Nsh * ((a.x + b.x) + (c.x + f.x));
-        const double k1 = d.Nsh * ((a.y + b.y) + (c.y + f.y));
+        const double2 hn = r + 1 < EPT ? hsum[r + 1] : gt[warp * GX + lx];  // row ly + 1
+        const double k0 = d.Nsh * (hsum[r].x + hn.x);
+        const double k1 = d.Nsh * (hsum[r].y + hn.y);
         const double im = ims[ly * IX + lx + (i0 - ie)];
         const int fl = (int)(dbits(im) & 7);  // 1: x constrained, 2: y constrained, 4: loaded
         double2 p = make_double2(0.0, 0.0);
