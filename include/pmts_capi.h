@@ -285,6 +285,10 @@ typedef struct {
     const int32_t* cpl_pd_dof;
     const int32_t* pairs;        /* [n_pairs][2] global element ids, find_pe_pairs order */
     const double* pe_weight;     /* [n_pairs] 1 - alpha at the bond midpoint */
+    const double* node_xyz;      /* [n_nodes][3] */
+    const int32_t* elem_nodes;   /* [n_elems][2^dim] */
+    const double* node_alpha;    /* [n_nodes] blend weight at the node (output sampling,
+                                    driver_run.hpp:24-35) */
 } pmts_mts_view;
 
 typedef struct {                 /* MacroReport (mts.hpp:41-63) */
@@ -308,6 +312,10 @@ int pmts_mts_get_state(pmts_mts* h, int32_t which, double* u, double* v, double*
 int pmts_mts_get_lambda(pmts_mts* h, double* lambda_out);
 /* per pair (pmts_mts_view.pairs order): 1 intact, 0 broken */
 int pmts_mts_get_intact(pmts_mts* h, uint8_t* out);
+/* damage_field (perifem.hpp:202-231) over the whole mesh: elem_out[n_elems],
+ * node_out[n_nodes]; elements without bonds (FE-only) read 0 and are left out of
+ * the nodal averages, as in the reference's coupled frames (driver_run.hpp:143-146) */
+int pmts_mts_damage(pmts_mts* h, double* elem_out, double* node_out);
 void pmts_mts_destroy(pmts_mts* h);
 
 #ifdef __cplusplus

@@ -92,7 +92,7 @@ class MtsView(C.Structure):
                 ("fe_k_val", _P), ("fe_mass", _P), ("fe_p_ext", _P), ("pd_mass", _P),
                 ("pd_p_ext", _P), ("fe_bc_dofs", _P), ("fe_bc_vel", _P), ("pd_bc_dofs", _P),
                 ("pd_bc_vel", _P), ("cpl_fe_dof", _P), ("cpl_pd_dof", _P), ("pairs", _P),
-                ("pe_weight", _P)]
+                ("pe_weight", _P), ("node_xyz", _P), ("elem_nodes", _P), ("node_alpha", _P)]
 
 
 class MtsReport(C.Structure):
@@ -142,6 +142,7 @@ SIGNATURES = {
     "pmts_mts_get_state": (C.c_int, [_P, _I, _P, _P, _P]),
     "pmts_mts_get_lambda": (C.c_int, [_P, _P]),
     "pmts_mts_get_intact": (C.c_int, [_P, _P]),
+    "pmts_mts_damage": (C.c_int, [_P, _P, _P]),
     "pmts_mts_destroy": (None, [_P]),
 }
 

@@ -1057,6 +1057,9 @@ int pmts_mts_view_get(const pmts_mts* h, pmts_mts_view* v) {
         v->cpl_pd_dof = s.cpl_pd.data();
         v->pairs = h->pairs.data();
         v->pe_weight = h->pe_weight.data();
+        v->node_xyz = s.nodes.data();
+        v->elem_nodes = s.conn.data();
+        v->node_alpha = s.node_alpha.data();
     });
 }
 
@@ -1127,6 +1130,20 @@ int pmts_mts_get_intact(pmts_mts* h, uint8_t* out) {
         if (!h || !out) throw ConfigError("bad arguments");
         if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
         check_pd(pmts_pd_get_intact(h->pd, out, h->npe));
+    });
+}
+
+int pmts_mts_damage(pmts_mts* h, double* elem_out, double* node_out) {
+    return guard([&] {
+        if (!h || !elem_out || !node_out) throw ConfigError("bad arguments");
+        if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        const MtsSystem& s = h->s;
+        std::vector<double> pe(s.pd_active.size()), pn(s.pd_active_nodes.size());
+        check_pd(pmts_pd_damage(h->pd, pe.data(), pn.data()));
+        std::fill(elem_out, elem_out + s.volume.size(), 0.0);
+        std::fill(node_out, node_out + s.nodes.size() / 3, 0.0);
+        for (size_t k = 0; k < s.pd_active.size(); ++k) elem_out[s.pd_active[k]] = pe[k];
+        for (size_t k = 0; k < s.pd_active_nodes.size(); ++k) node_out[s.pd_active_nodes[k]] = pn[k];
     });
 }
 

@@ -479,6 +479,8 @@ void build_mts_system(MtsSystem& s) {
     if (n_pd == 0) throw ConfigError("PD region must keep a core beyond the overlap bands");
     s.alpha.resize(E);
     for (int e = 0; e < E; ++e) s.alpha[e] = mts_alpha_at(s, s.centroid.data() + 3 * std::size_t(e));
+    s.node_alpha.resize(N);
+    for (int n = 0; n < N; ++n) s.node_alpha[n] = mts_alpha_at(s, s.nodes.data() + 3 * std::size_t(n));
     s.fe_active.clear();
     s.pd_active.clear();
     for (int e = 0; e < E; ++e) {

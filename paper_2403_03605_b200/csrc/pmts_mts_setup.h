@@ -55,6 +55,7 @@ struct MtsSystem {
     std::vector<int32_t> fe_bc_dofs, pd_bc_dofs;
     std::vector<double> fe_bc_vel, pd_bc_vel;
     std::vector<int32_t> cpl_fe, cpl_pd;  // coupling rows
+    std::vector<double> node_alpha;       // blend weight at each node (output sampling)
 };
 
 // assembles everything after the inputs and the mesh geometry are filled in

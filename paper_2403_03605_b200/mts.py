@@ -93,6 +93,10 @@ class MtsSolver:
             "pe_weight": _arr(v.pe_weight, f64, v.n_pairs),
             "delta": v.delta, "c0": v.c0, "l": v.l, "char_length": v.char_length,
             "load_ramp": v.load_ramp,
+            "node_xyz": _arr(v.node_xyz, f64, 3 * N, (N, 3)),
+            "elem_nodes": _arr(v.elem_nodes, i32, E * (4 if v.dim == 2 else 8),
+                               (E, 4 if v.dim == 2 else 8)),
+            "node_alpha": _arr(v.node_alpha, f64, N),
         }
 
     # -- integration --------------------------------------------------------
@@ -124,3 +128,11 @@ class MtsSolver:
         out = np.empty(self.n_pairs, dtype=np.uint8)
         check(lib().pmts_mts_get_intact(self.h, ptr(out)))
         return out
+
+    def damage_field(self):
+        """damage_field over the whole mesh (element, node)."""
+        e = np.empty(self.n_elems)
+        n = np.empty(self.n_nodes)
+        check(lib().pmts_mts_damage(self.h, ptr(e), ptr(n)))
+        return e, n
+
