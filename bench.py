@@ -9,8 +9,9 @@ bonds, per-bond s0 factor, constant micromodulus), synthetic geometry with
 the config's shapes.  value = unique bonds x K / device time of K steps
 (CUDA events on the handle's stream), max over ranks.  e2e = the same metric
 through the public C-ABI with host buffers: initial state H2D from pinned
-memory, per step the load scale in and the broken count + tracked
-displacements out, final state D2H, timed on the host clock.
+memory, the load scales in and the broken counts + tracked displacements
+out (the step kernel writes the tracked row to mapped pinned memory), final
+state D2H, timed on the host clock.
 
 --impl reference times the reference's own CPU loop (oracle/_ref/ref_driver,
 compiled from the unmodified reference headers) on all host cores, on a
@@ -378,9 +379,10 @@ def bench_native(args):
         e2e = {"value": B * K / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / K,
                "note": "per rank, one pmts_pd_step_tracked call for the K steps: state H2D "
-                       "from pinned memory, then per step (async on the stream) the step's "
-                       "load scale H2D, the step, its tracked displacement + broken count "
-                       "D2H; final state D2H"}
+                       "from pinned memory, the K load scales H2D in one copy, per step "
+                       "(async on the stream) the step, whose kernel writes its tracked "
+                       "displacement into mapped pinned memory; the K broken counts D2H in "
+                       "one copy; final state D2H"}
     except Exception as ex:  # pragma: no cover - reported, never silent
         e2e = {"value": None, "unit": UNIT, "error": repr(ex)}
 

@@ -45,6 +45,12 @@ struct FusedBufs {
     const uint32_t* mask_in;
     uint32_t* mask_out;
     const double* scale_dev = nullptr;  // tile9: per-step load scales copied H2D (or null)
+    // tile9, pmts_pd_step_tracked: one block copies the tracked dofs of the step's
+    // displacement straight into mapped pinned host memory (a separate kernel
+    // instance; n_trk = 0: none)
+    const int32_t* trk_dofs = nullptr;
+    int n_trk = 0;
+    double* trk_host = nullptr;  // this step's row (n_trk values)
 };
 
 void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,

@@ -254,7 +254,7 @@ int tile9_pair_offset(int k, int* a, int* b) {
     return 14;
 }
 
-template <bool DO_BREAK, bool PAIRS>
+template <bool DO_BREAK, bool PAIRS, bool REPORT>
 __global__ void __launch_bounds__(NT, kMinBlocks)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const __grid_constant__ PairStencil2D ps, const __grid_constant__ Tile9Maps maps,
@@ -287,6 +287,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         mbar_expect_tx(&bar[1], kRvBytes + kImBytes);
         tma_load_2d(sm + kOffRv, &maps.rv, 2 * i0, j0, &bar[1]);
         tma_load_2d(sm + kOffIm, &maps.im, ie, j0, &bar[1]);
+    }
+    if constexpr (REPORT) {
+        // pmts_pd_step_tracked: the step's u is the predictor it consumes (beta = 0);
+        // block (0, 0) copies the tracked dofs of it into mapped pinned host memory
+        if ((blockIdx.x | blockIdx.y) == 0)
+            for (int j = threadIdx.x; j < bf.n_trk; j += NT) bf.trk_host[j] = bf.rd_in[bf.trk_dofs[j]];
     }
     for (int y = warp; y < MY; y += NW) {
         const int gj = ay0 + y;
@@ -519,15 +525,26 @@ void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_
     *im_y = TY;
 }
 
+namespace {
+template <bool B, bool P, bool Q>
+void t9_set_smem() {
+    cudaError_t e = cudaFuncSetAttribute(k_tile9<B, P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmem);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+}  // namespace
+
 int tile9_configure() {
-    for (auto fn : {k_tile9<true, false>, k_tile9<false, false>, k_tile9<true, true>,
-                    k_tile9<false, true>}) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (e != cudaSuccess)
-            throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
-    }
+    t9_set_smem<true, false, false>();
+    t9_set_smem<false, false, false>();
+    t9_set_smem<true, true, false>();
+    t9_set_smem<false, true, false>();
+    t9_set_smem<true, false, true>();
+    t9_set_smem<false, false, true>();
+    t9_set_smem<true, true, true>();
+    t9_set_smem<false, true, true>();
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true, true>, NT, kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true, true, false>, NT, kSmem);
     return occ;
 }
 
@@ -537,17 +554,23 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
     dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
     const PairStencil2D none{};
     const PairStencil2D& p = ps ? *ps : none;
-    if (ps) {
-        if (do_break)
-            k_tile9<true, true><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
-        else
-            k_tile9<false, true><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
-    } else {
-        if (do_break)
-            k_tile9<true, false><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
-        else
-            k_tile9<false, false><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state);
+#define PMTS_T9_LAUNCH(B, P, Q) \
+    k_tile9<B, P, Q><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state)
+#define PMTS_T9_PICK(Q)                                              \
+    if (ps) {                                                        \
+        if (do_break) PMTS_T9_LAUNCH(true, true, Q);                 \
+        else PMTS_T9_LAUNCH(false, true, Q);                         \
+    } else {                                                         \
+        if (do_break) PMTS_T9_LAUNCH(true, false, Q);                \
+        else PMTS_T9_LAUNCH(false, false, Q);                        \
     }
+    if (b.n_trk > 0) {
+        PMTS_T9_PICK(true)
+    } else {
+        PMTS_T9_PICK(false)
+    }
+#undef PMTS_T9_PICK
+#undef PMTS_T9_LAUNCH
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }

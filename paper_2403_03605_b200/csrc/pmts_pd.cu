@@ -725,10 +725,16 @@ void ensure_counts(pmts_pd* h, int n) {
 
 // one fine step: bond gather + node update with the fused predictor
 void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev,
-                  bool last = true, const double* scale_dev = nullptr) {
+                  bool last = true, const double* scale_dev = nullptr,
+                  const FusedBufs* report = nullptr) {
     const int brk = h->fracture ? 1 : 0;
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt, scale_dev};
+        if (report) {
+            b.trk_dofs = report->trk_dofs;
+            b.n_trk = report->n_trk;
+            b.trk_host = report->trk_host;
+        }
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
         if (h->tile9)
             launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
@@ -1216,17 +1222,30 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
             if (n_tracked) upload(didx, dofs, n_tracked, h->stream);
         }
         // per step, all asynchronous on the handle's stream (one synchronisation at
-        // the end): the step (the tile9 kernel reads its load scale from device
-        // memory), then one tiny launch that writes the step's tracked row and
-        // broken count into mapped pinned host memory and moves the next step's
-        // scale from mapped pinned host memory to the device
-        if (n > 0) upload(dscl, h_scl, 1, h->stream);
-        for (int s = 0; s < n; ++s) {
+        // the end).  tile9: the scales go up in one copy, each step's kernel writes
+        // its tracked row into mapped pinned host memory from the node update, and
+        // the broken counts come back in one copy -- one launch per step.  Other
+        // paths: the step, then one tiny launch that writes the step's tracked row
+        // and broken count into mapped pinned host memory and moves the next step's
+        // scale from mapped pinned host memory to the device.
+        if (h->tile9 && n > 0) {
+            upload(dscl, h_scl, n, h->stream);
+            for (int s = 0; s < n; ++s) {
+                FusedBufs rep{};
+                rep.trk_dofs = didx;
+                rep.n_trk = n_tracked;
+                rep.trk_host = m_trk + (size_t)s * n_tracked;
+                enqueue_step(h, s, scales[s], false, nullptr, s == n - 1, dscl, &rep);
+            }
+            download(h_cnt, h->d_counts, n, h->stream);
+        } else if (n > 0) {
+            upload(dscl, h_scl, 1, h->stream);
+        }
+        for (int s = 0; s < n && !h->tile9; ++s) {
             // u of step s: the fused kernel's displacement is the step's predictor
             // (beta = 0), i.e. the rd buffer it consumed; the other paths write u
             const bool every = !h->fused;
-            enqueue_step(h, s, scales[s], false, nullptr, every || s == n - 1,
-                         h->tile9 ? dscl : nullptr);
+            enqueue_step(h, s, scales[s], false, nullptr, every || s == n - 1, nullptr);
             const double* src = h->fused ? h->rd_alt : h->d.u;
             launch_track(src, didx, n_tracked, m_trk + (size_t)s * n_tracked, h->d_counts + s,
                          m_cnt + s, s + 1 < n ? m_scl + s + 1 : nullptr,
