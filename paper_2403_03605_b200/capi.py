@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpmts.so")
+LIB_PATH = os.environ.get("PMTS_LIB_PATH") or os.path.join(HERE, "lib", "libpmts.so")
 
 PMTS_OK, PMTS_ERR_INTERNAL, PMTS_ERR_CONFIG, PMTS_ERR_SOLVER = 0, 1, 2, 3
 DETERMINISTIC, FAST = 0, 1

@@ -79,6 +79,7 @@ void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
 // flags in the three low mantissa bits).
 struct Tile9Maps {
     CUtensorMap rd, rv, im;
+    int prefetch_ahead;  // > 0: each CTA prefetches into L2 the boxes of tile id + this
 };
 void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y);
 // Pair-symmetric force constants of the 14 positive offsets of the 28-offset
@@ -93,6 +94,9 @@ struct PairStencil2D {
     int off[14];   // apron offset of o (dj * 38 + di)
     int pbit[14];  // mask bit of the positive offset o
     double h2;    // 2 h
+    int screen;   // 1: skip the candidate break pass on tiles the node-step bound
+                  // proves cold (pd_tile9.cu); results are bitwise the same
+    unsigned long long* hot_count;  // diagnostics (PMTS_T9_COUNT_HOT): [0] hot, [1] all tiles
 };
 int tile9_pair_offset(int k, int* a, int* b);
 int tile9_configure();  // returns resident CTAs per SM

@@ -25,6 +25,8 @@
 // 16-byte aligned global row starts (so the {1/M, flags} box starts at the
 // even column i0 & ~1 of rows padded to an even length).  Reference semantics
 // as in pd_stencil.cu.
+#include <cstring>
+#include <initializer_list>
 #include <stdexcept>
 #include <string>
 
@@ -47,7 +49,6 @@ constexpr int NW = PMTS_T9_NW, NT = 32 * NW;  // 8 warps x 4 rows (3 CTAs/SM) or
 constexpr int kMinBlocks = NW == 8 ? 3 : 2;
 constexpr int EPT = GY / NW;
 constexpr int SHALF = kFusedS / 2;
-constexpr int URB = (AY + NW - 1) / NW;
 static_assert(GX == 32 && EPT * NW == GY, "lane = column, warp = EPT rows");
 static_assert(AX == kFusedAX, "Stencil2D apron offsets assume this width");
 
@@ -63,7 +64,8 @@ constexpr int kOffMa = rup(kOffRv + kRvBytes, 16);  // AX x MY bond-state words
 constexpr int kOffUb = rup(kOffMa + AX * MY * 4, 16);
 constexpr int kOffBar = rup(kOffUb + AX * AY * 16, 8);
 constexpr int kOffPart = kOffUb + GX * GY * 16;  // in the ubar apron's tail, after G
-constexpr int kSmem = kOffBar + 16 + 128;        // + realignment slack of the dynamic base
+constexpr int kOffRed = kOffBar + 16;            // screen: per-warp node-step maxima
+constexpr int kSmem = kOffRed + 4 * NW * 4 + 8 + 128;  // + realignment slack of the dynamic base
 static_assert(GX * GY * 16 + 8 * NW <= AX * AY * 16, "G and the partial counts fit in ub");
 static_assert(TY < GY, "a band's last force row is never an owned node row");
 static_assert(kSmem + 1024 <= 233472 / 3, "three CTAs per SM");
@@ -96,6 +98,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(b))
         : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map),
+                 "r"(x), "r"(y)
+                 : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
@@ -244,6 +251,43 @@ __device__ __forceinline__ void pair_terms(const double2* ubq, const uint32_t* m
     }
 }
 
+// candidate break test of the bond e -> e + o (state kept at e) for the pairs of
+// one element; only run on tiles the screen could not prove cold
+template <bool MASKED, int K>
+__device__ __forceinline__ void cand_terms(const double2* uq, double2 ue, uint32_t m0, bool& anyc,
+                                           const PairStencil2D& ps) {
+    if constexpr (K < 14) {
+        constexpr int A = kPairA[K], B = kPairB[K];
+        const double2 up = uq[ps.off[K]];
+        const double ep0 = up.x - ue.x, ep1 = up.y - ue.y;
+        double tp;
+        if (B == 0) tp = A * ep0;
+        else if (A == 0) tp = B * ep1;
+        else tp = fma((double)A, ep0, B * ep1);
+        const bool act = !MASKED || ((m0 >> ps.pbit[K]) & 1u);
+        anyc |= act && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
+        cand_terms<MASKED, K + 1>(uq, ue, m0, anyc, ps);
+    }
+}
+
+__device__ __forceinline__ int ps_a(int k) {
+    return k == 13 ? 3 : (k >= 8 ? 2 : (k >= 3 ? 1 : 0));  // |A| of pair k
+}
+__device__ __forceinline__ int ps_b(int k) {
+    constexpr unsigned kB = 0u | (1u << 0) | (2u << 2) | (3u << 4) | (0u << 6) | (1u << 8) |
+                            (1u << 10) | (2u << 12) | (2u << 14) | (0u << 16) | (1u << 18) |
+                            (1u << 20) | (2u << 22) | (2u << 24) | (0u << 26);
+    return (kB >> (2 * k)) & 3u;  // |B| of pair k
+}
+
+// |d| <= hi_bound(max of hi_abs(d)): the high word of |d| orders like |d|
+__device__ __forceinline__ unsigned hi_abs(double d) {
+    return (unsigned)__double2hiint(d) & 0x7fffffffu;
+}
+__device__ __forceinline__ double hi_bound(unsigned m) {
+    return __hiloint2double((int)m, (int)0xffffffffu);
+}
+
 }  // namespace
 
 int tile9_pair_offset(int k, int* a, int* b) {
@@ -254,11 +298,15 @@ int tile9_pair_offset(int k, int* a, int* b) {
     return 14;
 }
 
+// PAIRS: the pair-symmetric force with the cold-tile break screen; otherwise the
+// per-offset sums of pd_stencil_fused.cu (bitwise equal to it)
 template <bool DO_BREAK, bool PAIRS, bool REPORT>
 __global__ void __launch_bounds__(NT, kMinBlocks)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
-        const __grid_constant__ PairStencil2D ps, const __grid_constant__ Tile9Maps maps,
-        FusedBufs bf, int step, double scale, int write_state) {
+        const __grid_constant__ PairStencil2D ps,
+        const __grid_constant__ Tile9Maps maps, FusedBufs bf, int step, double scale,
+        int write_state) {
+    constexpr bool SCREEN = PAIRS && DO_BREAK;
     extern __shared__ __align__(16) unsigned char smraw[];
     // the dynamic base is only guaranteed 16-byte aligned: realign for TMA
     unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
@@ -270,6 +318,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     double2* gt = ub;  // G aliases the ubar apron once the force pass is done
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
     unsigned long long* part = reinterpret_cast<unsigned long long*>(sm + kOffPart);
+    unsigned* red = reinterpret_cast<unsigned*>(sm + kOffRed);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
@@ -277,7 +326,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     const int ie = i0 & ~1;  // {1/M, flags} box start: 16-byte aligned global row start
 
     // (1) staging: TMA for the node apron and the node-update inputs; 4-byte
-    //     cp.async (zero-filled outside the domain) for the bond-state apron
+    //     cp.async (zero-filled outside the domain) for the bond-state apron (a
+    //     TMA box must start 16-byte aligned, so the mask box would be 3 columns
+    //     wider than the CTA's shared memory has room for; measured: no faster)
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -287,6 +338,18 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         mbar_expect_tx(&bar[1], kRvBytes + kImBytes);
         tma_load_2d(sm + kOffRv, &maps.rv, 2 * i0, j0, &bar[1]);
         tma_load_2d(sm + kOffIm, &maps.im, ie, j0, &bar[1]);
+        // warm L2 for the tile that takes this CTA's slot a wave later
+        const int ahead = maps.prefetch_ahead;
+        if (ahead > 0) {
+            const int t = blockIdx.y * gridDim.x + blockIdx.x + ahead;
+            if (t < gridDim.x * gridDim.y) {
+                const int pi0 = (t % gridDim.x) * TX, pj0 = (t / gridDim.x) * TY;
+                const int pax0 = pi0 - 1 - R, pay0 = pj0 - 1 - R;
+                tma_prefetch_2d(&maps.rd, 2 * pax0, pay0);
+                tma_prefetch_2d(&maps.rv, 2 * pi0, pj0);
+                tma_prefetch_2d(&maps.im, pi0 & ~1, pj0);
+            }
+        }
     }
     if constexpr (REPORT) {
         // pmts_pd_step_tracked: the step's u is the predictor it consumes (beta = 0);
@@ -311,33 +374,94 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     mbar_wait(&bar[0], 0);
 
     // (2) ubar of the apron (column walk with carried node-pair sums); the
-    //     positive-stencil completeness of every mask the force pass reads
+    //     positive-stencil completeness of every mask the force pass reads.
+    //     Work item = (column x, block of UR ub rows): 228 items, one per thread.
     constexpr uint32_t kPos = ((1u << kFusedS) - 1u) & ~((1u << SHALF) - 1u);
+    constexpr int UR = 7, NYB = (AY + UR - 1) / UR;
+    static_assert(AX * NYB <= NT, "one ubar work item per thread");
     bool tile_full = true;
+    // screen: maxima of |node step| over the in-domain nodes of the apron, per
+    // component and direction (x-step of u_x, y-step of u_x, x-step of u_y,
+    // y-step of u_y), as high words (out-of-domain nodes are TMA zero fill)
+    unsigned mxx = 0, mxy = 0, myx = 0, myy = 0;
+    if (threadIdx.x < AX * NYB) {
+        const int x = threadIdx.x % AX, y0 = (threadIdx.x / AX) * UR;
+        const bool ca = (unsigned)(ax0 + x) <= (unsigned)nx;      // node column x in the domain
+        const bool cb = (unsigned)(ax0 + x + 1) <= (unsigned)nx;  // node column x + 1
+        double2 hs[UR + 1];
+        double2 ap = make_double2(0.0, 0.0), bp = ap;
+        bool rp = false;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int x = lane + 32 * h;
-        const int y0 = URB * warp;
-        if (x < AX && y0 < AY) {
-            double2 hs[URB + 1];
-#pragma unroll
-            for (int i = 0; i <= URB; ++i) {
-                const int y = min(y0 + i, BY - 1);
-                const double2 a = nt[y * BX + x], b = nt[y * BX + x + 1];
-                hs[i] = make_double2(a.x + b.x, a.y + b.y);
-            }
-#pragma unroll
-            for (int i = 0; i < URB; ++i) {
-                const int y = y0 + i;
-                if (y < AY) {
-                    ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
-                                                  d.Nsh * (hs[i].y + hs[i + 1].y));
-                    if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
+        for (int i = 0; i <= UR; ++i) {
+            const int y = min(y0 + i, BY - 1);
+            const double2 a = nt[y * BX + x], b = nt[y * BX + x + 1];
+            hs[i] = make_double2(a.x + b.x, a.y + b.y);
+            if (SCREEN) {
+                const bool rw = (unsigned)(ay0 + y) <= (unsigned)ny;
+                if (rw && ca && cb) {
+                    mxx = max(mxx, hi_abs(b.x - a.x));
+                    myx = max(myx, hi_abs(b.y - a.y));
                 }
+                if (i > 0 && rw && rp) {
+                    if (ca) {
+                        mxy = max(mxy, hi_abs(a.x - ap.x));
+                        myy = max(myy, hi_abs(a.y - ap.y));
+                    }
+                    if (x == AX - 1 && cb) {
+                        mxy = max(mxy, hi_abs(b.x - bp.x));
+                        myy = max(myy, hi_abs(b.y - bp.y));
+                    }
+                }
+                ap = a;
+                bp = b;
+                rp = rw;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < UR; ++i) {
+            const int y = y0 + i;
+            if (y < AY) {
+                ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
+                                              d.Nsh * (hs[i].y + hs[i + 1].y));
+                if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
             }
         }
     }
+    if (SCREEN) {
+        mxx = __reduce_max_sync(0xffffffffu, mxx);
+        mxy = __reduce_max_sync(0xffffffffu, mxy);
+        myx = __reduce_max_sync(0xffffffffu, myx);
+        myy = __reduce_max_sync(0xffffffffu, myy);
+        if (lane == 0) {
+            red[4 * warp + 0] = mxx;
+            red[4 * warp + 1] = mxy;
+            red[4 * warp + 2] = myx;
+            red[4 * warp + 3] = myy;
+        }
+    }
     tile_full = __syncthreads_and(tile_full);
+    // hot: some bond of the tile could reach its candidate threshold.  With the
+    // node-step maxima D, |eta_x| <= E0 = |A| Dxx + |B| Dxy, |eta_y| <= E1 =
+    // |A| Dyx + |B| Dyy, so 2 xi.eta + |eta|^2 <= 2h (|A| E0 + |B| E1) + E0^2 + E1^2.
+    bool hot = DO_BREAK;
+    if (SCREEN && ps.screen) {
+        unsigned v = red[lane & (4 * NW - 1)];
+#pragma unroll
+        for (int o = 4; o < 4 * NW; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+        const double Dxx = hi_bound(__shfl_sync(0xffffffffu, v, 0));
+        const double Dxy = hi_bound(__shfl_sync(0xffffffffu, v, 1));
+        const double Dyx = hi_bound(__shfl_sync(0xffffffffu, v, 2));
+        const double Dyy = hi_bound(__shfl_sync(0xffffffffu, v, 3));
+        const int k = lane < 14 ? lane : 0;
+        const double A = fabs((double)ps_a(k)), B = fabs((double)ps_b(k));
+        const double E0 = A * Dxx + B * Dxy, E1 = A * Dyx + B * Dyy;
+        const double bound = fma(ps.h2, A * E0 + B * E1, E0 * E0 + E1 * E1) * (1.0 + 1e-6);
+        hot = __any_sync(0xffffffffu, lane < 14 && !(bound < __longlong_as_double(ps.cl[k])));
+        if (ps.hot_count && threadIdx.x == 0) {
+            atomicAdd(ps.hot_count, hot ? 1ull : 0ull);
+            atomicAdd(ps.hot_count + 1, 1ull);
+        }
+    }
 
     // (3) forces of the 32 x 32 region: column = lane, rows EPT*warp + r
     const int gx = lane, gy0 = warp * EPT;
@@ -356,13 +480,31 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     bool anyc[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) anyc[r] = false;
-    if (PAIRS && tile_full) {
-        pairs_blocked<DO_BREAK>(ub + q0, ue, G0, G1, anyc, ps);
-    } else if (PAIRS) {
-        uint32_t m0[EPT];
+    if constexpr (PAIRS) {
+        // candidate break tests first, on the tiles the screen could not prove cold
+        // (rolled over the rows: the registers are free before the force pass)
+        uint32_t cand = 0;
+        if (DO_BREAK && hot) {
+#pragma unroll 1
+            for (int r = 0; r < EPT; ++r) {
+                const int q = q0 + r * AX;
+                bool ac = false;
+                if (tile_full) cand_terms<false, 0>(ub + q, ub[q], 0u, ac, ps);
+                else cand_terms<true, 0>(ub + q, ub[q], ma[q], ac, ps);
+                cand |= (ac ? 1u : 0u) << r;
+            }
+        }
 #pragma unroll
-        for (int r = 0; r < EPT; ++r) m0[r] = ma[q0 + r * AX];
-        pair_terms<DO_BREAK, true, 0>(ub + q0, ma + q0, ue, m0, G0, G1, anyc, ps);
+        for (int r = 0; r < EPT; ++r) anyc[r] = (cand >> r) & 1u;
+        bool none[EPT];
+        if (tile_full) {
+            pairs_blocked<false>(ub + q0, ue, G0, G1, none, ps);
+        } else {
+            uint32_t m0[EPT];
+#pragma unroll
+            for (int r = 0; r < EPT; ++r) m0[r] = ma[q0 + r * AX];
+            pair_terms<false, true, 0>(ub + q0, ma + q0, ue, m0, G0, G1, none, ps);
+        }
     } else if (tile_full) {
 #pragma unroll
         for (int k = 0; k < kFusedS; ++k) {
@@ -425,8 +567,8 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             while (c) {
                 const int k = __ffs(c) - 1;
                 c &= c - 1;
-                const double2 up = ub[q0 + r * AX + st.aoff[k]];
-                const double e0 = up.x - ue[r].x, e1 = up.y - ue[r].y;
+                const double2 up = ub[q0 + r * AX + st.aoff[k]], uer = ub[q0 + r * AX];
+                const double e0 = up.x - uer.x, e1 = up.y - uer.y;
                 const double dot = fma(st.xi1[k], e1, st.xi0[k] * e0);
                 const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
                 double thr = st.cthr[k];

@@ -94,6 +94,7 @@ struct pmts_pd {
     bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
     int tile9_occ = 0;               // its resident CTAs per SM
     CUtensorMap t9_rd[2]{}, t9_rv{}, t9_im{};
+    int t9_prefetch = 0;  // L2 prefetch distance in tiles (resident CTAs of the device)
     bool pairs = false;              // tile9 with the pair-symmetric compile-time stencil
     PairStencil2D pst{};
     double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
@@ -350,6 +351,7 @@ Tile9Maps tile9_maps(const pmts_pd* h) {
     m.rd = h->t9_rd[h->d.rd == h->rd_buf[0] ? 0 : 1];
     m.rv = h->t9_rv;
     m.im = h->t9_im;
+    m.prefetch_ahead = h->t9_prefetch;
     return m;
 }
 
@@ -616,10 +618,17 @@ bool try_lattice(pmts_pd* h) {
             h->rd_buf[1] = h->rd_alt;
             build_tile9_maps(h);
             h->tile9_occ = tile9_configure();
+            {
+                int sms = 0;
+                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->desc.device));
+                h->t9_prefetch = sms * h->tile9_occ;
+                if (const char* e = std::getenv("PMTS_T9_PREFETCH")) h->t9_prefetch = std::atoi(e);
+            }
             // pair-symmetric force on the nominal lattice (PMTS_NO_PAIRS=1 keeps the
             // tile kernel's per-offset arithmetic, bitwise equal to pd_stencil_fused.cu)
             h->pairs = h->desc.lattice_h > 0.0 && !std::getenv("PMTS_NO_PAIRS");
             const double hh = h->desc.lattice_h;
+
             for (int k = 0; k < 14 && h->pairs; ++k) {
                 int A = 0, B = 0;
                 tile9_pair_offset(k, &A, &B);
@@ -640,6 +649,13 @@ bool try_lattice(pmts_pd* h) {
                 h->pst.pbit[k] = s;
             }
             h->pst.h2 = 2.0 * hh;
+            // cold-tile break screen (PMTS_T9_NO_SCREEN=1: candidate pass on every tile)
+            h->pst.screen = std::getenv("PMTS_T9_NO_SCREEN") ? 0 : 1;
+            h->pst.hot_count = nullptr;
+            if (std::getenv("PMTS_T9_COUNT_HOT")) {
+                h->pst.hot_count = h->alloc<unsigned long long>(2);
+                CK(cudaMemsetAsync(h->pst.hot_count, 0, 16, h->stream));
+            }
         }
         if (h->tma) {
             std::vector<double> aux(2 * (size_t)h->N);
@@ -961,6 +977,11 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
 }
 
 void pmts_pd_destroy(pmts_pd* h) {
+    if (h && h->pst.hot_count) {  // PMTS_T9_COUNT_HOT diagnostics
+        unsigned long long c[2] = {0, 0};
+        cudaMemcpy(c, h->pst.hot_count, 16, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "pmts: tile9 screen: %llu of %llu tiles hot\n", c[0], c[1]);
+    }
     if (h && h->comm) {
         if (h->stream) cudaStreamSynchronize(h->stream);
         nccl().comm_destroy((ncclComm_t)h->comm);

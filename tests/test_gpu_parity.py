@@ -194,6 +194,30 @@ def test_tile9_pairs_close_to_per_offset(nx, ny, monkeypatch):
         assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
 
 
+@pytest.mark.parametrize("nx,ny,steps", [(40, 16, 120), (124, 62, 300), (33, 65, 200), (64, 93, 200)])
+def test_tile9_screen_is_exact(nx, ny, steps, monkeypatch):
+    """The cold-tile break screen (default) only skips candidate tests the node-step
+    bound proves cannot fire: u, v, a and the bond states are bitwise those of the
+    candidate pass on every tile (PMTS_T9_NO_SCREEN=1)."""
+    sc = _plate(nx, ny)
+    out = {}
+    for screen in (True, False):
+        if screen:
+            monkeypatch.delenv("PMTS_T9_NO_SCREEN", raising=False)
+        else:
+            monkeypatch.setenv("PMTS_T9_NO_SCREEN", "1")
+        s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = s.step([sc.load_scale(i * sc.dt) for i in range(1, steps + 1)])
+        out[screen] = (nb, *s.state(), s.intact())
+    a, b = out[True], out[False]
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
+    if (nx, ny) == (40, 16):
+        assert a[0] > 0
+
+
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
 def test_step_tracked_reports_every_step(mode):
     """pmts_pd_step_tracked: per-step tracked displacements and broken counts equal
@@ -391,3 +415,23 @@ def test_cfg3_linearity_and_momentum(cfg3):
     f_int = P - cfg3.mass * a1
     assert abs(f_int[0::2].sum()) <= 1e-9 * np.abs(f_int).sum()
     assert abs(f_int[1::2].sum()) <= 1e-9 * np.abs(f_int).sum()
+
+
+def test_cfg3_screen_exact_over_baseline_horizon(cfg3, monkeypatch):
+    """BASELINE cfg3 over its full 1000-step horizon (cracks start near step 700):
+    the screened kernel's per-batch broken counts, bond states and fields are bitwise
+    those of the unscreened candidate pass."""
+    out = {}
+    for screen in (True, False):
+        if screen:
+            monkeypatch.delenv("PMTS_T9_NO_SCREEN", raising=False)
+        else:
+            monkeypatch.setenv("PMTS_T9_NO_SCREEN", "1")
+        s = PDSolver.from_scenario(cfg3, mode=capi.FAST).find_pe_pairs()
+        s.initial_acceleration(cfg3.load_scale(0.0))
+        nb = [s.step(cfg3.scales(i, 100)) for i in range(1, 1001, 100)]
+        out[screen] = (nb, *s.state(), s.intact())
+    a, b = out[True], out[False]
+    assert a[0] == b[0] and sum(a[0]) > 1000
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
