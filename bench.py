@@ -255,8 +255,9 @@ def bench_native(args):
     rank, local, world = _env_rank()
     dist = None
     mode = capi.FAST if args.mode == "fast" else capi.DETERMINISTIC
-    t0 = time.perf_counter()
-    if world > 1 or args.force_slabs:
+    K, W = args.steps, args.warmup
+    slabbed = world > 1 or args.force_slabs
+    if slabbed:
         # slab decomposition (paper_2403_03605_b200/slabs.py), weak scaling: the plate
         # grows with N so every rank owns one cfg3-sized slab; the halo exchange is
         # ncclSend/ncclRecv inside the library's step loop, the control plane is gloo
@@ -272,40 +273,51 @@ def bench_native(args):
             dist.init_process_group("gloo", rank=0, world_size=1)
         else:
             dist.init_process_group("gloo")
-        cfg = cf.stacked(args.workload, world)
-        sc = Scenario(cfg)
+        sc = Scenario(cf.stacked(args.workload, world))
         slab = slabs.make_slab(sc.lattice, sc.dim, rank, world)
-        s = slabs.solver_for_slab(sc, slab, mode, device=local).find_pe_pairs()
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            uid[:] = torch.frombuffer(bytearray(PDSolver.nccl_unique_id()), dtype=torch.uint8)
-        dist.broadcast(uid, 0)
-        s.comm_init(bytes(uid.tolist()), world, rank)
-        s.set_halo(*slab.halo)
-        lp = s.pairs()
-        own = int(((lp[:, 0] >= slab.own_elems[0]) & (lp[:, 0] < slab.own_elems[1])).sum())
-        tb = torch.tensor([own], dtype=torch.int64)
-        dist.all_reduce(tb)
-        B = int(tb.item())  # unique bonds of the whole plate
     else:
         sc = Scenario(cf.get(args.workload))
-        s = PDSolver.from_scenario(sc, mode=mode, device=local).find_pe_pairs()
+    B = None
+
+    def fresh():
+        """A new handle stepped through the W warm-up steps: every measurement below
+        (device time, roofline, end to end) covers the same steps W+1 .. W+K of the
+        BASELINE run, so they time the same physics (cracks start late in cfg3)."""
+        nonlocal B
+        if slabbed:
+            s = slabs.solver_for_slab(sc, slab, mode, device=local).find_pe_pairs()
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                uid[:] = torch.frombuffer(bytearray(PDSolver.nccl_unique_id()), dtype=torch.uint8)
+            dist.broadcast(uid, 0)
+            s.comm_init(bytes(uid.tolist()), world, rank)
+            s.set_halo(*slab.halo)
+            if B is None:
+                lp = s.pairs()
+                own = int(((lp[:, 0] >= slab.own_elems[0]) & (lp[:, 0] < slab.own_elems[1])).sum())
+                tb = torch.tensor([own], dtype=torch.int64)
+                dist.all_reduce(tb)
+                B = int(tb.item())  # unique bonds of the whole plate
+        else:
+            s = PDSolver.from_scenario(sc, mode=mode, device=local).find_pe_pairs()
+            if B is None:
+                B = s.info()["n_bonds"]
+        v0 = sc.initial_velocity()  # cfg4's impact patch (extension); zero for the plates
+        if v0.any():
+            if slabbed:  # this slab's nodes (halo included)
+                n0 = slab.node_first * sc.dim
+                v0 = v0[n0:n0 + s.n_dof]
+            z = np.zeros(s.n_dof)
+            s.set_state(z, v0, z)
+        s.initial_acceleration(sc.load_scale(0.0))
+        s.step(sc.scales(1, W))
+        return s
+
+    t0 = time.perf_counter()
+    s = fresh()
     t_setup = time.perf_counter() - t0
     info = s.info()
-    if world == 1 and not args.force_slabs:
-        B = info["n_bonds"]
-    K, W = args.steps, args.warmup
-    v0 = sc.initial_velocity()  # cfg4's impact patch (extension); zero for the plates
-    if v0.any():
-        if world > 1 or args.force_slabs:  # this slab's nodes (halo included)
-            n0 = slab.node_first * sc.dim
-            v0 = v0[n0:n0 + s.n_dof]
-        z = np.zeros(s.n_dof)
-        s.set_state(z, v0, z)
-    s.initial_acceleration(sc.load_scale(0.0))
-    step0 = 1
-    s.step(sc.scales(step0, W))
-    step0 += W
+    step0 = W + 1
 
     def barrier():
         if dist:
@@ -314,10 +326,10 @@ def bench_native(args):
     with Clocks(local) as clk:
         barrier()
         ms = s.step_timed(sc.scales(step0, K))  # synchronises the stream on both sides
-        step0 += K
         barrier()
-        bond_ms, tot_ms = s.profile(sc.scales(step0, K))
-        step0 += K
+    del s
+    s = fresh()
+    bond_ms, tot_ms = s.profile(sc.scales(step0, K))
     if dist:
         import torch
 
@@ -350,6 +362,8 @@ def bench_native(args):
     try:
         import torch
 
+        del s
+        s = fresh()
         nd = s.n_dof
         hu = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
         hv = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()

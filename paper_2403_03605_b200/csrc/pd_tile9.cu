@@ -317,7 +317,6 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     double2* ub = reinterpret_cast<double2*>(sm + kOffUb);
     double2* gt = ub;  // G aliases the ubar apron once the force pass is done
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
-    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm + kOffPart);
     unsigned* red = reinterpret_cast<unsigned*>(sm + kOffRed);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
@@ -646,14 +645,10 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         rdo[n] = make_double2(u0 + d.dt * v0 + d.c_pred_d * a0, u1 + d.dt * v1 + d.c_pred_d * a1);
     }
 
-    if (DO_BREAK) {
-        for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
-        if (lane == 0) part[warp] = nb;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long t = 0;
-            for (int w = 0; w < NW; ++w) t += part[w];
-            if (t) atomicAdd(d.broken_count + step, t);
+    if (DO_BREAK) {  // per warp (no CTA barrier at the tail; breaks are rare)
+        if (__any_sync(0xffffffffu, nb != 0)) {
+            for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+            if (lane == 0) atomicAdd(d.broken_count + step, nb);
         }
     }
 }
