@@ -323,4 +323,113 @@ void lattice_configure(int dim, int R, int S) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
+// ---- lattice encoding of device-resident ELL families (fast mode setup) ----
+// The generated mesh numbers element (i, j, k) as (k ny + j) nx + i
+// (mesh.hpp:170-219), so every family entry is an integer offset.  These two
+// passes replace the host walk over all F entries: the first collects the
+// offsets present (and the largest component), the host orders them into the
+// stencil (a few hundred at most), the second writes each element's intact bits.
+namespace {
+constexpr int kSpan17 = 17, kKeys17 = 17 * 17 * 17;
+__device__ __forceinline__ void lat_ijk(int e, int nx, int ny, int& i, int& j, int& k) {
+    i = e % nx;
+    const int r = e / nx;
+    j = r % ny;
+    k = r / ny;
+}
+
+__global__ void k_lat_scan(const int32_t* __restrict__ col, int E, int K, int nx, int ny,
+                           int* __restrict__ present, int* __restrict__ rmax) {
+    int lr = 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        int a, b, c;
+        lat_ijk(e, nx, ny, a, b, c);
+        for (int q = 0; q < K; ++q) {
+            const int p = col[(size_t)q * E + e];
+            if (p < 0) break;
+            int x, y, z;
+            lat_ijk(p, nx, ny, x, y, z);
+            const int di = x - a, dj = y - b, dk = z - c;
+            const int m = max(abs(di), max(abs(dj), abs(dk)));
+            lr = max(lr, m);
+            if (m <= 8) {
+                const int key = ((dk + 8) * kSpan17 + dj + 8) * kSpan17 + di + 8;
+                if (!present[key]) present[key] = 1;  // every writer stores 1
+            }
+        }
+    }
+    lr = __reduce_max_sync(0xffffffffu, lr);
+    if ((threadIdx.x & 31) == 0 && lr) atomicMax(rmax, lr);
+}
+
+__global__ void k_lat_mask(const int32_t* __restrict__ col, int E, int K, int nx, int ny,
+                           const int* __restrict__ slot17, int W, uint32_t* __restrict__ mask,
+                           unsigned long long* __restrict__ count) {
+    __shared__ int sl[kKeys17];
+    for (int i = threadIdx.x; i < kKeys17; i += blockDim.x) sl[i] = slot17[i];
+    __syncthreads();
+    unsigned long long cnt = 0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        int a, b, c;
+        lat_ijk(e, nx, ny, a, b, c);
+        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        for (int q = 0; q < K; ++q) {
+            const int p = col[(size_t)q * E + e];
+            if (p < 0) break;
+            int x, y, z;
+            lat_ijk(p, nx, ny, x, y, z);
+            const int sidx = sl[((z - c + 8) * kSpan17 + y - b + 8) * kSpan17 + x - a + 8];
+            const uint32_t bit = 1u << (sidx & 31);
+            const int w = sidx >> 5;
+            m0 |= w == 0 ? bit : 0u;
+            m1 |= w == 1 ? bit : 0u;
+            m2 |= w == 2 ? bit : 0u;
+            m3 |= w == 3 ? bit : 0u;
+            ++cnt;
+        }
+        mask[e] = m0;
+        if (W > 1) mask[(size_t)E + e] = m1;
+        if (W > 2) mask[2 * (size_t)E + e] = m2;
+        if (W > 3) mask[3 * (size_t)E + e] = m3;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(count, cnt);
+}
+}  // namespace
+
+int lattice_scan_device(const int32_t* d_col, int E, int K, int nx, int ny, int* present17,
+                        cudaStream_t s) {
+    int* dp = nullptr;
+    int* dr = nullptr;
+    cudaMallocAsync(&dp, sizeof(int) * (kKeys17 + 1), s);
+    dr = dp + kKeys17;
+    cudaMemsetAsync(dp, 0, sizeof(int) * (kKeys17 + 1), s);
+    k_lat_scan<<<1184, 256, 0, s>>>(d_col, E, K, nx, ny, dp, dr);
+    int R = 0;
+    cudaMemcpyAsync(present17, dp, sizeof(int) * kKeys17, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&R, dr, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(dp, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    return R;
+}
+
+long long lattice_mask_device(const int32_t* d_col, int E, int K, int nx, int ny,
+                              const int* slot17, int W, uint32_t* d_mask, cudaStream_t s) {
+    int* ds = nullptr;
+    unsigned long long* dc = nullptr;
+    cudaMallocAsync(&ds, sizeof(int) * kKeys17, s);
+    cudaMallocAsync(&dc, sizeof(unsigned long long), s);
+    cudaMemcpyAsync(ds, slot17, sizeof(int) * kKeys17, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(dc, 0, sizeof(unsigned long long), s);
+    k_lat_mask<<<1184, 256, 0, s>>>(d_col, E, K, nx, ny, ds, W, d_mask, dc);
+    unsigned long long F = 0;
+    cudaMemcpyAsync(&F, dc, sizeof(F), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(ds, s);
+    cudaFreeAsync(dc, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    return (long long)F;
+}
+
 }  // namespace pmts

@@ -130,6 +130,13 @@ void launch_strip2d_step(const DevPD& d, const LatticeDev& L, const StripStencil
                          const FusedBufs& b, int step, int do_break, double scale,
                          int write_state, int H, cudaStream_t s);
 
+// device lattice encoding (setup): offsets present as 17^3 flags (component + 8),
+// returns the largest |component| (> 8: not encodable); then the intact mask of
+// every element from the host-ordered slot table, returns the entry count F
+int lattice_scan_device(const int32_t* d_col, int E, int K, int nx, int ny, int* present17,
+                        cudaStream_t s);
+long long lattice_mask_device(const int32_t* d_col, int E, int K, int nx, int ny,
+                              const int* slot17, int W, uint32_t* d_mask, cudaStream_t s);
 size_t lattice_smem_bytes(int dim, int R, int S);
 void lattice_configure(int dim, int R, int S);
 struct Stencil3D;

@@ -154,7 +154,7 @@ double micromodulus(const pmts_pd_desc& dsc, int dim, double r) {
     return dsc.c0 * std::exp(-r / dsc.l);
 }
 
-bool try_lattice(pmts_pd* h);
+bool try_lattice(pmts_pd* h, const int32_t* dcol = nullptr);
 
 // ---- NCCL, resolved at run time (libpmts loads without it; the halo exchange
 // of the slab decomposition is the only user).  Types follow nccl.h 2.x.
@@ -355,10 +355,21 @@ Tile9Maps tile9_maps(const pmts_pd* h) {
     return m;
 }
 
+// host copy of the ELL families, fetched on first use when they were built and
+// encoded on the device
+void ensure_hcol(pmts_pd* h) {
+    if (!h->hcol.empty() || !h->d.col) return;
+    h->hcol.assign((size_t)h->d.K * h->E, -1);
+    download(h->hcol.data(), h->d.col, h->hcol.size(), h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+}
+
 // Stencil encoding of the families when the mesh is the generated lattice
 // (fast mode).  Returns false (ELL path stays) if any bond's offset falls
-// outside one shared stencil of <= kMaxStencil offsets.
-bool try_lattice(pmts_pd* h) {
+// outside one shared stencil of <= kMaxStencil offsets.  dcol: the families are
+// device-resident (no host copy); the offset scan and the mask run on the device
+// and the stencil constants must be the nominal ones (desc.lattice_h > 0).
+bool try_lattice(pmts_pd* h, const int32_t* dcol) {
     const int E = h->E, K = h->d.K, dim = h->dim;
     const int nx = h->desc.lattice[0], ny = h->desc.lattice[1];
     const int nz = dim == 3 ? h->desc.lattice[2] : 1;
@@ -369,34 +380,50 @@ bool try_lattice(pmts_pd* h) {
         j = (e / nx) % ny;
         k = e / (nx * ny);
     };
+    if (dcol && !(h->desc.lattice_h > 0.0)) return false;
     int R = 0;
-    for (int e = 0; e < E; ++e)
-        for (int q = 0; q < K; ++q) {
-            const int p = h->hcol[(size_t)q * E + e];
-            if (p < 0) break;
-            int a, b, c, x, y, z;
-            ijk(e, a, b, c);
-            ijk(p, x, y, z);
-            R = std::max({R, std::abs(x - a), std::abs(y - b), std::abs(z - c)});
-        }
+    std::vector<int> present17;
+    if (dcol) {
+        present17.assign(17 * 17 * 17, 0);
+        R = lattice_scan_device(dcol, E, K, nx, ny, present17.data(), h->stream);
+    } else {
+        for (int e = 0; e < E; ++e)
+            for (int q = 0; q < K; ++q) {
+                const int p = h->hcol[(size_t)q * E + e];
+                if (p < 0) break;
+                int a, b, c, x, y, z;
+                ijk(e, a, b, c);
+                ijk(p, x, y, z);
+                R = std::max({R, std::abs(x - a), std::abs(y - b), std::abs(z - c)});
+            }
+    }
     if (R == 0 || R > 8) return false;
     const int span = 2 * R + 1;
     std::vector<int> slot(span * span * span, -1);
     auto key = [&](int di, int dj, int dk) { return ((dk + R) * span + dj + R) * span + di + R; };
     std::vector<int> offs;  // keys
-    for (int e = 0; e < E; ++e)
-        for (int q = 0; q < K; ++q) {
-            const int p = h->hcol[(size_t)q * E + e];
-            if (p < 0) break;
-            int a, b, c, x, y, z;
-            ijk(e, a, b, c);
-            ijk(p, x, y, z);
-            const int kk = key(x - a, y - b, z - c);
-            if (slot[kk] < 0) {
-                slot[kk] = 0;
-                offs.push_back(kk);
-            }
+    if (dcol) {  // the device scan's offsets, in 17^3 key order
+        for (int k17 = 0; k17 < 17 * 17 * 17; ++k17) {
+            if (!present17[k17]) continue;
+            const int kk = key(k17 % 17 - 8, (k17 / 17) % 17 - 8, k17 / 289 - 8);
+            slot[kk] = 0;
+            offs.push_back(kk);
         }
+    } else {
+        for (int e = 0; e < E; ++e)
+            for (int q = 0; q < K; ++q) {
+                const int p = h->hcol[(size_t)q * E + e];
+                if (p < 0) break;
+                int a, b, c, x, y, z;
+                ijk(e, a, b, c);
+                ijk(p, x, y, z);
+                const int kk = key(x - a, y - b, z - c);
+                if (slot[kk] < 0) {
+                    slot[kk] = 0;
+                    offs.push_back(kk);
+                }
+            }
+    }
     // symmetric closure and ascending linear delta (== ascending partner id)
     auto decode = [&](int kk, int& di, int& dj, int& dk) {
         di = kk % span - R;
@@ -427,9 +454,35 @@ bool try_lattice(pmts_pd* h) {
     // evaluate bitwise-negated operands and agree on every break)
     std::vector<double> table(kTableRow * (size_t)S, 0.0);
     std::vector<char> have(S, 0);
-    std::vector<uint32_t> mask((size_t)W * E, 0u);
+    std::vector<uint32_t> mask(dcol ? 0 : (size_t)W * E, 0u);
     const double s0 = h->desc.s_crit, sl = s0 * (1.0 - h->desc.s_crit_spread);
-    for (int e = 0; e < E; ++e)
+    if (dcol) {  // nominal constants per positive offset (xi = h o, w = V^2) and its negation
+        const double hh = h->desc.lattice_h, wv = h->desc.lattice_vol * h->desc.lattice_vol;
+        for (int s = 0; s < S; ++s) {
+            if (lin(offs[s]) <= 0) continue;
+            int di, dj, dk;
+            decode(offs[s], di, dj, dk);
+            const double xi[3] = {di * hh, dj * hh, dk * hh};
+            const double x2 = xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2];
+            const double f = micromodulus(h->desc, dim, std::sqrt(x2)) * wv;
+            const int sn = slot[key(-di, -dj, -dk)];
+            const double cthr = (2.0 * s0 + s0 * s0) * x2;
+            const double clo =
+                h->desc.s_crit_spread != 0.0 ? (2.0 * sl + sl * sl) * x2 * (1.0 - 1e-12) : cthr;
+            const int xs[3] = {0, 1, 4};
+            for (int k = 0; k < 3; ++k) {
+                table[kTableRow * s + xs[k]] = xi[k];
+                table[kTableRow * sn + xs[k]] = -xi[k];
+            }
+            for (int r : {s, sn}) {
+                table[kTableRow * r + 2] = f;
+                table[kTableRow * r + 3] = cthr;
+                table[kTableRow * r + 5] = clo;
+                table[kTableRow * r + 6] = x2;
+            }
+        }
+    }
+    for (int e = 0; e < E && !dcol; ++e)
         for (int q = 0; q < K; ++q) {
             const int p = h->hcol[(size_t)q * E + e];
             if (p < 0) break;
@@ -542,7 +595,17 @@ bool try_lattice(pmts_pd* h) {
     // the stencil mask replaces the ELL mask; ELL coefficients are not needed
     h->release(h->d.mask);
     uint32_t* dmask = h->alloc<uint32_t>((size_t)W * E);
-    upload(dmask, mask.data(), (size_t)W * E, h->stream);
+    if (dcol) {
+        std::vector<int> slot17(17 * 17 * 17, -1);
+        for (int s = 0; s < S; ++s) {
+            int a, b, c;
+            decode(offs[s], a, b, c);
+            slot17[((c + 8) * 17 + b + 8) * 17 + a + 8] = s;
+        }
+        h->n_entries = lattice_mask_device(dcol, E, K, nx, ny, slot17.data(), W, dmask, h->stream);
+    } else {
+        upload(dmask, mask.data(), (size_t)W * E, h->stream);
+    }
     h->d.mask = dmask;
     h->d.W = W;
     h->release((void*)h->d.coef);
@@ -699,6 +762,7 @@ bool try_lattice(pmts_pd* h) {
 
 // ELL-layout intact mask (bit k = k-th family entry) from the stencil mask
 std::vector<uint32_t> ell_mask_host(pmts_pd* h) {
+    ensure_hcol(h);
     const int E = h->E, K = h->d.K;
     std::vector<uint32_t> m((size_t)h->d.W * E);
     download(m.data(), h->d.mask, m.size(), h->stream);
@@ -996,10 +1060,35 @@ int pmts_pd_build_families(pmts_pd* h) {
         FamilyBuild fb = build_families_device(
             h->dim, h->E, h->d.cen, h->lo, h->desc.delta, h->eps, (int)h->notch_npts.size(),
             h->notch_npts.data(), h->notch_pts.data(), h->stream);
+        // fast mode on the generated lattice with nominal constants: the families stay
+        // on the device and are encoded there (no host walk over the F entries; the
+        // host copy is fetched only if a caller asks for pairs / intact states)
+        if (h->mode == PMTS_FAST && h->desc.lattice_h > 0.0 && !std::getenv("PMTS_HOST_ENCODE")) {
+            if (h->d.coef) h->release((void*)h->d.coef);
+            if (h->d.mask) h->release(h->d.mask);
+            if (h->d.col) h->release((void*)h->d.col);
+            h->d.coef = nullptr;
+            h->d.mask = nullptr;
+            h->owned.push_back(fb.col);
+            h->device_bytes += 4.0 * fb.K * (double)h->E;
+            h->d.col = fb.col;
+            h->d.K = fb.K;
+            h->hcol.clear();
+            h->families = true;
+            h->lattice = false;
+            if (try_lattice(h, fb.col)) return;
+            // not encodable: the host path below (it re-uploads the families)
+            h->families = false;
+        }
         h->hcol.assign((size_t)fb.K * h->E, -1);
         download(h->hcol.data(), fb.col, (size_t)fb.K * h->E, h->stream);
         CK(cudaStreamSynchronize(h->stream));
-        cudaFree(fb.col);
+        if (h->d.col == fb.col) {
+            h->release(fb.col);
+            h->d.col = nullptr;
+        } else {
+            cudaFree(fb.col);
+        }
         finish_families(h, fb.K);
     });
 }
@@ -1042,6 +1131,7 @@ cudaStream_t pd_internal_stream(pmts_pd* h) { return h->stream; }
 // reference's f = coeff * qp.weight * micromodulus (perifem.hpp:247)
 void pd_internal_pair_weights(pmts_pd* h, const double* w) {
     require_families(h);
+    ensure_hcol(h);
     const int E = h->E, K = h->d.K;
     std::vector<int64_t> first(E + 1, 0);
     for (int e = 0; e < E; ++e) {
@@ -1082,6 +1172,7 @@ extern "C" {
 int pmts_pd_get_pairs(pmts_pd* h, int32_t* out, int64_t cap, int64_t* n_out) {
     return guard([&] {
         require_families(h);
+        ensure_hcol(h);
         const int E = h->E, K = h->d.K;
         int64_t n = 0;
         for (int e = 0; e < E; ++e)
@@ -1102,6 +1193,7 @@ int pmts_pd_get_pairs(pmts_pd* h, int32_t* out, int64_t cap, int64_t* n_out) {
 int pmts_pd_get_intact(pmts_pd* h, uint8_t* out, int64_t cap) {
     return guard([&] {
         require_families(h);
+        ensure_hcol(h);
         const int E = h->E, K = h->d.K;
         const std::vector<uint32_t> mask = ell_mask_host(h);
         int64_t n = 0;
