@@ -28,6 +28,7 @@ SOURCES = [
     ("pd_tma2d.cu", []),
     ("pd_tile9.cu", []),
     ("pd_lat3.cu", []),
+    ("pd_setup.cu", ["-fmad=false"]),
     ("pmts_pd.cu", ["-fmad=false"]),
     ("pd_mts.cu", ["-fmad=false"]),
     ("pmts_mts.cu", ["-fmad=false"]),

@@ -55,4 +55,18 @@ void corner_gradient(int dim, const double* xi, int a, double* g);
 double shape_value(int dim, const double* xi, int a);
 double jacobian_det(int dim, const int32_t* en, const double* nodes, const double* xi);
 
+// Device restatement of the generated-mesh setup (pd_setup.cu), bitwise equal to
+// the host one; used when a CUDA device is present (PMTS_HOST_SETUP=1: host).
+#include <vector>
+struct DeviceSetup;
+bool device_available();
+DeviceSetup* setup_device_begin(int dim, const int n[3], const double lo[3], double spacing,
+                                double rho, std::vector<double>& nodes,
+                                std::vector<int32_t>& conn, std::vector<double>& centroid,
+                                std::vector<double>& volume);
+// boxes: n_patch x (lo[3] hi[3] value[3]) in the host loop's patch order
+void setup_device_loads(DeviceSetup* ds, const double body[3], int n_patch, const double* boxes,
+                        std::vector<double>& mass, std::vector<double>& p_ext);
+void setup_device_end(DeviceSetup* ds);
+
 }  // namespace pmts

@@ -22,6 +22,12 @@
 
 #include "pd_common.cuh"
 #include "pd_stencil.cuh"
+
+namespace pmts {
+// compute_element_geometry on the device (pd_setup.cu)
+void element_geometry_device(int dim, int n_elems, int n_nodes, const int32_t* conn,
+                             const double* nodes, double* centroid, double* volume, cudaStream_t s);
+}
 #include "pmts_internal.h"
 
 using namespace pmts;
@@ -940,7 +946,14 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         // geometry (mesh.hpp:112-139), host restatement, bit-exact
         h->cen.resize(3 * (size_t)E);
         h->vol.resize(E);
-        element_geometry(dim, E, h->conn.data(), ds.node_xyz, h->cen.data(), h->vol.data());
+        // compute_element_geometry on the device (pd_setup.cu, bitwise the host's)
+        {
+            cudaStream_t gs = nullptr;
+            CK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+            element_geometry_device(dim, E, N, h->conn.data(), ds.node_xyz, h->cen.data(),
+                                    h->vol.data(), gs);
+            CK(cudaStreamDestroy(gs));
+        }
         h->cl = char_length(dim, E, h->vol.data());
         h->eps = 1e-12 * std::max(h->cl, 1e-300);  // mesh.hpp:435
         for (int k = 0; k < 3; ++k) h->lo[k] = 1e300;

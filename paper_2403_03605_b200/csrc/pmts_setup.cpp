@@ -6,6 +6,7 @@
 // bit-identical to the reference's; tests/test_setup_*.py pin that against the
 // reference's own dumps.  Citations: /root/reference/proj/include/perimts/.
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <cmath>
 #include <map>
@@ -229,7 +230,33 @@ void generate(pmts_scenario& s, const pmts_scenario_desc& d) {
 }
 
 void build(pmts_scenario& s, const pmts_scenario_desc& d) {
-    generate(s, d);
+    // geometry and lumped masses on the device when one is present (pd_setup.cu,
+    // bitwise the host restatement's values); the host loops otherwise
+    DeviceSetup* dev = nullptr;
+    struct DevGuard {
+        DeviceSetup*& p;
+        ~DevGuard() {
+            if (p) setup_device_end(p);
+        }
+    } dev_guard{dev};
+    if (!std::getenv("PMTS_HOST_SETUP") && device_available()) {
+        if (d.spacing <= 0.0) throw ConfigError("mesh spacing must be positive");
+        if (d.dim != 2 && d.dim != 3) throw ConfigError("mesh dimension must be 2 or 3");
+        s.dim = d.dim;
+        for (int k = 0; k < d.dim; ++k) {
+            const double len = d.hi[k] - d.lo[k];
+            if (len <= 0.0) throw ConfigError("degenerate extent along an axis");
+            const double cells = len / d.spacing;
+            const double rounded = std::round(cells);
+            if (std::abs(cells - rounded) > 1e-9 * std::max(1.0, cells) || rounded < 1.0)
+                throw ConfigError("extent along an axis is not a multiple of the spacing");
+            s.n[k] = static_cast<int>(rounded);
+        }
+        dev = setup_device_begin(d.dim, s.n, d.lo, d.spacing, d.rho, s.nodes, s.conn, s.centroid,
+                                 s.volume);
+    } else {
+        generate(s, d);
+    }
     const int dim = s.dim, nn = dim == 2 ? 4 : 8;
     const int N = int(s.nodes.size() / 3), E = int(s.volume.size());
     s.cl = char_length(dim, E, s.volume.data());
@@ -298,10 +325,20 @@ void build(pmts_scenario& s, const pmts_scenario_desc& d) {
     }
     // M and P_ext (perifem.hpp:331-348) with w = 1 - alpha = 1
     const std::size_t nd = std::size_t(N) * dim;
-    s.mass.assign(nd, 0.0);
-    s.p_ext.assign(nd, 0.0);
+    if (dev) {
+        std::vector<double> boxes;
+        for (std::size_t p = 0; p < patch_box.size(); ++p) {
+            for (int k = 0; k < 3; ++k) boxes.push_back(patch_box[p].lo[k]);
+            for (int k = 0; k < 3; ++k) boxes.push_back(patch_box[p].hi[k]);
+            for (int k = 0; k < 3; ++k) boxes.push_back(patch_val[p][k]);
+        }
+        setup_device_loads(dev, d.body_force, int(patch_box.size()), boxes.data(), s.mass, s.p_ext);
+    } else {
+        s.mass.assign(nd, 0.0);
+        s.p_ext.assign(nd, 0.0);
+    }
     const double g = 1.0 / std::sqrt(3.0);
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < E && !dev; ++e) {
         const int32_t* en = s.conn.data() + std::size_t(e) * nn;
         const double w = 1.0 - 0.0;
         // lumped_mass (fem.hpp:172-179) over gauss_points (fem.hpp:101-115)
