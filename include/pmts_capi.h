@@ -259,6 +259,11 @@ typedef struct {
     int32_t enforce_continuity;  /* run.enforce_continuity */
     int32_t track_energy;        /* output.energy */
     int32_t device;              /* CUDA ordinal */
+    double fe_spacing;           /* > 0: non-matching FE lattice of this spacing over the
+                                    domain, PD lattice (scenario spacing) over the PD boxes'
+                                    hull, coupling rows interpolating the FE velocity at the
+                                    PD overlap nodes (extension); 0: the
+                                    reference's single conforming mesh */
 } pmts_mts_desc;
 
 typedef struct {
@@ -289,6 +294,14 @@ typedef struct {
     const int32_t* elem_nodes;   /* [n_elems][2^dim] */
     const double* node_alpha;    /* [n_nodes] blend weight at the node (output sampling,
                                     driver_run.hpp:24-35) */
+    /* G_FE rows as CSR (one weight-1 entry per row on a conforming mesh) */
+    int64_t cpl_fe_nnz;
+    const int32_t* cpl_fe_rowptr;  /* [n_lambda + 1] */
+    const int32_t* cpl_fe_col;     /* FE dofs */
+    const double* cpl_fe_w;        /* shape-function weights */
+    /* non-matching meshes: elements [0, fe_mesh_elems) / nodes [0, fe_mesh_nodes) are
+       the FE lattice, the rest the PD lattice; -1 on a conforming mesh */
+    int32_t fe_mesh_elems, fe_mesh_nodes;
 } pmts_mts_view;
 
 typedef struct {                 /* MacroReport (mts.hpp:41-63) */

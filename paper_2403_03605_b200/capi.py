@@ -79,7 +79,7 @@ class MtsDesc(C.Structure):
     _fields_ = [("scenario", C.POINTER(ScenarioDesc)), ("n_pd_box", _I), ("pd_boxes", _P),
                 ("overlap_width_factor", _D), ("weight_kind", _I), ("gamma_fe", _D),
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
-                ("track_energy", _I), ("device", _I)]
+                ("track_energy", _I), ("device", _I), ("fe_spacing", _D)]
 
 
 class MtsView(C.Structure):
@@ -92,7 +92,9 @@ class MtsView(C.Structure):
                 ("fe_k_val", _P), ("fe_mass", _P), ("fe_p_ext", _P), ("pd_mass", _P),
                 ("pd_p_ext", _P), ("fe_bc_dofs", _P), ("fe_bc_vel", _P), ("pd_bc_dofs", _P),
                 ("pd_bc_vel", _P), ("cpl_fe_dof", _P), ("cpl_pd_dof", _P), ("pairs", _P),
-                ("pe_weight", _P), ("node_xyz", _P), ("elem_nodes", _P), ("node_alpha", _P)]
+                ("pe_weight", _P), ("node_xyz", _P), ("elem_nodes", _P), ("node_alpha", _P),
+                ("cpl_fe_nnz", C.c_int64), ("cpl_fe_rowptr", _P), ("cpl_fe_col", _P),
+                ("cpl_fe_w", _P), ("fe_mesh_elems", _I), ("fe_mesh_nodes", _I)]
 
 
 class MtsReport(C.Structure):

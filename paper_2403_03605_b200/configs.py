@@ -225,6 +225,34 @@ def scenarios() -> dict:
             "ext": {},
         }
         s[tag] = c2
+    # BASELINE cfg2 as written (non-matching meshes, an extension -- DESIGN.md 11): the
+    # PD band at 0.25 mm, FE elsewhere on a 1 mm lattice, explicit central-difference
+    # FE (beta_fe = 0, dt_fe = 100 ns < the 1 mm CFL limit), 2 mm linear gluing zones
+    nm = copy.deepcopy(s["cfg2"])
+    nm["mesh"]["fe_spacing"] = 1e-3
+    nm["time"]["beta_fe"] = 0.0
+    s["cfg2_nm"] = nm
+    # convergence family for the non-matching coupling: a 30 x 10 mm strip, PD at
+    # 0.25 mm in the middle third, 2 mm gluing zones, explicit FE, traction on the
+    # top face (FE and PD parts loaded at once), bottom face fixed;
+    # mesh.fe_spacing in {0.25, 0.5, 1} mm (tests)
+    cv = {
+        "mesh": {"kind": "generated", "dim": 2, "bounds": [0.0, 0.0, 0.03, 0.01],
+                 "spacing": 2.5e-4, "notch1": None, "fe_spacing": 1e-3},
+        "material": {"E": _E, "nu": 0.3333333333333333, "rho": _RHO,
+                     "formulation": "plane_stress"},
+        "pd": {"delta_factor": 3.015, "l_factor": 1.0, "s_crit": 0.0},
+        "region": {"pd_box1": [0.01, 0.0, 0.02, 0.01], "overlap_width_factor": 8.0,
+                   "weight_kind": "linear"},
+        "load": {"traction1": [-0.001, 0.01 - 1e-7, 0.031, 0.01 + 1e-7, 0.0, 40e6],
+                 "fixed1": [-0.001, -1e-7, 0.031, 1e-7]},
+        "time": {"dt_pd": 1e-8, "m": 2, "total_time": 1e-8 * 2 * 40, "gamma_fe": 0.5,
+                 "beta_fe": 0.0, "gamma_pd": 0.5, "beta_pd": 0.0},
+        "run": {"mode": "coupled_mts", "interface": "auto"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+    s["mts_nm_strip"] = cv
     return s
 
 

@@ -118,6 +118,30 @@ __global__ void k_gather(int n, const int32_t* idx, const double* src, double* d
     if (r < n) dst[r] = src[idx[r]];
 }
 
+// G_FE with interpolation rows (non-matching meshes): out[r] = sum_j w_j x[ci_j],
+// the first term alone when the row has one entry (the conforming map: bitwise
+// the plain gather)
+__global__ void k_gather_csr(int n, const int32_t* rp, const int32_t* ci, const double* w,
+                             const double* src, double* dst) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int j = rp[r];
+    double acc = w[j] * src[ci[j]];
+    for (++j; j < rp[r + 1]; ++j) acc += w[j] * src[ci[j]];
+    dst[r] = acc;
+}
+// dst[d] += sum over the rows of d (ascending) of w vals[row]: G_FE^T vals on the
+// touched dofs (td) through the transposed CSR (trp / tri / tw)
+__global__ void k_scatter_csr(int nt, const int32_t* td, const int32_t* trp, const int32_t* tri,
+                              const double* tw, const double* vals, double* dst) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nt) return;
+    int j = trp[q];
+    double acc = tw[j] * vals[tri[j]];
+    for (++j; j < trp[q + 1]; ++j) acc += tw[j] * vals[tri[j]];
+    dst[td[q]] += acc;
+}
+
 __global__ void k_add(int n, const double* x, double* y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] = y[i] + x[i];
@@ -553,6 +577,18 @@ void scatter_add(int n, const int32_t* idx, const double* vals, double* dst, cud
     if (n <= 0) return;
     k_scatter_add<<<blocks(n), kT, 0, s>>>(n, idx, vals, dst);
     check("scatter_add");
+}
+void gather_csr(int n, const int32_t* rp, const int32_t* ci, const double* w, const double* src,
+                double* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    k_gather_csr<<<blocks(n), kT, 0, s>>>(n, rp, ci, w, src, dst);
+    check("gather_csr");
+}
+void scatter_csr(int nt, const int32_t* td, const int32_t* trp, const int32_t* tri,
+                 const double* tw, const double* vals, double* dst, cudaStream_t s) {
+    if (nt <= 0) return;
+    k_scatter_csr<<<blocks(nt), kT, 0, s>>>(nt, td, trp, tri, tw, vals, dst);
+    check("scatter_csr");
 }
 void gather(int n, const int32_t* idx, const double* src, double* dst, cudaStream_t s) {
     if (n <= 0) return;

@@ -50,6 +50,10 @@ void init_acc(int n, const double* p, const double* ku, const double* M, const u
               double* a, cudaStream_t s);
 void scatter_add(int n, const int32_t* idx, const double* vals, double* dst, cudaStream_t s);
 void gather(int n, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+void gather_csr(int n, const int32_t* rp, const int32_t* ci, const double* w, const double* src,
+                double* dst, cudaStream_t s);
+void scatter_csr(int nt, const int32_t* td, const int32_t* trp, const int32_t* tri,
+                 const double* tw, const double* vals, double* dst, cudaStream_t s);
 void scale(int n, const double* x, double sc, double* y, cudaStream_t s);
 void add(int n, const double* x, double* y, cudaStream_t s);  // y += x
 void add_states(int n, const double* a0, const double* a1, const double* a2, const double* b0,

@@ -220,6 +220,39 @@ __global__ void k_geometry(int dim, long long E, const int32_t* __restrict__ con
     }
 }
 
+// volumes only (compute_element_geometry's sum), for Mesh::char_length of a lattice
+__global__ void k_volumes(Grid g, double* __restrict__ vol) {
+    const int nn = g.dim == 2 ? 4 : 8;
+    const long long E = (long long)g.nx * g.ny * (g.dim == 3 ? g.nz : 1);
+    const double gp = 1.0 / sqrt(3.0);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % g.nx), j = (int)((e / g.nx) % g.ny),
+                  k = (int)(e / ((long long)g.nx * g.ny));
+        double p[8][3];
+        const int ii[8] = {i, i + 1, i + 1, i, i, i + 1, i + 1, i};
+        const int jj[8] = {j, j, j + 1, j + 1, j, j, j + 1, j + 1};
+        for (int a = 0; a < nn; ++a) {
+            const int kk = a >= 4 ? k + 1 : k;
+            p[a][0] = g.lo[0] + ii[a] * g.h;
+            p[a][1] = g.lo[1] + jj[a] * g.h;
+            p[a][2] = g.dim == 3 ? g.lo[2] + kk * g.h : 0.0;
+        }
+        double v = 0.0;
+        for (int q = 0; q < (g.dim == 2 ? 4 : 8); ++q) {
+            const double xi[3] = {(q & 1) ? gp : -gp, (q & 2) ? gp : -gp, (q & 4) ? gp : -gp};
+            v += d_jacobian_det(g.dim, p, xi);
+        }
+        vol[e] = v;
+    }
+}
+// the reference's serial sum (mesh.hpp:51-57)
+__global__ void k_serial_sum(long long n, const double* __restrict__ x, double* out) {
+    double v = 0.0;
+    for (long long i = 0; i < n; ++i) v += x[i];
+    *out = v;
+}
+
 void ck(cudaError_t e) {
     if (e != cudaSuccess) throw InternalError(std::string("CUDA: ") + cudaGetErrorString(e));
 }
@@ -328,6 +361,29 @@ void setup_device_loads(DeviceSetup* ds, const double body[3], int n_patch, cons
 }
 
 void setup_device_end(DeviceSetup* ds) { delete ds; }
+
+double lattice_volume_sum_device(int dim, const int n[3], const double lo[3], double spacing) {
+    Grid g{};
+    g.dim = dim;
+    g.nx = n[0];
+    g.ny = n[1];
+    g.nz = dim == 3 ? n[2] : 1;
+    for (int k = 0; k < 3; ++k) g.lo[k] = lo[k];
+    g.h = spacing;
+    const size_t E = (size_t)g.nx * g.ny * g.nz;
+    cudaStream_t s = nullptr;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double* vol = dmalloc<double>(E + 1, s);
+    k_volumes<<<1184, 128, 0, s>>>(g, vol);
+    k_serial_sum<<<1, 1, 0, s>>>((long long)E, vol, vol + E);
+    ck(cudaGetLastError());
+    double sum = 0.0;
+    ck(cudaMemcpyAsync(&sum, vol + E, sizeof(double), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(vol, s);
+    ck(cudaStreamSynchronize(s));
+    ck(cudaStreamDestroy(s));
+    return sum;
+}
 
 void element_geometry_device(int dim, int n_elems, int n_nodes, const int32_t* conn,
                              const double* nodes, double* centroid, double* volume,

@@ -48,6 +48,7 @@ int guard(F&& f) {
 void element_geometry(int dim, int n_elems, const int32_t* conn, const double* nodes,
                       double* centroid, double* volume);
 double char_length(int dim, int n_elems, const double* volume);
+double lattice_char_length(int dim, const int n[3], const double lo[3], double h);
 double calibrate_c0(double E, double delta, double l, int formulation);
 // reference_shape gradients / values (fem.hpp:22-47) and the Jacobian
 // determinant of shape_and_gradients (fem.hpp:51-79); nodes are xyz triples
@@ -68,5 +69,8 @@ DeviceSetup* setup_device_begin(int dim, const int n[3], const double lo[3], dou
 void setup_device_loads(DeviceSetup* ds, const double body[3], int n_patch, const double* boxes,
                         std::vector<double>& mass, std::vector<double>& p_ext);
 void setup_device_end(DeviceSetup* ds);
+// sum of the element volumes of a generated lattice in element order (the first
+// half of Mesh::char_length, mesh.hpp:51-57), computed on the device
+double lattice_volume_sum_device(int dim, const int n[3], const double lo[3], double spacing);
 
 }  // namespace pmts

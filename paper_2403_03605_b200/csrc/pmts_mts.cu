@@ -164,6 +164,11 @@ struct pmts_mts {
     int counts_cap = 0;
     // device: coupling
     int32_t *cfe = nullptr, *cpd = nullptr;
+    // G_FE rows (CSR) and their transpose over the touched FE dofs
+    int32_t *gfe_rp = nullptr, *gfe_ci = nullptr, *gft_d = nullptr, *gft_rp = nullptr,
+            *gft_ri = nullptr;
+    double *gfe_w = nullptr, *gft_w = nullptr;
+    int gft_n = 0;
     // device: states and scratch
     DState ufe, upd, vfe, vpd, wst, yst, fe_prev;
     double *rd = nullptr, *rv = nullptr, *ra = nullptr, *kd = nullptr;     // size max(nf, np)
@@ -393,8 +398,13 @@ struct pmts_mts {
 
     // ---- coupling (coupling.hpp:46-68) ----
     std::vector<double> gather_fe(const double* x) {
-        mtsk::gather(nl, cfe, x, gvec, stream);
+        mtsk::gather_csr(nl, gfe_rp, gfe_ci, gfe_w, x, gvec, stream);
         return to_host(gvec, nl);
+    }
+    // dst += G_FE^T vals (host vals, uploaded)
+    void add_gt_fe(const std::vector<double>& vals, double* dst) {
+        to_dev(lam_tmp, vals);
+        mtsk::scatter_csr(gft_n, gft_d, gft_rp, gft_ri, gft_w, lam_tmp, dst, stream);
     }
     std::vector<double> gather_pd(const double* x) {
         mtsk::gather(nl, cpd, x, gvec, stream);
@@ -413,9 +423,12 @@ struct pmts_mts {
         zero_vec(ra, nf);
         zero_vec(rv, nf);
         zero_vec(rd, nf);
-        const double m1 = -1.0;
-        CKM(cudaMemcpyAsync(ra + s.cpl_fe[k], &m1, sizeof(double), cudaMemcpyHostToDevice, stream));
-        CKM(cudaStreamSynchronize(stream));
+        for (int j = s.cpl_fe_rp[k]; j < s.cpl_fe_rp[k + 1]; ++j) {
+            const double mw = -s.cpl_fe_w[j];
+            CKM(cudaMemcpyAsync(ra + s.cpl_fe_ci[j], &mw, sizeof(double), cudaMemcpyHostToDevice,
+                                stream));
+            CKM(cudaStreamSynchronize(stream));
+        }
         fe_solve(ra, 1.0, rv, rd, nullptr, nullptr, true, y);
     }
     void unit_pd_column(int k, const DState& y) {
@@ -503,7 +516,7 @@ struct pmts_mts {
     void initialize_accelerations() {
         // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
         mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
-        add_gt(cfe, scaled(lambda_prev, -1.0), ra);
+        add_gt_fe(scaled(lambda_prev, -1.0), ra);
         fe_K(ufe.u, kd);
         mtsk::init_acc(nf, ra, kd, fe_M, fe_cf, ufe.a, stream);
         mtsk::scale(np, pd_P, load_scale(t), ra, stream);
@@ -636,7 +649,7 @@ pmts_mts_report pmts_mts::macro_step() {
         zero_vec(ra, nf);
         zero_vec(rv, nf);
         zero_vec(rd, nf);
-        add_gt(cfe, scaled(lambda, -1.0), ra);
+        add_gt_fe(scaled(lambda, -1.0), ra);
         fe_solve(ra, 1.0, rv, rd, warm_fe_link, &warm_link_ok, true, wst);
         mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst.u, wst.v, wst.a, ufe.u, ufe.v, ufe.a, stream);
     }
@@ -730,36 +743,123 @@ pmts_mts_report pmts_mts::macro_step() {
 
 namespace {
 
+// a lattice without loads (tractions stay surface loads here) over [lo, hi]
+pmts_scenario* mts_lattice(const pmts_scenario_desc& sd, const double* lo, const double* hi,
+                           double spacing) {
+    pmts_scenario_desc g = sd;
+    g.n_traction = 0;
+    g.n_body_patch = 0;
+    g.n_velocity_bc = 0;
+    g.n_fixed = 0;
+    for (int k = 0; k < 3; ++k) {
+        g.lo[k] = lo[k];
+        g.hi[k] = hi[k];
+    }
+    g.spacing = spacing;
+    pmts_scenario* sc = nullptr;
+    check_pd(pmts_scenario_build(&g, &sc));
+    return sc;
+}
+
 void build_host(pmts_mts& h, const pmts_mts_desc& d) {
     const pmts_scenario_desc& sd = *d.scenario;
     MtsSystem& s = h.s;
     // mesh + geometry + material: the pure-PD scenario builder's generator
-    pmts_scenario* sc = nullptr;
-    {
-        // build a scenario without loads (tractions stay surface loads here)
-        pmts_scenario_desc g = sd;
-        g.n_traction = 0;
-        g.n_body_patch = 0;
-        g.n_velocity_bc = 0;
-        g.n_fixed = 0;
-        check_pd(pmts_scenario_build(&g, &sc));
+    if (sd.dim != 2 && sd.dim != 3) throw ConfigError("mesh dimension must be 2 or 3");
+    s.dim = sd.dim;
+    const int nn = sd.dim == 2 ? 4 : 8;
+    if (d.fe_spacing > 0.0) {
+        // non-matching meshes (extension): the FE lattice over the domain, the PD
+        // lattice (the scenario spacing, which sets delta) over the PD boxes' hull
+        const double ratio = d.fe_spacing / sd.spacing;
+        const int r = int(std::lround(ratio));
+        if (r < 1 || std::abs(ratio - r) > 1e-9 * ratio)
+            throw ConfigError("fe_spacing must be an integer multiple of the PD spacing");
+        double hlo[3] = {0, 0, 0}, hhi[3] = {0, 0, 0};
+        for (int k = 0; k < sd.dim; ++k) {
+            hlo[k] = 1e300;
+            hhi[k] = -1e300;
+            for (int b = 0; b < d.n_pd_box; ++b) {
+                hlo[k] = std::min(hlo[k], std::max(sd.lo[k], d.pd_boxes[6 * b + k]));
+                hhi[k] = std::min(sd.hi[k], std::max(hhi[k], d.pd_boxes[6 * b + 3 + k]));
+            }
+            for (double x : {hlo[k], hhi[k]}) {
+                const double c = (x - sd.lo[k]) / d.fe_spacing;
+                if (std::abs(c - std::round(c)) > 1e-9 * std::max(1.0, c))
+                    throw ConfigError("non-matching coupling: the PD boxes' hull must lie on "
+                                      "FE lattice lines");
+            }
+        }
+        pmts_scenario* fe = mts_lattice(sd, sd.lo, sd.hi, d.fe_spacing);
+        pmts_scenario* pd = mts_lattice(sd, hlo, hhi, sd.spacing);
+        pmts_scenario_view vf{}, vp{};
+        pmts_scenario_get(fe, &vf);
+        pmts_scenario_get(pd, &vp);
+        for (int k = 0; k < 3; ++k) {
+            s.n[k] = vp.lattice[k];
+            s.fe_n[k] = vf.lattice[k];
+            s.pd_n[k] = vp.lattice[k];
+            s.fe_lo[k] = sd.lo[k];
+            s.pd_lo[k] = hlo[k];
+        }
+        s.fe_h = d.fe_spacing;
+        s.pd_h = sd.spacing;
+        s.fe_ratio = r;
+        s.fe_mesh_elems = vf.n_elems;
+        s.fe_mesh_nodes = vf.n_nodes;
+        s.nodes.assign(vf.node_xyz, vf.node_xyz + 3 * (size_t)vf.n_nodes);
+        // PD nodes on the global PD lattice: lo + (offset + i) h, bitwise the nodes
+        // a conforming mesh of the PD spacing has there
+        const int pnx = vp.lattice[0] + 1, pny = vp.lattice[1] + 1;
+        long long off[3] = {0, 0, 0};
+        for (int k = 0; k < sd.dim; ++k) off[k] = std::llround((hlo[k] - sd.lo[k]) / sd.spacing);
+        std::vector<double> pxyz(3 * (size_t)vp.n_nodes);
+        for (int q = 0; q < vp.n_nodes; ++q) {
+            const long long ix[3] = {q % pnx, (q / pnx) % pny, q / ((long long)pnx * pny)};
+            for (int k = 0; k < 3; ++k)
+                pxyz[3 * (size_t)q + k] = k < sd.dim ? sd.lo[k] + (off[k] + ix[k]) * sd.spacing : 0.0;
+        }
+        std::vector<double> pcen(3 * (size_t)vp.n_elems), pvol(vp.n_elems);
+        element_geometry(sd.dim, vp.n_elems, vp.elem_nodes, pxyz.data(), pcen.data(), pvol.data());
+        s.nodes.insert(s.nodes.end(), pxyz.begin(), pxyz.end());
+        s.conn.assign(vf.elem_nodes, vf.elem_nodes + (size_t)nn * vf.n_elems);
+        for (size_t q = 0; q < (size_t)nn * vp.n_elems; ++q)
+            s.conn.push_back(vp.elem_nodes[q] + vf.n_nodes);
+        s.centroid.assign(vf.centroid, vf.centroid + 3 * (size_t)vf.n_elems);
+        s.centroid.insert(s.centroid.end(), pcen.begin(), pcen.end());
+        s.volume.assign(vf.volume, vf.volume + vf.n_elems);
+        s.volume.insert(s.volume.end(), pvol.begin(), pvol.end());
+        // the horizon and the overlap width follow the PD lattice: the char length a
+        // conforming mesh of the PD spacing over the domain has (build_scenario,
+        // driver.hpp:179-186), so a unit ratio rebuilds the reference's model bitwise
+        int nfull[3] = {1, 1, 1};
+        for (int k = 0; k < sd.dim; ++k)
+            nfull[k] = int(std::lround((sd.hi[k] - sd.lo[k]) / sd.spacing));
+        s.cl = lattice_char_length(sd.dim, nfull, sd.lo, sd.spacing);
+        s.delta = sd.delta_factor * s.cl;
+        s.l = s.delta / sd.l_factor;
+        s.c0 = calibrate_c0(sd.E, s.delta, s.l, sd.formulation);
+        s.ramp = vp.load_ramp;
+        for (int k = 0; k < 3; ++k) s.pd_lo[k] = k < sd.dim ? sd.lo[k] + off[k] * sd.spacing : 0.0;
+        pmts_scenario_destroy(fe);
+        pmts_scenario_destroy(pd);
+    } else {
+        pmts_scenario* sc = mts_lattice(sd, sd.lo, sd.hi, sd.spacing);
+        pmts_scenario_view v{};
+        pmts_scenario_get(sc, &v);
+        for (int k = 0; k < 3; ++k) s.n[k] = v.lattice[k];
+        s.nodes.assign(v.node_xyz, v.node_xyz + 3 * (size_t)v.n_nodes);
+        s.conn.assign(v.elem_nodes, v.elem_nodes + (size_t)nn * v.n_elems);
+        s.centroid.assign(v.centroid, v.centroid + 3 * (size_t)v.n_elems);
+        s.volume.assign(v.volume, v.volume + v.n_elems);
+        s.cl = v.char_length;
+        s.delta = v.delta;
+        s.l = v.l;
+        s.c0 = v.c0;
+        s.ramp = v.load_ramp;
+        pmts_scenario_destroy(sc);
     }
-    pmts_scenario_view v{};
-    pmts_scenario_get(sc, &v);
-    s.dim = v.dim;
-    for (int k = 0; k < 3; ++k) s.n[k] = v.lattice[k];
-    s.nodes.assign(v.node_xyz, v.node_xyz + 3 * (size_t)v.n_nodes);
-    const int nn = v.dim == 2 ? 4 : 8;
-    s.conn.assign(v.elem_nodes, v.elem_nodes + (size_t)nn * v.n_elems);
-    s.centroid.assign(v.centroid, v.centroid + 3 * (size_t)v.n_elems);
-    s.volume.assign(v.volume, v.volume + v.n_elems);
-    s.cl = v.char_length;
-    s.delta = v.delta;
-    s.l = v.l;
-    s.c0 = v.c0;
     s.s_crit = sd.s_crit;
-    s.ramp = v.load_ramp;
-    pmts_scenario_destroy(sc);
     s.E = sd.E;
     s.nu = sd.nu;
     s.rho = sd.rho;
@@ -956,6 +1056,31 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->pd_bcv = h->upload(bv);
         h->cfe = h->upload(s.cpl_fe);
         h->cpd = h->upload(s.cpl_pd);
+        h->gfe_rp = h->upload(s.cpl_fe_rp);
+        h->gfe_ci = h->upload(s.cpl_fe_ci);
+        h->gfe_w = h->upload(s.cpl_fe_w);
+        {  // transpose of G_FE over the touched FE dofs, rows ascending per dof
+            std::vector<std::vector<std::pair<int, double>>> col(h->nf);
+            for (int r = 0; r < h->nl; ++r)
+                for (int j = s.cpl_fe_rp[r]; j < s.cpl_fe_rp[r + 1]; ++j)
+                    col[s.cpl_fe_ci[j]].push_back({r, s.cpl_fe_w[j]});
+            std::vector<int32_t> td, trp(1, 0), tri;
+            std::vector<double> tw;
+            for (int d = 0; d < h->nf; ++d) {
+                if (col[d].empty()) continue;
+                td.push_back(d);
+                for (const auto& [r, w] : col[d]) {
+                    tri.push_back(r);
+                    tw.push_back(w);
+                }
+                trp.push_back(int32_t(tri.size()));
+            }
+            h->gft_n = int(td.size());
+            h->gft_d = h->upload(td);
+            h->gft_rp = h->upload(trp);
+            h->gft_ri = h->upload(tri);
+            h->gft_w = h->upload(tw);
+        }
         const int nmax = std::max({h->nf, h->np, h->nl});
         h->ufe = h->state(h->nf);
         h->vfe = h->state(h->nf);
@@ -1002,7 +1127,12 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         }
         // g_p_fe = G_FE P_ext (mts.hpp:110)
         h->g_p_fe.resize(h->nl);
-        for (int r = 0; r < h->nl; ++r) h->g_p_fe[r] = s.fe_p_ext[s.cpl_fe[r]];
+        for (int r = 0; r < h->nl; ++r) {
+            int j = s.cpl_fe_rp[r];
+            double acc = s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
+            for (++j; j < s.cpl_fe_rp[r + 1]; ++j) acc += s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
+            h->g_p_fe[r] = acc;
+        }
         CKM(cudaStreamSynchronize(h->stream));
         h->build_h_fe();
         if (h->use_dense) h->refresh_dense_interface();
@@ -1055,6 +1185,12 @@ int pmts_mts_view_get(const pmts_mts* h, pmts_mts_view* v) {
         v->pd_bc_vel = s.pd_bc_vel.data();
         v->cpl_fe_dof = s.cpl_fe.data();
         v->cpl_pd_dof = s.cpl_pd.data();
+        v->cpl_fe_nnz = int64_t(s.cpl_fe_ci.size());
+        v->cpl_fe_rowptr = s.cpl_fe_rp.data();
+        v->cpl_fe_col = s.cpl_fe_ci.data();
+        v->cpl_fe_w = s.cpl_fe_w.data();
+        v->fe_mesh_elems = s.fe_mesh_elems;
+        v->fe_mesh_nodes = s.fe_mesh_nodes;
         v->pairs = h->pairs.data();
         v->pe_weight = h->pe_weight.data();
         v->node_xyz = s.nodes.data();

@@ -471,7 +471,9 @@ void build_mts_system(MtsSystem& s) {
         } else {
             s.label[e] = 2;
             ++n_overlap;
-            for (int a = 0; a < nn; ++a) s.node_in_overlap[s.conn[std::size_t(e) * nn + a]] = 1;
+            // coupling rows sit on the PD side's overlap nodes
+            if (s.fe_mesh_elems < 0 || e >= s.fe_mesh_elems)
+                for (int a = 0; a < nn; ++a) s.node_in_overlap[s.conn[std::size_t(e) * nn + a]] = 1;
         }
     }
     if (n_pd + n_overlap == 0) throw ConfigError("PD region contains no elements");
@@ -484,9 +486,13 @@ void build_mts_system(MtsSystem& s) {
     s.fe_active.clear();
     s.pd_active.clear();
     for (int e = 0; e < E; ++e) {
-        if (s.label[e] != 1) s.fe_active.push_back(e);
-        if (s.label[e] != 0) s.pd_active.push_back(e);
+        const bool fe_mesh = s.fe_mesh_elems < 0 || e < s.fe_mesh_elems;
+        const bool pd_mesh = s.fe_mesh_elems < 0 || e >= s.fe_mesh_elems;
+        if (s.label[e] != 1 && fe_mesh) s.fe_active.push_back(e);
+        if (s.label[e] != 0 && pd_mesh) s.pd_active.push_back(e);
     }
+    if (s.fe_mesh_elems >= 0 && (s.fe_active.empty() || s.pd_active.empty()))
+        throw ConfigError("non-matching coupling: an empty FE or PD subdomain");
 
     const auto faces = boundary_faces(s);
     // tractions must select some boundary face overall (driver.hpp:195-209)
@@ -575,23 +581,98 @@ void build_mts_system(MtsSystem& s) {
     }
     resolve_bcs(s, s.fe_node_dof, s.fe_active_nodes, s.fe_bc_dofs, s.fe_bc_vel);
     resolve_bcs(s, s.pd_node_dof, s.pd_active_nodes, s.pd_bc_dofs, s.pd_bc_vel);
-    // build_coupling_map (coupling.hpp:72-105)
+    // build_coupling_map (coupling.hpp:72-105); non-matching: the row of a PD overlap
+    // node interpolates the FE velocity with the shape functions of the FE element
+    // containing it (local coordinates from lattice indices: exact, so a PD node on
+    // an FE node gets the single weight 1 -- the conforming map)
     s.cpl_fe.clear();
     s.cpl_pd.clear();
+    s.cpl_fe_rp.assign(1, 0);
+    s.cpl_fe_ci.clear();
+    s.cpl_fe_w.clear();
     int n_on = 0;
     for (int n = 0; n < N; ++n) n_on += s.node_in_overlap[n];
     if (n_on == 0) throw ConfigError("empty overlap: no coupling possible");
+    auto fe_bc = [&](int fd) {
+        return std::binary_search(s.fe_bc_dofs.begin(), s.fe_bc_dofs.end(), fd);
+    };
     for (int n = 0; n < N; ++n) {
         if (!s.node_in_overlap[n]) continue;
-        if (s.fe_node_dof[n] < 0 || s.pd_node_dof[n] < 0)
-            throw InternalError("overlap node missing from a subdomain dof map");
+        if (s.pd_node_dof[n] < 0) throw InternalError("overlap node missing from the PD dof map");
+        int fn[8], nfe = 0;  // FE nodes and weights of this row
+        double fw[8];
+        if (s.fe_mesh_elems < 0) {
+            if (s.fe_node_dof[n] < 0)
+                throw InternalError("overlap node missing from a subdomain dof map");
+            fn[0] = n;
+            fw[0] = 1.0;
+            nfe = 1;
+        } else {
+            // PD node (lattice index) -> FE element and local coordinates
+            const int q = n - s.fe_mesh_nodes;
+            const int pnx = s.pd_n[0] + 1, pny = s.pd_n[1] + 1;
+            const int pi[3] = {q % pnx, (q / pnx) % pny, q / (pnx * pny)};
+            int ei[3] = {0, 0, 0}, li[3] = {0, 0, 0};
+            for (int k = 0; k < dim; ++k) {
+                // fine index on the FE lattice: (pd_lo - fe_lo) / pd_h + pi, an integer
+                const long long g = std::llround((s.pd_lo[k] - s.fe_lo[k]) / s.pd_h) + pi[k];
+                long long c = g / s.fe_ratio;
+                if (c >= s.fe_n[k]) c = s.fe_n[k] - 1;  // the far face: last element
+                ei[k] = int(c);
+                li[k] = int(g - c * s.fe_ratio);  // 0 .. fe_ratio
+            }
+            // prefer an FE-active element among those sharing the point (ascending id)
+            int best = -1;
+            int cand[3][2], nc[3];
+            for (int k = 0; k < 3; ++k) {
+                nc[k] = 1;
+                cand[k][0] = ei[k];
+                if (k < dim && li[k] == 0 && ei[k] > 0) {
+                    cand[k][0] = ei[k] - 1;
+                    cand[k][1] = ei[k];
+                    nc[k] = 2;
+                }
+            }
+            int bl[3] = {0, 0, 0};
+            for (int a = 0; a < nc[2] && best < 0; ++a)
+                for (int b = 0; b < nc[1] && best < 0; ++b)
+                    for (int c = 0; c < nc[0] && best < 0; ++c) {
+                        const int ex = cand[0][c], ey = cand[1][b], ez = dim == 3 ? cand[2][a] : 0;
+                        const int e = (ez * s.fe_n[1] + ey) * s.fe_n[0] + ex;
+                        if (s.label[e] == 1) continue;  // FE-inactive (PD core)
+                        best = e;
+                        bl[0] = li[0] + (ex < ei[0] ? s.fe_ratio : 0);
+                        bl[1] = li[1] + (ey < ei[1] ? s.fe_ratio : 0);
+                        bl[2] = dim == 3 ? li[2] + (ez < ei[2] ? s.fe_ratio : 0) : 0;
+                    }
+            if (best < 0) throw ConfigError("a PD overlap node lies in no FE-active element");
+            const int32_t* en = s.conn.data() + std::size_t(best) * nn;
+            double xi[3] = {0, 0, 0};
+            for (int k = 0; k < dim; ++k) xi[k] = 2.0 * bl[k] / s.fe_ratio - 1.0;  // exact
+            for (int a = 0; a < nn; ++a) {
+                const double w = shape_value(dim, xi, a);
+                if (w == 0.0) continue;
+                fn[nfe] = en[a];
+                fw[nfe] = w;
+                ++nfe;
+            }
+        }
         for (int c = 0; c < dim; ++c) {
-            const int fd = s.fe_node_dof[n] + c, pdof = s.pd_node_dof[n] + c;
-            if (std::binary_search(s.fe_bc_dofs.begin(), s.fe_bc_dofs.end(), fd) ||
-                std::binary_search(s.pd_bc_dofs.begin(), s.pd_bc_dofs.end(), pdof))
-                continue;
-            s.cpl_fe.push_back(fd);
+            const int pdof = s.pd_node_dof[n] + c;
+            if (std::binary_search(s.pd_bc_dofs.begin(), s.pd_bc_dofs.end(), pdof)) continue;
+            bool all_bc = true;
+            for (int a = 0; a < nfe; ++a) {
+                if (s.fe_node_dof[fn[a]] < 0) throw InternalError("FE node without a dof");
+                all_bc = all_bc && fe_bc(s.fe_node_dof[fn[a]] + c);
+            }
+            if (all_bc) continue;
+            s.cpl_fe.push_back(s.fe_node_dof[fn[0]] + c);
             s.cpl_pd.push_back(pdof);
+            for (int a = 0; a < nfe; ++a) {
+                s.cpl_fe_ci.push_back(s.fe_node_dof[fn[a]] + c);
+                s.cpl_fe_w.push_back(fw[a]);
+            }
+            s.cpl_fe_rp.push_back(int32_t(s.cpl_fe_ci.size()));
         }
     }
     if (s.cpl_fe.empty()) throw ConfigError("empty overlap: all coupling rows constrained");

@@ -54,8 +54,19 @@ struct MtsSystem {
     std::vector<double> fe_val, fe_mass, fe_p_ext, pd_mass, pd_p_ext;
     std::vector<int32_t> fe_bc_dofs, pd_bc_dofs;
     std::vector<double> fe_bc_vel, pd_bc_vel;
-    std::vector<int32_t> cpl_fe, cpl_pd;  // coupling rows
+    std::vector<int32_t> cpl_fe, cpl_pd;  // coupling rows (cpl_fe: the row's first FE dof)
+    // G_FE as CSR over the rows: FE dofs and weights (one entry of weight 1 per row
+    // on the reference's conforming mesh; shape-function interpolation otherwise)
+    std::vector<int32_t> cpl_fe_rp, cpl_fe_ci;
+    std::vector<double> cpl_fe_w;
     std::vector<double> node_alpha;       // blend weight at each node (output sampling)
+    // non-matching meshes (extension): elements [0, fe_mesh_elems) and
+    // nodes [0, fe_mesh_nodes) are the FE lattice (spacing fe_h), the rest the PD
+    // lattice over the PD boxes' hull (spacing pd_h, fe_h / pd_h = fe_ratio); -1:
+    // one conforming mesh (the reference's model)
+    int fe_mesh_elems = -1, fe_mesh_nodes = -1;
+    int fe_n[3] = {1, 1, 1}, pd_n[3] = {1, 1, 1}, fe_ratio = 1;
+    double fe_lo[3] = {0, 0, 0}, pd_lo[3] = {0, 0, 0}, fe_h = 0, pd_h = 0;
 };
 
 // assembles everything after the inputs and the mesh geometry are filled in

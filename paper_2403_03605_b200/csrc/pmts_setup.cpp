@@ -102,6 +102,45 @@ double char_length(int dim, int n_elems, const double* volume) {
     return dim == 2 ? std::sqrt(v) : std::cbrt(v);
 }
 
+// Mesh::char_length (mesh.hpp:51-57) of the generated lattice n[0] x n[1] (x n[2])
+// at spacing h from lo, without storing it: the volume sum on the device when
+// one is present, else the same sum streamed on the host
+double lattice_char_length(int dim, const int n[3], const double lo[3], double h) {
+    const long long E = (long long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
+    if (E <= 0) return 0.0;
+    double v = 0.0;
+    if (!std::getenv("PMTS_HOST_SETUP") && device_available()) {
+        v = lattice_volume_sum_device(dim, n, lo, h);
+    } else {
+        const double gp = 1.0 / std::sqrt(3.0);
+        const int nx = n[0] + 1, ny = n[1] + 1;
+        std::vector<double> nodes(3 * 8);
+        int32_t en[8];
+        for (long long e = 0; e < E; ++e) {
+            const int i = int(e % n[0]), j = int((e / n[0]) % n[1]), k = int(e / ((long long)n[0] * n[1]));
+            const int ii[8] = {i, i + 1, i + 1, i, i, i + 1, i + 1, i};
+            const int jj[8] = {j, j, j + 1, j + 1, j, j, j + 1, j + 1};
+            for (int a = 0; a < (dim == 2 ? 4 : 8); ++a) {
+                const int kk = a >= 4 ? k + 1 : k;
+                nodes[3 * a] = lo[0] + ii[a] * h;
+                nodes[3 * a + 1] = lo[1] + jj[a] * h;
+                nodes[3 * a + 2] = dim == 3 ? lo[2] + kk * h : 0.0;
+                en[a] = a;
+            }
+            (void)nx;
+            (void)ny;
+            double vol = 0.0;
+            for (int q = 0; q < (dim == 2 ? 4 : 8); ++q) {
+                const double xi[3] = {(q & 1) ? gp : -gp, (q & 2) ? gp : -gp, (q & 4) ? gp : -gp};
+                vol += jacobian_det(dim, en, nodes.data(), xi);
+            }
+            v += vol;
+        }
+    }
+    v /= static_cast<double>(E);
+    return dim == 2 ? std::sqrt(v) : std::cbrt(v);
+}
+
 // GK15 adaptive quadrature (material.hpp:92-142) and calibrate_c0 (:150-165)
 namespace {
 const double kXk[15] = {-0.991455371120813, -0.949107912342759, -0.864864423359769,

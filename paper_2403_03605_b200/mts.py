@@ -56,6 +56,8 @@ class MtsSolver:
         d.enforce_continuity = 1 if run.get("enforce_continuity", True) else 0
         d.track_energy = 1 if sc.get("output", {}).get("energy", True) else 0
         d.device = device
+        # extension: non-matching FE lattice (mesh.fe_spacing), DESIGN.md section 11
+        d.fe_spacing = float(sc["mesh"].get("fe_spacing") or 0.0)
         h = C.c_void_p()
         check(lib().pmts_mts_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -97,6 +99,10 @@ class MtsSolver:
             "elem_nodes": _arr(v.elem_nodes, i32, E * (4 if v.dim == 2 else 8),
                                (E, 4 if v.dim == 2 else 8)),
             "node_alpha": _arr(v.node_alpha, f64, N),
+            "cpl_fe_rowptr": _arr(v.cpl_fe_rowptr, i32, v.n_lambda + 1),
+            "cpl_fe_col": _arr(v.cpl_fe_col, i32, v.cpl_fe_nnz),
+            "cpl_fe_w": _arr(v.cpl_fe_w, f64, v.cpl_fe_nnz),
+            "fe_mesh_elems": v.fe_mesh_elems, "fe_mesh_nodes": v.fe_mesh_nodes,
         }
 
     # -- integration --------------------------------------------------------
