@@ -44,6 +44,9 @@ WORKLOADS = {
             "exponential kernel l = delta)",
     "cfg4": "cfg4 (BASELINE configs[3]: 3D 200x200x50 hex8 block, dx 0.5 mm, delta 3.015 dx, "
             "constant micromodulus, 20 m/s +-5% impact patch)",
+    "cfg5_core": "cfg5 PD core (BASELINE configs[4], the largest PD config) as a pure-PD run: "
+                 "3D 400x800x40 hex8 at 0.25 mm, 755M bonds, 40 mm pre-notch, 12 MPa bands, "
+                 "constant micromodulus, dt 4 ns",
 }
 
 
@@ -350,7 +353,8 @@ def bench_native(args):
     achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
     fused = {"tile9": "k_tile9", "tile": "k_fused2d", "tma": "k_tma2d", "strip": "k_strip2d"}
     kname = {2: fused.get(os.environ.get("PMTS_FUSED_KERNEL", "tile9"), "k_tile9"),
-             1: "k_lat_bond"}.get(info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
+             1: "k_lat3_bond" if info["stencil_size"] == 122 else "k_lat_bond"}.get(
+                 info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": _ncu_traffic(kname),
             "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],

@@ -145,6 +145,38 @@ def scenarios() -> dict:
                                           hi=[0.007, 0.007, 0.005 + 1e-7])
     c4s["time"]["total_time"] = 2e-8 * 100
     s["cfg4_small"] = c4s
+    # BASELINE cfg5's PD core as a pure-PD run -- the largest PD configuration (the
+    # north star's scaling target): 100 x 200 x 10 mm at 0.25 mm (400 x 800 x 40 =
+    # 12.8M hexes, 755M bonds), a 40 mm through-thickness pre-notch at mid-height
+    # from the left edge, 12 MPa on the top / bottom faces (horizon bands), constant
+    # micromodulus with nu = 1/4, dt = 4 ns; 2000 fine steps = cfg5's 100 coarse x m=20
+    d5 = 3.015 * 2.5e-4
+    K5 = _E / (3.0 * (1.0 - 2.0 * 0.25))
+    c5 = {
+        "mesh": {"kind": "generated", "dim": 3, "bounds": [0, 0, 0, 0.1, 0.2, 0.01],
+                 "spacing": 2.5e-4,
+                 "notch1": [-0.001, 0.1, -0.001, 0.04, 0.1, -0.001, 0.04, 0.1, 0.011,
+                            -0.001, 0.1, 0.011]},
+        "material": {"E": _E, "nu": 0.25, "rho": _RHO, "formulation": "three_d"},
+        "pd": {"delta_factor": 3.015, "l_factor": 1.0,
+               "s_crit": round(s0_3d(_E, 0.25, _G0, d5), 7)},
+        "load": {"traction1": [-1, 0.2 - 1e-7, -1, 1, 0.2 + 1e-7, 1, 0, 12e6, 0],
+                 "traction2": [-1, -1e-7, -1, 1, 1e-7, 1, 0, -12e6, 0]},
+        "time": {"dt_pd": 4e-9, "m": 1, "total_time": 4e-9 * 2000, "gamma_pd": 0.5,
+                 "beta_pd": 0.0},
+        "run": {"mode": "pure_pd"},
+        "output": {"interval": 0.0},
+        "ext": {"micromodulus": "constant", "c": 18.0 * K5 / (math.pi * d5 ** 4)},
+    }
+    s["cfg5_core"] = c5
+    c5s = copy.deepcopy(c5)  # small twin for tests: 10 x 20 x 2.5 mm at 0.25 mm
+    c5s["mesh"]["bounds"] = [0, 0, 0, 0.01, 0.02, 0.0025]
+    c5s["mesh"]["notch1"] = [-0.001, 0.01, -0.001, 0.004, 0.01, -0.001, 0.004, 0.01, 0.0035,
+                             -0.001, 0.01, 0.0035]
+    c5s["load"] = {"traction1": [-1, 0.02 - 1e-7, -1, 1, 0.02 + 1e-7, 1, 0, 12e6, 0],
+                   "traction2": [-1, -1e-7, -1, 1, 1e-7, 1, 0, -12e6, 0]}
+    c5s["time"]["total_time"] = 4e-9 * 200
+    s["cfg5_core_small"] = c5s
 
     # --- coupled MTS --------------------------------
     # Miniature coupled strip: 30 x 10 elements at 1 mm, PD box = middle third
@@ -265,9 +297,16 @@ def stacked(name: str, n: int) -> dict:
     m = sc["mesh"]
     if m["dim"] == 3:  # 3D blocks stack along z (the slab axis); the impact patch stays on top
         b = list(m["bounds"])
+        ztop = b[5]
         lz = (b[5] - b[2]) * n
         b[5] = b[2] + lz
         m["bounds"] = b
+        for k in [k for k in m if k.startswith("notch") and m[k]]:  # through the new thickness
+            pts = list(m[k])
+            for q in range(2, len(pts), 3):
+                if pts[q] > ztop:
+                    pts[q] = b[5] + (pts[q] - ztop)
+            m[k] = pts
         iv = sc["ext"].get("initial_velocity")
         if iv:
             iv["lo"][2] = b[5] - 1e-7

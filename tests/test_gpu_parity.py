@@ -289,6 +289,49 @@ def test_cfg4_small_impact_3d(mode):
             assert 1.0 - np.logical_xor(mine, ref).sum() / ref.sum() >= 0.999
 
 
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_cfg5_core_small_notched_3d(mode):
+    """BASELINE cfg5's PD core physics at 40x80x10 (0.25 mm, 3D polygon pre-notch
+    through the thickness, 12 MPa horizon bands, constant micromodulus, dt 4 ns):
+    device families == oracle pairs (notch cut included); deterministic bitwise vs
+    the matrix-free oracle; fast mode within the north-star tolerances."""
+    sc = Scenario(cf.get("cfg5_core_small"))
+    s = PDSolver.from_scenario(sc, mode=mode).find_pe_pairs()
+    if mode == capi.FAST:
+        assert s.info()["path"] == 1 and s.info()["stencil_size"] == 122
+    pairs = po.find_pairs(3, sc.centroid, sc.volume, sc.delta, sc.notches())
+    assert np.array_equal(s.pairs(), pairs)
+    assert len(pairs) < len(po.find_pairs(3, sc.centroid, sc.volume, sc.delta))  # the notch cuts
+    ext = sc.cfg["ext"]
+    o = po.OraclePD(dict(dim=3, n_nodes=sc.n_nodes, conn=sc.conn, centroid=sc.centroid,
+                         volume=sc.volume, pairs=pairs, mass=sc.mass, p_ext=sc.p_ext,
+                         delta=sc.delta, s_crit=sc.s_crit, dt=sc.dt, micromodulus=1,
+                         c_const=ext["c"]), po.MF)
+    s.initial_acceleration(sc.load_scale(0.0))
+    o.init(sc.load_scale(0.0))
+    scales = sc.scales(1, 120)
+    if mode == capi.DETERMINISTIC:
+        nb = s.step(scales)
+        br, _ = o.step(scales)
+        u, v, a = s.state()
+        ou, ov, oa = o.state()
+        assert nb == len(br)
+        assert np.array_equal(u, ou) and np.array_equal(v, ov) and np.array_equal(a, oa)
+        assert np.array_equal(s.intact(), o.mu())
+    else:
+        s.step(scales[:10])
+        o.step(scales[:10])
+        u, v, _ = s.state()
+        ou, ov, _ = o.state()
+        assert np.linalg.norm(u - ou) <= 1e-9 * np.linalg.norm(ou)
+        assert np.linalg.norm(v - ov) <= 1e-9 * np.linalg.norm(ov)
+        s.step(scales[10:])
+        o.step(scales[10:])
+        mine, ref = s.intact() == 0, o.mu() == 0
+        if ref.sum():
+            assert 1.0 - np.logical_xor(mine, ref).sum() / ref.sum() >= 0.999
+
+
 # ----- known-answer tests on the device (test_perifem.cpp) ------------------
 
 def _kat_solver(mesh, pairs, s_crit, mode, delta=1.5, l=0.375):

@@ -48,7 +48,7 @@ def _run_slabs(sc, nranks, mode, steps):
 
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
 @pytest.mark.parametrize("name,nranks,steps", [("mini", 3, 80), ("cfg1", 4, 120),
-                                               ("cfg4_small", 2, 60)])
+                                               ("cfg4_small", 2, 60), ("cfg5_core_small", 2, 120)])
 def test_slabs_equal_single_domain(mode, name, nranks, steps):
     sc = Scenario(cf.get(name))
     one = PDSolver.from_scenario(sc, mode=mode).find_pe_pairs()
