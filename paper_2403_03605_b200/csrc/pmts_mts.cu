@@ -21,6 +21,7 @@
 // device CG reductions), so parity is to rounding (tests/test_gpu_mts.py), the
 // setup arrays bitwise (tests/test_mts_setup.py).
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -179,6 +180,7 @@ struct pmts_mts {
     int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
     double* hfe_v = nullptr;
     int64_t hfe_nnz = 0;
+    double* iface_jac = nullptr;  // interface CG preconditioner (null: the reference's plain CG)
     double *sv_d = nullptr, *gp_free_d = nullptr, *gp_link_d = nullptr;    // m or m+1 rows of nl
     double* pd_ubar = nullptr;                                             // E_pd x dim
     int32_t* row_of = nullptr;                                             // PD dof -> coupling row
@@ -478,6 +480,20 @@ struct pmts_mts {
                 rp[r + 1] = int32_t(ci.size());
             }
             hfe_nnz = int64_t(vv.size());
+            // Jacobi preconditioner of the matrix-free interface CG (an addition: the
+            // reference's CG is unpreconditioned, mts.hpp:194-213): diag(H_FE) plus the
+            // free-mass velocity of a PD dof after the m ramped substeps, m dt / (2 M) --
+            // the (1 - alpha)-weighted PD masses span orders of magnitude across the
+            // gluing zone, which is what slows the plain CG
+            if (!std::getenv("PMTS_MTS_PLAIN_CG")) {
+                std::vector<double> jd(nl, 0.0);
+                for (int r = 0; r < nl; ++r) {
+                    jd[r] = h_fe[(size_t)r * nl + r] +
+                            double(m) * s.dt_pd / (2.0 * s.pd_mass[s.cpl_pd[r]]);
+                    if (!(jd[r] > 0.0)) jd[r] = 0.0;  // precond() leaves such rows unscaled
+                }
+                iface_jac = upload(jd);
+            }
             hfe_rp = upload(rp);
             hfe_ci = upload(ci);
             hfe_v = upload(vv);
@@ -547,7 +563,7 @@ struct pmts_mts {
                                  apply_h_pd(in, iface_tmp);
                                  mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
                              },
-                             b, lam_d, interface_cg_tol, max_iter, nullptr, 1);
+                             b, lam_d, interface_cg_tol, max_iter, iface_jac, 1);
         } catch (const SolverError&) {
             use_dense = true;
             h_valid = false;
