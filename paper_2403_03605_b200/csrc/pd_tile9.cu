@@ -356,14 +356,23 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         if ((blockIdx.x | blockIdx.y) == 0)
             for (int j = threadIdx.x; j < bf.n_trk; j += NT) bf.trk_host[j] = bf.rd_in[bf.trk_dofs[j]];
     }
-    for (int y = warp; y < MY; y += NW) {
-        const int gj = ay0 + y;
+    if (ax0 >= 0 && ay0 >= 0 && ax0 + AX <= nx && ay0 + MY <= ny) {
+        // interior tile (most of them): no per-word bounds checks
+        const uint32_t* src = bf.mask_in + (size_t)ay0 * nx + ax0;
+        for (int y = warp; y < MY; y += NW) {
+            cp_async4(ma + y * AX + lane, src + (size_t)y * nx + lane, true);
+            if (lane < AX - 32) cp_async4(ma + y * AX + 32 + lane, src + (size_t)y * nx + 32 + lane, true);
+        }
+    } else {
+        for (int y = warp; y < MY; y += NW) {
+            const int gj = ay0 + y;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int x = lane + 32 * h, gi = ax0 + x;
-            if (x < AX) {
-                const bool in = gi >= 0 && gj >= 0 && gi < nx && gj < ny;
-                cp_async4(ma + y * AX + x, bf.mask_in + (in ? (size_t)gj * nx + gi : 0), in);
+            for (int h = 0; h < 2; ++h) {
+                const int x = lane + 32 * h, gi = ax0 + x;
+                if (x < AX) {
+                    const bool in = gi >= 0 && gj >= 0 && gi < nx && gj < ny;
+                    cp_async4(ma + y * AX + x, bf.mask_in + (in ? (size_t)gj * nx + gi : 0), in);
+                }
             }
         }
     }
