@@ -25,6 +25,7 @@
 // 16-byte aligned global row starts (so the {1/M, flags} box starts at the
 // even column i0 & ~1 of rows padded to an even length).  Reference semantics
 // as in pd_stencil.cu.
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <stdexcept>
@@ -328,10 +329,17 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     //     cp.async (zero-filled outside the domain) for the bond-state apron (a
     //     TMA box must start 16-byte aligned, so the mask box would be 3 columns
     //     wider than the CTA's shared memory has room for; measured: no faster)
+    // programmatic dependent launch: the next step's grid may launch now (its CTAs
+    // take SM slots as this grid's last wave drains); everything this step reads was
+    // written by the previous step, so wait for it before the first global access
+    asm volatile("griddepcontrol.launch_dependents;\n" ::);
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (threadIdx.x == 0) {
         mbar_expect_tx(&bar[0], kNtBytes);
         tma_load_2d(sm + kOffNt, &maps.rd, 2 * ax0, ay0, &bar[0]);
         mbar_expect_tx(&bar[1], kRvBytes + kImBytes);
@@ -694,14 +702,30 @@ int tile9_configure() {
     return occ;
 }
 
+// PMTS_T9_NO_PDL=1: plain stream-ordered launches
+bool pdl_enabled() {
+    static const bool on = !std::getenv("PMTS_T9_NO_PDL");
+    return on;
+}
+
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
                        int step, int do_break, double scale, int write_state, cudaStream_t s) {
     dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
     const PairStencil2D none{};
     const PairStencil2D& p = ps ? *ps : none;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
 #define PMTS_T9_LAUNCH(B, P, Q) \
-    k_tile9<B, P, Q><<<grid, NT, kSmem, s>>>(d, L, st, p, maps, b, step, scale, write_state)
+    cudaLaunchKernelEx(&cfg, k_tile9<B, P, Q>, d, L, st, p, maps, b, step, scale, write_state)
 #define PMTS_T9_PICK(Q)                                              \
     if (ps) {                                                        \
         if (do_break) PMTS_T9_LAUNCH(true, true, Q);                 \
