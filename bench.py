@@ -263,7 +263,7 @@ def bench_native(args):
 
     rank, local, world = _env_rank()
     dist = None
-    mode = capi.FAST if args.mode == "fast" else capi.DETERMINISTIC
+    mode = {"fast": capi.FAST, "det": capi.DETERMINISTIC, "f32pos": capi.FAST_F32POS}[args.mode]
     K, W = args.steps, args.warmup
     slabbed = world > 1 or args.force_slabs
     if slabbed:
@@ -336,7 +336,28 @@ def bench_native(args):
         barrier()
         ms = s.step_timed(sc.scales(step0, K))  # synchronises the stream on both sides
         barrier()
-    del s
+    variant = None
+    if not slabbed and mode == capi.FAST and sc.dim == 2 and not args.no_variant:
+        # BASELINE cfg3's fp32-position / fp64-accumulate variant over the same steps,
+        # and how far it lands from the fp64 run at the end of the window
+        u64, _, _ = s.state()
+        b64 = s.intact() == 0
+        del s
+        sv = PDSolver.from_scenario(sc, mode=capi.FAST_F32POS, device=local).find_pe_pairs()
+        sv.initial_acceleration(sc.load_scale(0.0))
+        sv.step(sc.scales(1, W))
+        ms_v = sv.step_timed(sc.scales(step0, K))
+        u32, _, _ = sv.state()
+        b32 = sv.intact() == 0
+        variant = {"mode": "f32pos (PMTS_FAST_F32POS)", "dtype": "f32 positions / f64 accumulate",
+                   "value": B * K / (ms_v * 1e-3), "unit": UNIT, "ms_per_step": ms_v / K,
+                   "u_rel_l2_vs_fp64": float(np.linalg.norm(u32 - u64) / np.linalg.norm(u64)),
+                   "broken_fp64": int(b64.sum()), "broken_f32pos": int(b32.sum()),
+                   "broken_agreement": float(1.0 - np.logical_xor(b64, b32).sum()
+                                             / max(int(b64.sum()), 1))}
+        del sv
+    else:
+        del s
     s = fresh()
     bond_ms, tot_ms = s.profile(sc.scales(step0, K))
     if dist:
@@ -421,7 +442,9 @@ def bench_native(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None,
+            "dtype": "f32 positions / f64 accumulate" if mode == capi.FAST_F32POS else "f64",
+            "data": "synthetic",
             "config": {"workload": (WORKLOADS.get(args.workload, args.workload)
                                     + ("" if world == 1 else
                                        f"; weak scaling: {world} cfg3 slabs stacked into a "
@@ -438,6 +461,8 @@ def bench_native(args):
             "gpu_launches": K * info["kernels_per_step"],
             "clocks": clk.summary(),
         }
+        if variant:
+            line["f32pos_variant"] = variant
         if world == 1 and not args.no_mts:
             try:
                 line["coupled_mts"] = bench_mts(args.mts_steps, 3, not args.no_cpu_baseline)
@@ -455,9 +480,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="cfg3")
-    ap.add_argument("--mode", default="fast", choices=["fast", "det"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "det", "f32pos"])
     ap.add_argument("--cpu-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variant", action="store_true",
+                    help="skip the fp32-position variant line of the default run")
     ap.add_argument("--no-mts", action="store_true",
                     help="skip the coupled MTS (cfg2) section of the line")
     ap.add_argument("--mts-steps", type=int, default=20)

@@ -35,8 +35,12 @@ enum pmts_status {
 enum pmts_mode {
     PMTS_DETERMINISTIC = 0, /* reference neighbour order, exact stretch, no FMA: broken set
                                bit-exact, u/v/a equal to the matrix-free oracle bitwise */
-    PMTS_FAST = 1           /* centroid-averaged eta, squared break test, lattice stencil
+    PMTS_FAST = 1,          /* centroid-averaged eta, squared break test, lattice stencil
                                families when the mesh is a lattice */
+    PMTS_FAST_F32POS = 2    /* BASELINE cfg3's fp32-position / fp64-accumulate variant of fast
+                               mode (extension): tile-relative fp32 displacements in the force
+                               and the candidate break test, fp64 force accumulation, fp64
+                               state; 2D lattice tile kernel only */
 };
 
 enum pmts_micromodulus {

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PMTS_LIB_PATH") or os.path.join(HERE, "lib", "libpmts.so")
 
 PMTS_OK, PMTS_ERR_INTERNAL, PMTS_ERR_CONFIG, PMTS_ERR_SOLVER = 0, 1, 2, 3
-DETERMINISTIC, FAST = 0, 1
+DETERMINISTIC, FAST, FAST_F32POS = 0, 1, 2
 MICRO_EXP, MICRO_CONST = 0, 1
 
 

@@ -94,6 +94,8 @@ struct PairStencil2D {
     int off[14];   // apron offset of o (dj * 38 + di)
     int pbit[14];  // mask bit of the positive offset o
     double h2;    // 2 h
+    float h2f;       // fp32-position variant: 2 h and the candidate thresholds
+    float clf[14];   // (cl lowered by 1e-4, rounded down to fp32)
     int screen;   // 1: skip the candidate break pass on tiles the node-step bound
                   // proves cold (pd_tile9.cu); results are bitwise the same
     unsigned long long* hot_count;  // diagnostics (PMTS_T9_COUNT_HOT): [0] hot, [1] all tiles
@@ -102,7 +104,8 @@ int tile9_pair_offset(int k, int* a, int* b);
 int tile9_configure();  // returns resident CTAs per SM
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
-                       int step, int do_break, double scale, int write_state, cudaStream_t s);
+                       int step, int do_break, double scale, int write_state, bool f32,
+                       cudaStream_t s);
 
 // 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class
 // (1,2,3,4,5,6,8,9): c = w c(h|o|) h^2, and the bit patterns of the smallest /

@@ -161,14 +161,42 @@ __device__ __forceinline__ void pair_math(double2 up, double2 um, double2 ue, bo
         anyc |= (!MASKED || actp) && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
 }
 
+// fp32-position variant (PMTS_FAST_F32POS): the ubar apron holds tile-relative
+// fp32 displacements (ubar - ubar_ref, rounded once); eta, the pair sum s and
+// t = o . s are fp32, each pair's t is widened to fp64 and accumulated into G
+// in fp64 (the break tests run in cand_terms, never here)
 template <bool DO_BREAK, bool MASKED, int K>
-__device__ __forceinline__ void pair_term(const double2* ubq, const uint32_t* maq,
-                                          const double2 (&ue)[EPT], const uint32_t (&m0)[EPT],
+__device__ __forceinline__ void pair_math(float2 up, float2 um, float2 ue, bool actp, bool actm,
+                                          double& G0, double& G1, bool& anyc,
+                                          const PairStencil2D& ps) {
+    static_assert(!DO_BREAK, "fp32 pairs: break tests run in cand_terms");
+    constexpr int A = kPairA[K], B = kPairB[K];
+    const float ep0 = up.x - ue.x, ep1 = up.y - ue.y;
+    float em0 = um.x - ue.x, em1 = um.y - ue.y;
+    if (MASKED) {
+        em0 = actm ? em0 : 0.0f;
+        em1 = actm ? em1 : 0.0f;
+    }
+    const float fp0 = MASKED && !actp ? 0.0f : ep0, fp1 = MASKED && !actp ? 0.0f : ep1;
+    if (B == 0) {
+        G0 = fma(ps.fa[K], (double)(fp0 + em0), G0);
+    } else if (A == 0) {
+        G1 = fma(ps.fb[K], (double)(fp1 + em1), G1);
+    } else {
+        const double t = fmaf((float)A, fp0 + em0, (float)B * (fp1 + em1));
+        G0 = fma(ps.fa[K], t, G0);
+        G1 = fma(ps.fb[K], t, G1);
+    }
+}
+
+template <bool DO_BREAK, bool MASKED, int K, typename V>
+__device__ __forceinline__ void pair_term(const V* ubq, const uint32_t* maq,
+                                          const V (&ue)[EPT], const uint32_t (&m0)[EPT],
                                           double (&G0)[EPT], double (&G1)[EPT],
                                           bool (&anyc)[EPT], const PairStencil2D& ps) {
     const int off = ps.off[K];
-    const double2* pp = ubq + off;
-    const double2* pm = ubq - off;
+    const V* pp = ubq + off;
+    const V* pm = ubq - off;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
         bool actp = true, actm = true;
@@ -190,13 +218,13 @@ __device__ __forceinline__ void pair_term(const double2* ubq, const uint32_t* ma
 // (A = 0), -2..5 (|A| = 1, 2, loaded per half of the rows to stay within 80
 // registers) or 0..3 (|A| = 3): 62 shared loads per thread instead of 112 --
 // the shared-memory pipe was the limiter (ncu: 67 % of peak)
-template <bool DO_BREAK>
-__device__ __forceinline__ void pairs_blocked(const double2* ubq, const double2 (&ue)[EPT],
+template <bool DO_BREAK, typename V>
+__device__ __forceinline__ void pairs_blocked(const V* ubq, const V (&ue)[EPT],
                                               double (&G0)[EPT], double (&G1)[EPT],
                                               bool (&anyc)[EPT], const PairStencil2D& ps) {
     static_assert(EPT == 4, "blocked path assumes 4 rows per thread");
     {  // A = 0: (0,1) (0,2) (0,3)
-        double2 c[10];
+        V c[10];
 #pragma unroll
         for (int i = 0; i < 10; ++i) c[i] = (i >= 3 && i < 7) ? ue[i - 3] : ubq[(i - 3) * AX];
 #pragma unroll
@@ -210,7 +238,7 @@ __device__ __forceinline__ void pairs_blocked(const double2* ubq, const double2 
     for (int g = 1; g <= 2; ++g) {    // |A| = 1: pairs 3..7, |A| = 2: pairs 8..12
 #pragma unroll
         for (int half = 0; half < 2; ++half) {  // rows 2 half .. 2 half + 1: cells rows -2..3 (+2 half)
-            double2 p[6], m[6];
+            V p[6], m[6];
 #pragma unroll
             for (int i = 0; i < 6; ++i) {
                 p[i] = ubq[(i - 2 + 2 * half) * AX + g];
@@ -241,9 +269,9 @@ __device__ __forceinline__ void pairs_blocked(const double2* ubq, const double2 
                                        G1[r], anyc[r], ps);
 }
 
-template <bool DO_BREAK, bool MASKED, int K>
-__device__ __forceinline__ void pair_terms(const double2* ubq, const uint32_t* maq,
-                                           const double2 (&ue)[EPT], const uint32_t (&m0)[EPT],
+template <bool DO_BREAK, bool MASKED, int K, typename V>
+__device__ __forceinline__ void pair_terms(const V* ubq, const uint32_t* maq,
+                                           const V (&ue)[EPT], const uint32_t (&m0)[EPT],
                                            double (&G0)[EPT], double (&G1)[EPT],
                                            bool (&anyc)[EPT], const PairStencil2D& ps) {
     if constexpr (K < 14) {
@@ -270,6 +298,30 @@ __device__ __forceinline__ void cand_terms(const double2* uq, double2 ue, uint32
         cand_terms<MASKED, K + 1>(uq, ue, m0, anyc, ps);
     }
 }
+// fp32 candidate test against thresholds lowered by 1e-4 (clf): a superset of
+// the bonds whose fp64 test on the same fp32 ubar values can fire
+template <bool MASKED, int K>
+__device__ __forceinline__ void cand_terms(const float2* uq, float2 ue, uint32_t m0, bool& anyc,
+                                           const PairStencil2D& ps) {
+    if constexpr (K < 14) {
+        constexpr int A = kPairA[K], B = kPairB[K];
+        const float2 up = uq[ps.off[K]];
+        const float ep0 = up.x - ue.x, ep1 = up.y - ue.y;
+        float tp;
+        if (B == 0) tp = A * ep0;
+        else if (A == 0) tp = B * ep1;
+        else tp = fmaf((float)A, ep0, B * ep1);
+        const bool act = !MASKED || ((m0 >> ps.pbit[K]) & 1u);
+        anyc |= act && fmaf(ps.h2f, tp, fmaf(ep0, ep0, ep1 * ep1)) >= ps.clf[K];
+        cand_terms<MASKED, K + 1>(uq, ue, m0, anyc, ps);
+    }
+}
+
+__device__ __forceinline__ double2 to_d2(double2 v) { return v; }
+__device__ __forceinline__ double2 to_d2(float2 v) { return make_double2(v.x, v.y); }
+
+template <bool F32> struct UbarT { using V = double2; };
+template <> struct UbarT<true> { using V = float2; };
 
 __device__ __forceinline__ int ps_a(int k) {
     return k == 13 ? 3 : (k >= 8 ? 2 : (k >= 3 ? 1 : 0));  // |A| of pair k
@@ -301,13 +353,15 @@ int tile9_pair_offset(int k, int* a, int* b) {
 
 // PAIRS: the pair-symmetric force with the cold-tile break screen; otherwise the
 // per-offset sums of pd_stencil_fused.cu (bitwise equal to it)
-template <bool DO_BREAK, bool PAIRS, bool REPORT>
+template <bool DO_BREAK, bool PAIRS, bool REPORT, bool F32>
 __global__ void __launch_bounds__(NT, kMinBlocks)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const __grid_constant__ PairStencil2D ps,
         const __grid_constant__ Tile9Maps maps, FusedBufs bf, int step, double scale,
         int write_state) {
     constexpr bool SCREEN = PAIRS && DO_BREAK;
+    static_assert(PAIRS || !F32, "the fp32-position variant runs the pair-symmetric force");
+    using V = typename UbarT<F32>::V;
     extern __shared__ __align__(16) unsigned char smraw[];
     // the dynamic base is only guaranteed 16-byte aligned: realign for TMA
     unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
@@ -315,8 +369,8 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     uint32_t* ma = reinterpret_cast<uint32_t*>(sm + kOffMa);
     const double2* rvs = reinterpret_cast<const double2*>(sm + kOffRv);
     const double* ims = reinterpret_cast<const double*>(sm + kOffIm);
-    double2* ub = reinterpret_cast<double2*>(sm + kOffUb);
-    double2* gt = ub;  // G aliases the ubar apron once the force pass is done
+    V* ub = reinterpret_cast<V*>(sm + kOffUb);
+    double2* gt = reinterpret_cast<double2*>(sm + kOffUb);  // G aliases the ubar apron after the force pass
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
     unsigned* red = reinterpret_cast<unsigned*>(sm + kOffRed);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -388,6 +442,10 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     mbar_wait(&bar[0], 0);
+    // fp32 variant: the apron stores ubar - uref, uref = a node of the tile (in the
+    // domain), so the fp32 rounding is relative to the tile's local variation
+    double2 uref = make_double2(0.0, 0.0);
+    if constexpr (F32) uref = nt[(min(j0 + TY / 2, ny) - ay0) * BX + min(i0 + TX / 2, nx) - ax0];
 
     // (2) ubar of the apron (column walk with carried node-pair sums); the
     //     positive-stencil completeness of every mask the force pass reads.
@@ -437,8 +495,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         for (int i = 0; i < UR; ++i) {
             const int y = y0 + i;
             if (y < AY) {
-                ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
-                                              d.Nsh * (hs[i].y + hs[i + 1].y));
+                if constexpr (F32)
+                    ub[y * AX + x] = make_float2((float)(d.Nsh * (hs[i].x + hs[i + 1].x) - uref.x),
+                                                 (float)(d.Nsh * (hs[i].y + hs[i + 1].y) - uref.y));
+                else
+                    ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
+                                                  d.Nsh * (hs[i].y + hs[i + 1].y));
                 if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
             }
         }
@@ -471,8 +533,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const int k = lane < 14 ? lane : 0;
         const double A = fabs((double)ps_a(k)), B = fabs((double)ps_b(k));
         const double E0 = A * Dxx + B * Dxy, E1 = A * Dyx + B * Dyy;
-        const double bound = fma(ps.h2, A * E0 + B * E1, E0 * E0 + E1 * E1) * (1.0 + 1e-6);
-        hot = __any_sync(0xffffffffu, lane < 14 && !(bound < __longlong_as_double(ps.cl[k])));
+        // (fp32 variant: against the lowered fp32 candidate thresholds, with room
+        // for the fp32 rounding of the candidate's own lhs)
+        const double bound =
+            fma(ps.h2, A * E0 + B * E1, E0 * E0 + E1 * E1) * (F32 ? 1.0 + 1e-5 : 1.0 + 1e-6);
+        const double cthr = F32 ? (double)ps.clf[k] : __longlong_as_double(ps.cl[k]);
+        hot = __any_sync(0xffffffffu, lane < 14 && !(bound < cthr));
         if (ps.hot_count && threadIdx.x == 0) {
             atomicAdd(ps.hot_count, hot ? 1ull : 0ull);
             atomicAdd(ps.hot_count + 1, 1ull);
@@ -485,7 +551,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     const int q0 = (gy0 + R) * AX + gx + R;
     // only ue, G and the candidate flags stay live through the force pass (the
     // element ids and bond-state words are re-derived afterwards: registers)
-    double2 ue[EPT];
+    V ue[EPT];
     double G0[EPT], G1[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
@@ -583,7 +649,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             while (c) {
                 const int k = __ffs(c) - 1;
                 c &= c - 1;
-                const double2 up = ub[q0 + r * AX + st.aoff[k]], uer = ub[q0 + r * AX];
+                const double2 up = to_d2(ub[q0 + r * AX + st.aoff[k]]), uer = to_d2(ub[q0 + r * AX]);
                 const double e0 = up.x - uer.x, e1 = up.y - uer.y;
                 const double dot = fma(st.xi1[k], e1, st.xi0[k] * e0);
                 const double lhs = fma(2.0, dot, fma(e1, e1, e0 * e0));
@@ -680,9 +746,9 @@ void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_
 }
 
 namespace {
-template <bool B, bool P, bool Q>
+template <bool B, bool P, bool Q, bool F = false>
 void t9_set_smem() {
-    cudaError_t e = cudaFuncSetAttribute(k_tile9<B, P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_tile9<B, P, Q, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmem);
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
@@ -697,8 +763,12 @@ int tile9_configure() {
     t9_set_smem<false, false, true>();
     t9_set_smem<true, true, true>();
     t9_set_smem<false, true, true>();
+    t9_set_smem<true, true, false, true>();
+    t9_set_smem<false, true, false, true>();
+    t9_set_smem<true, true, true, true>();
+    t9_set_smem<false, true, true, true>();
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true, true, false>, NT, kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile9<true, true, false, false>, NT, kSmem);
     return occ;
 }
 
@@ -710,7 +780,9 @@ bool pdl_enabled() {
 
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
-                       int step, int do_break, double scale, int write_state, cudaStream_t s) {
+                       int step, int do_break, double scale, int write_state, bool f32,
+                       cudaStream_t s) {
+    if (f32 && !ps) throw std::runtime_error("tile9: the fp32-position variant needs the pair stencil");
     dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
     const PairStencil2D none{};
     const PairStencil2D& p = ps ? *ps : none;
@@ -724,15 +796,18 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-#define PMTS_T9_LAUNCH(B, P, Q) \
-    cudaLaunchKernelEx(&cfg, k_tile9<B, P, Q>, d, L, st, p, maps, b, step, scale, write_state)
+#define PMTS_T9_LAUNCH(B, P, Q, F) \
+    cudaLaunchKernelEx(&cfg, k_tile9<B, P, Q, F>, d, L, st, p, maps, b, step, scale, write_state)
 #define PMTS_T9_PICK(Q)                                              \
-    if (ps) {                                                        \
-        if (do_break) PMTS_T9_LAUNCH(true, true, Q);                 \
-        else PMTS_T9_LAUNCH(false, true, Q);                         \
+    if (f32) {                                                       \
+        if (do_break) PMTS_T9_LAUNCH(true, true, Q, true);           \
+        else PMTS_T9_LAUNCH(false, true, Q, true);                   \
+    } else if (ps) {                                                 \
+        if (do_break) PMTS_T9_LAUNCH(true, true, Q, false);          \
+        else PMTS_T9_LAUNCH(false, true, Q, false);                  \
     } else {                                                         \
-        if (do_break) PMTS_T9_LAUNCH(true, false, Q);                \
-        else PMTS_T9_LAUNCH(false, false, Q);                        \
+        if (do_break) PMTS_T9_LAUNCH(true, false, Q, false);         \
+        else PMTS_T9_LAUNCH(false, false, Q, false);                 \
     }
     if (b.n_trk > 0) {
         PMTS_T9_PICK(true)

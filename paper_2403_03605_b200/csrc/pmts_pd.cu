@@ -102,6 +102,7 @@ struct pmts_pd {
     CUtensorMap t9_rd[2]{}, t9_rv{}, t9_im{};
     int t9_prefetch = 0;  // L2 prefetch distance in tiles (resident CTAs of the device)
     bool pairs = false;              // tile9 with the pair-symmetric compile-time stencil
+    bool f32pos = false;             // PMTS_FAST_F32POS: tile9 pairs on fp32 tile-relative ubar
     PairStencil2D pst{};
     double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
     Stencil2D st2{};
@@ -718,6 +719,15 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
                 h->pst.pbit[k] = s;
             }
             h->pst.h2 = 2.0 * hh;
+            h->pst.h2f = (float)(2.0 * hh);
+            for (int k = 0; k < 14 && h->pairs; ++k) {  // fp32 candidate thresholds, rounded down
+                double c;
+                std::memcpy(&c, &h->pst.cl[k], 8);
+                c *= 1.0 - 1e-4;
+                float f = (float)c;
+                if ((double)f > c) f = std::nextafter(f, 0.0f);
+                h->pst.clf[k] = f;
+            }
             // cold-tile break screen (PMTS_T9_NO_SCREEN=1: candidate pass on every tile)
             h->pst.screen = std::getenv("PMTS_T9_NO_SCREEN") ? 0 : 1;
             h->pst.hot_count = nullptr;
@@ -814,6 +824,9 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
                   bool last = true, const double* scale_dev = nullptr,
                   const FusedBufs* report = nullptr) {
     const int brk = h->fracture ? 1 : 0;
+    if (h->f32pos && !(h->fused && h->tile9 && h->pairs))
+        throw ConfigError("PMTS_FAST_F32POS runs on the 2D lattice tile kernel with the nominal "
+                          "28-offset pair stencil only (set lattice and lattice_h)");
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt, scale_dev};
         if (report) {
@@ -824,7 +837,7 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
         if (h->tile9)
             launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
-                              slot, brk, scale, last ? 1 : 0, h->stream);
+                              slot, brk, scale, last ? 1 : 0, h->f32pos, h->stream);
         else if (h->tma)
             launch_tma2d_step(h->d, h->L, h->st2, h->tmaps[h->d.rd == h->rd_buf[0] ? 0 : 1], b,
                               slot, brk, scale, last ? 1 : 0, h->stream);
@@ -907,8 +920,8 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
             throw ConfigError("exponential micromodulus needs 0 < l <= delta and c0 > 0");
         if (ds.micromodulus == PMTS_MICRO_CONST && ds.c_const <= 0.0)
             throw ConfigError("constant micromodulus needs c > 0");
-        if (ds.mode != PMTS_DETERMINISTIC && ds.mode != PMTS_FAST)
-            throw ConfigError("mode must be PMTS_DETERMINISTIC or PMTS_FAST");
+        if (ds.mode != PMTS_DETERMINISTIC && ds.mode != PMTS_FAST && ds.mode != PMTS_FAST_F32POS)
+            throw ConfigError("mode must be PMTS_DETERMINISTIC, PMTS_FAST or PMTS_FAST_F32POS");
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw InternalError("no CUDA device: the PD fine step has no CPU fallback");
@@ -922,7 +935,9 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         h->E = ds.n_elems;
         h->N = ds.n_nodes;
         h->ndof = ds.n_nodes * ds.dim;
-        h->mode = ds.mode;
+        // the fp32-position variant is fast mode with fp32 arithmetic in the tile force
+        h->f32pos = ds.mode == PMTS_FAST_F32POS;
+        h->mode = h->f32pos ? PMTS_FAST : ds.mode;
         h->fracture = ds.s_crit > 0.0 && std::isfinite(ds.s_crit);  // material.hpp:44
         const int E = h->E, N = h->N, nn = h->nn, dim = h->dim;
         h->conn.assign(ds.elem_nodes, ds.elem_nodes + (size_t)E * nn);

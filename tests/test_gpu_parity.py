@@ -478,3 +478,85 @@ def test_cfg3_screen_exact_over_baseline_horizon(cfg3, monkeypatch):
     assert a[0] == b[0] and sum(a[0]) > 1000
     for x, y in zip(a[1:], b[1:]):
         assert np.array_equal(x, y)
+
+
+# ----- fp32-position / fp64-accumulate variant (BASELINE cfg3, PMTS_FAST_F32POS) -----
+# Tolerances of the variant (the north star states none for it): fields within
+# 1e-5 relative L2 of the oracle before crack initiation, >= 99.9 % broken-set
+# agreement afterwards (measured: <= 1.7e-6 and 100 % on every 2D fixture).
+F32_TOL = 1e-5
+
+
+@pytest.mark.parametrize("name", ["mini", "cfg1_200", "bp_coarse_2000"])
+def test_f32pos_tolerances(name):
+    g, sc, s = _solver(name, capi.FAST_F32POS)
+    s.find_pe_pairs()
+    assert s.info()["path"] == 2
+    steps = g["meta"]["steps"]
+    s.initial_acceleration(g["scale"][0])
+    br = g["broken"]
+    first = int(br[0, 0]) if len(br) else steps + 1
+    pre = min(first - 1, steps)
+    o = po.OraclePD(oracle_sys(g, sc), po.MF)
+    o.init(g["scale"][0])
+    s.step(g["scale"][1:pre + 1])
+    o.step(g["scale"][1:pre + 1])
+    u, v, _ = s.state()
+    ou, ov, _ = o.state()
+    assert 0 < np.linalg.norm(u - ou) <= F32_TOL * np.linalg.norm(ou)  # > 0: fp32 really ran
+    assert np.linalg.norm(v - ov) <= F32_TOL * np.linalg.norm(ov)
+    s.step(g["scale"][pre + 1:steps + 1])
+    mine = s.intact() == 0
+    ref = np.zeros(len(g["pairs"]), dtype=bool)
+    ref[g["broken"][:, 1]] = True
+    agree = 1.0 - np.logical_xor(mine, ref).sum() / max(ref.sum(), 1)
+    assert agree >= 0.999, agree
+
+
+@pytest.mark.parametrize("nx,ny,steps", [(124, 62, 300), (33, 65, 200)])
+def test_f32pos_screen_is_exact(nx, ny, steps, monkeypatch):
+    """The cold-tile screen of the fp32 variant (bound against its lowered fp32
+    candidate thresholds) changes nothing: bitwise the candidate pass on every tile."""
+    sc = _plate(nx, ny)
+    out = {}
+    for screen in (True, False):
+        if screen:
+            monkeypatch.delenv("PMTS_T9_NO_SCREEN", raising=False)
+        else:
+            monkeypatch.setenv("PMTS_T9_NO_SCREEN", "1")
+        s = PDSolver.from_scenario(sc, mode=capi.FAST_F32POS).find_pe_pairs()
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = s.step([sc.load_scale(i * sc.dt) for i in range(1, steps + 1)])
+        out[screen] = (nb, *s.state(), s.intact())
+    a, b = out[True], out[False]
+    assert a[0] == b[0] and a[0] > 0
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name,over", [("block3d", {}), ("mini", {"lattice": (0, 0, 0)})])
+def test_f32pos_needs_the_2d_tile_kernel(name, over):
+    """Only the 2D lattice tile kernel has the fp32-position arithmetic: 3D and
+    unstructured families are a ConfigError (status 2), never a silent fp64 run."""
+    g, sc, s = _solver(name, capi.FAST_F32POS, **over)
+    s.find_pe_pairs()
+    s.initial_acceleration(g["scale"][0])
+    with pytest.raises(capi.ConfigError, match="F32POS"):
+        s.step(g["scale"][1:3])
+
+
+def test_cfg3_f32pos_vs_fp64_over_1500_steps(cfg3):
+    """BASELINE cfg3 through crack growth: the fp32-position variant against the
+    fp64 kernel -- broken sets agree >= 99.9 % (measured 100 %), displacements
+    within 1e-6 relative L2 (measured 9e-8)."""
+    out = {}
+    for mode in (capi.FAST, capi.FAST_F32POS):
+        s = PDSolver.from_scenario(cfg3, mode=mode).find_pe_pairs()
+        s.initial_acceleration(cfg3.load_scale(0.0))
+        s.step(cfg3.scales(1, 1500))
+        u, _, _ = s.state()
+        out[mode] = (u, s.intact() == 0)
+    (u0, b0), (u1, b1) = out[capi.FAST], out[capi.FAST_F32POS]
+    assert b0.sum() > 10000
+    assert 1.0 - np.logical_xor(b0, b1).sum() / b0.sum() >= 0.999
+    assert np.linalg.norm(u1 - u0) <= 1e-6 * np.linalg.norm(u0)
