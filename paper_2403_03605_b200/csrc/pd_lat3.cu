@@ -134,6 +134,114 @@ bool lat3_offsets_match(const int8_t* di, const int8_t* dj, const int8_t* dk, in
 }
 int lat3_class_of(int d2) { return cls_of(d2); }
 
+namespace {
+__device__ __forceinline__ unsigned hi_abs3(double d) {
+    return (unsigned)__double2hiint(d) & 0x7fffffffu;
+}
+__device__ __forceinline__ double hi_bound3(unsigned m) {  // >= every |d| with hi_abs3(d) <= m
+    return __hiloint2double((int)m, (int)0xffffffffu);
+}
+}  // namespace
+
+// ubar of the 3D lattice, one CTA per bond-kernel tile (16 x 4 x 4 elements), plus
+// the cold-tile screen's input: per tile, the maxima over its elements' edges of
+// |u(n + e_a) - u(n)|_c for axis a and component c (9 values, as the high words of
+// the doubles, which order like the magnitudes).  ubar is summed in k_lat_ubar<3>'s
+// order, so it is bitwise the same.
+__global__ void __launch_bounds__(NT)
+k_lat3_ubar(DevPD d, LatticeDev L, unsigned* tmax) {
+    __shared__ unsigned red[NT / 32][9];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
+    const int i = blockIdx.x * TX + tx, j = blockIdx.y * TY + ty, k = blockIdx.z * TZ + tz;
+    unsigned mx[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) mx[q] = 0u;
+    if (i < L.nx && j < L.ny && k < L.nz) {
+        const int NX = L.nx + 1, NY = L.ny + 1, up = NX * NY;
+        const int n00 = (k * NY + j) * NX + i;
+        const int nd[8] = {n00, n00 + 1, n00 + NX + 1, n00 + NX,
+                           n00 + up, n00 + up + 1, n00 + up + NX + 1, n00 + up + NX};
+        double u[8][3];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) u[a][c] = d.rd[(size_t)nd[a] * 3 + c];
+        double s[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) s[c] += u[a][c];
+        const int e = (k * L.ny + j) * L.nx + i;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d.ubar[(size_t)e * 3 + c] = d.Nsh * s[c];
+        if (tmax) {
+            // edges: x (0,1) (3,2) (4,5) (7,6); y (0,3) (1,2) (4,7) (5,6); z (a, a + 4)
+            constexpr int EA[3][4] = {{0, 3, 4, 7}, {0, 1, 4, 5}, {0, 1, 2, 3}};
+            constexpr int EB[3][4] = {{1, 2, 5, 6}, {3, 2, 7, 6}, {4, 5, 6, 7}};
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        mx[3 * ax + c] = max(mx[3 * ax + c], hi_abs3(u[EB[ax][q]][c] - u[EA[ax][q]][c]));
+        }
+    }
+    if (!tmax) return;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        mx[q] = __reduce_max_sync(0xffffffffu, mx[q]);
+        if (lane == 0) red[warp][q] = mx[q];
+    }
+    __syncthreads();
+    if (tid < 9) {
+        unsigned v = 0u;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) v = max(v, red[w][tid]);
+        tmax[((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 9 + tid] = v;
+    }
+}
+
+// Cold-tile break screen: every partner of a tile element lies in the tile or its 26
+// neighbours (apron 3 < tile extents 16, 4, 4), and eta = ubar_p - ubar_e is the mean
+// of the 8 node differences u(n + o) - u(n), each a sum of |o_a| edge steps along a
+// monotone lattice path inside those tiles' elements: |eta_c| <= E_c = sum_a |o_a|
+// D_ac, so 2h o.eta + |eta|^2 <= 2h sum_c |o_c| E_c + sum_c E_c^2.  A tile where that
+// bound (x (1 + 1e-6)) stays below every offset's candidate threshold runs the force
+// without the break test: bitwise the same result, no candidate could fire.
+__device__ __forceinline__ bool lat3_tile_hot(const Stencil3D& st, const LatticeDev& L) {
+    __shared__ unsigned dmax[9];
+    const int tid = threadIdx.x;
+    if (tid < 9) dmax[tid] = 0u;
+    __syncthreads();
+    if (tid < 27 * 9) {
+        const int t = tid / 9, q = tid % 9;
+        const int bx = blockIdx.x + t % 3 - 1, by = blockIdx.y + (t / 3) % 3 - 1,
+                  bz = blockIdx.z + t / 9 - 1;
+        if (bx >= 0 && by >= 0 && bz >= 0 && bx < (int)gridDim.x && by < (int)gridDim.y &&
+            bz < (int)gridDim.z)
+            atomicMax(&dmax[q], st.tmax[((size_t)(bz * gridDim.y + by) * gridDim.x + bx) * 9 + q]);
+    }
+    __syncthreads();
+    bool h = false;
+    if (tid < S3) {
+        const double a0 = fabs((double)L.di[tid]), a1 = fabs((double)L.dj[tid]),
+                     a2 = fabs((double)L.dk[tid]);
+        double D[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = hi_bound3(dmax[q]);
+        const double E0 = a0 * D[0] + a1 * D[3] + a2 * D[6];
+        const double E1 = a0 * D[1] + a1 * D[4] + a2 * D[7];
+        const double E2 = a0 * D[2] + a1 * D[5] + a2 * D[8];
+        const int d2 = (int)(a0 * a0 + a1 * a1 + a2 * a2);
+        const double bound =
+            fma(st.h2, a0 * E0 + a1 * E1 + a2 * E2, E0 * E0 + E1 * E1 + E2 * E2) * (1.0 + 1e-6);
+        h = !(bound < __longlong_as_double(st.clo[cls_of(d2)]));
+    }
+    return __syncthreads_or(h);
+}
+
 template <bool DO_BREAK>
 __global__ void __launch_bounds__(NT, 3)
 k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int step) {
@@ -153,7 +261,16 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
         uy[q] = in ? d.ubar[ge * 3 + 1] : 0.0;
         uz[q] = in ? d.ubar[ge * 3 + 2] : 0.0;
     }
-    __syncthreads();
+    bool hot = DO_BREAK;
+    if (DO_BREAK && st.tmax) {
+        hot = lat3_tile_hot(st, L);  // (its barriers also close the staging)
+        if (st.hot_count && tid == 0) {
+            atomicAdd(st.hot_count, hot ? 1ull : 0ull);
+            atomicAdd(st.hot_count + 1, 1ull);
+        }
+    } else {
+        __syncthreads();
+    }
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
     const int gi = i0 + tx, gj = j0 + ty, gk = k0 + tz;
     unsigned long long nb = 0;
@@ -171,7 +288,8 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
         for (int w = 0; w < 4; ++w) c.m[w] = d.mask[(size_t)w * d.E + e];
         c.gx = c.gy = c.gz = 0.0;
         c.anyc = false;
-        Unroll<0, DO_BREAK>::run(c, st);
+        if (hot) Unroll<0, DO_BREAK>::run(c, st);
+        else Unroll<0, false>::run(c, st);
         if (DO_BREAK && c.anyc) {  // rare: exact per-bond thresholds (generic table)
             uint32_t mw[4] = {c.m[0], c.m[1], c.m[2], c.m[3]};
             for (int w = 0; w < 4; ++w) {
@@ -218,6 +336,14 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
             if (t) atomicAdd(d.broken_count + step, t);
         }
     }
+}
+
+void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s) {
+    dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
+    k_lat3_ubar<<<grid, NT, 0, s>>>(d, L, tmax);
+}
+size_t lat3_tile_count(const LatticeDev& L) {
+    return (size_t)((L.nx + TX - 1) / TX) * ((L.ny + TY - 1) / TY) * ((L.nz + TZ - 1) / TZ);
 }
 
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,

@@ -285,7 +285,8 @@ void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_b
                          cudaStream_t s, const Stencil3D* st3) {
     const int nb = (d.N + 255) / 256;
     if (d.dim == 3 && st3) {  // the specialised 122-offset kernel (pd_lat3.cu)
-        k_lat_ubar<3><<<(d.E + 255) / 256, 256, 0, s>>>(d, L);
+        // tiled ubar + the cold-tile screen's edge maxima (only when the break test runs)
+        launch_lat3_ubar(d, L, do_break ? const_cast<unsigned*>(st3->tmax) : nullptr, s);
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[0], s));
         launch_lat3_bond(d, L, *st3, step, do_break, s);
         if (time_bond) PMTS_CUDA_S(cudaEventRecord(ev[1], s));

@@ -115,11 +115,17 @@ struct Stencil3D {
     long long clo[8], cthr[8];
     double h2;  // 2 h
     double hh;  // h^2
+    // cold-tile break screen (pd_lat3.cu): per-tile node-edge maxima written by
+    // k_lat3_ubar (null: no screen); diagnostics (hot / all tiles)
+    const unsigned* tmax;
+    unsigned long long* hot_count;
 };
 bool lat3_offsets_match(const int8_t* di, const int8_t* dj, const int8_t* dk, int S);
 int lat3_class_of(int d2);
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
                       int do_break, cudaStream_t s);
+void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s);
+size_t lat3_tile_count(const LatticeDev& L);
 
 // Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
 // positive offsets, in that kernel's order.

@@ -644,6 +644,19 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
         }
         h->st3.h2 = 2.0 * hh;
         h->st3.hh = hh * hh;
+        // cold-tile break screen (PMTS_LAT3_NO_SCREEN=1: break test on every tile)
+        h->st3.tmax = nullptr;
+        if (ok && !std::getenv("PMTS_LAT3_NO_SCREEN")) {
+            const size_t nt = lat3_tile_count(h->L);
+            unsigned* tm = h->alloc<unsigned>(9 * nt);
+            CK(cudaMemsetAsync(tm, 0, 9 * nt * sizeof(unsigned), h->stream));
+            h->st3.tmax = tm;
+        }
+        h->st3.hot_count = nullptr;
+        if (std::getenv("PMTS_T9_COUNT_HOT")) {
+            h->st3.hot_count = h->alloc<unsigned long long>(2);
+            CK(cudaMemsetAsync(h->st3.hot_count, 0, 16, h->stream));
+        }
         h->lat3 = ok;
     }
     h->fused = false;
@@ -1073,6 +1086,11 @@ void pmts_pd_destroy(pmts_pd* h) {
         unsigned long long c[2] = {0, 0};
         cudaMemcpy(c, h->pst.hot_count, 16, cudaMemcpyDeviceToHost);
         std::fprintf(stderr, "pmts: tile9 screen: %llu of %llu tiles hot\n", c[0], c[1]);
+    }
+    if (h && h->lat3 && h->st3.hot_count) {
+        unsigned long long c[2] = {0, 0};
+        cudaMemcpy(c, h->st3.hot_count, 16, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "pmts: lat3 screen: %llu of %llu tiles hot\n", c[0], c[1]);
     }
     if (h && h->comm) {
         if (h->stream) cudaStreamSynchronize(h->stream);

@@ -289,6 +289,34 @@ def test_cfg4_small_impact_3d(mode):
             assert 1.0 - np.logical_xor(mine, ref).sum() / ref.sum() >= 0.999
 
 
+@pytest.mark.parametrize("name,steps", [("cfg4_small", 100), ("cfg5_core_small", 200),
+                                        ("block3d", 300)])
+def test_lat3_screen_is_exact(name, steps, monkeypatch):
+    """The 3D cold-tile break screen (per-tile node-edge maxima from the tiled ubar
+    kernel) only skips break tests its bound proves cannot fire: fields, bond
+    states and broken counts are bitwise those of the test on every tile."""
+    sc = Scenario(cf.get(name))
+    out = {}
+    for screen in (True, False):
+        if screen:
+            monkeypatch.delenv("PMTS_LAT3_NO_SCREEN", raising=False)
+        else:
+            monkeypatch.setenv("PMTS_LAT3_NO_SCREEN", "1")
+        s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+        assert s.info()["stencil_size"] == 122
+        v0 = sc.initial_velocity()
+        if v0.any():
+            z = np.zeros(sc.n_dof)
+            s.set_state(z, v0, z)
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = [s.step(sc.scales(i, 20)) for i in range(1, steps + 1, 20)]
+        out[screen] = (nb, *s.state(), s.intact())
+    a, b = out[True], out[False]
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
 def test_cfg5_core_small_notched_3d(mode):
     """BASELINE cfg5's PD core physics at 40x80x10 (0.25 mm, 3D polygon pre-notch
