@@ -26,7 +26,12 @@ namespace {
 
 constexpr int TX = 16, TY = 4, TZ = 4, R = 3;
 constexpr int AX = TX + 2 * R, AY = TY + 2 * R, AZ = TZ + 2 * R;
-constexpr int NA = AX * AY * AZ;
+// the ubar apron in shared memory is AoS (x, y, z per cell) with rows of AXT cells
+// starting one column early (global columns i0 - 4 .. i0 + 19): the TMA box must
+// start 16-byte aligned in global memory and be a multiple of 16 bytes wide
+constexpr int AXT = 24, X0 = R + 1;
+constexpr int NAT = AXT * AY * AZ;
+constexpr int kApronBytes = NAT * 3 * 8;  // 57,600 B: three CTAs per SM
 constexpr int NT = TX * TY * TZ;
 constexpr int S3 = 122;
 
@@ -59,7 +64,7 @@ struct Ofs {
     static constexpr int di = o.di[K], dj = o.dj[K], dk = o.dk[K];
     static constexpr int d2 = di * di + dj * dj + dk * dk;
     static constexpr int cls = cls_of(d2);
-    static constexpr int aoff = (dk * AY + dj) * AX + di;
+    static constexpr int aoff = 3 * ((dk * AY + dj) * AXT + di);  // doubles
 };
 
 // c * e for a small compile-time integer c (exact for |c| <= 3 as adds)
@@ -82,10 +87,8 @@ __device__ __forceinline__ double iaxpy(double acc, double e) {
 }
 
 struct Ctx {
-    const double* ux;
-    const double* uy;
-    const double* uz;
-    int q0;
+    const double* ua;  // AoS apron
+    int q0;            // element's first double in ua
     double ex, ey, ez;
     uint32_t m[4];
     double gx, gy, gz;
@@ -96,7 +99,7 @@ template <int K, bool DO_BREAK>
 __device__ __forceinline__ void bond(Ctx& c, const Stencil3D& st) {
     using O = Ofs<K>;
     const int q = c.q0 + O::aoff;
-    const double e0 = c.ux[q] - c.ex, e1 = c.uy[q] - c.ey, e2 = c.uz[q] - c.ez;
+    const double e0 = c.ua[q] - c.ex, e1 = c.ua[q + 1] - c.ey, e2 = c.ua[q + 2] - c.ez;
     double dot = imul<O::di>(e0);
     dot = iaxpy<O::dj>(dot, e1);
     dot = iaxpy<O::dk>(dot, e2);
@@ -242,24 +245,42 @@ __device__ __forceinline__ bool lat3_tile_hot(const Stencil3D& st, const Lattice
     return __syncthreads_or(h);
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
 template <bool DO_BREAK>
 __global__ void __launch_bounds__(NT, 3)
 k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int step) {
-    extern __shared__ double sm3[];
-    double* ux = sm3;
-    double* uy = sm3 + NA;
-    double* uz = sm3 + 2 * NA;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    // realign the dynamic base to 128 bytes for the TMA destination
+    double* ua = reinterpret_cast<double*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ua + 3 * NAT);
     const int tid = threadIdx.x;
     const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY, k0 = blockIdx.z * TZ;
-    for (int q = tid; q < NA; q += NT) {
-        const int ax = q % AX, r = q / AX;
-        const int ay = r % AY, az = r / AY;
-        const int gi = i0 + ax - R, gj = j0 + ay - R, gk = k0 + az - R;
-        const bool in = gi >= 0 && gj >= 0 && gk >= 0 && gi < L.nx && gj < L.ny && gk < L.nz;
-        const size_t ge = ((size_t)gk * L.ny + gj) * L.nx + gi;
-        ux[q] = in ? d.ubar[ge * 3] : 0.0;
-        uy[q] = in ? d.ubar[ge * 3 + 1] : 0.0;
-        uz[q] = in ? d.ubar[ge * 3 + 2] : 0.0;
+    if (st.use_tma) {
+        // one bulk tensor copy of the apron; out-of-domain boxes arrive zero-filled
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                         "r"(kApronBytes));
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(ua)),
+                "l"(&st.ub), "r"(3 * (i0 - X0)), "r"(j0 - R), "r"(k0 - R), "r"(smem_u32(bar))
+                : "memory");
+        }
+    } else {
+        for (int q = tid; q < NAT; q += NT) {
+            const int ax = q % AXT, r = q / AXT;
+            const int ay = r % AY, az = r / AY;
+            const int gi = i0 + ax - X0, gj = j0 + ay - R, gk = k0 + az - R;
+            const bool in = gi >= 0 && gj >= 0 && gk >= 0 && gi < L.nx && gj < L.ny && gk < L.nz;
+            const size_t ge = ((size_t)gk * L.ny + gj) * L.nx + gi;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ua[3 * q + c] = in ? d.ubar[ge * 3 + c] : 0.0;
+        }
     }
     bool hot = DO_BREAK;
     if (DO_BREAK && st.tmax) {
@@ -273,19 +294,32 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     }
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
     const int gi = i0 + tx, gj = j0 + ty, gk = k0 + tz;
-    unsigned long long nb = 0;
-    if (gi < L.nx && gj < L.ny && gk < L.nz) {
-        const int e = (gk * L.ny + gj) * L.nx + gi;
-        Ctx c;
-        c.ux = ux;
-        c.uy = uy;
-        c.uz = uz;
-        c.q0 = ((tz + R) * AY + ty + R) * AX + tx + R;
-        c.ex = ux[c.q0];
-        c.ey = uy[c.q0];
-        c.ez = uz[c.q0];
+    const bool own = gi < L.nx && gj < L.ny && gk < L.nz;
+    const int e = own ? (gk * L.ny + gj) * L.nx + gi : 0;
+    uint32_t m4[4] = {0u, 0u, 0u, 0u};  // bond states, loaded while the apron is in flight
+    if (own) {
 #pragma unroll
-        for (int w = 0; w < 4; ++w) c.m[w] = d.mask[(size_t)w * d.E + e];
+        for (int w = 0; w < 4; ++w) m4[w] = d.mask[(size_t)w * d.E + e];
+    }
+    if (st.use_tma) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared.b64 P1, [%0], 0;\n"
+            "@!P1 bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_u32(bar)));
+    }
+    unsigned long long nb = 0;
+    if (own) {
+        Ctx c;
+        c.ua = ua;
+        c.q0 = 3 * (((tz + R) * AY + ty + R) * AXT + tx + X0);
+        c.ex = ua[c.q0];
+        c.ey = ua[c.q0 + 1];
+        c.ez = ua[c.q0 + 2];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c.m[w] = m4[w];
         c.gx = c.gy = c.gz = 0.0;
         c.anyc = false;
         if (hot) Unroll<0, DO_BREAK>::run(c, st);
@@ -298,9 +332,8 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
                     const int b = __ffs(live) - 1;
                     live &= live - 1;
                     const int s = 32 * w + b;
-                    const int a = (L.dk[s] * AY + L.dj[s]) * AX + L.di[s];
-                    const double e0 = ux[c.q0 + a] - c.ex, e1 = uy[c.q0 + a] - c.ey,
-                                 e2 = uz[c.q0 + a] - c.ez;
+                    const int a = c.q0 + 3 * ((L.dk[s] * AY + L.dj[s]) * AXT + L.di[s]);
+                    const double e0 = ua[a] - c.ex, e1 = ua[a + 1] - c.ey, e2 = ua[a + 2] - c.ez;
                     const double dot = fma((double)L.dk[s], e2,
                                            fma((double)L.dj[s], e1, (double)L.di[s] * e0));
                     const double lhs = fma(st.h2, dot, fma(e2, e2, fma(e1, e1, e0 * e0)));
@@ -342,6 +375,11 @@ void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaS
     dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
     k_lat3_ubar<<<grid, NT, 0, s>>>(d, L, tmax);
 }
+void lat3_apron_box(int* bx, int* by, int* bz) {
+    *bx = 3 * AXT;
+    *by = AY;
+    *bz = AZ;
+}
 size_t lat3_tile_count(const LatticeDev& L) {
     return (size_t)((L.nx + TX - 1) / TX) * ((L.ny + TY - 1) / TY) * ((L.nz + TZ - 1) / TZ);
 }
@@ -349,7 +387,7 @@ size_t lat3_tile_count(const LatticeDev& L) {
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
                       int do_break, cudaStream_t s) {
     dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
-    constexpr size_t smem = sizeof(double) * 3 * NA;
+    constexpr size_t smem = kApronBytes + 8 + 128;  // + mbarrier + realignment slack
     static bool configured = false;
     if (!configured) {
         for (auto fn : {k_lat3_bond<true>, k_lat3_bond<false>})

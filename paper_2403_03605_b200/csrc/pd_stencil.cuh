@@ -111,6 +111,8 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
 // (1,2,3,4,5,6,8,9): c = w c(h|o|) h^2, and the bit patterns of the smallest /
 // scalar thresholds (2 s + s^2) h^2 |o|^2.
 struct Stencil3D {
+    CUtensorMap ub;  // ubar as [nz][ny][3 nx] doubles (use_tma: nx even)
+    int use_tma;
     double c[8];
     long long clo[8], cthr[8];
     double h2;  // 2 h
@@ -126,6 +128,7 @@ void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, 
                       int do_break, cudaStream_t s);
 void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s);
 size_t lat3_tile_count(const LatticeDev& L);
+void lat3_apron_box(int* bx, int* by, int* bz);  // TMA box of the ubar apron (doubles, rows, layers)
 
 // Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
 // positive offsets, in that kernel's order.

@@ -288,7 +288,7 @@ void finish_families(pmts_pd* h, int K) {
 
 // TMA tensor maps for the persistent 2D kernel: rd (both ping-pong buffers),
 // rv, and the packed {1/M, flags}, all viewed as [NY][2 NX] doubles.
-void build_tma_maps(pmts_pd* h) {
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -298,6 +298,11 @@ void build_tma_maps(pmts_pd* h) {
             throw InternalError("cuTensorMapEncodeTiled unavailable");
         encode = (PFN_cuTensorMapEncodeTiled)fn;
     }
+    return encode;
+}
+
+void build_tma_maps(pmts_pd* h) {
+    const PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
     const int NX = h->L.nx + 1, NY = h->L.ny + 1;
     auto make = [&](CUtensorMap* m, void* base, int bx, int by) {
         const cuuint64_t dims[2] = {(cuuint64_t)2 * NX, (cuuint64_t)NY};
@@ -321,15 +326,7 @@ void build_tma_maps(pmts_pd* h) {
 // TMA tensor maps of the tile9 kernel: rd of both ping-pong buffers, rv and
 // {1/M | flags}.  Box sizes come from pd_tile9.cu.
 void build_tile9_maps(pmts_pd* h) {
-    static PFN_cuTensorMapEncodeTiled encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess)
-            throw InternalError("cuTensorMapEncodeTiled unavailable");
-        encode = (PFN_cuTensorMapEncodeTiled)fn;
-    }
+    const PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
     const int nx = h->L.nx, ny = h->L.ny, NX = nx + 1, NY = ny + 1, NXP = (NX + 1) & ~1;
     int rdx, rdy, rvx, rvy, imx, imy;
     tile9_boxes(&rdx, &rdy, &rvx, &rvy, &imx, &imy);
@@ -644,6 +641,23 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
         }
         h->st3.h2 = 2.0 * hh;
         h->st3.hh = hh * hh;
+        // TMA staging of the ubar apron (global rows must be 16-byte multiples: nx even)
+        h->st3.use_tma = 0;
+        if (ok && L.nx % 2 == 0 && !std::getenv("PMTS_LAT3_NO_TMA")) {
+            const cuuint64_t dims[3] = {(cuuint64_t)3 * L.nx, (cuuint64_t)L.ny, (cuuint64_t)L.nz};
+            const cuuint64_t strides[2] = {(cuuint64_t)3 * L.nx * 8, (cuuint64_t)3 * L.nx * L.ny * 8};
+            int bx, by, bz;
+            lat3_apron_box(&bx, &by, &bz);
+            const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            const CUresult r = tensor_map_encoder()(
+                &h->st3.ub, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->d.ubar, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                throw InternalError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+            h->st3.use_tma = 1;
+        }
         // cold-tile break screen (PMTS_LAT3_NO_SCREEN=1: break test on every tile)
         h->st3.tmax = nullptr;
         if (ok && !std::getenv("PMTS_LAT3_NO_SCREEN")) {
