@@ -425,8 +425,9 @@ def bench_native(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / K,
                "note": "per rank, one pmts_pd_step_tracked call for the K steps: state H2D "
                        "from pinned memory, the K load scales H2D in one copy, per step "
-                       "(async on the stream) the step, whose kernel writes its tracked "
-                       "displacement into mapped pinned memory; the K broken counts D2H in "
+                       "(async on the stream) the step and its tracked displacement written into "
+                       "mapped pinned memory (2D: by the step kernel; 3D lattice: by a tiny "
+                       "launch reading the step's predictor); the K broken counts D2H in "
                        "one copy; final state D2H"}
     except Exception as ex:  # pragma: no cover - reported, never silent
         e2e = {"value": None, "unit": UNIT, "error": repr(ex)}

@@ -331,7 +331,7 @@ __global__ void k_track(const double* src, const int32_t* idx, int n, double* tr
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) trk_host[i] = src[idx[i]];
     if (i == 0) {
-        *cnt_host = *cnt_dev;
+        if (cnt_dev) *cnt_host = *cnt_dev;
         if (scl_dev_next) *scl_dev_next = *scl_host_next;
     }
 }

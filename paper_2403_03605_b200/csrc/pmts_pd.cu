@@ -1411,10 +1411,21 @@ int pmts_pd_step_tracked(pmts_pd* h, int32_t n, const double* scales, int32_t n_
                 enqueue_step(h, s, scales[s], false, nullptr, s == n - 1, dscl, &rep);
             }
             download(h_cnt, h->d_counts, n, h->stream);
+        } else if (n > 0 && h->lattice && !h->fused) {
+            // lattice path (3D): with beta = 0 the step's u is the predictor rd it
+            // starts from (u = rd + (beta dt) dt a), so the tracked row is read from rd
+            // before the step -- no per-step u, v, a materialisation; the broken counts
+            // come back in one copy at the end
+            for (int s = 0; s < n; ++s) {
+                launch_track(h->d.rd, didx, n_tracked, m_trk + (size_t)s * n_tracked, nullptr,
+                             nullptr, nullptr, nullptr, h->stream);
+                enqueue_step(h, s, scales[s], false, nullptr, s == n - 1, nullptr);
+            }
+            download(h_cnt, h->d_counts, n, h->stream);
         } else if (n > 0) {
             upload(dscl, h_scl, 1, h->stream);
         }
-        for (int s = 0; s < n && !h->tile9; ++s) {
+        for (int s = 0; s < n && !h->tile9 && !(h->lattice && !h->fused); ++s) {
             // u of step s: the fused kernel's displacement is the step's predictor
             // (beta = 0), i.e. the rd buffer it consumed; the other paths write u
             const bool every = !h->fused;

@@ -218,12 +218,13 @@ def test_tile9_screen_is_exact(nx, ny, steps, monkeypatch):
         assert a[0] > 0
 
 
+@pytest.mark.parametrize("name", ["mini", "block3d"])
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
-def test_step_tracked_reports_every_step(mode):
+def test_step_tracked_reports_every_step(mode, name):
     """pmts_pd_step_tracked: per-step tracked displacements and broken counts equal
-    single-step stepping (and, deterministic, the oracle's u at every step)."""
-    g, sc, s = _solver("mini", mode)
-    _, _, s2 = _solver("mini", mode)
+    single-step stepping (2D tile kernel, 3D lattice path, deterministic ELL)."""
+    g, sc, s = _solver(name, mode)
+    _, _, s2 = _solver(name, mode)
     s.find_pe_pairs()
     s2.find_pe_pairs()
     steps = 40
