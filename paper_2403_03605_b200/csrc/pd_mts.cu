@@ -217,6 +217,84 @@ __global__ void k_sum_partials(int nb, const double* part, double* out) {
 // CG scalars on the device: alpha = rz / pap, beta = rz_new / rz
 __global__ void k_ratio(const double* num, const double* den, double* out) { *out = *num / *den; }
 
+// One-launch dot product(s) for the CG iteration graph: the block partials of
+// k_dot_partial (same grid, same per-thread order, same tree) and, in the last
+// block to finish, the reduction of k_sum_partials over them -- bitwise the same
+// sums as the two-launch form -- followed by the CG scalar:
+//   mode 1 (alpha):  out = x.y,             *sc = *num / out
+//   mode 2 (beta):   out = x.y, out2 = x2.y2, *sc = out / *num, then *num = out
+__global__ void __launch_bounds__(kT) k_dot_fin(int n, const double* x, const double* y,
+                                                const double* x2, const double* y2,
+                                                double* part, unsigned* ticket, double* out,
+                                                double* out2, int mode, double* num, double* sc) {
+    __shared__ double sh[kT], sh2[kT];
+    __shared__ bool last;
+    const int nb = gridDim.x;
+    double s = 0.0, s2 = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        s += x[i] * y[i];
+        if (x2) s2 += x2[i] * y2[i];
+    }
+    sh[threadIdx.x] = s;
+    sh2[threadIdx.x] = s2;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sh[threadIdx.x] += sh[threadIdx.x + o];
+            sh2[threadIdx.x] += sh2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        part[nb + blockIdx.x] = sh2[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)nb - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const volatile double* vp = part;
+    double t = 0.0, t2 = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        t += vp[i];
+        t2 += vp[nb + i];
+    }
+    sh[threadIdx.x] = t;
+    sh2[threadIdx.x] = t2;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sh[threadIdx.x] += sh[threadIdx.x + o];
+            sh2[threadIdx.x] += sh2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *out = sh[0];
+        if (x2) *out2 = sh2[0];
+        if (mode == 1) *sc = *num / sh[0];
+        if (mode == 2) {
+            *sc = sh[0] / *num;
+            *num = sh[0];
+        }
+        *ticket = 0u;  // ready for the next replay
+    }
+}
+
+// x += alpha p; r -= alpha ap; z = precond(r): k_cg_update then k_precond, fused
+__global__ void k_cg_update_precond(int n, const double* alpha_dev, const double* p,
+                                    const double* ap, double* x, double* r, const double* jac,
+                                    double* z) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double al = *alpha_dev;
+    x[i] += al * p[i];
+    const double ri = r[i] + -al * ap[i];
+    r[i] = ri;
+    z[i] = jac ? (jac[i] != 0.0 ? ri / jac[i] : ri) : ri;
+}
+
 // y = A x, CSR, one warp per row (long rows: the interface's H_FE)
 __global__ void k_csr_warp(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            const double* __restrict__ v, const double* __restrict__ x,
@@ -385,6 +463,59 @@ __global__ void __launch_bounds__(kT) k_pd_force_lin(DevPD d, const double* __re
         for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
 }
 
+// Entry-major copy of the families for the warp-per-element linear force: lane k
+// of element e reads colT[e K + k], coefT[e K + k] and xiT[(e K + k) DIM + c] =
+// cen_c(p) - cen_c(e) (the subtraction k_pd_force_lin performs) with coalesced
+// loads, where the [k E + e] layout put every lane on its own cache line.
+template <int DIM>
+__global__ void k_family_transpose(DevPD d, int32_t* colT, double* coefT, double* xiT) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // q = e K + k
+    if (q >= (long long)d.E * d.K) return;
+    const int e = (int)(q / d.K), k = (int)(q % d.K);
+    const int p = d.col[(size_t)k * d.E + e];
+    colT[q] = p;
+    coefT[q] = p >= 0 ? d.coef[(size_t)k * d.E + e] : 0.0;
+    for (int c = 0; c < DIM; ++c)
+        xiT[q * DIM + c] = p >= 0 ? d.cen[(size_t)c * d.E + p] - d.cen[(size_t)c * d.E + e] : 0.0;
+}
+
+// k_pd_force_lin on the entry-major families: the same per-lane arithmetic and
+// warp-tree sum, so bitwise the same G
+template <int DIM>
+__global__ void __launch_bounds__(kT) k_pd_force_lin_t(DevPD d, const int32_t* __restrict__ colT,
+                                                       const double* __restrict__ coefT,
+                                                       const double* __restrict__ xiT,
+                                                       const double* __restrict__ ub,
+                                                       const uint32_t* __restrict__ mask) {
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (e >= d.E) return;
+    const int E = d.E, K = d.K;
+    double ue[DIM], G[DIM];
+    for (int c = 0; c < DIM; ++c) {
+        ue[c] = ub[(size_t)e * DIM + c];
+        G[c] = 0.0;
+    }
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        const size_t q = (size_t)e * K + k;
+        const int p = k < K ? colT[q] : -1;
+        const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
+        if (p >= 0 && ((word >> lane) & 1u)) {
+            double xi[DIM], dot = 0.0;
+            for (int c = 0; c < DIM; ++c) {
+                xi[c] = xiT[q * DIM + c];
+                dot = dot + xi[c] * (ub[(size_t)p * DIM + c] - ue[c]);
+            }
+            const double t = coefT[q] * dot;
+            for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+        }
+    }
+    for (int c = 0; c < DIM; ++c)
+        for (int o = 16; o > 0; o >>= 1) G[c] += __shfl_down_sync(0xffffffffu, G[c], o);
+    if (lane == 0)
+        for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
+}
+
 // (K x)_n from the incident elements' G, fused with the explicit block solve
 // of the node's dofs (newmark.hpp:122-131, 150-158)
 template <int DIM>
@@ -491,6 +622,25 @@ void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double*
         k_pd_force_lin<3><<<(int)(((long long)d.E * 32 + kT - 1) / kT), kT, 0, s>>>(d, ubar, mask);
     }
     check("pd_force_lin");
+}
+void family_transpose(const DevPD& d, int32_t* colT, double* coefT, double* xiT, cudaStream_t s) {
+    const long long n = (long long)d.E * d.K;
+    const int b = (int)((n + kT - 1) / kT);
+    if (d.dim == 2) k_family_transpose<2><<<b, kT, 0, s>>>(d, colT, coefT, xiT);
+    else k_family_transpose<3><<<b, kT, 0, s>>>(d, colT, coefT, xiT);
+    check("family_transpose");
+}
+void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* xiT,
+                    const double* x, const uint32_t* mask, double* ubar, cudaStream_t s) {
+    const int b = (int)(((long long)d.E * 32 + kT - 1) / kT);
+    if (d.dim == 2) {
+        k_pd_ubar<2><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+        k_pd_force_lin_t<2><<<b, kT, 0, s>>>(d, colT, coefT, xiT, ubar, mask);
+    } else {
+        k_pd_ubar<3><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+        k_pd_force_lin_t<3><<<b, kT, 0, s>>>(d, colT, coefT, xiT, ubar, mask);
+    }
+    check("pd_force_lin_t");
 }
 void pd_node_explicit(const DevPD& d, const double* ra, double ra_scale, const double* M,
                       const uint8_t* cf, const double* rv, const double* rd, double gdt,
@@ -628,6 +778,17 @@ void dot(int n, const double* x, const double* y, double* part, double* out, cud
     k_dot_partial<<<nb, kT, 0, s>>>(n, x, y, part);
     k_sum_partials<<<1, kT, 0, s>>>(nb, part, out);
     check("dot");
+}
+void dot_fin(int n, const double* x, const double* y, const double* x2, const double* y2,
+             double* part, unsigned* ticket, double* out, double* out2, int mode, double* num,
+             double* sc, cudaStream_t s) {
+    k_dot_fin<<<dot_partials(), kT, 0, s>>>(n, x, y, x2, y2, part, ticket, out, out2, mode, num, sc);
+    check("dot_fin");
+}
+void cg_update_precond(int n, const double* alpha_dev, const double* p, const double* ap,
+                       double* x, double* r, const double* jac, double* z, cudaStream_t s) {
+    k_cg_update_precond<<<blocks(n), kT, 0, s>>>(n, alpha_dev, p, ap, x, r, jac, z);
+    check("cg_update_precond");
 }
 void ratio(const double* num, const double* den, double* out, cudaStream_t s) {
     k_ratio<<<1, 1, 0, s>>>(num, den, out);

@@ -66,6 +66,17 @@ void xpby(int n, const double* z, const double* beta_dev, double* p, cudaStream_
 int dot_partials();
 void dot(int n, const double* x, const double* y, double* part, double* out, cudaStream_t s);
 void ratio(const double* num, const double* den, double* out, cudaStream_t s);
+// entry-major families (colT, coefT: E K; xiT: E K dim) and the linear force on them
+void family_transpose(const DevPD& d, int32_t* colT, double* coefT, double* xiT, cudaStream_t s);
+void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* xiT,
+                    const double* x, const uint32_t* mask, double* ubar, cudaStream_t s);
+// fused CG steps (bitwise the unfused sequence): dot(s) + the CG scalar in one launch
+// (part: 2 dot_partials() doubles, ticket: a zeroed counter), update + precondition
+void dot_fin(int n, const double* x, const double* y, const double* x2, const double* y2,
+             double* part, unsigned* ticket, double* out, double* out2, int mode, double* num,
+             double* sc, cudaStream_t s);
+void cg_update_precond(int n, const double* alpha_dev, const double* p, const double* ap,
+                       double* x, double* r, const double* jac, double* z, cudaStream_t s);
 void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream_t s);
 void csr_spmv_warp(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
                    double* y, cudaStream_t s);

@@ -176,6 +176,12 @@ struct pmts_mts {
     double *cg_b = nullptr, *cg_x = nullptr, *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr,
            *cg_ap = nullptr, *cg_kx = nullptr;                             // size max(nf, nl)
     double *part = nullptr, *scal = nullptr;                               // reductions
+    double* part2 = nullptr;      // fused CG dots: two partial rows
+    unsigned* ticket = nullptr;   // their last-block counter
+    bool fused_cg = true;         // PMTS_MTS_UNFUSED_CG=1: the eleven-node iteration
+    int32_t* famT_col = nullptr;  // entry-major families (PMTS_MTS_NO_TRANSPOSE=1: none)
+    double* famT_coef = nullptr;
+    double* famT_xi = nullptr;
     double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
     int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
     double* hfe_v = nullptr;
@@ -259,6 +265,12 @@ struct pmts_mts {
     void fe_K(const double* x, double* y) { mtsk::csr_spmv(nf, fe_rp, fe_ci, fe_v, x, y, stream); }
     // K^PD x with the given bond mask; do_break: the inclusive stretch test on x
     // updates that mask (count into slot)
+    // linear PD force (centroid form) on the entry-major families when built
+    void force_lin(const double* x, const uint32_t* mask) {
+        if (famT_col) mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, famT_xi, x, mask, pd_ubar, stream);
+        else mtsk::pd_force_lin(pdv, x, mask, pd_ubar, stream);
+    }
+
     void pd_K(const double* x, double* y, uint32_t* mask, bool do_break, int slot) {
         mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream);
         launch_node_force(pdv, y, stream);
@@ -294,8 +306,18 @@ struct pmts_mts {
         double rnorm = std::sqrt(scalar(s_rr));
         // the iteration body (same arithmetic as the reference's loop) as one CUDA
         // graph over fixed buffers: one launch and one 16-byte readback per iteration
+        // (fused: p.Ap and alpha in one launch, the update with the preconditioner,
+        // r.z, r.r, beta and rz <- rz_new in one launch -- bitwise the unfused order)
         auto body = [&] {
             op(p, ap);
+            if (fused_cg) {
+                mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
+                              s_alpha, stream);
+                mtsk::cg_update_precond(n, s_alpha, p, ap, x, r, jac, z, stream);
+                mtsk::dot_fin(n, r, z, r, r, part2, ticket, s_rzn, s_rr, 2, s_rz, s_beta, stream);
+                mtsk::xpby(n, z, s_beta, p, stream);
+                return;
+            }
             mtsk::dot(n, p, ap, part, s_pap, stream);
             mtsk::ratio(s_rz, s_pap, s_alpha, stream);
             mtsk::cg_update(n, s_alpha, p, ap, x, r, stream);
@@ -393,7 +415,7 @@ struct pmts_mts {
         if (do_break || !homog)  // free substeps: the deterministic per-entry arithmetic
             mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream);
         else  // homogeneous linear substeps (unit, link, interface): centroid form
-            mtsk::pd_force_lin(pdv, rdp, mask, pd_ubar, stream);
+            force_lin(rdp, mask);
         mtsk::pd_node_explicit(pdv, ra, ra_scale, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
                                pd_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
     }
@@ -449,7 +471,7 @@ struct pmts_mts {
         zero_vec(rd, np);
         zero_vec(rv, np);
         for (int j = 1; j <= m; ++j) {
-            if (j > 1) mtsk::pd_force_lin(pdv, rd, mask_sync, pd_ubar, stream);
+            if (j > 1) force_lin(rd, mask_sync);
             double* out = out_rows ? out_rows + (size_t)j * nl : (j == m ? out_last : nullptr);
             mtsk::pd_node_lin(pdv, j > 1 ? 1 : 0, w_dev, row_of, double(j) / m, pd_M, pd_cf,
                               pd_nm.gdt, pd_nm.bdt2, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, y.u, y.v, y.a,
@@ -1039,6 +1061,13 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         pd_internal_pair_weights(h->pd, h->pe_weight.data());
         h->pdv = pd_internal_dev(h->pd);
         h->mask_live = h->pdv.mask;
+        if (!std::getenv("PMTS_MTS_NO_TRANSPOSE")) {
+            const size_t ek = (size_t)h->pdv.E * h->pdv.K;
+            h->famT_col = h->alloc<int32_t>(ek);
+            h->famT_coef = h->alloc<double>(ek);
+            h->famT_xi = h->alloc<double>(ek * h->pdv.dim);
+            mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->famT_xi, h->stream);
+        }
         h->mask_words = (size_t)h->pdv.W * h->pdv.E;
         h->mask_sync = h->alloc<uint32_t>(h->mask_words);
         CKM(cudaMemcpy(h->mask_sync, h->mask_live, sizeof(uint32_t) * h->mask_words,
@@ -1112,6 +1141,10 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         for (double** p : {&h->cg_b, &h->cg_x, &h->cg_r, &h->cg_z, &h->cg_p, &h->cg_ap, &h->cg_kx})
             *p = h->alloc<double>(nmax);
         h->part = h->alloc<double>(mtsk::dot_partials());
+        h->part2 = h->alloc<double>(2 * mtsk::dot_partials());
+        h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
+        CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
+        h->fused_cg = !std::getenv("PMTS_MTS_UNFUSED_CG");
         CKM(cudaMallocHost(&h->h_pin, 4 * sizeof(double)));
         h->scal = h->alloc<double>(16);
         h->lam_d = h->alloc<double>(h->nl);
