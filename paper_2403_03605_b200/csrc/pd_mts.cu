@@ -282,6 +282,27 @@ __global__ void __launch_bounds__(kT) k_dot_fin(int n, const double* x, const do
     }
 }
 
+// The CG loop test of cg_solve (linalg.hpp:243-296) on the device, at the end of
+// each iteration of the graph's WHILE body: the host's checks in the host's order
+// (p'Ap <= 0 -> not positive definite; sqrt(rr) / sqrt(bb) > tol -> continue;
+// continuing past max_iter -> no convergence), with IEEE sqrt and division, so the
+// iteration count is the host loop's.  status: 0 converged, 1 not SPD, 2 max_iter.
+__global__ void k_cg_cond(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
+                          const double* s_pap, double tol, int max_iter, int* it_status) {
+    const int it = ++it_status[0];
+    bool more = false;
+    if (*s_pap <= 0.0) {
+        it_status[1] = 1;
+    } else {
+        more = sqrt(*s_rr) / sqrt(*s_bb) > tol;
+        if (more && it >= max_iter) {
+            it_status[1] = 2;
+            more = false;
+        }
+    }
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
 // x += alpha p; r -= alpha ap; z = precond(r): k_cg_update then k_precond, fused
 __global__ void k_cg_update_precond(int n, const double* alpha_dev, const double* p,
                                     const double* ap, double* x, double* r, const double* jac,
@@ -784,6 +805,11 @@ void dot_fin(int n, const double* x, const double* y, const double* x2, const do
              double* sc, cudaStream_t s) {
     k_dot_fin<<<dot_partials(), kT, 0, s>>>(n, x, y, x2, y2, part, ticket, out, out2, mode, num, sc);
     check("dot_fin");
+}
+void cg_cond(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
+             const double* s_pap, double tol, int max_iter, int* it_status, cudaStream_t s) {
+    k_cg_cond<<<1, 1, 0, s>>>(h, s_bb, s_rr, s_pap, tol, max_iter, it_status);
+    check("cg_cond");
 }
 void cg_update_precond(int n, const double* alpha_dev, const double* p, const double* ap,
                        double* x, double* r, const double* jac, double* z, cudaStream_t s) {

@@ -70,6 +70,9 @@ void ratio(const double* num, const double* den, double* out, cudaStream_t s);
 void family_transpose(const DevPD& d, int32_t* colT, double* coefT, double* xiT, cudaStream_t s);
 void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* xiT,
                     const double* x, const uint32_t* mask, double* ubar, cudaStream_t s);
+// the CG loop test on the device (conditional WHILE graph node); it_status: {iterations, status}
+void cg_cond(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
+             const double* s_pap, double tol, int max_iter, int* it_status, cudaStream_t s);
 // fused CG steps (bitwise the unfused sequence): dot(s) + the CG scalar in one launch
 // (part: 2 dot_partials() doubles, ticket: a zeroed counter), update + precondition
 void dot_fin(int n, const double* x, const double* y, const double* x2, const double* y2,

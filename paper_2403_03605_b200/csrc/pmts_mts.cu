@@ -205,6 +205,8 @@ struct pmts_mts {
         if (stream) cudaStreamSynchronize(stream);
         for (auto& g : cg_graph)
             if (g) cudaGraphExecDestroy(g);
+        for (auto& g : cg_loop)
+            if (g) cudaGraphExecDestroy(g);
         if (h_pin) cudaFreeHost(h_pin);
         for (void* p : owned) cudaFree(p);
         if (pd) pmts_pd_destroy(pd);
@@ -328,6 +330,59 @@ struct pmts_mts {
             CKM(cudaMemcpyAsync(s_rz, s_rzn, sizeof(double), cudaMemcpyDeviceToDevice, stream));
             mtsk::dot(n, r, r, part, s_rr, stream);
         };
+        if (device_loop) {
+            // the whole loop as one graph: a conditional WHILE node whose body is the
+            // iteration plus the loop test (k_cg_cond) -- no host round trip per iteration
+            cudaGraphExec_t& gl = cg_loop[graph_id];
+            if (gl && (cg_loop_x[graph_id] != x || cg_loop_tol[graph_id] != tol ||
+                       cg_loop_max[graph_id] != max_iter)) {
+                cudaGraphExecDestroy(gl);
+                gl = nullptr;
+            }
+            if (!gl) {
+                cudaGraph_t g;
+                CKM(cudaGraphCreate(&g, 0));
+                cudaGraphConditionalHandle hnd;
+                CKM(cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault));
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = hnd;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t node;
+                CKM(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+                cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+                CKM(cudaStreamBeginCaptureToGraph(stream, bodyg, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+                body();
+                mtsk::cg_cond(hnd, s_bb, s_rr, s_pap, tol, max_iter, it_status, stream);
+                CKM(cudaStreamEndCapture(stream, &bodyg));
+                CKM(cudaGraphInstantiate(&gl, g, 0));
+                cudaGraphDestroy(g);
+                cg_loop_x[graph_id] = x;
+                cg_loop_tol[graph_id] = tol;
+                cg_loop_max[graph_id] = max_iter;
+            }
+            if (!(rnorm / bnorm > tol)) return 0;
+            if (max_iter <= 0)
+                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
+                                  " iterations, residual " + std::to_string(rnorm / bnorm));
+            CKM(cudaMemsetAsync(it_status, 0, 2 * sizeof(int), stream));
+            CKM(cudaGraphLaunch(gl, stream));
+            CKM(cudaMemcpyAsync(h_pin, scal + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+            CKM(cudaMemcpyAsync(h_pin + 2, it_status, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CKM(cudaStreamSynchronize(stream));
+            int hs[2];
+            std::memcpy(hs, h_pin + 2, sizeof(hs));
+            if (hs[1] == 1)
+                throw SolverError("cg: operator not positive definite (p'Ap = " +
+                                  std::to_string(h_pin[1]) + ")");
+            if (hs[1] == 2)
+                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
+                                  " iterations, residual " +
+                                  std::to_string(std::sqrt(h_pin[0]) / bnorm));
+            return hs[0];
+        }
         cudaGraphExec_t& ge = cg_graph[graph_id];
         if (ge && cg_graph_x[graph_id] != x) {  // x is baked into the graph
             cudaGraphExecDestroy(ge);
@@ -360,6 +415,12 @@ struct pmts_mts {
         return it;
     }
     cudaGraphExec_t cg_graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t cg_loop[2] = {nullptr, nullptr};  // device-side loops (conditional node)
+    const double* cg_loop_x[2] = {nullptr, nullptr};
+    double cg_loop_tol[2] = {0.0, 0.0};
+    int cg_loop_max[2] = {0, 0};
+    int* it_status = nullptr;  // {iterations, status} of the device-side loop
+    bool device_loop = true;   // PMTS_MTS_HOST_CG=1: host-driven loop, one graph per iteration
     const double* cg_graph_x[2] = {nullptr, nullptr};
     double* h_pin = nullptr;  // pinned: (rr, pap) of the last iteration
     void sub(int n, const double* b, const double* ap, double* r) {
@@ -1145,6 +1206,8 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
         CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
         h->fused_cg = !std::getenv("PMTS_MTS_UNFUSED_CG");
+        h->device_loop = !std::getenv("PMTS_MTS_HOST_CG");
+        h->it_status = reinterpret_cast<int*>(h->alloc<double>(1));
         CKM(cudaMallocHost(&h->h_pin, 4 * sizeof(double)));
         h->scal = h->alloc<double>(16);
         h->lam_d = h->alloc<double>(h->nl);
