@@ -76,3 +76,12 @@ def test_scenario_config_errors():
     sc["mesh"]["spacing"] = 0.0013  # not a divisor of the extent (mesh.hpp:181-183)
     with pytest.raises(capi.ConfigError):
         Scenario(sc)
+
+
+def test_mode_enum_matches_binding():
+    """enum pmts_mode of the header (deterministic, fast, fp32-position variant) and
+    the Python constants agree."""
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    vals = dict((k, int(v)) for k, v in re.findall(r"\b(PMTS_(?:DETERMINISTIC|FAST|FAST_F32POS))\s*=\s*(\d+)", text))
+    assert vals == {"PMTS_DETERMINISTIC": capi.DETERMINISTIC, "PMTS_FAST": capi.FAST,
+                    "PMTS_FAST_F32POS": capi.FAST_F32POS}
