@@ -111,12 +111,15 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full capture."""
+def _ncu_traffic(kernel: str, workload: str = ""):
+    """dram bytes per launch of `kernel` (on `workload` when captured per workload)
+    from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+            t = json.load(f)
+        e = t.get(f"{kernel}@{workload}") or t.get(kernel, {})
+        return e.get("dram_bytes_per_launch")
     return None
 
 
@@ -377,7 +380,7 @@ def bench_native(args):
              1: "k_lat3_bond" if info["stencil_size"] == 122 else "k_lat_bond"}.get(
                  info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": _ncu_traffic(kname),
+            "frac": achieved / peak, "traffic": _ncu_traffic(kname, args.workload),
             "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],
             "avg_launch_us": bond_avg_s * 1e6,
             "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
