@@ -80,6 +80,8 @@ void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
 struct Tile9Maps {
     CUtensorMap rd, rv, im;
     int prefetch_ahead;  // > 0: each CTA prefetches into L2 the boxes of tile id + this
+    int row_base = 0;    // first tile row of this launch (set by launch_tile9_step)
+    int grid_rows = 0;   // tile rows of the whole lattice
 };
 void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y);
 // Pair-symmetric force constants of the 14 positive offsets of the 28-offset
@@ -105,7 +107,9 @@ int tile9_configure();  // returns resident CTAs per SM
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
                        int step, int do_break, double scale, int write_state, bool f32,
-                       cudaStream_t s);
+                       cudaStream_t s, int row_first = 0, int row_end = -1);
+int tile9_rows(const LatticeDev& L);  // tile rows of the grid (node rows j0 = 31 r ...)
+int tile9_tile_rows();                // element rows per tile (31)
 
 // 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class
 // (1,2,3,4,5,6,8,9): c = w c(h|o|) h^2, and the bit patterns of the smallest /

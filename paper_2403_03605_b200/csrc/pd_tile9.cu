@@ -375,7 +375,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     unsigned* red = reinterpret_cast<unsigned*>(sm + kOffRed);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nx = L.nx, ny = L.ny, NX = nx + 1, NY = ny + 1;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    // a launch may cover a range of tile rows (halo-overlap split, pmts_pd.cu)
+    const int by = maps.row_base + blockIdx.y;
+    const int i0 = blockIdx.x * TX, j0 = by * TY;
     const int ax0 = i0 - 1 - R, ay0 = j0 - 1 - R;
     const int ie = i0 & ~1;  // {1/M, flags} box start: 16-byte aligned global row start
 
@@ -402,8 +404,8 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         // warm L2 for the tile that takes this CTA's slot a wave later
         const int ahead = maps.prefetch_ahead;
         if (ahead > 0) {
-            const int t = blockIdx.y * gridDim.x + blockIdx.x + ahead;
-            if (t < gridDim.x * gridDim.y) {
+            const int t = by * gridDim.x + blockIdx.x + ahead;
+            if (t < gridDim.x * maps.grid_rows) {
                 const int pi0 = (t % gridDim.x) * TX, pj0 = (t / gridDim.x) * TY;
                 const int pax0 = pi0 - 1 - R, pay0 = pj0 - 1 - R;
                 tma_prefetch_2d(&maps.rd, 2 * pax0, pay0);
@@ -415,7 +417,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     if constexpr (REPORT) {
         // pmts_pd_step_tracked: the step's u is the predictor it consumes (beta = 0);
         // block (0, 0) copies the tracked dofs of it into mapped pinned host memory
-        if ((blockIdx.x | blockIdx.y) == 0)
+        if ((blockIdx.x | by) == 0)
             for (int j = threadIdx.x; j < bf.n_trk; j += NT) bf.trk_host[j] = bf.rd_in[bf.trk_dofs[j]];
     }
     if (ax0 >= 0 && ay0 >= 0 && ax0 + AX <= nx && ay0 + MY <= ny) {
@@ -688,7 +690,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     //     The grid has floor(n/31) + 1 blocks per axis, so the last block owns at
     //     most 31 node columns / rows including the domain's far node line.
     const int ox = (blockIdx.x == gridDim.x - 1) ? NX - i0 : TX;
-    const int oy = (blockIdx.y == gridDim.y - 1) ? NY - j0 : TY;
+    const int oy = (by == maps.grid_rows - 1) ? NY - j0 : TY;
     double2* rdo = reinterpret_cast<double2*>(bf.rd_out);
     double2* rv2 = reinterpret_cast<double2*>(d.rv);
     const double2* P2 = reinterpret_cast<const double2*>(d.P);
@@ -736,6 +738,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
 }
 
+int tile9_rows(const LatticeDev& L) { return L.ny / TY + 1; }
+int tile9_tile_rows() { return TY; }
+
 void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y) {
     *rd_x = 2 * BX;
     *rd_y = BY;
@@ -781,9 +786,15 @@ bool pdl_enabled() {
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
                        int step, int do_break, double scale, int write_state, bool f32,
-                       cudaStream_t s) {
+                       cudaStream_t s, int row_first, int row_end) {
     if (f32 && !ps) throw std::runtime_error("tile9: the fp32-position variant needs the pair stencil");
-    dim3 grid(L.nx / TX + 1, L.ny / TY + 1, 1);
+    const int rows = tile9_rows(L);
+    if (row_end < 0) row_end = rows;
+    if (row_first >= row_end) return;
+    dim3 grid(L.nx / TX + 1, row_end - row_first, 1);
+    Tile9Maps mp = maps;
+    mp.row_base = row_first;
+    mp.grid_rows = rows;
     const PairStencil2D none{};
     const PairStencil2D& p = ps ? *ps : none;
     cudaLaunchConfig_t cfg{};
@@ -797,7 +808,7 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
 #define PMTS_T9_LAUNCH(B, P, Q, F) \
-    cudaLaunchKernelEx(&cfg, k_tile9<B, P, Q, F>, d, L, st, p, maps, b, step, scale, write_state)
+    cudaLaunchKernelEx(&cfg, k_tile9<B, P, Q, F>, d, L, st, p, mp, b, step, scale, write_state)
 #define PMTS_T9_PICK(Q)                                              \
     if (f32) {                                                       \
         if (do_break) PMTS_T9_LAUNCH(true, true, Q, true);           \

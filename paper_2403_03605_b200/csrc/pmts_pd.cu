@@ -114,6 +114,11 @@ struct pmts_pd {
     // slab decomposition: NCCL clique + halo rows (node ranges, local ids)
     void* comm = nullptr;            // ncclComm_t
     int peer_lo = -1, peer_hi = -1;
+    // halo overlap (tile kernel with peers): the tile rows holding halo send / receive
+    // rows launch first, the exchange runs on xstream while the interior rows compute
+    int split_a = -1, split_b = -1;  // edge rows [0, a) and [b, rows); -1: not planned
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_edge = nullptr, ev_x = nullptr;
     int send_lo = 0, recv_lo = 0, n_lo = 0, send_hi = 0, recv_hi = 0, n_hi = 0;
     unsigned long long* h_counts = nullptr;  // pinned
     void* h_map = nullptr;                   // mapped pinned staging (step_tracked)
@@ -162,6 +167,7 @@ double micromodulus(const pmts_pd_desc& dsc, int dim, double r) {
 }
 
 bool try_lattice(pmts_pd* h, const int32_t* dcol = nullptr);
+void plan_split(pmts_pd* h);
 
 // ---- NCCL, resolved at run time (libpmts loads without it; the halo exchange
 // of the slab decomposition is the only user).  Types follow nccl.h 2.x.
@@ -213,23 +219,24 @@ void nccl_check(ncclResult_t r, const char* what) {
 constexpr ncclDataType_t kNcclFloat64 = ncclFloat64;
 
 // halo exchange of the predictor displacement after a fine step
-void exchange_halo(pmts_pd* h) {
+void exchange_halo(pmts_pd* h, double* rd = nullptr, cudaStream_t st = nullptr) {
     if (!h->comm || (h->peer_lo < 0 && h->peer_hi < 0)) return;
     NcclApi& a = nccl();
     const int dim = h->dim;
-    double* rd = h->d.rd;
+    if (!rd) rd = h->d.rd;
+    if (!st) st = h->stream;
     nccl_check(a.group_start(), "group");
     if (h->peer_lo >= 0) {
         nccl_check(a.send(rd + (size_t)h->send_lo * dim, (size_t)h->n_lo * dim, kNcclFloat64,
-                          h->peer_lo, (ncclComm_t)h->comm, h->stream), "send");
+                          h->peer_lo, (ncclComm_t)h->comm, st), "send");
         nccl_check(a.recv(rd + (size_t)h->recv_lo * dim, (size_t)h->n_lo * dim, kNcclFloat64,
-                          h->peer_lo, (ncclComm_t)h->comm, h->stream), "recv");
+                          h->peer_lo, (ncclComm_t)h->comm, st), "recv");
     }
     if (h->peer_hi >= 0) {
         nccl_check(a.send(rd + (size_t)h->send_hi * dim, (size_t)h->n_hi * dim, kNcclFloat64,
-                          h->peer_hi, (ncclComm_t)h->comm, h->stream), "send");
+                          h->peer_hi, (ncclComm_t)h->comm, st), "send");
         nccl_check(a.recv(rd + (size_t)h->recv_hi * dim, (size_t)h->n_hi * dim, kNcclFloat64,
-                          h->peer_hi, (ncclComm_t)h->comm, h->stream), "recv");
+                          h->peer_hi, (ncclComm_t)h->comm, st), "recv");
     }
     nccl_check(a.group_end(), "group");
 }
@@ -746,6 +753,7 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
                 h->pst.pbit[k] = s;
             }
             h->pst.h2 = 2.0 * hh;
+            plan_split(h);
             h->pst.h2f = (float)(2.0 * hh);
             for (int k = 0; k < 14 && h->pairs; ++k) {  // fp32 candidate thresholds, rounded down
                 double c;
@@ -846,6 +854,45 @@ void ensure_counts(pmts_pd* h, int n) {
     h->d.broken_count = h->d_counts;
 }
 
+// Halo overlap plan of the tile kernel (opt-in, PMTS_T9_SPLIT=1): the tile rows that
+// own a node row the exchange sends or receives go first ([0, a) and [b, rows)); the
+// interior rows [a, b) run while ncclSend/ncclRecv move the halo on a second stream.
+// Without peers the first and last tile rows are split off, which exercises the
+// launch split on one GPU.  Off by default: on one B200 the split costs 15 us per
+// cfg3 step (three launches, the cross-stream events break programmatic dependent
+// launch) -- about the NCCL latency it would hide.
+void plan_split(pmts_pd* h) {
+    const bool peers = h->comm && (h->peer_lo >= 0 || h->peer_hi >= 0);
+    const bool forced = std::getenv("PMTS_T9_SPLIT") != nullptr;
+    h->split_a = h->split_b = -1;
+    if (!h->tile9 || !forced) return;
+    const int rows = tile9_rows(h->L), ty = tile9_tile_rows(), NX = h->L.nx + 1;
+    auto tile_row = [&](int node) { return std::min(node / NX / ty, rows - 1); };
+    int a = forced && !peers ? 1 : 0, b = forced && !peers ? rows - 1 : rows;
+    auto cover_lo = [&](int first, int n) {
+        if (n > 0) a = std::max(a, tile_row(first + n - 1) + 1);
+    };
+    auto cover_hi = [&](int first, int n) {
+        if (n > 0) b = std::min(b, tile_row(first));
+    };
+    if (h->peer_lo >= 0) {
+        cover_lo(h->send_lo, h->n_lo);
+        cover_lo(h->recv_lo, h->n_lo);
+    }
+    if (h->peer_hi >= 0) {
+        cover_hi(h->send_hi, h->n_hi);
+        cover_hi(h->recv_hi, h->n_hi);
+    }
+    if (a > b) return;  // the halo rows span the slab: no interior to overlap with
+    if (!h->xstream) {
+        CK(cudaStreamCreateWithFlags(&h->xstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_edge, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
+    }
+    h->split_a = a;
+    h->split_b = b;
+}
+
 // one fine step: bond gather + node update with the fused predictor
 void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_t* ev,
                   bool last = true, const double* scale_dev = nullptr,
@@ -862,6 +909,27 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
             b.trk_host = report->trk_host;
         }
         if (time_bond) CK(cudaEventRecord(ev[0], h->stream));
+        if (h->tile9 && h->split_a >= 0) {
+            // edge tile rows, then the halo exchange on xstream overlapping the interior
+            const Tile9Maps mp = tile9_maps(h);
+            const PairStencil2D* ps = h->pairs ? &h->pst : nullptr;
+            const int rows = tile9_rows(h->L);
+            launch_tile9_step(h->d, h->L, h->st2, ps, mp, b, slot, brk, scale, last ? 1 : 0,
+                              h->f32pos, h->stream, 0, h->split_a);
+            launch_tile9_step(h->d, h->L, h->st2, ps, mp, b, slot, brk, scale, last ? 1 : 0,
+                              h->f32pos, h->stream, h->split_b, rows);
+            CK(cudaEventRecord(h->ev_edge, h->stream));
+            CK(cudaStreamWaitEvent(h->xstream, h->ev_edge, 0));
+            exchange_halo(h, h->rd_alt, h->xstream);  // the buffer this step just wrote
+            CK(cudaEventRecord(h->ev_x, h->xstream));
+            launch_tile9_step(h->d, h->L, h->st2, ps, mp, b, slot, brk, scale, last ? 1 : 0,
+                              h->f32pos, h->stream, h->split_a, h->split_b);
+            CK(cudaStreamWaitEvent(h->stream, h->ev_x, 0));  // before anything that follows
+            if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
+            std::swap(h->d.rd, h->rd_alt);
+            std::swap(h->d.mask, h->mask_alt);
+            return;
+        }
         if (h->tile9)
             launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
                               slot, brk, scale, last ? 1 : 0, h->f32pos, h->stream);
@@ -1105,6 +1173,13 @@ void pmts_pd_destroy(pmts_pd* h) {
         unsigned long long c[2] = {0, 0};
         cudaMemcpy(c, h->st3.hot_count, 16, cudaMemcpyDeviceToHost);
         std::fprintf(stderr, "pmts: lat3 screen: %llu of %llu tiles hot\n", c[0], c[1]);
+    }
+    if (h && h->xstream) {
+        cudaStreamSynchronize(h->xstream);
+        cudaStreamDestroy(h->xstream);
+        cudaEventDestroy(h->ev_edge);
+        cudaEventDestroy(h->ev_x);
+        h->xstream = nullptr;
     }
     if (h && h->comm) {
         if (h->stream) cudaStreamSynchronize(h->stream);
@@ -1631,6 +1706,7 @@ int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t
         h->send_hi = send_hi_first;
         h->recv_hi = recv_hi_first;
         h->n_hi = n_hi;
+        plan_split(h);
     });
 }
 

@@ -589,3 +589,27 @@ def test_cfg3_f32pos_vs_fp64_over_1500_steps(cfg3):
     assert b0.sum() > 10000
     assert 1.0 - np.logical_xor(b0, b1).sum() / b0.sum() >= 0.999
     assert np.linalg.norm(u1 - u0) <= 1e-6 * np.linalg.norm(u0)
+
+
+@pytest.mark.parametrize("nx,ny,steps", [(124, 62, 200), (64, 93, 150), (60, 35, 150)])
+def test_tile9_split_launch_bitwise(nx, ny, steps, monkeypatch):
+    """The halo-overlap launch split (edge tile rows, then the interior while the
+    exchange runs; forced on one GPU by PMTS_T9_SPLIT=1) is bitwise the single
+    launch: same fields, bond states and per-step broken counts, tracked rows too."""
+    sc = _plate(nx, ny)
+    out = {}
+    for split in (True, False):
+        if split:
+            monkeypatch.setenv("PMTS_T9_SPLIT", "1")
+        else:
+            monkeypatch.delenv("PMTS_T9_SPLIT", raising=False)
+        s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+        s.initial_acceleration(sc.load_scale(0.0))
+        nb = s.step([sc.load_scale(i * sc.dt) for i in range(1, steps + 1)])
+        trk, cnt = s.step_tracked([sc.load_scale(i * sc.dt) for i in range(steps + 1, steps + 21)],
+                                  np.array([1, 2 * (sc.n_nodes // 2), 2 * sc.n_nodes - 1], np.int32))
+        out[split] = (nb, *s.state(), s.intact(), trk, cnt)
+    a, b = out[True], out[False]
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
