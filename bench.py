@@ -374,6 +374,15 @@ def bench_native(args):
     # roofline of the dominant (bond) kernel
     peak, peak_src = _peaks()
     bond_avg_s = bond_ms * 1e-3 / K
+    timing = "each launch between its own pair of CUDA events (profile pass)"
+    if info["kernels_per_step"] == 1 and not dist:
+        # one kernel per step (the 2D tile kernel): the timed region's K back-to-back
+        # launches between two events on the launching stream ARE the kernel's launches;
+        # per-launch events would break programmatic dependent launch, which overlaps
+        # each launch with the previous one's tail
+        bond_avg_s = ms * 1e-3 / K
+        timing = ("timed region: K back-to-back launches of the step's only kernel between two "
+                  "CUDA events on its stream (programmatic dependent launch on)")
     achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
     fused = {"tile9": "k_tile9", "tile": "k_fused2d", "tma": "k_tma2d", "strip": "k_strip2d"}
     kname = {2: fused.get(os.environ.get("PMTS_FUSED_KERNEL", "tile9"), "k_tile9"),
@@ -382,7 +391,8 @@ def bench_native(args):
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": _ncu_traffic(kname, args.workload),
             "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],
-            "avg_launch_us": bond_avg_s * 1e6,
+            "avg_launch_us": bond_avg_s * 1e6, "launch_timing": timing,
+            "avg_launch_us_isolated": bond_ms * 1e3 / K,
             "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
     # the bond work is fp64-arithmetic heavy: 14 flops per directed entry in fast
     # mode (eta 2, xi.eta 3, force 4, |eta|^2 3, test 2) = 28 per unique bond
