@@ -5,11 +5,14 @@
  * rounds exactly as the reference's.  Citations are
  * /root/reference/proj/<path>:<line>.
  */
+#define _POSIX_C_SOURCE 200809L
 #include "pd_oracle.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <pthread.h>
+#include <unistd.h>
 
 #define MAXNN 8
 
@@ -505,10 +508,43 @@ double po_bond_stretch(const po_pd* h, int64_t pair, const double* u) {
     return stretch_q(h, pair, u);
 }
 
+/* Independent-iteration loops over a few host threads (pthreads; no OpenMP
+ * runtime in this image).  Every iteration writes only its own outputs, so the
+ * results do not depend on the thread count.  PO_THREADS overrides the count. */
+typedef struct { po_pd* h; const double* x; double* y; } mf_ctx;
+typedef void (*range_fn)(void*, int64_t, int64_t);
+typedef struct { range_fn fn; void* ctx; int64_t lo, hi; } par_job;
+static void* par_run(void* a) {
+    par_job* j = (par_job*)a;
+    j->fn(j->ctx, j->lo, j->hi);
+    return 0;
+}
+static void par_for(int64_t n, range_fn fn, void* ctx) {
+    static int nt = 0;
+    if (!nt) {
+        const char* e = getenv("PO_THREADS");
+        nt = e ? atoi(e) : (int)sysconf(_SC_NPROCESSORS_ONLN);
+        if (nt < 1) nt = 1;
+        if (nt > 64) nt = 64;
+    }
+    int t = n < 65536 ? 1 : nt;
+    if (t == 1) { fn(ctx, 0, n); return; }
+    pthread_t th[64];
+    par_job jb[64];
+    for (int k = 0; k < t; ++k) {
+        jb[k].fn = fn; jb[k].ctx = ctx;
+        jb[k].lo = n * k / t; jb[k].hi = n * (k + 1) / t;
+        if (k) pthread_create(&th[k], 0, par_run, &jb[k]);
+    }
+    par_run(&jb[0]);
+    for (int k = 1; k < t; ++k) pthread_join(th[k], 0);
+}
+static void mf_elems(void* vc, int64_t e0, int64_t e1);
+static void mf_nodes(void* vc, int64_t n0, int64_t n1);
+
 /* K*x into y: CSR row sums in column order (linalg.hpp:209-221) or the
  * matrix-free element/node gathers (DESIGN.md deterministic order). */
 static void apply_k(po_pd* h, const double* x, double* y) {
-    const int d = h->dim, nn = h->nn;
     if (h->variant == PO_CSR) {
         for (int r = 0; r < h->n_dof; ++r) {
             double s = 0.0;
@@ -517,7 +553,18 @@ static void apply_k(po_pd* h, const double* x, double* y) {
         }
         return;
     }
-    for (int e = 0; e < h->n_elems; ++e) {
+    /* per element / per node gathers are independent: threads change nothing */
+    mf_ctx ctx = {h, x, y};
+    par_for(h->n_elems, mf_elems, &ctx);
+    par_for(h->n_nodes, mf_nodes, &ctx);
+}
+
+static void mf_elems(void* vc, int64_t e0, int64_t e1) {
+    const mf_ctx* cx = (const mf_ctx*)vc;
+    po_pd* h = cx->h;
+    const double* x = cx->x;
+    const int d = h->dim, nn = h->nn;
+    for (int e = (int)e0; e < (int)e1; ++e) {
         double G[3] = {0.0, 0.0, 0.0};
         for (int k = h->fptr[e]; k < h->fptr[e + 1]; ++k) {
             const int64_t q = h->fpair[k];
@@ -544,13 +591,26 @@ static void apply_k(po_pd* h, const double* x, double* y) {
         }
         for (int c = 0; c < d; ++c) h->G[3 * e + c] = G[c];
     }
-    for (int n = 0; n < h->n_nodes; ++n)
+}
+
+static void mf_nodes(void* vc, int64_t n0, int64_t n1) {
+    const mf_ctx* cx = (const mf_ctx*)vc;
+    const po_pd* h = cx->h;
+    double* y = cx->y;
+    const int d = h->dim;
+    for (int n = (int)n0; n < (int)n1; ++n)
         for (int c = 0; c < d; ++c) {
             double s = 0.0;
             for (int k = h->nptr[n]; k < h->nptr[n + 1]; ++k)
                 s = s + h->N * h->G[3 * h->nel[k] + c];
             y[n * d + c] = s;
         }
+}
+
+static void mark_breaks(void* vc, int64_t q0, int64_t q1) {
+    po_pd* h = ((mf_ctx*)vc)->h;
+    for (int64_t q = q0; q < q1; ++q)
+        if (h->mu[q] && stretch_q(h, q, h->u) >= h->scrit[q]) h->mu[q] = 2;
 }
 
 void po_pd_init(po_pd* h, double scale0) {
@@ -586,14 +646,16 @@ int64_t po_pd_step(po_pd* h, int n, const double* scales, int32_t* broken_out,
         for (int c = 0; c < h->n_bc; ++c) h->v[h->bc_dofs[c]] = h->bc_vel[c];
         /* update_bond_states perifem.hpp:170-193 (s >= s_crit inclusive) */
         if (!(h->s_crit > 0.0 && isfinite(h->s_crit))) continue;
+        /* the per-pair test in parallel (mu 2 = breaks this step), then the
+         * delta list in ascending pe order, as the reference appends it */
+        mf_ctx bx = {h, 0, 0};
+        par_for(h->n_pairs, mark_breaks, &bx);
         int64_t nnew = 0;
-        for (int64_t q = 0; q < h->n_pairs; ++q) {
-            if (!h->mu[q]) continue;
-            if (stretch_q(h, q, h->u) >= h->scrit[q]) {
+        for (int64_t q = 0; q < h->n_pairs; ++q)
+            if (h->mu[q] == 2) {
                 h->mu[q] = 0;
                 h->brk[nnew++] = (int32_t)q;
             }
-        }
         /* incremental_stiffness_update perifem.hpp:356-364, broken (pe,qp) order */
         if (h->variant == PO_CSR)
             for (int64_t k = 0; k < nnew; ++k) scatter_pe(h, h->brk[k], -1.0);

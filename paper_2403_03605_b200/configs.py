@@ -81,6 +81,14 @@ def scenarios() -> dict:
     s["cfg3"]["ext"] = {"micromodulus": "constant",
                         "c": 9.0 * _E / (math.pi * 1e-3 * d3 ** 3), "h": 1e-3,
                         "s_crit_spread": 0.05, "seed": 0x5eed5 + 3}
+    # cfg3's own physics (constant micromodulus c h / r^3, per-bond s0 spread, the
+    # same seed) on a 400 x 160 sub-plate at the same dx: 20 x 8 mm, the pre-crack
+    # from the left edge to mid-width at mid-height, the same 12 MPa bands.  The
+    # oracle finishes it in seconds; it cracks near step 150 (tests/test_gpu_cfg3_physics.py).
+    s["cfg3_sub"] = _plate2d(400, 160, 5e-5, E=_E, rho=_RHO, delta_factor=3.015,
+                             l_factor=1.0, s_crit=s["cfg3"]["pd"]["s_crit"], dt=5e-9,
+                             steps=400, notch=(-0.001, 0.004, 0.01, 0.004))
+    s["cfg3_sub"]["ext"] = copy.deepcopy(s["cfg3"]["ext"])
     # Reference-native analog of cfg3 (exponential kernel, scalar s_crit): the
     # form the reference arm and the deterministic path run at full size.
     s["cfg3_native"] = copy.deepcopy(s["cfg3"])

@@ -1,0 +1,266 @@
+"""BASELINE cfg3's own arithmetic on the device against the oracle.
+
+cfg3 runs two extensions of the reference (SURVEY.md 8(c) "CPU restatement for
+BASELINE-only features"): the 2D constant micromodulus c h / r^3 in place of
+material.hpp:84-88's exponential kernel, and a per-bond critical stretch
+s0 * U[0.95, 1.05] from a counter hash of (min id, max id, seed) in place of
+perifem.hpp:170-193's scalar s_crit.  The oracle (oracle/pd_oracle.c:230-250)
+restates both; here the device kernels run them:
+
+* ``cfg3_sub`` -- cfg3's physics, dx, horizon, seed and loads on a 400 x 160
+  sub-plate (cracks near step 150) -- through crack initiation and growth:
+  deterministic mode bitwise (broken list and order, u/v/a) against the
+  matrix-free oracle; the fast tile kernel (k_tile9, fp64) within the north-star
+  tolerances (1e-9 relative L2 before the first break, >= 99.9 % broken-set
+  agreement after, crack tip and crack path within one horizon); the
+  fp32-position variant within its stated tolerance (1e-5) and the same bars
+  after cracking; a 2-slab run (global-id offset in the hash) bitwise against one
+  domain.
+* full-size cfg3 (2000 x 800, 22,331,624 bonds): the device fast-forwards to the
+  first 20-step batch with breaks; the oracle takes the device state 20 steps
+  earlier and both run 80 steps through crack initiation -- fields within 1e-9
+  before the first break, broken sets >= 99.9 %, tip and path within delta.
+"""
+import numpy as np
+import pytest
+
+from crack import agreement, broken_midpoints, crack_tip, hausdorff
+from oracle import pyoracle as po
+from paper_2403_03605_b200 import capi, slabs
+from paper_2403_03605_b200 import configs as cf
+from paper_2403_03605_b200.pd import PDSolver, Scenario
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5  # fp32-position variant
+CHECK = (200, 300, 400)  # checkpoints after crack initiation
+
+
+def _oracle(sc, pairs, variant=po.MF):
+    ext = sc.cfg["ext"]
+    return po.OraclePD(dict(dim=sc.dim, n_nodes=sc.n_nodes, conn=sc.conn, centroid=sc.centroid,
+                            volume=sc.volume, pairs=pairs, mass=sc.mass, p_ext=sc.p_ext,
+                            bc_dofs=sc.bc_dofs, bc_vel=sc.bc_vel, delta=sc.delta, l=sc.l,
+                            c0=sc.c0, s_crit=sc.s_crit, dt=sc.dt, gamma=sc.gamma,
+                            beta=sc.beta, micromodulus=po.MICRO_CONST, c_const=ext["c"],
+                            h=ext["h"], s_crit_spread=ext["s_crit_spread"],
+                            seed=int(ext["seed"])), variant)
+
+
+def _rel(x, ref):
+    return np.linalg.norm(x - ref) / np.linalg.norm(ref)
+
+
+@pytest.fixture(scope="module")
+def sub():
+    """The oracle's cfg3_sub run: first break, pre-crack state, broken list, bond
+    states at the checkpoints and final state."""
+    sc = Scenario(cf.get("cfg3_sub"))
+    ext = sc.cfg["ext"]
+    assert ext["micromodulus"] == "constant" and ext["s_crit_spread"] == 0.05
+    pairs = po.find_pairs(2, sc.centroid, sc.volume, sc.delta, sc.notches())
+    o = _oracle(sc, pairs)
+    o.init(sc.load_scale(0.0))
+    out = {"sc": sc, "pairs": pairs, "broken": [], "mu": {}}
+    step, first = 0, None
+    while first is None:  # 10-step batches until the first break
+        pre = o.state()
+        br, st = o.step(sc.scales(step + 1, 10))
+        if len(br):
+            first = step + int(st[0])
+            o.set_state(*pre)  # replay up to the step before it
+            o.set_mu(np.ones(len(pairs), np.uint8))
+            if first - 1 > step:
+                o.step(sc.scales(step + 1, first - 1 - step))
+            step = first - 1
+        else:
+            step += 10
+        assert step < CHECK[0]
+    out["pre_state"], out["pre_step"] = o.state(), step
+    for c in CHECK:
+        br, st = o.step(sc.scales(step + 1, c - step))
+        out["broken"] += [(step + int(t), int(q)) for q, t in zip(br, st)]
+        out["mu"][c] = o.mu().copy()
+        step = c
+    out["final"] = o.state()
+    out["first"] = first
+    assert first is not None and 100 < first < CHECK[0]
+    assert len(out["broken"]) > 1000
+    return out
+
+
+def _device(sc, mode, **over):
+    s = PDSolver.from_scenario(sc, mode=mode, **over).find_pe_pairs()
+    s.initial_acceleration(sc.load_scale(0.0))
+    return s
+
+
+def test_cfg3_sub_device_families_and_constants(sub):
+    sc = sub["sc"]
+    s = PDSolver.from_scenario(sc, mode=capi.FAST).find_pe_pairs()
+    assert np.array_equal(s.pairs(), sub["pairs"])
+    assert s.info()["path"] == 2  # the fused 2D tile kernel (k_tile9)
+    # the per-bond hash: the device's critical stretches are the oracle's
+    # (checked through the break test below); here the hash itself on a sample
+    ext = sc.cfg["ext"]
+    vals = [po.bond_s_crit(sc.s_crit, ext["s_crit_spread"], ext["seed"], int(i), int(j))
+            for i, j in sub["pairs"][::9973]]
+    assert min(vals) >= sc.s_crit * 0.95 and max(vals) <= sc.s_crit * 1.05
+    assert max(vals) - min(vals) > 0.09 * sc.s_crit
+
+
+def test_cfg3_sub_deterministic_bitwise(sub):
+    """Deterministic mode on cfg3's arithmetic: the broken list (step, pe order),
+    u, v, a and the bond states bitwise the matrix-free oracle's."""
+    sc = sub["sc"]
+    s = _device(sc, capi.DETERMINISTIC)
+    s.step(sc.scales(1, sub["pre_step"]))
+    u, v, a = s.state()
+    for x, y in zip((u, v, a), sub["pre_state"]):
+        assert np.array_equal(x, y)
+    s.break_log(0)
+    n = CHECK[-1] - sub["pre_step"]
+    nb = s.step(sc.scales(sub["pre_step"] + 1, n))
+    log = s.break_log(nb)
+    idx = {(int(i), int(j)): q for q, (i, j) in enumerate(sub["pairs"])}
+    got = [(int(st), idx[(int(i), int(j))]) for st, i, j in log]  # global steps
+    assert got == sub["broken"]
+    assert np.array_equal(s.intact(), sub["mu"][CHECK[-1]])
+    for x, y in zip(s.state(), sub["final"]):
+        assert np.array_equal(x, y)
+
+
+def _fast_vs_oracle(sub, mode, tol):
+    sc = sub["sc"]
+    s = _device(sc, mode)
+    s.step(sc.scales(1, sub["pre_step"]))
+    u, v, _ = s.state()
+    ou, ov, _ = sub["pre_state"]
+    ru, rv = _rel(u, ou), _rel(v, ov)
+    print(f"[cfg3_sub mode {mode}] pre-crack step {sub['pre_step']}: relL2 u {ru:.3e} v {rv:.3e}")
+    assert ru <= tol and rv <= tol, (ru, rv)
+    assert s.broken_total() == 0
+    st = sub["pre_step"]
+    cen = sc.centroid
+    for c in CHECK:
+        s.step(sc.scales(st + 1, c - st))
+        st = c
+        mine, ref = s.intact() == 0, sub["mu"][c] == 0
+        agree = agreement(mine, ref)
+        assert agree >= 0.999, (c, agree)
+        mm = broken_midpoints(sub["pairs"], mine, cen)
+        mr = broken_midpoints(sub["pairs"], ref, cen)
+        tip_d = np.linalg.norm(crack_tip(mm) - crack_tip(mr))
+        path = hausdorff(mm, mr)
+        print(f"[cfg3_sub mode {mode}] step {c}: broken {int(ref.sum())} oracle / "
+              f"{int(mine.sum())} device, agreement {agree:.6f}, tip distance "
+              f"{tip_d / sc.delta:.3f} delta, path (Hausdorff) {path / sc.delta:.3f} delta")
+        assert tip_d <= sc.delta and path <= sc.delta, (c, tip_d, path)
+        # the crack has grown past the pre-crack tip (x = 10 mm)
+        assert crack_tip(mr)[0] > 0.01
+    return ru
+
+
+def test_cfg3_sub_fast_fp64_vs_oracle(sub):
+    ru = _fast_vs_oracle(sub, capi.FAST, 1e-9)
+    assert ru <= 1e-9
+
+
+def test_cfg3_sub_f32pos_vs_oracle(sub):
+    ru = _fast_vs_oracle(sub, capi.FAST_F32POS, F32_TOL)
+    assert ru > 0  # the fp32 arithmetic really ran
+
+
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_cfg3_sub_two_slabs_bitwise(sub, mode):
+    """Two slab handles (host-mediated halo exchange, one GPU): the hash keys use
+    global ids (global_id_offset) -- owned fields and bond states bitwise one domain."""
+    sc = sub["sc"]
+    steps = 220
+    one = _device(sc, mode)
+    nb1 = one.step(sc.scales(1, steps))
+    u, v, a = one.state()
+    intact = one.intact()
+    idx = {(int(i), int(j)): q for q, (i, j) in enumerate(sub["pairs"])}
+    hs = [slabs.solver_for_slab(sc, slabs.make_slab(sc.lattice, 2, r, 2), mode)
+          for r in range(2)]
+    for h in hs:
+        h.find_pe_pairs()
+        h.initial_acceleration(sc.load_scale(0.0))
+
+    def exchange():
+        msgs = []
+        for h in hs:
+            plo, slo, rlo, nlo, phi, shi, rhi, nhi = h.slab.halo
+            if plo >= 0:
+                msgs.append((plo, hs[plo].slab.halo[6], nlo, h.get_rows(slo, nlo)))
+            if phi >= 0:
+                msgs.append((phi, hs[phi].slab.halo[2], nhi, h.get_rows(shi, nhi)))
+        for dst, first, n, vals in msgs:
+            hs[dst].set_rows(first, n, vals)
+
+    exchange()
+    nb = 0
+    for i in range(1, steps + 1):
+        for h in hs:
+            nb += h.step([sc.load_scale(i * sc.dt)])
+        exchange()
+    assert nb == nb1 and nb1 > 100
+    for h in hs:
+        s = h.slab
+        lu, lv, la = h.state()
+        n0, n1 = s.own_nodes
+        g0, g1 = s.global_nodes(n0, n1)
+        assert np.array_equal(lu[n0 * 2:n1 * 2], u[g0 * 2:g1 * 2])
+        assert np.array_equal(lv[n0 * 2:n1 * 2], v[g0 * 2:g1 * 2])
+        assert np.array_equal(la[n0 * 2:n1 * 2], a[g0 * 2:g1 * 2])
+        lp, li = h.pairs(), h.intact()
+        own = (lp[:, 0] >= s.own_elems[0]) & (lp[:, 0] < s.own_elems[1])
+        gl = lp[own] + s.elem_first
+        q = np.array([idx[(int(i), int(j))] for i, j in gl])
+        assert np.array_equal(li[own], intact[q])
+
+
+def test_cfg3_full_size_window_through_crack_initiation():
+    """Full-size BASELINE cfg3 (fp64 fast mode, the bench's kernel): fast-forward on
+    the device to the first 20-step batch with breaks (step i..i+19), hand the
+    device state after step i-21 to the oracle, run both to step i+59."""
+    sc = Scenario(cf.get("cfg3"))
+    s = _device(sc, capi.FAST)
+    pairs = s.pairs()
+    assert len(pairs) == 22_331_624
+    B = 20
+    i = 1
+    snaps = []
+    while True:
+        snaps = (snaps + [s.state()])[-2:]
+        nb = s.step(sc.scales(i, B))
+        if nb:
+            break
+        i += B
+        assert i < 1500, "no crack initiation within 1500 steps"
+    assert len(snaps) == 2 and i > 2 * B
+    k0 = i - 1 - B  # oracle starts from the device state after step k0
+    o = _oracle(sc, pairs)
+    o.set_state(*snaps[0])
+    o.step(sc.scales(k0 + 1, B))
+    ou, ov, _ = o.state()
+    du, dv, _ = snaps[1]
+    assert o.mu().all()
+    print(f"[cfg3 full size] first broken batch at step {i}; oracle from step {k0}: relL2 "
+          f"u {_rel(du, ou):.3e} v {_rel(dv, ov):.3e} at step {i - 1}")
+    assert _rel(du, ou) <= 1e-9 and _rel(dv, ov) <= 1e-9
+    W = 60
+    s.step(sc.scales(i + B, W - B))
+    o.step(sc.scales(i, W))
+    mine, ref = s.intact() == 0, o.mu() == 0
+    mm = broken_midpoints(pairs, mine, sc.centroid)
+    mr = broken_midpoints(pairs, ref, sc.centroid)
+    tip_d = np.linalg.norm(crack_tip(mm) - crack_tip(mr))
+    path = hausdorff(mm, mr)
+    print(f"[cfg3 full size] step {i + W - 1}: broken {int(ref.sum())} oracle / "
+          f"{int(mine.sum())} device, agreement {agreement(mine, ref):.6f}, tip distance "
+          f"{tip_d / sc.delta:.3f} delta, path {path / sc.delta:.3f} delta")
+    assert ref.sum() > 10
+    assert agreement(mine, ref) >= 0.999
+    assert tip_d <= sc.delta and path <= sc.delta
