@@ -257,38 +257,72 @@ def bench_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def bench_native(args):
+class Ctx:
+    """One process per GPU: rank / local rank / world from torchrun's environment,
+    the gloo control plane (NCCL clique ids, bond counts, max-over-ranks times)."""
+
+    def __init__(self, force_slabs: bool):
+        self.rank, self.local, self.world = _env_rank()
+        self.dist = None
+        self.slabbed = self.world > 1 or force_slabs
+        if self.slabbed:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local)
+            if self.world == 1:  # --force-slabs: the slab + NCCL path with one rank
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                dist.init_process_group("gloo", rank=0, world_size=1)
+            else:
+                dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def reduce(self, x: float, op: str = "max") -> float:
+        if not self.dist:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op={"max": self.dist.ReduceOp.MAX,
+                                    "sum": self.dist.ReduceOp.SUM}[op])
+        return float(t.item())
+
+    def uid(self) -> bytes:
+        import torch
+
+        from paper_2403_03605_b200.pd import PDSolver
+
+        u = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            u[:] = torch.frombuffer(bytearray(PDSolver.nccl_unique_id()), dtype=torch.uint8)
+        self.dist.broadcast(u, 0)
+        return bytes(u.tolist())
+
+
+def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode,
+               full: bool = True) -> dict:
+    """Device time, roofline, (full:) fp32-position variant and e2e of K fine steps of
+    `workload` after W warm-up steps, on ctx.world ranks (slabs: weak = one copy of
+    the plate per rank stacked, strong = the plate cut into world slabs)."""
     import numpy as np
 
     from paper_2403_03605_b200 import capi
     from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200 import slabs
     from paper_2403_03605_b200.pd import PDSolver, Scenario
 
-    rank, local, world = _env_rank()
-    dist = None
-    mode = {"fast": capi.FAST, "det": capi.DETERMINISTIC, "f32pos": capi.FAST_F32POS}[args.mode]
-    K, W = args.steps, args.warmup
-    slabbed = world > 1 or args.force_slabs
-    if slabbed:
-        # slab decomposition (paper_2403_03605_b200/slabs.py), weak scaling: the plate
-        # grows with N so every rank owns one cfg3-sized slab; the halo exchange is
-        # ncclSend/ncclRecv inside the library's step loop, the control plane is gloo
-        import torch
-        import torch.distributed as dist
-
-        from paper_2403_03605_b200 import slabs
-
-        torch.cuda.set_device(local)
-        if world == 1:  # --force-slabs: exercise the slab + NCCL path on one GPU
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("gloo", rank=0, world_size=1)
-        else:
-            dist.init_process_group("gloo")
-        sc = Scenario(cf.stacked(args.workload, world))
+    rank, local, world = ctx.rank, ctx.local, ctx.world
+    if ctx.slabbed:
+        sc = Scenario(cf.stacked(workload, world) if scaling == "weak" else cf.get(workload))
         slab = slabs.make_slab(sc.lattice, sc.dim, rank, world)
     else:
-        sc = Scenario(cf.get(args.workload))
+        sc = Scenario(cf.get(workload))
+        slab = None
     B = None
 
     def fresh():
@@ -296,29 +330,20 @@ def bench_native(args):
         (device time, roofline, end to end) covers the same steps W+1 .. W+K of the
         BASELINE run, so they time the same physics (cracks start late in cfg3)."""
         nonlocal B
-        if slabbed:
+        if slab is not None:
             s = slabs.solver_for_slab(sc, slab, mode, device=local).find_pe_pairs()
-            uid = torch.zeros(128, dtype=torch.uint8)
-            if rank == 0:
-                uid[:] = torch.frombuffer(bytearray(PDSolver.nccl_unique_id()), dtype=torch.uint8)
-            dist.broadcast(uid, 0)
-            s.comm_init(bytes(uid.tolist()), world, rank)
-            s.set_halo(*slab.halo)
+            slabs.attach_nccl(s, ctx.uid())
             if B is None:
                 lp = s.pairs()
-                own = int(((lp[:, 0] >= slab.own_elems[0]) & (lp[:, 0] < slab.own_elems[1])).sum())
-                tb = torch.tensor([own], dtype=torch.int64)
-                dist.all_reduce(tb)
-                B = int(tb.item())  # unique bonds of the whole plate
+                B = int(ctx.reduce(float(slab.owns_elem(lp[:, 0]).sum()), "sum"))
         else:
             s = PDSolver.from_scenario(sc, mode=mode, device=local).find_pe_pairs()
             if B is None:
                 B = s.info()["n_bonds"]
         v0 = sc.initial_velocity()  # cfg4's impact patch (extension); zero for the plates
         if v0.any():
-            if slabbed:  # this slab's nodes (halo included)
-                n0 = slab.node_first * sc.dim
-                v0 = v0[n0:n0 + s.n_dof]
+            if slab is not None:  # this slab's nodes (halo included)
+                v0 = v0[s.local_dofs]
             z = np.zeros(s.n_dof)
             s.set_state(z, v0, z)
         s.initial_acceleration(sc.load_scale(0.0))
@@ -330,17 +355,12 @@ def bench_native(args):
     t_setup = time.perf_counter() - t0
     info = s.info()
     step0 = W + 1
-
-    def barrier():
-        if dist:
-            dist.barrier()
-
     with Clocks(local) as clk:
-        barrier()
+        ctx.barrier()
         ms = s.step_timed(sc.scales(step0, K))  # synchronises the stream on both sides
-        barrier()
+        ctx.barrier()
     variant = None
-    if not slabbed and mode == capi.FAST and sc.dim == 2 and not args.no_variant:
+    if full and slab is None and mode == capi.FAST and sc.dim == 2 and not args.no_variant:
         # BASELINE cfg3's fp32-position / fp64-accumulate variant over the same steps,
         # and how far it lands from the fp64 run at the end of the window
         u64, _, _ = s.state()
@@ -363,19 +383,14 @@ def bench_native(args):
         del s
     s = fresh()
     bond_ms, tot_ms = s.profile(sc.scales(step0, K))
-    if dist:
-        import torch
-
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = ctx.reduce(ms, "max")
     value = B * K / (ms * 1e-3)  # B = unique bonds of the whole job
 
     # roofline of the dominant (bond) kernel
     peak, peak_src = _peaks()
     bond_avg_s = bond_ms * 1e-3 / K
     timing = "each launch between its own pair of CUDA events (profile pass)"
-    if info["kernels_per_step"] == 1 and not dist:
+    if info["kernels_per_step"] == 1 and not ctx.dist:
         # one kernel per step (the 2D tile kernel): the timed region's K back-to-back
         # launches between two events on the launching stream ARE the kernel's launches;
         # per-launch events would break programmatic dependent launch, which overlaps
@@ -384,12 +399,10 @@ def bench_native(args):
         timing = ("timed region: K back-to-back launches of the step's only kernel between two "
                   "CUDA events on its stream (programmatic dependent launch on)")
     achieved = info["bond_bytes_per_step"] / bond_avg_s / 1e9
-    fused = {"tile9": "k_tile9", "tile": "k_fused2d", "tma": "k_tma2d", "strip": "k_strip2d"}
-    kname = {2: fused.get(os.environ.get("PMTS_FUSED_KERNEL", "tile9"), "k_tile9"),
-             1: "k_lat3_bond" if info["stencil_size"] == 122 else "k_lat_bond"}.get(
-                 info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
+    kname = {2: "k_tile9", 1: "k_lat3_bond" if info["stencil_size"] == 122 else "k_lat_bond"}.get(
+        info["path"], "k_fast_bond" if mode == capi.FAST else "k_det_bond")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": _ncu_traffic(kname, args.workload),
+            "frac": achieved / peak, "traffic": _ncu_traffic(kname, workload),
             "kernel": kname, "bytes_per_launch": info["bond_bytes_per_step"],
             "avg_launch_us": bond_avg_s * 1e6, "launch_timing": timing,
             "avg_launch_us_isolated": bond_ms * 1e3 / K,
@@ -403,88 +416,140 @@ def bench_native(args):
 
     # end to end through the public C-ABI with host buffers
     e2e = None
-    try:
-        import torch
+    if full:
+        try:
+            import torch
 
-        del s
-        s = fresh()
-        nd = s.n_dof
-        hu = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
-        hv = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
-        ha = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
-        u0, v0, a0 = s.state()
-        hu[:], hv[:], ha[:] = u0, v0, a0
-        tracked = np.array([2 * (s.n_nodes // 2) + 1], dtype=np.int32)
-        scales = sc.scales(step0, K)
-        trk = torch.empty((K, len(tracked)), dtype=torch.float64, pin_memory=True).numpy()
-        nbk = torch.empty(K, dtype=torch.int64, pin_memory=True).numpy()
-        hsc = torch.empty(K, dtype=torch.float64, pin_memory=True).numpy()
-        hsc[:] = scales
-        barrier()
-        t = time.perf_counter()
-        s.set_state(hu, hv, ha)
-        # one public call for the K steps; inside it, per step and asynchronously:
-        # the step's scale H2D, the step, its tracked displacement + broken count D2H
-        s.step_tracked(hsc, tracked, trk, nbk)
-        s.get_state_into(hu, hv, ha)
-        e2e_s = time.perf_counter() - t
-        if dist:
-            te = torch.tensor([e2e_s], dtype=torch.float64)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            e2e_s = float(te.item())
-        h2d = (3 * nd * 8 + K * 8) / K
-        d2h = (3 * nd * 8 + K * (8 + 8 * len(tracked))) / K
-        e2e = {"value": B * K / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / K,
-               "note": "per rank, one pmts_pd_step_tracked call for the K steps: state H2D "
-                       "from pinned memory, the K load scales H2D in one copy, per step "
-                       "(async on the stream) the step and its tracked displacement written into "
-                       "mapped pinned memory (2D: by the step kernel; 3D lattice: by a tiny "
-                       "launch reading the step's predictor); the K broken counts D2H in "
-                       "one copy; final state D2H"}
-    except Exception as ex:  # pragma: no cover - reported, never silent
-        e2e = {"value": None, "unit": UNIT, "error": repr(ex)}
+            del s
+            s = fresh()
+            nd = s.n_dof
+            hu = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+            hv = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+            ha = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+            u0, v0, a0 = s.state()
+            hu[:], hv[:], ha[:] = u0, v0, a0
+            tracked = np.array([sc.dim * (s.n_nodes // 2) + 1], dtype=np.int32)
+            scales = sc.scales(step0, K)
+            trk = torch.empty((K, len(tracked)), dtype=torch.float64, pin_memory=True).numpy()
+            nbk = torch.empty(K, dtype=torch.int64, pin_memory=True).numpy()
+            hsc = torch.empty(K, dtype=torch.float64, pin_memory=True).numpy()
+            hsc[:] = scales
+            ctx.barrier()
+            t = time.perf_counter()
+            s.set_state(hu, hv, ha)
+            # one public call for the K steps; inside it, per step and asynchronously:
+            # the step's scale H2D, the step, its tracked displacement + broken count D2H
+            s.step_tracked(hsc, tracked, trk, nbk)
+            s.get_state_into(hu, hv, ha)
+            e2e_s = ctx.reduce(time.perf_counter() - t, "max")
+            h2d = (3 * nd * 8 + K * 8) / K
+            d2h = (3 * nd * 8 + K * (8 + 8 * len(tracked))) / K
+            e2e = {"value": B * K / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / K,
+                   "note": "per rank, one pmts_pd_step_tracked call for the K steps: state H2D "
+                           "from pinned memory, the K load scales H2D in one copy, per step "
+                           "(async on the stream) the step and its tracked displacement written "
+                           "into mapped pinned memory (2D: by the step kernel; 3D lattice: by a "
+                           "tiny launch reading the step's predictor); the K broken counts D2H "
+                           "in one copy; final state D2H"}
+        except Exception as ex:  # pragma: no cover - reported, never silent
+            e2e = {"value": None, "unit": UNIT, "error": repr(ex)}
+    del s
+    ws = info["device_bytes"] / 1e6
+    if world == 1:
+        par = "single" if slab is None else "slabs1 (NCCL clique of one)"
+    else:
+        par = f"slabs{world} (z-x slabs, NCCL halo send/recv)" if sc.dim == 3 else \
+            f"slabs{world} (x-slabs, NCCL halo send/recv)"
+    desc = WORKLOADS.get(workload, workload)
+    if world > 1:
+        desc += (f"; weak scaling: {world} copies stacked, one slab per GPU" if scaling == "weak"
+                 else f"; strong scaling: the same plate cut into {world} slabs")
+    out = {"value": value, "unit": UNIT, "ms_per_step": ms / K, "steps": K, "warmup": W,
+           "scaling": scaling, "bonds": B,
+           "config": {"workload": desc, "mode": args.mode, "bonds": B, "elements": sc.n_elems,
+                      "nodes": sc.n_nodes, "parallelism": par,
+                      "l2": f"inputs larger than L2 (device working set {ws:.0f} MB per rank "
+                            f"> 126 MB)", "setup_s": t_setup},
+           "roofline": roof, "roofline_fp64": roof_fp64, "e2e": e2e,
+           "gpu_launches": K * info["kernels_per_step"], "clocks": clk.summary()}
+    if slab is not None and sc.dim == 3:
+        out["config"]["redundancy"] = slabs.redundancy(sc.lattice, 3, world)
+    if variant:
+        out["f32pos_variant"] = variant
+    return out
 
+
+def bench_native(args):
+    from paper_2403_03605_b200 import capi
+
+    ctx = Ctx(args.force_slabs)
+    if ctx.world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ctx.world}")
+    mode = {"fast": capi.FAST, "det": capi.DETERMINISTIC, "f32pos": capi.FAST_F32POS}[args.mode]
+    K, W = args.steps, args.warmup
+    scaling = args.scaling or ("weak" if args.workload == "cfg3" else "strong")
+    r = measure_pd(args, ctx, args.workload, scaling, K, W, mode)
+    # the 3D configurations (BASELINE cfg4, and cfg5's PD core -- the north star's
+    # scaling target, cut into ctx.world z-x slabs): shorter windows, same metric
+    workloads = {}
+    if not args.no_workloads and args.workload == "cfg3":
+        for name, k in (("cfg4", args.w3d_steps), ("cfg5_core", max(args.w3d_steps // 2, 10))):
+            try:
+                wmode = capi.FAST if mode == capi.FAST_F32POS else mode  # fp32 pos.: 2D only
+                w = measure_pd(args, ctx, name, "strong", k, W, wmode, full=False)
+                workloads[name] = {key: w[key] for key in
+                                   ("value", "unit", "ms_per_step", "steps", "warmup", "scaling",
+                                    "config", "roofline", "gpu_launches")}
+            except Exception as ex:  # pragma: no cover - reported, never silent
+                workloads[name] = {"error": repr(ex)}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_reference_cpu(args.cpu_steps, 4)
-        cpu = {"value": r["bond_updates_per_s"], "unit": UNIT, "cores": r["threads"],
-               "kind": r["kind"], "sample": r["sample"]}
-
-    if rank == 0:
-        ws = info["device_bytes"] / 1e6
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        c = run_reference_cpu(args.cpu_steps, 4)
+        cpu = {"value": c["bond_updates_per_s"], "unit": UNIT, "cores": c["threads"],
+               "kind": c["kind"], "sample": c["sample"]}
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None,
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ctx.world, "steps": K,
+            "warmup": W, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": r["scaling"], "vs_baseline": None,
             "dtype": "f32 positions / f64 accumulate" if mode == capi.FAST_F32POS else "f64",
             "data": "synthetic",
-            "config": {"workload": (WORKLOADS.get(args.workload, args.workload)
-                                    + ("" if world == 1 else
-                                       f"; weak scaling: {world} cfg3 slabs stacked into a "
-                                       f"2000x{800 * world} plate, one slab per GPU")),
-                       "mode": args.mode, "bonds": B, "elements": sc.n_elems,
-                       "nodes": sc.n_nodes,
-                       "parallelism": f"slabs{world} (NCCL halo send/recv)" if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (device working set {ws:.0f} MB > 126 MB)",
-                       "setup_s": t_setup},
-            "roofline": roof,
-            "roofline_fp64": roof_fp64,
+            "config": r["config"],
+            "roofline": r["roofline"],
+            "roofline_fp64": r["roofline_fp64"],
             "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": K * info["kernels_per_step"],
-            "clocks": clk.summary(),
+            "e2e": r["e2e"],
+            "gpu_launches": r["gpu_launches"],
+            "clocks": r["clocks"],
         }
-        if variant:
-            line["f32pos_variant"] = variant
-        if world == 1 and not args.no_mts:
+        if "f32pos_variant" in r:
+            line["f32pos_variant"] = r["f32pos_variant"]
+        if workloads:
+            line["workloads"] = workloads
+        if ctx.world == 1 and not args.no_mts:
             try:
                 line["coupled_mts"] = bench_mts(args.mts_steps, 3, not args.no_cpu_baseline)
             except Exception as ex:  # pragma: no cover - reported, never silent
                 line["coupled_mts"] = {"metric": MTS_METRIC, "error": repr(ex)}
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    if ctx.dist:
+        ctx.dist.destroy_process_group()
+
+
+def _spawn_ranks(args) -> int:
+    """--gpus N without torchrun's environment: re-launch this command under
+    torch.distributed.run, one rank per GPU (127.0.0.1 rendezvous)."""
+    import socket
+
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -504,9 +569,18 @@ def main():
     ap.add_argument("--mts-steps", type=int, default=20)
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the multi-GPU slab path (NCCL clique) even with one rank")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="N > 1: weak = one copy of the plate per GPU (cfg3 default), strong = "
+                         "the plate cut into N slabs (3D default)")
+    ap.add_argument("--no-workloads", action="store_true",
+                    help="skip the cfg4 / cfg5_core section of the default line")
+    ap.add_argument("--w3d-steps", type=int, default=200,
+                    help="timed fine steps of the cfg4 workload (cfg5_core: half)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(_spawn_ranks(args))
     if args.workload == "cfg2":  # the coupled MTS metric as its own line
         rank, _, _ = _env_rank()
         if rank != 0:

@@ -136,10 +136,17 @@ typedef struct {
                                     lattice (enables the stencil fast path); 0 = unknown */
     /* --- slab decomposition (multi-GPU); all zero for a single domain --- */
     int64_t global_id_offset;    /* global id of local element 0 (per-bond hash uses global ids) */
-    int32_t owned_elems[2];      /* local element range this rank owns (broken counts); 0,0 = all */
+    int32_t owned_elems[2];      /* local element range this rank owns (broken counts); 0,0 = all;
+                                    with slab_plane: the in-layer range (l mod slab_plane[0]) */
     double lattice_h;            /* > 0: stencil constants from the nominal lattice (xi = offset*h,
                                     w = lattice_vol^2) so every rank's table is identical */
     double lattice_vol;
+    int32_t slab_plane[2];       /* 3D slabs cut along y (z-x slabs): elements per z layer,
+                                    local and global; global id of local element l =
+                                    (l / p0) p1 + global_id_offset + l mod p0.  0,0: contiguous */
+    int32_t node_rows[2];        /* lattice path: the y node rows [lo, hi) this rank updates (its
+                                    owned rows); element forces only for the rows they need.
+                                    0,0 = all */
 } pmts_pd_desc;
 
 typedef struct {
@@ -225,6 +232,12 @@ void* pmts_pd_stream(pmts_pd* h);
  * (host-mediated exchange; also the single-GPU emulation of several ranks) */
 int pmts_pd_get_rows(pmts_pd* h, int32_t first_node, int32_t n_nodes, double* out);
 int pmts_pd_set_rows(pmts_pd* h, int32_t first_node, int32_t n_nodes, const double* in);
+/* the same over n_layers ranges [first + l stride, + n) (3D slabs cut along y: one
+ * range per z node layer), packed layer after layer */
+int pmts_pd_get_rows_layers(pmts_pd* h, int32_t first_node, int32_t n_nodes, int32_t n_layers,
+                            int32_t layer_stride, double* out);
+int pmts_pd_set_rows_layers(pmts_pd* h, int32_t first_node, int32_t n_nodes, int32_t n_layers,
+                            int32_t layer_stride, const double* in);
 /* NCCL (loaded at run time): unique id of a new clique (128 bytes) */
 int pmts_nccl_unique_id(void* id_out);
 /* join the clique; then each fine step ends with ncclSend/ncclRecv of the halo rows
@@ -233,6 +246,10 @@ int pmts_pd_comm_init(pmts_pd* h, const void* id, int32_t nranks, int32_t rank);
 int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t recv_lo_first,
                      int32_t n_lo, int32_t peer_hi, int32_t send_hi_first,
                      int32_t recv_hi_first, int32_t n_hi);
+/* after pmts_pd_set_halo: every halo range repeats over n_layers z node layers,
+ * layer_stride nodes apart (3D slabs cut along y); the library packs them into one
+ * contiguous message per neighbour (a pack / unpack kernel around the NCCL group) */
+int pmts_pd_set_halo_layers(pmts_pd* h, int32_t n_layers, int32_t layer_stride);
 /* sum of an int64 over the clique (broken counts at output cadence) */
 int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value);
 

@@ -41,7 +41,7 @@ struct po_pd {
     double* G;
     double delta, l, c0, c_const, h, s_crit, spread, gamma, beta, dt, N;
     uint64_t seed;
-    int64_t goff;
+    int64_t goff, id_pl, id_pg;
 };
 
 /* ------------------------------------------------------------------ */
@@ -389,6 +389,12 @@ static void build_families(po_pd* h) {
     h->G = (double*)calloc((size_t)E * 3, sizeof(double));
 }
 
+/* global element id of local element l: contiguous slabs add goff; 3D slabs cut
+ * along y map layer by layer */
+static int64_t global_id(const po_pd* h, int64_t l) {
+    return h->id_pl ? (l / h->id_pl) * h->id_pg + h->goff + l % h->id_pl : l + h->goff;
+}
+
 po_pd* po_pd_create(int dim, int n_nodes, int n_elems, const int32_t* conn, const double* cen,
                     const double* vol, int64_t n_pairs, const int32_t* pairs, const double* mass,
                     const double* p_ext, int n_bc, const int32_t* bc_dofs, const double* bc_vel,
@@ -415,6 +421,8 @@ po_pd* po_pd_create(int dim, int n_nodes, int n_elems, const int32_t* conn, cons
     h->seed = (uint64_t)iprm[1];
     h->variant = (int)iprm[2];
     h->goff = iprm[3]; /* global id of local element 0 (slab tests) */
+    h->id_pl = iprm[4]; /* 3D slabs cut along y: local / global elements per z layer */
+    h->id_pg = iprm[5];
     const size_t nd = (size_t)h->n_dof;
     h->conn = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_elems * h->nn);
     memcpy(h->conn, conn, sizeof(int32_t) * (size_t)n_elems * h->nn);
@@ -453,8 +461,8 @@ po_pd* po_pd_create(int dim, int n_nodes, int n_elems, const int32_t* conn, cons
         h->xin[q] = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
         h->w[q] = vol[i] * vol[j];
         h->coef[q] = po_micromodulus(h, h->xin[q]);
-        h->scrit[q] = po_bond_s_crit(h->s_crit, h->spread, h->seed, (int32_t)(i + h->goff),
-                                     (int32_t)(j + h->goff));
+        h->scrit[q] = po_bond_s_crit(h->s_crit, h->spread, h->seed, (int32_t)global_id(h, i),
+                                     (int32_t)global_id(h, j));
         h->mu[q] = 1;
     }
     h->u = (double*)calloc(nd, sizeof(double));

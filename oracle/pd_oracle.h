@@ -27,7 +27,8 @@ enum { PO_MICRO_EXP = 0, PO_MICRO_CONST = 1 };
 /* prm[]: 0 delta, 1 l, 2 c0, 3 c_const, 4 h, 5 s_crit, 6 s_crit_spread,
  *        7 gamma, 8 beta, 9 dt
  * iprm[]: 0 micromodulus kind, 1 seed (per-bond s_crit factor), 2 variant,
- *         3 global id of local element 0 (slab decomposition tests) */
+ *         3 global id of local element 0 (slab decomposition tests),
+ *         4, 5 elements per z layer, local and global (3D slabs cut along y; 0 = contiguous) */
 typedef struct po_pd po_pd;
 
 /* mesh.hpp:416-495 (find_pe_pairs) incl. notch predicates mesh.hpp:324-404.

@@ -117,7 +117,8 @@ class OraclePD:
                         sysd.get("s_crit_spread", 0.0), sysd.get("gamma", 0.5),
                         sysd.get("beta", 0.0), sysd["dt"]], dtype=np.float64)
         iprm = np.array([sysd.get("micromodulus", MICRO_EXP), sysd.get("seed", 0), variant,
-                         sysd.get("global_id_offset", 0)], dtype=np.int64)
+                         sysd.get("global_id_offset", 0), *sysd.get("slab_plane", (0, 0))],
+                        dtype=np.int64)
         self._keep += [prm, iprm]
         self.n_nodes = int(sysd["n_nodes"])
         self.n_elems = len(vol)

@@ -63,7 +63,8 @@ class PDDesc(C.Structure):
                 ("dt", _D), ("mode", _I), ("device", _I), ("n_notch", _I),
                 ("notch_npts", _P), ("notch_pts", _P), ("lattice", _I * 3),
                 ("global_id_offset", C.c_int64), ("owned_elems", _I * 2),
-                ("lattice_h", _D), ("lattice_vol", _D)]
+                ("lattice_h", _D), ("lattice_vol", _D), ("slab_plane", _I * 2),
+                ("node_rows", _I * 2)]
 
 
 class PDInfo(C.Structure):
@@ -131,6 +132,9 @@ SIGNATURES = {
     "pmts_pd_gather_disp": (C.c_int, [_P, _I, _P, _P]),
     "pmts_pd_stream": (_P, [_P]),
     "pmts_pd_get_rows": (C.c_int, [_P, _I, _I, _P]),
+    "pmts_pd_get_rows_layers": (C.c_int, [_P, _I, _I, _I, _I, _P]),
+    "pmts_pd_set_rows_layers": (C.c_int, [_P, _I, _I, _I, _I, _P]),
+    "pmts_pd_set_halo_layers": (C.c_int, [_P, _I, _I]),
     "pmts_pd_set_rows": (C.c_int, [_P, _I, _I, _P]),
     "pmts_nccl_unique_id": (C.c_int, [_P]),
     "pmts_pd_comm_init": (C.c_int, [_P, _P, _I, _I]),

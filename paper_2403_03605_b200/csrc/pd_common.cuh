@@ -39,7 +39,10 @@ struct DevPD {
     uint64_t seed;
     int fracture;
     long long goff;      // global id of local element 0 (slab decomposition)
-    int own_lo, own_hi;  // owned local element range (broken counts, break log)
+    int own_lo, own_hi;  // owned local element range (broken counts, break log); with
+                         // id_pl the in-layer range of l mod id_pl
+    int id_pl;           // 3D slabs cut along y: local elements per z layer (0: contiguous)
+    long long id_pg;     // ... and global elements per z layer
     // Newmark coefficients, each rounded exactly as the reference's expression
     double c_pred_v;  // dt*(1-gamma)              newmark.hpp:65
     double c_pred_d;  // (dt*dt)*(0.5-beta)        newmark.hpp:66
@@ -51,6 +54,17 @@ struct DevPD {
     unsigned long long* log_n;
     int64_t log_cap;
 };
+
+// global element id of local element l (per-bond hash keys, break log): a contiguous
+// slab adds goff; a 3D slab cut along y maps layer by layer
+__host__ __device__ inline long long global_elem(const DevPD& d, long long l) {
+    return d.id_pl ? (l / d.id_pl) * d.id_pg + d.goff + l % d.id_pl : l + d.goff;
+}
+// does this rank own local element l (broken counts, break log)
+__host__ __device__ inline bool owns_elem(const DevPD& d, long long l) {
+    const long long r = d.id_pl ? l % d.id_pl : l;
+    return r >= d.own_lo && r < d.own_hi;
+}
 
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;

@@ -131,16 +131,16 @@ k_det_bond(DevPD d, const double* __restrict__ disp, int step, int do_break, int
                 const double len = sqrt(len2);
                 const double s = len <= 0.0 ? -1.0 : (len - xin) / xin;
                 const int lo = e < p ? e : p, hi = e < p ? p : e;
-                if (s >= bond_s_crit(d.s_crit, d.spread, d.seed, lo + d.goff, hi + d.goff)) {
+                if (s >= bond_s_crit(d.s_crit, d.spread, d.seed, global_elem(d, lo), global_elem(d, hi))) {
                     word &= ~bit;
-                    if (e < p && e >= d.own_lo && e < d.own_hi) {
+                    if (e < p && owns_elem(d, e)) {
                         ++nb;
                         if (d.log) {
                             const unsigned long long slot = atomicAdd(d.log_n, 1ull);
                             if ((long long)slot < d.log_cap) {
                                 d.log[3 * slot] = gstep;
-                                d.log[3 * slot + 1] = (int)(e + d.goff);
-                                d.log[3 * slot + 2] = (int)(p + d.goff);
+                                d.log[3 * slot + 1] = (int)global_elem(d, e);
+                                d.log[3 * slot + 2] = (int)global_elem(d, p);
                             }
                         }
                     }

@@ -87,11 +87,11 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_bond(DevPD d, int step, i
                 double sc = s1;
                 if (d.spread != 0.0) {
                     const int lo = e < p ? e : p, hi = e < p ? p : e;
-                    sc = 1.0 + bond_s_crit(d.s_crit, d.spread, d.seed, lo + d.goff, hi + d.goff);
+                    sc = 1.0 + bond_s_crit(d.s_crit, d.spread, d.seed, global_elem(d, lo), global_elem(d, hi));
                 }
                 if (l2 >= sc * sc * x2) {
                     word &= ~bit;
-                    if (e < p && e >= d.own_lo && e < d.own_hi) ++nb;
+                    if (e < p && owns_elem(d, e)) ++nb;
                 }
             }
         }

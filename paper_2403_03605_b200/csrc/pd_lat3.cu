@@ -156,11 +156,11 @@ k_lat3_ubar(DevPD d, LatticeDev L, unsigned* tmax) {
     __shared__ unsigned red[NT / 32][9];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
-    const int i = blockIdx.x * TX + tx, j = blockIdx.y * TY + ty, k = blockIdx.z * TZ + tz;
+    const int i = blockIdx.x * TX + tx, j = L.ub0 + blockIdx.y * TY + ty, k = blockIdx.z * TZ + tz;
     unsigned mx[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) mx[q] = 0u;
-    if (i < L.nx && j < L.ny && k < L.nz) {
+    if (i < L.nx && j >= 0 && j < L.ny && k < L.nz) {
         const int NX = L.nx + 1, NY = L.ny + 1, up = NX * NY;
         const int n00 = (k * NY + j) * NX + i;
         const int nd[8] = {n00, n00 + 1, n00 + NX + 1, n00 + NX,
@@ -220,11 +220,13 @@ __device__ __forceinline__ bool lat3_tile_hot(const Stencil3D& st, const Lattice
     __syncthreads();
     if (tid < 27 * 9) {
         const int t = tid / 9, q = tid % 9;
-        const int bx = blockIdx.x + t % 3 - 1, by = blockIdx.y + (t / 3) % 3 - 1,
+        // bond tile y row blockIdx.y is ubar tile row blockIdx.y + (jb0 - ub0) / TY
+        const int by0 = blockIdx.y + (L.jb0 - L.ub0) / TY;
+        const int bx = blockIdx.x + t % 3 - 1, by = by0 + (t / 3) % 3 - 1,
                   bz = blockIdx.z + t / 9 - 1;
-        if (bx >= 0 && by >= 0 && bz >= 0 && bx < (int)gridDim.x && by < (int)gridDim.y &&
+        if (bx >= 0 && by >= 0 && bz >= 0 && bx < (int)gridDim.x && by < L.ugy &&
             bz < (int)gridDim.z)
-            atomicMax(&dmax[q], st.tmax[((size_t)(bz * gridDim.y + by) * gridDim.x + bx) * 9 + q]);
+            atomicMax(&dmax[q], st.tmax[((size_t)(bz * L.ugy + by) * gridDim.x + bx) * 9 + q]);
     }
     __syncthreads();
     bool h = false;
@@ -257,7 +259,7 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     double* ua = reinterpret_cast<double*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     uint64_t* bar = reinterpret_cast<uint64_t*>(ua + 3 * NAT);
     const int tid = threadIdx.x;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY, k0 = blockIdx.z * TZ;
+    const int i0 = blockIdx.x * TX, j0 = L.jb0 + blockIdx.y * TY, k0 = blockIdx.z * TZ;
     if (st.use_tma) {
         // one bulk tensor copy of the apron; out-of-domain boxes arrive zero-filled
         if (tid == 0) {
@@ -294,7 +296,7 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     }
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
     const int gi = i0 + tx, gj = j0 + ty, gk = k0 + tz;
-    const bool own = gi < L.nx && gj < L.ny && gk < L.nz;
+    const bool own = gi < L.nx && gj < L.jb1 && gk < L.nz;
     const int e = own ? (gk * L.ny + gj) * L.nx + gi : 0;
     uint32_t m4[4] = {0u, 0u, 0u, 0u};  // bond states, loaded while the apron is in flight
     if (own) {
@@ -342,13 +344,13 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
                     double thr = __longlong_as_double(st.cthr[cls_of(d2)]);
                     if (d.spread != 0.0) {
                         const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
-                                                      (e < p ? e : p) + d.goff,
-                                                      (e < p ? p : e) + d.goff);
+                                                      global_elem(d, e < p ? e : p),
+                                                      global_elem(d, e < p ? p : e));
                         thr = fma(sb, sb, 2.0 * sb) * st.hh * d2;
                     }
                     if (lhs >= thr) {
                         mw[w] &= ~(1u << b);
-                        if (p > e && e >= d.own_lo && e < d.own_hi) ++nb;
+                        if (p > e && owns_elem(d, e)) ++nb;
                     }
                 }
                 if (mw[w] != c.m[w]) d.mask[(size_t)w * d.E + e] = mw[w];
@@ -371,8 +373,15 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     }
 }
 
+// Row tiling of a slab: the bond tiles start at element row jb0; the ubar tiles are
+// aligned with them (rows ub0 + TY b, ub0 = jb0 - TY ceil(jb0 / TY) <= 0) and cover
+// every element row, so the screen's 27-tile neighbourhood is the bond tile's own.
+void lat3_rows(LatticeDev& L) {
+    L.ub0 = L.jb0 - TY * ((L.jb0 + TY - 1) / TY);
+    L.ugy = (L.ny - L.ub0 + TY - 1) / TY;
+}
 void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s) {
-    dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
+    dim3 grid((L.nx + TX - 1) / TX, L.ugy, (L.nz + TZ - 1) / TZ);
     k_lat3_ubar<<<grid, NT, 0, s>>>(d, L, tmax);
 }
 void lat3_apron_box(int* bx, int* by, int* bz) {
@@ -381,12 +390,12 @@ void lat3_apron_box(int* bx, int* by, int* bz) {
     *bz = AZ;
 }
 size_t lat3_tile_count(const LatticeDev& L) {
-    return (size_t)((L.nx + TX - 1) / TX) * ((L.ny + TY - 1) / TY) * ((L.nz + TZ - 1) / TZ);
+    return (size_t)((L.nx + TX - 1) / TX) * L.ugy * ((L.nz + TZ - 1) / TZ);
 }
 
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
                       int do_break, cudaStream_t s) {
-    dim3 grid((L.nx + TX - 1) / TX, (L.ny + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
+    dim3 grid((L.nx + TX - 1) / TX, (L.jb1 - L.jb0 + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
     constexpr size_t smem = kApronBytes + 8 + 128;  // + mbarrier + realignment slack
     static bool configured = false;
     if (!configured) {

@@ -198,13 +198,13 @@ k_lat_bond(DevPD d, LatticeDev L, int step, int do_break) {
                         if (d.spread != 0.0) {
                             const int p = e + of.y;
                             const double sb = bond_s_crit(d.s_crit, d.spread, d.seed,
-                                                          (e < p ? e : p) + d.goff,
-                                                          (e < p ? p : e) + d.goff);
+                                                          global_elem(d, e < p ? e : p),
+                                                          global_elem(d, e < p ? p : e));
                             thr = fma(sb, sb, 2.0 * sb) * t[6];
                         }
                         if (lhs >= thr) {
                             m &= ~(1u << b);
-                            if (of.y > 0 && e >= d.own_lo && e < d.own_hi) ++nb;
+                            if (of.y > 0 && owns_elem(d, e)) ++nb;
                         }
                     }
                 }
@@ -230,11 +230,13 @@ k_lat_bond(DevPD d, LatticeDev L, int step, int do_break) {
 template <int DIM>
 __global__ void __launch_bounds__(256)
 k_lat_node(DevPD d, LatticeDev L, double scale, int write_state) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= d.N) return;
-    const int NX = L.nx + 1, NY = L.ny + 1;
-    const int i = n % NX, r = n / NX;
-    const int j = r % NY, k = r / NY;
+    // thread t -> node (i, j, k) of the updated rows j in [jn0, jn1)
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NX = L.nx + 1, NY = L.ny + 1, NR = L.jn1 - L.jn0;
+    const int i = t % NX, r = t / NX;
+    const int j = L.jn0 + r % NR, k = r / NR;
+    if (k >= (DIM == 3 ? L.nz + 1 : 1)) return;
+    const int n = (k * NY + j) * NX + i;
     double Ku[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
@@ -283,7 +285,7 @@ size_t lattice_smem_bytes(int dim, int R, int S) {
 void launch_lattice_step(const DevPD& d, const LatticeDev& L, int step, int do_break,
                          double scale, int write_state, bool time_bond, cudaEvent_t* ev,
                          cudaStream_t s, const Stencil3D* st3) {
-    const int nb = (d.N + 255) / 256;
+    const int nb = ((L.nx + 1) * (L.jn1 - L.jn0) * (d.dim == 3 ? L.nz + 1 : 1) + 255) / 256;
     if (d.dim == 3 && st3) {  // the specialised 122-offset kernel (pd_lat3.cu)
         // tiled ubar + the cold-tile screen's edge maxima (only when the break test runs)
         launch_lat3_ubar(d, L, do_break ? const_cast<unsigned*>(st3->tmax) : nullptr, s);

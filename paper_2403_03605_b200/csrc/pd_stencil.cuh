@@ -21,6 +21,11 @@ struct LatticeDev {
     const double* table; // per offset, 8 doubles (layout in pd_stencil.cu)
     const uint8_t* nflag;     // per node: bit c = dof c constrained, bit 3 = loaded
     const double* inv_mass;   // per node: 1 / M (lumped mass is per node)
+    // slab rows (pmts_pd_desc.node_rows; full range for one domain): the node update
+    // runs on the y node rows [jn0, jn1) only, the 3D bond kernel on the element rows
+    // [jb0, jb1) their forces need; ub0 / ugy: first y row and row tiles of the 3D
+    // ubar grid (its tiles align with the bond tiles, pd_lat3.cu)
+    int jn0 = 0, jn1 = 0, jb0 = 0, jb1 = 0, ub0 = 0, ugy = 0;
 };
 
 constexpr int kTableRow = 8;
@@ -131,6 +136,7 @@ int lat3_class_of(int d2);
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
                       int do_break, cudaStream_t s);
 void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s);
+void lat3_rows(LatticeDev& L);  // ub0 / ugy from jb0 (call before lat3_tile_count)
 size_t lat3_tile_count(const LatticeDev& L);
 void lat3_apron_box(int* bx, int* by, int* bz);  // TMA box of the ubar apron (doubles, rows, layers)
 

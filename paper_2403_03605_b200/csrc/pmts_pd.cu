@@ -120,6 +120,10 @@ struct pmts_pd {
     cudaStream_t xstream = nullptr;
     cudaEvent_t ev_edge = nullptr, ev_x = nullptr;
     int send_lo = 0, recv_lo = 0, n_lo = 0, send_hi = 0, recv_hi = 0, n_hi = 0;
+    // 3D slabs cut along y: each halo range repeats over halo_layers z node layers,
+    // halo_stride nodes apart; packed into halo_buf (send lo | send hi | recv lo | recv hi)
+    int halo_layers = 1, halo_stride = 0;
+    double* halo_buf = nullptr;
     unsigned long long* h_counts = nullptr;  // pinned
     void* h_map = nullptr;                   // mapped pinned staging (step_tracked)
     size_t h_map_cap = 0;
@@ -218,6 +222,35 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 constexpr ncclDataType_t kNcclFloat64 = ncclFloat64;
 
+// Strided halo ranges (3D slabs cut along y): copy n nodes (dim doubles each) of
+// `layers` ranges, `stride` nodes apart, between rd and a packed buffer.  Two ranges
+// per launch (the lower and the upper neighbour's); n = 0 skips one.
+__global__ void k_halo_pack(double* rd, double* buf, int first_a, int first_b, int n_a, int n_b,
+                            int layers, int stride, int dim, int unpack) {
+    const long long per = (long long)(n_a + n_b) * dim;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= per * layers) return;
+    const int l = (int)(t / per);
+    long long q = t % per;
+    const bool b = q >= (long long)n_a * dim;
+    if (b) q -= (long long)n_a * dim;
+    const long long g = ((long long)(b ? first_b : first_a) + (long long)l * stride) * dim + q;
+    const long long p = (b ? (long long)n_a * dim * layers : 0) + (long long)l *
+                        (b ? n_b : n_a) * dim + q;
+    if (unpack) rd[g] = buf[p];
+    else buf[p] = rd[g];
+}
+
+void halo_pack(pmts_pd* h, double* rd, double* buf, int fa, int fb, int na, int nb, bool unpack,
+               cudaStream_t st) {
+    const long long tot = (long long)(na + nb) * h->dim * h->halo_layers;
+    if (!tot) return;
+    k_halo_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(rd, buf, fa, fb, na, nb,
+                                                              h->halo_layers, h->halo_stride,
+                                                              h->dim, unpack ? 1 : 0);
+    CK(cudaGetLastError());
+}
+
 // halo exchange of the predictor displacement after a fine step
 void exchange_halo(pmts_pd* h, double* rd = nullptr, cudaStream_t st = nullptr) {
     if (!h->comm || (h->peer_lo < 0 && h->peer_hi < 0)) return;
@@ -225,6 +258,28 @@ void exchange_halo(pmts_pd* h, double* rd = nullptr, cudaStream_t st = nullptr) 
     const int dim = h->dim;
     if (!rd) rd = h->d.rd;
     if (!st) st = h->stream;
+    if (h->halo_layers > 1) {
+        // pack both send ranges, one message per neighbour, unpack both receive ranges
+        const int nl = h->peer_lo >= 0 ? h->n_lo : 0, nh = h->peer_hi >= 0 ? h->n_hi : 0;
+        const size_t ml = (size_t)nl * dim * h->halo_layers, mh = (size_t)nh * dim * h->halo_layers;
+        double* sb = h->halo_buf;
+        double* rb = h->halo_buf + ml + mh;
+        halo_pack(h, rd, sb, h->send_lo, h->send_hi, nl, nh, false, st);
+        nccl_check(a.group_start(), "group");
+        if (nl) {
+            nccl_check(a.send(sb, ml, kNcclFloat64, h->peer_lo, (ncclComm_t)h->comm, st), "send");
+            nccl_check(a.recv(rb, ml, kNcclFloat64, h->peer_lo, (ncclComm_t)h->comm, st), "recv");
+        }
+        if (nh) {
+            nccl_check(a.send(sb + ml, mh, kNcclFloat64, h->peer_hi, (ncclComm_t)h->comm, st),
+                       "send");
+            nccl_check(a.recv(rb + ml, mh, kNcclFloat64, h->peer_hi, (ncclComm_t)h->comm, st),
+                       "recv");
+        }
+        nccl_check(a.group_end(), "group");
+        halo_pack(h, rd, rb, h->recv_lo, h->recv_hi, nl, nh, true, st);
+        return;
+    }
     nccl_check(a.group_start(), "group");
     if (h->peer_lo >= 0) {
         nccl_check(a.send(rd + (size_t)h->send_lo * dim, (size_t)h->n_lo * dim, kNcclFloat64,
@@ -558,6 +613,20 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
     L.R = R;
     L.S = S;
     L.W = W;
+    // slab rows: node update on the owned y node rows, element forces on the rows
+    // those nodes touch (pmts_pd_desc.node_rows; one domain: everything)
+    L.jn0 = 0;
+    L.jn1 = ny + 1;
+    if (h->desc.node_rows[0] != 0 || h->desc.node_rows[1] != 0) {
+        if (h->desc.node_rows[0] < 0 || h->desc.node_rows[1] > ny + 1 ||
+            h->desc.node_rows[0] >= h->desc.node_rows[1])
+            throw ConfigError("node_rows out of the lattice");
+        L.jn0 = h->desc.node_rows[0];
+        L.jn1 = h->desc.node_rows[1];
+    }
+    L.jb0 = std::max(0, L.jn0 - 1);
+    L.jb1 = std::min(ny, L.jn1);
+    lat3_rows(L);
     int8_t* ddi = h->alloc<int8_t>(S);
     int8_t* ddj = h->alloc<int8_t>(S);
     int8_t* ddk = h->alloc<int8_t>(S);
@@ -1088,10 +1157,19 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         d.seed = ds.seed;
         d.fracture = h->fracture;
         d.goff = ds.global_id_offset;
+        d.id_pl = 0;
+        d.id_pg = 0;
+        if (ds.slab_plane[0] != 0 || ds.slab_plane[1] != 0) {
+            if (dim != 3 || ds.slab_plane[0] <= 0 || ds.slab_plane[1] < ds.slab_plane[0] ||
+                E % ds.slab_plane[0] != 0)
+                throw ConfigError("slab_plane: 3D only, 0 < local <= global, divides n_elems");
+            d.id_pl = ds.slab_plane[0];
+            d.id_pg = ds.slab_plane[1];
+        }
         d.own_lo = 0;
-        d.own_hi = E;
+        d.own_hi = d.id_pl ? d.id_pl : E;
         if (ds.owned_elems[0] != 0 || ds.owned_elems[1] != 0) {
-            if (ds.owned_elems[0] < 0 || ds.owned_elems[1] > E ||
+            if (ds.owned_elems[0] < 0 || ds.owned_elems[1] > d.own_hi ||
                 ds.owned_elems[0] > ds.owned_elems[1])
                 throw ConfigError("owned element range out of bounds");
             d.own_lo = ds.owned_elems[0];
@@ -1650,22 +1728,42 @@ int pmts_pd_gather_disp(pmts_pd* h, int32_t n, const int32_t* dofs, double* out)
 
 void* pmts_pd_stream(pmts_pd* h) { return h ? (void*)h->stream : nullptr; }
 
-int pmts_pd_get_rows(pmts_pd* h, int32_t first, int32_t n, double* out) {
+int pmts_pd_get_rows_layers(pmts_pd* h, int32_t first, int32_t n, int32_t layers,
+                            int32_t stride, double* out) {
     return guard([&] {
         if (!h) throw ConfigError("null handle");
-        if (first < 0 || n < 0 || first + n > h->N) throw ConfigError("node range out of bounds");
-        download(out, h->d.rd + (size_t)first * h->dim, (size_t)n * h->dim, h->stream);
+        if (first < 0 || n < 0 || layers < 1 || stride < 0 ||
+            (int64_t)first + (int64_t)(layers - 1) * stride + n > h->N)
+            throw ConfigError("node range out of bounds");
+        const size_t w = (size_t)n * h->dim * sizeof(double);
+        CK(cudaMemcpy2DAsync(out, w, h->d.rd + (size_t)first * h->dim,
+                             (size_t)stride * h->dim * sizeof(double), w, layers,
+                             cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
 }
 
-int pmts_pd_set_rows(pmts_pd* h, int32_t first, int32_t n, const double* in) {
+int pmts_pd_set_rows_layers(pmts_pd* h, int32_t first, int32_t n, int32_t layers, int32_t stride,
+                            const double* in) {
     return guard([&] {
         if (!h) throw ConfigError("null handle");
-        if (first < 0 || n < 0 || first + n > h->N) throw ConfigError("node range out of bounds");
-        upload(h->d.rd + (size_t)first * h->dim, in, (size_t)n * h->dim, h->stream);
+        if (first < 0 || n < 0 || layers < 1 || stride < 0 ||
+            (int64_t)first + (int64_t)(layers - 1) * stride + n > h->N)
+            throw ConfigError("node range out of bounds");
+        const size_t w = (size_t)n * h->dim * sizeof(double);
+        CK(cudaMemcpy2DAsync(h->d.rd + (size_t)first * h->dim,
+                             (size_t)stride * h->dim * sizeof(double), in, w, w, layers,
+                             cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
+}
+
+int pmts_pd_get_rows(pmts_pd* h, int32_t first, int32_t n, double* out) {
+    return pmts_pd_get_rows_layers(h, first, n, 1, 0, out);
+}
+
+int pmts_pd_set_rows(pmts_pd* h, int32_t first, int32_t n, const double* in) {
+    return pmts_pd_set_rows_layers(h, first, n, 1, 0, in);
 }
 
 int pmts_nccl_unique_id(void* id_out) {
@@ -1707,6 +1805,26 @@ int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t
         h->recv_hi = recv_hi_first;
         h->n_hi = n_hi;
         plan_split(h);
+    });
+}
+
+int pmts_pd_set_halo_layers(pmts_pd* h, int32_t layers, int32_t stride) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (layers < 1 || stride < 0) throw ConfigError("bad halo layers");
+        auto ok = [&](int f, int n) {
+            return (int64_t)f + (int64_t)(layers - 1) * stride + n <= h->N;
+        };
+        if ((h->peer_lo >= 0 && (!ok(h->send_lo, h->n_lo) || !ok(h->recv_lo, h->n_lo))) ||
+            (h->peer_hi >= 0 && (!ok(h->send_hi, h->n_hi) || !ok(h->recv_hi, h->n_hi))))
+            throw ConfigError("layered halo range out of bounds");
+        if (layers > 1 && h->split_a >= 0) throw ConfigError("layered halos: no launch split");
+        h->halo_layers = layers;
+        h->halo_stride = stride;
+        if (h->halo_buf) h->release(h->halo_buf);
+        h->halo_buf = nullptr;
+        if (layers > 1)
+            h->halo_buf = h->alloc<double>(2 * (size_t)(h->n_lo + h->n_hi) * h->dim * layers);
     });
 }
 

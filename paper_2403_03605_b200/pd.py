@@ -202,7 +202,8 @@ class PDSolver:
                  micromodulus=capi.MICRO_EXP, c0=0.0, l=1.0, c_const=0.0, h=1.0, s_crit=0.0,
                  s_crit_spread=0.0, seed=0, gamma=0.5, beta=0.0, mode=capi.DETERMINISTIC,
                  device=0, notch_npts=None, notch_pts=None, lattice=(0, 0, 0),
-                 global_id_offset=0, owned_elems=(0, 0), lattice_h=0.0, lattice_vol=0.0):
+                 global_id_offset=0, owned_elems=(0, 0), lattice_h=0.0, lattice_vol=0.0,
+                 slab_plane=(0, 0), node_rows=(0, 0)):
         self.dim = dim
         self._nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
         self._conn = np.ascontiguousarray(conn, dtype=np.int32)
@@ -233,6 +234,8 @@ class PDSolver:
         d.global_id_offset = int(global_id_offset)
         d.owned_elems[0], d.owned_elems[1] = int(owned_elems[0]), int(owned_elems[1])
         d.lattice_h, d.lattice_vol = float(lattice_h), float(lattice_vol)
+        d.slab_plane[0], d.slab_plane[1] = int(slab_plane[0]), int(slab_plane[1])
+        d.node_rows[0], d.node_rows[1] = int(node_rows[0]), int(node_rows[1])
         self.n_nodes, self.n_elems = d.n_nodes, d.n_elems
         self.n_dof = self.n_nodes * dim
         self.mode = mode
@@ -374,14 +377,18 @@ class PDSolver:
         return out
 
     # -- slab decomposition ---------------------------------------------------
-    def get_rows(self, first, n) -> np.ndarray:
-        out = np.zeros(n * self.dim)
-        check(lib().pmts_pd_get_rows(self.h, first, n, ptr(out)))
+    def get_rows(self, first, n, layers=1, stride=0) -> np.ndarray:
+        out = np.zeros(n * self.dim * layers)
+        check(lib().pmts_pd_get_rows_layers(self.h, first, n, layers, stride, ptr(out)))
         return out
 
-    def set_rows(self, first, n, vals):
+    def set_rows(self, first, n, vals, layers=1, stride=0):
         v = np.ascontiguousarray(vals, dtype=np.float64)
-        check(lib().pmts_pd_set_rows(self.h, first, n, ptr(v)))
+        assert v.size == n * self.dim * layers
+        check(lib().pmts_pd_set_rows_layers(self.h, first, n, layers, stride, ptr(v)))
+
+    def set_halo_layers(self, layers, stride):
+        check(lib().pmts_pd_set_halo_layers(self.h, layers, stride))
 
     def comm_init(self, uid: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(uid, 128)

@@ -26,7 +26,7 @@ import pytest
 
 from crack import agreement, broken_midpoints, crack_tip, hausdorff
 from oracle import pyoracle as po
-from paper_2403_03605_b200 import capi, slabs
+from paper_2403_03605_b200 import capi
 from paper_2403_03605_b200 import configs as cf
 from paper_2403_03605_b200.pd import PDSolver, Scenario
 
@@ -175,50 +175,13 @@ def test_cfg3_sub_f32pos_vs_oracle(sub):
 def test_cfg3_sub_two_slabs_bitwise(sub, mode):
     """Two slab handles (host-mediated halo exchange, one GPU): the hash keys use
     global ids (global_id_offset) -- owned fields and bond states bitwise one domain."""
+    from test_gpu_slabs import assert_slabs_equal, run_slabs, single_domain
+
     sc = sub["sc"]
-    steps = 220
-    one = _device(sc, mode)
-    nb1 = one.step(sc.scales(1, steps))
-    u, v, a = one.state()
-    intact = one.intact()
-    idx = {(int(i), int(j)): q for q, (i, j) in enumerate(sub["pairs"])}
-    hs = [slabs.solver_for_slab(sc, slabs.make_slab(sc.lattice, 2, r, 2), mode)
-          for r in range(2)]
-    for h in hs:
-        h.find_pe_pairs()
-        h.initial_acceleration(sc.load_scale(0.0))
-
-    def exchange():
-        msgs = []
-        for h in hs:
-            plo, slo, rlo, nlo, phi, shi, rhi, nhi = h.slab.halo
-            if plo >= 0:
-                msgs.append((plo, hs[plo].slab.halo[6], nlo, h.get_rows(slo, nlo)))
-            if phi >= 0:
-                msgs.append((phi, hs[phi].slab.halo[2], nhi, h.get_rows(shi, nhi)))
-        for dst, first, n, vals in msgs:
-            hs[dst].set_rows(first, n, vals)
-
-    exchange()
-    nb = 0
-    for i in range(1, steps + 1):
-        for h in hs:
-            nb += h.step([sc.load_scale(i * sc.dt)])
-        exchange()
+    one, nb1 = single_domain(sc, mode, 220)
+    hs, nb = run_slabs(sc, 2, mode, 220)
     assert nb == nb1 and nb1 > 100
-    for h in hs:
-        s = h.slab
-        lu, lv, la = h.state()
-        n0, n1 = s.own_nodes
-        g0, g1 = s.global_nodes(n0, n1)
-        assert np.array_equal(lu[n0 * 2:n1 * 2], u[g0 * 2:g1 * 2])
-        assert np.array_equal(lv[n0 * 2:n1 * 2], v[g0 * 2:g1 * 2])
-        assert np.array_equal(la[n0 * 2:n1 * 2], a[g0 * 2:g1 * 2])
-        lp, li = h.pairs(), h.intact()
-        own = (lp[:, 0] >= s.own_elems[0]) & (lp[:, 0] < s.own_elems[1])
-        gl = lp[own] + s.elem_first
-        q = np.array([idx[(int(i), int(j))] for i, j in gl])
-        assert np.array_equal(li[own], intact[q])
+    assert_slabs_equal(sc, one, hs)
 
 
 def test_cfg3_full_size_window_through_crack_initiation():
