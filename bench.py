@@ -193,15 +193,23 @@ def bench_mts(steps: int, warmup: int, with_cpu: bool) -> dict:
 
     out = {"metric": MTS_METRIC, "unit": MTS_UNIT, "higher_is_better": True}
     res = {}
-    for name in ("cfg2", "cfg2_0p5", "cfg2_nm"):
+    # the interface CG Jacobi-preconditioned (run.interface_precond = jacobi, an addition;
+    # DESIGN.md 9) on every workload, and cfg2's analog once more with the reference's
+    # plain CG (the library default)
+    for name, pc in (("cfg2", "jacobi"), ("cfg2_0p5", "jacobi"), ("cfg2_nm", "jacobi"),
+                     ("cfg2", "none")):
+        c = cf.get(name)
+        c["run"]["interface_precond"] = pc
+        key = name if pc == "jacobi" else name + "_plain_cg"
         t0 = time.perf_counter()
-        s = MtsSolver(cf.get(name))
+        s = MtsSolver(c)
         setup = time.perf_counter() - t0
         s.initialize()
         s.macro_step(warmup)
         ms = s.macro_step_timed(steps)
         reps = s.macro_step(1)
-        res[name] = {"value": steps / (ms * 1e-3), "ms_per_step": ms / steps, "setup_s": setup,
+        res[key] = {"value": steps / (ms * 1e-3), "ms_per_step": ms / steps, "setup_s": setup,
+                    "interface_precond": pc,
                      "n_lambda": s.n_lambda, "fe_dof": s.fe_n_dof, "pd_dof": s.pd_n_dof,
                      "dense_interface": s.dense,
                      "interface_iterations": reps[0]["interface_iterations"]}
@@ -214,6 +222,7 @@ def bench_mts(steps: int, warmup: int, with_cpu: bool) -> dict:
                                    "explicit PD, m=10, dt_pd 10 ns",
                        **{k: v for k, v in res["cfg2"].items() if k not in ("value", "ms_per_step")}},
                at_0p5mm=res["cfg2_0p5"],
+               reference_plain_cg=res["cfg2_plain_cg"],
                as_written={**res["cfg2_nm"],
                            "workload": "cfg2 as BASELINE writes it (non-matching meshes, an "
                                        "extension the reference cannot run): PD band at 0.25 mm, "

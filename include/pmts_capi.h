@@ -83,6 +83,9 @@ typedef struct {
     double total_time;
     double load_ramp;            /* < 0: auto (= m dt_pd), driver.hpp:187-191 */
     double gamma, beta;
+    int32_t host_setup;          /* 1: the setup loops on the host (the restatement the device
+                                    setup is tested against, tests/test_gpu_setup.py); 0: on the
+                                    device when one is present */
 } pmts_scenario_desc;
 
 typedef struct {
@@ -159,6 +162,8 @@ typedef struct {
     double bytes_per_step;       /* algorithmic HBM bytes per fine step */
     double bond_bytes_per_step;  /* ... of which the bond kernel (roofline numerator) */
     double device_bytes;         /* device memory held by the handle */
+    int64_t hot_tiles;           /* PMTS_OPT_COUNT_HOT: tiles whose break test ran / */
+    int64_t tested_tiles;        /* tiles the cold-tile screen examined, since enabled */
 } pmts_pd_info;
 
 const char* pmts_last_error(void);
@@ -250,6 +255,19 @@ int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t
  * layer_stride nodes apart (3D slabs cut along y); the library packs them into one
  * contiguous message per neighbour (a pack / unpack kernel around the NCCL group) */
 int pmts_pd_set_halo_layers(pmts_pd* h, int32_t n_layers, int32_t layer_stride);
+
+/* Run-time options of a handle (any time between steps).  All of them leave the
+ * results bitwise unchanged (tests/test_gpu_parity.py screen tests,
+ * test_tile9_split_launch_bitwise); they exist for those tests and diagnostics. */
+enum pmts_option {
+    PMTS_OPT_BREAK_SCREEN = 1,   /* 1 (default): skip the break test on tiles the
+                                    node-step bound proves cold; 0: test every tile */
+    PMTS_OPT_HALO_OVERLAP = 2,   /* 2D slabs: 1 = edge tile rows first, the NCCL halo on
+                                    a second stream under the interior rows (default 0;
+                                    without peers it splits the launch anyway) */
+    PMTS_OPT_COUNT_HOT = 3,      /* 1: count hot / tested tiles (pmts_pd_info) */
+};
+int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value);
 /* sum of an int64 over the clique (broken counts at output cadence) */
 int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value);
 
@@ -285,6 +303,9 @@ typedef struct {
                                     hull, coupling rows interpolating the FE velocity at the
                                     PD overlap nodes (extension); 0: the
                                     reference's single conforming mesh */
+    int32_t interface_precond;   /* matrix-free interface CG: 0 = the reference's plain CG
+                                    (mts.hpp:194-213, default); 1 = Jacobi-preconditioned with
+                                    diag(H_FE) + m dt / (2 M_PD) (an addition) */
 } pmts_mts_desc;
 
 typedef struct {

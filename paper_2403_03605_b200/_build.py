@@ -23,9 +23,6 @@ SOURCES = [
     ("pd_det.cu", ["-fmad=false"]),
     ("pd_fast.cu", []),
     ("pd_stencil.cu", []),
-    ("pd_stencil_fused.cu", []),
-    ("pd_strip2d.cu", []),
-    ("pd_tma2d.cu", []),
     ("pd_tile9.cu", []),
     ("pd_lat3.cu", []),
     ("pd_setup.cu", ["-fmad=false"]),

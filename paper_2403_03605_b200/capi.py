@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("PMTS_LIB_PATH") or os.path.join(HERE, "lib", "libpmts
 PMTS_OK, PMTS_ERR_INTERNAL, PMTS_ERR_CONFIG, PMTS_ERR_SOLVER = 0, 1, 2, 3
 DETERMINISTIC, FAST, FAST_F32POS = 0, 1, 2
 MICRO_EXP, MICRO_CONST = 0, 1
+OPT_BREAK_SCREEN, OPT_HALO_OVERLAP, OPT_COUNT_HOT = 1, 2, 3
 
 
 class PmtsError(RuntimeError):
@@ -43,7 +44,7 @@ class ScenarioDesc(C.Structure):
                 ("n_body_patch", _I), ("body_patch", _P), ("body_force", _D * 3),
                 ("n_velocity_bc", _I), ("velocity_bc", _P), ("n_fixed", _I), ("fixed", _P),
                 ("dt_pd", _D), ("m", _I), ("total_time", _D), ("load_ramp", _D),
-                ("gamma", _D), ("beta", _D)]
+                ("gamma", _D), ("beta", _D), ("host_setup", _I)]
 
 
 class ScenarioView(C.Structure):
@@ -71,7 +72,7 @@ class PDInfo(C.Structure):
     _fields_ = [("n_bonds", C.c_int64), ("n_entries", C.c_int64), ("max_family", _I),
                 ("path", _I), ("kernels_per_step", _I), ("stencil_size", _I),
                 ("bytes_per_step", _D), ("bond_bytes_per_step", _D),
-                ("device_bytes", _D)]
+                ("device_bytes", _D), ("hot_tiles", C.c_int64), ("tested_tiles", C.c_int64)]
 
 
 # exported symbols, with ctypes signatures: the CPU test checks the library
@@ -80,7 +81,8 @@ class MtsDesc(C.Structure):
     _fields_ = [("scenario", C.POINTER(ScenarioDesc)), ("n_pd_box", _I), ("pd_boxes", _P),
                 ("overlap_width_factor", _D), ("weight_kind", _I), ("gamma_fe", _D),
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
-                ("track_energy", _I), ("device", _I), ("fe_spacing", _D)]
+                ("track_energy", _I), ("device", _I), ("fe_spacing", _D),
+                ("interface_precond", _I)]
 
 
 class MtsView(C.Structure):
@@ -135,6 +137,7 @@ SIGNATURES = {
     "pmts_pd_get_rows_layers": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "pmts_pd_set_rows_layers": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "pmts_pd_set_halo_layers": (C.c_int, [_P, _I, _I]),
+    "pmts_pd_set_option": (C.c_int, [_P, _I, _I]),
     "pmts_pd_set_rows": (C.c_int, [_P, _I, _I, _P]),
     "pmts_nccl_unique_id": (C.c_int, [_P]),
     "pmts_pd_comm_init": (C.c_int, [_P, _P, _I, _I]),

@@ -91,6 +91,8 @@ void launch_det_bond(const DevPD& d, const double* disp, int step, int do_break,
                      cudaStream_t s);
 void launch_node_update(const DevPD& d, double scale, int predict_next, cudaStream_t s);
 void launch_predict(const DevPD& d, cudaStream_t s);
+void launch_damage_node(const DevPD& d, const double* elem, const uint8_t* has, double* node,
+                        cudaStream_t s);
 void launch_init_acc(const DevPD& d, double scale, cudaStream_t s);
 void launch_node_force(const DevPD& d, double* kx, cudaStream_t s);
 void launch_damage(const DevPD& d, double* elem, double* node, cudaStream_t s);

@@ -300,12 +300,17 @@ __global__ void k_damage_node(DevPD d, const double* phi, const uint8_t* has, do
     node[n] = cnt > 0 ? s / (double)cnt : 0.0;
 }
 
+void launch_damage_node(const DevPD& d, const double* elem, const uint8_t* has, double* node,
+                        cudaStream_t s) {
+    k_damage_node<<<(d.N + kThreads - 1) / kThreads, kThreads, 0, s>>>(d, elem, has, node);
+    PMTS_CUDA(cudaGetLastError());
+}
+
 void launch_damage(const DevPD& d, double* elem, double* node, cudaStream_t s) {
     uint8_t* has = nullptr;
     PMTS_CUDA(cudaMallocAsync(&has, (size_t)d.E, s));
     k_damage_elem<<<(d.E + kThreads - 1) / kThreads, kThreads, 0, s>>>(d, elem, has);
-    k_damage_node<<<(d.N + kThreads - 1) / kThreads, kThreads, 0, s>>>(d, elem, has, node);
-    PMTS_CUDA(cudaGetLastError());
+    launch_damage_node(d, elem, has, node, s);
     PMTS_CUDA(cudaFreeAsync(has, s));
 }
 

@@ -23,6 +23,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <cub/cub.cuh>
+
 #include "pd_stencil.cuh"
 
 namespace pmts {
@@ -415,6 +417,86 @@ int lattice_scan_device(const int32_t* d_col, int E, int K, int nx, int ny, int*
     const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
     return R;
+}
+
+// ---- damage_field (perifem.hpp:202-231) and the intact export on the lattice ----
+// `present` is the stencil mask as encoded (the bonds that exist); `mask` the live
+// one.  pos_only: the fused 2D kernels keep a bond's state at its lower element only,
+// so the negative offset s of e is read at the partner with the reversed offset
+// S - 1 - s.  The stencil is sorted by ascending linear delta, so s ascending is
+// partner id ascending -- the family order the ELL damage kernel sums in.
+namespace {
+__device__ __forceinline__ bool lat_bit(const uint32_t* m, int E, int e, int s) {
+    return (m[(size_t)(s >> 5) * E + e] >> (s & 31)) & 1u;
+}
+__global__ void k_lat_damage_elem(DevPD d, LatticeDev L, const uint32_t* present, int pos_only,
+                                  double* phi, uint8_t* has) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= d.E) return;
+    const int S = L.S;
+    double total = 0.0, intact = 0.0;
+    for (int s = 0; s < S; ++s) {
+        if (!lat_bit(present, d.E, e, s)) continue;
+        const int p = e + L.delta_id[s];
+        const int lo = e < p ? e : p, hi = e < p ? p : e;
+        // explicit roundings: this file builds with FMA contraction on, and the sums
+        // must round like damage_field's (pd_det.cu builds with -fmad=false)
+        const double w = __dmul_rn(d.vol[lo], d.vol[hi]);
+        total = __dadd_rn(total, w);
+        const bool live = (pos_only && p < e) ? lat_bit(d.mask, d.E, p, S - 1 - s)
+                                              : lat_bit(d.mask, d.E, e, s);
+        if (live) intact = __dadd_rn(intact, w);
+    }
+    phi[e] = total > 0.0 ? __dadd_rn(1.0, -__ddiv_rn(intact, total)) : 0.0;
+    has[e] = total != 0.0;
+}
+__global__ void k_lat_bond_count(const uint32_t* present, int E, int S, int W, int* cnt) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > E) return;
+    if (e == E) {  // the exclusive scan's total lands past the end
+        cnt[e] = 0;
+        return;
+    }
+    int c = 0;
+    for (int s = S / 2; s < S; ++s) c += lat_bit(present, E, e, s) ? 1 : 0;
+    cnt[e] = c;
+}
+__global__ void k_lat_intact(DevPD d, LatticeDev L, const uint32_t* present, const int* offs,
+                             uint8_t* out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= d.E) return;
+    int q = offs[e];
+    for (int s = L.S / 2; s < L.S; ++s)
+        if (lat_bit(present, d.E, e, s)) out[q++] = lat_bit(d.mask, d.E, e, s) ? 1 : 0;
+}
+}  // namespace
+
+void launch_lat_damage(const DevPD& d, const LatticeDev& L, const uint32_t* present, bool pos_only,
+                       double* elem, double* node, cudaStream_t s) {
+    uint8_t* has = nullptr;
+    PMTS_CUDA_S(cudaMallocAsync(&has, (size_t)d.E, s));
+    k_lat_damage_elem<<<(d.E + 255) / 256, 256, 0, s>>>(d, L, present, pos_only ? 1 : 0, elem, has);
+    launch_damage_node(d, elem, has, node, s);
+    PMTS_CUDA_S(cudaFreeAsync(has, s));
+}
+
+long long launch_lat_intact(const DevPD& d, const LatticeDev& L, const uint32_t* present,
+                            uint8_t* out_dev, cudaStream_t s) {
+    int* cnt = nullptr;
+    PMTS_CUDA_S(cudaMallocAsync(&cnt, sizeof(int) * ((size_t)d.E + 1), s));
+    k_lat_bond_count<<<(d.E + 256) / 256, 256, 0, s>>>(present, d.E, L.S, L.W, cnt);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, cnt, d.E + 1, s);
+    void* tmp = nullptr;
+    PMTS_CUDA_S(cudaMallocAsync(&tmp, tmp_bytes, s));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, cnt, d.E + 1, s);
+    int total = 0;
+    PMTS_CUDA_S(cudaMemcpyAsync(&total, cnt + d.E, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (out_dev) k_lat_intact<<<(d.E + 255) / 256, 256, 0, s>>>(d, L, present, cnt, out_dev);
+    PMTS_CUDA_S(cudaFreeAsync(tmp, s));
+    PMTS_CUDA_S(cudaFreeAsync(cnt, s));
+    PMTS_CUDA_S(cudaStreamSynchronize(s));
+    return total;
 }
 
 long long lattice_mask_device(const int32_t* d_col, int E, int K, int nx, int ny,

@@ -30,11 +30,11 @@ struct LatticeDev {
 
 constexpr int kTableRow = 8;
 
-// Fused single-kernel 2D step (pd_stencil_fused.cu) for the stencil sizes it is
-// instantiated for; per-offset constants travel in the kernel's parameter space.
+// Fused single-kernel 2D step (pd_tile9.cu) for the 28-offset stencil; per-offset
+// constants travel in the kernel's parameter space.
 constexpr int kFusedS = 28;  // delta in [3, sqrt(10)) dx: the paper's / BASELINE's 3.015 dx
 constexpr int kFusedR = 3;
-constexpr int kFusedTX = 31, kFusedTY = 15;  // own elements; force region 32 x 16
+constexpr int kFusedTX = 31;  // owned elements per tile row; force region 32 wide
 constexpr int kFusedAX = kFusedTX + 1 + 2 * kFusedR;
 struct Stencil2D {
     double xi0[kFusedS], xi1[kFusedS];    // representative xi of the offset
@@ -58,26 +58,6 @@ struct FusedBufs {
     double* trk_host = nullptr;  // this step's row (n_trk values)
 };
 
-void launch_fused2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
-                         const FusedBufs& b, int step, int do_break, double scale,
-                         int write_state, cudaStream_t s);
-void fused2d_configure();
-
-// TMA-pipelined persistent variant (pd_tma2d.cu): tensor maps of the current
-// predictor displacement (as [NY][2NX] doubles), rv and the packed {1/M, flags}.
-struct TmaMaps {
-    CUtensorMap rd, rv, aux;
-};
-int tma2d_tile_x();
-int tma2d_tile_y();
-int tma2d_apron_box_x();
-int tma2d_apron_box_y();
-int tma2d_in_box_x();
-int tma2d_in_box_y();
-void tma2d_configure();
-void launch_tma2d_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
-                       const TmaMaps& maps, const FusedBufs& b, int step, int do_break,
-                       double scale, int write_state, cudaStream_t s);
 
 // One-shot TMA-staged variant (pd_tile9.cu): tensor maps of the current rd
 // ([NY][2 NX] doubles), rv, and {1/M | flags} ([NY][NXP] doubles, NXP even,
@@ -137,20 +117,15 @@ void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, 
                       int do_break, cudaStream_t s);
 void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s);
 void lat3_rows(LatticeDev& L);  // ub0 / ugy from jb0 (call before lat3_tile_count)
+// damage_field (perifem.hpp:202-231) over the stencil bits (present = the encoded
+// mask: the bonds that exist); the intact state of every bond (i < j) in the pair
+// order (ascending i, then j) into out_dev (null: count only); returns the bonds
+void launch_lat_damage(const DevPD& d, const LatticeDev& L, const uint32_t* present, bool pos_only,
+                       double* elem, double* node, cudaStream_t s);
+long long launch_lat_intact(const DevPD& d, const LatticeDev& L, const uint32_t* present,
+                            uint8_t* out_dev, cudaStream_t s);
 size_t lat3_tile_count(const LatticeDev& L);
 void lat3_apron_box(int* bx, int* by, int* bz);  // TMA box of the ubar apron (doubles, rows, layers)
-
-// Row-streaming bond-symmetric variant (pd_strip2d.cu): constants of the 14
-// positive offsets, in that kernel's order.
-struct StripStencil {
-    double xi0[14], xi1[14], fx0[14], fx1[14], clo[14], cthr[14], x2[14];
-    long long did[14];
-};
-int strip2d_pos_offset(int k, int* di, int* dj);  // returns the offset's stencil index
-void strip2d_configure();
-void launch_strip2d_step(const DevPD& d, const LatticeDev& L, const StripStencil& st,
-                         const FusedBufs& b, int step, int do_break, double scale,
-                         int write_state, int H, cudaStream_t s);
 
 // device lattice encoding (setup): offsets present as 17^3 flags (component + 8),
 // returns the largest |component| (> 8: not encodable); then the intact mask of

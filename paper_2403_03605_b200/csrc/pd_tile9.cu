@@ -1,8 +1,6 @@
 // One-shot fused 2D fine step with TMA staging (tile v9), 28-offset stencil,
-// fast mode.  Arithmetic is the tile kernel's (pd_stencil_fused.cu: 31 x 31
-// owned elements, 32 x 32 force region, bond state at the lower end, integer
-// candidate compare) -- the two kernels are bitwise equal -- what changes is
-// how the CTA gets its inputs:
+// fast mode: 31 x 31 owned elements, 32 x 32 force region (own + one recomputed
+// ring), bond state at the lower end, integer candidate compare.  Inputs:
 //
 //   * at launch one thread issues three cp.async.bulk.tensor loads completing
 //     on two mbarriers -- the node apron of the predictor displacement (needed
@@ -351,8 +349,8 @@ int tile9_pair_offset(int k, int* a, int* b) {
     return 14;
 }
 
-// PAIRS: the pair-symmetric force with the cold-tile break screen; otherwise the
-// per-offset sums of pd_stencil_fused.cu (bitwise equal to it)
+// PAIRS: the pair-symmetric force with the cold-tile break screen; otherwise
+// per-offset sums with representative per-bond constants (lattice_h = 0)
 template <bool DO_BREAK, bool PAIRS, bool REPORT, bool F32>
 __global__ void __launch_bounds__(NT, kMinBlocks)
 k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
@@ -777,11 +775,6 @@ int tile9_configure() {
     return occ;
 }
 
-// PMTS_T9_NO_PDL=1: plain stream-ordered launches
-bool pdl_enabled() {
-    static const bool on = !std::getenv("PMTS_T9_NO_PDL");
-    return on;
-}
 
 void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        const PairStencil2D* ps, const Tile9Maps& maps, const FusedBufs& b,
@@ -804,7 +797,7 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
 #define PMTS_T9_LAUNCH(B, P, Q, F) \

@@ -48,7 +48,7 @@ int guard(F&& f) {
 void element_geometry(int dim, int n_elems, const int32_t* conn, const double* nodes,
                       double* centroid, double* volume);
 double char_length(int dim, int n_elems, const double* volume);
-double lattice_char_length(int dim, const int n[3], const double lo[3], double h);
+double lattice_char_length(int dim, const int n[3], const double lo[3], double h, bool host);
 double calibrate_c0(double E, double delta, double l, int formulation);
 // reference_shape gradients / values (fem.hpp:22-47) and the Jacobian
 // determinant of shape_and_gradients (fem.hpp:51-79); nodes are xyz triples

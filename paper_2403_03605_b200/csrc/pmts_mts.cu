@@ -148,6 +148,7 @@ struct pmts_mts {
     int nf = 0, np = 0, nl = 0, npe = 0, m = 1;
     Nm fe_nm, pd_nm;
     int iface_mode = 0;
+    bool interface_precond = false;  // pmts_mts_desc.interface_precond
     bool enforce_continuity = true, track_energy = true, fracture = false;
     double continuity_tol = 1e-8, cg_tol = 1e-10, interface_cg_tol = 1e-11;
     int fe_cg_max = 100;
@@ -178,7 +179,6 @@ struct pmts_mts {
     double *part = nullptr, *scal = nullptr;                               // reductions
     double* part2 = nullptr;      // fused CG dots: two partial rows
     unsigned* ticket = nullptr;   // their last-block counter
-    bool fused_cg = true;         // PMTS_MTS_UNFUSED_CG=1: the eleven-node iteration
     int32_t* famT_col = nullptr;  // entry-major families (PMTS_MTS_NO_TRANSPOSE=1: none)
     double* famT_coef = nullptr;
     double* famT_xi = nullptr;
@@ -203,8 +203,6 @@ struct pmts_mts {
 
     ~pmts_mts() {
         if (stream) cudaStreamSynchronize(stream);
-        for (auto& g : cg_graph)
-            if (g) cudaGraphExecDestroy(g);
         for (auto& g : cg_loop)
             if (g) cudaGraphExecDestroy(g);
         if (h_pin) cudaFreeHost(h_pin);
@@ -269,8 +267,7 @@ struct pmts_mts {
     // updates that mask (count into slot)
     // linear PD force (centroid form) on the entry-major families when built
     void force_lin(const double* x, const uint32_t* mask) {
-        if (famT_col) mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, famT_xi, x, mask, pd_ubar, stream);
-        else mtsk::pd_force_lin(pdv, x, mask, pd_ubar, stream);
+        mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, famT_xi, x, mask, pd_ubar, stream);
     }
 
     void pd_K(const double* x, double* y, uint32_t* mask, bool do_break, int slot) {
@@ -312,30 +309,21 @@ struct pmts_mts {
         // r.z, r.r, beta and rz <- rz_new in one launch -- bitwise the unfused order)
         auto body = [&] {
             op(p, ap);
-            if (fused_cg) {
-                mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
-                              s_alpha, stream);
-                mtsk::cg_update_precond(n, s_alpha, p, ap, x, r, jac, z, stream);
-                mtsk::dot_fin(n, r, z, r, r, part2, ticket, s_rzn, s_rr, 2, s_rz, s_beta, stream);
-                mtsk::xpby(n, z, s_beta, p, stream);
-                return;
-            }
-            mtsk::dot(n, p, ap, part, s_pap, stream);
-            mtsk::ratio(s_rz, s_pap, s_alpha, stream);
-            mtsk::cg_update(n, s_alpha, p, ap, x, r, stream);
-            mtsk::precond(n, r, jac, z, stream);
-            mtsk::dot(n, r, z, part, s_rzn, stream);
-            mtsk::ratio(s_rzn, s_rz, s_beta, stream);
+            mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
+                          s_alpha, stream);
+            mtsk::cg_update_precond(n, s_alpha, p, ap, x, r, jac, z, stream);
+            mtsk::dot_fin(n, r, z, r, r, part2, ticket, s_rzn, s_rr, 2, s_rz, s_beta, stream);
             mtsk::xpby(n, z, s_beta, p, stream);
-            CKM(cudaMemcpyAsync(s_rz, s_rzn, sizeof(double), cudaMemcpyDeviceToDevice, stream));
-            mtsk::dot(n, r, r, part, s_rr, stream);
         };
-        if (device_loop) {
+        {
             // the whole loop as one graph: a conditional WHILE node whose body is the
             // iteration plus the loop test (k_cg_cond) -- no host round trip per iteration
+            // the graph bakes in every pointer the iteration and the operator touch:
+            // rebuilt when any of its inputs changes or the operator's buffers are
+            // reallocated (invalidate_cg_graphs)
             cudaGraphExec_t& gl = cg_loop[graph_id];
-            if (gl && (cg_loop_x[graph_id] != x || cg_loop_tol[graph_id] != tol ||
-                       cg_loop_max[graph_id] != max_iter)) {
+            const CgKey key{x, b, jac, n, tol, max_iter, op_epoch};
+            if (gl && !(cg_key[graph_id] == key)) {
                 cudaGraphExecDestroy(gl);
                 gl = nullptr;
             }
@@ -359,9 +347,7 @@ struct pmts_mts {
                 CKM(cudaStreamEndCapture(stream, &bodyg));
                 CKM(cudaGraphInstantiate(&gl, g, 0));
                 cudaGraphDestroy(g);
-                cg_loop_x[graph_id] = x;
-                cg_loop_tol[graph_id] = tol;
-                cg_loop_max[graph_id] = max_iter;
+                cg_key[graph_id] = key;
             }
             if (!(rnorm / bnorm > tol)) return 0;
             if (max_iter <= 0)
@@ -383,45 +369,23 @@ struct pmts_mts {
                                   std::to_string(std::sqrt(h_pin[0]) / bnorm));
             return hs[0];
         }
-        cudaGraphExec_t& ge = cg_graph[graph_id];
-        if (ge && cg_graph_x[graph_id] != x) {  // x is baked into the graph
-            cudaGraphExecDestroy(ge);
-            ge = nullptr;
-        }
-        if (!ge) {
-            cudaGraph_t g;
-            CKM(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-            body();
-            CKM(cudaStreamEndCapture(stream, &g));
-            CKM(cudaGraphInstantiate(&ge, g, 0));
-            cudaGraphDestroy(g);
-            cg_graph_x[graph_id] = x;
-        }
-        int it = 0;
-        while (rnorm / bnorm > tol) {
-            if (it >= max_iter)
-                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
-                                  " iterations, residual " + std::to_string(rnorm / bnorm));
-            CKM(cudaGraphLaunch(ge, stream));
-            CKM(cudaMemcpyAsync(h_pin, scal + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
-            CKM(cudaStreamSynchronize(stream));
-            const double pap = h_pin[1];
-            if (pap <= 0.0)
-                throw SolverError("cg: operator not positive definite (p'Ap = " +
-                                  std::to_string(pap) + ")");
-            rnorm = std::sqrt(h_pin[0]);
-            ++it;
-        }
-        return it;
     }
-    cudaGraphExec_t cg_graph[2] = {nullptr, nullptr};
     cudaGraphExec_t cg_loop[2] = {nullptr, nullptr};  // device-side loops (conditional node)
-    const double* cg_loop_x[2] = {nullptr, nullptr};
-    double cg_loop_tol[2] = {0.0, 0.0};
-    int cg_loop_max[2] = {0, 0};
+    struct CgKey {
+        const double *x = nullptr, *b = nullptr, *jac = nullptr;
+        int n = 0;
+        double tol = 0.0;
+        int max_iter = 0;
+        unsigned epoch = 0;
+        bool operator==(const CgKey& o) const {
+            return x == o.x && b == o.b && jac == o.jac && n == o.n && tol == o.tol &&
+                   max_iter == o.max_iter && epoch == o.epoch;
+        }
+    };
+    CgKey cg_key[2];
+    unsigned op_epoch = 0;  // bumped whenever a buffer an operator captures is reallocated
+    void invalidate_cg_graphs() { ++op_epoch; }
     int* it_status = nullptr;  // {iterations, status} of the device-side loop
-    bool device_loop = true;   // PMTS_MTS_HOST_CG=1: host-driven loop, one graph per iteration
-    const double* cg_graph_x[2] = {nullptr, nullptr};
     double* h_pin = nullptr;  // pinned: (rr, pap) of the last iteration
     void sub(int n, const double* b, const double* ap, double* r) {
         // r = b - ap, elementwise, exactly as the reference's r[i] = b[i] - ap[i]
@@ -568,7 +532,7 @@ struct pmts_mts {
             // free-mass velocity of a PD dof after the m ramped substeps, m dt / (2 M) --
             // the (1 - alpha)-weighted PD masses span orders of magnitude across the
             // gluing zone, which is what slows the plain CG
-            if (!std::getenv("PMTS_MTS_PLAIN_CG")) {
+            if (interface_precond) {
                 std::vector<double> jd(nl, 0.0);
                 for (int r = 0; r < nl; ++r) {
                     jd[r] = h_fe[(size_t)r * nl + r] +
@@ -580,6 +544,7 @@ struct pmts_mts {
             hfe_rp = upload(rp);
             hfe_ci = upload(ci);
             hfe_v = upload(vv);
+            invalidate_cg_graphs();  // the interface operator captures these
         }
     }
     void refresh_dense_interface() {
@@ -934,7 +899,7 @@ void build_host(pmts_mts& h, const pmts_mts_desc& d) {
         int nfull[3] = {1, 1, 1};
         for (int k = 0; k < sd.dim; ++k)
             nfull[k] = int(std::lround((sd.hi[k] - sd.lo[k]) / sd.spacing));
-        s.cl = lattice_char_length(sd.dim, nfull, sd.lo, sd.spacing);
+        s.cl = lattice_char_length(sd.dim, nfull, sd.lo, sd.spacing, sd.host_setup != 0);
         s.delta = sd.delta_factor * s.cl;
         s.l = s.delta / sd.l_factor;
         s.c0 = calibrate_c0(sd.E, s.delta, s.l, sd.formulation);
@@ -1042,6 +1007,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->nl = int(s.cpl_fe.size());
         h->m = s.m;
         h->iface_mode = desc->interface_mode;
+        h->interface_precond = desc->interface_precond != 0;
         // interface mode (mts.hpp:111-114); the PD side is explicit
         h->use_dense = h->iface_mode == 1 || (h->iface_mode == 0 && h->nl <= 400);
         if (h->device < 0) {  // host-only: the assembled systems (view), no integrator
@@ -1122,7 +1088,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         pd_internal_pair_weights(h->pd, h->pe_weight.data());
         h->pdv = pd_internal_dev(h->pd);
         h->mask_live = h->pdv.mask;
-        if (!std::getenv("PMTS_MTS_NO_TRANSPOSE")) {
+        {  // entry-major families for the linear PD force (coalesced lanes)
             const size_t ek = (size_t)h->pdv.E * h->pdv.K;
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
@@ -1205,8 +1171,6 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->part2 = h->alloc<double>(2 * mtsk::dot_partials());
         h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
         CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
-        h->fused_cg = !std::getenv("PMTS_MTS_UNFUSED_CG");
-        h->device_loop = !std::getenv("PMTS_MTS_HOST_CG");
         h->it_status = reinterpret_cast<int*>(h->alloc<double>(1));
         CKM(cudaMallocHost(&h->h_pin, 4 * sizeof(double)));
         h->scal = h->alloc<double>(16);

@@ -89,14 +89,15 @@ struct pmts_pd {
     bool lattice = false;
     LatticeDev L{};
     std::vector<int> stencil_delta;  // linear id delta per stencil offset (ascending)
-    bool fused = false;              // one-kernel 2D step (pd_stencil_fused.cu / pd_strip2d.cu)
-    bool strip = false;              // ... the row-streaming bond-symmetric variant
-    bool tma = false;                // ... the TMA-pipelined persistent variant
+    bool fused = false;              // one-kernel 2D step (the TMA-staged tile kernel, pd_tile9.cu)
     bool pos_only = false;           // mask bits of negative offsets not maintained
-    int strip_h = 16;                // node rows per strip segment
-    TmaMaps tmaps[2]{};              // tensor maps with rd = buffer 0 / buffer 1
+    uint32_t* mask0 = nullptr;       // lattice: the stencil mask as encoded (bonds that exist)
+    // pmts_pd_set_option: the exact cold-tile break screens (default on) and the
+    // 2D halo-overlap launch split (default off)
+    bool screen = true, halo_overlap = false;
+    unsigned* lat3_tmax = nullptr;   // the 3D screen's per-tile maxima (kept when screen is off)
+    unsigned long long* hot_count = nullptr;  // PMTS_OPT_COUNT_HOT: {hot, tested} tiles
     double* rd_buf[2] = {nullptr, nullptr};
-    double* d_aux = nullptr;         // per node {1/M, flags} (TMA path)
     bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
     int tile9_occ = 0;               // its resident CTAs per SM
     CUtensorMap t9_rd[2]{}, t9_rv{}, t9_im{};
@@ -106,7 +107,6 @@ struct pmts_pd {
     PairStencil2D pst{};
     double* d_imf = nullptr;         // per node {1/M | flags}, rows padded to an even count
     Stencil2D st2{};
-    StripStencil sst{};
     bool lat3 = false;               // 3D 122-offset nominal-lattice bond kernel
     Stencil3D st3{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
@@ -363,27 +363,6 @@ PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
     return encode;
 }
 
-void build_tma_maps(pmts_pd* h) {
-    const PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
-    const int NX = h->L.nx + 1, NY = h->L.ny + 1;
-    auto make = [&](CUtensorMap* m, void* base, int bx, int by) {
-        const cuuint64_t dims[2] = {(cuuint64_t)2 * NX, (cuuint64_t)NY};
-        const cuuint64_t strides[1] = {(cuuint64_t)2 * NX * sizeof(double)};
-        const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
-        const cuuint32_t estr[2] = {1, 1};
-        const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box,
-                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            throw InternalError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    };
-    for (int b = 0; b < 2; ++b) {
-        make(&h->tmaps[b].rd, h->rd_buf[b], tma2d_apron_box_x(), tma2d_apron_box_y());
-        make(&h->tmaps[b].rv, h->d.rv, tma2d_in_box_x(), tma2d_in_box_y());
-        make(&h->tmaps[b].aux, h->d_aux, tma2d_in_box_x(), tma2d_in_box_y());
-    }
-}
 
 // TMA tensor maps of the tile9 kernel: rd of both ping-pong buffers, rv and
 // {1/M | flags}.  Box sizes come from pd_tile9.cu.
@@ -688,14 +667,18 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
     }
     h->d.mask = dmask;
     h->d.W = W;
+    // the encoded mask = the bonds that exist (damage_field's weights, the pair export)
+    if (h->mask0) h->release(h->mask0);
+    h->mask0 = h->alloc<uint32_t>((size_t)W * E);
+    CK(cudaMemcpyAsync(h->mask0, dmask, sizeof(uint32_t) * W * E, cudaMemcpyDeviceToDevice,
+                       h->stream));
     h->release((void*)h->d.coef);
     h->d.coef = nullptr;
     h->stencil_delta = dl;
     lattice_configure(dim, R, S);
     // 3D, 122 offsets, nominal constants: class-constant table for pd_lat3.cu
     h->lat3 = false;
-    if (dim == 3 && h->desc.lattice_h > 0.0 && lat3_offsets_match(di.data(), dj.data(), dk.data(), S) &&
-        !std::getenv("PMTS_NO_LAT3")) {
+    if (dim == 3 && h->desc.lattice_h > 0.0 && lat3_offsets_match(di.data(), dj.data(), dk.data(), S)) {
         const double hh = h->desc.lattice_h;
         bool ok = true, seen[8] = {false, false, false, false, false, false, false, false};
         for (int s = 0; s < S && ok; ++s) {
@@ -719,7 +702,7 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
         h->st3.hh = hh * hh;
         // TMA staging of the ubar apron (global rows must be 16-byte multiples: nx even)
         h->st3.use_tma = 0;
-        if (ok && L.nx % 2 == 0 && !std::getenv("PMTS_LAT3_NO_TMA")) {
+        if (ok && L.nx % 2 == 0) {
             const cuuint64_t dims[3] = {(cuuint64_t)3 * L.nx, (cuuint64_t)L.ny, (cuuint64_t)L.nz};
             const cuuint64_t strides[2] = {(cuuint64_t)3 * L.nx * 8, (cuuint64_t)3 * L.nx * L.ny * 8};
             int bx, by, bz;
@@ -734,23 +717,23 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
                 throw InternalError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
             h->st3.use_tma = 1;
         }
-        // cold-tile break screen (PMTS_LAT3_NO_SCREEN=1: break test on every tile)
+        // cold-tile break screen (pmts_pd_set_option PMTS_OPT_BREAK_SCREEN = 0: the
+        // break test on every tile)
         h->st3.tmax = nullptr;
-        if (ok && !std::getenv("PMTS_LAT3_NO_SCREEN")) {
+        h->lat3_tmax = nullptr;
+        if (ok) {
+            h->st3.hot_count = h->pst.hot_count = h->hot_count;
             const size_t nt = lat3_tile_count(h->L);
             unsigned* tm = h->alloc<unsigned>(9 * nt);
             CK(cudaMemsetAsync(tm, 0, 9 * nt * sizeof(unsigned), h->stream));
-            h->st3.tmax = tm;
+            h->lat3_tmax = tm;
+            if (h->screen) h->st3.tmax = tm;
         }
-        h->st3.hot_count = nullptr;
-        if (std::getenv("PMTS_T9_COUNT_HOT")) {
-            h->st3.hot_count = h->alloc<unsigned long long>(2);
-            CK(cudaMemsetAsync(h->st3.hot_count, 0, 16, h->stream));
-        }
+
         h->lat3 = ok;
     }
     h->fused = false;
-    if (dim == 2 && S == kFusedS && R == kFusedR && !std::getenv("PMTS_NO_FUSED")) {
+    if (dim == 2 && S == kFusedS && R == kFusedR) {
         Stencil2D& st = h->st2;
         for (int s = 0; s < S; ++s) {
             const double* t = table.data() + kTableRow * (size_t)s;
@@ -767,15 +750,9 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
         if (!h->rd_alt) h->rd_alt = h->alloc<double>(h->ndof);
         if (h->mask_alt) h->release(h->mask_alt);
         h->mask_alt = h->alloc<uint32_t>((size_t)E);
-        fused2d_configure();
         h->fused = true;
-        // kernel variant: PMTS_FUSED_KERNEL = tile9 (default) | tile | tma | strip
-        const char* kv = std::getenv("PMTS_FUSED_KERNEL");
-        const std::string kvs = kv ? kv : "tile9";
-        h->strip = kvs == "strip";
-        h->tma = kvs == "tma";
-        h->tile9 = kvs == "tile9";
-        h->pos_only = !h->strip && !h->tma;  // the tile kernels keep bond state at the lower end
+        h->tile9 = true;
+        h->pos_only = true;  // the tile kernel keeps a bond's state at its lower end
         if (h->tile9) {
             // {1/M | flags}: flags (1 x, 2 y constrained, 4 loaded) in the low mantissa bits
             const int NX = h->L.nx + 1, NY = h->L.ny + 1, NXP = (NX + 1) & ~1;
@@ -795,11 +772,10 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
                 int sms = 0;
                 CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->desc.device));
                 h->t9_prefetch = sms * h->tile9_occ;
-                if (const char* e = std::getenv("PMTS_T9_PREFETCH")) h->t9_prefetch = std::atoi(e);
             }
-            // pair-symmetric force on the nominal lattice (PMTS_NO_PAIRS=1 keeps the
-            // tile kernel's per-offset arithmetic, bitwise equal to pd_stencil_fused.cu)
-            h->pairs = h->desc.lattice_h > 0.0 && !std::getenv("PMTS_NO_PAIRS");
+            // pair-symmetric force on the nominal lattice (representative per-bond
+            // constants, lattice_h = 0: the per-offset sums)
+            h->pairs = h->desc.lattice_h > 0.0;
             const double hh = h->desc.lattice_h;
 
             for (int k = 0; k < 14 && h->pairs; ++k) {
@@ -832,47 +808,9 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
                 if ((double)f > c) f = std::nextafter(f, 0.0f);
                 h->pst.clf[k] = f;
             }
-            // cold-tile break screen (PMTS_T9_NO_SCREEN=1: candidate pass on every tile)
-            h->pst.screen = std::getenv("PMTS_T9_NO_SCREEN") ? 0 : 1;
-            h->pst.hot_count = nullptr;
-            if (std::getenv("PMTS_T9_COUNT_HOT")) {
-                h->pst.hot_count = h->alloc<unsigned long long>(2);
-                CK(cudaMemsetAsync(h->pst.hot_count, 0, 16, h->stream));
-            }
-        }
-        if (h->tma) {
-            std::vector<double> aux(2 * (size_t)h->N);
-            for (int n = 0; n < h->N; ++n) {
-                aux[2 * (size_t)n] = im[n];
-                aux[2 * (size_t)n + 1] = (double)nflag[n];
-            }
-            if (!h->d_aux) h->d_aux = h->alloc<double>(2 * (size_t)h->N);
-            upload(h->d_aux, aux.data(), aux.size(), h->stream);
-            h->rd_buf[0] = h->d.rd;
-            h->rd_buf[1] = h->rd_alt;
-            build_tma_maps(h);
-            tma2d_configure();
-        }
-        if (h->strip) {
-            for (int k = 0; k < 14; ++k) {
-                int pdi = 0, pdj = 0;
-                const int s = strip2d_pos_offset(k, &pdi, &pdj);
-                if (di[s] != pdi || dj[s] != pdj) {
-                    h->strip = false;  // host stencil order differs: keep the tile kernel
-                    break;
-                }
-                const double* t = table.data() + kTableRow * (size_t)s;
-                h->sst.xi0[k] = t[0];
-                h->sst.xi1[k] = t[1];
-                h->sst.fx0[k] = t[2] * t[0];
-                h->sst.fx1[k] = t[2] * t[1];
-                h->sst.cthr[k] = t[3];
-                h->sst.clo[k] = t[5];
-                h->sst.x2[k] = t[6];
-                h->sst.did[k] = dl[s];
-            }
-            if (const char* e = std::getenv("PMTS_STRIP_H")) h->strip_h = std::max(8, std::atoi(e));
-            if (h->strip) strip2d_configure();
+            // cold-tile break screen (PMTS_OPT_BREAK_SCREEN = 0: candidate pass on every tile)
+            h->pst.screen = h->screen ? 1 : 0;
+            h->pst.hot_count = h->hot_count;
         }
     }
     CK(cudaStreamSynchronize(h->stream));
@@ -881,31 +819,12 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
 }
 
 // ELL-layout intact mask (bit k = k-th family entry) from the stencil mask
+// the live ELL bond mask on the host (ELL paths; the lattice has its own kernels)
 std::vector<uint32_t> ell_mask_host(pmts_pd* h) {
-    ensure_hcol(h);
-    const int E = h->E, K = h->d.K;
-    std::vector<uint32_t> m((size_t)h->d.W * E);
+    std::vector<uint32_t> m((size_t)h->d.W * h->E);
     download(m.data(), h->d.mask, m.size(), h->stream);
     CK(cudaStreamSynchronize(h->stream));
-    if (!h->lattice) return m;
-    const int We = std::max(1, (K + 31) / 32);
-    std::vector<uint32_t> out((size_t)We * E, 0u);
-    std::map<int, int> sidx;
-    for (size_t s = 0; s < h->stencil_delta.size(); ++s) sidx[h->stencil_delta[s]] = (int)s;
-    const int S = (int)h->stencil_delta.size();
-    for (int e = 0; e < E; ++e)
-        for (int q = 0; q < K; ++q) {
-            const int p = h->hcol[(size_t)q * E + e];
-            if (p < 0) break;
-            int s = sidx.at(p - e), owner = e;
-            if (h->pos_only && p < e) {  // state kept by the lower element, reverse offset
-                s = S - 1 - s;
-                owner = p;
-            }
-            if ((m[(size_t)(s >> 5) * E + owner] >> (s & 31)) & 1u)
-                out[(size_t)(q >> 5) * E + e] |= 1u << (q & 31);
-        }
-    return out;
+    return m;
 }
 
 void require_families(pmts_pd* h) {
@@ -932,7 +851,7 @@ void ensure_counts(pmts_pd* h, int n) {
 // launch) -- about the NCCL latency it would hide.
 void plan_split(pmts_pd* h) {
     const bool peers = h->comm && (h->peer_lo >= 0 || h->peer_hi >= 0);
-    const bool forced = std::getenv("PMTS_T9_SPLIT") != nullptr;
+    const bool forced = h->halo_overlap;
     h->split_a = h->split_b = -1;
     if (!h->tile9 || !forced) return;
     const int rows = tile9_rows(h->L), ty = tile9_tile_rows(), NX = h->L.nx + 1;
@@ -999,17 +918,8 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
             std::swap(h->d.mask, h->mask_alt);
             return;
         }
-        if (h->tile9)
-            launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b,
-                              slot, brk, scale, last ? 1 : 0, h->f32pos, h->stream);
-        else if (h->tma)
-            launch_tma2d_step(h->d, h->L, h->st2, h->tmaps[h->d.rd == h->rd_buf[0] ? 0 : 1], b,
-                              slot, brk, scale, last ? 1 : 0, h->stream);
-        else if (h->strip)
-            launch_strip2d_step(h->d, h->L, h->sst, b, slot, brk, scale, last ? 1 : 0,
-                                h->strip_h, h->stream);
-        else
-            launch_fused2d_step(h->d, h->L, h->st2, b, slot, brk, scale, last ? 1 : 0, h->stream);
+        launch_tile9_step(h->d, h->L, h->st2, h->pairs ? &h->pst : nullptr, tile9_maps(h), b, slot,
+                          brk, scale, last ? 1 : 0, h->f32pos, h->stream);
         if (time_bond) CK(cudaEventRecord(ev[1], h->stream));
         std::swap(h->d.rd, h->rd_alt);
         std::swap(h->d.mask, h->mask_alt);
@@ -1242,16 +1152,6 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
 }
 
 void pmts_pd_destroy(pmts_pd* h) {
-    if (h && h->pst.hot_count) {  // PMTS_T9_COUNT_HOT diagnostics
-        unsigned long long c[2] = {0, 0};
-        cudaMemcpy(c, h->pst.hot_count, 16, cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "pmts: tile9 screen: %llu of %llu tiles hot\n", c[0], c[1]);
-    }
-    if (h && h->lat3 && h->st3.hot_count) {
-        unsigned long long c[2] = {0, 0};
-        cudaMemcpy(c, h->st3.hot_count, 16, cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "pmts: lat3 screen: %llu of %llu tiles hot\n", c[0], c[1]);
-    }
     if (h && h->xstream) {
         cudaStreamSynchronize(h->xstream);
         cudaStreamDestroy(h->xstream);
@@ -1276,7 +1176,7 @@ int pmts_pd_build_families(pmts_pd* h) {
         // fast mode on the generated lattice with nominal constants: the families stay
         // on the device and are encoded there (no host walk over the F entries; the
         // host copy is fetched only if a caller asks for pairs / intact states)
-        if (h->mode == PMTS_FAST && h->desc.lattice_h > 0.0 && !std::getenv("PMTS_HOST_ENCODE")) {
+        if (h->mode == PMTS_FAST && h->desc.lattice_h > 0.0) {
             if (h->d.coef) h->release((void*)h->d.coef);
             if (h->d.mask) h->release(h->d.mask);
             if (h->d.col) h->release((void*)h->d.col);
@@ -1406,6 +1306,16 @@ int pmts_pd_get_pairs(pmts_pd* h, int32_t* out, int64_t cap, int64_t* n_out) {
 int pmts_pd_get_intact(pmts_pd* h, uint8_t* out, int64_t cap) {
     return guard([&] {
         require_families(h);
+        if (h->lattice) {  // on the device, over the stencil bits
+            const long long nb = launch_lat_intact(h->d, h->L, h->mask0, nullptr, h->stream);
+            uint8_t* dv = nullptr;
+            CK(cudaMallocAsync(&dv, (size_t)std::max(nb, 1LL), h->stream));
+            launch_lat_intact(h->d, h->L, h->mask0, dv, h->stream);
+            download(out, dv, (size_t)std::max<int64_t>(0, std::min<int64_t>(cap, nb)), h->stream);
+            CK(cudaFreeAsync(dv, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            return;
+        }
         ensure_hcol(h);
         const int E = h->E, K = h->d.K;
         const std::vector<uint32_t> mask = ell_mask_host(h);
@@ -1463,6 +1373,14 @@ int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
             }
         }
         info->device_bytes = h->device_bytes;
+        info->hot_tiles = info->tested_tiles = 0;
+        if (h->hot_count) {
+            unsigned long long c[2] = {0, 0};
+            download(c, h->hot_count, 2, h->stream);
+            CK(cudaStreamSynchronize(h->stream));
+            info->hot_tiles = (int64_t)c[0];
+            info->tested_tiles = (int64_t)c[1];
+        }
     });
 }
 
@@ -1696,17 +1614,10 @@ int pmts_pd_damage(pmts_pd* h, double* elem, double* node) {
         double* dn = nullptr;
         CK(cudaMallocAsync(&de, sizeof(double) * h->E, h->stream));
         CK(cudaMallocAsync(&dn, sizeof(double) * h->N, h->stream));
-        DevPD dd = h->d;
-        uint32_t* tmp = nullptr;
-        if (h->lattice) {  // damage walks ELL families: translate the stencil bits
-            const std::vector<uint32_t> m = ell_mask_host(h);
-            CK(cudaMallocAsync(&tmp, sizeof(uint32_t) * m.size(), h->stream));
-            upload(tmp, m.data(), m.size(), h->stream);
-            dd.mask = tmp;
-            dd.W = std::max(1, (h->d.K + 31) / 32);
-        }
-        launch_damage(dd, de, dn, h->stream);
-        if (tmp) CK(cudaFreeAsync(tmp, h->stream));
+        if (h->lattice)  // over the stencil bits on the device
+            launch_lat_damage(h->d, h->L, h->mask0, h->pos_only, de, dn, h->stream);
+        else
+            launch_damage(h->d, de, dn, h->stream);
         if (elem) download(elem, de, h->E, h->stream);
         if (node) download(node, dn, h->N, h->stream);
         CK(cudaFreeAsync(de, h->stream));
@@ -1805,6 +1716,39 @@ int pmts_pd_set_halo(pmts_pd* h, int32_t peer_lo, int32_t send_lo_first, int32_t
         h->recv_hi = recv_hi_first;
         h->n_hi = n_hi;
         plan_split(h);
+    });
+}
+
+int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        switch (option) {
+            case PMTS_OPT_BREAK_SCREEN:
+                h->screen = value != 0;
+                h->pst.screen = h->screen ? 1 : 0;
+                h->st3.tmax = h->screen ? h->lat3_tmax : nullptr;
+                break;
+            case PMTS_OPT_HALO_OVERLAP:
+                h->halo_overlap = value != 0;
+                if (h->halo_overlap && h->halo_layers > 1)
+                    throw ConfigError("halo overlap: 2D slabs only");
+                if (h->families) plan_split(h);
+                break;
+            case PMTS_OPT_COUNT_HOT: {
+                unsigned long long* c = nullptr;
+                if (value) {
+                    c = h->hot_count ? h->hot_count : h->alloc<unsigned long long>(2);
+                    CK(cudaMemsetAsync(c, 0, 16, h->stream));
+                }
+                h->hot_count = c ? c : h->hot_count;
+                h->pst.hot_count = c;
+                h->st3.hot_count = c;
+                break;
+            }
+            default:
+                throw ConfigError("unknown option " + std::to_string(option));
+        }
+        CK(cudaStreamSynchronize(h->stream));
     });
 }
 

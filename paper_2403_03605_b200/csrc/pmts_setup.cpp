@@ -105,11 +105,11 @@ double char_length(int dim, int n_elems, const double* volume) {
 // Mesh::char_length (mesh.hpp:51-57) of the generated lattice n[0] x n[1] (x n[2])
 // at spacing h from lo, without storing it: the volume sum on the device when
 // one is present, else the same sum streamed on the host
-double lattice_char_length(int dim, const int n[3], const double lo[3], double h) {
+double lattice_char_length(int dim, const int n[3], const double lo[3], double h, bool host) {
     const long long E = (long long)n[0] * n[1] * (dim == 3 ? n[2] : 1);
     if (E <= 0) return 0.0;
     double v = 0.0;
-    if (!std::getenv("PMTS_HOST_SETUP") && device_available()) {
+    if (!host && device_available()) {
         v = lattice_volume_sum_device(dim, n, lo, h);
     } else {
         const double gp = 1.0 / std::sqrt(3.0);
@@ -278,7 +278,7 @@ void build(pmts_scenario& s, const pmts_scenario_desc& d) {
             if (p) setup_device_end(p);
         }
     } dev_guard{dev};
-    if (!std::getenv("PMTS_HOST_SETUP") && device_available()) {
+    if (!d.host_setup && device_available()) {
         if (d.spacing <= 0.0) throw ConfigError("mesh spacing must be positive");
         if (d.dim != 2 && d.dim != 3) throw ConfigError("mesh dimension must be 2 or 3");
         s.dim = d.dim;

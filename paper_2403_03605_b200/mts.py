@@ -58,6 +58,9 @@ class MtsSolver:
         d.device = device
         # extension: non-matching FE lattice (mesh.fe_spacing), DESIGN.md section 11
         d.fe_spacing = float(sc["mesh"].get("fe_spacing") or 0.0)
+        # extension: Jacobi-preconditioned interface CG (run.interface_precond = jacobi);
+        # the default is the reference's plain CG
+        d.interface_precond = 1 if run.get("interface_precond", "none") == "jacobi" else 0
         h = C.c_void_p()
         check(lib().pmts_mts_create(C.byref(d), C.byref(h)))
         self.h = h

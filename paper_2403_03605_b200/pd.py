@@ -123,10 +123,11 @@ def scenario_desc(sc: dict, keep: list) -> "capi.ScenarioDesc":
 class Scenario:
     """build_scenario for a generated pure-PD run (host C++ setup in libpmts)."""
 
-    def __init__(self, sc: dict):
+    def __init__(self, sc: dict, host_setup: bool = False):
         self.cfg = sc
         self._keep = []
         d = scenario_desc(sc, self._keep)
+        d.host_setup = 1 if host_setup else 0
         self.notch_npts, self.notch_pts = self._keep[0], self._keep[1]
         h = C.c_void_p()
         check(lib().pmts_scenario_build(C.byref(d), C.byref(h)))
@@ -386,6 +387,11 @@ class PDSolver:
         v = np.ascontiguousarray(vals, dtype=np.float64)
         assert v.size == n * self.dim * layers
         check(lib().pmts_pd_set_rows_layers(self.h, first, n, layers, stride, ptr(v)))
+
+    def set_option(self, option: int, value: int):
+        """pmts_pd_set_option (capi.OPT_*): results are bitwise unchanged."""
+        check(lib().pmts_pd_set_option(self.h, int(option), int(value)))
+        return self
 
     def set_halo_layers(self, layers, stride):
         check(lib().pmts_pd_set_halo_layers(self.h, layers, stride))

@@ -87,17 +87,17 @@ def test_mts_fracture_breaks_bonds():
     assert sum(r["newly_broken"] for r in reps) == len(g["broken"]) > 0
 
 
-def test_interface_preconditioner_same_solution(monkeypatch):
-    """The Jacobi-preconditioned interface CG (default; diag(H_FE) + the free-mass PD
-    response m dt / 2M) reaches the plain CG's multipliers (the reference's solver,
-    PMTS_MTS_PLAIN_CG=1) within the CG tolerance, in no more iterations."""
+def test_interface_preconditioner_same_solution():
+    """The Jacobi-preconditioned interface CG (opt-in, run.interface_precond = jacobi:
+    diag(H_FE) + the free-mass PD response m dt / 2M) reaches the multipliers of the
+    reference's plain CG (the default) within the CG tolerance, in no more iterations."""
     out = {}
     for plain in (False, True):
-        if plain:
-            monkeypatch.setenv("PMTS_MTS_PLAIN_CG", "1")
-        else:
-            monkeypatch.delenv("PMTS_MTS_PLAIN_CG", raising=False)
-        g, s = _run("mts_mini_mfree")
+        g = load_golden("mts_mini_mfree")
+        c = cf.get(g["meta"]["scenario"])
+        c["run"]["interface_precond"] = "none" if plain else "jacobi"
+        s = MtsSolver(c)
+        s.initialize()
         reps = s.macro_step(g["meta"]["steps"])
         out[plain] = (s.lam(), s.state("pd")[0], sum(r["interface_iterations"] for r in reps))
     (lp, up, ip), (lq, uq, iq) = out[False], out[True]

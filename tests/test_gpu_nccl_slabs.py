@@ -40,11 +40,10 @@ def _worker(rank, world, port, name, mode, steps, split, out_dir):
     import sys
 
     sys.path.insert(0, ROOT)
-    if split:
-        os.environ["PMTS_T9_SPLIT"] = "1"
     import torch
     import torch.distributed as dist
 
+    from paper_2403_03605_b200 import capi
     from paper_2403_03605_b200 import configs as cf
     from paper_2403_03605_b200 import slabs
     from paper_2403_03605_b200.pd import PDSolver, Scenario
@@ -59,6 +58,8 @@ def _worker(rank, world, port, name, mode, steps, split, out_dir):
         uid[:] = torch.frombuffer(bytearray(PDSolver.nccl_unique_id()), dtype=torch.uint8)
     dist.broadcast(uid, 0)
     slabs.attach_nccl(h, bytes(uid.tolist()))
+    if split:  # edge tile rows first, the NCCL halo on a second stream under the interior
+        h.set_option(capi.OPT_HALO_OVERLAP, 1)
     v0 = sc.initial_velocity()
     if v0.any():
         z = np.zeros(h.n_dof)

@@ -15,11 +15,9 @@ SCALARS = ["n_nodes", "n_elems", "delta", "l", "c0", "char_length", "dt", "s_cri
 
 
 @pytest.mark.parametrize("name", ["mini", "block3d", "cfg1", "bp_coarse", "cfg3", "cfg4"])
-def test_device_setup_bitwise_equals_host(name, monkeypatch):
-    monkeypatch.delenv("PMTS_HOST_SETUP", raising=False)
+def test_device_setup_bitwise_equals_host(name):
     dev = Scenario(cf.get(name))
-    monkeypatch.setenv("PMTS_HOST_SETUP", "1")
-    host = Scenario(cf.get(name))
+    host = Scenario(cf.get(name), host_setup=True)
     for f in SCALARS:
         assert getattr(dev, f) == getattr(host, f), f
     for f in FIELDS:
