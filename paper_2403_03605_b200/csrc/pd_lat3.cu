@@ -144,6 +144,27 @@ __device__ __forceinline__ unsigned hi_abs3(double d) {
 __device__ __forceinline__ double hi_bound3(unsigned m) {  // >= every |d| with hi_abs3(d) <= m
     return __hiloint2double((int)m, (int)0xffffffffu);
 }
+
+// Launch order of the 3D tiles (both kernels, a 1D grid): z fastest, then x, then y.
+// A CTA's ubar apron reaches 3 layers into the z-neighbour tiles; in (x, y, z) order
+// those were ~gx gy CTAs back (cfg5: 5000, ~300 MB of ubar earlier -- evicted from
+// L2, the 1.48x DRAM traffic of the round-1 capture); in this order the whole z column
+// of a tile and its x neighbours are adjacent in launch order, and the y neighbours
+// are one (gx gz)-tile row back (cfg5: 250 tiles, a few MB).
+struct Tile3 {
+    int x, y, z, gx, gz;
+};
+__device__ __forceinline__ Tile3 tile3(const LatticeDev& L) {
+    Tile3 t;
+    t.gx = (L.nx + TX - 1) / TX;
+    t.gz = (L.nz + TZ - 1) / TZ;
+    const int b = blockIdx.x;
+    t.z = b % t.gz;
+    const int r = b / t.gz;
+    t.x = r % t.gx;
+    t.y = r / t.gx;
+    return t;
+}
 }  // namespace
 
 // ubar of the 3D lattice, one CTA per bond-kernel tile (16 x 4 x 4 elements), plus
@@ -156,7 +177,8 @@ k_lat3_ubar(DevPD d, LatticeDev L, unsigned* tmax) {
     __shared__ unsigned red[NT / 32][9];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
-    const int i = blockIdx.x * TX + tx, j = L.ub0 + blockIdx.y * TY + ty, k = blockIdx.z * TZ + tz;
+    const Tile3 T = tile3(L);
+    const int i = T.x * TX + tx, j = L.ub0 + T.y * TY + ty, k = T.z * TZ + tz;
     unsigned mx[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) mx[q] = 0u;
@@ -202,7 +224,7 @@ k_lat3_ubar(DevPD d, LatticeDev L, unsigned* tmax) {
         unsigned v = 0u;
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w) v = max(v, red[w][tid]);
-        tmax[((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 9 + tid] = v;
+        tmax[((size_t)(T.z * L.ugy + T.y) * T.gx + T.x) * 9 + tid] = v;
     }
 }
 
@@ -213,20 +235,19 @@ k_lat3_ubar(DevPD d, LatticeDev L, unsigned* tmax) {
 // D_ac, so 2h o.eta + |eta|^2 <= 2h sum_c |o_c| E_c + sum_c E_c^2.  A tile where that
 // bound (x (1 + 1e-6)) stays below every offset's candidate threshold runs the force
 // without the break test: bitwise the same result, no candidate could fire.
-__device__ __forceinline__ bool lat3_tile_hot(const Stencil3D& st, const LatticeDev& L) {
+__device__ __forceinline__ bool lat3_tile_hot(const Stencil3D& st, const LatticeDev& L,
+                                              const Tile3& T) {
     __shared__ unsigned dmax[9];
     const int tid = threadIdx.x;
     if (tid < 9) dmax[tid] = 0u;
     __syncthreads();
     if (tid < 27 * 9) {
         const int t = tid / 9, q = tid % 9;
-        // bond tile y row blockIdx.y is ubar tile row blockIdx.y + (jb0 - ub0) / TY
-        const int by0 = blockIdx.y + (L.jb0 - L.ub0) / TY;
-        const int bx = blockIdx.x + t % 3 - 1, by = by0 + (t / 3) % 3 - 1,
-                  bz = blockIdx.z + t / 9 - 1;
-        if (bx >= 0 && by >= 0 && bz >= 0 && bx < (int)gridDim.x && by < L.ugy &&
-            bz < (int)gridDim.z)
-            atomicMax(&dmax[q], st.tmax[((size_t)(bz * L.ugy + by) * gridDim.x + bx) * 9 + q]);
+        // bond tile y row T.y is ubar tile row T.y + (jb0 - ub0) / TY
+        const int by0 = T.y + (L.jb0 - L.ub0) / TY;
+        const int bx = T.x + t % 3 - 1, by = by0 + (t / 3) % 3 - 1, bz = T.z + t / 9 - 1;
+        if (bx >= 0 && by >= 0 && bz >= 0 && bx < T.gx && by < L.ugy && bz < T.gz)
+            atomicMax(&dmax[q], st.tmax[((size_t)(bz * L.ugy + by) * T.gx + bx) * 9 + q]);
     }
     __syncthreads();
     bool h = false;
@@ -259,7 +280,8 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     double* ua = reinterpret_cast<double*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     uint64_t* bar = reinterpret_cast<uint64_t*>(ua + 3 * NAT);
     const int tid = threadIdx.x;
-    const int i0 = blockIdx.x * TX, j0 = L.jb0 + blockIdx.y * TY, k0 = blockIdx.z * TZ;
+    const Tile3 T = tile3(L);
+    const int i0 = T.x * TX, j0 = L.jb0 + T.y * TY, k0 = T.z * TZ;
     if (st.use_tma) {
         // one bulk tensor copy of the apron; out-of-domain boxes arrive zero-filled
         if (tid == 0) {
@@ -286,7 +308,7 @@ k_lat3_bond(DevPD d, LatticeDev L, const __grid_constant__ Stencil3D st, int ste
     }
     bool hot = DO_BREAK;
     if (DO_BREAK && st.tmax) {
-        hot = lat3_tile_hot(st, L);  // (its barriers also close the staging)
+        hot = lat3_tile_hot(st, L, T);  // (its barriers also close the staging)
         if (st.hot_count && tid == 0) {
             atomicAdd(st.hot_count, hot ? 1ull : 0ull);
             atomicAdd(st.hot_count + 1, 1ull);
@@ -381,7 +403,7 @@ void lat3_rows(LatticeDev& L) {
     L.ugy = (L.ny - L.ub0 + TY - 1) / TY;
 }
 void launch_lat3_ubar(const DevPD& d, const LatticeDev& L, unsigned* tmax, cudaStream_t s) {
-    dim3 grid((L.nx + TX - 1) / TX, L.ugy, (L.nz + TZ - 1) / TZ);
+    const unsigned grid = (unsigned)((L.nx + TX - 1) / TX) * L.ugy * ((L.nz + TZ - 1) / TZ);
     k_lat3_ubar<<<grid, NT, 0, s>>>(d, L, tmax);
 }
 void lat3_apron_box(int* bx, int* by, int* bz) {
@@ -395,7 +417,8 @@ size_t lat3_tile_count(const LatticeDev& L) {
 
 void launch_lat3_bond(const DevPD& d, const LatticeDev& L, const Stencil3D& st, int step,
                       int do_break, cudaStream_t s) {
-    dim3 grid((L.nx + TX - 1) / TX, (L.jb1 - L.jb0 + TY - 1) / TY, (L.nz + TZ - 1) / TZ);
+    const unsigned grid = (unsigned)((L.nx + TX - 1) / TX) * ((L.jb1 - L.jb0 + TY - 1) / TY) *
+                          ((L.nz + TZ - 1) / TZ);
     constexpr size_t smem = kApronBytes + 8 + 128;  // + mbarrier + realignment slack
     static bool configured = false;
     if (!configured) {
