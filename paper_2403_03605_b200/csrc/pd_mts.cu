@@ -4,6 +4,7 @@
 // reductions for the conjugate-gradient solves.  Built with -fmad=false so
 // every expression rounds as the reference's does.
 // Citations: /root/reference/proj/include/perimts/.
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -828,6 +829,344 @@ void csr_spmv_warp(int n, const int32_t* rp, const int32_t* ci, const double* v,
 void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream_t s) {
     k_dense_matvec<<<(n * 32 + kT - 1) / kT, kT, 0, s>>>(n, A, x, y);
     check("dense_matvec");
+}
+
+
+// ---- the coupled step's bookkeeping on the device (mts.hpp:152-241, 309-317,
+// 447-504): multiplier loads, interface rhs, energies, continuity, dense LU ----
+namespace {
+
+// LoadSpec ramp, driver.hpp:187-191: clamp(t / ramp, 0, 1) as std::clamp evaluates it
+__device__ __forceinline__ double d_load_scale(double tt, double ramp) {
+    if (ramp <= 0.0) return 1.0;
+    const double x = tt / ramp;
+    return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x);
+}
+
+// S_j = (1 - w) lambda_prev + [ls(t + j dt) - (1 - w) ls(t) - w ls(t + dt_fe)] G P,
+// w = j / m, for j = 1..m (mts.hpp:152-158), rows j - 1 of sv
+__global__ void k_s_vectors(int nl, int m, double t, double dt_pd, double dt_fe, double ramp,
+                            const double* lamp, const double* gpfe, double* sv) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)nl * m) return;
+    const int j = (int)(q / nl) + 1, r = (int)(q % nl);
+    const double w = double(j) / m;
+    const double bracket = d_load_scale(t + j * dt_pd, ramp) - (1.0 - w) * d_load_scale(t, ramp) -
+                           w * d_load_scale(t + dt_fe, ramp);
+    sv[q] = (1.0 - w) * lamp[r] + bracket * gpfe[r];
+}
+
+__global__ void k_sub_idx(int n, const int32_t* idx, const double* x, double* b) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) b[r] = b[r] - x[idx[r]];
+}
+__global__ void k_neg(int n, const double* x, double* y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = -x[i];
+}
+__global__ void k_sub2(int n, const double* a, const double* b, double* o) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = a[i] - b[i];
+}
+// the quadratic FE energy term's weights: M da + f K da
+__global__ void k_quad_w(int n, const double* da, const double* M, double f, const double* kda,
+                         double* w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) w[i] = M[i] * da[i] + f * kda[i];
+}
+// lambda_pd terms of the energy record (mts.hpp:480-500): per (j, r), j = 1..m,
+// A = vel_j - vel_{j-1}, B = lam_j - lam_{j-1}; S_0 = lambda_prev
+__global__ void k_lpd_terms(int nl, int m, const double* gpf, const double* gpl, const double* sv,
+                            const double* lamp, const double* lam, double* A, double* B) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)nl * m) return;
+    const int j = (int)(q / nl) + 1, r = (int)(q % nl);
+    const double vel_j = gpf[(size_t)j * nl + r] + gpl[(size_t)j * nl + r];
+    const double vel_jm = gpf[(size_t)(j - 1) * nl + r] + (j > 1 ? gpl[(size_t)(j - 1) * nl + r] : 0.0);
+    const double sj = sv[(size_t)(j - 1) * nl + r];
+    const double sjm = j > 1 ? sv[(size_t)(j - 2) * nl + r] : lamp[r];
+    const double lam_j = sj + (double(j) / m) * lam[r];
+    const double lam_jm = sjm + (double(j - 1) / m) * lam[r];
+    A[q] = vel_j - vel_jm;
+    B[q] = lam_j - lam_jm;
+}
+// max |x| (or max |x - y[idx]| with idx) into *out as the bits of a non-negative
+// double (they order like the values): order-independent, exact
+__global__ void k_max_abs(int n, const double* x, const int32_t* idx, const double* y,
+                          unsigned long long* out) {
+    unsigned long long m = 0ull;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = idx ? fabs(x[i] - y[idx[i]]) : fabs(x[i]);
+        m = max(m, (unsigned long long)__double_as_longlong(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// DenseLu (linalg.hpp:368-412) on the device: partial pivoting with the host
+// restatement's order of operations (-fmad=false: bitwise its factor).
+// One column step = k_lu_pivot (one block: argmax |a_ik|, i >= k, first index on
+// ties; singularity flag; row swap) + k_lu_col (multipliers) + k_lu_update.
+__global__ void k_lu_pivot(int n, int k, double* A, int* perm, const unsigned long long* amax,
+                           int* flag) {
+    __shared__ double bv[1024];
+    __shared__ int bi[1024];
+    double best = -1.0;
+    int piv = n;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+        const double v = fabs(A[(size_t)i * n + k]);
+        if (v > best) {
+            best = v;
+            piv = i;
+        }
+    }
+    bv[threadIdx.x] = best;
+    bi[threadIdx.x] = piv;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            const double v2 = bv[threadIdx.x + o];
+            const int i2 = bi[threadIdx.x + o];
+            if (v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < bi[threadIdx.x])) {
+                bv[threadIdx.x] = v2;
+                bi[threadIdx.x] = i2;
+            }
+        }
+        __syncthreads();
+    }
+    const double thr = 1e-14 * fmax(__longlong_as_double((long long)*amax), 1e-300);
+    const int p = bi[0];
+    if (bv[0] <= thr) {
+        if (threadIdx.x == 0) *flag = 1;
+        return;
+    }
+    if (p != k) {
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            const double a = A[(size_t)k * n + j];
+            A[(size_t)k * n + j] = A[(size_t)p * n + j];
+            A[(size_t)p * n + j] = a;
+        }
+        if (threadIdx.x == 0) {
+            const int t = perm[k];
+            perm[k] = perm[p];
+            perm[p] = t;
+        }
+    }
+}
+__global__ void k_lu_col(int n, int k, double* A, const int* flag) {
+    const int i = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || *flag) return;
+    const double inv = 1.0 / A[(size_t)k * n + k];
+    A[(size_t)i * n + k] = A[(size_t)i * n + k] * inv;
+}
+__global__ void k_lu_update(int n, int k, double* A, const int* flag) {
+    const int j = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = k + 1 + blockIdx.y;
+    if (j >= n || i >= n || *flag) return;
+    const double f = A[(size_t)i * n + k];
+    if (f == 0.0) return;
+    A[(size_t)i * n + j] -= f * A[(size_t)k * n + j];
+}
+// x = A^-1 b from the factor: the forward substitution accumulates each x_i over
+// ascending j like the host's row loop (bitwise); the backward one is column-
+// oriented (subtracting j descending: rounding-level differences from the host).
+// One block; x in global memory (n of any size)
+__global__ void k_lu_solve(int n, const double* A, const int* perm, const double* b, double* x) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[perm[i]];
+    __syncthreads();
+    for (int j = 0; j + 1 < n; ++j) {
+        const double xj = x[j];
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x)
+            x[i] = x[i] - A[(size_t)i * n + j] * xj;
+        __syncthreads();
+    }
+    for (int jj = n - 1; jj >= 0; --jj) {
+        if (threadIdx.x == 0) x[jj] = x[jj] / A[(size_t)jj * n + jj];
+        __syncthreads();
+        const double xj = x[jj];
+        for (int i = threadIdx.x; i < jj; i += blockDim.x) x[i] = x[i] - A[(size_t)i * n + jj] * xj;
+        __syncthreads();
+    }
+}
+
+// the loop test before the first CG iteration (cg_solve, linalg.hpp:251-262): b = 0
+// -> x = 0, converged; else continue while sqrt(rr) / sqrt(bb) > tol (past max_iter
+// -> status 2); sets the WHILE node's condition and resets the iteration count
+__global__ void k_cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
+                           double tol, int max_iter, int* it_status, double* x, int n) {
+    const double bb = *s_bb;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bb == 0.0 && i < n) x[i] = 0.0;
+    if (i != 0) return;
+    it_status[0] = 0;
+    it_status[1] = 0;
+    bool more = false;
+    if (bb != 0.0) {
+        more = sqrt(*s_rr) / sqrt(bb) > tol;
+        if (more && max_iter <= 0) {
+            it_status[1] = 2;
+            more = false;
+        }
+    }
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// dense column k of a column-major n x n matrix: D[k n + r] = -x[r]  (H_FE unit columns)
+__global__ void k_col_neg(int n, int k, const double* x, double* D) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) D[(size_t)k * n + r] = -x[r];
+}
+// row-major H[r n + k] += x[cpd[r]] (the PD unit responses of the dense interface)
+__global__ void k_add_col_gather(int n, int k, const int32_t* idx, const double* x, double* H) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) H[(size_t)r * n + k] += x[idx[r]];
+}
+// the unit load of coupling row k on the FE side: ra = 0 except ra[ci_j] = -w_j
+__global__ void k_unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int k,
+                           double* ra) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nf) ra[i] = 0.0;
+}
+__global__ void k_unit_row_set(const int32_t* rp, const int32_t* ci, const double* w, int k,
+                               double* ra) {
+    for (int j = rp[k] + threadIdx.x; j < rp[k + 1]; j += blockDim.x) ra[ci[j]] = -w[j];
+}
+__global__ void k_unit_vec(int n, int k, double* x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = i == k ? 1.0 : 0.0;
+}
+// column-major dense (n x n) -> row-major dense
+__global__ void k_transpose(int n, const double* D, double* H) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)n * n) return;
+    const int r = (int)(q / n), k = (int)(q % n);
+    H[q] = D[(size_t)k * n + r];
+}
+// nonzeros of row r of the column-major D (ascending k), count then fill
+__global__ void k_row_nnz(int n, const double* D, int* cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) {
+        cnt[n] = 0;
+        return;
+    }
+    int c = 0;
+    for (int k = 0; k < n; ++k) c += D[(size_t)k * n + r] != 0.0 ? 1 : 0;
+    cnt[r] = c;
+}
+__global__ void k_row_fill(int n, const double* D, const int* rp, int32_t* ci, double* v) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int q = rp[r];
+    for (int k = 0; k < n; ++k) {
+        const double x = D[(size_t)k * n + r];
+        if (x != 0.0) {
+            ci[q] = k;
+            v[q] = x;
+            ++q;
+        }
+    }
+}
+// Jacobi preconditioner of the interface CG: diag(H_FE) + m dt / (2 M_PD)
+__global__ void k_iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd,
+                            const double* Mpd, double* jd) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double v = D[(size_t)r * n + r] + double(m) * dt_pd / (2.0 * Mpd[cpd[r]]);
+    if (!(v > 0.0)) v = 0.0;
+    jd[r] = v;
+}
+
+}  // namespace
+
+void s_vectors(int nl, int m, double t, double dt_pd, double dt_fe, double ramp,
+               const double* lamp, const double* gpfe, double* sv, cudaStream_t s) {
+    k_s_vectors<<<blocks((long long)nl * m), kT, 0, s>>>(nl, m, t, dt_pd, dt_fe, ramp, lamp, gpfe, sv);
+    check("s_vectors");
+}
+void sub_idx(int n, const int32_t* idx, const double* x, double* b, cudaStream_t s) {
+    k_sub_idx<<<blocks(n), kT, 0, s>>>(n, idx, x, b);
+    check("sub_idx");
+}
+void neg(int n, const double* x, double* y, cudaStream_t s) {
+    k_neg<<<blocks(n), kT, 0, s>>>(n, x, y);
+    check("neg");
+}
+void sub2(int n, const double* a, const double* b, double* o, cudaStream_t s) {
+    k_sub2<<<blocks(n), kT, 0, s>>>(n, a, b, o);
+    check("sub2");
+}
+void quad_w(int n, const double* da, const double* M, double f, const double* kda, double* w,
+            cudaStream_t s) {
+    k_quad_w<<<blocks(n), kT, 0, s>>>(n, da, M, f, kda, w);
+    check("quad_w");
+}
+void lpd_terms(int nl, int m, const double* gpf, const double* gpl, const double* sv,
+               const double* lamp, const double* lam, double* A, double* B, cudaStream_t s) {
+    k_lpd_terms<<<blocks((long long)nl * m), kT, 0, s>>>(nl, m, gpf, gpl, sv, lamp, lam, A, B);
+    check("lpd_terms");
+}
+void max_abs(int n, const double* x, const int32_t* idx, const double* y,
+             unsigned long long* out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_max_abs<<<std::min(blocks(n), 592), kT, 0, s>>>(n, x, idx, y, out);
+    check("max_abs");
+}
+void lu_factor(int n, double* A, int* perm, unsigned long long* amax, int* flag, cudaStream_t s) {
+    k_max_abs<<<std::min(blocks((long long)n * n), 2048), kT, 0, s>>>(n * n, A, nullptr, nullptr, amax);
+    for (int k = 0; k < n; ++k) {
+        k_lu_pivot<<<1, 1024, 0, s>>>(n, k, A, perm, amax, flag);
+        const int rest = n - k - 1;
+        if (rest > 0) {
+            k_lu_col<<<blocks(rest), kT, 0, s>>>(n, k, A, flag);
+            k_lu_update<<<dim3(blocks(rest), rest), kT, 0, s>>>(n, k, A, flag);
+        }
+    }
+    check("lu_factor");
+}
+void lu_solve(int n, const double* A, const int* perm, const double* b, double* x, cudaStream_t s) {
+    k_lu_solve<<<1, 1024, 0, s>>>(n, A, perm, b, x);
+    check("lu_solve");
+}
+void cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr, double tol,
+              int max_iter, int* it_status, double* x, int n, cudaStream_t s) {
+    k_cg_start<<<blocks(std::max(n, 1)), kT, 0, s>>>(h, s_bb, s_rr, tol, max_iter, it_status, x, n);
+    check("cg_start");
+}
+void col_neg(int n, int k, const double* x, double* D, cudaStream_t s) {
+    k_col_neg<<<blocks(n), kT, 0, s>>>(n, k, x, D);
+    check("col_neg");
+}
+void add_col_gather(int n, int k, const int32_t* idx, const double* x, double* H, cudaStream_t s) {
+    k_add_col_gather<<<blocks(n), kT, 0, s>>>(n, k, idx, x, H);
+    check("add_col_gather");
+}
+void unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int k, double* ra,
+              cudaStream_t s) {
+    k_unit_row<<<blocks(nf), kT, 0, s>>>(nf, rp, ci, w, k, ra);
+    k_unit_row_set<<<1, 32, 0, s>>>(rp, ci, w, k, ra);
+    check("unit_row");
+}
+void unit_vec(int n, int k, double* x, cudaStream_t s) {
+    k_unit_vec<<<blocks(n), kT, 0, s>>>(n, k, x);
+    check("unit_vec");
+}
+void transpose(int n, const double* D, double* H, cudaStream_t s) {
+    k_transpose<<<blocks((long long)n * n), kT, 0, s>>>(n, D, H);
+    check("transpose");
+}
+void row_nnz(int n, const double* D, int* cnt, cudaStream_t s) {
+    k_row_nnz<<<blocks(n + 1), kT, 0, s>>>(n, D, cnt);
+    check("row_nnz");
+}
+void row_fill(int n, const double* D, const int* rp, int32_t* ci, double* v, cudaStream_t s) {
+    k_row_fill<<<blocks(n), kT, 0, s>>>(n, D, rp, ci, v);
+    check("row_fill");
+}
+void iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd, const double* Mpd,
+               double* jd, cudaStream_t s) {
+    k_iface_jac<<<blocks(n), kT, 0, s>>>(n, D, m, dt_pd, cpd, Mpd, jd);
+    check("iface_jac");
 }
 
 }  // namespace mtsk

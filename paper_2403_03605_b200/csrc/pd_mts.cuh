@@ -84,5 +84,33 @@ void dense_matvec(int n, const double* A, const double* x, double* y, cudaStream
 void csr_spmv_warp(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
                    double* y, cudaStream_t s);
 
+// coupled-step bookkeeping on the device (pd_mts.cu): S_j rows, interface rhs,
+// energy terms, continuity maxima (as double bits), dense LU, H_FE assembly
+void s_vectors(int nl, int m, double t, double dt_pd, double dt_fe, double ramp,
+               const double* lamp, const double* gpfe, double* sv, cudaStream_t s);
+void sub_idx(int n, const int32_t* idx, const double* x, double* b, cudaStream_t s);
+void neg(int n, const double* x, double* y, cudaStream_t s);
+void sub2(int n, const double* a, const double* b, double* o, cudaStream_t s);
+void quad_w(int n, const double* da, const double* M, double f, const double* kda, double* w,
+            cudaStream_t s);
+void lpd_terms(int nl, int m, const double* gpf, const double* gpl, const double* sv,
+               const double* lamp, const double* lam, double* A, double* B, cudaStream_t s);
+void max_abs(int n, const double* x, const int32_t* idx, const double* y,
+             unsigned long long* out, cudaStream_t s);
+void lu_factor(int n, double* A, int* perm, unsigned long long* amax, int* flag, cudaStream_t s);
+void lu_solve(int n, const double* A, const int* perm, const double* b, double* x, cudaStream_t s);
+void cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr, double tol,
+              int max_iter, int* it_status, double* x, int n, cudaStream_t s);
+void col_neg(int n, int k, const double* x, double* D, cudaStream_t s);
+void add_col_gather(int n, int k, const int32_t* idx, const double* x, double* H, cudaStream_t s);
+void unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int k, double* ra,
+              cudaStream_t s);
+void unit_vec(int n, int k, double* x, cudaStream_t s);
+void transpose(int n, const double* D, double* H, cudaStream_t s);
+void row_nnz(int n, const double* D, int* cnt, cudaStream_t s);
+void row_fill(int n, const double* D, const int* rp, int32_t* ci, double* v, cudaStream_t s);
+void iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd, const double* Mpd,
+               double* jd, cudaStream_t s);
+
 }  // namespace mtsk
 }  // namespace pmts

@@ -61,59 +61,6 @@ double now_s() {
         .count();
 }
 
-// DenseLu (linalg.hpp:368-412), host: the interface factor
-struct HostLu {
-    std::vector<double> lu;
-    std::vector<int> perm;
-    int n = 0;
-    void factor(std::vector<double> a, int nn) {
-        n = nn;
-        lu = std::move(a);
-        double amax = 0.0;
-        for (double v : lu) amax = std::max(amax, std::abs(v));
-        perm.resize(n);
-        for (int i = 0; i < n; ++i) perm[i] = i;
-        for (int k = 0; k < n; ++k) {
-            int piv = k;
-            double best = std::abs(lu[(size_t)k * n + k]);
-            for (int i = k + 1; i < n; ++i) {
-                const double v = std::abs(lu[(size_t)i * n + k]);
-                if (v > best) {
-                    best = v;
-                    piv = i;
-                }
-            }
-            if (best <= 1e-14 * std::max(amax, 1e-300))
-                throw SolverError("singular interface system: coincident or disconnected overlap");
-            if (piv != k) {
-                std::swap(perm[k], perm[piv]);
-                for (int j = 0; j < n; ++j) std::swap(lu[(size_t)k * n + j], lu[(size_t)piv * n + j]);
-            }
-            const double inv = 1.0 / lu[(size_t)k * n + k];
-            for (int i = k + 1; i < n; ++i) {
-                const double f = lu[(size_t)i * n + k] * inv;
-                lu[(size_t)i * n + k] = f;
-                if (f == 0.0) continue;
-                for (int j = k + 1; j < n; ++j) lu[(size_t)i * n + j] -= f * lu[(size_t)k * n + j];
-            }
-        }
-    }
-    std::vector<double> solve(const std::vector<double>& b) const {
-        std::vector<double> x(n);
-        for (int i = 0; i < n; ++i) x[i] = b[perm[i]];
-        for (int i = 1; i < n; ++i) {
-            double s = x[i];
-            for (int j = 0; j < i; ++j) s -= lu[(size_t)i * n + j] * x[j];
-            x[i] = s;
-        }
-        for (int ii = n; ii-- > 0;) {
-            double s = x[ii];
-            for (int j = ii + 1; j < n; ++j) s -= lu[(size_t)ii * n + j] * x[j];
-            x[ii] = s / lu[(size_t)ii * n + ii];
-        }
-        return x;
-    }
-};
 
 struct DState {
     double *u = nullptr, *v = nullptr, *a = nullptr;
@@ -192,13 +139,22 @@ struct pmts_mts {
     int32_t* row_of = nullptr;                                             // PD dof -> coupling row
     double *warm_fe_free = nullptr, *warm_fe_link = nullptr;
     bool warm_free_ok = false, warm_link_ok = false;
-    // host interface state
-    std::vector<double> lambda_prev, lambda, g_p_fe, h_fe, h;
-    HostLu lu;
+    // interface state, device resident: multipliers (previous / current), G_FE P_ext,
+    // the FE coupling velocities at the start of the macro step, the dense interface
+    // (row-major H and its LU factor with the row permutation)
+    double *lamp_d = nullptr, *gpfe_d = nullptr, *gprev_d = nullptr;
+    double *h_d = nullptr, *hfe_dense = nullptr;  // dense mode: H and H_FE (row-major nl x nl)
+    int* perm_d = nullptr;
     bool h_valid = false, unit_stale = false, use_dense = true;
     double t = 0.0;
-    std::vector<std::vector<double>> gp_free, gp_link;
-    std::vector<double> fe_prev_gvel;
+    // per macro step results read back in one copy: CG {iterations, status} per solve
+    // slot, energy sums, continuity maxima (double bits), the LU singularity flag
+    enum { CG_FE_FREE = 0, CG_FE_LINK = 1, CG_IFACE = 2, CG_UNIT = 3, N_CG = 4 };
+    int* cg_status = nullptr;                 // 2 ints per slot
+    double* en_d = nullptr;                   // quad_fe, lambda_fe, lambda_pd
+    unsigned long long* cmax_d = nullptr;     // |gf - gp|, |v_FE|, |v_PD|, LU amax
+    int* lu_flag = nullptr;
+    double *ta_d = nullptr, *tb_d = nullptr;  // energy term scratch, m nl each
     int64_t broken_total = 0;
 
     ~pmts_mts() {
@@ -275,38 +231,27 @@ struct pmts_mts {
         launch_node_force(pdv, y, stream);
     }
 
-    // reference cg_solve (linalg.hpp:243-296) on the device; A applied by op(x, y)
+    // reference cg_solve (linalg.hpp:243-296) on the device, the whole solve one graph
+    // launch: the setup (b.b, r = b - A x, z, p, r.z, r.r), the loop test before the
+    // first iteration (k_cg_start: b = 0 -> x = 0) and a conditional WHILE node whose
+    // body is the iteration plus the loop test (k_cg_cond) -- no host round trip.  The
+    // solve's {iterations, status} land in cg_status[slot]; cg_result reads them.  The
+    // graph bakes in every pointer the iteration and the operator touch: it is rebuilt
+    // when one of its inputs changes or the operator's buffers are reallocated
+    // (invalidate_cg_graphs).
     template <class Op>
-    int cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac,
-           int graph_id) {
+    void cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac,
+            int slot) {
         double* r = cg_r;
         double* z = cg_z;
         double* p = cg_p;
         double* ap = cg_ap;
-        double* s_bb = scal + 0;
-        double* s_rz = scal + 1;
-        double* s_rr = scal + 2;
-        double* s_pap = scal + 3;
-        double* s_alpha = scal + 4;
-        double* s_rzn = scal + 5;
-        double* s_beta = scal + 6;
-        mtsk::dot(n, b, b, part, s_bb, stream);
-        const double bnorm = std::sqrt(scalar(s_bb));
-        if (bnorm == 0.0) {
-            CKM(cudaMemsetAsync(x, 0, sizeof(double) * n, stream));
-            return 0;
-        }
-        op(x, ap);
-        sub(n, b, ap, r);  // r = b - A x
-        mtsk::precond(n, r, jac, z, stream);
-        CKM(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
-        mtsk::dot(n, r, z, part, s_rz, stream);
-        mtsk::dot(n, r, r, part, s_rr, stream);
-        double rnorm = std::sqrt(scalar(s_rr));
-        // the iteration body (same arithmetic as the reference's loop) as one CUDA
-        // graph over fixed buffers: one launch and one 16-byte readback per iteration
-        // (fused: p.Ap and alpha in one launch, the update with the preconditioner,
-        // r.z, r.r, beta and rz <- rz_new in one launch -- bitwise the unfused order)
+        double* sc = scal + 8 * slot;
+        double *s_bb = sc + 0, *s_rz = sc + 1, *s_rr = sc + 2, *s_pap = sc + 3, *s_alpha = sc + 4,
+               *s_rzn = sc + 5, *s_beta = sc + 6;
+        int* st = cg_status + 2 * slot;
+        // fused iteration: p.Ap and alpha in one launch, the update with the
+        // preconditioner, r.z, r.r, beta and rz <- rz_new in one launch
         auto body = [&] {
             op(p, ap);
             mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
@@ -315,62 +260,71 @@ struct pmts_mts {
             mtsk::dot_fin(n, r, z, r, r, part2, ticket, s_rzn, s_rr, 2, s_rz, s_beta, stream);
             mtsk::xpby(n, z, s_beta, p, stream);
         };
-        {
-            // the whole loop as one graph: a conditional WHILE node whose body is the
-            // iteration plus the loop test (k_cg_cond) -- no host round trip per iteration
-            // the graph bakes in every pointer the iteration and the operator touch:
-            // rebuilt when any of its inputs changes or the operator's buffers are
-            // reallocated (invalidate_cg_graphs)
-            cudaGraphExec_t& gl = cg_loop[graph_id];
-            const CgKey key{x, b, jac, n, tol, max_iter, op_epoch};
-            if (gl && !(cg_key[graph_id] == key)) {
-                cudaGraphExecDestroy(gl);
-                gl = nullptr;
-            }
-            if (!gl) {
-                cudaGraph_t g;
-                CKM(cudaGraphCreate(&g, 0));
-                cudaGraphConditionalHandle hnd;
-                CKM(cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault));
-                cudaGraphNodeParams cp = {};
-                cp.type = cudaGraphNodeTypeConditional;
-                cp.conditional.handle = hnd;
-                cp.conditional.type = cudaGraphCondTypeWhile;
-                cp.conditional.size = 1;
-                cudaGraphNode_t node;
-                CKM(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
-                cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
-                CKM(cudaStreamBeginCaptureToGraph(stream, bodyg, nullptr, nullptr, 0,
-                                                  cudaStreamCaptureModeThreadLocal));
-                body();
-                mtsk::cg_cond(hnd, s_bb, s_rr, s_pap, tol, max_iter, it_status, stream);
-                CKM(cudaStreamEndCapture(stream, &bodyg));
-                CKM(cudaGraphInstantiate(&gl, g, 0));
-                cudaGraphDestroy(g);
-                cg_key[graph_id] = key;
-            }
-            if (!(rnorm / bnorm > tol)) return 0;
-            if (max_iter <= 0)
-                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
-                                  " iterations, residual " + std::to_string(rnorm / bnorm));
-            CKM(cudaMemsetAsync(it_status, 0, 2 * sizeof(int), stream));
-            CKM(cudaGraphLaunch(gl, stream));
-            CKM(cudaMemcpyAsync(h_pin, scal + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
-            CKM(cudaMemcpyAsync(h_pin + 2, it_status, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
-            CKM(cudaStreamSynchronize(stream));
-            int hs[2];
-            std::memcpy(hs, h_pin + 2, sizeof(hs));
-            if (hs[1] == 1)
-                throw SolverError("cg: operator not positive definite (p'Ap = " +
-                                  std::to_string(h_pin[1]) + ")");
-            if (hs[1] == 2)
-                throw SolverError("cg: no convergence after " + std::to_string(max_iter) +
-                                  " iterations, residual " +
-                                  std::to_string(std::sqrt(h_pin[0]) / bnorm));
-            return hs[0];
+        cudaGraphExec_t& gl = cg_loop[slot];
+        const CgKey key{x, b, jac, n, tol, max_iter, op_epoch};
+        if (gl && !(cg_key[slot] == key)) {
+            cudaGraphExecDestroy(gl);
+            gl = nullptr;
         }
+        if (!gl) {
+            cudaGraph_t g;
+            CKM(cudaGraphCreate(&g, 0));
+            cudaGraphConditionalHandle hnd;
+            CKM(cudaGraphConditionalHandleCreate(&hnd, g, 0, 0));
+            CKM(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+            mtsk::dot(n, b, b, part, s_bb, stream);
+            op(x, ap);
+            sub(n, b, ap, r);  // r = b - A x
+            mtsk::precond(n, r, jac, z, stream);
+            CKM(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+            mtsk::dot(n, r, z, part, s_rz, stream);
+            mtsk::dot(n, r, r, part, s_rr, stream);
+            mtsk::cg_start(hnd, s_bb, s_rr, tol, max_iter, st, x, n, stream);
+            // the WHILE node behind the captured setup
+            cudaStreamCaptureStatus cst;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            CKM(cudaStreamGetCaptureInfo(stream, &cst, nullptr, nullptr, &deps, &nd));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = hnd;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            CKM(cudaGraphAddNode(&node, g, deps, nd, &cp));
+            CKM(cudaStreamUpdateCaptureDependencies(stream, &node, 1,
+                                                    cudaStreamSetCaptureDependencies));
+            CKM(cudaStreamEndCapture(stream, &g));
+            cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+            CKM(cudaStreamBeginCaptureToGraph(stream, bodyg, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+            body();
+            mtsk::cg_cond(hnd, s_bb, s_rr, s_pap, tol, max_iter, st, stream);
+            CKM(cudaStreamEndCapture(stream, &bodyg));
+            CKM(cudaGraphInstantiate(&gl, g, 0));
+            cudaGraphDestroy(g);
+            cg_key[slot] = key;
+        }
+        cg_max[slot] = max_iter;
+        CKM(cudaGraphLaunch(gl, stream));
     }
-    cudaGraphExec_t cg_loop[2] = {nullptr, nullptr};  // device-side loops (conditional node)
+    // {iterations, status} of a finished solve (host copy h_stat after a readback)
+    int cg_check(const int* hs, int slot) const {
+        if (hs[2 * slot + 1] == 1) throw SolverError("cg: operator not positive definite");
+        if (hs[2 * slot + 1] == 2)
+            throw SolverError("cg: no convergence after " + std::to_string(cg_max[slot]) +
+                              " iterations");
+        return hs[2 * slot];
+    }
+    int cg_result(int slot) {  // reads back now
+        int hs[2 * N_CG];
+        CKM(cudaMemcpyAsync(hs, cg_status, sizeof(hs), cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        return cg_check(hs, slot);
+    }
+    cudaGraphExec_t cg_loop[N_CG] = {nullptr, nullptr, nullptr, nullptr};
+    int cg_max[N_CG] = {0, 0, 0, 0};
     struct CgKey {
         const double *x = nullptr, *b = nullptr, *jac = nullptr;
         int n = 0;
@@ -382,11 +336,10 @@ struct pmts_mts {
                    max_iter == o.max_iter && epoch == o.epoch;
         }
     };
-    CgKey cg_key[2];
+    CgKey cg_key[N_CG];
     unsigned op_epoch = 0;  // bumped whenever a buffer an operator captures is reallocated
     void invalidate_cg_graphs() { ++op_epoch; }
-    int* it_status = nullptr;  // {iterations, status} of the device-side loop
-    double* h_pin = nullptr;  // pinned: (rr, pap) of the last iteration
+    void* h_pin = nullptr;  // pinned: the macro step's readback
     void sub(int n, const double* b, const double* ap, double* r) {
         // r = b - ap, elementwise, exactly as the reference's r[i] = b[i] - ap[i]
         mtsk::rhs(n, b, 1.0, ap, zero_flags(n), r, stream);
@@ -403,9 +356,10 @@ struct pmts_mts {
     }
 
     // BlockOperator::solve (newmark.hpp:122-159) for the FE subdomain.  rhs.a =
-    // ra * ra_scale (ra nullable); rv, rd the predictor rows.
+    // ra * ra_scale (ra nullable); rv, rd the predictor rows.  Implicit: the CG's
+    // status goes to cg_status[slot].
     void fe_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
-                  double* warm, bool* warm_ok, bool homog, const DState& out) {
+                  double* warm, bool* warm_ok, bool homog, const DState& out, int slot) {
         fe_K(rdp, kd);
         if (fe_nm.explicit_scheme()) {
             mtsk::explicit_solve(nf, ra, ra_scale, kd, fe_M, fe_cf, rvp, rdp, fe_nm.gdt, fe_nm.bdt2,
@@ -425,7 +379,7 @@ struct pmts_mts {
                fe_K(x, cg_kx);
                mtsk::apply_a(nf, x, cg_kx, fe_M, fe_cf, bdt2, y, stream);
            },
-           cg_b, cg_x, cg_tol, fe_cg_max, fe_jac, 0);
+           cg_b, cg_x, cg_tol, fe_cg_max, fe_jac, slot);
         mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
         if (warm) {
             CKM(cudaMemcpyAsync(warm, cg_x, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
@@ -445,47 +399,28 @@ struct pmts_mts {
                                pd_bcv, homog ? 1 : 0, out.u, out.v, out.a, stream);
     }
 
-    // ---- coupling (coupling.hpp:46-68) ----
-    std::vector<double> gather_fe(const double* x) {
-        mtsk::gather_csr(nl, gfe_rp, gfe_ci, gfe_w, x, gvec, stream);
-        return to_host(gvec, nl);
+    // ---- coupling (coupling.hpp:46-68), all on the device ----
+    void gather_fe(const double* x, double* out) {
+        mtsk::gather_csr(nl, gfe_rp, gfe_ci, gfe_w, x, out, stream);
     }
-    // dst += G_FE^T vals (host vals, uploaded)
-    void add_gt_fe(const std::vector<double>& vals, double* dst) {
-        to_dev(lam_tmp, vals);
+    // dst += G_FE^T (-vals): the reference's scatter of scaled(lambda, -1)
+    void add_gt_fe_neg(const double* vals, double* dst) {
+        mtsk::neg(nl, vals, lam_tmp, stream);
         mtsk::scatter_csr(gft_n, gft_d, gft_rp, gft_ri, gft_w, lam_tmp, dst, stream);
-    }
-    std::vector<double> gather_pd(const double* x) {
-        mtsk::gather(nl, cpd, x, gvec, stream);
-        return to_host(gvec, nl);
-    }
-    // dst[cpl[r]] += vals[r] (host vals, uploaded)
-    void add_gt(const int32_t* cpl, const std::vector<double>& vals, double* dst) {
-        to_dev(lam_tmp, vals);
-        mtsk::scatter_add(nl, cpl, lam_tmp, dst, stream);
     }
     void zero_vec(double* x, int n) { CKM(cudaMemsetAsync(x, 0, sizeof(double) * n, stream)); }
 
     // ---- unit responses (mts.hpp:389-445) ----
     void unit_fe_column(int k, const DState& y) {
         // M_block Y = -G^T e_k, homogeneous, no warm start
-        zero_vec(ra, nf);
+        mtsk::unit_row(nf, gfe_rp, gfe_ci, gfe_w, k, ra, stream);
         zero_vec(rv, nf);
         zero_vec(rd, nf);
-        for (int j = s.cpl_fe_rp[k]; j < s.cpl_fe_rp[k + 1]; ++j) {
-            const double mw = -s.cpl_fe_w[j];
-            CKM(cudaMemcpyAsync(ra + s.cpl_fe_ci[j], &mw, sizeof(double), cudaMemcpyHostToDevice,
-                                stream));
-            CKM(cudaStreamSynchronize(stream));
-        }
-        fe_solve(ra, 1.0, rv, rd, nullptr, nullptr, true, y);
+        fe_solve(ra, 1.0, rv, rd, nullptr, nullptr, true, y, CG_UNIT);
     }
     void unit_pd_column(int k, const DState& y) {
         // w = e_k: the ramped unit load at pd_dof[k] (mts.hpp:398-407)
-        zero_vec(lam_tmp, nl);
-        const double one = 1.0;
-        CKM(cudaMemcpyAsync(lam_tmp + k, &one, sizeof(double), cudaMemcpyHostToDevice, stream));
-        CKM(cudaStreamSynchronize(stream));
+        mtsk::unit_vec(nl, k, lam_tmp, stream);
         lin_substeps(lam_tmp, nullptr, nullptr, y);
     }
     // the m homogeneous linear substeps on k_sync (mts.hpp:230-238, 398-418):
@@ -503,58 +438,79 @@ struct pmts_mts {
                               rd, rv, out, stream);
         }
     }
+    // H_FE = -G_FE vel(Y_FE) column by column on the device (mts.hpp:389-397): the
+    // columns go into a column-major nl x nl scratch, from which the dense form (dense
+    // interface) or the exact nonzeros in CSR (matrix-free interface: each unit column
+    // is a CG solve whose support grows one stiffness neighbourhood per iteration, and
+    // disconnected FE parts never couple -- lossless) are extracted on the device
     void build_h_fe() {
-        h_fe.assign((size_t)nl * nl, 0.0);
+        double* D = nullptr;
+        CKM(cudaMallocAsync(&D, sizeof(double) * (size_t)nl * nl, stream));
         for (int k = 0; k < nl; ++k) {
             unit_fe_column(k, yst);
-            const std::vector<double> g = gather_fe(yst.v);
-            for (int r = 0; r < nl; ++r) h_fe[(size_t)r * nl + k] = -g[r];
+            gather_fe(yst.v, gvec);
+            mtsk::col_neg(nl, k, gvec, D, stream);
+            if (!fe_nm.explicit_scheme() && (k % 256 == 255 || k == nl - 1))
+                cg_result(CG_UNIT);  // the unit columns' CG status, now and then
+        }
+        if (use_dense || iface_mode == 1) {
+            if (!hfe_dense) hfe_dense = alloc<double>((size_t)nl * nl);
+            mtsk::transpose(nl, D, hfe_dense, stream);
         }
         if (!use_dense || iface_mode == 2) {
-            // H_FE is exactly sparse: each unit column is a CG solve from one overlap
-            // dof, whose support grows by one stiffness neighbourhood per iteration, and
-            // disconnected FE parts never couple -- keep the nonzeros (lossless) in CSR
-            std::vector<int32_t> rp(nl + 1, 0), ci;
-            std::vector<double> vv;
-            for (int r = 0; r < nl; ++r) {
-                for (int k = 0; k < nl; ++k) {
-                    const double x = h_fe[(size_t)r * nl + k];
-                    if (x != 0.0) {
-                        ci.push_back(k);
-                        vv.push_back(x);
-                    }
-                }
-                rp[r + 1] = int32_t(ci.size());
-            }
-            hfe_nnz = int64_t(vv.size());
             // Jacobi preconditioner of the matrix-free interface CG (an addition: the
             // reference's CG is unpreconditioned, mts.hpp:194-213): diag(H_FE) plus the
             // free-mass velocity of a PD dof after the m ramped substeps, m dt / (2 M) --
             // the (1 - alpha)-weighted PD masses span orders of magnitude across the
             // gluing zone, which is what slows the plain CG
             if (interface_precond) {
-                std::vector<double> jd(nl, 0.0);
-                for (int r = 0; r < nl; ++r) {
-                    jd[r] = h_fe[(size_t)r * nl + r] +
-                            double(m) * s.dt_pd / (2.0 * s.pd_mass[s.cpl_pd[r]]);
-                    if (!(jd[r] > 0.0)) jd[r] = 0.0;  // precond() leaves such rows unscaled
-                }
-                iface_jac = upload(jd);
+                iface_jac = alloc<double>(nl);
+                mtsk::iface_jac(nl, D, m, s.dt_pd, cpd, pd_M, iface_jac, stream);
             }
+            int* cnt = nullptr;
+            CKM(cudaMallocAsync(&cnt, sizeof(int) * ((size_t)nl + 1), stream));
+            mtsk::row_nnz(nl, D, cnt, stream);
+            std::vector<int> hc(nl + 1);
+            CKM(cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * ((size_t)nl + 1), cudaMemcpyDeviceToHost,
+                                stream));
+            CKM(cudaStreamSynchronize(stream));
+            std::vector<int32_t> rp(nl + 1, 0);
+            for (int r = 0; r < nl; ++r) rp[r + 1] = rp[r] + hc[r];
+            hfe_nnz = rp[nl];
             hfe_rp = upload(rp);
-            hfe_ci = upload(ci);
-            hfe_v = upload(vv);
+            hfe_ci = alloc<int32_t>(std::max<int64_t>(hfe_nnz, 1));
+            hfe_v = alloc<double>(std::max<int64_t>(hfe_nnz, 1));
+            mtsk::row_fill(nl, D, hfe_rp, hfe_ci, hfe_v, stream);
+            CKM(cudaFreeAsync(cnt, stream));
             invalidate_cg_graphs();  // the interface operator captures these
         }
+        CKM(cudaFreeAsync(D, stream));
+        CKM(cudaStreamSynchronize(stream));
     }
+    // H = H_FE + G_PD vel(Y_PD) (mts.hpp:422-445) and its LU factor, on the device
     void refresh_dense_interface() {
-        h = h_fe;
+        if (!h_d) {
+            h_d = alloc<double>((size_t)nl * nl);
+            perm_d = alloc<int>(nl);
+        }
+        CKM(cudaMemcpyAsync(h_d, hfe_dense, sizeof(double) * (size_t)nl * nl,
+                            cudaMemcpyDeviceToDevice, stream));
         for (int k = 0; k < nl; ++k) {
             unit_pd_column(k, yst);
-            const std::vector<double> g = gather_pd(yst.v);
-            for (int r = 0; r < nl; ++r) h[(size_t)r * nl + k] += g[r];
+            mtsk::add_col_gather(nl, k, cpd, yst.v, h_d, stream);
         }
-        lu.factor(h, nl);
+        {
+            std::vector<int> id(nl);
+            for (int i = 0; i < nl; ++i) id[i] = i;
+            CKM(cudaMemcpyAsync(perm_d, id.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, stream));
+        }
+        CKM(cudaMemsetAsync(cmax_d + 3, 0, sizeof(unsigned long long), stream));
+        CKM(cudaMemsetAsync(lu_flag, 0, sizeof(int), stream));
+        mtsk::lu_factor(nl, h_d, perm_d, cmax_d + 3, lu_flag, stream);
+        int flag = 0;
+        CKM(cudaMemcpyAsync(&flag, lu_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        if (flag) throw SolverError("singular interface system: coincident or disconnected overlap");
         h_valid = true;
     }
     // G_PD vel(Y_PD_m) w without materialising Y (mts.hpp:410-420), device in/out
@@ -562,64 +518,61 @@ struct pmts_mts {
         lin_substeps(w_dev, out_dev, nullptr, yst);
     }
 
-    // ---- the macro step (mts.hpp:133-306) ----
-    std::vector<double> s_vector(int j) const {
-        const double w = double(j) / m;
-        std::vector<double> sv(nl);
-        const double bracket = load_scale(t + j * s.dt_pd) - (1.0 - w) * load_scale(t) -
-                               w * load_scale(t + dt_fe());
-        for (int r = 0; r < nl; ++r) sv[r] = (1.0 - w) * lambda_prev[r] + bracket * g_p_fe[r];
-        return sv;
-    }
-    static std::vector<double> scaled(const std::vector<double>& v, double f) {
-        std::vector<double> o = v;
-        for (double& x : o) x *= f;
-        return o;
-    }
-
     void initialize_accelerations() {
         // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
         mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
-        add_gt_fe(scaled(lambda_prev, -1.0), ra);
+        add_gt_fe_neg(lamp_d, ra);
         fe_K(ufe.u, kd);
         mtsk::init_acc(nf, ra, kd, fe_M, fe_cf, ufe.a, stream);
         mtsk::scale(np, pd_P, load_scale(t), ra, stream);
-        add_gt(cpd, lambda_prev, ra);
+        mtsk::scatter_add(nl, cpd, lamp_d, ra, stream);
         pd_K(upd.u, kd, mask_live, false, 0);
         mtsk::init_acc(np, ra, kd, pd_M, pd_cf, upd.a, stream);
         CKM(cudaStreamSynchronize(stream));
     }
 
-    std::vector<double> interface_solve(int* iterations) {
-        std::vector<double> rhs = gather_fe(vfe.v);
-        const std::vector<double> gp = gather_pd(vpd.v);
-        for (int r = 0; r < nl; ++r) rhs[r] -= gp[r];
+    // the interface solve (mts.hpp:184-215) into lam_d: rhs = G_FE v_FE - G_PD v_PD on
+    // the device; the dense LU solve, or the matrix-free CG warm-started from
+    // lambda_prev (its status read here: a failed CG falls back to the dense form)
+    void interface_solve(int* iterations) {
+        double* b = alloc_iface_b();
+        gather_fe(vfe.v, b);
+        mtsk::sub_idx(nl, cpd, vpd.v, b, stream);
         if (use_dense) {
             if (!h_valid) throw InternalError("interface solve with stale unit response");
             *iterations = 0;
-            return lu.solve(rhs);
+            mtsk::lu_solve(nl, h_d, perm_d, b, lam_d, stream);
+            return;
         }
-        // matrix-free CG (no preconditioner), warm start lambda_prev
-        to_dev(lam_d, lambda_prev);
-        double* b = alloc_iface_b();
-        to_dev(b, rhs);
+        CKM(cudaMemcpyAsync(lam_d, lamp_d, sizeof(double) * nl, cudaMemcpyDeviceToDevice, stream));
+        const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
+        cg(nl,
+           [&](const double* in, double* out) {
+               mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
+               apply_h_pd(in, iface_tmp);
+               mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
+           },
+           b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
         try {
-            const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
-            *iterations = cg(nl,
-                             [&](const double* in, double* out) {
-                                 mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
-                                 apply_h_pd(in, iface_tmp);
-                                 mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
-                             },
-                             b, lam_d, interface_cg_tol, max_iter, iface_jac, 1);
+            *iterations = cg_result(CG_IFACE);
         } catch (const SolverError&) {
             use_dense = true;
             h_valid = false;
+            if (!hfe_dense) {  // dense H_FE from the CSR (fallback only)
+                std::vector<int32_t> rp(nl + 1);
+                CKM(cudaMemcpy(rp.data(), hfe_rp, sizeof(int32_t) * (nl + 1), cudaMemcpyDeviceToHost));
+                std::vector<int32_t> ci(hfe_nnz);
+                std::vector<double> v(hfe_nnz), dense((size_t)nl * nl, 0.0);
+                CKM(cudaMemcpy(ci.data(), hfe_ci, sizeof(int32_t) * hfe_nnz, cudaMemcpyDeviceToHost));
+                CKM(cudaMemcpy(v.data(), hfe_v, sizeof(double) * hfe_nnz, cudaMemcpyDeviceToHost));
+                for (int r = 0; r < nl; ++r)
+                    for (int q = rp[r]; q < rp[r + 1]; ++q) dense[(size_t)r * nl + ci[q]] = v[q];
+                hfe_dense = upload(dense);
+            }
             refresh_dense_interface();
             *iterations = 0;
-            return lu.solve(rhs);
+            mtsk::lu_solve(nl, h_d, perm_d, b, lam_d, stream);
         }
-        return to_host(lam_d, nl);
     }
     double* iface_b = nullptr;
     double* iface_tmp = nullptr;
@@ -656,7 +609,7 @@ pmts_mts_report pmts_mts::macro_step() {
     pmts_mts_report rep{};
     // snapshot_previous (mts.hpp:507-510)
     CKM(cudaMemcpyAsync(fe_prev.a, ufe.a, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
-    fe_prev_gvel = gather_fe(ufe.v);
+    gather_fe(ufe.v, gprev_d);
     // unit-response upkeep (mts.hpp:249-260)
     {
         const double t0 = now_s();
@@ -667,7 +620,6 @@ pmts_mts_report pmts_mts::macro_step() {
             unit_stale = false;
             if (use_dense) refresh_dense_interface();
         }
-        CKM(cudaStreamSynchronize(stream));
         rep.t_unit = now_s() - t0;
     }
     if (counts_cap < m + 1) {
@@ -678,20 +630,11 @@ pmts_mts_report pmts_mts::macro_step() {
     // free FE solve (mts.hpp:143-147)
     const double tk0 = now_s();
     mtsk::predict(nf, ufe.u, ufe.v, ufe.a, rd, rv, fe_nm.dt, fe_nm.cpv, fe_nm.cpd, stream);
-    fe_solve(fe_P, load_scale(t + dt_fe()), rv, rd, warm_fe_free, &warm_free_ok, false, vfe);
-    CKM(cudaStreamSynchronize(stream));
-    const double fe_seconds = now_s() - tk0;
-    // free PD solve, m substeps with the known multiplier load S_j (mts.hpp:152-180)
-    const double tp0 = now_s();
-    // the substep multiplier loads S_j are known up front: one upload
-    {
-        std::vector<double> sv((size_t)m * nl);
-        for (int j = 1; j <= m; ++j) {
-            const std::vector<double> sj = s_vector(j);
-            std::copy(sj.begin(), sj.end(), sv.begin() + (size_t)(j - 1) * nl);
-        }
-        to_dev(sv_d, sv);
-    }
+    fe_solve(fe_P, load_scale(t + dt_fe()), rv, rd, warm_fe_free, &warm_free_ok, false, vfe,
+             CG_FE_FREE);
+    // free PD solve, m substeps with the multiplier loads S_j (mts.hpp:152-180), the S_j
+    // rows formed on the device
+    mtsk::s_vectors(nl, m, t, s.dt_pd, dt_fe(), s.ramp, lamp_d, gpfe_d, sv_d, stream);
     mtsk::gather(nl, cpd, upd.v, gp_free_d, stream);
     copy(vpd, upd, np);
     for (int j = 1; j <= m; ++j) {
@@ -701,106 +644,103 @@ pmts_mts_report pmts_mts::macro_step() {
         pd_solve(ra, 1.0, rv, rd, mask_live, fracture, j, false, vpd);
         mtsk::gather(nl, cpd, vpd.v, gp_free_d + (size_t)j * nl, stream);
     }
-    CKM(cudaStreamSynchronize(stream));
-    const double pd_seconds = now_s() - tp0;
-    rep.t_kinematic = std::max(fe_seconds, pd_seconds);
+    rep.t_kinematic = now_s() - tk0;  // enqueue time (the work is asynchronous)
     // interface solve + recombination (mts.hpp:184-241)
     const double tl0 = now_s();
     int iters = 0;
-    lambda = interface_solve(&iters);
+    interface_solve(&iters);
     rep.interface_iterations = iters;
     {  // FE correction: M_block W = -G^T lambda
         zero_vec(ra, nf);
         zero_vec(rv, nf);
         zero_vec(rd, nf);
-        add_gt_fe(scaled(lambda, -1.0), ra);
-        fe_solve(ra, 1.0, rv, rd, warm_fe_link, &warm_link_ok, true, wst);
+        add_gt_fe_neg(lam_d, ra);
+        fe_solve(ra, 1.0, rv, rd, warm_fe_link, &warm_link_ok, true, wst, CG_FE_LINK);
         mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst.u, wst.v, wst.a, ufe.u, ufe.v, ufe.a, stream);
     }
     {  // PD correction: m substeps under the ramped multiplier load, on k_sync
-        to_dev(lam_d, lambda);
         zero_vec(gp_link_d, nl);
         lin_substeps(lam_d, nullptr, gp_link_d, wst);
         mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
     }
-    CKM(cudaStreamSynchronize(stream));
     rep.t_lambda = now_s() - tl0;
-    if (track_energy) {
-        const std::vector<double> gf = to_host(gp_free_d, (m + 1) * nl);
-        const std::vector<double> gl = to_host(gp_link_d, (m + 1) * nl);
-        gp_free.assign(m + 1, std::vector<double>(nl));
-        gp_link.assign(m + 1, std::vector<double>(nl));
-        for (int j = 0; j <= m; ++j) {
-            std::copy(gf.begin() + (size_t)j * nl, gf.begin() + (size_t)(j + 1) * nl, gp_free[j].begin());
-            std::copy(gl.begin() + (size_t)j * nl, gl.begin() + (size_t)(j + 1) * nl, gp_link[j].begin());
-        }
-    }
     // bonds broken in the free substeps, then the post-recombination audit
     const double tu0 = now_s();
-    if (fracture) {
-        pd_K(upd.u, kd, mask_live, true, 0);  // slot 0: the audit
-        std::vector<unsigned long long> cnt(m + 1);
-        CKM(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(unsigned long long) * (m + 1),
-                            cudaMemcpyDeviceToHost, stream));
-        CKM(cudaStreamSynchronize(stream));
-        long long nb = 0;
-        for (auto c : cnt) nb += (long long)c;
-        if (nb > 0) unit_stale = true;
-        rep.newly_broken = (int32_t)nb;
-        broken_total += nb;
-    }
+    if (fracture) pd_K(upd.u, kd, mask_live, true, 0);  // slot 0: the audit
     rep.t_update = now_s() - tu0;
-    // energy record (mts.hpp:447-504)
+    // energy record (mts.hpp:447-504) and continuity residual (mts.hpp:309-317), reduced
+    // on the device; everything the host needs comes back in one copy
+    CKM(cudaMemsetAsync(cmax_d, 0, 3 * sizeof(unsigned long long), stream));
+    CKM(cudaMemsetAsync(en_d, 0, 3 * sizeof(double), stream));
     if (track_energy) {
         if (fe_nm.gamma != 0.5) {
             double* da = cg_kx;  // scratch, nf
             mtsk::rhs(nf, ufe.a, 1.0, fe_prev.a, zero_flags(nf), da, stream);  // da = acc - prev
-            const std::vector<double> dah = to_host(da, nf);
             fe_K(da, cg_ap);
-            const std::vector<double> ka = to_host(cg_ap, nf);
-            double quad = 0.0;
             const double f = fe_nm.dt * fe_nm.dt * (fe_nm.beta - fe_nm.gamma / 2.0);
-            for (int i = 0; i < nf; ++i) quad += dah[i] * (s.fe_mass[i] * dah[i] + f * ka[i]);
-            rep.quad_fe = -(fe_nm.gamma - 0.5) * quad;
+            mtsk::quad_w(nf, da, fe_M, f, cg_ap, cg_r, stream);
+            mtsk::dot(nf, da, cg_r, part, en_d + 0, stream);
         }
-        {
-            const std::vector<double> gf_m = gather_fe(ufe.v);
-            double sum = 0.0;
-            for (int r = 0; r < nl; ++r)
-                sum += (gf_m[r] - fe_prev_gvel[r]) * (lambda[r] - lambda_prev[r]);
-            rep.lambda_fe = sum / dt_fe();
-        }
-        {
-            double sum = 0.0;
-            for (int j = 1; j <= m; ++j) {
-                const std::vector<double> sj = s_vector(j), sjm = s_vector(j - 1);
-                for (int r = 0; r < nl; ++r) {
-                    const double vel_j = gp_free[j][r] + gp_link[j][r];
-                    const double vel_jm = gp_free[j - 1][r] + (j > 1 ? gp_link[j - 1][r] : 0.0);
-                    const double lam_j = sj[r] + (double(j) / m) * lambda[r];
-                    const double lam_jm = sjm[r] + (double(j - 1) / m) * lambda[r];
-                    sum += (vel_j - vel_jm) * (lam_j - lam_jm);
-                }
-            }
-            rep.lambda_pd = -sum / s.dt_pd;
-        }
+        gather_fe(ufe.v, gvec);
+        mtsk::sub2(nl, gvec, gprev_d, ta_d, stream);
+        mtsk::sub2(nl, lam_d, lamp_d, tb_d, stream);
+        mtsk::dot(nl, ta_d, tb_d, part, en_d + 1, stream);
+        mtsk::lpd_terms(nl, m, gp_free_d, gp_link_d, sv_d, lamp_d, lam_d, ta_d, tb_d, stream);
+        mtsk::dot(nl * m, ta_d, tb_d, part, en_d + 2, stream);
     }
-    // continuity residual (mts.hpp:309-317)
+    gather_fe(ufe.v, gvec);
+    mtsk::max_abs(nl, gvec, cpd, upd.v, cmax_d + 0, stream);
+    mtsk::max_abs(nf, ufe.v, nullptr, nullptr, cmax_d + 1, stream);
+    mtsk::max_abs(np, upd.v, nullptr, nullptr, cmax_d + 2, stream);
+    // lambda_prev <- lambda
+    CKM(cudaMemcpyAsync(lamp_d, lam_d, sizeof(double) * nl, cudaMemcpyDeviceToDevice, stream));
+    struct Back {
+        int st[2 * N_CG];
+        double en[3];
+        unsigned long long cmax[3];
+        unsigned long long cnt[64];
+    };
+    static_assert(sizeof(Back) <= 1024, "pinned readback buffer");
+    Back* hb = reinterpret_cast<Back*>(h_pin);
+    CKM(cudaMemcpyAsync(hb->st, cg_status, sizeof(hb->st), cudaMemcpyDeviceToHost, stream));
+    CKM(cudaMemcpyAsync(hb->en, en_d, sizeof(hb->en), cudaMemcpyDeviceToHost, stream));
+    CKM(cudaMemcpyAsync(hb->cmax, cmax_d, sizeof(hb->cmax), cudaMemcpyDeviceToHost, stream));
+    const int nc = std::min(m + 1, 64);
+    CKM(cudaMemcpyAsync(hb->cnt, d_counts, sizeof(unsigned long long) * nc, cudaMemcpyDeviceToHost,
+                        stream));
+    CKM(cudaStreamSynchronize(stream));
+    if (!fe_nm.explicit_scheme()) {
+        cg_check(hb->st, CG_FE_FREE);
+        cg_check(hb->st, CG_FE_LINK);
+    }
+    if (fracture) {
+        long long nb = 0;
+        for (int q = 0; q < nc; ++q) nb += (long long)hb->cnt[q];
+        if (m + 1 > 64) {  // (not met by the configurations: m <= 63)
+            std::vector<unsigned long long> c(m + 1);
+            CKM(cudaMemcpy(c.data(), d_counts, sizeof(unsigned long long) * (m + 1),
+                           cudaMemcpyDeviceToHost));
+            nb = 0;
+            for (auto x : c) nb += (long long)x;
+        }
+        if (nb > 0) unit_stale = true;
+        rep.newly_broken = (int32_t)nb;
+        broken_total += nb;
+    }
+    if (track_energy) {
+        if (fe_nm.gamma != 0.5) rep.quad_fe = -(fe_nm.gamma - 0.5) * hb->en[0];
+        rep.lambda_fe = hb->en[1] / dt_fe();
+        rep.lambda_pd = -hb->en[2] / s.dt_pd;
+    }
     {
-        const std::vector<double> gf = gather_fe(ufe.v), gp = gather_pd(upd.v);
-        double resid = 0.0;
-        for (int r = 0; r < nl; ++r) resid = std::max(resid, std::abs(gf[r] - gp[r]));
-        const std::vector<double> vf = to_host(ufe.v, nf), vp = to_host(upd.v, np);
-        double nf_inf = 0.0, np_inf = 0.0;
-        for (double x : vf) nf_inf = std::max(nf_inf, std::abs(x));
-        for (double x : vp) np_inf = std::max(np_inf, std::abs(x));
-        rep.continuity = resid / std::max(1.0, std::max(nf_inf, np_inf));
+        double mx[3];
+        for (int q = 0; q < 3; ++q) std::memcpy(&mx[q], &hb->cmax[q], sizeof(double));
+        rep.continuity = mx[0] / std::max(1.0, std::max(mx[1], mx[2]));
         if (enforce_continuity && rep.continuity > continuity_tol)
             throw SolverError("velocity continuity violated: residual " +
                               std::to_string(rep.continuity) + " at t=" +
                               std::to_string(t + dt_fe()));
     }
-    lambda_prev = lambda;
     t += dt_fe();
     return rep;
 }
@@ -1171,9 +1111,19 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->part2 = h->alloc<double>(2 * mtsk::dot_partials());
         h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
         CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
-        h->it_status = reinterpret_cast<int*>(h->alloc<double>(1));
-        CKM(cudaMallocHost(&h->h_pin, 4 * sizeof(double)));
-        h->scal = h->alloc<double>(16);
+        h->zero_flags(nmax);  // allocated before any CG graph capture uses it
+        h->cg_status = h->alloc<int>(2 * pmts_mts::N_CG);
+        CKM(cudaMemsetAsync(h->cg_status, 0, sizeof(int) * 2 * pmts_mts::N_CG, h->stream));
+        CKM(cudaMallocHost(&h->h_pin, 1024));
+        h->scal = h->alloc<double>(8 * pmts_mts::N_CG);
+        h->en_d = h->alloc<double>(3);
+        h->cmax_d = h->alloc<unsigned long long>(4);
+        h->lu_flag = h->alloc<int>(1);
+        h->lamp_d = h->alloc<double>(h->nl);
+        h->gprev_d = h->alloc<double>(h->nl);
+        h->ta_d = h->alloc<double>((size_t)h->m * h->nl);
+        h->tb_d = h->alloc<double>((size_t)h->m * h->nl);
+        CKM(cudaMemsetAsync(h->lamp_d, 0, sizeof(double) * h->nl, h->stream));
         h->lam_d = h->alloc<double>(h->nl);
         h->lam_tmp = h->alloc<double>(h->nl);
         h->gvec = h->alloc<double>(h->nl);
@@ -1190,8 +1140,6 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->warm_fe_link = h->alloc<double>(h->nf);
         h->d_counts = h->alloc<unsigned long long>(h->m + 1);
         h->counts_cap = h->m + 1;
-        h->lambda_prev.assign(h->nl, 0.0);
-        h->lambda.assign(h->nl, 0.0);
         // BC velocities on the initial states (mts.hpp:107-108)
         {
             std::vector<double> z(h->nf, 0.0);
@@ -1202,12 +1150,15 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             h->to_dev(h->upd.v, zp);
         }
         // g_p_fe = G_FE P_ext (mts.hpp:110)
-        h->g_p_fe.resize(h->nl);
-        for (int r = 0; r < h->nl; ++r) {
-            int j = s.cpl_fe_rp[r];
-            double acc = s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
-            for (++j; j < s.cpl_fe_rp[r + 1]; ++j) acc += s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
-            h->g_p_fe[r] = acc;
+        {
+            std::vector<double> g(h->nl);
+            for (int r = 0; r < h->nl; ++r) {
+                int j = s.cpl_fe_rp[r];
+                double acc = s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
+                for (++j; j < s.cpl_fe_rp[r + 1]; ++j) acc += s.cpl_fe_w[j] * s.fe_p_ext[s.cpl_fe_ci[j]];
+                g[r] = acc;
+            }
+            h->gpfe_d = h->upload(g);
         }
         CKM(cudaStreamSynchronize(h->stream));
         h->build_h_fe();
@@ -1333,7 +1284,13 @@ int pmts_mts_get_state(pmts_mts* h, int32_t which, double* u, double* v, double*
 int pmts_mts_get_lambda(pmts_mts* h, double* out) {
     return guard([&] {
         if (!h || !out) throw ConfigError("bad arguments");
-        std::copy(h->lambda_prev.begin(), h->lambda_prev.end(), out);
+        if (h->device < 0 || !h->lamp_d) {
+            std::fill(out, out + h->nl, 0.0);
+            return;
+        }
+        CKM(cudaMemcpyAsync(out, h->lamp_d, sizeof(double) * h->nl, cudaMemcpyDeviceToHost,
+                            h->stream));
+        CKM(cudaStreamSynchronize(h->stream));
     });
 }
 
