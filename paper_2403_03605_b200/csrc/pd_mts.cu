@@ -5,6 +5,7 @@
 // every expression rounds as the reference's does.
 // Citations: /root/reference/proj/include/perimts/.
 #include <algorithm>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -1168,6 +1169,241 @@ void iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd, 
     k_iface_jac<<<blocks(n), kT, 0, s>>>(n, D, m, dt_pd, cpd, Mpd, jd);
     check("iface_jac");
 }
+
+
+// ---- batched CG: B independent solves of the implicit FE block at once -- the unit
+// columns of H_FE (mts.hpp:389-397).  Column c of every vector is [c nf, (c + 1) nf);
+// each column runs cg_solve's arithmetic (the single-solve kernels' expressions, its
+// own scalars, loop test and iteration count); finished columns stop updating.
+// Per-column scalars: sc[8 c + {0 bb, 1 rz, 2 rr, 3 pap, 4 alpha, 5 beta}];
+// act[c] = 1 while iterating; stat[2 c] = iterations, stat[2 c + 1] = status.
+namespace {
+constexpr int kBNB = 64;  // dot partial blocks per column
+
+__global__ void k_bunit_rhs(int nf, int k0, int nl, const int32_t* rp, const int32_t* ci,
+                            const double* w, const uint8_t* cf, double* b) {
+    const int c = blockIdx.x, k = k0 + c;
+    if (k >= nl) return;
+    for (int j = rp[k] + threadIdx.x; j < rp[k + 1]; j += blockDim.x) {
+        const int i = ci[j];
+        const double ra = -w[j];  // unit_row: ra = -w; rhs: ra * 1 - K 0
+        b[(size_t)c * nf + i] = cf[i] ? 0.0 : ra * 1.0 - 0.0;
+    }
+}
+// r = b - A 0 = b, z = precond(r), p = z
+__global__ void k_binit(long long n, const double* b, const double* jac, int nf, double* r,
+                        double* z, double* p) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int i = (int)(q % nf);
+    const double ri = b[q] - 0.0;
+    r[q] = ri;
+    const double zi = jac ? (jac[i] != 0.0 ? ri / jac[i] : ri) : ri;
+    z[q] = zi;
+    p[q] = zi;
+}
+// block partials of x.y (and x2.y2) over column c = blockIdx.y
+__global__ void __launch_bounds__(kT) k_bdot(int nf, const double* x, const double* y,
+                                             const double* x2, const double* y2, const int* act,
+                                             double* part) {
+    const int c = blockIdx.y;
+    if (act && !act[c]) return;
+    __shared__ double sh[kT], sh2[kT];
+    const size_t o = (size_t)c * nf;
+    double s = 0.0, s2 = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+        s += x[o + i] * y[o + i];
+        if (x2) s2 += x2[o + i] * y2[o + i];
+    }
+    sh[threadIdx.x] = s;
+    sh2[threadIdx.x] = s2;
+    __syncthreads();
+    for (int k = kT / 2; k > 0; k >>= 1) {
+        if ((int)threadIdx.x < k) {
+            sh[threadIdx.x] += sh[threadIdx.x + k];
+            sh2[threadIdx.x] += sh2[threadIdx.x + k];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[((size_t)c * gridDim.x + blockIdx.x) * 2] = sh[0];
+        part[((size_t)c * gridDim.x + blockIdx.x) * 2 + 1] = sh2[0];
+    }
+}
+// per column (block c): the partial sums, then
+//   mode 0: bb, rz;  mode 1: rr and the start test;  mode 2: pap -> alpha (or status 1);
+//   mode 3: rz_new, rr -> beta, rz <- rz_new, the loop test
+__global__ void k_bfin(int nb, int mode, const double* part, double* sc, int* act, int* stat,
+                       double tol, int max_iter, int* n_active) {
+    const int c = blockIdx.x;
+    if (mode >= 2 && !act[c]) return;
+    __shared__ double sh[32], sh2[32];
+    double t = 0.0, t2 = 0.0;
+    for (int k = threadIdx.x; k < nb; k += 32) {
+        t += part[((size_t)c * nb + k) * 2];
+        t2 += part[((size_t)c * nb + k) * 2 + 1];
+    }
+    sh[threadIdx.x] = t;
+    sh2[threadIdx.x] = t2;
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < 32; ++k) {
+        s1 += sh[k];
+        s2 += sh2[k];
+    }
+    double* q = sc + 8 * c;
+    if (mode == 0) {
+        q[0] = s1;
+        q[1] = s2;
+    } else if (mode == 1) {
+        q[2] = s1;
+        stat[2 * c] = 0;
+        stat[2 * c + 1] = 0;
+        bool more = false;
+        if (q[0] != 0.0) {
+            more = sqrt(s1) / sqrt(q[0]) > tol;
+            if (more && max_iter <= 0) {
+                stat[2 * c + 1] = 2;
+                more = false;
+            }
+        }
+        act[c] = more ? 1 : 0;
+        if (more) atomicAdd(n_active, 1);
+    } else if (mode == 2) {
+        q[3] = s1;
+        if (s1 <= 0.0) {
+            stat[2 * c + 1] = 1;
+            act[c] = 0;
+            return;
+        }
+        q[4] = q[1] / s1;
+    } else {
+        q[5] = s1 / q[1];
+        q[1] = s1;
+        q[2] = s2;
+        const int it = ++stat[2 * c];
+        bool more = sqrt(s2) / sqrt(q[0]) > tol;
+        if (more && it >= max_iter) {
+            stat[2 * c + 1] = 2;
+            more = false;
+        }
+        act[c] = more ? 1 : 2;  // 2: finished this iteration (p still updated below)
+        if (more) atomicAdd(n_active, 1);
+    }
+}
+// ap = A p for every active column: K p (CSR, the row read once for all columns)
+// and apply_a's M p + bdt2 K p
+__global__ void k_bspmm(int nf, int B, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                        const double* __restrict__ v, const double* M, const uint8_t* cf,
+                        double bdt2, const int* act, const double* P, double* AP) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const int p0 = rp[i], p1 = rp[i + 1];
+    for (int c = 0; c < B; ++c) {
+        if (act[c] != 1) continue;
+        const size_t o = (size_t)c * nf;
+        double s = 0.0;
+        for (int p = p0; p < p1; ++p) s += v[p] * P[o + ci[p]];
+        AP[o + i] = cf[i] ? P[o + i] : M[i] * P[o + i] + bdt2 * s;
+    }
+}
+// x += alpha p; r -= alpha ap; z = precond(r)
+__global__ void k_bupdate(long long n, int nf, const double* sc, const int* act, const double* P,
+                          const double* AP, double* X, double* R, const double* jac, double* Z) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int c = (int)(q / nf), i = (int)(q % nf);
+    if (act[c] != 1) return;
+    const double al = sc[8 * c + 4];
+    X[q] += al * P[q];
+    const double ri = R[q] + -al * AP[q];
+    R[q] = ri;
+    Z[q] = jac ? (jac[i] != 0.0 ? ri / jac[i] : ri) : ri;
+}
+// p = z + beta p (columns that ran this iteration, finished ones included)
+__global__ void k_bxpby(long long n, int nf, const double* sc, int* act, const double* Z,
+                        double* P) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int c = (int)(q / nf);
+    if (act[c] == 0) return;
+    P[q] = Z[q] + sc[8 * c + 5] * P[q];
+}
+__global__ void k_bact_settle(int B, int* act) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < B && act[c] == 2) act[c] = 0;
+}
+// finish (homogeneous: v = 0 + gdt acc, constrained 0) + G_FE gather, negated into
+// column k0 + c of the column-major nl x nl D
+__global__ void k_bgather(int nl, int nf, int k0, int B, const int32_t* rp, const int32_t* ci,
+                          const double* w, const uint8_t* cf, double gdt, const double* X,
+                          double* D) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)nl * B) return;
+    const int c = (int)(q / nl), r = (int)(q % nl);
+    if (k0 + c >= nl) return;
+    const size_t o = (size_t)c * nf;
+    auto vel = [&](int i) { return cf[i] ? 0.0 : 0.0 + gdt * X[o + i]; };
+    int j = rp[r];
+    double acc = w[j] * vel(ci[j]);
+    for (++j; j < rp[r + 1]; ++j) acc += w[j] * vel(ci[j]);
+    D[(size_t)(k0 + c) * nl + r] = -acc;
+}
+}  // namespace
+
+// the unit columns k0 .. k0 + B - 1 of H_FE (implicit FE) into D; scratch: 6 B nf
+// doubles (b, x, r, z, p, ap), part (2 kBNB B doubles), sc (8 B), act/stat/n_active
+// ints; returns 0, or the first failing column's status (1 not SPD, 2 no convergence)
+int batched_unit_columns(int nf, int nl, int k0, int B, const int32_t* krp, const int32_t* kci,
+                         const double* kv, const double* M, const uint8_t* cf, const double* jac,
+                         double bdt2, double gdt, const int32_t* grp, const int32_t* gci,
+                         const double* gw, double tol, int max_iter, double* scratch, double* part,
+                         double* sc, int* act, int* stat, int* n_active, int* h_count, double* D,
+                         int* iters_out, cudaStream_t s) {
+    const long long n = (long long)B * nf;
+    double *b = scratch, *x = b + n, *r = x + n, *z = r + n, *p = z + n, *ap = p + n;
+    cudaMemsetAsync(b, 0, sizeof(double) * n, s);
+    cudaMemsetAsync(x, 0, sizeof(double) * n, s);
+    k_bunit_rhs<<<B, 32, 0, s>>>(nf, k0, nl, grp, gci, gw, cf, b);
+    k_binit<<<blocks(n), kT, 0, s>>>(n, b, jac, nf, r, z, p);
+    cudaMemsetAsync(n_active, 0, sizeof(int), s);
+    const dim3 dg(kBNB, B);
+    k_bdot<<<dg, kT, 0, s>>>(nf, b, b, r, z, nullptr, part);
+    k_bfin<<<B, 32, 0, s>>>(kBNB, 0, part, sc, act, stat, tol, max_iter, n_active);
+    k_bdot<<<dg, kT, 0, s>>>(nf, r, r, nullptr, nullptr, nullptr, part);
+    k_bfin<<<B, 32, 0, s>>>(kBNB, 1, part, sc, act, stat, tol, max_iter, n_active);
+    int it = 0;
+    for (;;) {
+        cudaMemcpyAsync(h_count, n_active, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (*h_count == 0) break;
+        cudaMemsetAsync(n_active, 0, sizeof(int), s);
+        k_bspmm<<<blocks(nf), kT, 0, s>>>(nf, B, krp, kci, kv, M, cf, bdt2, act, p, ap);
+        k_bdot<<<dg, kT, 0, s>>>(nf, p, ap, nullptr, nullptr, act, part);
+        k_bfin<<<B, 32, 0, s>>>(kBNB, 2, part, sc, act, stat, tol, max_iter, n_active);
+        k_bupdate<<<blocks(n), kT, 0, s>>>(n, nf, sc, act, p, ap, x, r, jac, z);
+        k_bdot<<<dg, kT, 0, s>>>(nf, r, z, r, r, act, part);
+        k_bfin<<<B, 32, 0, s>>>(kBNB, 3, part, sc, act, stat, tol, max_iter, n_active);
+        k_bxpby<<<blocks(n), kT, 0, s>>>(n, nf, sc, act, z, p);
+        k_bact_settle<<<1, 1024, 0, s>>>(B, act);
+        ++it;
+    }
+    std::vector<int> st(2 * B);
+    cudaMemcpyAsync(st.data(), stat, sizeof(int) * 2 * B, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    int bad = 0, mx = 0;
+    for (int c = 0; c < B && k0 + c < nl; ++c) {
+        mx = std::max(mx, st[2 * c]);
+        if (st[2 * c + 1] && !bad) bad = st[2 * c + 1];
+    }
+    if (!bad)
+        k_bgather<<<blocks((long long)nl * B), kT, 0, s>>>(nl, nf, k0, B, grp, gci, gw, cf, gdt, x, D);
+    check("batched_unit_columns");
+    if (iters_out) *iters_out = mx;
+    return bad;
+}
+int batched_partials() { return kBNB; }
 
 }  // namespace mtsk
 }  // namespace pmts

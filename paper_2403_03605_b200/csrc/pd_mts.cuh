@@ -111,6 +111,15 @@ void row_nnz(int n, const double* D, int* cnt, cudaStream_t s);
 void row_fill(int n, const double* D, const int* rp, int32_t* ci, double* v, cudaStream_t s);
 void iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd, const double* Mpd,
                double* jd, cudaStream_t s);
+// the implicit-FE unit columns k0 .. k0 + B - 1 of H_FE as B simultaneous CG solves
+// (see pd_mts.cu); returns 0 or the first failing column's CG status
+int batched_unit_columns(int nf, int nl, int k0, int B, const int32_t* krp, const int32_t* kci,
+                         const double* kv, const double* M, const uint8_t* cf, const double* jac,
+                         double bdt2, double gdt, const int32_t* grp, const int32_t* gci,
+                         const double* gw, double tol, int max_iter, double* scratch, double* part,
+                         double* sc, int* act, int* stat, int* n_active, int* h_count, double* D,
+                         int* iters_out, cudaStream_t s);
+int batched_partials();
 
 }  // namespace mtsk
 }  // namespace pmts

@@ -446,12 +446,43 @@ struct pmts_mts {
     void build_h_fe() {
         double* D = nullptr;
         CKM(cudaMallocAsync(&D, sizeof(double) * (size_t)nl * nl, stream));
-        for (int k = 0; k < nl; ++k) {
-            unit_fe_column(k, yst);
-            gather_fe(yst.v, gvec);
-            mtsk::col_neg(nl, k, gvec, D, stream);
-            if (!fe_nm.explicit_scheme() && (k % 256 == 255 || k == nl - 1))
-                cg_result(CG_UNIT);  // the unit columns' CG status, now and then
+        if (fe_nm.explicit_scheme()) {
+            for (int k = 0; k < nl; ++k) {
+                unit_fe_column(k, yst);
+                gather_fe(yst.v, gvec);
+                mtsk::col_neg(nl, k, gvec, D, stream);
+            }
+        } else {
+            // implicit FE: the unit columns as batches of simultaneous CG solves (one
+            // sparse-matrix read per iteration for the whole batch)
+            const int B = std::min(nl, 64);
+            double *scr = nullptr, *part = nullptr, *sc = nullptr;
+            int *act = nullptr, *stat = nullptr, *nact = nullptr, *hcount = nullptr;
+            CKM(cudaMallocAsync(&scr, sizeof(double) * 6 * (size_t)B * nf, stream));
+            CKM(cudaMallocAsync(&part, sizeof(double) * 2 * mtsk::batched_partials() * (size_t)B,
+                                stream));
+            CKM(cudaMallocAsync(&sc, sizeof(double) * 8 * (size_t)B, stream));
+            CKM(cudaMallocAsync(&act, sizeof(int) * (3 * (size_t)B + 1), stream));
+            stat = act + B;
+            nact = stat + 2 * B;
+            CKM(cudaMallocHost(&hcount, sizeof(int)));
+            for (int k0 = 0; k0 < nl; k0 += B) {
+                int iters = 0;
+                const int bad = mtsk::batched_unit_columns(
+                    nf, nl, k0, B, fe_rp, fe_ci, fe_v, fe_M, fe_cf, fe_jac, fe_nm.bdt2, fe_nm.gdt,
+                    gfe_rp, gfe_ci, gfe_w, cg_tol, fe_cg_max, scr, part, sc, act, stat, nact,
+                    hcount, D, &iters, stream);
+                if (bad == 1) throw SolverError("cg: operator not positive definite");
+                if (bad == 2)
+                    throw SolverError("cg: no convergence after " + std::to_string(fe_cg_max) +
+                                      " iterations");
+            }
+            CKM(cudaFreeAsync(scr, stream));
+            CKM(cudaFreeAsync(part, stream));
+            CKM(cudaFreeAsync(sc, stream));
+            CKM(cudaFreeAsync(act, stream));
+            CKM(cudaStreamSynchronize(stream));
+            cudaFreeHost(hcount);
         }
         if (use_dense || iface_mode == 1) {
             if (!hfe_dense) hfe_dense = alloc<double>((size_t)nl * nl);
