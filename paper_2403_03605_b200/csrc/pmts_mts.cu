@@ -88,6 +88,26 @@ struct pmts_mts {
     MtsSystem s;
     int device = 0;
     cudaStream_t stream = nullptr;
+    // a second stream for the FE side: the FE and PD halves of the macro step are
+    // independent between the multiplier updates (fork / join by events; captured into
+    // the CG graphs as well: H_FE w next to the PD recursion of the interface operator)
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_join2 = nullptr;
+    void fork(cudaEvent_t e) {  // stream2 waits for the work enqueued on stream so far
+        CKM(cudaEventRecord(e, stream));
+        CKM(cudaStreamWaitEvent(stream2, e, 0));
+    }
+    void join(cudaEvent_t e) {  // stream waits for stream2
+        CKM(cudaEventRecord(e, stream2));
+        CKM(cudaStreamWaitEvent(stream, e, 0));
+    }
+    struct OnStream2 {  // route the member-stream calls of a block to stream2
+        pmts_mts* h;
+        explicit OnStream2(pmts_mts* hh) : h(hh) { std::swap(h->stream, h->stream2); }
+        ~OnStream2() { std::swap(h->stream, h->stream2); }
+    };
+    double *rd_fe = nullptr, *rv_fe = nullptr, *ra_fe = nullptr, *lam_tmp_fe = nullptr;
+    DState wst_fe;
     pmts_pd* pd = nullptr;
     DevPD pdv{};
     std::vector<int32_t> pairs;  // global ids
@@ -165,6 +185,9 @@ struct pmts_mts {
         for (void* p : owned) cudaFree(p);
         if (pd) pmts_pd_destroy(pd);
         if (stream) cudaStreamDestroy(stream);
+        if (stream2) cudaStreamDestroy(stream2);
+        for (cudaEvent_t e : {ev_fork, ev_join, ev_fork2, ev_join2})
+            if (e) cudaEventDestroy(e);
     }
     template <class T>
     T* alloc(size_t n) {
@@ -403,10 +426,11 @@ struct pmts_mts {
     void gather_fe(const double* x, double* out) {
         mtsk::gather_csr(nl, gfe_rp, gfe_ci, gfe_w, x, out, stream);
     }
-    // dst += G_FE^T (-vals): the reference's scatter of scaled(lambda, -1)
-    void add_gt_fe_neg(const double* vals, double* dst) {
-        mtsk::neg(nl, vals, lam_tmp, stream);
-        mtsk::scatter_csr(gft_n, gft_d, gft_rp, gft_ri, gft_w, lam_tmp, dst, stream);
+    // dst += G_FE^T (-vals): the reference's scatter of scaled(lambda, -1); tmp: nl scratch
+    void add_gt_fe_neg(const double* vals, double* dst, double* tmp = nullptr) {
+        if (!tmp) tmp = lam_tmp;
+        mtsk::neg(nl, vals, tmp, stream);
+        mtsk::scatter_csr(gft_n, gft_d, gft_rp, gft_ri, gft_w, tmp, dst, stream);
     }
     void zero_vec(double* x, int n) { CKM(cudaMemsetAsync(x, 0, sizeof(double) * n, stream)); }
 
@@ -579,8 +603,13 @@ struct pmts_mts {
         const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
         cg(nl,
            [&](const double* in, double* out) {
-               mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
+               fork(ev_fork2);
+               {
+                   OnStream2 on(this);
+                   mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
+               }
                apply_h_pd(in, iface_tmp);
+               join(ev_join2);
                mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
            },
            b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
@@ -660,9 +689,13 @@ pmts_mts_report pmts_mts::macro_step() {
     CKM(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * (m + 1), stream));
     // free FE solve (mts.hpp:143-147)
     const double tk0 = now_s();
-    mtsk::predict(nf, ufe.u, ufe.v, ufe.a, rd, rv, fe_nm.dt, fe_nm.cpv, fe_nm.cpd, stream);
-    fe_solve(fe_P, load_scale(t + dt_fe()), rv, rd, warm_fe_free, &warm_free_ok, false, vfe,
-             CG_FE_FREE);
+    fork(ev_fork);  // the FE half on stream2, the PD half on stream
+    {
+        OnStream2 on(this);
+        mtsk::predict(nf, ufe.u, ufe.v, ufe.a, rd_fe, rv_fe, fe_nm.dt, fe_nm.cpv, fe_nm.cpd, stream);
+        fe_solve(fe_P, load_scale(t + dt_fe()), rv_fe, rd_fe, warm_fe_free, &warm_free_ok, false,
+                 vfe, CG_FE_FREE);
+    }
     // free PD solve, m substeps with the multiplier loads S_j (mts.hpp:152-180), the S_j
     // rows formed on the device
     mtsk::s_vectors(nl, m, t, s.dt_pd, dt_fe(), s.ramp, lamp_d, gpfe_d, sv_d, stream);
@@ -675,25 +708,30 @@ pmts_mts_report pmts_mts::macro_step() {
         pd_solve(ra, 1.0, rv, rd, mask_live, fracture, j, false, vpd);
         mtsk::gather(nl, cpd, vpd.v, gp_free_d + (size_t)j * nl, stream);
     }
+    join(ev_join);
     rep.t_kinematic = now_s() - tk0;  // enqueue time (the work is asynchronous)
     // interface solve + recombination (mts.hpp:184-241)
     const double tl0 = now_s();
     int iters = 0;
     interface_solve(&iters);
     rep.interface_iterations = iters;
-    {  // FE correction: M_block W = -G^T lambda
-        zero_vec(ra, nf);
-        zero_vec(rv, nf);
-        zero_vec(rd, nf);
-        add_gt_fe_neg(lam_d, ra);
-        fe_solve(ra, 1.0, rv, rd, warm_fe_link, &warm_link_ok, true, wst, CG_FE_LINK);
-        mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst.u, wst.v, wst.a, ufe.u, ufe.v, ufe.a, stream);
+    fork(ev_fork);
+    {  // FE correction: M_block W = -G^T lambda (stream2)
+        OnStream2 on(this);
+        zero_vec(ra_fe, nf);
+        zero_vec(rv_fe, nf);
+        zero_vec(rd_fe, nf);
+        add_gt_fe_neg(lam_d, ra_fe, lam_tmp_fe);
+        fe_solve(ra_fe, 1.0, rv_fe, rd_fe, warm_fe_link, &warm_link_ok, true, wst_fe, CG_FE_LINK);
+        mtsk::add_states(nf, vfe.u, vfe.v, vfe.a, wst_fe.u, wst_fe.v, wst_fe.a, ufe.u, ufe.v, ufe.a,
+                         stream);
     }
     {  // PD correction: m substeps under the ramped multiplier load, on k_sync
         zero_vec(gp_link_d, nl);
         lin_substeps(lam_d, nullptr, gp_link_d, wst);
         mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
     }
+    join(ev_join);
     rep.t_lambda = now_s() - tl0;
     // bonds broken in the free substeps, then the post-recombination audit
     const double tu0 = now_s();
@@ -987,6 +1025,9 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         }
         CKM(cudaSetDevice(h->device));
         CKM(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CKM(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&h->ev_fork, &h->ev_join, &h->ev_fork2, &h->ev_join2})
+            CKM(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         h->nf = s.fe_n_dof;
         h->np = s.pd_n_dof;
         h->nl = int(s.cpl_fe.size());
@@ -1143,6 +1184,11 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
         CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
         h->zero_flags(nmax);  // allocated before any CG graph capture uses it
+        h->rd_fe = h->alloc<double>(h->nf);
+        h->rv_fe = h->alloc<double>(h->nf);
+        h->ra_fe = h->alloc<double>(h->nf);
+        h->lam_tmp_fe = h->alloc<double>(h->nl);
+        h->wst_fe = h->state(h->nf);
         h->cg_status = h->alloc<int>(2 * pmts_mts::N_CG);
         CKM(cudaMemsetAsync(h->cg_status, 0, sizeof(int) * 2 * pmts_mts::N_CG, h->stream));
         CKM(cudaMallocHost(&h->h_pin, 1024));
