@@ -306,6 +306,11 @@ typedef struct {
     int32_t interface_precond;   /* matrix-free interface CG: 0 = the reference's plain CG
                                     (mts.hpp:194-213, default); 1 = Jacobi-preconditioned with
                                     diag(H_FE) + m dt / (2 M_PD) (an addition) */
+    int32_t interface_recursion; /* matrix-free interface: 1 = G_PD vel(Y_PD) w by the m-substep
+                                    recursion in every CG iteration (apply_h_pd, mts.hpp:410-420);
+                                    0 (default) = that operator precomputed once as an exact
+                                    sparse matrix (coloured simultaneous unit loads), used until
+                                    bonds break */
 } pmts_mts_desc;
 
 typedef struct {

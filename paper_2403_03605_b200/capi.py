@@ -82,7 +82,7 @@ class MtsDesc(C.Structure):
                 ("overlap_width_factor", _D), ("weight_kind", _I), ("gamma_fe", _D),
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
                 ("track_energy", _I), ("device", _I), ("fe_spacing", _D),
-                ("interface_precond", _I)]
+                ("interface_precond", _I), ("interface_recursion", _I)]
 
 
 class MtsView(C.Structure):

@@ -1405,5 +1405,29 @@ int batched_unit_columns(int nf, int nl, int k0, int B, const int32_t* krp, cons
 }
 int batched_partials() { return kBNB; }
 
+
+namespace {
+__global__ void k_set_ones(int n, const int32_t* idx, double* x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[idx[i]] = 1.0;
+}
+__global__ void k_gather_slots(int n, const int32_t* rows, const int64_t* slots, const double* g,
+                               double* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[slots[i]] = g[rows[i]];
+}
+}  // namespace
+void set_ones(int n, const int32_t* idx, double* x, cudaStream_t s) {
+    if (n <= 0) return;
+    k_set_ones<<<blocks(n), kT, 0, s>>>(n, idx, x);
+    check("set_ones");
+}
+void gather_slots(int n, const int32_t* rows, const int64_t* slots, const double* g, double* dst,
+                  cudaStream_t s) {
+    if (n <= 0) return;
+    k_gather_slots<<<blocks(n), kT, 0, s>>>(n, rows, slots, g, dst);
+    check("gather_slots");
+}
+
 }  // namespace mtsk
 }  // namespace pmts

@@ -120,6 +120,10 @@ int batched_unit_columns(int nf, int nl, int k0, int B, const int32_t* krp, cons
                          double* sc, int* act, int* stat, int* n_active, int* h_count, double* D,
                          int* iters_out, cudaStream_t s);
 int batched_partials();
+// x[idx[i]] = 1 (i < n); dst[slots[i]] = g[rows[i]] (H_PD columns by colour)
+void set_ones(int n, const int32_t* idx, double* x, cudaStream_t s);
+void gather_slots(int n, const int32_t* rows, const int64_t* slots, const double* g, double* dst,
+                  cudaStream_t s);
 
 }  // namespace mtsk
 }  // namespace pmts

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <unordered_map>
 #include <vector>
 
 #include "pd_common.cuh"
@@ -116,6 +117,7 @@ struct pmts_mts {
     Nm fe_nm, pd_nm;
     int iface_mode = 0;
     bool interface_precond = false;  // pmts_mts_desc.interface_precond
+    bool iface_precompute = true;    // pmts_mts_desc.interface_h_pd (precomputed H_PD)
     bool enforce_continuity = true, track_energy = true, fracture = false;
     double continuity_tol = 1e-8, cg_tol = 1e-10, interface_cg_tol = 1e-11;
     int fe_cg_max = 100;
@@ -573,6 +575,150 @@ struct pmts_mts {
         lin_substeps(w_dev, out_dev, nullptr, yst);
     }
 
+    // ---- H_PD = G_PD vel(Y_PD) as an exact sparse matrix (matrix-free interface) ----
+    // The m homogeneous linear substeps spread a unit load at a coupling dof by at most
+    // delta + h_e per substep after the first (node -> incident element -> partner
+    // within delta -> its nodes; h_e the element diameter), so column k's nonzeros lie
+    // within R = (m - 1)(delta + h_e) of the load.  Columns whose loads are more than 2R
+    // apart have disjoint supports and are computed together by ONE recursion (a
+    // colouring of the coupling dofs): the responses superpose with exact zeros, so each
+    // column is bitwise its single-load run (unit_pd_column).  Built once at setup;
+    // when bonds break the k_sync snapshot changes and the interface goes back to the
+    // matrix-free recursion (apply_h_pd).
+    bool hpd_valid = false;
+    int32_t *hpd_rp = nullptr, *hpd_ci = nullptr;
+    double* hpd_v = nullptr;
+    int64_t hpd_nnz = 0;
+    int hpd_colours = 0;
+    void build_h_pd() {
+        const int dim = s.dim;
+        std::vector<int> dof2node(np, -1);
+        for (size_t nd = 0; nd < s.pd_node_dof.size(); ++nd)
+            if (s.pd_node_dof[nd] >= 0)
+                for (int c = 0; c < dim; ++c) dof2node[s.pd_node_dof[nd] + c] = (int)nd;
+        std::vector<double> pos(3 * (size_t)nl);
+        for (int r = 0; r < nl; ++r) {
+            const int nd = dof2node[s.cpl_pd[r]];
+            if (nd < 0) throw InternalError("coupling row without a PD node");
+            for (int c = 0; c < 3; ++c) pos[3 * (size_t)r + c] = s.nodes[3 * (size_t)nd + c];
+        }
+        const int nn = dim == 2 ? 4 : 8;
+        double he = 0.0;
+        for (int e : s.pd_active)
+            for (int a = 0; a < nn; ++a)
+                for (int b = a + 1; b < nn; ++b) {
+                    const double* p = &s.nodes[3 * (size_t)s.conn[(size_t)e * nn + a]];
+                    const double* q = &s.nodes[3 * (size_t)s.conn[(size_t)e * nn + b]];
+                    double d2 = 0.0;
+                    for (int c = 0; c < 3; ++c) d2 += (p[c] - q[c]) * (p[c] - q[c]);
+                    he = std::max(he, std::sqrt(d2));
+                }
+        // support radius of a column (a relative margin for the rounding of positions)
+        const double R = (m - 1) * (s.delta + he) * (1.0 + 1e-9) + 1e-12 * he;
+        const double cell = std::max(2.0 * R, 1e-12);
+        auto key = [&](int r, int dx, int dy, int dz) {
+            const long long i = (long long)std::floor(pos[3 * (size_t)r] / cell) + dx;
+            const long long j = (long long)std::floor(pos[3 * (size_t)r + 1] / cell) + dy;
+            const long long k = (long long)std::floor(pos[3 * (size_t)r + 2] / cell) + dz;
+            return (i * 1000003LL + j) * 1000033LL + k;
+        };
+        std::unordered_map<long long, std::vector<int>> grid;
+        for (int r = 0; r < nl; ++r) grid[key(r, 0, 0, 0)].push_back(r);
+        auto dist2 = [&](int a, int b) {
+            double d2 = 0.0;
+            for (int c = 0; c < 3; ++c) {
+                const double d = pos[3 * (size_t)a + c] - pos[3 * (size_t)b + c];
+                d2 += d * d;
+            }
+            return d2;
+        };
+        // rows within R of each source (the column structure) and within 2R (conflicts)
+        std::vector<std::vector<int>> near(nl);  // rows within R, ascending
+        std::vector<int> colour(nl, -1);
+        std::vector<int> forbid;
+        const int dzr = dim == 3 ? 1 : 0;
+        for (int k = 0; k < nl; ++k) {
+            forbid.clear();
+            for (int dz = -dzr; dz <= dzr; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        auto it = grid.find(key(k, dx, dy, dz));
+                        if (it == grid.end()) continue;
+                        for (int r : it->second) {
+                            const double d2 = dist2(k, r);
+                            if (d2 <= R * R) near[k].push_back(r);
+                            if (d2 < 4.0 * R * R * (1.0 + 1e-9) && colour[r] >= 0)
+                                forbid.push_back(colour[r]);
+                        }
+                    }
+            std::sort(near[k].begin(), near[k].end());
+            std::sort(forbid.begin(), forbid.end());
+            int c = 0;
+            for (int f : forbid) {
+                if (f == c) ++c;
+                else if (f > c) break;
+            }
+            colour[k] = c;
+            hpd_colours = std::max(hpd_colours, c + 1);
+        }
+        // CSR by rows: row r holds the sources k with r in near[k], ascending k
+        std::vector<int32_t> rp(nl + 1, 0);
+        for (int k = 0; k < nl; ++k)
+            for (int r : near[k]) ++rp[r + 1];
+        for (int r = 0; r < nl; ++r) rp[r + 1] += rp[r];
+        hpd_nnz = rp[nl];
+        std::vector<int32_t> ci(hpd_nnz);
+        std::vector<int64_t> slot_of;  // per (k, r in near[k]) in k order
+        {
+            std::vector<int32_t> fill(rp.begin(), rp.end() - 1);
+            slot_of.reserve(hpd_nnz);
+            for (int k = 0; k < nl; ++k)  // k ascending: each row's columns ascending
+                for (int r : near[k]) {
+                    ci[fill[r]] = k;
+                    slot_of.push_back(fill[r]++);
+                }
+        }
+        // per colour: its sources, and the (row, slot) pairs of its columns
+        std::vector<int64_t> pstart(nl + 1, 0);
+        for (int k = 0; k < nl; ++k) pstart[k + 1] = pstart[k] + (int64_t)near[k].size();
+        std::vector<std::vector<int>> members(hpd_colours);
+        for (int k = 0; k < nl; ++k) members[colour[k]].push_back(k);
+        std::vector<int32_t> src_all, rows_all;
+        std::vector<int64_t> slots_all;
+        std::vector<int64_t> c_src(hpd_colours + 1, 0), c_pair(hpd_colours + 1, 0);
+        rows_all.reserve(hpd_nnz);
+        slots_all.reserve(hpd_nnz);
+        for (int c = 0; c < hpd_colours; ++c) {
+            for (int k : members[c]) {
+                src_all.push_back(k);
+                for (size_t q = 0; q < near[k].size(); ++q) {
+                    rows_all.push_back(near[k][q]);
+                    slots_all.push_back(slot_of[pstart[k] + q]);
+                }
+            }
+            c_src[c + 1] = (int64_t)src_all.size();
+            c_pair[c + 1] = (int64_t)rows_all.size();
+        }
+        hpd_rp = upload(rp);
+        hpd_ci = upload(ci);
+        hpd_v = alloc<double>(std::max<int64_t>(hpd_nnz, 1));
+        CKM(cudaMemsetAsync(hpd_v, 0, sizeof(double) * std::max<int64_t>(hpd_nnz, 1), stream));
+        int32_t* d_src = upload(src_all);
+        int32_t* d_rows = upload(rows_all);
+        int64_t* d_slots = upload(slots_all);
+        for (int c = 0; c < hpd_colours; ++c) {
+            zero_vec(lam_tmp, nl);
+            mtsk::set_ones((int)(c_src[c + 1] - c_src[c]), d_src + c_src[c], lam_tmp, stream);
+            lin_substeps(lam_tmp, nullptr, nullptr, yst);
+            mtsk::gather(nl, cpd, yst.v, gvec, stream);
+            mtsk::gather_slots((int)(c_pair[c + 1] - c_pair[c]), d_rows + c_pair[c],
+                               d_slots + c_pair[c], gvec, hpd_v, stream);
+        }
+        CKM(cudaStreamSynchronize(stream));
+        hpd_valid = true;
+        invalidate_cg_graphs();
+    }
+
     void initialize_accelerations() {
         // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
         mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
@@ -608,7 +754,10 @@ struct pmts_mts {
                    OnStream2 on(this);
                    mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
                }
-               apply_h_pd(in, iface_tmp);
+               if (hpd_valid)  // the precomputed G_PD vel(Y_PD) (exact sparse)
+                   mtsk::csr_spmv_warp(nl, hpd_rp, hpd_ci, hpd_v, in, iface_tmp, stream);
+               else  // the m-substep recursion on the current k_sync
+                   apply_h_pd(in, iface_tmp);
                join(ev_join2);
                mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
            },
@@ -677,6 +826,10 @@ pmts_mts_report pmts_mts::macro_step() {
             CKM(cudaMemcpyAsync(mask_sync, mask_live, sizeof(uint32_t) * mask_words,
                                 cudaMemcpyDeviceToDevice, stream));
             h_valid = false;
+            if (hpd_valid) {  // k_sync changed: the recursion from here on
+                hpd_valid = false;
+                invalidate_cg_graphs();
+            }
             unit_stale = false;
             if (use_dense) refresh_dense_interface();
         }
@@ -1017,6 +1170,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->m = s.m;
         h->iface_mode = desc->interface_mode;
         h->interface_precond = desc->interface_precond != 0;
+        h->iface_precompute = desc->interface_recursion == 0;
         // interface mode (mts.hpp:111-114); the PD side is explicit
         h->use_dense = h->iface_mode == 1 || (h->iface_mode == 0 && h->nl <= 400);
         if (h->device < 0) {  // host-only: the assembled systems (view), no integrator
@@ -1240,6 +1394,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         CKM(cudaStreamSynchronize(h->stream));
         h->build_h_fe();
         if (h->use_dense) h->refresh_dense_interface();
+        else if (h->iface_precompute) h->build_h_pd();
         CKM(cudaStreamSynchronize(h->stream));
         *out = h.release();
     });

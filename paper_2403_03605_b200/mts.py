@@ -61,6 +61,8 @@ class MtsSolver:
         # extension: Jacobi-preconditioned interface CG (run.interface_precond = jacobi);
         # the default is the reference's plain CG
         d.interface_precond = 1 if run.get("interface_precond", "none") == "jacobi" else 0
+        # run.interface_h_pd = precompute (default) | recursion
+        d.interface_recursion = 1 if run.get("interface_h_pd", "precompute") == "recursion" else 0
         h = C.c_void_p()
         check(lib().pmts_mts_create(C.byref(d), C.byref(h)))
         self.h = h

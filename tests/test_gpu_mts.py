@@ -103,3 +103,24 @@ def test_interface_preconditioner_same_solution():
     (lp, up, ip), (lq, uq, iq) = out[False], out[True]
     assert _rel(lp, lq) <= 1e-9 and _rel(up, uq) <= 1e-9
     assert ip <= iq
+
+
+@pytest.mark.parametrize("name", ["mts_mini_mfree", "mts_bar3d"])
+def test_precomputed_h_pd_equals_recursion(name):
+    """The matrix-free interface with G_PD vel(Y_PD) precomputed as an exact sparse
+    matrix (coloured simultaneous unit loads; default) against the m-substep recursion
+    in every CG iteration (the reference's apply_h_pd): the same multipliers and states
+    within the CG tolerance, the same iteration counts within one."""
+    out = {}
+    for mode in ("precompute", "recursion"):
+        g = load_golden(name)
+        c = cf.get(g["meta"]["scenario"])
+        c["run"]["interface"] = "matrix_free"
+        c["run"]["interface_h_pd"] = mode
+        s = MtsSolver(c)
+        s.initialize()
+        reps = s.macro_step(g["meta"]["steps"])
+        out[mode] = (s.lam(), s.state("pd")[0], [r["interface_iterations"] for r in reps])
+    (la, ua, ia), (lb, ub, ib) = out["precompute"], out["recursion"]
+    assert _rel(la, lb) <= 1e-9 and _rel(ua, ub) <= 1e-9
+    assert all(abs(x - y) <= 1 for x, y in zip(ia, ib))
