@@ -123,14 +123,25 @@ def _ncu_traffic(kernel: str, workload: str = ""):
     return None
 
 
-def run_reference_cpu(steps: int, warmup: int, threads: int | None = None) -> dict:
-    """The reference's own loop (ref_driver) on the bounded cfg3 sample."""
+REF_DESC = {
+    "cfg3_sample": "500x200 sub-plate of cfg3 (dx 0.05 mm, delta 3.015 dx, E 72 GPa, 12 MPa "
+                   "bands, exponential kernel l=delta, scalar s_crit)",
+    "cfg3_native": "the full cfg3 plate, 2000x800 at dx 0.05 mm (delta 3.015 dx, E 72 GPa, 12 MPa "
+                   "bands), in the reference's own arithmetic: exponential kernel l=delta, scalar "
+                   "s_crit (it has no constant micromodulus or per-bond s0); setup outside the "
+                   "timed loop",
+}
+
+
+def run_reference_cpu(steps: int, warmup: int, threads: int | None = None,
+                      name: str = REF_SAMPLE) -> dict:
+    """The reference's own loop (ref_driver) on a cfg3 plate (the bounded sample by default)."""
     from oracle import pyoracle as po
     from paper_2403_03605_b200 import configs as cf
 
     threads = threads or os.cpu_count() or 1
     env = dict(os.environ, PERIMTS_WORKERS=str(threads))
-    sc = cf.get(REF_SAMPLE)
+    sc = cf.get(name)
     with tempfile.TemporaryDirectory() as tmp:
         if os.path.exists(po.REF_DRIVER):
             r = po.run_ref(cf.render_cfg(sc), tmp, steps=steps + warmup, dump=False,
@@ -157,9 +168,8 @@ def run_reference_cpu(steps: int, warmup: int, threads: int | None = None) -> di
             kind, threads = "port", 1
     r["kind"] = kind
     r["threads"] = threads
-    r["sample"] = (f"{REF_SAMPLE}: 500x200 sub-plate of cfg3 (dx 0.05 mm, delta 3.015 dx, "
-                   f"E 72 GPa, 12 MPa bands, exponential kernel l=delta, scalar s_crit), "
-                   f"{steps} timed fine steps after {warmup}, {r['bonds']} bonds")
+    r["sample"] = (f"{name}: {REF_DESC[name]}, {steps} timed fine steps after {warmup}, "
+                   f"{r['bonds']} bonds")
     return r
 
 
@@ -250,14 +260,16 @@ def bench_reference(args):
     if rank != 0:
         return
     fine = args.steps * REF_FINE_PER_STEP
-    r = run_reference_cpu(fine, max(args.warmup, 1) * REF_FINE_PER_STEP)
+    r = run_reference_cpu(fine, max(args.warmup, 1) * REF_FINE_PER_STEP, name=args.ref_workload)
     v = r["bond_updates_per_s"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * r["loop_s"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3 (BASELINE configs[2]) bounded CPU sample",
+        "config": {"workload": ("cfg3 (BASELINE configs[2]) at full size in the reference's "
+                                "arithmetic" if args.ref_workload == "cfg3_native" else
+                                "cfg3 (BASELINE configs[2]) bounded CPU sample"),
                    "sample": r["sample"], "fine_steps_per_step": REF_FINE_PER_STEP},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                          "sample": r["sample"]},
@@ -463,6 +475,56 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
                            "in one copy; final state D2H"}
         except Exception as ex:  # pragma: no cover - reported, never silent
             e2e = {"value": None, "unit": UNIT, "error": repr(ex)}
+    # the late regime of the BASELINE run (cfg3: cracks start near step 700, so the
+    # default window W+1..W+K is the cold-tile screen's best case): steps 1001..1000+K2
+    # after fast-forwarding a fresh handle, with the fraction of tiles the screen let
+    # through; and the end-to-end number over 1000 steps (state copies amortised)
+    late = steady = None
+    if full and slab is None and sc.dim == 2:
+        try:
+            import torch
+
+            del s
+            K2 = 200
+            s = PDSolver.from_scenario(sc, mode=mode, device=local).find_pe_pairs()
+            s.initial_acceleration(sc.load_scale(0.0))
+            s.step(sc.scales(1, 1000))
+            s.set_option(capi.OPT_COUNT_HOT, 1)
+            ms_l = s.step_timed(sc.scales(1001, K2))
+            inf = s.info()
+            late = {"steps": f"1001..{1000 + K2}", "value": B * K2 / (ms_l * 1e-3), "unit": UNIT,
+                    "ms_per_step": ms_l / K2, "broken_total": s.broken_total(),
+                    "hot_tile_fraction": inf["hot_tiles"] / max(inf["tested_tiles"], 1),
+                    "note": "fresh handle fast-forwarded through steps 1..1000; hot tiles = "
+                            "tiles whose break test the cold-tile screen could not skip"}
+            if K < 1000:
+                del s
+                s = fresh()
+                nd = s.n_dof
+                hu = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+                hv = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+                ha = torch.empty(nd, dtype=torch.float64, pin_memory=True).numpy()
+                u0, v0, a0 = s.state()
+                hu[:], hv[:], ha[:] = u0, v0, a0
+                K3 = 1000
+                tracked = np.array([sc.dim * (s.n_nodes // 2) + 1], dtype=np.int32)
+                trk = torch.empty((K3, 1), dtype=torch.float64, pin_memory=True).numpy()
+                nbk = torch.empty(K3, dtype=torch.int64, pin_memory=True).numpy()
+                hsc = torch.empty(K3, dtype=torch.float64, pin_memory=True).numpy()
+                hsc[:] = sc.scales(step0, K3)
+                t = time.perf_counter()
+                s.set_state(hu, hv, ha)
+                s.step_tracked(hsc, tracked, trk, nbk)
+                s.get_state_into(hu, hv, ha)
+                e3 = time.perf_counter() - t
+                steady = {"steps": K3, "value": B * K3 / e3, "unit": UNIT,
+                          "ms_per_step": 1e3 * e3 / K3,
+                          "h2d_bytes_per_step": (3 * nd * 8 + K3 * 8) / K3,
+                          "d2h_bytes_per_step": (3 * nd * 8 + K3 * 16) / K3,
+                          "note": "the e2e procedure over 1000 steps in one call: the state "
+                                  "copies amortised as in a production run"}
+        except Exception as ex:  # pragma: no cover - reported, never silent
+            late = {"error": repr(ex)}
     del s
     ws = info["device_bytes"] / 1e6
     if world == 1:
@@ -486,6 +548,10 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
         out["config"]["redundancy"] = slabs.redundancy(sc.lattice, 3, world)
     if variant:
         out["f32pos_variant"] = variant
+    if late:
+        out["late_window"] = late
+    if steady:
+        out["e2e_1000_steps"] = steady
     return out
 
 
@@ -532,8 +598,9 @@ def bench_native(args):
             "gpu_launches": r["gpu_launches"],
             "clocks": r["clocks"],
         }
-        if "f32pos_variant" in r:
-            line["f32pos_variant"] = r["f32pos_variant"]
+        for key in ("f32pos_variant", "late_window", "e2e_1000_steps"):
+            if key in r:
+                line[key] = r[key]
         if workloads:
             line["workloads"] = workloads
         if ctx.world == 1 and not args.no_mts:
@@ -570,6 +637,8 @@ def main():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--mode", default="fast", choices=["fast", "det", "f32pos"])
     ap.add_argument("--cpu-steps", type=int, default=200)
+    ap.add_argument("--ref-workload", default="cfg3_native", choices=["cfg3_native", "cfg3_sample"],
+                    help="--impl reference: the full cfg3 plate (default) or the 500x200 sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true",
                     help="skip the fp32-position variant line of the default run")
