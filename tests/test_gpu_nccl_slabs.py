@@ -114,3 +114,42 @@ def test_nccl_slabs_bitwise(tmp_path, name, steps, split, mode):
         assert int(z["nb"]) == nb1
         covered += len(z["g"])
     assert covered == sc.n_nodes and nb1 > 0
+
+
+@pytest.mark.parametrize("name", ["cfg4_small", "mini"])
+def test_halo_nccl_loopback_one_gpu(name):
+    """The NCCL halo path on one GPU: a handle in a clique of one whose lower and upper
+    'neighbour' is itself.  exchange_halo runs ncclSend/ncclRecv to self in one group
+    (the k-th send to a peer meets the k-th receive from it) -- in 3D around the pack /
+    unpack kernels of the strided ranges (one 4-row range per z node layer), in 2D on
+    the contiguous rows: afterwards each receive range holds the matching send range's
+    predictor displacement, every other row is untouched."""
+    if not gpu_available():
+        pytest.skip("needs a GPU")
+    from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200 import slabs
+    from paper_2403_03605_b200.pd import PDSolver, Scenario
+
+    sc = Scenario(cf.get(name))
+    d = sc.dim
+    slab = slabs.make_slab(sc.lattice, d, 0, 1)
+    h = slabs.solver_for_slab(sc, slab, 1).find_pe_pairs()
+    h.comm_init(PDSolver.nccl_unique_id(), 1, 0)
+    nx, ny = sc.lattice[0], sc.lattice[1]
+    layers = sc.lattice[2] + 1 if d == 3 else 1
+    NX, NYL = nx + 1, ny + 1
+    n = 4 * NX  # 4 node rows of one layer
+    send_lo, recv_lo, send_hi, recv_hi = 0, 4 * NX, 8 * NX, 12 * NX
+    h.set_halo(0, send_lo, recv_lo, n, 0, send_hi, recv_hi, n)
+    if layers > 1:
+        h.set_halo_layers(layers, NX * NYL)
+    rng = np.random.default_rng(7)
+    u = rng.normal(size=h.n_dof)
+    z = np.zeros(h.n_dof)
+    h.set_state(u, z, z)  # predictor = u exactly (v = a = 0), then the exchange
+    rd = h.get_rows(0, NX * NYL, layers, NX * NYL).reshape(layers, NYL, NX, d)
+    u4 = u.reshape(layers, NYL, NX, d)
+    exp = u4.copy()
+    exp[:, 4:8] = u4[:, 0:4]     # recv_lo <- send_lo (loopback: first send meets first receive)
+    exp[:, 12:16] = u4[:, 8:12]  # recv_hi <- send_hi
+    assert np.array_equal(rd, exp)
