@@ -2,7 +2,8 @@
 // (/root/reference/proj/include/perimts/driver_run.hpp:160-246) with the fine
 // step -- advance_dynamic_step + update_bond_states + incremental_stiffness_update
 // (:214-236) and damage_field for the frames (:142-158) -- on the B200 through
-// include/pmts_capi.h.  Everything else is the reference's own code, called from
+// include/pmts_capi.h; and its coupled branch (:247-295) with the CoupledIntegrator
+// on the device (pmts_mts_*).  Everything else is the reference's own code, called from
 // its unmodified headers (nothing is copied): build_scenario, find_pe_pairs,
 // build_peri_elements, assemble_pd_global (M, P_ext), resolve_bcs_quiet, the
 // tracked-point sampler, the frame writer and finalize_outputs.  The artifacts it
@@ -184,6 +185,189 @@ RunArtifacts run_built_pure_pd(BuiltScenario& b, const std::string& out_dir, int
     return art;
 }
 
+// the reference's ScenarioConfig (scenario.hpp:24-62) as the C ABI's descriptors
+struct Descs {
+    pmts_scenario_desc sd{};
+    pmts_mts_desc md{};
+    std::vector<int32_t> npts;
+    std::vector<double> pts, trac, body, vel, fixed, boxes;
+};
+void box6(const BoundsBox& b, std::vector<double>& out) {
+    for (int k = 0; k < 3; ++k) out.push_back(b.lo[k]);
+    for (int k = 0; k < 3; ++k) out.push_back(b.hi[k]);
+}
+void fill_descs(const ScenarioConfig& sc, Descs& D) {
+    if (!sc.mesh_generated) throw ConfigError("b200_run: generated meshes only");
+    if (!sc.loads.pressures.empty()) throw ConfigError("b200_run: pressure loads unsupported");
+    pmts_scenario_desc& d = D.sd;
+    d.dim = sc.dim;
+    for (int k = 0; k < 3; ++k) {
+        d.lo[k] = sc.bounds.lo[k];
+        d.hi[k] = sc.bounds.hi[k];
+    }
+    d.spacing = sc.spacing;
+    d.E = sc.material.E;
+    d.nu = sc.material.nu;
+    d.rho = sc.material.rho;
+    d.formulation = sc.material.formulation == Formulation::plane_stress   ? 0
+                    : sc.material.formulation == Formulation::plane_strain ? 1
+                                                                           : 2;
+    d.delta_factor = sc.delta_factor;
+    d.l_factor = sc.l_factor;
+    d.s_crit = sc.s_crit;
+    for (const auto& n : sc.notches) {
+        D.npts.push_back(static_cast<int32_t>(n.points.size()));
+        for (const auto& p : n.points) D.pts.insert(D.pts.end(), p.begin(), p.end());
+    }
+    for (const auto& t : sc.loads.tractions) {
+        box6(t.box, D.trac);
+        D.trac.insert(D.trac.end(), t.value.begin(), t.value.end());
+    }
+    for (const auto& t : sc.loads.body_patches) {
+        box6(t.box, D.body);
+        D.body.insert(D.body.end(), t.value.begin(), t.value.end());
+    }
+    for (const auto& k : sc.loads.kinematic) {
+        if (k.fix_all) {
+            box6(k.box, D.fixed);
+        } else {
+            box6(k.box, D.vel);
+            D.vel.push_back(k.component);
+            D.vel.push_back(k.velocity);
+        }
+    }
+    d.n_notch = static_cast<int32_t>(D.npts.size());
+    d.notch_npts = D.npts.data();
+    d.notch_pts = D.pts.data();
+    d.n_traction = static_cast<int32_t>(D.trac.size() / 9);
+    d.traction = D.trac.data();
+    d.n_body_patch = static_cast<int32_t>(D.body.size() / 9);
+    d.body_patch = D.body.data();
+    for (int k = 0; k < 3; ++k) d.body_force[k] = sc.loads.body_force[k];
+    d.n_velocity_bc = static_cast<int32_t>(D.vel.size() / 8);
+    d.velocity_bc = D.vel.data();
+    d.n_fixed = static_cast<int32_t>(D.fixed.size() / 6);
+    d.fixed = D.fixed.data();
+    d.dt_pd = sc.dt_pd;
+    d.m = sc.m;
+    d.total_time = sc.total_time;
+    d.load_ramp = sc.load_ramp;
+    d.gamma = sc.pd_nm.gamma;
+    d.beta = sc.pd_nm.beta;
+    pmts_mts_desc& m = D.md;
+    m.scenario = &D.sd;
+    if (sc.region.pd_sector) throw ConfigError("b200_run: PD sectors unsupported");
+    for (const auto& b : sc.region.pd_boxes) box6(b, D.boxes);
+    m.n_pd_box = static_cast<int32_t>(sc.region.pd_boxes.size());
+    m.pd_boxes = D.boxes.data();
+    m.overlap_width_factor = sc.overlap_width_factor;
+    m.weight_kind = static_cast<int32_t>(sc.weight_kind);
+    m.gamma_fe = sc.fe_nm.gamma;
+    m.beta_fe = sc.fe_nm.beta;
+    m.interface_mode = static_cast<int32_t>(sc.interface_mode);
+    m.enforce_continuity = sc.enforce_continuity ? 1 : 0;
+    m.track_energy = sc.track_energy ? 1 : 0;
+    m.device = 0;
+}
+
+struct MtsHandle {
+    pmts_mts* h = nullptr;
+    ~MtsHandle() {
+        if (h) pmts_mts_destroy(h);
+    }
+};
+
+// run_built's coupled branch (driver_run.hpp:247-295) with the whole integrator on the
+// device (pmts_mts_*): the reference's own labels, blend weights, tracked-point sampler,
+// frame writer and finalize_outputs around it
+RunArtifacts run_built_coupled(BuiltScenario& b, const std::string& out_dir) {
+    RunArtifacts art;
+    art.mesh_hash = mesh_hash(b.mesh);
+    art.dim = b.mesh.dim;
+    art.n_nodes = b.mesh.node_count();
+    art.n_elements = b.mesh.element_count();
+    art.n_tracked = static_cast<int>(b.tracked_nodes.size());
+    if (!out_dir.empty()) std::filesystem::create_directories(out_dir);
+    const Mesh& mesh = b.mesh;
+    detail::FrameWriter frames(b, out_dir, art);
+    std::vector<int> label_field(mesh.element_count());
+    for (int e = 0; e < mesh.element_count(); ++e)
+        label_field[e] = static_cast<int>(b.labels.element_label[e]);
+
+    Descs D;
+    fill_descs(b.sc, D);
+    MtsHandle hm;
+    check(pmts_mts_create(&D.md, &hm.h));  // CoupledIntegrator ctor, mts.hpp:81-118
+    pmts_mts* h = hm.h;
+    check(pmts_mts_init(h));  // initialize_accelerations, mts.hpp:133-140
+    pmts_mts_view v{};
+    check(pmts_mts_view_get(h, &v));
+    if (v.n_nodes != mesh.node_count() || v.n_elems != mesh.element_count())
+        throw InternalError("b200_run: device mesh differs from the reference's");
+    auto dofmap = [&](const int32_t* nd, int n_dof) {
+        DofMap m;
+        m.dim = mesh.dim;
+        m.n_dof = n_dof;
+        m.node_dof.assign(nd, nd + mesh.node_count());
+        for (int n = 0; n < mesh.node_count(); ++n)
+            if (m.node_dof[n] >= 0) m.active_nodes.push_back(n);
+        return m;
+    };
+    const DofMap fe_dofs = dofmap(v.fe_node_dof, v.fe_n_dof);
+    const DofMap pd_dofs = dofmap(v.pd_node_dof, v.pd_n_dof);
+    KinematicState fe = KinematicState::zero(v.fe_n_dof), pd = KinematicState::zero(v.pd_n_dof);
+    auto pull = [&]() {
+        check(pmts_mts_get_state(h, 0, fe.disp.data(), fe.vel.data(), fe.acc.data()));
+        check(pmts_mts_get_state(h, 1, pd.disp.data(), pd.vel.data(), pd.acc.data()));
+    };
+    detail::NodalFieldSampler sampler{b, &fe_dofs, &pd_dofs};
+    std::vector<double> dmg_e(mesh.element_count()), dmg_n(mesh.node_count());
+    auto fields = [&]() {
+        VtkFields f;
+        sampler.fill(&fe, &pd, f);
+        f.subdomain_label = label_field;
+        f.alpha = b.alpha_elem;
+        check(pmts_mts_damage(h, dmg_e.data(), dmg_n.data()));  // damage_field on the device
+        f.damage = dmg_e;
+        f.damage_avg = dmg_n;
+        return f;
+    };
+    auto record = [&](double t) {
+        art.tracked_times.push_back(t);
+        art.tracked_values.push_back(sampler.tracked_row(&fe, &pd));
+    };
+    pull();
+    record(0.0);
+    if (frames.due(0.0)) frames.emit(0.0, fields());
+    const int n_macro = static_cast<int>(std::llround(b.sc.total_time / b.sc.dt_fe()));
+    for (int i = 1; i <= n_macro; ++i) {
+        pmts_mts_report r{};
+        check(pmts_mts_macro_step(h, 1, &r));  // macro_step, mts.hpp:244-306
+        const double t = i * b.sc.dt_fe();
+        TimingRecord tr;
+        tr.t_kinematic = r.t_kinematic;
+        tr.t_update = r.t_update;
+        tr.t_lambda = r.t_lambda;
+        tr.t_unit = r.t_unit;
+        art.timing.push_back(tr);
+        EnergyRecord er;
+        er.quad_fe = r.quad_fe;
+        er.quad_pd = r.quad_pd;
+        er.lambda_fe = r.lambda_fe;
+        er.lambda_pd = r.lambda_pd;
+        art.energy.push_back(er);
+        art.continuity.push_back(r.continuity);
+        art.broken_per_step.push_back(r.newly_broken);
+        art.broken_total += r.newly_broken;
+        pull();
+        record(t);
+        if (frames.due(t)) frames.emit(t, fields());
+    }
+    art.steps = n_macro;
+    detail::finalize_outputs(b, art, out_dir, frames.frame_index);
+    return art;
+}
+
 }  // namespace b200
 
 int main(int argc, char** argv) {
@@ -211,7 +395,9 @@ int main(int argc, char** argv) {
         }
         const ScenarioConfig sc = load_scenario(cfg);
         BuiltScenario b = build_scenario(sc);
-        const RunArtifacts art = b200::run_built_pure_pd(b, argv[2], mode, device_families);
+        const RunArtifacts art = sc.mode == RunMode::coupled_mts
+                                     ? b200::run_built_coupled(b, argv[2])
+                                     : b200::run_built_pure_pd(b, argv[2], mode, device_families);
         std::printf("{\"steps\": %d, \"broken\": %lld, \"frames\": %zu}\n", art.steps,
                     art.broken_total, art.frame_times.size());
     } catch (const ConfigError& e) {

@@ -132,6 +132,7 @@ def test_fast_mode_tolerances(name, path):
     if ref.sum():
         agree = 1.0 - np.logical_xor(mine, ref).sum() / max(ref.sum(), 1)
         assert agree >= 0.999, agree
+        _crack_within_delta(g["pairs"], mine, ref, sc, tip=False)
 
 
 def _plate(nx, ny):
@@ -250,6 +251,19 @@ def test_step_tracked_reports_every_step(mode, name):
     assert np.array_equal(u1, u2) and np.array_equal(v1, v2) and np.array_equal(a1, a2)
 
 
+def _crack_within_delta(pairs, mine, ref, sc, tip):
+    """North star (fast mode after cracking): the damage path within one horizon of the
+    oracle's -- Hausdorff distance of the broken-bond midpoints, and the tip (largest x)
+    of a crack growing from a left-edge notch."""
+    from crack import broken_midpoints, crack_tip, hausdorff
+
+    mm = broken_midpoints(pairs, mine, sc.centroid)
+    mr = broken_midpoints(pairs, ref, sc.centroid)
+    assert hausdorff(mm, mr) <= sc.delta
+    if tip:
+        assert np.linalg.norm(crack_tip(mm) - crack_tip(mr)) <= sc.delta
+
+
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
 def test_cfg4_small_impact_3d(mode):
     """BASELINE cfg4 physics at 20x20x10 (3D hex8, constant micromodulus, seeded
@@ -295,6 +309,7 @@ def test_cfg4_small_impact_3d(mode):
         mine, ref = s.intact() == 0, o.mu() == 0
         if ref.sum():
             assert 1.0 - np.logical_xor(mine, ref).sum() / ref.sum() >= 0.999
+            _crack_within_delta(pairs, mine, ref, sc, tip=False)
 
 
 @pytest.mark.parametrize("name,steps", [("cfg4_small", 100), ("cfg5_core_small", 200),
@@ -363,6 +378,7 @@ def test_cfg5_core_small_notched_3d(mode):
         mine, ref = s.intact() == 0, o.mu() == 0
         if ref.sum():
             assert 1.0 - np.logical_xor(mine, ref).sum() / ref.sum() >= 0.999
+            _crack_within_delta(pairs, mine, ref, sc, tip=True)
 
 
 # ----- known-answer tests on the device (test_perifem.cpp) ------------------

@@ -28,6 +28,13 @@ def _json(cmd):
 
 def _cfg(name):
     c = cf.get(name)
+    if name == "mts_mini_frac":
+        c["output"].update(interval=6e-7, tracked1=[0.015, 0.005], tracked2=[0.029, 0.009])
+        return c
+    if name == "mts_bar3d":
+        c["output"].update(interval=2e-7, tracked1=[0.006, 0.002, 0.002],
+                           tracked2=[0.0115, 0.002, 0.002])
+        return c
     if name == "mini":
         c["output"].update(interval=1e-6, tracked1=[0.02, 0.008], tracked2=[0.039, 0.015])
     else:  # the BASELINE cfg1 analog: 1000 steps, frames every 250
@@ -67,3 +74,24 @@ def test_shim_run_scored_by_reference_compare(name, mode, fam):
         assert abs(mine["broken"] - ref["broken"]) <= 1e-3 * max(ref["broken"], 1)
         assert rep["min_damage_agreement"] >= 0.999
         assert max(rep["tracked_error_pct"]) <= 1e-4
+
+
+@pytest.mark.gpu
+@need
+@pytest.mark.parametrize("name", ["mts_mini_frac", "mts_bar3d"])
+def test_shim_coupled_run_scored_by_reference_compare(name):
+    """run_built's coupled branch with the CoupledIntegrator on the device: scored by the
+    reference's compare_runs against the reference's own coupled run."""
+    with tempfile.TemporaryDirectory() as tmp:
+        cfgp = os.path.join(tmp, "s.cfg")
+        with open(cfgp, "w") as f:
+            f.write(cf.render_cfg(_cfg(name)))
+        ref = _json([REF_ART, "run", cfgp, os.path.join(tmp, "ref")])
+        mine = _json([SHIM, cfgp, os.path.join(tmp, "dev")])
+        assert (mine["steps"], mine["frames"]) == (ref["steps"], ref["frames"])
+        rep = _json([REF_ART, "compare", os.path.join(tmp, "dev"), os.path.join(tmp, "ref")])
+    print(f"[shim {name}] broken {mine['broken']} vs ref {ref['broken']}; compare {rep}")
+    assert mine["broken"] == ref["broken"]
+    assert rep["has_damage_frames"] and rep["frames_compared"] == ref["frames"]
+    assert rep["min_damage_agreement"] == 1.0
+    assert max(rep["tracked_error_pct"]) <= 1e-6  # percent
