@@ -5,6 +5,7 @@
 // every expression rounds as the reference's does.
 // Citations: /root/reference/proj/include/perimts/.
 #include <algorithm>
+#include <climits>
 #include <vector>
 #include <stdexcept>
 #include <string>
@@ -1427,6 +1428,73 @@ void gather_slots(int n, const int32_t* rows, const int64_t* slots, const double
     if (n <= 0) return;
     k_gather_slots<<<blocks(n), kT, 0, s>>>(n, rows, slots, g, dst);
     check("gather_slots");
+}
+
+
+// ---- H = H_FE + H_PD as one CSR (the sparse interface operator): per row the
+// union of the two sorted column lists, values summed where both have the entry ----
+namespace {
+__global__ void k_merge_count(int n, const int32_t* arp, const int32_t* aci, const int32_t* brp,
+                              const int32_t* bci, int* cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) {
+        cnt[n] = 0;
+        return;
+    }
+    int i = arp[r], j = brp[r], c = 0;
+    const int ie = arp[r + 1], je = brp[r + 1];
+    while (i < ie || j < je) {
+        const int x = i < ie ? aci[i] : INT_MAX, y = j < je ? bci[j] : INT_MAX;
+        i += x <= y;
+        j += y <= x;
+        ++c;
+    }
+    cnt[r] = c;
+}
+__global__ void k_merge_fill(int n, const int32_t* arp, const int32_t* aci, const double* av,
+                             const int32_t* brp, const int32_t* bci, const double* bv,
+                             const int32_t* rp, int32_t* ci, double* v) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int i = arp[r], j = brp[r], q = rp[r];
+    const int ie = arp[r + 1], je = brp[r + 1];
+    while (i < ie || j < je) {
+        const int x = i < ie ? aci[i] : INT_MAX, y = j < je ? bci[j] : INT_MAX;
+        double val;
+        if (x < y) val = av[i++];
+        else if (y < x) val = bv[j++];
+        else val = av[i++] + bv[j++];
+        ci[q] = x < y ? x : y;
+        v[q] = val;
+        ++q;
+    }
+}
+__global__ void k_csr_diag(int n, const int32_t* rp, const int32_t* ci, const double* v,
+                           double* d) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double x = 0.0;
+    for (int q = rp[r]; q < rp[r + 1]; ++q)
+        if (ci[q] == r) x = v[q];
+    d[r] = x > 0.0 ? x : 0.0;
+}
+}  // namespace
+void merge_count(int n, const int32_t* arp, const int32_t* aci, const int32_t* brp,
+                 const int32_t* bci, int* cnt, cudaStream_t s) {
+    k_merge_count<<<blocks(n + 1), kT, 0, s>>>(n, arp, aci, brp, bci, cnt);
+    check("merge_count");
+}
+void merge_fill(int n, const int32_t* arp, const int32_t* aci, const double* av, const int32_t* brp,
+                const int32_t* bci, const double* bv, const int32_t* rp, int32_t* ci, double* v,
+                cudaStream_t s) {
+    k_merge_fill<<<blocks(n), kT, 0, s>>>(n, arp, aci, av, brp, bci, bv, rp, ci, v);
+    check("merge_fill");
+}
+void csr_diag(int n, const int32_t* rp, const int32_t* ci, const double* v, double* d,
+              cudaStream_t s) {
+    k_csr_diag<<<blocks(n), kT, 0, s>>>(n, rp, ci, v, d);
+    check("csr_diag");
 }
 
 }  // namespace mtsk

@@ -124,6 +124,15 @@ int batched_partials();
 void set_ones(int n, const int32_t* idx, double* x, cudaStream_t s);
 void gather_slots(int n, const int32_t* rows, const int64_t* slots, const double* g, double* dst,
                   cudaStream_t s);
+// C = A + B for two CSR matrices with sorted rows (count, then fill into rp from the
+// exclusive scan of the counts); the diagonal of a CSR matrix (non-positive -> 0)
+void merge_count(int n, const int32_t* arp, const int32_t* aci, const int32_t* brp,
+                 const int32_t* bci, int* cnt, cudaStream_t s);
+void merge_fill(int n, const int32_t* arp, const int32_t* aci, const double* av, const int32_t* brp,
+                const int32_t* bci, const double* bv, const int32_t* rp, int32_t* ci, double* v,
+                cudaStream_t s);
+void csr_diag(int n, const int32_t* rp, const int32_t* ci, const double* v, double* d,
+              cudaStream_t s);
 
 }  // namespace mtsk
 }  // namespace pmts

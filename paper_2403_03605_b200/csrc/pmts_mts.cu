@@ -714,10 +714,38 @@ struct pmts_mts {
             mtsk::gather_slots((int)(c_pair[c + 1] - c_pair[c]), d_rows + c_pair[c],
                                d_slots + c_pair[c], gvec, hpd_v, stream);
         }
+        // H = H_FE + H_PD as one CSR: one sparse read per interface iteration (the two
+        // supports overlap, the union is little larger than H_PD alone); its exact
+        // diagonal is the Jacobi preconditioner when one is asked for
+        {
+            int* cnt = nullptr;
+            CKM(cudaMallocAsync(&cnt, sizeof(int) * ((size_t)nl + 1), stream));
+            mtsk::merge_count(nl, hfe_rp, hfe_ci, hpd_rp, hpd_ci, cnt, stream);
+            std::vector<int> hc(nl + 1);
+            CKM(cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * ((size_t)nl + 1),
+                                cudaMemcpyDeviceToHost, stream));
+            CKM(cudaStreamSynchronize(stream));
+            std::vector<int32_t> hrp(nl + 1, 0);
+            for (int r = 0; r < nl; ++r) hrp[r + 1] = hrp[r] + hc[r];
+            h_nnz = hrp[nl];
+            h_rp = upload(hrp);
+            h_ci = alloc<int32_t>(std::max<int64_t>(h_nnz, 1));
+            h_v = alloc<double>(std::max<int64_t>(h_nnz, 1));
+            mtsk::merge_fill(nl, hfe_rp, hfe_ci, hfe_v, hpd_rp, hpd_ci, hpd_v, h_rp, h_ci, h_v,
+                             stream);
+            CKM(cudaFreeAsync(cnt, stream));
+            if (interface_precond) {
+                h_jac = alloc<double>(nl);
+                mtsk::csr_diag(nl, h_rp, h_ci, h_v, h_jac, stream);
+            }
+        }
         CKM(cudaStreamSynchronize(stream));
         hpd_valid = true;
         invalidate_cg_graphs();
     }
+    int32_t *h_rp = nullptr, *h_ci = nullptr;  // H = H_FE + H_PD (CSR)
+    double *h_v = nullptr, *h_jac = nullptr;
+    int64_t h_nnz = 0;
 
     void initialize_accelerations() {
         // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
@@ -747,21 +775,25 @@ struct pmts_mts {
         }
         CKM(cudaMemcpyAsync(lam_d, lamp_d, sizeof(double) * nl, cudaMemcpyDeviceToDevice, stream));
         const int max_iter = std::max(200, 10 * int(std::sqrt(double(nl))));
-        cg(nl,
-           [&](const double* in, double* out) {
-               fork(ev_fork2);
-               {
-                   OnStream2 on(this);
-                   mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
-               }
-               if (hpd_valid)  // the precomputed G_PD vel(Y_PD) (exact sparse)
-                   mtsk::csr_spmv_warp(nl, hpd_rp, hpd_ci, hpd_v, in, iface_tmp, stream);
-               else  // the m-substep recursion on the current k_sync
+        if (hpd_valid)  // H = H_FE + H_PD precomputed (exact sparse): one SpMV
+            cg(nl,
+               [&](const double* in, double* out) {
+                   mtsk::csr_spmv_warp(nl, h_rp, h_ci, h_v, in, out, stream);
+               },
+               b, lam_d, interface_cg_tol, max_iter, h_jac ? h_jac : iface_jac, CG_IFACE);
+        else  // H_FE w next to the m-substep recursion on the current k_sync
+            cg(nl,
+               [&](const double* in, double* out) {
+                   fork(ev_fork2);
+                   {
+                       OnStream2 on(this);
+                       mtsk::csr_spmv_warp(nl, hfe_rp, hfe_ci, hfe_v, in, out, stream);
+                   }
                    apply_h_pd(in, iface_tmp);
-               join(ev_join2);
-               mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
-           },
-           b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
+                   join(ev_join2);
+                   mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
+               },
+               b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
         try {
             *iterations = cg_result(CG_IFACE);
         } catch (const SolverError&) {
