@@ -1497,5 +1497,114 @@ void csr_diag(int n, const int32_t* rp, const int32_t* ci, const double* v, doub
     check("csr_diag");
 }
 
+
+// ---- fused CG stages (bitwise the separate kernels they replace) ----
+namespace {
+// the implicit FE operator in one pass: y = cf ? x : M x + bdt2 (K x) (k_csr + k_apply_a)
+__global__ void k_csr_apply_a(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                              const double* __restrict__ v, const double* __restrict__ x,
+                              const double* M, const uint8_t* cf, double bdt2, double* y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) s += v[p] * x[ci[p]];
+    y[i] = cf[i] ? x[i] : M[i] * x[i] + bdt2 * s;
+}
+// x += alpha p; r -= alpha ap; z = precond(r) for the elements of this thread, then
+// r.z and r.r over them -- the grid and per-thread order of k_dot_fin, so the sums
+// are bitwise its sums over the updated vectors -- and in the last block: beta =
+// rz_new / rz, rz <- rz_new, rr, and the loop test of k_cg_cond (WHILE condition)
+__global__ void __launch_bounds__(kT) k_cg_update_dots(
+    int n, const double* alpha_dev, const double* p, const double* ap, double* x, double* r,
+    const double* jac, double* z, double* part, unsigned* ticket, double* s_rzn, double* s_rr,
+    double* s_rz, double* s_beta, const double* s_bb, const double* s_pap, double tol,
+    int max_iter, int* it_status, cudaGraphConditionalHandle h) {
+    __shared__ double sh[kT], sh2[kT];
+    __shared__ bool last;
+    const int nb = gridDim.x;
+    const double al = *alpha_dev;
+    double sacc = 0.0, sacc2 = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        x[i] += al * p[i];
+        const double ri = r[i] + -al * ap[i];
+        r[i] = ri;
+        const double zi = jac ? (jac[i] != 0.0 ? ri / jac[i] : ri) : ri;
+        z[i] = zi;
+        sacc += ri * zi;
+        sacc2 += ri * ri;
+    }
+    sh[threadIdx.x] = sacc;
+    sh2[threadIdx.x] = sacc2;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sh[threadIdx.x] += sh[threadIdx.x + o];
+            sh2[threadIdx.x] += sh2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        part[nb + blockIdx.x] = sh2[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)nb - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const volatile double* vp = part;
+    double t = 0.0, t2 = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        t += vp[i];
+        t2 += vp[nb + i];
+    }
+    sh[threadIdx.x] = t;
+    sh2[threadIdx.x] = t2;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) {
+            sh[threadIdx.x] += sh[threadIdx.x + o];
+            sh2[threadIdx.x] += sh2[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *s_rzn = sh[0];
+        *s_rr = sh2[0];
+        *s_beta = sh[0] / *s_rz;
+        *s_rz = sh[0];
+        *ticket = 0u;
+        // k_cg_cond
+        const int it = ++it_status[0];
+        bool more = false;
+        if (*s_pap <= 0.0) {
+            it_status[1] = 1;
+        } else {
+            more = sqrt(sh2[0]) / sqrt(*s_bb) > tol;
+            if (more && it >= max_iter) {
+                it_status[1] = 2;
+                more = false;
+            }
+        }
+        cudaGraphSetConditional(h, more ? 1u : 0u);
+    }
+}
+}  // namespace
+void csr_apply_a(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                 const double* M, const uint8_t* cf, double bdt2, double* y, cudaStream_t s) {
+    k_csr_apply_a<<<blocks(n), kT, 0, s>>>(n, rp, ci, v, x, M, cf, bdt2, y);
+    check("csr_apply_a");
+}
+void cg_update_dots(int n, const double* alpha_dev, const double* p, const double* ap, double* x,
+                    double* r, const double* jac, double* z, double* part, unsigned* ticket,
+                    double* s_rzn, double* s_rr, double* s_rz, double* s_beta, const double* s_bb,
+                    const double* s_pap, double tol, int max_iter, int* it_status,
+                    cudaGraphConditionalHandle h, cudaStream_t s) {
+    k_cg_update_dots<<<dot_partials(), kT, 0, s>>>(n, alpha_dev, p, ap, x, r, jac, z, part, ticket,
+                                                   s_rzn, s_rr, s_rz, s_beta, s_bb, s_pap, tol,
+                                                   max_iter, it_status, h);
+    check("cg_update_dots");
+}
+
 }  // namespace mtsk
 }  // namespace pmts

@@ -133,6 +133,16 @@ void merge_fill(int n, const int32_t* arp, const int32_t* aci, const double* av,
                 cudaStream_t s);
 void csr_diag(int n, const int32_t* rp, const int32_t* ci, const double* v, double* d,
               cudaStream_t s);
+// fused CG stages: the implicit FE operator in one pass; the update + preconditioner +
+// r.z / r.r + beta + the loop test (bitwise k_cg_update_precond, k_dot_fin mode 2 and
+// k_cg_cond in sequence)
+void csr_apply_a(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                 const double* M, const uint8_t* cf, double bdt2, double* y, cudaStream_t s);
+void cg_update_dots(int n, const double* alpha_dev, const double* p, const double* ap, double* x,
+                    double* r, const double* jac, double* z, double* part, unsigned* ticket,
+                    double* s_rzn, double* s_rr, double* s_rz, double* s_beta, const double* s_bb,
+                    const double* s_pap, double tol, int max_iter, int* it_status,
+                    cudaGraphConditionalHandle h, cudaStream_t s);
 
 }  // namespace mtsk
 }  // namespace pmts

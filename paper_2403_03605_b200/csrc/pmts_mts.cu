@@ -277,12 +277,15 @@ struct pmts_mts {
         int* st = cg_status + 2 * slot;
         // fused iteration: p.Ap and alpha in one launch, the update with the
         // preconditioner, r.z, r.r, beta and rz <- rz_new in one launch
+        // (the update, r.z, r.r, beta and the loop test in one launch; the WHILE
+        // condition is set there, the body ends with p = z + beta p)
+        cudaGraphConditionalHandle hnd_body{};
         auto body = [&] {
             op(p, ap);
             mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
                           s_alpha, stream);
-            mtsk::cg_update_precond(n, s_alpha, p, ap, x, r, jac, z, stream);
-            mtsk::dot_fin(n, r, z, r, r, part2, ticket, s_rzn, s_rr, 2, s_rz, s_beta, stream);
+            mtsk::cg_update_dots(n, s_alpha, p, ap, x, r, jac, z, part2, ticket, s_rzn, s_rr, s_rz,
+                                 s_beta, s_bb, s_pap, tol, max_iter, st, hnd_body, stream);
             mtsk::xpby(n, z, s_beta, p, stream);
         };
         cudaGraphExec_t& gl = cg_loop[slot];
@@ -324,8 +327,8 @@ struct pmts_mts {
             cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
             CKM(cudaStreamBeginCaptureToGraph(stream, bodyg, nullptr, nullptr, 0,
                                               cudaStreamCaptureModeThreadLocal));
+            hnd_body = hnd;
             body();
-            mtsk::cg_cond(hnd, s_bb, s_rr, s_pap, tol, max_iter, st, stream);
             CKM(cudaStreamEndCapture(stream, &bodyg));
             CKM(cudaGraphInstantiate(&gl, g, 0));
             cudaGraphDestroy(g);
@@ -400,9 +403,8 @@ struct pmts_mts {
         }
         const double bdt2 = fe_nm.bdt2;
         cg(nf,
-           [&](const double* x, double* y) {
-               fe_K(x, cg_kx);
-               mtsk::apply_a(nf, x, cg_kx, fe_M, fe_cf, bdt2, y, stream);
+           [&](const double* x, double* y) {  // M + bdt2 K in one pass
+               mtsk::csr_apply_a(nf, fe_rp, fe_ci, fe_v, x, fe_M, fe_cf, bdt2, y, stream);
            },
            cg_b, cg_x, cg_tol, fe_cg_max, fe_jac, slot);
         mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
