@@ -1606,5 +1606,97 @@ void cg_update_dots(int n, const double* alpha_dev, const double* p, const doubl
     check("cg_update_dots");
 }
 
+
+// ---- the CG operator fused with p.Ap and alpha = rz / pAp (last-block reduction over
+// the row blocks' partials, in block order) ----
+namespace {
+__device__ __forceinline__ void pap_finish(double mine, double* part, unsigned* ticket,
+                                           double* s_pap, const double* s_rz, double* s_alpha) {
+    __shared__ double sh[kT];
+    __shared__ bool last;
+    const int nb = gridDim.x;
+    sh[threadIdx.x] = mine;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = sh[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == (unsigned)nb - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const volatile double* vp = part;
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) t += vp[i];
+    sh[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = kT / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *s_pap = sh[0];
+        *s_alpha = *s_rz / sh[0];
+        *ticket = 0u;
+    }
+}
+__global__ void __launch_bounds__(kT) k_csr_apply_a_pap(
+    int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+    const double* __restrict__ v, const double* __restrict__ x, const double* M, const uint8_t* cf,
+    double bdt2, double* y, double* part, unsigned* ticket, double* s_pap, const double* s_rz,
+    double* s_alpha) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double mine = 0.0;
+    if (i < n) {
+        double s = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) s += v[p] * x[ci[p]];
+        const double yi = cf[i] ? x[i] : M[i] * x[i] + bdt2 * s;
+        y[i] = yi;
+        mine = x[i] * yi;
+    }
+    pap_finish(mine, part, ticket, s_pap, s_rz, s_alpha);
+}
+// y = A x (one warp per row), p.Ap, alpha
+__global__ void __launch_bounds__(kT) k_csr_warp_pap(
+    int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+    const double* __restrict__ v, const double* __restrict__ x, double* __restrict__ y,
+    double* part, unsigned* ticket, double* s_pap, const double* s_rz, double* s_alpha) {
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    double mine = 0.0;
+    if (row < n) {
+        double s = 0.0;
+        for (int p = rp[row] + lane; p < rp[row + 1]; p += 32) s += v[p] * x[ci[p]];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            y[row] = s;
+            mine = x[row] * s;
+        }
+    }
+    pap_finish(mine, part, ticket, s_pap, s_rz, s_alpha);
+}
+}  // namespace
+int pap_partials(int n, bool warp_rows) {
+    return warp_rows ? blocks((long long)n * 32) : blocks(n);
+}
+void csr_apply_a_pap(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                     const double* M, const uint8_t* cf, double bdt2, double* y, double* part,
+                     unsigned* ticket, double* s_pap, const double* s_rz, double* s_alpha,
+                     cudaStream_t s) {
+    k_csr_apply_a_pap<<<blocks(n), kT, 0, s>>>(n, rp, ci, v, x, M, cf, bdt2, y, part, ticket,
+                                               s_pap, s_rz, s_alpha);
+    check("csr_apply_a_pap");
+}
+void csr_warp_pap(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                  double* y, double* part, unsigned* ticket, double* s_pap, const double* s_rz,
+                  double* s_alpha, cudaStream_t s) {
+    k_csr_warp_pap<<<blocks((long long)n * 32), kT, 0, s>>>(n, rp, ci, v, x, y, part, ticket, s_pap,
+                                                            s_rz, s_alpha);
+    check("csr_warp_pap");
+}
+
 }  // namespace mtsk
 }  // namespace pmts

@@ -143,6 +143,15 @@ void cg_update_dots(int n, const double* alpha_dev, const double* p, const doubl
                     double* s_rzn, double* s_rr, double* s_rz, double* s_beta, const double* s_bb,
                     const double* s_pap, double tol, int max_iter, int* it_status,
                     cudaGraphConditionalHandle h, cudaStream_t s);
+// the CG operator fused with p.Ap and alpha (part: pap_partials() doubles, ticket zeroed)
+int pap_partials(int n, bool warp_rows);
+void csr_apply_a_pap(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                     const double* M, const uint8_t* cf, double bdt2, double* y, double* part,
+                     unsigned* ticket, double* s_pap, const double* s_rz, double* s_alpha,
+                     cudaStream_t s);
+void csr_warp_pap(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                  double* y, double* part, unsigned* ticket, double* s_pap, const double* s_rz,
+                  double* s_alpha, cudaStream_t s);
 
 }  // namespace mtsk
 }  // namespace pmts

@@ -148,6 +148,8 @@ struct pmts_mts {
     double *part = nullptr, *scal = nullptr;                               // reductions
     double* part2 = nullptr;      // fused CG dots: two partial rows
     unsigned* ticket = nullptr;   // their last-block counter
+    double* part3 = nullptr;      // operator-fused p.Ap partials (one per row block)
+    unsigned* ticket3 = nullptr;
     int32_t* famT_col = nullptr;  // entry-major families (PMTS_MTS_NO_TRANSPOSE=1: none)
     double* famT_coef = nullptr;
     double* famT_xi = nullptr;
@@ -264,9 +266,11 @@ struct pmts_mts {
     // graph bakes in every pointer the iteration and the operator touch: it is rebuilt
     // when one of its inputs changes or the operator's buffers are reallocated
     // (invalidate_cg_graphs).
-    template <class Op>
-    void cg(int n, Op&& op, const double* b, double* x, double tol, int max_iter, const double* jac,
-            int slot) {
+    // opdot(p, ap, s_pap, s_rz, s_alpha): the operator fused with p.Ap and alpha = rz / pAp;
+    // returns false where the operator has no fused form (op, then the separate dot)
+    template <class Op, class OpDot>
+    void cg(int n, Op&& op, OpDot&& opdot, const double* b, double* x, double tol, int max_iter,
+            const double* jac, int slot) {
         double* r = cg_r;
         double* z = cg_z;
         double* p = cg_p;
@@ -281,9 +285,11 @@ struct pmts_mts {
         // condition is set there, the body ends with p = z + beta p)
         cudaGraphConditionalHandle hnd_body{};
         auto body = [&] {
-            op(p, ap);
-            mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
-                          s_alpha, stream);
+            if (!opdot(p, ap, s_pap, s_rz, s_alpha)) {
+                op(p, ap);
+                mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
+                              s_alpha, stream);
+            }
             mtsk::cg_update_dots(n, s_alpha, p, ap, x, r, jac, z, part2, ticket, s_rzn, s_rr, s_rz,
                                  s_beta, s_bb, s_pap, tol, max_iter, st, hnd_body, stream);
             mtsk::xpby(n, z, s_beta, p, stream);
@@ -405,6 +411,11 @@ struct pmts_mts {
         cg(nf,
            [&](const double* x, double* y) {  // M + bdt2 K in one pass
                mtsk::csr_apply_a(nf, fe_rp, fe_ci, fe_v, x, fe_M, fe_cf, bdt2, y, stream);
+           },
+           [&](const double* pp, double* y, double* s_pap, const double* s_rz, double* s_alpha) {
+               mtsk::csr_apply_a_pap(nf, fe_rp, fe_ci, fe_v, pp, fe_M, fe_cf, bdt2, y, part3,
+                                     ticket3, s_pap, s_rz, s_alpha, stream);
+               return true;
            },
            cg_b, cg_x, cg_tol, fe_cg_max, fe_jac, slot);
         mtsk::zero_constrained(nf, fe_cf, cg_x, stream);
@@ -782,6 +793,11 @@ struct pmts_mts {
                [&](const double* in, double* out) {
                    mtsk::csr_spmv_warp(nl, h_rp, h_ci, h_v, in, out, stream);
                },
+               [&](const double* pp, double* y, double* s_pap, const double* s_rz, double* s_alpha) {
+                   mtsk::csr_warp_pap(nl, h_rp, h_ci, h_v, pp, y, part3, ticket3, s_pap, s_rz,
+                                      s_alpha, stream);
+                   return true;
+               },
                b, lam_d, interface_cg_tol, max_iter, h_jac ? h_jac : iface_jac, CG_IFACE);
         else  // H_FE w next to the m-substep recursion on the current k_sync
             cg(nl,
@@ -795,6 +811,7 @@ struct pmts_mts {
                    join(ev_join2);
                    mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
                },
+               [](const double*, double*, double*, const double*, double*) { return false; },
                b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
         try {
             *iterations = cg_result(CG_IFACE);
@@ -1369,6 +1386,10 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             *p = h->alloc<double>(nmax);
         h->part = h->alloc<double>(mtsk::dot_partials());
         h->part2 = h->alloc<double>(2 * mtsk::dot_partials());
+        h->part3 = h->alloc<double>(std::max(mtsk::pap_partials(nmax, false),
+                                             mtsk::pap_partials(h->nl, true)));
+        h->ticket3 = reinterpret_cast<unsigned*>(h->alloc<double>(1));
+        CKM(cudaMemsetAsync(h->ticket3, 0, sizeof(double), h->stream));
         h->ticket = reinterpret_cast<unsigned*>(h->alloc<double>(1));
         CKM(cudaMemsetAsync(h->ticket, 0, sizeof(double), h->stream));
         h->zero_flags(nmax);  // allocated before any CG graph capture uses it
