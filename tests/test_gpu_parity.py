@@ -655,3 +655,52 @@ def test_lattice_damage_and_intact_on_device(name, steps):
     e, n = s.damage_field()
     assert np.array_equal(e, oe) and np.array_equal(n, on)
     assert e.max() > 0
+
+
+# ----- edge cases: empty families, one element, empty batches ----------------
+
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_no_bonds_steps_like_the_oracle(mode):
+    """A horizon below the element spacing (no family has a member) and a single-element
+    mesh: the neighbour build returns no pairs, stepping runs the free Newmark update
+    under the loads, and the fields are the oracle's (bitwise in deterministic mode);
+    an empty batch of steps changes nothing."""
+    one = {"mesh.bounds": [0.0, 0.0, 1e-3, 1e-3], "mesh.notch1": None,
+           "load.traction2": [1e-3 - 1e-4, -1.0, 1e-3 + 1e-4, 1.0, 16e6, 0.0]}
+    for over in ({"pd.delta_factor": 0.4}, one):
+        c = cf.get("mini", **over)
+        sc = Scenario(c)
+        s = PDSolver.from_scenario(sc, mode=mode).find_pe_pairs()
+        assert len(s.pairs()) == 0 and s.info()["n_bonds"] == 0
+        assert len(s.intact()) == 0
+        o = po.OraclePD(dict(dim=2, n_nodes=sc.n_nodes, conn=sc.conn, centroid=sc.centroid,
+                             volume=sc.volume, pairs=np.zeros((0, 2), np.int32), mass=sc.mass,
+                             p_ext=sc.p_ext, bc_dofs=sc.bc_dofs, bc_vel=sc.bc_vel,
+                             delta=sc.delta, l=sc.l, c0=sc.c0, s_crit=sc.s_crit, dt=sc.dt),
+                        po.MF)
+        s.initial_acceleration(sc.load_scale(0.0))
+        o.init(sc.load_scale(0.0))
+        assert s.step([]) == 0
+        assert s.step(sc.scales(1, 30)) == 0
+        o.step(sc.scales(1, 30))
+        u, v, a = s.state()
+        ou, ov, oa = o.state()
+        if mode == capi.DETERMINISTIC:
+            assert np.array_equal(u, ou) and np.array_equal(v, ov) and np.array_equal(a, oa)
+        else:
+            assert np.linalg.norm(u - ou) <= 1e-12 * max(np.linalg.norm(ou), 1e-300)
+        e, _ = s.damage_field()
+        assert (e == 0).all()
+
+
+@pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
+def test_set_pairs_empty_and_break_log_empty(mode):
+    """set_pairs with an empty list (the reference's find_pe_pairs may return none) and
+    an empty break log."""
+    m = km.disjoint_quads()
+    s = _kat_solver(m, np.zeros((0, 2), np.int32), 0.1, mode)
+    z = np.zeros(16)
+    s.set_state(z, z, z)
+    assert s.step([0.0, 0.0]) == 0
+    if mode == capi.DETERMINISTIC:  # (the (step, i, j) log is a deterministic-mode record)
+        assert len(s.break_log(10)) == 0
