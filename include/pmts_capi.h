@@ -268,6 +268,24 @@ enum pmts_option {
     PMTS_OPT_COUNT_HOT = 3,      /* 1: count hot / tested tiles (pmts_pd_info) */
 };
 int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value);
+
+/* ------------------------------------------------------------------------
+ * Coupled-integrator hooks (deterministic mode): the PD side of a
+ * reference CoupledIntegrator (mts.hpp:79-535) that keeps its own FE side.
+ * ------------------------------------------------------------------------ */
+/* G_PD^T S_j of free_solve_pd (mts.hpp:160-162): vals at dofs added to P * load_scale in
+ * every following step (and pmts_pd_init) until replaced; n = 0 clears it */
+int pmts_pd_set_constraint_load(pmts_pd* h, int32_t n, const int32_t* dofs, const double* vals);
+/* k_sync_ = the live bond states (mts.hpp:98, 252): the mask the recursion uses */
+int pmts_pd_snapshot_bonds(pmts_pd* h);
+/* the m homogeneous linear substeps from rest on k_sync_ (unit_pd_column / apply_h_pd /
+ * recombine, mts.hpp:230-238, 398-420): load w[r] j / m at dofs[r] in substep j.
+ * vel_out (nullable, (m + 1) x n rows): the velocities at the dofs after each substep
+ * (row 0 = 0); u/v/a_out (nullable, n_dof): the final state y_m.  The handle's own
+ * state is untouched. */
+int pmts_pd_homogeneous_recursion(pmts_pd* h, int32_t m, int32_t n, const int32_t* dofs,
+                                  const double* w, double* vel_out, double* u_out, double* v_out,
+                                  double* a_out);
 /* sum of an int64 over the clique (broken counts at output cadence) */
 int pmts_pd_allreduce_sum(pmts_pd* h, int64_t* value);
 

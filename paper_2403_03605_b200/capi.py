@@ -138,6 +138,9 @@ SIGNATURES = {
     "pmts_pd_set_rows_layers": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "pmts_pd_set_halo_layers": (C.c_int, [_P, _I, _I]),
     "pmts_pd_set_option": (C.c_int, [_P, _I, _I]),
+    "pmts_pd_set_constraint_load": (C.c_int, [_P, _I, _P, _P]),
+    "pmts_pd_snapshot_bonds": (C.c_int, [_P]),
+    "pmts_pd_homogeneous_recursion": (C.c_int, [_P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "pmts_pd_set_rows": (C.c_int, [_P, _I, _I, _P]),
     "pmts_nccl_unique_id": (C.c_int, [_P]),
     "pmts_pd_comm_init": (C.c_int, [_P, _P, _I, _I]),

@@ -42,6 +42,7 @@ struct DevPD {
     int own_lo, own_hi;  // owned local element range (broken counts, break log); with
                          // id_pl the in-layer range of l mod id_pl
     int id_pl;           // 3D slabs cut along y: local elements per z layer (0: contiguous)
+    const double* extra;  // per dof: constraint load added to P * scale (coupled hooks; null: none)
     long long id_pg;     // ... and global elements per z layer
     // Newmark coefficients, each rounded exactly as the reference's expression
     double c_pred_v;  // dt*(1-gamma)              newmark.hpp:65

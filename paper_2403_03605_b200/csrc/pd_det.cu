@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kThreads) k_node_update(DevPD d, double scale,
         const bool bc = d.bcflag[i] != 0;
         double pt = d.P[i];
         pt = pt * scale;
+        if (d.extra) pt = pt + d.extra[i];  // + G_PD^T S_j (mts.hpp:160-162)
         const double acc = bc ? 0.0 : (pt - Ku[c]) / d.M[i];
         double vel = d.rv[i] + d.c_corr_v * acc;
         const double dis = d.rd[i] + d.c_corr_d * acc;
@@ -230,7 +231,8 @@ __global__ void k_init_acc(DevPD d, double scale) {
     }
     for (int c = 0; c < DIM; ++c) {
         const size_t i = (size_t)n * DIM + c;
-        const double p = d.P[i] * scale;
+        double p = d.P[i] * scale;
+        if (d.extra) p = p + d.extra[i];
         d.a[i] = d.bcflag[i] ? 0.0 : (p - Ku[c]) / d.M[i];
     }
 }

@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include "pd_common.cuh"
+#include "pd_mts.cuh"
 #include "pd_stencil.cuh"
 
 namespace pmts {
@@ -97,6 +98,16 @@ struct pmts_pd {
     bool screen = true, halo_overlap = false;
     unsigned* lat3_tmax = nullptr;   // the 3D screen's per-tile maxima (kept when screen is off)
     unsigned long long* hot_count = nullptr;  // PMTS_OPT_COUNT_HOT: {hot, tested} tiles
+    // coupled-integrator hooks (deterministic mode): constraint load, k_sync snapshot,
+    // entry-major families and scratch of the homogeneous recursion
+    double* d_extra = nullptr;
+    uint32_t* mask_sync = nullptr;
+    int32_t* famT_col = nullptr;
+    double *famT_coef = nullptr, *famT_xi = nullptr;
+    double *rec_rd = nullptr, *rec_rv = nullptr, *rec_u = nullptr, *rec_v = nullptr,
+           *rec_a = nullptr, *rec_w = nullptr, *rec_out = nullptr;
+    int32_t* rec_row_of = nullptr;
+    int rec_rows_cap = 0, rec_m_cap = 0;
     double* rd_buf[2] = {nullptr, nullptr};
     bool tile9 = false;              // ... the one-shot TMA-staged tile kernel (default)
     int tile9_occ = 0;               // its resident CTAs per SM
@@ -1067,6 +1078,7 @@ int pmts_pd_create(const pmts_pd_desc* desc, pmts_pd** out) {
         d.seed = ds.seed;
         d.fracture = h->fracture;
         d.goff = ds.global_id_offset;
+        d.extra = nullptr;
         d.id_pl = 0;
         d.id_pg = 0;
         if (ds.slab_plane[0] != 0 || ds.slab_plane[1] != 0) {
@@ -1749,6 +1761,99 @@ int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value) {
                 throw ConfigError("unknown option " + std::to_string(option));
         }
         CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+// ---- coupled-integrator hooks: the PD side of a reference
+// CoupledIntegrator that keeps its own FE side (deterministic mode) ----
+int pmts_pd_set_constraint_load(pmts_pd* h, int32_t n, const int32_t* dofs, const double* vals) {
+    return guard([&] {
+        if (!h) throw ConfigError("null handle");
+        if (h->mode != PMTS_DETERMINISTIC)
+            throw ConfigError("constraint loads: PMTS_DETERMINISTIC handles only");
+        if (n < 0) throw ConfigError("negative count");
+        if (n == 0) {
+            h->d.extra = nullptr;
+            return;
+        }
+        if (!h->d_extra) h->d_extra = h->alloc<double>(h->ndof);
+        std::vector<double> e(h->ndof, 0.0);
+        for (int k = 0; k < n; ++k) {
+            if (dofs[k] < 0 || dofs[k] >= h->ndof) throw ConfigError("dof out of range");
+            e[dofs[k]] = vals[k];  // G_PD is Boolean: one value per coupling dof
+        }
+        upload(h->d_extra, e.data(), h->ndof, h->stream);
+        h->d.extra = h->d_extra;
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_snapshot_bonds(pmts_pd* h) {
+    return guard([&] {
+        require_families(h);
+        if (h->mode != PMTS_DETERMINISTIC) throw ConfigError("PMTS_DETERMINISTIC handles only");
+        const size_t words = (size_t)h->d.W * h->E;
+        if (!h->mask_sync) h->mask_sync = h->alloc<uint32_t>(words);
+        CK(cudaMemcpyAsync(h->mask_sync, h->d.mask, sizeof(uint32_t) * words,
+                           cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int pmts_pd_homogeneous_recursion(pmts_pd* h, int32_t m, int32_t n, const int32_t* dofs,
+                                  const double* w, double* vel_out, double* u_out, double* v_out,
+                                  double* a_out) {
+    return guard([&] {
+        require_families(h);
+        if (h->mode != PMTS_DETERMINISTIC) throw ConfigError("PMTS_DETERMINISTIC handles only");
+        if (m < 1 || n < 0) throw ConfigError("bad m / n");
+        if (!h->mask_sync) throw ConfigError("pmts_pd_snapshot_bonds first");
+        const int nd = h->ndof;
+        cudaStream_t s = h->stream;
+        if (!h->famT_col) {  // entry-major families of the linear force
+            const size_t ek = (size_t)h->E * h->d.K;
+            h->famT_col = h->alloc<int32_t>(ek);
+            h->famT_coef = h->alloc<double>(ek);
+            h->famT_xi = h->alloc<double>(ek * h->dim);
+            mtsk::family_transpose(h->d, h->famT_col, h->famT_coef, h->famT_xi, s);
+            for (double** p : {&h->rec_rd, &h->rec_rv, &h->rec_u, &h->rec_v, &h->rec_a})
+                *p = h->alloc<double>(nd);
+            h->rec_row_of = h->alloc<int32_t>(nd);
+        }
+        if (n > h->rec_rows_cap || m > h->rec_m_cap) {
+            if (h->rec_w) h->release(h->rec_w);
+            if (h->rec_out) h->release(h->rec_out);
+            h->rec_rows_cap = std::max(n, 1);
+            h->rec_m_cap = m;
+            h->rec_w = h->alloc<double>(h->rec_rows_cap);
+            h->rec_out = h->alloc<double>((size_t)(m + 1) * h->rec_rows_cap);
+        }
+        std::vector<int32_t> ro(nd, -1);
+        for (int r = 0; r < n; ++r) {
+            if (dofs[r] < 0 || dofs[r] >= nd) throw ConfigError("dof out of range");
+            ro[dofs[r]] = r;
+        }
+        upload(h->rec_row_of, ro.data(), nd, s);
+        if (n) upload(h->rec_w, w, n, s);
+        CK(cudaMemsetAsync(h->rec_out, 0, sizeof(double) * (size_t)(m + 1) * h->rec_rows_cap, s));
+        CK(cudaMemsetAsync(h->rec_rd, 0, sizeof(double) * nd, s));
+        CK(cudaMemsetAsync(h->rec_rv, 0, sizeof(double) * nd, s));
+        const DevPD& d = h->d;
+        for (int j = 1; j <= m; ++j) {
+            if (j > 1)
+                mtsk::pd_force_lin_t(d, h->famT_col, h->famT_coef, h->famT_xi, h->rec_rd,
+                                     h->mask_sync, d.ubar, s);
+            mtsk::pd_node_lin(d, j > 1 ? 1 : 0, h->rec_w, h->rec_row_of, double(j) / m, d.M,
+                              d.bcflag, d.c_corr_v, d.c_corr_d, d.dt, d.c_pred_v, d.c_pred_d,
+                              h->rec_u, h->rec_v, h->rec_a, h->rec_rd, h->rec_rv,
+                              h->rec_out + (size_t)j * h->rec_rows_cap, s);
+        }
+        for (int j = 0; vel_out && j <= m; ++j)
+            download(vel_out + (size_t)j * n, h->rec_out + (size_t)j * h->rec_rows_cap, n, s);
+        if (u_out) download(u_out, h->rec_u, nd, s);
+        if (v_out) download(v_out, h->rec_v, nd, s);
+        if (a_out) download(a_out, h->rec_a, nd, s);
+        CK(cudaStreamSynchronize(s));
     });
 }
 

@@ -393,6 +393,27 @@ class PDSolver:
         check(lib().pmts_pd_set_option(self.h, int(option), int(value)))
         return self
 
+    # -- coupled-integrator hooks (deterministic mode) ------------------------
+    def set_constraint_load(self, dofs, vals):
+        """G_PD^T S_j (mts.hpp:160-162): added to P * load_scale until replaced."""
+        d = np.ascontiguousarray(dofs, dtype=np.int32)
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        check(lib().pmts_pd_set_constraint_load(self.h, len(d), ptr(d), ptr(v)))
+
+    def snapshot_bonds(self):
+        check(lib().pmts_pd_snapshot_bonds(self.h))
+
+    def homogeneous_recursion(self, m, dofs, w, state=False):
+        """The m homogeneous linear substeps from rest on the bond snapshot
+        (mts.hpp:230-238, 398-420): velocities at dofs after each substep, (m+1) x n."""
+        d = np.ascontiguousarray(dofs, dtype=np.int32)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        vel = np.zeros((m + 1, len(d)))
+        u, v, a = (np.zeros(self.n_dof) for _ in range(3)) if state else (None, None, None)
+        check(lib().pmts_pd_homogeneous_recursion(self.h, m, len(d), ptr(d), ptr(w), ptr(vel),
+                                                  ptr(u), ptr(v), ptr(a)))
+        return (vel, (u, v, a)) if state else vel
+
     def set_halo_layers(self, layers, stride):
         check(lib().pmts_pd_set_halo_layers(self.h, layers, stride))
 
