@@ -428,12 +428,15 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
             "avg_launch_us": bond_avg_s * 1e6, "launch_timing": timing,
             "avg_launch_us_isolated": bond_ms * 1e3 / K,
             "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
-    # the bond work is fp64-arithmetic heavy: 14 flops per directed entry in fast
-    # mode (eta 2, xi.eta 3, force 4, |eta|^2 3, test 2) = 28 per unique bond
-    flops = 28.0 * (B / world) / bond_avg_s / 1e12
+    # the bond work is fp64-arithmetic heavy.  2D: 14 flops per directed entry in fast
+    # mode (eta 2, xi.eta 3, force 4, |eta|^2 3, test 2) = 28 per unique bond; 3D (the
+    # 122-offset kernel, break test screened off on cold tiles): eta 3, o.eta 3 (small-
+    # integer multiplies as adds), scale 1, force 3 = 10 per directed entry, 20 per bond
+    fpb = 28 if sc.dim == 2 else 20
+    flops = fpb * (B / world) / bond_avg_s / 1e12
     roof_fp64 = {"bound": "fp64", "achieved": flops, "peak": FP64_PEAK_TFLOPS,
                  "unit": "TFLOP/s", "frac": flops / FP64_PEAK_TFLOPS,
-                 "flops_per_bond": 28, "peak_source": "nominal B200 FP64 (no measured fp64 peak)"}
+                 "flops_per_bond": fpb, "peak_source": "nominal B200 FP64 (no measured fp64 peak)"}
 
     # end to end through the public C-ABI with host buffers
     e2e = None
@@ -575,7 +578,7 @@ def bench_native(args):
                 w = measure_pd(args, ctx, name, "strong", k, W, wmode, full=False)
                 workloads[name] = {key: w[key] for key in
                                    ("value", "unit", "ms_per_step", "steps", "warmup", "scaling",
-                                    "config", "roofline", "gpu_launches")}
+                                    "config", "roofline", "roofline_fp64", "gpu_launches")}
             except Exception as ex:  # pragma: no cover - reported, never silent
                 workloads[name] = {"error": repr(ex)}
     cpu = None
