@@ -483,6 +483,15 @@ struct pmts_mts {
     // is a CG solve whose support grows one stiffness neighbourhood per iteration, and
     // disconnected FE parts never couple -- lossless) are extracted on the device
     void build_h_fe() {
+        // (the column-major scratch is n_lambda^2 doubles: refuse what cannot fit)
+        {
+            size_t free_b = 0, total_b = 0;
+            CKM(cudaMemGetInfo(&free_b, &total_b));
+            if (sizeof(double) * (size_t)nl * nl > free_b / 2)
+                throw ConfigError("interface of " + std::to_string(nl) +
+                                  " multipliers: the H_FE unit-column scratch (n_lambda^2 "
+                                  "doubles) does not fit in device memory");
+        }
         double* D = nullptr;
         CKM(cudaMallocAsync(&D, sizeof(double) * (size_t)nl * nl, stream));
         if (fe_nm.explicit_scheme()) {
