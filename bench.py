@@ -662,6 +662,8 @@ def main():
         args.warmup = 3
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         raise SystemExit(_spawn_ranks(args))
+    if "WORLD_SIZE" in os.environ and _env_rank()[2] != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {_env_rank()[2]}")
     if args.workload == "cfg2":  # the coupled MTS metric as its own line
         rank, _, _ = _env_rank()
         if rank != 0:
