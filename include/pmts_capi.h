@@ -329,6 +329,15 @@ typedef struct {
                                     0 (default) = that operator precomputed once as an exact
                                     sparse matrix (coloured simultaneous unit loads), used until
                                     bonds break */
+    int32_t shard_world;         /* > 1: a sharded coupled run (north star item 5): this handle
+                                    is PD shard shard_rank of shard_world -- slabs of PD element
+                                    layers along the slowest lattice axis with one-horizon ghost
+                                    layers exchanged every fine substep; shard 0 also holds the
+                                    FE side; the interface solve runs on every shard.  Join the
+                                    shards with pmts_mts_group_join (one process) or
+                                    pmts_mts_comm_init (NCCL, one process per GPU), then
+                                    pmts_mts_init / pmts_mts_group_init.  0 or 1: one domain */
+    int32_t shard_rank;
 } pmts_mts_desc;
 
 typedef struct {
@@ -395,6 +404,30 @@ int pmts_mts_get_intact(pmts_mts* h, uint8_t* out);
  * the nodal averages, as in the reference's coupled frames (driver_run.hpp:143-146) */
 int pmts_mts_damage(pmts_mts* h, double* elem_out, double* node_out);
 void pmts_mts_destroy(pmts_mts* h);
+
+/* ---- sharded coupled runs (pmts_mts_desc.shard_world > 1) ---- */
+typedef struct {
+    int32_t world, rank, axis;        /* cut axis: the slowest lattice axis (1 in 2D, 2 in 3D) */
+    int32_t reach_layers, n_layers;   /* D = floor(delta / h); PD element layers along the axis */
+    int32_t n_local_nodes, n_local_elems;
+    int32_t own_elem_lo, own_elem_hi; /* the owned local elements */
+    const int32_t* local_nodes;       /* local node -> compact PD node (its PD dofs: * dim + c);
+                                         pmts_mts_get_state(1) is in this local order */
+    const int32_t* local_elems;       /* local element -> PD-active element index */
+    const uint8_t* node_owned;        /* per local node */
+    const int32_t* layer_bounds;      /* [world + 1] element-layer bounds of the shards */
+} pmts_mts_shard_view;
+int pmts_mts_shard_view_get(const pmts_mts* h, pmts_mts_shard_view* view);
+/* one process drives all shards (tests, single-node emulation): join them, then
+ * initialize and step them together -- one host thread per shard, host barriers and
+ * device copies between the shards' buffers at every exchange; reports: shard 0's */
+int pmts_mts_group_join(pmts_mts* const* handles, int32_t n);
+int pmts_mts_group_init(pmts_mts* const* handles, int32_t n);
+int pmts_mts_group_macro_step(pmts_mts* const* handles, int32_t n, int32_t steps,
+                              pmts_mts_report* reports);
+/* one process per GPU: join the NCCL clique (pmts_nccl_unique_id from shard 0); then
+ * pmts_mts_init / pmts_mts_macro_step on every rank in lockstep */
+int pmts_mts_comm_init(pmts_mts* h, const void* nccl_unique_id);
 
 #ifdef __cplusplus
 }

@@ -82,7 +82,15 @@ class MtsDesc(C.Structure):
                 ("overlap_width_factor", _D), ("weight_kind", _I), ("gamma_fe", _D),
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
                 ("track_energy", _I), ("device", _I), ("fe_spacing", _D),
-                ("interface_precond", _I), ("interface_recursion", _I)]
+                ("interface_precond", _I), ("interface_recursion", _I), ("shard_world", _I),
+                ("shard_rank", _I)]
+
+
+class MtsShardView(C.Structure):
+    _fields_ = [("world", _I), ("rank", _I), ("axis", _I), ("reach_layers", _I),
+                ("n_layers", _I), ("n_local_nodes", _I), ("n_local_elems", _I),
+                ("own_elem_lo", _I), ("own_elem_hi", _I), ("local_nodes", _P),
+                ("local_elems", _P), ("node_owned", _P), ("layer_bounds", _P)]
 
 
 class MtsView(C.Structure):
@@ -156,6 +164,11 @@ SIGNATURES = {
     "pmts_mts_get_intact": (C.c_int, [_P, _P]),
     "pmts_mts_damage": (C.c_int, [_P, _P, _P]),
     "pmts_mts_destroy": (None, [_P]),
+    "pmts_mts_shard_view_get": (C.c_int, [_P, C.POINTER(MtsShardView)]),
+    "pmts_mts_group_join": (C.c_int, [_P, _I]),
+    "pmts_mts_group_init": (C.c_int, [_P, _I]),
+    "pmts_mts_group_macro_step": (C.c_int, [_P, _I, _I, _P]),
+    "pmts_mts_comm_init": (C.c_int, [_P, _P]),
 }
 
 _lib = None

@@ -111,14 +111,32 @@ __global__ void k_init_acc(int n, const double* p, const double* ku, const doubl
     a[i] = cf[i] ? 0.0 : (p[i] - ku[i]) / M[i];
 }
 
+// idx[r] < 0: a row this shard does not own (sharded coupled run): no load; its
+// gathered value is -0.0, the identity of the owner-sum across shards (x + -0.0 == x
+// for every x, -0.0 included)
 __global__ void k_scatter_add(int n, const int32_t* idx, const double* vals, double* dst) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) dst[idx[r]] += vals[r];
+    if (r < n && idx[r] >= 0) dst[idx[r]] += vals[r];
 }
 
 __global__ void k_gather(int n, const int32_t* idx, const double* src, double* dst) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) dst[r] = src[idx[r]];
+    if (r < n) dst[r] = idx[r] >= 0 ? src[idx[r]] : -0.0;
+}
+
+__global__ void k_fill(long long n, double v, double* x) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = v;
+}
+// dst[didx[i]] = src[sidx[i]] (halo copies between shard buffers; src may be a peer's)
+__global__ void k_copy_idx(int n, const double* src, const int32_t* sidx, double* dst,
+                           const int32_t* didx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[didx[i]] = src[sidx[i]];
+}
+__global__ void k_scatter_set(int n, const int32_t* idx, const double* vals, double* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[idx[i]] = vals[i];
 }
 
 // G_FE with interpolation rows (non-matching meshes): out[r] = sum_j w_j x[ci_j],
@@ -418,7 +436,7 @@ __global__ void __launch_bounds__(kT) k_pd_force_warp(DevPD d, const double* __r
                 const double len = sqrt(len2);
                 const double sv = len <= 0.0 ? -1.0 : (len - xin) / xin;
                 brk = sv >= d.s_crit;
-                if (brk && e < p) ++nb;
+                if (brk && e < p && owns_elem(d, e)) ++nb;  // once per bond, by its owner
             }
         }
         if (do_break) {
@@ -769,6 +787,22 @@ void gather(int n, const int32_t* idx, const double* src, double* dst, cudaStrea
     k_gather<<<blocks(n), kT, 0, s>>>(n, idx, src, dst);
     check("gather");
 }
+void fill(long long n, double v, double* x, cudaStream_t s) {
+    if (n <= 0) return;
+    k_fill<<<(unsigned)((n + kT - 1) / kT), kT, 0, s>>>(n, v, x);
+    check("fill");
+}
+void copy_idx(int n, const double* src, const int32_t* sidx, double* dst, const int32_t* didx,
+              cudaStream_t s) {
+    if (n <= 0) return;
+    k_copy_idx<<<blocks(n), kT, 0, s>>>(n, src, sidx, dst, didx);
+    check("copy_idx");
+}
+void scatter_set(int n, const int32_t* idx, const double* vals, double* dst, cudaStream_t s) {
+    if (n <= 0) return;
+    k_scatter_set<<<blocks(n), kT, 0, s>>>(n, idx, vals, dst);
+    check("scatter_set");
+}
 void add(int n, const double* x, double* y, cudaStream_t s) {
     k_add<<<blocks(n), kT, 0, s>>>(n, x, y);
     check("add");
@@ -995,7 +1029,8 @@ __global__ void k_lu_solve(int n, const double* A, const int* perm, const double
 // -> x = 0, converged; else continue while sqrt(rr) / sqrt(bb) > tol (past max_iter
 // -> status 2); sets the WHILE node's condition and resets the iteration count
 __global__ void k_cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
-                           double tol, int max_iter, int* it_status, double* x, int n) {
+                           double tol, int max_iter, int* it_status, double* x, int n,
+                           int* more_out) {
     const double bb = *s_bb;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (bb == 0.0 && i < n) x[i] = 0.0;
@@ -1010,7 +1045,8 @@ __global__ void k_cg_start(cudaGraphConditionalHandle h, const double* s_bb, con
             more = false;
         }
     }
-    cudaGraphSetConditional(h, more ? 1u : 0u);
+    if (more_out) *more_out = more ? 1 : 0;  // host-driven loop (sharded coupled runs)
+    else cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
 // dense column k of a column-major n x n matrix: D[k n + r] = -x[r]  (H_FE unit columns)
@@ -1131,8 +1167,9 @@ void lu_solve(int n, const double* A, const int* perm, const double* b, double* 
     check("lu_solve");
 }
 void cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr, double tol,
-              int max_iter, int* it_status, double* x, int n, cudaStream_t s) {
-    k_cg_start<<<blocks(std::max(n, 1)), kT, 0, s>>>(h, s_bb, s_rr, tol, max_iter, it_status, x, n);
+              int max_iter, int* it_status, double* x, int n, cudaStream_t s, int* more_out) {
+    k_cg_start<<<blocks(std::max(n, 1)), kT, 0, s>>>(h, s_bb, s_rr, tol, max_iter, it_status, x, n,
+                                                     more_out);
     check("cg_start");
 }
 void col_neg(int n, int k, const double* x, double* D, cudaStream_t s) {
@@ -1518,7 +1555,7 @@ __global__ void __launch_bounds__(kT) k_cg_update_dots(
     int n, const double* alpha_dev, const double* p, const double* ap, double* x, double* r,
     const double* jac, double* z, double* part, unsigned* ticket, double* s_rzn, double* s_rr,
     double* s_rz, double* s_beta, const double* s_bb, const double* s_pap, double tol,
-    int max_iter, int* it_status, cudaGraphConditionalHandle h) {
+    int max_iter, int* it_status, cudaGraphConditionalHandle h, int* more_out) {
     __shared__ double sh[kT], sh2[kT];
     __shared__ bool last;
     const int nb = gridDim.x;
@@ -1586,7 +1623,8 @@ __global__ void __launch_bounds__(kT) k_cg_update_dots(
                 more = false;
             }
         }
-        cudaGraphSetConditional(h, more ? 1u : 0u);
+        if (more_out) *more_out = more ? 1 : 0;
+        else cudaGraphSetConditional(h, more ? 1u : 0u);
     }
 }
 }  // namespace
@@ -1599,10 +1637,10 @@ void cg_update_dots(int n, const double* alpha_dev, const double* p, const doubl
                     double* r, const double* jac, double* z, double* part, unsigned* ticket,
                     double* s_rzn, double* s_rr, double* s_rz, double* s_beta, const double* s_bb,
                     const double* s_pap, double tol, int max_iter, int* it_status,
-                    cudaGraphConditionalHandle h, cudaStream_t s) {
+                    cudaGraphConditionalHandle h, cudaStream_t s, int* more_out) {
     k_cg_update_dots<<<dot_partials(), kT, 0, s>>>(n, alpha_dev, p, ap, x, r, jac, z, part, ticket,
                                                    s_rzn, s_rr, s_rz, s_beta, s_bb, s_pap, tol,
-                                                   max_iter, it_status, h);
+                                                   max_iter, it_status, h, more_out);
     check("cg_update_dots");
 }
 

@@ -49,7 +49,13 @@ void zero_constrained(int n, const uint8_t* cf, double* x, cudaStream_t s);
 void init_acc(int n, const double* p, const double* ku, const double* M, const uint8_t* cf,
               double* a, cudaStream_t s);
 void scatter_add(int n, const int32_t* idx, const double* vals, double* dst, cudaStream_t s);
+// idx[r] < 0: no load (scatter_add) / -0.0 (gather) -- rows a shard does not own
 void gather(int n, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+void fill(long long n, double v, double* x, cudaStream_t s);
+// dst[didx[i]] = src[sidx[i]]; dst[idx[i]] = vals[i]
+void copy_idx(int n, const double* src, const int32_t* sidx, double* dst, const int32_t* didx,
+              cudaStream_t s);
+void scatter_set(int n, const int32_t* idx, const double* vals, double* dst, cudaStream_t s);
 void gather_csr(int n, const int32_t* rp, const int32_t* ci, const double* w, const double* src,
                 double* dst, cudaStream_t s);
 void scatter_csr(int nt, const int32_t* td, const int32_t* trp, const int32_t* tri,
@@ -99,8 +105,10 @@ void max_abs(int n, const double* x, const int32_t* idx, const double* y,
              unsigned long long* out, cudaStream_t s);
 void lu_factor(int n, double* A, int* perm, unsigned long long* amax, int* flag, cudaStream_t s);
 void lu_solve(int n, const double* A, const int* perm, const double* b, double* x, cudaStream_t s);
+// more_out (nullable): the loop flag for a host-driven loop instead of the WHILE condition
 void cg_start(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr, double tol,
-              int max_iter, int* it_status, double* x, int n, cudaStream_t s);
+              int max_iter, int* it_status, double* x, int n, cudaStream_t s,
+              int* more_out = nullptr);
 void col_neg(int n, int k, const double* x, double* D, cudaStream_t s);
 void add_col_gather(int n, int k, const int32_t* idx, const double* x, double* H, cudaStream_t s);
 void unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int k, double* ra,
@@ -142,7 +150,7 @@ void cg_update_dots(int n, const double* alpha_dev, const double* p, const doubl
                     double* r, const double* jac, double* z, double* part, unsigned* ticket,
                     double* s_rzn, double* s_rr, double* s_rz, double* s_beta, const double* s_bb,
                     const double* s_pap, double tol, int max_iter, int* it_status,
-                    cudaGraphConditionalHandle h, cudaStream_t s);
+                    cudaGraphConditionalHandle h, cudaStream_t s, int* more_out = nullptr);
 // the CG operator fused with p.Ap and alpha (part: pap_partials() doubles, ticket zeroed)
 int pap_partials(int n, bool warp_rows);
 void csr_apply_a_pap(int n, const int32_t* rp, const int32_t* ci, const double* v, const double* x,

@@ -25,13 +25,17 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
 #include "pd_common.cuh"
 #include "pd_mts.cuh"
 #include "pmts_mts_setup.h"
+#include "nccl_rt.h"
 
 namespace pmts {
 DevPD pd_internal_dev(pmts_pd* h);
@@ -83,6 +87,129 @@ struct Nm {
     bool explicit_scheme() const { return beta == 0.0; }
 };
 
+// ---- PD shards of the coupled run (north star item 5) ----
+// The PD-active elements are cut into slabs of element layers along the slowest
+// lattice axis (y in 2D, z in 3D -- the PD numbering's slowest axis, so the elements a
+// shard owns are one contiguous local range).  Shard r owns the element layers
+// [b_r, b_{r+1}) and the node layers [b_r, b_{r+1}) (the last shard also the far
+// layer); it holds every element within D + 1 layers of them (D = floor(delta / h),
+// the largest layer distance of a bond), so the elements incident to its nodes have
+// complete families.  Local elements and nodes keep the global order: the families,
+// the per-entry arithmetic and its e < p branches run exactly as in one domain.
+struct ShardLink {
+    int peer = -1;
+    std::vector<int32_t> send, recv;  // local dofs; my send list is the peer's recv list
+};
+struct ShardPlan {
+    int world = 1, rank = 0, axis = 0, D = 0, layers = 0;
+    std::vector<int> bounds;  // world + 1 element-layer bounds
+    std::vector<int> elems;   // local element -> PD-active index (ascending)
+    std::vector<int> nodes;   // local node -> compact PD node (ascending)
+    int own_e0 = 0, own_e1 = 0;
+    std::vector<uint8_t> node_own;  // per local node
+    std::vector<ShardLink> links;   // lower, then upper neighbour
+};
+
+ShardPlan make_shard_plan(const MtsSystem& s, double h, int world, int rank) {
+    ShardPlan p;
+    p.world = world;
+    p.rank = rank;
+    const int dim = s.dim, nn = dim == 2 ? 4 : 8;
+    p.axis = dim - 1;
+    const int NE = int(s.pd_active.size()), NN = int(s.pd_active_nodes.size());
+    std::vector<int> compact(s.nodes.size() / 3, -1);
+    for (int c = 0; c < NN; ++c) compact[s.pd_active_nodes[c]] = c;
+    for (int c = 0; c < NN; ++c)
+        for (int k = 0; k < dim; ++k)
+            if (s.pd_node_dof[s.pd_active_nodes[c]] != c * dim)
+                throw InternalError("PD dofs are not in compact node order");
+    double org = 1e300;
+    for (int c = 0; c < NN; ++c)
+        org = std::min(org, s.nodes[3 * (size_t)s.pd_active_nodes[c] + p.axis]);
+    std::vector<int> el(NE), nlay(NN);
+    int L = 0;
+    for (int k = 0; k < NE; ++k) {
+        const double x = s.centroid[3 * (size_t)s.pd_active[k] + p.axis];
+        el[k] = int(std::llround((x - org) / h - 0.5));
+        if (k && el[k] < el[k - 1])
+            throw ConfigError("sharded coupled run: the PD elements are not ordered along the cut axis");
+        L = std::max(L, el[k] + 1);
+    }
+    for (int c = 0; c < NN; ++c)
+        nlay[c] = int(std::llround((s.nodes[3 * (size_t)s.pd_active_nodes[c] + p.axis] - org) / h));
+    p.layers = L;
+    p.D = int(std::floor(s.delta / h * (1.0 + 1e-9)));
+    p.bounds.resize(world + 1);
+    for (int r = 0; r <= world; ++r) p.bounds[r] = int((long long)r * L / world);
+    for (int r = 0; r < world; ++r)
+        if (p.bounds[r + 1] - p.bounds[r] < p.D + 1)  // (ghosts from the neighbours only)
+            throw ConfigError("sharded coupled run: " + std::to_string(world) + " shards of " +
+                              std::to_string(L) + " PD element layers leave fewer than D + 1 = " +
+                              std::to_string(p.D + 1) + " layers per shard");
+    auto owner = [&](int c) {
+        const int l = nlay[c];
+        for (int r = world - 1; r >= 0; --r)
+            if (l >= p.bounds[r]) return r;
+        return 0;
+    };
+    auto local_of = [&](int q, std::vector<int>& E, std::vector<int>& N) {
+        const int lo = p.bounds[q] - 1 - p.D, hi = p.bounds[q + 1] + p.D;
+        E.clear();
+        for (int k = 0; k < NE; ++k)
+            if (el[k] >= lo && el[k] < hi) E.push_back(k);
+        std::vector<char> mark(NN, 0);
+        for (int k : E)
+            for (int a = 0; a < nn; ++a) mark[compact[s.conn[(size_t)s.pd_active[k] * nn + a]]] = 1;
+        N.clear();
+        for (int c = 0; c < NN; ++c)
+            if (mark[c]) N.push_back(c);
+    };
+    local_of(rank, p.elems, p.nodes);
+    p.own_e0 = p.own_e1 = 0;
+    for (size_t i = 0; i < p.elems.size(); ++i) {
+        if (el[p.elems[i]] < p.bounds[rank]) p.own_e0 = int(i) + 1;
+        if (el[p.elems[i]] < p.bounds[rank + 1]) p.own_e1 = int(i) + 1;
+    }
+    p.node_own.resize(p.nodes.size());
+    std::vector<int> g2l(NN, -1);
+    for (size_t i = 0; i < p.nodes.size(); ++i) {
+        g2l[p.nodes[i]] = int(i);
+        const int o = owner(p.nodes[i]);
+        p.node_own[i] = o == rank;
+        if (o != rank && o != rank - 1 && o != rank + 1)
+            throw InternalError("shard halo reaches past a neighbour");
+    }
+    for (int q : {rank - 1, rank + 1}) {
+        if (q < 0 || q >= world) continue;
+        std::vector<int> qE, qN;
+        local_of(q, qE, qN);
+        ShardLink lk;
+        lk.peer = q;
+        for (int c : p.nodes)
+            if (owner(c) == q)
+                for (int k = 0; k < dim; ++k) lk.recv.push_back(g2l[c] * dim + k);
+        for (int c : qN)
+            if (owner(c) == rank)
+                for (int k = 0; k < dim; ++k) lk.send.push_back(g2l[c] * dim + k);
+        p.links.push_back(std::move(lk));
+    }
+    return p;
+}
+
+// collectives of the sharded coupled step, all stream-ordered on the handle's stream
+// and called by every shard in the same order (in-process group: host barriers and
+// device copies between the shards' buffers; NCCL: one clique, send/recv + reductions)
+struct MtsComm {
+    virtual ~MtsComm() = default;
+    // the halo dofs of x (a local PD vector) from their owners
+    virtual void halo(pmts_mts& h, double* x) = 0;
+    // x (n doubles) <- the sum over shards, every entry owned by one shard and -0.0
+    // elsewhere: exact in any order (x + -0.0 == x)
+    virtual void sum_owned(pmts_mts& h, double* x, size_t n) = 0;
+    virtual void bcast(pmts_mts& h, void* x, size_t bytes) = 0;  // from shard 0
+    virtual void reduce_u64(pmts_mts& h, unsigned long long* x, int n, bool max) = 0;
+};
+
 }  // namespace
 
 struct pmts_mts {
@@ -111,6 +238,42 @@ struct pmts_mts {
     DState wst_fe;
     pmts_pd* pd = nullptr;
     DevPD pdv{};
+    // ---- sharded coupled run (pmts_mts_desc.shard_world > 1): this
+    // handle holds one PD shard (local nodes / elements of plan); shard 0 also the FE
+    // side.  The interface solve is replicated on every shard (identical arithmetic:
+    // the same multipliers everywhere, no broadcast of lambda)
+    ShardPlan plan;
+    bool sharded = false, root = true, setup_done = true;
+    std::unique_ptr<MtsComm> comm;
+    bool group_comm = false;
+    int32_t* cpd_own = nullptr;  // coupling row -> local PD dof when this shard owns it, else -1
+    int32_t* ident = nullptr;    // 0 .. nl - 1
+    int32_t* own_dofs = nullptr;  // the owned local PD dofs
+    double* own_zero = nullptr;   // zeros, one per owned dof
+    int n_own_dofs = 0;
+    double* gpd_now = nullptr;    // G_PD v at the macro step's end (continuity residual)
+    struct LinkDev {
+        int peer = -1, n_send = 0, n_recv = 0;
+        int32_t *send = nullptr, *recv = nullptr;
+        double *sbuf = nullptr, *rbuf = nullptr;
+    };
+    std::vector<LinkDev> links;
+    double* sum_scratch = nullptr;
+    size_t sum_cap = 0;
+    int* more_d = nullptr;  // host-driven CG loop flag (device, pinned copy)
+    int* more_h = nullptr;
+    MtsComm& cm() {
+        if (!comm) throw ConfigError("sharded coupled handle without a transport "
+                                     "(pmts_mts_group_join / pmts_mts_comm_init)");
+        return *comm;
+    }
+    void halo(double* x) {
+        if (sharded) cm().halo(*this, x);
+    }
+    void sum_owned(double* x, size_t n) {
+        if (sharded) cm().sum_owned(*this, x, n);
+    }
+    const int32_t* cpd_g() const { return sharded ? cpd_own : cpd; }
     std::vector<int32_t> pairs;  // global ids
     std::vector<double> pe_weight;
     int nf = 0, np = 0, nl = 0, npe = 0, m = 1;
@@ -253,7 +416,8 @@ struct pmts_mts {
         mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, famT_xi, x, mask, pd_ubar, stream);
     }
 
-    void pd_K(const double* x, double* y, uint32_t* mask, bool do_break, int slot) {
+    void pd_K(double* x, double* y, uint32_t* mask, bool do_break, int slot) {
+        halo(x);  // sharded: the halo dofs of x from their owners
         mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream);
         launch_node_force(pdv, y, stream);
     }
@@ -270,7 +434,11 @@ struct pmts_mts {
     // returns false where the operator has no fused form (op, then the separate dot)
     template <class Op, class OpDot>
     void cg(int n, Op&& op, OpDot&& opdot, const double* b, double* x, double tol, int max_iter,
-            const double* jac, int slot) {
+            const double* jac, int slot, bool host_loop = false) {
+        if (host_loop) {
+            cg_host(n, op, opdot, b, x, tol, max_iter, jac, slot);
+            return;
+        }
         double* r = cg_r;
         double* z = cg_z;
         double* p = cg_p;
@@ -342,6 +510,42 @@ struct pmts_mts {
         }
         cg_max[slot] = max_iter;
         CKM(cudaGraphLaunch(gl, stream));
+    }
+    // the same solve with the loop on the host (sharded coupled runs whose operator holds
+    // collectives: each iteration's exchanges are host-synchronised in the in-process
+    // group): the same kernels in the same order, the loop flag read back per iteration
+    template <class Op, class OpDot>
+    void cg_host(int n, Op&& op, OpDot&& opdot, const double* b, double* x, double tol,
+                 int max_iter, const double* jac, int slot) {
+        double *r = cg_r, *z = cg_z, *p = cg_p, *ap = cg_ap;
+        double* sc = scal + 8 * slot;
+        double *s_bb = sc + 0, *s_rz = sc + 1, *s_rr = sc + 2, *s_pap = sc + 3, *s_alpha = sc + 4,
+               *s_rzn = sc + 5, *s_beta = sc + 6;
+        int* st = cg_status + 2 * slot;
+        mtsk::dot(n, b, b, part, s_bb, stream);
+        op(x, ap);
+        sub(n, b, ap, r);
+        mtsk::precond(n, r, jac, z, stream);
+        CKM(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+        mtsk::dot(n, r, z, part, s_rz, stream);
+        mtsk::dot(n, r, r, part, s_rr, stream);
+        mtsk::cg_start(0, s_bb, s_rr, tol, max_iter, st, x, n, stream, more_d);
+        cg_max[slot] = max_iter;
+        auto more = [&] {
+            CKM(cudaMemcpyAsync(more_h, more_d, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CKM(cudaStreamSynchronize(stream));
+            return *more_h != 0;
+        };
+        while (more()) {
+            if (!opdot(p, ap, s_pap, s_rz, s_alpha)) {
+                op(p, ap);
+                mtsk::dot_fin(n, p, ap, nullptr, nullptr, part2, ticket, s_pap, nullptr, 1, s_rz,
+                              s_alpha, stream);
+            }
+            mtsk::cg_update_dots(n, s_alpha, p, ap, x, r, jac, z, part2, ticket, s_rzn, s_rr, s_rz,
+                                 s_beta, s_bb, s_pap, tol, max_iter, st, 0, stream, more_d);
+            mtsk::xpby(n, z, s_beta, p, stream);
+        }
     }
     // {iterations, status} of a finished solve (host copy h_stat after a readback)
     int cg_check(const int* hs, int slot) const {
@@ -469,12 +673,23 @@ struct pmts_mts {
     void lin_substeps(const double* w_dev, double* out_last, double* out_rows, const DState& y) {
         zero_vec(rd, np);
         zero_vec(rv, np);
+        if (sharded) {  // rows other shards own: -0.0, then the owner-sum
+            if (out_last) mtsk::fill(nl, -0.0, out_last, stream);
+            if (out_rows) mtsk::fill((long long)m * nl, -0.0, out_rows + nl, stream);
+        }
         for (int j = 1; j <= m; ++j) {
-            if (j > 1) force_lin(rd, mask_sync);
+            if (j > 1) {
+                halo(rd);
+                force_lin(rd, mask_sync);
+            }
             double* out = out_rows ? out_rows + (size_t)j * nl : (j == m ? out_last : nullptr);
             mtsk::pd_node_lin(pdv, j > 1 ? 1 : 0, w_dev, row_of, double(j) / m, pd_M, pd_cf,
                               pd_nm.gdt, pd_nm.bdt2, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, y.u, y.v, y.a,
                               rd, rv, out, stream);
+        }
+        if (sharded) {
+            if (out_last) sum_owned(out_last, nl);
+            if (out_rows) sum_owned(out_rows + nl, (size_t)m * nl);
         }
     }
     // H_FE = -G_FE vel(Y_FE) column by column on the device (mts.hpp:389-397): the
@@ -614,7 +829,7 @@ struct pmts_mts {
     int hpd_colours = 0;
     void build_h_pd() {
         const int dim = s.dim;
-        std::vector<int> dof2node(np, -1);
+        std::vector<int> dof2node(s.pd_n_dof, -1);  // global PD dofs
         for (size_t nd = 0; nd < s.pd_node_dof.size(); ++nd)
             if (s.pd_node_dof[nd] >= 0)
                 for (int c = 0; c < dim; ++c) dof2node[s.pd_node_dof[nd] + c] = (int)nd;
@@ -732,7 +947,8 @@ struct pmts_mts {
             zero_vec(lam_tmp, nl);
             mtsk::set_ones((int)(c_src[c + 1] - c_src[c]), d_src + c_src[c], lam_tmp, stream);
             lin_substeps(lam_tmp, nullptr, nullptr, yst);
-            mtsk::gather(nl, cpd, yst.v, gvec, stream);
+            mtsk::gather(nl, cpd_g(), yst.v, gvec, stream);
+            sum_owned(gvec, nl);
             mtsk::gather_slots((int)(c_pair[c + 1] - c_pair[c]), d_rows + c_pair[c],
                                d_slots + c_pair[c], gvec, hpd_v, stream);
         }
@@ -771,12 +987,14 @@ struct pmts_mts {
 
     void initialize_accelerations() {
         // FE: p = P_fe ls(t) + G_FE^T (-lambda_prev)
-        mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
-        add_gt_fe_neg(lamp_d, ra);
-        fe_K(ufe.u, kd);
-        mtsk::init_acc(nf, ra, kd, fe_M, fe_cf, ufe.a, stream);
+        if (root) {
+            mtsk::scale(nf, fe_P, load_scale(t), ra, stream);
+            add_gt_fe_neg(lamp_d, ra);
+            fe_K(ufe.u, kd);
+            mtsk::init_acc(nf, ra, kd, fe_M, fe_cf, ufe.a, stream);
+        }
         mtsk::scale(np, pd_P, load_scale(t), ra, stream);
-        mtsk::scatter_add(nl, cpd, lamp_d, ra, stream);
+        mtsk::scatter_add(nl, cpd_g(), lamp_d, ra, stream);
         pd_K(upd.u, kd, mask_live, false, 0);
         mtsk::init_acc(np, ra, kd, pd_M, pd_cf, upd.a, stream);
         CKM(cudaStreamSynchronize(stream));
@@ -787,8 +1005,14 @@ struct pmts_mts {
     // lambda_prev (its status read here: a failed CG falls back to the dense form)
     void interface_solve(int* iterations) {
         double* b = alloc_iface_b();
-        gather_fe(vfe.v, b);
-        mtsk::sub_idx(nl, cpd, vpd.v, b, stream);
+        if (!sharded) {
+            gather_fe(vfe.v, b);
+            mtsk::sub_idx(nl, cpd, vpd.v, b, stream);
+        } else {  // G_FE v from shard 0; G_PD v = the free substeps' last row (owner-summed)
+            if (root) gather_fe(vfe.v, b);
+            cm().bcast(*this, b, sizeof(double) * nl);
+            mtsk::sub_idx(nl, ident, gp_free_d + (size_t)m * nl, b, stream);
+        }
         if (use_dense) {
             if (!h_valid) throw InternalError("interface solve with stale unit response");
             *iterations = 0;
@@ -821,10 +1045,11 @@ struct pmts_mts {
                    mtsk::add(nl, iface_tmp, out, stream);  // out[r] += gpw[r]
                },
                [](const double*, double*, double*, const double*, double*) { return false; },
-               b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE);
+               b, lam_d, interface_cg_tol, max_iter, iface_jac, CG_IFACE, sharded);
         try {
             *iterations = cg_result(CG_IFACE);
         } catch (const SolverError&) {
+            if (sharded) throw;  // (no dense fallback across shards)
             use_dense = true;
             h_valid = false;
             if (!hfe_dense) {  // dense H_FE from the CSR (fallback only)
@@ -854,6 +1079,28 @@ struct pmts_mts {
     }
 
     pmts_mts_report macro_step();
+
+    // collective setup of a sharded run (every shard, once, before the first step):
+    // H_FE from shard 0 to every shard, H_PD by coloured recursions across the shards
+    void shard_setup() {
+        if (!root) hfe_rp = alloc<int32_t>(nl + 1);
+        cm().bcast(*this, hfe_rp, sizeof(int32_t) * (nl + 1));
+        int32_t nnz = 0;
+        CKM(cudaMemcpyAsync(&nnz, hfe_rp + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        CKM(cudaStreamSynchronize(stream));
+        if (!root) {
+            hfe_nnz = nnz;
+            hfe_ci = alloc<int32_t>(std::max<int64_t>(nnz, 1));
+            hfe_v = alloc<double>(std::max<int64_t>(nnz, 1));
+        }
+        if (nnz) {
+            cm().bcast(*this, hfe_ci, sizeof(int32_t) * (size_t)nnz);
+            cm().bcast(*this, hfe_v, sizeof(double) * (size_t)nnz);
+        }
+        invalidate_cg_graphs();
+        if (iface_precompute) build_h_pd();
+        setup_done = true;
+    }
 };
 
 namespace {
@@ -876,9 +1123,13 @@ std::vector<double> jacobi_diag(const MtsSystem& s, double bdt2) {
 
 pmts_mts_report pmts_mts::macro_step() {
     pmts_mts_report rep{};
+    if (sharded && !setup_done) throw ConfigError("sharded coupled handle: pmts_mts_init first");
     // snapshot_previous (mts.hpp:507-510)
-    CKM(cudaMemcpyAsync(fe_prev.a, ufe.a, sizeof(double) * nf, cudaMemcpyDeviceToDevice, stream));
-    gather_fe(ufe.v, gprev_d);
+    if (root) {
+        CKM(cudaMemcpyAsync(fe_prev.a, ufe.a, sizeof(double) * nf, cudaMemcpyDeviceToDevice,
+                            stream));
+        gather_fe(ufe.v, gprev_d);
+    }
     // unit-response upkeep (mts.hpp:249-260)
     {
         const double t0 = now_s();
@@ -902,8 +1153,8 @@ pmts_mts_report pmts_mts::macro_step() {
     CKM(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * (m + 1), stream));
     // free FE solve (mts.hpp:143-147)
     const double tk0 = now_s();
-    fork(ev_fork);  // the FE half on stream2, the PD half on stream
-    {
+    if (root) {  // the FE half on stream2, the PD half on stream
+        fork(ev_fork);
         OnStream2 on(this);
         mtsk::predict(nf, ufe.u, ufe.v, ufe.a, rd_fe, rv_fe, fe_nm.dt, fe_nm.cpv, fe_nm.cpd, stream);
         fe_solve(fe_P, load_scale(t + dt_fe()), rv_fe, rd_fe, warm_fe_free, &warm_free_ok, false,
@@ -912,24 +1163,26 @@ pmts_mts_report pmts_mts::macro_step() {
     // free PD solve, m substeps with the multiplier loads S_j (mts.hpp:152-180), the S_j
     // rows formed on the device
     mtsk::s_vectors(nl, m, t, s.dt_pd, dt_fe(), s.ramp, lamp_d, gpfe_d, sv_d, stream);
-    mtsk::gather(nl, cpd, upd.v, gp_free_d, stream);
+    mtsk::gather(nl, cpd_g(), upd.v, gp_free_d, stream);
     copy(vpd, upd, np);
     for (int j = 1; j <= m; ++j) {
         mtsk::predict(np, vpd.u, vpd.v, vpd.a, rd, rv, pd_nm.dt, pd_nm.cpv, pd_nm.cpd, stream);
+        halo(rd);  // sharded: one-horizon ghosts, every fine substep
         mtsk::scale(np, pd_P, load_scale(t + j * s.dt_pd), ra, stream);
-        mtsk::scatter_add(nl, cpd, sv_d + (size_t)(j - 1) * nl, ra, stream);
+        mtsk::scatter_add(nl, cpd_g(), sv_d + (size_t)(j - 1) * nl, ra, stream);
         pd_solve(ra, 1.0, rv, rd, mask_live, fracture, j, false, vpd);
-        mtsk::gather(nl, cpd, vpd.v, gp_free_d + (size_t)j * nl, stream);
+        mtsk::gather(nl, cpd_g(), vpd.v, gp_free_d + (size_t)j * nl, stream);
     }
-    join(ev_join);
+    sum_owned(gp_free_d, (size_t)(m + 1) * nl);  // G_PD v rows of every shard's owned rows
+    if (root) join(ev_join);
     rep.t_kinematic = now_s() - tk0;  // enqueue time (the work is asynchronous)
     // interface solve + recombination (mts.hpp:184-241)
     const double tl0 = now_s();
     int iters = 0;
     interface_solve(&iters);
     rep.interface_iterations = iters;
-    fork(ev_fork);
-    {  // FE correction: M_block W = -G^T lambda (stream2)
+    if (root) {  // FE correction: M_block W = -G^T lambda (stream2)
+        fork(ev_fork);
         OnStream2 on(this);
         zero_vec(ra_fe, nf);
         zero_vec(rv_fe, nf);
@@ -944,7 +1197,7 @@ pmts_mts_report pmts_mts::macro_step() {
         lin_substeps(lam_d, nullptr, gp_link_d, wst);
         mtsk::add_states(np, vpd.u, vpd.v, vpd.a, wst.u, wst.v, wst.a, upd.u, upd.v, upd.a, stream);
     }
-    join(ev_join);
+    if (root) join(ev_join);
     rep.t_lambda = now_s() - tl0;
     // bonds broken in the free substeps, then the post-recombination audit
     const double tu0 = now_s();
@@ -954,7 +1207,7 @@ pmts_mts_report pmts_mts::macro_step() {
     // on the device; everything the host needs comes back in one copy
     CKM(cudaMemsetAsync(cmax_d, 0, 3 * sizeof(unsigned long long), stream));
     CKM(cudaMemsetAsync(en_d, 0, 3 * sizeof(double), stream));
-    if (track_energy) {
+    if (track_energy && root) {
         if (fe_nm.gamma != 0.5) {
             double* da = cg_kx;  // scratch, nf
             mtsk::rhs(nf, ufe.a, 1.0, fe_prev.a, zero_flags(nf), da, stream);  // da = acc - prev
@@ -970,10 +1223,25 @@ pmts_mts_report pmts_mts::macro_step() {
         mtsk::lpd_terms(nl, m, gp_free_d, gp_link_d, sv_d, lamp_d, lam_d, ta_d, tb_d, stream);
         mtsk::dot(nl * m, ta_d, tb_d, part, en_d + 2, stream);
     }
-    gather_fe(ufe.v, gvec);
-    mtsk::max_abs(nl, gvec, cpd, upd.v, cmax_d + 0, stream);
-    mtsk::max_abs(nf, ufe.v, nullptr, nullptr, cmax_d + 1, stream);
-    mtsk::max_abs(np, upd.v, nullptr, nullptr, cmax_d + 2, stream);
+    if (!sharded) {
+        gather_fe(ufe.v, gvec);
+        mtsk::max_abs(nl, gvec, cpd, upd.v, cmax_d + 0, stream);
+        mtsk::max_abs(nf, ufe.v, nullptr, nullptr, cmax_d + 1, stream);
+        mtsk::max_abs(np, upd.v, nullptr, nullptr, cmax_d + 2, stream);
+    } else {  // the same maxima from owner-summed rows / owned dofs; one verdict everywhere
+        mtsk::gather(nl, cpd_own, upd.v, gpd_now, stream);
+        sum_owned(gpd_now, nl);
+        if (root) {
+            gather_fe(ufe.v, gvec);
+            mtsk::max_abs(nl, gvec, ident, gpd_now, cmax_d + 0, stream);
+            mtsk::max_abs(nf, ufe.v, nullptr, nullptr, cmax_d + 1, stream);
+        }
+        mtsk::max_abs(n_own_dofs, own_zero, own_dofs, upd.v, cmax_d + 2, stream);
+        cm().reduce_u64(*this, cmax_d + 2, 1, true);
+        cm().bcast(*this, cmax_d, 2 * sizeof(unsigned long long));
+        cm().reduce_u64(*this, d_counts, m + 1, false);
+        cm().bcast(*this, cg_status, sizeof(int) * 2 * N_CG);
+    }
     // lambda_prev <- lambda
     CKM(cudaMemcpyAsync(lamp_d, lam_d, sizeof(double) * nl, cudaMemcpyDeviceToDevice, stream));
     struct Back {
@@ -1213,6 +1481,148 @@ void build_host(pmts_mts& h, const pmts_mts_desc& d) {
     build_mts_system(s);
 }
 
+// ---- transports of the sharded coupled step ----
+
+// in-process group: one host thread per shard (pmts_mts_group_*), host barriers, device
+// copies between the shards' buffers (same device, or peers with P2P access)
+struct ShardGroup {
+    std::vector<pmts_mts*> h;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    bool aborted = false;
+    int first_error = -1;
+    std::vector<void*> slot;
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (aborted) throw InternalError("shard group aborted");
+        const long long g0 = gen;
+        if (++arrived == int(h.size())) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return;
+        }
+        cv.wait(lk, [&] { return gen != g0 || aborted; });
+        if (aborted) throw InternalError("shard group aborted");
+    }
+    void abort(int rank) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (first_error < 0) first_error = rank;
+        aborted = true;
+        cv.notify_all();
+    }
+};
+
+struct GroupComm : MtsComm {
+    std::shared_ptr<ShardGroup> g;
+    int rank = 0;
+    void publish(pmts_mts& h, void* x) {
+        CKM(cudaStreamSynchronize(h.stream));
+        g->slot[rank] = x;
+        g->wait();
+    }
+    void done(pmts_mts& h) {  // nobody reads or rewrites a published buffer before all copied
+        CKM(cudaStreamSynchronize(h.stream));
+        g->wait();
+    }
+    void halo(pmts_mts& h, double* x) override {
+        publish(h, x);
+        for (const auto& l : h.links) {
+            const pmts_mts* q = g->h[l.peer];
+            const pmts_mts::LinkDev* ql = nullptr;
+            for (const auto& k : q->links)
+                if (k.peer == rank) ql = &k;
+            if (!ql || ql->n_send != l.n_recv) throw InternalError("shard link mismatch");
+            mtsk::copy_idx(l.n_recv, static_cast<const double*>(g->slot[l.peer]), ql->send, x,
+                           l.recv, h.stream);
+        }
+        done(h);
+    }
+    void sum_owned(pmts_mts& h, double* x, size_t n) override {
+        if (n > h.sum_cap) throw InternalError("owner-sum larger than its scratch");
+        publish(h, x);
+        // every shard forms the same sum in shard order (exact: one owner per entry)
+        CKM(cudaMemcpyAsync(h.sum_scratch, g->slot[0], sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, h.stream));
+        for (size_t q = 1; q < g->h.size(); ++q)
+            mtsk::add(int(n), static_cast<const double*>(g->slot[q]), h.sum_scratch, h.stream);
+        done(h);
+        CKM(cudaMemcpyAsync(x, h.sum_scratch, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                            h.stream));
+    }
+    void bcast(pmts_mts& h, void* x, size_t bytes) override {
+        publish(h, x);
+        if (rank != 0 && bytes)
+            CKM(cudaMemcpyAsync(x, g->slot[0], bytes, cudaMemcpyDeviceToDevice, h.stream));
+        done(h);
+    }
+    void reduce_u64(pmts_mts& h, unsigned long long* x, int n, bool max) override {
+        publish(h, x);
+        std::vector<unsigned long long> acc(n, 0ull), t(n);
+        for (size_t q = 0; q < g->h.size(); ++q) {
+            CKM(cudaMemcpy(t.data(), g->slot[q], sizeof(unsigned long long) * n,
+                           cudaMemcpyDeviceToHost));
+            for (int i = 0; i < n; ++i) acc[i] = max ? std::max(acc[i], t[i]) : acc[i] + t[i];
+        }
+        g->wait();
+        CKM(cudaMemcpy(x, acc.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice));
+    }
+};
+
+// one NCCL clique, one rank per GPU (a process per GPU): everything stream-ordered
+struct NcclComm : MtsComm {
+    ncclComm_t c = nullptr;
+    ~NcclComm() override {
+        if (c) nccl().comm_destroy(c);
+    }
+    void halo(pmts_mts& h, double* x) override {
+        NcclApi& a = nccl();
+        for (const auto& l : h.links) mtsk::gather(l.n_send, l.send, x, l.sbuf, h.stream);
+        nccl_check(a.group_start(), "group");
+        for (const auto& l : h.links) {
+            nccl_check(a.send(l.sbuf, l.n_send, ncclFloat64, l.peer, c, h.stream), "send");
+            nccl_check(a.recv(l.rbuf, l.n_recv, ncclFloat64, l.peer, c, h.stream), "recv");
+        }
+        nccl_check(a.group_end(), "group");
+        for (const auto& l : h.links) mtsk::scatter_set(l.n_recv, l.recv, l.rbuf, x, h.stream);
+    }
+    void sum_owned(pmts_mts& h, double* x, size_t n) override {
+        nccl_check(nccl().all_reduce(x, x, n, ncclFloat64, ncclSum, c, h.stream), "all_reduce");
+    }
+    void bcast(pmts_mts& h, void* x, size_t bytes) override {
+        nccl_check(nccl().broadcast(x, x, bytes, ncclUint8, 0, c, h.stream), "broadcast");
+    }
+    void reduce_u64(pmts_mts& h, unsigned long long* x, int n, bool max) override {
+        nccl_check(nccl().all_reduce(x, x, n, ncclUint64, max ? ncclMax : ncclSum, c, h.stream),
+                   "all_reduce");
+    }
+};
+
+// run f(handle, rank) on every shard of a group, one host thread each; the first
+// shard's error is rethrown (the others only saw the group abort)
+template <class F>
+void run_group(pmts_mts* const* hs, int n, F&& f) {
+    if (!hs || n < 1 || !hs[0] || !hs[0]->group_comm) throw ConfigError("not a joined shard group");
+    std::shared_ptr<ShardGroup> g = static_cast<GroupComm*>(hs[0]->comm.get())->g;
+    if (int(g->h.size()) != n) throw ConfigError("shard group size mismatch");
+    std::vector<std::exception_ptr> err(n);
+    std::vector<std::thread> th;
+    for (int r = 0; r < n; ++r)
+        th.emplace_back([&, r] {
+            try {
+                CKM(cudaSetDevice(hs[r]->device));
+                f(hs[r], r);
+            } catch (...) {
+                err[r] = std::current_exception();
+                g->abort(r);
+            }
+        });
+    for (auto& t : th) t.join();
+    if (g->first_error >= 0) std::rethrow_exception(err[g->first_error]);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1233,6 +1643,20 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->iface_precompute = desc->interface_recursion == 0;
         // interface mode (mts.hpp:111-114); the PD side is explicit
         h->use_dense = h->iface_mode == 1 || (h->iface_mode == 0 && h->nl <= 400);
+        if (desc->shard_world > 1) {  // the shard plan (host; a host-only handle exposes it)
+            if (desc->shard_rank < 0 || desc->shard_rank >= desc->shard_world)
+                throw ConfigError("shard_rank out of range");
+            if (h->use_dense)
+                throw ConfigError("sharded coupled runs use the matrix-free interface "
+                                  "(interface_mode = 2, or n_lambda > 400)");
+            if (h->interface_precond)
+                throw ConfigError("sharded coupled runs: interface_precond is not supported");
+            h->sharded = true;
+            h->root = desc->shard_rank == 0;
+            h->setup_done = false;
+            h->plan = make_shard_plan(s, desc->scenario->spacing, desc->shard_world,
+                                      desc->shard_rank);
+        }
         if (h->device < 0) {  // host-only: the assembled systems (view), no integrator
             *out = h.release();
             return;
@@ -1243,7 +1667,6 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         for (cudaEvent_t* e : {&h->ev_fork, &h->ev_join, &h->ev_fork2, &h->ev_join2})
             CKM(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         h->nf = s.fe_n_dof;
-        h->np = s.pd_n_dof;
         h->nl = int(s.cpl_fe.size());
         h->m = s.m;
         h->fe_nm.set(s.fe_gamma, s.fe_beta, s.m * s.dt_pd);
@@ -1256,28 +1679,61 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             throw ConfigError("energy tracking of the PD quadratic term needs gamma_pd = 1/2");
         h->fe_cg_max = std::max(100, int(40 * std::sqrt(double(h->nf))));
 
-        // ---- PD subdomain handle: compact nodes / elements of the PD-active set ----
+        // ---- PD subdomain handle: compact nodes / elements of the PD-active set (a
+        // sharded run: this shard's local part of them, in the same order) ----
         const int dim = s.dim, nn = dim == 2 ? 4 : 8;
-        const int NPn = int(s.pd_active_nodes.size());
+        const int NPall = int(s.pd_active_nodes.size()), NEall = int(s.pd_active.size());
+        if (!h->sharded) {
+            h->plan.elems.resize(NEall);
+            h->plan.nodes.resize(NPall);
+            for (int k = 0; k < NEall; ++k) h->plan.elems[k] = k;
+            for (int k = 0; k < NPall; ++k) h->plan.nodes[k] = k;
+            h->plan.own_e0 = 0;
+            h->plan.own_e1 = NEall;
+            h->plan.node_own.assign(NPall, 1);
+        }
+        const std::vector<int>& lel = h->plan.elems;
+        const std::vector<int>& lnd = h->plan.nodes;
+        const int NPn = int(lnd.size());
+        h->np = NPn * dim;
         std::vector<int> compact(s.nodes.size() / 3, -1);
-        for (int k = 0; k < NPn; ++k) compact[s.pd_active_nodes[k]] = k;
+        for (int k = 0; k < NPall; ++k) compact[s.pd_active_nodes[k]] = k;
+        std::vector<int> c2l(NPall, -1);  // compact node -> local node
+        for (int k = 0; k < NPn; ++k) c2l[lnd[k]] = k;
         std::vector<double> pxyz(3 * (size_t)NPn);
         for (int k = 0; k < NPn; ++k)
-            for (int c = 0; c < 3; ++c) pxyz[3 * (size_t)k + c] = s.nodes[3 * (size_t)s.pd_active_nodes[k] + c];
+            for (int c = 0; c < 3; ++c)
+                pxyz[3 * (size_t)k + c] = s.nodes[3 * (size_t)s.pd_active_nodes[lnd[k]] + c];
         std::vector<int32_t> pconn;
-        for (int e : s.pd_active)
-            for (int a = 0; a < nn; ++a) pconn.push_back(compact[s.conn[(size_t)e * nn + a]]);
+        for (int e : lel)
+            for (int a = 0; a < nn; ++a)
+                pconn.push_back(c2l[compact[s.conn[(size_t)s.pd_active[e] * nn + a]]]);
+        // per-dof PD arrays of the local nodes (PD dof = compact node * dim + component)
+        std::vector<double> lmass(h->np), lpext(h->np);
+        for (int k = 0; k < NPn; ++k)
+            for (int c = 0; c < dim; ++c) {
+                lmass[(size_t)k * dim + c] = s.pd_mass[(size_t)lnd[k] * dim + c];
+                lpext[(size_t)k * dim + c] = s.pd_p_ext[(size_t)lnd[k] * dim + c];
+            }
+        std::vector<int32_t> lbc;
+        std::vector<double> lbcv;
+        for (size_t q = 0; q < s.pd_bc_dofs.size(); ++q) {
+            const int l = c2l[s.pd_bc_dofs[q] / dim];
+            if (l < 0) continue;
+            lbc.push_back(l * dim + s.pd_bc_dofs[q] % dim);
+            lbcv.push_back(s.pd_bc_vel[q]);
+        }
         pmts_pd_desc pdd{};
         pdd.dim = dim;
         pdd.n_nodes = NPn;
-        pdd.n_elems = int(s.pd_active.size());
+        pdd.n_elems = int(lel.size());
         pdd.node_xyz = pxyz.data();
         pdd.elem_nodes = pconn.data();
-        pdd.mass = s.pd_mass.data();
-        pdd.p_ext = s.pd_p_ext.data();
-        pdd.n_bc = int(s.pd_bc_dofs.size());
-        pdd.bc_dofs = s.pd_bc_dofs.data();
-        pdd.bc_vel = s.pd_bc_vel.data();
+        pdd.mass = lmass.data();
+        pdd.p_ext = lpext.data();
+        pdd.n_bc = int(lbc.size());
+        pdd.bc_dofs = lbc.data();
+        pdd.bc_vel = lbcv.data();
         pdd.delta = s.delta;
         pdd.micromodulus = PMTS_MICRO_EXP;
         pdd.c0 = s.c0;
@@ -1291,6 +1747,10 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         pdd.n_notch = desc->scenario->n_notch;
         pdd.notch_npts = desc->scenario->notch_npts;
         pdd.notch_pts = desc->scenario->notch_pts;
+        if (h->sharded) {  // broken bonds are counted by the shard owning the lower element
+            pdd.owned_elems[0] = h->plan.own_e0;
+            pdd.owned_elems[1] = h->plan.own_e1;
+        }
         check_pd(pmts_pd_create(&pdd, &h->pd));
         check_pd(pmts_pd_build_families(h->pd));
         int64_t npairs = 0;
@@ -1301,7 +1761,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->pairs.resize(cp.size());
         h->pe_weight.resize(npairs);
         for (int64_t p = 0; p < npairs; ++p) {
-            const int gi = s.pd_active[cp[2 * p]], gj = s.pd_active[cp[2 * p + 1]];
+            const int gi = s.pd_active[lel[cp[2 * p]]], gj = s.pd_active[lel[cp[2 * p + 1]]];
             h->pairs[2 * p] = gi;
             h->pairs[2 * p + 1] = gj;
             double mid[3];
@@ -1347,13 +1807,50 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->fe_cf = h->upload(cf);
         h->fe_bcv = h->upload(bv);
         h->fe_jac = h->upload(jacobi_diag(s, h->fe_nm.bdt2));
-        h->pd_M = h->upload(s.pd_mass);
-        h->pd_P = h->upload(s.pd_p_ext);
-        flags(h->np, s.pd_bc_dofs, s.pd_bc_vel, cf, bv);
+        h->pd_M = h->upload(lmass);
+        h->pd_P = h->upload(lpext);
+        flags(h->np, lbc, lbcv, cf, bv);
         h->pd_cf = h->upload(cf);
         h->pd_bcv = h->upload(bv);
         h->cfe = h->upload(s.cpl_fe);
-        h->cpd = h->upload(s.cpl_pd);
+        // coupling rows -> local PD dofs (sharded: the rows this shard owns, else -1)
+        std::vector<int32_t> lcpd(h->nl, -1);
+        for (int r = 0; r < h->nl; ++r) {
+            const int l = c2l[s.cpl_pd[r] / dim];
+            if (l >= 0 && h->plan.node_own[l]) lcpd[r] = l * dim + s.cpl_pd[r] % dim;
+        }
+        h->cpd = h->upload(lcpd);
+        if (h->sharded) {
+            h->cpd_own = h->cpd;
+            std::vector<int32_t> id(h->nl);
+            for (int r = 0; r < h->nl; ++r) id[r] = r;
+            h->ident = h->upload(id);
+            std::vector<int32_t> od;
+            for (int k = 0; k < NPn; ++k)
+                if (h->plan.node_own[k])
+                    for (int c = 0; c < dim; ++c) od.push_back(k * dim + c);
+            h->n_own_dofs = int(od.size());
+            h->own_dofs = h->upload(od);
+            h->own_zero = h->alloc<double>(od.size());
+            CKM(cudaMemsetAsync(h->own_zero, 0, sizeof(double) * std::max<size_t>(od.size(), 1),
+                                h->stream));
+            h->gpd_now = h->alloc<double>(h->nl);
+            for (const ShardLink& lk : h->plan.links) {
+                pmts_mts::LinkDev ld;
+                ld.peer = lk.peer;
+                ld.n_send = int(lk.send.size());
+                ld.n_recv = int(lk.recv.size());
+                ld.send = h->upload(lk.send);
+                ld.recv = h->upload(lk.recv);
+                ld.sbuf = h->alloc<double>(lk.send.size());
+                ld.rbuf = h->alloc<double>(lk.recv.size());
+                h->links.push_back(ld);
+            }
+            h->sum_cap = (size_t)(h->m + 1) * h->nl;
+            h->sum_scratch = h->alloc<double>(h->sum_cap);
+            h->more_d = h->alloc<int>(1);
+            CKM(cudaMallocHost(&h->more_h, sizeof(int)));
+        }
         h->gfe_rp = h->upload(s.cpl_fe_rp);
         h->gfe_ci = h->upload(s.cpl_fe_ci);
         h->gfe_w = h->upload(s.cpl_fe_w);
@@ -1426,7 +1923,8 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->pd_ubar = h->alloc<double>((size_t)h->pdv.E * dim);
         {
             std::vector<int32_t> ro(h->np, -1);
-            for (int r = 0; r < h->nl; ++r) ro[s.cpl_pd[r]] = r;
+            for (int r = 0; r < h->nl; ++r)
+                if (lcpd[r] >= 0) ro[lcpd[r]] = r;
             h->row_of = h->upload(ro);
         }
         h->gp_free_d = h->alloc<double>((size_t)(h->m + 1) * h->nl);
@@ -1441,7 +1939,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             for (size_t c = 0; c < s.fe_bc_dofs.size(); ++c) z[s.fe_bc_dofs[c]] = s.fe_bc_vel[c];
             h->to_dev(h->ufe.v, z);
             std::vector<double> zp(h->np, 0.0);
-            for (size_t c = 0; c < s.pd_bc_dofs.size(); ++c) zp[s.pd_bc_dofs[c]] = s.pd_bc_vel[c];
+            for (size_t c = 0; c < lbc.size(); ++c) zp[lbc[c]] = lbcv[c];
             h->to_dev(h->upd.v, zp);
         }
         // g_p_fe = G_FE P_ext (mts.hpp:110)
@@ -1456,9 +1954,11 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             h->gpfe_d = h->upload(g);
         }
         CKM(cudaStreamSynchronize(h->stream));
-        h->build_h_fe();
-        if (h->use_dense) h->refresh_dense_interface();
-        else if (h->iface_precompute) h->build_h_pd();
+        if (h->root) h->build_h_fe();
+        if (!h->sharded) {
+            if (h->use_dense) h->refresh_dense_interface();
+            else if (h->iface_precompute) h->build_h_pd();
+        }  // sharded: H_FE goes to every shard and H_PD is built across them in pmts_mts_init
         CKM(cudaStreamSynchronize(h->stream));
         *out = h.release();
     });
@@ -1526,8 +2026,98 @@ int pmts_mts_init(pmts_mts* h) {
     return guard([&] {
         if (!h) throw ConfigError("null handle");
         if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        if (h->group_comm) throw ConfigError("in-process shard group: pmts_mts_group_init");
         CKM(cudaSetDevice(h->device));
+        if (h->sharded && !h->setup_done) h->shard_setup();
         h->initialize_accelerations();
+    });
+}
+
+int pmts_mts_shard_view_get(const pmts_mts* h, pmts_mts_shard_view* v) {
+    return guard([&] {
+        if (!h || !v) throw ConfigError("null argument");
+        const ShardPlan& p = h->plan;
+        *v = pmts_mts_shard_view{};
+        v->world = h->sharded ? p.world : 1;
+        v->rank = h->sharded ? p.rank : 0;
+        v->axis = p.axis;
+        v->reach_layers = p.D;
+        v->n_layers = p.layers;
+        v->n_local_nodes = int32_t(p.nodes.size());
+        v->n_local_elems = int32_t(p.elems.size());
+        v->own_elem_lo = p.own_e0;
+        v->own_elem_hi = p.own_e1;
+        v->local_nodes = reinterpret_cast<const int32_t*>(p.nodes.data());
+        v->local_elems = reinterpret_cast<const int32_t*>(p.elems.data());
+        v->node_owned = p.node_own.data();
+        v->layer_bounds = reinterpret_cast<const int32_t*>(p.bounds.data());
+    });
+}
+
+int pmts_mts_group_join(pmts_mts* const* hs, int32_t n) {
+    return guard([&] {
+        if (!hs || n < 2) throw ConfigError("a shard group needs at least 2 handles");
+        auto g = std::make_shared<ShardGroup>();
+        g->h.assign(hs, hs + n);
+        g->slot.assign(n, nullptr);
+        for (int r = 0; r < n; ++r) {
+            pmts_mts* h = hs[r];
+            if (!h || h->device < 0 || !h->sharded || h->plan.world != n || h->plan.rank != r)
+                throw ConfigError("handle " + std::to_string(r) + " is not shard " +
+                                  std::to_string(r) + " of " + std::to_string(n));
+            if (h->comm) throw ConfigError("shard already has a transport");
+        }
+        for (int r = 0; r < n; ++r)  // device copies between shards on different GPUs
+            for (int q = 0; q < n; ++q)
+                if (hs[r]->device != hs[q]->device) {
+                    CKM(cudaSetDevice(hs[r]->device));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(hs[q]->device, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CKM(e);
+                    cudaGetLastError();
+                }
+        for (int r = 0; r < n; ++r) {
+            auto c = std::make_unique<GroupComm>();
+            c->g = g;
+            c->rank = r;
+            hs[r]->comm = std::move(c);
+            hs[r]->group_comm = true;
+        }
+    });
+}
+
+int pmts_mts_group_init(pmts_mts* const* hs, int32_t n) {
+    return guard([&] {
+        run_group(hs, n, [](pmts_mts* h, int) {
+            if (!h->setup_done) h->shard_setup();
+            h->initialize_accelerations();
+        });
+    });
+}
+
+int pmts_mts_group_macro_step(pmts_mts* const* hs, int32_t n, int32_t steps,
+                              pmts_mts_report* reports) {
+    return guard([&] {
+        if (steps < 0) throw ConfigError("bad step count");
+        run_group(hs, n, [&](pmts_mts* h, int r) {
+            for (int i = 0; i < steps; ++i) {
+                const pmts_mts_report rep = h->macro_step();
+                if (reports && r == 0) reports[i] = rep;
+            }
+        });
+    });
+}
+
+int pmts_mts_comm_init(pmts_mts* h, const void* nccl_id) {
+    return guard([&] {
+        if (!h || !nccl_id) throw ConfigError("null argument");
+        if (!h->sharded || h->device < 0) throw ConfigError("not a device shard handle");
+        if (h->comm) throw ConfigError("shard already has a transport");
+        ncclUniqueId uid;
+        std::memcpy(&uid, nccl_id, sizeof(uid));
+        CKM(cudaSetDevice(h->device));
+        auto c = std::make_unique<NcclComm>();
+        nccl_check(nccl().comm_init_rank(&c->c, h->plan.world, uid, h->plan.rank), "comm init");
+        h->comm = std::move(c);
     });
 }
 
@@ -1535,6 +2125,7 @@ int pmts_mts_macro_step(pmts_mts* h, int32_t n, pmts_mts_report* reports) {
     return guard([&] {
         if (!h || n < 0) throw ConfigError("bad arguments");
         if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        if (h->group_comm) throw ConfigError("in-process shard group: pmts_mts_group_macro_step");
         CKM(cudaSetDevice(h->device));
         for (int i = 0; i < n; ++i) {
             const pmts_mts_report r = h->macro_step();
@@ -1547,6 +2138,7 @@ int pmts_mts_macro_step_timed(pmts_mts* h, int32_t n, float* ms_out) {
     return guard([&] {
         if (!h || n < 0) throw ConfigError("bad arguments");
         if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
+        if (h->group_comm) throw ConfigError("in-process shard group: pmts_mts_group_macro_step");
         CKM(cudaSetDevice(h->device));
         cudaEvent_t e0, e1;
         CKM(cudaEventCreate(&e0));
@@ -1603,12 +2195,14 @@ int pmts_mts_damage(pmts_mts* h, double* elem_out, double* node_out) {
         if (!h || !elem_out || !node_out) throw ConfigError("bad arguments");
         if (h->device < 0) throw ConfigError("host-only handle (device < 0)");
         const MtsSystem& s = h->s;
-        std::vector<double> pe(s.pd_active.size()), pn(s.pd_active_nodes.size());
+        const ShardPlan& p = h->plan;  // a shard fills its owned elements / nodes only
+        std::vector<double> pe(p.elems.size()), pn(p.nodes.size());
         check_pd(pmts_pd_damage(h->pd, pe.data(), pn.data()));
         std::fill(elem_out, elem_out + s.volume.size(), 0.0);
         std::fill(node_out, node_out + s.nodes.size() / 3, 0.0);
-        for (size_t k = 0; k < s.pd_active.size(); ++k) elem_out[s.pd_active[k]] = pe[k];
-        for (size_t k = 0; k < s.pd_active_nodes.size(); ++k) node_out[s.pd_active_nodes[k]] = pn[k];
+        for (int k = p.own_e0; k < p.own_e1; ++k) elem_out[s.pd_active[p.elems[k]]] = pe[k];
+        for (size_t k = 0; k < p.nodes.size(); ++k)
+            if (p.node_own[k]) node_out[s.pd_active_nodes[p.nodes[k]]] = pn[k];
     });
 }
 

@@ -32,7 +32,9 @@ class MtsSolver:
     """One coupled run (reference config vocabulary: [region], time.m, gamma_fe,
     beta_fe, run.interface, ...)."""
 
-    def __init__(self, sc: dict, device: int = 0):
+    def __init__(self, sc: dict, device: int = 0, shard: tuple[int, int] | None = None):
+        """shard = (rank, world): PD shard `rank` of a sharded run; join the
+        shards with ShardGroup (one process) or comm_init (NCCL, one process per GPU)."""
         self.cfg = sc
         self._keep = []
         sd = scenario_desc(sc, self._keep)
@@ -63,6 +65,8 @@ class MtsSolver:
         d.interface_precond = 1 if run.get("interface_precond", "none") == "jacobi" else 0
         # run.interface_h_pd = precompute (default) | recursion
         d.interface_recursion = 1 if run.get("interface_h_pd", "precompute") == "recursion" else 0
+        if shard is not None:
+            d.shard_rank, d.shard_world = int(shard[0]), int(shard[1])
         h = C.c_void_p()
         check(lib().pmts_mts_create(C.byref(d), C.byref(h)))
         self.h = h
@@ -75,6 +79,23 @@ class MtsSolver:
         self.dt_pd = v.dt_pd
         self.dt_fe = v.m * v.dt_pd
         self.n_pairs = v.n_pairs
+        sv = capi.MtsShardView()
+        check(lib().pmts_mts_shard_view_get(h, C.byref(sv)))
+        self.shard = {
+            "world": sv.world, "rank": sv.rank, "axis": sv.axis, "reach_layers": sv.reach_layers,
+            "n_layers": sv.n_layers, "own_elems": (sv.own_elem_lo, sv.own_elem_hi),
+            "local_nodes": _arr(sv.local_nodes, C.c_int32, sv.n_local_nodes),
+            "local_elems": _arr(sv.local_elems, C.c_int32, sv.n_local_elems),
+            "node_owned": _arr(sv.node_owned, C.c_uint8, sv.n_local_nodes).astype(bool),
+            "layer_bounds": _arr(sv.layer_bounds, C.c_int32, sv.world + 1),
+        }
+        self.pd_local_dofs = (self.shard["local_nodes"][:, None] * self.dim
+                              + np.arange(self.dim)[None, :]).reshape(-1)
+
+    def comm_init(self, uid: bytes):
+        """Join the NCCL clique of a sharded run (uid: pmts_nccl_unique_id of shard 0)."""
+        buf = C.create_string_buffer(uid, 128)
+        check(lib().pmts_mts_comm_init(self.h, buf))
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -125,7 +146,9 @@ class MtsSolver:
         return ms.value
 
     def state(self, which: str):
-        n = self.fe_n_dof if which == "fe" else self.pd_n_dof
+        """(u, v, a) of the FE or PD subdomain; a PD shard returns its local dofs
+        (self.pd_local_dofs order)."""
+        n = self.fe_n_dof if which == "fe" else len(self.pd_local_dofs)
         u, v, a = np.empty(n), np.empty(n), np.empty(n)
         check(lib().pmts_mts_get_state(self.h, 0 if which == "fe" else 1, ptr(u), ptr(v), ptr(a)))
         return u, v, a
@@ -147,3 +170,68 @@ class MtsSolver:
         check(lib().pmts_mts_damage(self.h, ptr(e), ptr(n)))
         return e, n
 
+
+
+class ShardGroup:
+    """The PD shards of one coupled run driven from one process: one
+    handle per shard on `devices` (all on one GPU by default -- the shards exchange
+    through device copies at host barriers, no kernel waits on another), stepped
+    together; the assembled outputs compare one-to-one with a single-domain MtsSolver."""
+
+    def __init__(self, sc: dict, world: int, devices=None):
+        devices = list(devices or [0] * world)
+        self.world = world
+        self.shards = [MtsSolver(sc, device=devices[r], shard=(r, world)) for r in range(world)]
+        self._arr = (C.c_void_p * world)(*[s.h.value for s in self.shards])
+        check(lib().pmts_mts_group_join(self._arr, world))
+        r0 = self.shards[0]
+        self.dim, self.fe_n_dof, self.pd_n_dof = r0.dim, r0.fe_n_dof, r0.pd_n_dof
+        self.n_lambda, self.n_elems, self.n_nodes = r0.n_lambda, r0.n_elems, r0.n_nodes
+
+    def initialize(self):
+        check(lib().pmts_mts_group_init(self._arr, self.world))
+
+    def macro_step(self, n: int = 1) -> list[dict]:
+        reps = (capi.MtsReport * max(n, 1))()
+        check(lib().pmts_mts_group_macro_step(self._arr, self.world, n, reps))
+        return [{f: getattr(r, f) for f, _ in capi.MtsReport._fields_} for r in reps[:n]]
+
+    def state(self, which: str):
+        if which == "fe":
+            return self.shards[0].state("fe")
+        out = [np.full(self.pd_n_dof, np.nan) for _ in range(3)]
+        for s in self.shards:
+            own = np.repeat(s.shard["node_owned"], self.dim)
+            dofs = s.pd_local_dofs[own]
+            for o, x in zip(out, s.state("pd")):
+                o[dofs] = x[own]
+        return tuple(out)
+
+    def lam(self):
+        return self.shards[0].lam()
+
+    def pairs_intact(self):
+        """{(i, j): intact} over every bond, each taken from the shard owning i."""
+        out = {}
+        for s in self.shards:
+            sy = s.system()
+            lo, hi = s.shard["own_elems"]
+            le = s.shard["local_elems"]
+            # local element index of each pair's first element (global ids -> PD-active)
+            pa = np.flatnonzero(sy["labels"] != 0)  # PD-active elements, ascending
+            g2l = {int(pa[e]): k for k, e in enumerate(le)}
+            it = s.intact()
+            for (i, j), v in zip(sy["pairs"], it):
+                k = g2l[int(i)]
+                if lo <= k < hi:
+                    out[(int(i), int(j))] = int(v)
+        return out
+
+    def damage_field(self):
+        e = np.zeros(self.n_elems)
+        n = np.zeros(self.n_nodes)
+        for s in self.shards:
+            de, dn = s.damage_field()
+            e += de
+            n += dn
+        return e, n
