@@ -240,6 +240,17 @@ def scenarios() -> dict:
         "ext": {},
     }
     s["mts_bar3d"] = m3
+    # the same bar 8 mm deep (8 element layers along z, the slowest axis): a 3D coupled
+    # run that two PD shards can split (tests/test_gpu_mts_shards.py), with fracture
+    m3t = copy.deepcopy(m3)
+    m3t["mesh"]["bounds"] = [0, 0, 0, 0.012, 0.004, 0.008]
+    m3t["region"]["pd_box1"] = [0.004, 0.0, 0.0, 0.008, 0.004, 0.008]
+    m3t["load"] = {"traction1": [0.012 - 1e-7, -0.001, -0.001, 0.012 + 1e-7, 0.005, 0.009,
+                                 30e6, 0.0, 0.0],
+                   "fixed1": [-1e-7, -0.001, -0.001, 1e-7, 0.005, 0.009]}
+    m3t["pd"]["s_crit"] = 1e-4
+    m3t["time"]["total_time"] = 2e-8 * 2 * 40
+    s["mts_bar3d_tall"] = m3t
 
     # BASELINE cfg2, conforming analog: the cfg1 plate and
     # material, PD band 100 x 20 mm in the middle, FE elsewhere -- both at 0.25 mm
