@@ -558,6 +558,40 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
     return out
 
 
+def bench_mts_sharded(args):
+    """Coupled MTS with the PD band sharded across N GPUs (north star item 5; DESIGN.md
+    9a): shard r on GPU r, ghost layers over NCCL every fine substep, FE on rank 0, the
+    interface solve replicated (the reference's plain CG: the Jacobi option is single-
+    domain only).  Device time of K macro steps per rank (CUDA events), max over ranks."""
+    from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200.mts import MtsSolver
+
+    ctx = Ctx(False)
+    c = cf.get("cfg2")
+    c["run"]["interface"] = "matrix_free"
+    t0 = time.perf_counter()
+    s = MtsSolver(c, device=ctx.local, shard=(ctx.rank, ctx.world))
+    s.comm_init(ctx.uid())
+    s.initialize()
+    setup = ctx.reduce(time.perf_counter() - t0)
+    s.macro_step(args.warmup)
+    ctx.barrier()
+    ms = ctx.reduce(s.macro_step_timed(args.steps))
+    if ctx.rank == 0:
+        v = args.steps / (ms * 1e-3)
+        print(json.dumps({
+            "metric": MTS_METRIC, "value": v, "unit": MTS_UNIT, "n_gpus": ctx.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "gpu_launches": None,
+            "config": {"workload": "cfg2 conforming analog, PD band sharded in y slabs "
+                                   "(DESIGN.md 9a), interface plain CG", "setup_s": setup,
+                       "parallelism": f"pd_shards{ctx.world}",
+                       "pd_local_elems": len(s.shard["local_elems"]),
+                       "pd_layers": s.shard["n_layers"]}}), flush=True)
+    del s
+
+
 def bench_native(args):
     from paper_2403_03605_b200 import capi
 
@@ -664,6 +698,9 @@ def main():
         raise SystemExit(_spawn_ranks(args))
     if "WORLD_SIZE" in os.environ and _env_rank()[2] != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {_env_rank()[2]}")
+    if args.workload == "cfg2" and args.impl != "reference" and _env_rank()[2] > 1:
+        bench_mts_sharded(args)  # the PD band sharded across the ranks
+        return
     if args.workload == "cfg2":  # the coupled MTS metric as its own line
         rank, _, _ = _env_rank()
         if rank != 0:
