@@ -338,6 +338,10 @@ typedef struct {
                                     pmts_mts_comm_init (NCCL, one process per GPU), then
                                     pmts_mts_init / pmts_mts_group_init.  0 or 1: one domain */
     int32_t shard_rank;
+    int32_t interface_h_fe;      /* matrix-free interface with an explicit FE side: 0 (default)
+                                    = H_FE as a direct sparse product, bitwise the unit
+                                    columns, no n_lambda^2 scratch; 1 = the unit columns
+                                    (unit_fe_column, mts.hpp:389-397) through the scratch */
 } pmts_mts_desc;
 
 typedef struct {

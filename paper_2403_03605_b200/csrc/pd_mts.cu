@@ -1105,6 +1105,60 @@ __global__ void k_row_fill(int n, const double* D, const int* rp, int32_t* ci, d
         }
     }
 }
+// H_FE of an explicit FE side as a sparse product, entry by entry bitwise the unit-column
+// construction (unit_row -> explicit solve -> G_FE gather -> negate; build_h_fe): column
+// k's FE velocity is vel_k[d] = 0 + gdt ((-w_kd) / M_d) on the unconstrained dofs of row
+// k and +0 elsewhere, and row r's gather sums w_rj vel_k[ci_j] left to right -- the zero
+// terms change no nonzero partial sum, so only the shared dofs are visited.  Warp per
+// row; candidates (rows sharing an unconstrained FE dof with r) ascending.
+__global__ void k_hfe_explicit(int nl, const long long* crp, const int32_t* cci,
+                               const int32_t* grp, const int32_t* gci, const double* gw,
+                               const double* M, const uint8_t* cf, double gdt, double* vals) {
+    const int r = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= nl) return;
+    const int j0 = grp[r], j1 = grp[r + 1];
+    for (long long q = crp[r] + lane; q < crp[r + 1]; q += 32) {
+        const int k = cci[q];
+        const int k0 = grp[k], k1 = grp[k + 1];
+        double acc = 0.0;
+        for (int j = j0; j < j1; ++j) {
+            const int d = gci[j];
+            if (cf[d]) continue;
+            for (int i = k0; i < k1; ++i)
+                if (gci[i] == d) {
+                    const double x = 0.0 + gdt * ((-gw[i]) / M[d]);
+                    if (x != 0.0) acc = acc + gw[j] * x;
+                    break;
+                }
+        }
+        vals[q] = -acc;
+    }
+}
+__global__ void k_nz_count(int n, const long long* rp, const double* v, int* cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) {
+        cnt[n] = 0;
+        return;
+    }
+    int c = 0;
+    for (long long q = rp[r]; q < rp[r + 1]; ++q) c += v[q] != 0.0 ? 1 : 0;
+    cnt[r] = c;
+}
+__global__ void k_nz_fill(int n, const long long* rp, const int32_t* ci, const double* v,
+                          const int32_t* orp, int32_t* oci, double* ov) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int o = orp[r];
+    for (long long q = rp[r]; q < rp[r + 1]; ++q)
+        if (v[q] != 0.0) {
+            oci[o] = ci[q];
+            ov[o] = v[q];
+            ++o;
+        }
+}
+
 // Jacobi preconditioner of the interface CG: diag(H_FE) + m dt / (2 M_PD)
 __global__ void k_iface_jac(int n, const double* D, int m, double dt_pd, const int32_t* cpd,
                             const double* Mpd, double* jd) {
@@ -1189,6 +1243,24 @@ void unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int
 void unit_vec(int n, int k, double* x, cudaStream_t s) {
     k_unit_vec<<<blocks(n), kT, 0, s>>>(n, k, x);
     check("unit_vec");
+}
+void hfe_explicit(int nl, const long long* crp, const int32_t* cci, const int32_t* grp,
+                  const int32_t* gci, const double* gw, const double* M, const uint8_t* cf,
+                  double gdt, double* vals, cudaStream_t s) {
+    if (nl <= 0) return;
+    k_hfe_explicit<<<(unsigned)(((long long)nl * 32 + kT - 1) / kT), kT, 0, s>>>(
+        nl, crp, cci, grp, gci, gw, M, cf, gdt, vals);
+    check("hfe_explicit");
+}
+void nz_count(int n, const long long* rp, const double* v, int* cnt, cudaStream_t s) {
+    k_nz_count<<<blocks(n + 1), kT, 0, s>>>(n, rp, v, cnt);
+    check("nz_count");
+}
+void nz_fill(int n, const long long* rp, const int32_t* ci, const double* v, const int32_t* orp,
+             int32_t* oci, double* ov, cudaStream_t s) {
+    if (n <= 0) return;
+    k_nz_fill<<<blocks(n), kT, 0, s>>>(n, rp, ci, v, orp, oci, ov);
+    check("nz_fill");
 }
 void transpose(int n, const double* D, double* H, cudaStream_t s) {
     k_transpose<<<blocks((long long)n * n), kT, 0, s>>>(n, D, H);

@@ -114,6 +114,14 @@ void add_col_gather(int n, int k, const int32_t* idx, const double* x, double* H
 void unit_row(int nf, const int32_t* rp, const int32_t* ci, const double* w, int k, double* ra,
               cudaStream_t s);
 void unit_vec(int n, int k, double* x, cudaStream_t s);
+// H_FE of an explicit FE side directly as CSR (candidates crp / cci, values bitwise the
+// unit-column construction; exact zeros kept), then the nonzeros counted / compacted
+void hfe_explicit(int nl, const long long* crp, const int32_t* cci, const int32_t* grp,
+                  const int32_t* gci, const double* gw, const double* M, const uint8_t* cf,
+                  double gdt, double* vals, cudaStream_t s);
+void nz_count(int n, const long long* rp, const double* v, int* cnt, cudaStream_t s);
+void nz_fill(int n, const long long* rp, const int32_t* ci, const double* v, const int32_t* orp,
+             int32_t* oci, double* ov, cudaStream_t s);
 void transpose(int n, const double* D, double* H, cudaStream_t s);
 void row_nnz(int n, const double* D, int* cnt, cudaStream_t s);
 void row_fill(int n, const double* D, const int* rp, int32_t* ci, double* v, cudaStream_t s);

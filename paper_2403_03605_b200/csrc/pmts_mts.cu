@@ -697,7 +697,13 @@ struct pmts_mts {
     // interface) or the exact nonzeros in CSR (matrix-free interface: each unit column
     // is a CG solve whose support grows one stiffness neighbourhood per iteration, and
     // disconnected FE parts never couple -- lossless) are extracted on the device
+    bool hfe_unit_columns = false;  // pmts_mts_desc.interface_h_fe = 1
     void build_h_fe() {
+        if (fe_nm.explicit_scheme() && !use_dense && iface_mode != 1 && !interface_precond &&
+            !hfe_unit_columns) {
+            build_h_fe_explicit();
+            return;
+        }
         // (the column-major scratch is n_lambda^2 doubles: refuse what cannot fit)
         {
             size_t free_b = 0, total_b = 0;
@@ -780,6 +786,99 @@ struct pmts_mts {
         }
         CKM(cudaFreeAsync(D, stream));
         CKM(cudaStreamSynchronize(stream));
+    }
+    // H_FE of an explicit FE side (M_block = the lumped mass) without unit columns: row r
+    // couples to the rows k sharing an unconstrained FE dof with it, H_FE[r][k] =
+    // -sum_j w_rj gdt (-w_kd) / M_d -- computed entry by entry exactly as the unit-column
+    // construction rounds it (k_hfe_explicit), exact zeros dropped; no n_lambda^2 scratch
+    // (BASELINE cfg5's 1.8M multipliers).  The candidate structure is host work in
+    // parallel row chunks.
+    void build_h_fe_explicit() {
+        const std::vector<int32_t>& grp = s.cpl_fe_rp;
+        const std::vector<int32_t>& gci = s.cpl_fe_ci;
+        std::vector<uint8_t> cfh(nf, 0);
+        for (int32_t d : s.fe_bc_dofs) cfh[d] = 1;
+        std::vector<int64_t> drp(nf + 1, 0);  // unconstrained FE dof -> rows (ascending)
+        for (int r = 0; r < nl; ++r)
+            for (int j = grp[r]; j < grp[r + 1]; ++j)
+                if (!cfh[gci[j]]) ++drp[gci[j] + 1];
+        for (int d = 0; d < nf; ++d) drp[d + 1] += drp[d];
+        std::vector<int32_t> dri(drp[nf]);
+        {
+            std::vector<int64_t> f(drp.begin(), drp.end() - 1);
+            for (int r = 0; r < nl; ++r)
+                for (int j = grp[r]; j < grp[r + 1]; ++j)
+                    if (!cfh[gci[j]]) dri[f[gci[j]]++] = r;
+        }
+        const int nth = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+        auto rows_of = [&](int r, std::vector<int32_t>& out) {
+            out.clear();
+            for (int j = grp[r]; j < grp[r + 1]; ++j) {
+                const int d = gci[j];
+                if (cfh[d]) continue;
+                out.insert(out.end(), dri.begin() + drp[d], dri.begin() + drp[d + 1]);
+            }
+            std::sort(out.begin(), out.end());
+            out.erase(std::unique(out.begin(), out.end()), out.end());
+        };
+        auto parallel = [&](auto&& fn) {
+            std::vector<std::thread> th;
+            for (int t = 0; t < nth; ++t)
+                th.emplace_back([&, t] {
+                    std::vector<int32_t> tmp;
+                    for (int r = int((long long)nl * t / nth); r < int((long long)nl * (t + 1) / nth); ++r)
+                        fn(r, tmp);
+                });
+            for (auto& x : th) x.join();
+        };
+        std::vector<long long> crp(nl + 1, 0);
+        parallel([&](int r, std::vector<int32_t>& tmp) {
+            rows_of(r, tmp);
+            crp[r + 1] = (long long)tmp.size();
+        });
+        for (int r = 0; r < nl; ++r) crp[r + 1] += crp[r];
+        std::vector<int32_t> cci(crp[nl]);
+        parallel([&](int r, std::vector<int32_t>& tmp) {
+            rows_of(r, tmp);
+            std::copy(tmp.begin(), tmp.end(), cci.begin() + crp[r]);
+        });
+        const long long nc = crp[nl];
+        long long* d_crp = nullptr;
+        int32_t* d_cci = nullptr;
+        double* d_val = nullptr;
+        int* cnt = nullptr;
+        CKM(cudaMallocAsync(&d_crp, sizeof(long long) * (nl + 1), stream));
+        CKM(cudaMallocAsync(&d_cci, sizeof(int32_t) * std::max(nc, 1LL), stream));
+        CKM(cudaMallocAsync(&d_val, sizeof(double) * std::max(nc, 1LL), stream));
+        CKM(cudaMallocAsync(&cnt, sizeof(int) * ((size_t)nl + 1), stream));
+        CKM(cudaMemcpyAsync(d_crp, crp.data(), sizeof(long long) * (nl + 1), cudaMemcpyHostToDevice,
+                            stream));
+        if (nc)
+            CKM(cudaMemcpyAsync(d_cci, cci.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice,
+                                stream));
+        mtsk::hfe_explicit(nl, d_crp, d_cci, gfe_rp, gfe_ci, gfe_w, fe_M, fe_cf, fe_nm.gdt, d_val,
+                           stream);
+        mtsk::nz_count(nl, d_crp, d_val, cnt, stream);
+        std::vector<int> hc(nl + 1);
+        CKM(cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * ((size_t)nl + 1), cudaMemcpyDeviceToHost,
+                            stream));
+        CKM(cudaStreamSynchronize(stream));
+        std::vector<int32_t> rp(nl + 1, 0);
+        long long tot = 0;
+        for (int r = 0; r < nl; ++r) {
+            tot += hc[r];
+            if (tot > INT32_MAX) throw ConfigError("H_FE has more than 2^31 nonzeros");
+            rp[r + 1] = int32_t(tot);
+        }
+        hfe_nnz = rp[nl];
+        hfe_rp = upload(rp);
+        hfe_ci = alloc<int32_t>(std::max<int64_t>(hfe_nnz, 1));
+        hfe_v = alloc<double>(std::max<int64_t>(hfe_nnz, 1));
+        mtsk::nz_fill(nl, d_crp, d_cci, d_val, hfe_rp, hfe_ci, hfe_v, stream);
+        for (void* p : {(void*)d_crp, (void*)d_cci, (void*)d_val, (void*)cnt})
+            CKM(cudaFreeAsync(p, stream));
+        CKM(cudaStreamSynchronize(stream));
+        invalidate_cg_graphs();
     }
     // H = H_FE + G_PD vel(Y_PD) (mts.hpp:422-445) and its LU factor, on the device
     void refresh_dense_interface() {
@@ -1641,6 +1740,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->iface_mode = desc->interface_mode;
         h->interface_precond = desc->interface_precond != 0;
         h->iface_precompute = desc->interface_recursion == 0;
+        h->hfe_unit_columns = desc->interface_h_fe == 1;
         // interface mode (mts.hpp:111-114); the PD side is explicit
         h->use_dense = h->iface_mode == 1 || (h->iface_mode == 0 && h->nl <= 400);
         if (desc->shard_world > 1) {  // the shard plan (host; a host-only handle exposes it)

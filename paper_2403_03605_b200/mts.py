@@ -65,6 +65,8 @@ class MtsSolver:
         d.interface_precond = 1 if run.get("interface_precond", "none") == "jacobi" else 0
         # run.interface_h_pd = precompute (default) | recursion
         d.interface_recursion = 1 if run.get("interface_h_pd", "precompute") == "recursion" else 0
+        # run.interface_h_fe = sparse (default) | unit_columns (explicit FE side)
+        d.interface_h_fe = 1 if run.get("interface_h_fe", "sparse") == "unit_columns" else 0
         if shard is not None:
             d.shard_rank, d.shard_world = int(shard[0]), int(shard[1])
         h = C.c_void_p()

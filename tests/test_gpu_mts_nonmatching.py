@@ -74,3 +74,28 @@ def test_3d_nonmatching_bar_runs():
                     for r in range(len(rp) - 1)])
     gpd = s.state("pd")[1][sy["pd_dof"]]
     assert np.abs(gfe - gpd).max() <= 1e-8 * max(1.0, np.abs(gpd).max())
+
+
+@pytest.mark.parametrize("name,fe,steps", [("mts_nm_strip", 1e-3, 40), ("mts_nm_strip", 5e-4, 40),
+                                           ("cfg2_nm", None, 5)])
+def test_sparse_explicit_h_fe_bitwise_unit_columns(name, fe, steps):
+    """An explicit FE side's H_FE built directly as a sparse product (the default, no
+    n_lambda^2 scratch: what BASELINE cfg5's 1.8M multipliers need) is bitwise the
+    unit-column construction: same multipliers, states and iteration counts."""
+    out = {}
+    for mode in ("sparse", "unit_columns"):
+        sc = cf.get(name)
+        if fe:
+            sc["mesh"]["fe_spacing"] = fe
+        sc["run"]["interface"] = "matrix_free"
+        sc["run"]["interface_h_fe"] = mode
+        s = MtsSolver(sc)
+        s.initialize()
+        reps = s.macro_step(steps)
+        out[mode] = (s.lam(), s.state("fe"), s.state("pd"),
+                     [(r["interface_iterations"], r["newly_broken"]) for r in reps])
+    a, b = out["sparse"], out["unit_columns"]
+    assert np.array_equal(a[0], b[0]) and a[3] == b[3]
+    for w in (1, 2):
+        for x, y in zip(a[w], b[w]):
+            assert np.array_equal(x, y)
