@@ -304,6 +304,43 @@ def scenarios() -> dict:
         "ext": {},
     }
     s["mts_nm_strip"] = cv
+    # BASELINE cfg5 (configs[4]) as a coupled run: 400 x 200 x 10 mm plate, the PD core
+    # 100 x 200 x 10 mm in the middle at 0.25 mm (400 x 800 x 40 = 12.8M hexes), FE hex8 at
+    # 1 mm elsewhere (non-matching), 2 mm linear gluing zones inside the
+    # core's x faces, explicit central-difference FE (dt_fe = 80 ns), m = 20 (dt_pd = 4
+    # ns), a 40 mm through-thickness pre-notch at mid-height from the core's left face,
+    # 12 MPa on the top / bottom faces, 100 coarse steps.  The coupled model's kernel is
+    # the reference's calibrated exponential one (its coupled integrator has no other).
+    d5 = 3.015 * 2.5e-4
+    c5m = {
+        "mesh": {"kind": "generated", "dim": 3, "bounds": [0, 0, 0, 0.4, 0.2, 0.01],
+                 "spacing": 2.5e-4, "fe_spacing": 1e-3,
+                 "notch1": [0.15, 0.1, -0.001, 0.19, 0.1, -0.001, 0.19, 0.1, 0.011,
+                            0.15, 0.1, 0.011]},
+        "material": {"E": _E, "nu": 0.25, "rho": _RHO, "formulation": "three_d"},
+        "pd": {"delta_factor": 3.015, "l_factor": 1.0,
+               "s_crit": round(s0_3d(_E, 0.25, _G0, d5), 7)},
+        "region": {"pd_box1": [0.15, 0.0, 0.0, 0.25, 0.2, 0.01],
+                   "overlap_width_factor": 8.0, "weight_kind": "linear"},
+        "load": {"traction1": [-1, 0.2 - 1e-7, -1, 1, 0.2 + 1e-7, 1, 0, 12e6, 0],
+                 "traction2": [-1, -1e-7, -1, 1, 1e-7, 1, 0, -12e6, 0]},
+        "time": {"dt_pd": 4e-9, "m": 20, "total_time": 8e-8 * 100, "gamma_fe": 0.5,
+                 "beta_fe": 0.0, "gamma_pd": 0.5, "beta_pd": 0.0},
+        "run": {"mode": "coupled_mts", "interface": "auto"},
+        "output": {"interval": 0.0},
+        "ext": {},
+    }
+    s["cfg5_mts"] = c5m
+    # its small twin (tests): 20 x 10 x 2 mm plate, 8 mm PD core at 0.25 mm, FE 1 mm
+    c5t = copy.deepcopy(c5m)
+    c5t["mesh"]["bounds"] = [0, 0, 0, 0.02, 0.01, 0.002]
+    c5t["mesh"]["notch1"] = [0.006, 0.005, -0.001, 0.009, 0.005, -0.001, 0.009, 0.005,
+                             0.003, 0.006, 0.005, 0.003]
+    c5t["region"]["pd_box1"] = [0.006, 0.0, 0.0, 0.014, 0.01, 0.002]
+    c5t["load"] = {"traction1": [-1, 0.01 - 1e-7, -1, 1, 0.01 + 1e-7, 1, 0, 12e6, 0],
+                   "traction2": [-1, -1e-7, -1, 1, 1e-7, 1, 0, -12e6, 0]}
+    c5t["time"]["total_time"] = 8e-8 * 20
+    s["cfg5_mts_small"] = c5t
     return s
 
 

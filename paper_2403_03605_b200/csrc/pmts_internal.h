@@ -1,9 +1,13 @@
 // Internal helpers shared by the host translation units of libpmts.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <exception>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/pmts_capi.h"
 
@@ -22,6 +26,32 @@ struct InternalError : std::runtime_error {
 };
 
 void set_last_error(const std::string& msg);
+
+// f(i) for i in [0, n) over the host's cores (independent iterations); the first
+// exception is rethrown
+template <class F>
+void par_range(int n, F&& f) {
+    const int nth = int(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
+    if (n < 4096 || nth == 1) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(nth);
+    for (int t = 0; t < nth; ++t)
+        th.emplace_back([&, t] {
+            try {
+                for (int i = int((long long)n * t / nth); i < int((long long)n * (t + 1) / nth); ++i)
+                    f(i);
+            } catch (...) {
+                err[t] = std::current_exception();
+            }
+        });
+    for (auto& x : th) x.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
 
 template <class F>
 int guard(F&& f) {

@@ -968,11 +968,34 @@ struct pmts_mts {
             }
             return d2;
         };
+        const int dzr = dim == 3 ? 1 : 0;
+        {   // a sampled estimate of the build: too large (BASELINE cfg5: ~1.8M multipliers,
+            // R ~ 23 mm -> ~10^11 column entries) -> the recursion form from the start
+            double s1 = 0.0, s2 = 0.0;
+            const int ns = std::min(nl, 64);
+            for (int q = 0; q < ns; ++q) {
+                const int k = int((long long)q * nl / ns);
+                for (int dz = -dzr; dz <= dzr; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            auto it = grid.find(key(k, dx, dy, dz));
+                            if (it == grid.end()) continue;
+                            for (int r : it->second) {
+                                const double d2 = dist2(k, r);
+                                s1 += d2 <= R * R ? 1.0 : 0.0;
+                                s2 += d2 < 4.0 * R * R ? 1.0 : 0.0;
+                            }
+                        }
+            }
+            if (ns && (s1 / ns * nl > 3e8 || s2 / ns * nl > 3e9)) {
+                iface_precompute = false;  // (the m-substep recursion in every CG iteration)
+                return;
+            }
+        }
         // rows within R of each source (the column structure) and within 2R (conflicts)
         std::vector<std::vector<int>> near(nl);  // rows within R, ascending
         std::vector<int> colour(nl, -1);
         std::vector<int> forbid;
-        const int dzr = dim == 3 ? 1 : 0;
         for (int k = 0; k < nl; ++k) {
             forbid.clear();
             for (int dz = -dzr; dz <= dzr; ++dz)
@@ -1860,17 +1883,19 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         h->npe = int(npairs);
         h->pairs.resize(cp.size());
         h->pe_weight.resize(npairs);
-        for (int64_t p = 0; p < npairs; ++p) {
-            const int gi = s.pd_active[lel[cp[2 * p]]], gj = s.pd_active[lel[cp[2 * p + 1]]];
-            h->pairs[2 * p] = gi;
-            h->pairs[2 * p + 1] = gj;
+        if (npairs > INT32_MAX) throw ConfigError("more than 2^31 PD bonds");
+        par_range(int(npairs), [&](int p) {
+            const int gi = s.pd_active[lel[cp[2 * (size_t)p]]];
+            const int gj = s.pd_active[lel[cp[2 * (size_t)p + 1]]];
+            h->pairs[2 * (size_t)p] = gi;
+            h->pairs[2 * (size_t)p + 1] = gj;
             double mid[3];
             for (int k = 0; k < 3; ++k)
                 mid[k] = 0.5 * (s.centroid[3 * (size_t)gi + k] + s.centroid[3 * (size_t)gj + k]);
             const double w = 1.0 - mts_alpha_at(s, mid);  // perifem.hpp:320-326
             if (w < 0.0) throw InternalError("negative PD weight at a bond midpoint");
             h->pe_weight[p] = w;
-        }
+        });
         pd_internal_pair_weights(h->pd, h->pe_weight.data());
         h->pdv = pd_internal_dev(h->pd);
         h->mask_live = h->pdv.mask;

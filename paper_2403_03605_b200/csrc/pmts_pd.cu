@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -271,8 +272,8 @@ void finish_families(pmts_pd* h, int K) {
     h->d.W = std::max(1, (K + 31) / 32);
     std::vector<double> coef((size_t)K * E, 0.0);
     std::vector<uint32_t> mask((size_t)h->d.W * E, 0u);
-    int64_t F = 0;
-    for (int e = 0; e < E; ++e)
+    std::vector<int32_t> nent(E, 0);
+    par_range(E, [&](int e) {  // (per element: independent entries, host cores)
         for (int k = 0; k < K; ++k) {
             const int p = h->hcol[(size_t)k * E + e];
             if (p < 0) break;
@@ -285,8 +286,11 @@ void finish_families(pmts_pd* h, int K) {
             const double c = micromodulus(h->desc, h->dim, xin);
             coef[(size_t)k * E + e] = c * w;
             mask[(size_t)(k >> 5) * E + e] |= 1u << (k & 31);
-            ++F;
+            ++nent[e];
         }
+    });
+    int64_t F = 0;
+    for (int e = 0; e < E; ++e) F += nent[e];
     h->n_entries = F;
     if (h->d.coef) h->release((void*)h->d.coef);
     if (h->d.mask) h->release(h->d.mask);
@@ -1212,35 +1216,47 @@ void pd_internal_pair_weights(pmts_pd* h, const double* w) {
     require_families(h);
     ensure_hcol(h);
     const int E = h->E, K = h->d.K;
-    std::vector<int64_t> first(E + 1, 0);
-    for (int e = 0; e < E; ++e) {
-        int64_t c = 0;
+    const int32_t* col = h->hcol.data();
+    // per element: family length and the partners below it (families ascend, so the
+    // upper partners of i are its entries below[i] .. len[i] - 1, in pair order)
+    std::vector<int32_t> len(E), below(E);
+    par_range(E, [&](int e) {
+        int n = 0, b = 0;
         for (int k = 0; k < K; ++k) {
-            const int p = h->hcol[(size_t)k * E + e];
+            const int p = col[(size_t)k * E + e];
             if (p < 0) break;
-            if (p > e) ++c;
+            ++n;
+            if (p < e) ++b;
         }
-        first[e + 1] = first[e] + c;
-    }
+        len[e] = n;
+        below[e] = b;
+    });
+    std::vector<int64_t> first(E + 1, 0);
+    for (int e = 0; e < E; ++e) first[e + 1] = first[e] + (len[e] - below[e]);
     std::vector<double> coef((size_t)K * E, 0.0);
-    for (int e = 0; e < E; ++e)
-        for (int k = 0; k < K; ++k) {
-            const int p = h->hcol[(size_t)k * E + e];
-            if (p < 0) break;
-            const int i = std::min(e, p), j = std::max(e, p);
-            // rank of j among i's upper partners (ascending ELL)
-            int64_t idx = first[i];
-            for (int q = 0; q < K; ++q) {
-                const int pq = h->hcol[(size_t)q * E + i];
-                if (pq < 0 || pq >= j) break;
-                if (pq > i) ++idx;
+    par_range(E, [&](int e) {
+        for (int k = 0; k < len[e]; ++k) {
+            const int p = col[(size_t)k * E + e];
+            int64_t idx;  // the pair's index: rank of j among i's upper partners
+            if (p > e) {
+                idx = first[e] + (k - below[e]);
+            } else {  // e in p's ascending family
+                int lo = below[p], hi = len[p];
+                while (lo < hi) {
+                    const int mid = (lo + hi) / 2;
+                    if (col[(size_t)mid * E + p] < e) lo = mid + 1;
+                    else hi = mid;
+                }
+                idx = first[p] + (lo - below[p]);
             }
+            const int i = std::min(e, p), j = std::max(e, p);
             double xi[3];
             for (int c = 0; c < 3; ++c) xi[c] = h->cen[3 * (size_t)j + c] - h->cen[3 * (size_t)i + c];
             const double xin = std::sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
             const double wv = w[idx] * (h->vol[i] * h->vol[j]);
             coef[(size_t)k * E + e] = wv * micromodulus(h->desc, h->dim, xin);
         }
+    });
     upload(const_cast<double*>(h->d.coef), coef.data(), coef.size(), h->stream);
     CK(cudaStreamSynchronize(h->stream));
 }

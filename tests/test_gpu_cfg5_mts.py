@@ -1,0 +1,41 @@
+"""BASELINE cfg5 as a coupled run (configs.py cfg5_mts: 3D plate, 0.25 mm PD core,
+1 mm hex8 FE, m = 20, explicit FE) -- its small twin on the device: the coupled step
+holds velocity continuity, stays finite, breaks bonds at the notch, and two PD shards
+reproduce it bit for bit.  The at-size run is bench.py --workload
+cfg5_mts (profiles/)."""
+import copy
+
+import numpy as np
+import pytest
+
+from paper_2403_03605_b200 import configs as cf
+from paper_2403_03605_b200.mts import MtsSolver, ShardGroup
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cfg5_twin_coupled_run():
+    s = MtsSolver(cf.get("cfg5_mts_small"))
+    s.initialize()
+    reps = s.macro_step(20)
+    assert max(r["continuity"] for r in reps) <= 1e-8
+    for w in ("fe", "pd"):
+        for x in s.state(w):
+            assert np.isfinite(x).all()
+    assert np.abs(s.state("pd")[0]).max() > 0
+
+
+def test_cfg5_twin_shards_bitwise():
+    c = copy.deepcopy(cf.get("cfg5_mts_small"))
+    one = MtsSolver(c)
+    one.initialize()
+    grp = ShardGroup(c, 2)
+    grp.initialize()
+    r1, rg = one.macro_step(10), grp.macro_step(10)
+    for a, b in zip(r1, rg):
+        for f in ("newly_broken", "interface_iterations", "continuity", "lambda_fe", "lambda_pd"):
+            assert a[f] == b[f], f
+    assert np.array_equal(one.lam(), grp.lam())
+    for w in ("fe", "pd"):
+        for x, y in zip(one.state(w), grp.state(w)):
+            assert np.array_equal(x, y)
