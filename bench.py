@@ -558,6 +558,43 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
     return out
 
 
+def bench_cfg5_mts(steps: int, warmup: int) -> dict:
+    """BASELINE cfg5 (configs[4]) as the coupled run it describes (configs.py cfg5_mts:
+    12.8M-hex PD core at 0.25 mm, 1 mm hex8 FE, m = 20, 1.77M multipliers) on one GPU:
+    setup time, then K macro steps (CUDA events), the interface operator in its
+    recursion form (the precomputed H_PD would be ~10^11 entries)."""
+    import torch
+
+    from paper_2403_03605_b200 import configs as cf
+    from paper_2403_03605_b200.mts import MtsSolver
+
+    t0 = time.perf_counter()
+    s = MtsSolver(cf.get("cfg5_mts"))
+    t1 = time.perf_counter()
+    s.initialize()
+    setup = time.perf_counter() - t0
+    free_b, total_b = torch.cuda.mem_get_info(0)
+    reps = s.macro_step(warmup)
+    ms = s.macro_step_timed(steps)
+    last = s.macro_step(1)[0]
+    u = s.state("pd")[0]
+    return {"metric": MTS_METRIC, "unit": MTS_UNIT, "value": steps / (ms * 1e-3),
+            "ms_per_step": ms / steps, "steps": steps, "warmup": warmup, "n_gpus": 1,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "BASELINE cfg5 coupled: 400x200x10 mm plate, PD core "
+                                   "100x200x10 mm at 0.25 mm (12.8M hexes), FE hex8 1 mm "
+                                   "(non-matching), 2 mm linear gluing zones, explicit FE, "
+                                   "m=20, dt_pd 4 ns, 40 mm pre-notch, 12 MPa",
+                       "n_lambda": s.n_lambda, "fe_dof": s.fe_n_dof, "pd_dof": s.pd_n_dof,
+                       "pd_pairs": int(s.n_pairs), "create_s": t1 - t0, "setup_s": setup,
+                       "device_mem_used_gb": (total_b - free_b) / 1e9},
+            "interface_iterations": [r["interface_iterations"] for r in reps] +
+                                    [last["interface_iterations"]],
+            "continuity_max": max(r["continuity"] for r in reps + [last]),
+            "newly_broken": [r["newly_broken"] for r in reps] + [last["newly_broken"]],
+            "pd_u_max": float(abs(u).max())}
+
+
 def bench_mts_sharded(args):
     """Coupled MTS with the PD band sharded across N GPUs (north star item 5; DESIGN.md
     9a): shard r on GPU r, ghost layers over NCCL every fine substep, FE on rank 0, the
@@ -700,6 +737,10 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {_env_rank()[2]}")
     if args.workload == "cfg2" and args.impl != "reference" and _env_rank()[2] > 1:
         bench_mts_sharded(args)  # the PD band sharded across the ranks
+        return
+    if args.workload == "cfg5_mts":  # BASELINE cfg5 as a coupled run, at size
+        if _env_rank()[0] == 0:
+            print(json.dumps(bench_cfg5_mts(args.steps, args.warmup)), flush=True)
         return
     if args.workload == "cfg2":  # the coupled MTS metric as its own line
         rank, _, _ = _env_rank()
