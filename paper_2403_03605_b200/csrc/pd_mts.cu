@@ -510,31 +510,31 @@ __global__ void __launch_bounds__(kT) k_pd_force_lin(DevPD d, const double* __re
 // cen_c(p) - cen_c(e) (the subtraction k_pd_force_lin performs) with coalesced
 // loads, where the [k E + e] layout put every lane on its own cache line.
 template <int DIM>
-__global__ void k_family_transpose(DevPD d, int32_t* colT, double* coefT, double* xiT) {
+__global__ void k_family_transpose(DevPD d, int32_t* colT, double* coefT) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // q = e K + k
     if (q >= (long long)d.E * d.K) return;
     const int e = (int)(q / d.K), k = (int)(q % d.K);
     const int p = d.col[(size_t)k * d.E + e];
     colT[q] = p;
     coefT[q] = p >= 0 ? d.coef[(size_t)k * d.E + e] : 0.0;
-    for (int c = 0; c < DIM; ++c)
-        xiT[q * DIM + c] = p >= 0 ? d.cen[(size_t)c * d.E + p] - d.cen[(size_t)c * d.E + e] : 0.0;
 }
 
 // k_pd_force_lin on the entry-major families: the same per-lane arithmetic and
-// warp-tree sum, so bitwise the same G
+// warp-tree sum, so bitwise the same G.  xi = cen_p - cen_e is formed from the
+// centroids (cached gathers) instead of a stored E K dim table: 12 B per entry from
+// HBM instead of 36 (BASELINE cfg5's 1.6e9 entries: 19 GB per substep, not 59)
 template <int DIM>
 __global__ void __launch_bounds__(kT) k_pd_force_lin_t(DevPD d, const int32_t* __restrict__ colT,
                                                        const double* __restrict__ coefT,
-                                                       const double* __restrict__ xiT,
                                                        const double* __restrict__ ub,
                                                        const uint32_t* __restrict__ mask) {
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (e >= d.E) return;
     const int E = d.E, K = d.K;
-    double ue[DIM], G[DIM];
+    double ue[DIM], G[DIM], ce[DIM];
     for (int c = 0; c < DIM; ++c) {
         ue[c] = ub[(size_t)e * DIM + c];
+        ce[c] = d.cen[(size_t)c * E + e];
         G[c] = 0.0;
     }
     for (int k0 = 0; k0 < K; k0 += 32) {
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kT) k_pd_force_lin_t(DevPD d, const int32_t* _
         if (p >= 0 && ((word >> lane) & 1u)) {
             double xi[DIM], dot = 0.0;
             for (int c = 0; c < DIM; ++c) {
-                xi[c] = xiT[q * DIM + c];
+                xi[c] = __ldg(d.cen + (size_t)c * E + p) - ce[c];
                 dot = dot + xi[c] * (ub[(size_t)p * DIM + c] - ue[c]);
             }
             const double t = coefT[q] * dot;
@@ -665,22 +665,22 @@ void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double*
     }
     check("pd_force_lin");
 }
-void family_transpose(const DevPD& d, int32_t* colT, double* coefT, double* xiT, cudaStream_t s) {
+void family_transpose(const DevPD& d, int32_t* colT, double* coefT, cudaStream_t s) {
     const long long n = (long long)d.E * d.K;
     const int b = (int)((n + kT - 1) / kT);
-    if (d.dim == 2) k_family_transpose<2><<<b, kT, 0, s>>>(d, colT, coefT, xiT);
-    else k_family_transpose<3><<<b, kT, 0, s>>>(d, colT, coefT, xiT);
+    if (d.dim == 2) k_family_transpose<2><<<b, kT, 0, s>>>(d, colT, coefT);
+    else k_family_transpose<3><<<b, kT, 0, s>>>(d, colT, coefT);
     check("family_transpose");
 }
-void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* xiT,
-                    const double* x, const uint32_t* mask, double* ubar, cudaStream_t s) {
+void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* x,
+                    const uint32_t* mask, double* ubar, cudaStream_t s) {
     const int b = (int)(((long long)d.E * 32 + kT - 1) / kT);
     if (d.dim == 2) {
         k_pd_ubar<2><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
-        k_pd_force_lin_t<2><<<b, kT, 0, s>>>(d, colT, coefT, xiT, ubar, mask);
+        k_pd_force_lin_t<2><<<b, kT, 0, s>>>(d, colT, coefT, ubar, mask);
     } else {
         k_pd_ubar<3><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
-        k_pd_force_lin_t<3><<<b, kT, 0, s>>>(d, colT, coefT, xiT, ubar, mask);
+        k_pd_force_lin_t<3><<<b, kT, 0, s>>>(d, colT, coefT, ubar, mask);
     }
     check("pd_force_lin_t");
 }
@@ -1169,7 +1169,28 @@ __global__ void k_iface_jac(int n, const double* D, int m, double dt_pd, const i
     jd[r] = v;
 }
 
+// the same from H_FE in CSR (a missing diagonal entry reads 0, as in the dense form)
+__global__ void k_iface_jac_csr(int n, const int32_t* rp, const int32_t* ci, const double* hv,
+                                int m, double dt_pd, const int32_t* cpd, const double* Mpd,
+                                double* jd) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double dg = 0.0;
+    for (int q = rp[r]; q < rp[r + 1]; ++q)
+        if (ci[q] == r) dg = hv[q];
+    double v = dg + double(m) * dt_pd / (2.0 * Mpd[cpd[r]]);
+    if (!(v > 0.0)) v = 0.0;
+    jd[r] = v;
+}
+
 }  // namespace
+
+void iface_jac_csr(int n, const int32_t* rp, const int32_t* ci, const double* hv, int m,
+                   double dt_pd, const int32_t* cpd, const double* Mpd, double* jd,
+                   cudaStream_t s) {
+    k_iface_jac_csr<<<blocks(n), kT, 0, s>>>(n, rp, ci, hv, m, dt_pd, cpd, Mpd, jd);
+    check("iface_jac_csr");
+}
 
 void s_vectors(int nl, int m, double t, double dt_pd, double dt_fe, double ramp,
                const double* lamp, const double* gpfe, double* sv, cudaStream_t s) {

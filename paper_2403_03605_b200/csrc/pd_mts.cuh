@@ -73,9 +73,12 @@ int dot_partials();
 void dot(int n, const double* x, const double* y, double* part, double* out, cudaStream_t s);
 void ratio(const double* num, const double* den, double* out, cudaStream_t s);
 // entry-major families (colT, coefT: E K; xiT: E K dim) and the linear force on them
-void family_transpose(const DevPD& d, int32_t* colT, double* coefT, double* xiT, cudaStream_t s);
-void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* xiT,
-                    const double* x, const uint32_t* mask, double* ubar, cudaStream_t s);
+void family_transpose(const DevPD& d, int32_t* colT, double* coefT, cudaStream_t s);
+void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* x,
+                    const uint32_t* mask, double* ubar, cudaStream_t s);
+void iface_jac_csr(int n, const int32_t* rp, const int32_t* ci, const double* hv, int m,
+                   double dt_pd, const int32_t* cpd, const double* Mpd, double* jd,
+                   cudaStream_t s);
 // the CG loop test on the device (conditional WHILE graph node); it_status: {iterations, status}
 void cg_cond(cudaGraphConditionalHandle h, const double* s_bb, const double* s_rr,
              const double* s_pap, double tol, int max_iter, int* it_status, cudaStream_t s);

@@ -315,7 +315,6 @@ struct pmts_mts {
     unsigned* ticket3 = nullptr;
     int32_t* famT_col = nullptr;  // entry-major families (PMTS_MTS_NO_TRANSPOSE=1: none)
     double* famT_coef = nullptr;
-    double* famT_xi = nullptr;
     double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
     int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
     double* hfe_v = nullptr;
@@ -413,7 +412,7 @@ struct pmts_mts {
     // updates that mask (count into slot)
     // linear PD force (centroid form) on the entry-major families when built
     void force_lin(const double* x, const uint32_t* mask) {
-        mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, famT_xi, x, mask, pd_ubar, stream);
+        mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, x, mask, pd_ubar, stream);
     }
 
     void pd_K(double* x, double* y, uint32_t* mask, bool do_break, int slot) {
@@ -699,9 +698,13 @@ struct pmts_mts {
     // disconnected FE parts never couple -- lossless) are extracted on the device
     bool hfe_unit_columns = false;  // pmts_mts_desc.interface_h_fe = 1
     void build_h_fe() {
-        if (fe_nm.explicit_scheme() && !use_dense && iface_mode != 1 && !interface_precond &&
-            !hfe_unit_columns) {
+        if (fe_nm.explicit_scheme() && !use_dense && iface_mode != 1 && !hfe_unit_columns) {
             build_h_fe_explicit();
+            if (interface_precond) {  // (the Jacobi option: from the CSR's diagonal)
+                iface_jac = alloc<double>(nl);
+                mtsk::iface_jac_csr(nl, hfe_rp, hfe_ci, hfe_v, m, s.dt_pd, cpd, pd_M, iface_jac,
+                                    stream);
+            }
             return;
         }
         // (the column-major scratch is n_lambda^2 doubles: refuse what cannot fit)
@@ -1903,8 +1906,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             const size_t ek = (size_t)h->pdv.E * h->pdv.K;
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
-            h->famT_xi = h->alloc<double>(ek * h->pdv.dim);
-            mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->famT_xi, h->stream);
+            mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->stream);
         }
         h->mask_words = (size_t)h->pdv.W * h->pdv.E;
         h->mask_sync = h->alloc<uint32_t>(h->mask_words);

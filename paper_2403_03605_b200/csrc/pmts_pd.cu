@@ -105,7 +105,7 @@ struct pmts_pd {
     double* d_extra = nullptr;
     uint32_t* mask_sync = nullptr;
     int32_t* famT_col = nullptr;
-    double *famT_coef = nullptr, *famT_xi = nullptr;
+    double* famT_coef = nullptr;
     double *rec_rd = nullptr, *rec_rv = nullptr, *rec_u = nullptr, *rec_v = nullptr,
            *rec_a = nullptr, *rec_w = nullptr, *rec_out = nullptr;
     int32_t* rec_row_of = nullptr;
@@ -1784,8 +1784,7 @@ int pmts_pd_homogeneous_recursion(pmts_pd* h, int32_t m, int32_t n, const int32_
             const size_t ek = (size_t)h->E * h->d.K;
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
-            h->famT_xi = h->alloc<double>(ek * h->dim);
-            mtsk::family_transpose(h->d, h->famT_col, h->famT_coef, h->famT_xi, s);
+            mtsk::family_transpose(h->d, h->famT_col, h->famT_coef, s);
             for (double** p : {&h->rec_rd, &h->rec_rv, &h->rec_u, &h->rec_v, &h->rec_a})
                 *p = h->alloc<double>(nd);
             h->rec_row_of = h->alloc<int32_t>(nd);
@@ -1811,7 +1810,7 @@ int pmts_pd_homogeneous_recursion(pmts_pd* h, int32_t m, int32_t n, const int32_
         const DevPD& d = h->d;
         for (int j = 1; j <= m; ++j) {
             if (j > 1)
-                mtsk::pd_force_lin_t(d, h->famT_col, h->famT_coef, h->famT_xi, h->rec_rd,
+                mtsk::pd_force_lin_t(d, h->famT_col, h->famT_coef, h->rec_rd,
                                      h->mask_sync, d.ubar, s);
             mtsk::pd_node_lin(d, j > 1 ? 1 : 0, h->rec_w, h->rec_row_of, double(j) / m, d.M,
                               d.bcflag, d.c_corr_v, d.c_corr_d, d.dt, d.c_pred_v, d.c_pred_d,
