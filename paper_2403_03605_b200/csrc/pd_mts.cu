@@ -523,7 +523,7 @@ __global__ void k_family_transpose(DevPD d, int32_t* colT, double* coefT) {
 // warp-tree sum, so bitwise the same G.  xi = cen_p - cen_e is formed from the
 // centroids (cached gathers) instead of a stored E K dim table: 12 B per entry from
 // HBM instead of 36 (BASELINE cfg5's 1.6e9 entries: 19 GB per substep, not 59)
-template <int DIM>
+template <int DIM, int KCH = DIM == 2 ? 1 : 4>
 __global__ void __launch_bounds__(kT) k_pd_force_lin_t(DevPD d, const int32_t* __restrict__ colT,
                                                        const double* __restrict__ coefT,
                                                        const double* __restrict__ ub,
@@ -537,25 +537,96 @@ __global__ void __launch_bounds__(kT) k_pd_force_lin_t(DevPD d, const int32_t* _
         ce[c] = d.cen[(size_t)c * E + e];
         G[c] = 0.0;
     }
-    for (int k0 = 0; k0 < K; k0 += 32) {
-        const int k = k0 + lane;
-        const size_t q = (size_t)e * K + k;
-        const int p = k < K ? colT[q] : -1;
-        const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
-        if (p >= 0 && ((word >> lane) & 1u)) {
-            double xi[DIM], dot = 0.0;
+    if (K <= 32 * KCH) {
+        // families of up to KCH x 32 entries (the 2D and 3D stencils): every chunk's
+        // entry loads issued first, then every gather, then the arithmetic in the chunk
+        // order -- a latency-bound warp per element keeps 2 dependent round trips in
+        // flight instead of 2 per chunk (same per-lane sums: bitwise the loop below)
+        int pk[KCH];
+        double cq[KCH];
+        uint32_t wk[KCH];
+#pragma unroll
+        for (int i = 0; i < KCH; ++i) {
+            const int k = 32 * i + lane;
+            const bool in = k < K;
+            pk[i] = in ? colT[(size_t)e * K + k] : -1;
+            cq[i] = in ? coefT[(size_t)e * K + k] : 0.0;
+            wk[i] = 32 * i < K ? mask[(size_t)i * E + e] : 0u;
+        }
+        double up[KCH][DIM], cp[KCH][DIM];
+#pragma unroll
+        for (int i = 0; i < KCH; ++i) {
+            const bool on = pk[i] >= 0 && ((wk[i] >> lane) & 1u);
             for (int c = 0; c < DIM; ++c) {
-                xi[c] = __ldg(d.cen + (size_t)c * E + p) - ce[c];
-                dot = dot + xi[c] * (ub[(size_t)p * DIM + c] - ue[c]);
+                up[i][c] = on ? ub[(size_t)pk[i] * DIM + c] : 0.0;
+                cp[i][c] = on ? __ldg(d.cen + (size_t)c * E + pk[i]) : 0.0;
             }
-            const double t = coefT[q] * dot;
-            for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+        }
+#pragma unroll
+        for (int i = 0; i < KCH; ++i) {
+            if (pk[i] >= 0 && ((wk[i] >> lane) & 1u)) {
+                double xi[DIM], dot = 0.0;
+                for (int c = 0; c < DIM; ++c) {
+                    xi[c] = cp[i][c] - ce[c];
+                    dot = dot + xi[c] * (up[i][c] - ue[c]);
+                }
+                const double t = cq[i] * dot;
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+            }
+        }
+    } else {
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            const int k = k0 + lane;
+            const size_t q = (size_t)e * K + k;
+            const int p = k < K ? colT[q] : -1;
+            const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
+            if (p >= 0 && ((word >> lane) & 1u)) {
+                double xi[DIM], dot = 0.0;
+                for (int c = 0; c < DIM; ++c) {
+                    xi[c] = __ldg(d.cen + (size_t)c * E + p) - ce[c];
+                    dot = dot + xi[c] * (ub[(size_t)p * DIM + c] - ue[c]);
+                }
+                const double t = coefT[q] * dot;
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+            }
         }
     }
     for (int c = 0; c < DIM; ++c)
         for (int o = 16; o > 0; o >>= 1) G[c] += __shfl_down_sync(0xffffffffu, G[c], o);
     if (lane == 0)
         for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
+}
+
+// sum_q Nsh G[e_q] over a node's incident elements (ascending, -1 ends the list), the
+// index loads and the G gathers issued up front (2 round trips, not 2 per element)
+template <int DIM>
+__device__ __forceinline__ void node_sum(const DevPD& d, int n, double* Ku) {
+    constexpr int NEM = DIM == 2 ? 4 : 8;
+    if (d.NE <= NEM) {
+        int eq[NEM];
+#pragma unroll
+        for (int q = 0; q < NEM; ++q) eq[q] = q < d.NE ? d.ne[(size_t)q * d.N + n] : -1;
+        bool live = true;
+#pragma unroll
+        for (int q = 0; q < NEM; ++q) {  // the list ends at the first -1
+            live = live && eq[q] >= 0;
+            if (!live) eq[q] = -1;
+        }
+        double g[NEM][DIM];
+#pragma unroll
+        for (int q = 0; q < NEM; ++q)
+            for (int c = 0; c < DIM; ++c) g[q][c] = eq[q] >= 0 ? d.G[(size_t)eq[q] * DIM + c] : 0.0;
+#pragma unroll
+        for (int q = 0; q < NEM; ++q)
+            if (eq[q] >= 0)
+                for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * g[q][c];
+        return;
+    }
+    for (int q = 0; q < d.NE; ++q) {
+        const int e = d.ne[(size_t)q * d.N + n];
+        if (e < 0) break;
+        for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
+    }
 }
 
 // (K x)_n from the incident elements' G, fused with the explicit block solve
@@ -569,11 +640,7 @@ __global__ void k_pd_node_explicit(DevPD d, const double* ra, double ra_scale, c
     if (n >= d.N) return;
     double Ku[DIM];
     for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
-    for (int q = 0; q < d.NE; ++q) {
-        const int e = d.ne[(size_t)q * d.N + n];
-        if (e < 0) break;
-        for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
-    }
+    node_sum<DIM>(d, n, Ku);
     for (int c = 0; c < DIM; ++c) {
         const size_t i = (size_t)n * DIM + c;
         const bool cc = cf[i] != 0;
@@ -603,12 +670,7 @@ __global__ void k_pd_node_lin(DevPD d, int with_force, const double* w, const in
     if (n >= d.N) return;
     double Ku[DIM];
     for (int c = 0; c < DIM; ++c) Ku[c] = 0.0;
-    if (with_force)
-        for (int q = 0; q < d.NE; ++q) {
-            const int e = d.ne[(size_t)q * d.N + n];
-            if (e < 0) break;
-            for (int c = 0; c < DIM; ++c) Ku[c] = Ku[c] + d.Nsh * d.G[(size_t)e * DIM + c];
-        }
+    if (with_force) node_sum<DIM>(d, n, Ku);
     for (int c = 0; c < DIM; ++c) {
         const size_t i = (size_t)n * DIM + c;
         const bool cc = cf[i] != 0;
