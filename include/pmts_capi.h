@@ -266,6 +266,9 @@ enum pmts_option {
                                     a second stream under the interior rows (default 0;
                                     without peers it splits the launch anyway) */
     PMTS_OPT_COUNT_HOT = 3,      /* 1: count hot / tested tiles (pmts_pd_info) */
+    PMTS_OPT_CLEAN_TILES = 4,    /* 1 (default): 2D tile kernel -- tiles whose bonds are all
+                                    intact (and whose neighbours' are) neither stage nor
+                                    re-write their bond states; 0: every tile does */
 };
 int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value);
 

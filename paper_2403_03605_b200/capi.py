@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PMTS_LIB_PATH") or os.path.join(HERE, "lib", "libpmts
 PMTS_OK, PMTS_ERR_INTERNAL, PMTS_ERR_CONFIG, PMTS_ERR_SOLVER = 0, 1, 2, 3
 DETERMINISTIC, FAST, FAST_F32POS = 0, 1, 2
 MICRO_EXP, MICRO_CONST = 0, 1
-OPT_BREAK_SCREEN, OPT_HALO_OVERLAP, OPT_COUNT_HOT = 1, 2, 3
+OPT_BREAK_SCREEN, OPT_HALO_OVERLAP, OPT_COUNT_HOT, OPT_CLEAN_TILES = 1, 2, 3, 4
 
 
 class PmtsError(RuntimeError):

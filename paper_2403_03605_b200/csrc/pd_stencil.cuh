@@ -56,6 +56,10 @@ struct FusedBufs {
     const int32_t* trk_dofs = nullptr;
     int n_trk = 0;
     double* trk_host = nullptr;  // this step's row (n_trk values)
+    // tile9: per tile 1 = every owned element has its full positive stencil intact in
+    // BOTH bond-state buffers (so the words need neither staging nor re-writing); a
+    // tile that breaks a bond clears its flag for good (null: stage on every tile)
+    uint32_t* tclean = nullptr;
 };
 
 
@@ -94,6 +98,11 @@ void launch_tile9_step(const DevPD& d, const LatticeDev& L, const Stencil2D& st,
                        int step, int do_break, double scale, int write_state, bool f32,
                        cudaStream_t s, int row_first = 0, int row_end = -1);
 int tile9_rows(const LatticeDev& L);  // tile rows of the grid (node rows j0 = 31 r ...)
+int tile9_cols(const LatticeDev& L);
+// the clean-tile flags of the current bond states; also copies mask -> mask_alt so both
+// ping-pong buffers hold every word
+void launch_tile9_flags(const LatticeDev& L, const uint32_t* mask, uint32_t* mask_alt,
+                        uint32_t* tclean, cudaStream_t s);
 int tile9_tile_rows();                // element rows per tile (31)
 
 // 3D 122-offset bond kernel on the nominal lattice (pd_lat3.cu): per |o|^2 class

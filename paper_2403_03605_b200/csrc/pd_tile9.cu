@@ -45,10 +45,10 @@ constexpr int IX = 32;                           // {1/M, flags} box row (from a
 #define PMTS_T9_NW 8
 #endif
 constexpr int NW = PMTS_T9_NW, NT = 32 * NW;  // 8 warps x 4 rows (3 CTAs/SM) or 16 x 2 (2 CTAs/SM)
-constexpr int kMinBlocks = NW == 8 ? 3 : 2;
+constexpr int kMinBlocks = NW <= 8 ? 3 : 2;
 constexpr int EPT = GY / NW;
 constexpr int SHALF = kFusedS / 2;
-static_assert(GX == 32 && EPT * NW == GY, "lane = column, warp = EPT rows");
+static_assert(GX == 32 && EPT * NW == GY && EPT % 4 == 0, "lane = column, warp = EPT rows in blocks of 4");
 static_assert(AX == kFusedAX, "Stencil2D apron offsets assume this width");
 
 constexpr int rup(int x, int a) { return (x + a - 1) / a * a; }
@@ -217,10 +217,10 @@ __device__ __forceinline__ void pair_term(const V* ubq, const uint32_t* maq,
 // registers) or 0..3 (|A| = 3): 62 shared loads per thread instead of 112 --
 // the shared-memory pipe was the limiter (ncu: 67 % of peak)
 template <bool DO_BREAK, typename V>
-__device__ __forceinline__ void pairs_blocked(const V* ubq, const V (&ue)[EPT],
-                                              double (&G0)[EPT], double (&G1)[EPT],
-                                              bool (&anyc)[EPT], const PairStencil2D& ps) {
-    static_assert(EPT == 4, "blocked path assumes 4 rows per thread");
+__device__ __forceinline__ void pairs_blocked(const V* ubq, const V* ue, double* G0, double* G1,
+                                              bool* anyc, const PairStencil2D& ps) {
+    // one block of 4 consecutive rows of the thread (ubq, ue, G, anyc at its first row)
+    constexpr int EPT = 4;
     {  // A = 0: (0,1) (0,2) (0,3)
         V c[10];
 #pragma unroll
@@ -418,7 +418,23 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         if ((blockIdx.x | by) == 0)
             for (int j = threadIdx.x; j < bf.n_trk; j += NT) bf.trk_host[j] = bf.rd_in[bf.trk_dofs[j]];
     }
-    if (ax0 >= 0 && ay0 >= 0 && ax0 + AX <= nx && ay0 + MY <= ny) {
+    // clean tiles: the apron lies in the domain and the six tiles it overlaps (this one,
+    // left, right and the three below: a bond's state lives at its lower element) have
+    // every positive-stencil bit set in both bond-state buffers -- nothing to stage, test
+    // or write back.  A flag read while its tile clears it in this same step is harmless:
+    // the step's input words are still the full ones, and the full and the masked force
+    // round identically for intact bonds.
+    const bool interior = ax0 >= 0 && ay0 >= 0 && ax0 + AX <= nx && ay0 + MY <= ny;
+    bool skip = false;
+    if (bf.tclean && interior) {
+        const uint32_t* tf = bf.tclean + (size_t)by * gridDim.x + blockIdx.x;
+        const uint32_t* tb = tf - gridDim.x;
+        skip = (tf[-1] & tf[0] & tf[1] & tb[-1] & tb[0] & tb[1]) != 0u;
+    }
+    // (re-read from shared memory after the force pass: no register held across it)
+    if (threadIdx.x == 0) red[4 * NW] = skip ? 1u : 0u;
+    if (skip) {
+    } else if (interior) {
         // interior tile (most of them): no per-word bounds checks
         const uint32_t* src = bf.mask_in + (size_t)ay0 * nx + ax0;
         for (int y = warp; y < MY; y += NW) {
@@ -451,7 +467,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     //     positive-stencil completeness of every mask the force pass reads.
     //     Work item = (column x, block of UR ub rows): 228 items, one per thread.
     constexpr uint32_t kPos = ((1u << kFusedS) - 1u) & ~((1u << SHALF) - 1u);
-    constexpr int UR = 7, NYB = (AY + UR - 1) / UR;
+    constexpr int UR = NW >= 8 ? 7 : 13, NYB = (AY + UR - 1) / UR;
     static_assert(AX * NYB <= NT, "one ubar work item per thread");
     bool tile_full = true;
     // screen: maxima of |node step| over the in-domain nodes of the apron, per
@@ -501,7 +517,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                 else
                     ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
                                                   d.Nsh * (hs[i].y + hs[i + 1].y));
-                if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
+                if (!skip && y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
             }
         }
     }
@@ -580,7 +596,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         for (int r = 0; r < EPT; ++r) anyc[r] = (cand >> r) & 1u;
         bool none[EPT];
         if (tile_full) {
-            pairs_blocked<false>(ub + q0, ue, G0, G1, none, ps);
+#pragma unroll
+            for (int sb = 0; sb < EPT; sb += 4)
+                pairs_blocked<false>(ub + q0 + sb * AX, ue + sb, G0 + sb, G1 + sb, none + sb, ps);
         } else {
             uint32_t m0[EPT];
 #pragma unroll
@@ -633,18 +651,21 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
     int e[EPT];
     uint32_t m0[EPT], m[EPT];
+    const bool skip2 = red[4 * NW] != 0u;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
         const int ej = j0 - 1 + gy0 + r;
         const bool in = ei >= 0 && ej >= 0 && ei < nx && ej < ny;
         e[r] = in ? ej * nx + ei : -1;
-        m0[r] = ma[q0 + r * AX];
+        m0[r] = skip2 ? 0u : ma[q0 + r * AX];
         m[r] = m0[r];
     }
     unsigned long long nb = 0;
+    bool changed = false;
     if (DO_BREAK) {  // rare: exact per-bond thresholds for the flagged elements
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
+            if (skip2 && anyc[r]) m0[r] = m[r] = bf.mask_in[e[r]];  // (a clean tile staged nothing)
             uint32_t c = anyc[r] ? (m0[r] & kPos) : 0u;
             while (c) {
                 const int k = __ffs(c) - 1;
@@ -669,7 +690,11 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
 #pragma unroll
     for (int r = 0; r < EPT; ++r)
-        if (e[r] >= 0 && gx >= 1 && gy0 + r >= 1) bf.mask_out[e[r]] = m[r];
+        if (e[r] >= 0 && gx >= 1 && gy0 + r >= 1) {
+            if (!skip2 || m[r] != m0[r]) bf.mask_out[e[r]] = m[r];
+            changed |= m[r] != m0[r];
+        }
+    if (DO_BREAK && bf.tclean && changed) bf.tclean[(size_t)by * gridDim.x + blockIdx.x] = 0u;
     // the node update needs, per node, (G(x,y) + G(x+1,y)) + (G(x,y+1) + G(x+1,y+1)):
     // the horizontal pair sums come from the neighbour lane, the vertical partner
     // row from this thread's next row -- except for a band's last row, whose
@@ -736,7 +761,34 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
 }
 
+// clean-tile flags from the current bond states (and mask -> mask_alt, so that both
+// ping-pong buffers hold every word before tiles stop re-writing theirs)
+__global__ void __launch_bounds__(256) k_tile9_flags(int nx, int ny, const uint32_t* mask,
+                                                     uint32_t* mask_alt, uint32_t* tclean) {
+    constexpr uint32_t kPos = ((1u << kFusedS) - 1u) & ~((1u << SHALF) - 1u);
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    bool full = true;
+    for (int t = threadIdx.x; t < TX * TY; t += 256) {
+        const int i = i0 + t % TX, j = j0 + t / TX;
+        if (i < nx && j < ny) {
+            const uint32_t m = mask[(size_t)j * nx + i];
+            mask_alt[(size_t)j * nx + i] = m;
+            full = full && (m & kPos) == kPos;
+        }
+    }
+    full = __syncthreads_and(full);
+    if (threadIdx.x == 0) tclean[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = full ? 1u : 0u;
+}
+
 int tile9_rows(const LatticeDev& L) { return L.ny / TY + 1; }
+int tile9_cols(const LatticeDev& L) { return L.nx / TX + 1; }
+void launch_tile9_flags(const LatticeDev& L, const uint32_t* mask, uint32_t* mask_alt,
+                        uint32_t* tclean, cudaStream_t s) {
+    k_tile9_flags<<<dim3(tile9_cols(L), tile9_rows(L)), 256, 0, s>>>(L.nx, L.ny, mask, mask_alt,
+                                                                     tclean);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
 int tile9_tile_rows() { return TY; }
 
 void tile9_boxes(int* rd_x, int* rd_y, int* rv_x, int* rv_y, int* im_x, int* im_y) {

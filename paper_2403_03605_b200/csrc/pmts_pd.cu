@@ -124,6 +124,10 @@ struct pmts_pd {
     Stencil3D st3{};
     double* rd_alt = nullptr;        // ping-pong partners of d.rd / d.mask
     uint32_t* mask_alt = nullptr;
+    // tile9 clean-tile flags (pd_tile9.cu): computed from the bond states before the
+    // first step after they were (re)built; PMTS_OPT_CLEAN_TILES = 0 turns them off
+    uint32_t* t9_clean = nullptr;
+    bool t9_clean_ready = false, t9_clean_on = true;
     // slab decomposition: NCCL clique + halo rows (node ranges, local ids)
     void* comm = nullptr;            // ncclComm_t
     int peer_lo = -1, peer_hi = -1;
@@ -719,6 +723,7 @@ bool try_lattice(pmts_pd* h, const int32_t* dcol) {
         if (!h->rd_alt) h->rd_alt = h->alloc<double>(h->ndof);
         if (h->mask_alt) h->release(h->mask_alt);
         h->mask_alt = h->alloc<uint32_t>((size_t)E);
+        h->t9_clean_ready = false;
         h->fused = true;
         h->tile9 = true;
         h->pos_only = true;  // the tile kernel keeps a bond's state at its lower end
@@ -860,6 +865,15 @@ void enqueue_step(pmts_pd* h, int slot, double scale, bool time_bond, cudaEvent_
                           "28-offset pair stencil only (set lattice and lattice_h)");
     if (h->fused) {
         FusedBufs b{h->d.rd, h->rd_alt, h->d.mask, h->mask_alt, scale_dev};
+        if (h->tile9 && h->t9_clean_on) {
+            if (!h->t9_clean_ready) {
+                if (!h->t9_clean)
+                    h->t9_clean = h->alloc<uint32_t>((size_t)tile9_cols(h->L) * tile9_rows(h->L));
+                launch_tile9_flags(h->L, h->d.mask, h->mask_alt, h->t9_clean, h->stream);
+                h->t9_clean_ready = true;
+            }
+            b.tclean = h->t9_clean;
+        }
         if (report) {
             b.trk_dofs = report->trk_dofs;
             b.n_trk = report->n_trk;
@@ -1727,6 +1741,12 @@ int pmts_pd_set_option(pmts_pd* h, int32_t option, int32_t value) {
                 h->st3.hot_count = c;
                 break;
             }
+            case PMTS_OPT_CLEAN_TILES:
+                // off: every tile stages and re-writes its bond states again; turning it
+                // back on recomputes the flags from the current states
+                h->t9_clean_on = value != 0;
+                h->t9_clean_ready = false;
+                break;
             default:
                 throw ConfigError("unknown option " + std::to_string(option));
         }

@@ -226,6 +226,39 @@ def test_tile9_screen_is_exact(nx, ny, steps, monkeypatch):
         assert a[0] > 0
 
 
+@pytest.mark.parametrize("mode", [capi.FAST, capi.FAST_F32POS])
+@pytest.mark.parametrize("nx,ny,steps", [(124, 62, 300), (190, 130, 700), (97, 160, 700)])
+def test_tile9_clean_tiles_are_exact(nx, ny, steps, mode):
+    """Clean tiles (default: a tile whose own and neighbouring bonds are all intact
+    neither stages nor re-writes its bond states) change nothing: fields, bond states,
+    broken counts and the damage field are bitwise those of staging every tile
+    (PMTS_OPT_CLEAN_TILES = 0), through crack growth, and switching the option in the
+    middle of a run recomputes the flags from the live bond states."""
+    sc = _plate(nx, ny)
+    scales = [sc.load_scale(i * sc.dt) for i in range(1, steps + 1)]
+    out = {}
+    for clean in ("on", "off", "toggle"):
+        s = PDSolver.from_scenario(sc, mode=mode).find_pe_pairs()
+        s.set_option(capi.OPT_CLEAN_TILES, 0 if clean == "off" else 1)
+        s.initial_acceleration(sc.load_scale(0.0))
+        h = steps // 2
+        nb = [s.step(scales[:h])]
+        if clean == "toggle":
+            s.set_option(capi.OPT_CLEAN_TILES, 0)
+            nb.append(s.step(scales[h:h + 7]))
+            s.set_option(capi.OPT_CLEAN_TILES, 1)
+            nb.append(s.step(scales[h + 7:]))
+            nb = [nb[0], nb[1] + nb[2]]
+        else:
+            nb.append(s.step(scales[h:]))
+        out[clean] = (nb, *s.state(), s.intact(), *s.damage_field())
+    assert sum(out["on"][0]) > 0
+    for k in ("off", "toggle"):
+        assert out["on"][0] == out[k][0]
+        for x, y in zip(out["on"][1:], out[k][1:]):
+            assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("name", ["mini", "block3d"])
 @pytest.mark.parametrize("mode", [capi.DETERMINISTIC, capi.FAST])
 def test_step_tracked_reports_every_step(mode, name):
@@ -514,16 +547,19 @@ def test_cfg3_screen_exact_over_baseline_horizon(cfg3, monkeypatch):
     the screened kernel's per-batch broken counts, bond states and fields are bitwise
     those of the unscreened candidate pass."""
     out = {}
-    for screen in (True, False):
+    for screen, clean in ((True, True), (False, True), (True, False)):
         s = PDSolver.from_scenario(cfg3, mode=capi.FAST).find_pe_pairs()
         s.set_option(capi.OPT_BREAK_SCREEN, 1 if screen else 0)
+        s.set_option(capi.OPT_CLEAN_TILES, 1 if clean else 0)
         s.initial_acceleration(cfg3.load_scale(0.0))
         nb = [s.step(cfg3.scales(i, 100)) for i in range(1, 1001, 100)]
-        out[screen] = (nb, *s.state(), s.intact())
-    a, b = out[True], out[False]
-    assert a[0] == b[0] and sum(a[0]) > 1000
-    for x, y in zip(a[1:], b[1:]):
-        assert np.array_equal(x, y)
+        out[screen, clean] = (nb, *s.state(), s.intact())
+    a = out[True, True]
+    assert sum(a[0]) > 1000
+    for b in (out[False, True], out[True, False]):  # (clean tiles off: every tile staged)
+        assert a[0] == b[0]
+        for x, y in zip(a[1:], b[1:]):
+            assert np.array_equal(x, y)
 
 
 # ----- fp32-position / fp64-accumulate variant (BASELINE cfg3, PMTS_FAST_F32POS) -----
