@@ -428,6 +428,14 @@ def measure_pd(args, ctx: Ctx, workload: str, scaling: str, K: int, W: int, mode
             "avg_launch_us": bond_avg_s * 1e6, "launch_timing": timing,
             "avg_launch_us_isolated": bond_ms * 1e3 / K,
             "bond_share_of_step": bond_ms / tot_ms if tot_ms else None, "peak_source": peak_src}
+    if info["path"] == 2:
+        # round 2 restated the model: 72 B per node (rd, rv in and out, {1/M | flags}) plus
+        # 8 B per element only on the tiles that still stage and re-write their bond
+        # states (clean tiles touch none); round 1 counted 81 B per element everywhere
+        r1 = s.n_nodes * 73.0 + s.n_elems * 8.0
+        roof["bytes_model"] = ("72 B/node + 8 B/element on tiles staging bond states "
+                               "(info at the window's start)")
+        roof["frac_round1_model"] = r1 / bond_avg_s / 1e9 / peak
     # the bond work is fp64-arithmetic heavy.  2D: 14 flops per directed entry in fast
     # mode (eta 2, xi.eta 3, force 4, |eta|^2 3, test 2) = 28 per unique bond; 3D (the
     # 122-offset kernel, break test screened off on cold tiles): eta 3, o.eta 3 (small-

@@ -28,6 +28,7 @@
 #include <initializer_list>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "pd_stencil.cuh"
 
@@ -131,7 +132,11 @@ template <bool DO_BREAK, bool MASKED, int K>
 __device__ __forceinline__ void pair_math(double2 up, double2 um, double2 ue, bool actp, bool actm,
                                           double& G0, double& G1, bool& anyc,
                                           const PairStencil2D& ps) {
+    static_assert(!DO_BREAK, "break tests run in cand_terms");
     constexpr int A = kPairA[K], B = kPairB[K];
+    // s = eta_o + eta_-o with a broken bond's eta an exact zero.  (Measured: forming s as
+    // (u_o + u_-o) - 2 u_e -- 4 instead of 6 fp64 operations per pair -- is not faster
+    // here, 37.8 vs 37.3 us per cfg3 step; the fp32 variant below does use it.)
     const double ep0 = up.x - ue.x, ep1 = up.y - ue.y;
     double em0 = um.x - ue.x, em1 = um.y - ue.y;
     if (MASKED) {
@@ -139,49 +144,44 @@ __device__ __forceinline__ void pair_math(double2 up, double2 um, double2 ue, bo
         em1 = actm ? em1 : 0.0;
     }
     const double fp0 = MASKED && !actp ? 0.0 : ep0, fp1 = MASKED && !actp ? 0.0 : ep1;
-    double tp;
     if (B == 0) {
-        const double s0 = fp0 + em0;
-        G0 = fma(ps.fa[K], s0, G0);
-        tp = A * ep0;
+        G0 = fma(ps.fa[K], fp0 + em0, G0);
     } else if (A == 0) {
-        const double s1 = fp1 + em1;
-        G1 = fma(ps.fb[K], s1, G1);
-        tp = B * ep1;
+        G1 = fma(ps.fb[K], fp1 + em1, G1);
     } else {
         const double s0 = fp0 + em0, s1 = fp1 + em1;
         const double t = fma((double)A, s0, B * s1);
         G0 = fma(ps.fa[K], t, G0);
         G1 = fma(ps.fb[K], t, G1);
-        tp = fma((double)A, ep0, B * ep1);
     }
-    if (DO_BREAK)
-        anyc |= (!MASKED || actp) && dbits(fma(ps.h2, tp, fma(ep0, ep0, ep1 * ep1))) >= ps.cl[K];
 }
 
 // fp32-position variant (PMTS_FAST_F32POS): the ubar apron holds tile-relative
-// fp32 displacements (ubar - ubar_ref, rounded once); eta, the pair sum s and
-// t = o . s are fp32, each pair's t is widened to fp64 and accumulated into G
-// in fp64 (the break tests run in cand_terms, never here)
+// fp32 displacements (ubar - ubar_ref, rounded once); the pair sum s = (u_o + u_-o) -
+// 2 u_e (the masked form drops a broken bond's u and lowers the factor: -1 gives the
+// single eta rounded once, 0 an exact zero) and t = o . s are fp32, each pair's t is
+// widened to fp64 and accumulated into G in fp64 (the break tests run in cand_terms)
 template <bool DO_BREAK, bool MASKED, int K>
 __device__ __forceinline__ void pair_math(float2 up, float2 um, float2 ue, bool actp, bool actm,
                                           double& G0, double& G1, bool& anyc,
                                           const PairStencil2D& ps) {
-    static_assert(!DO_BREAK, "fp32 pairs: break tests run in cand_terms");
+    static_assert(!DO_BREAK, "break tests run in cand_terms");
     constexpr int A = kPairA[K], B = kPairB[K];
-    const float ep0 = up.x - ue.x, ep1 = up.y - ue.y;
-    float em0 = um.x - ue.x, em1 = um.y - ue.y;
+    float c = -2.0f;
     if (MASKED) {
-        em0 = actm ? em0 : 0.0f;
-        em1 = actm ? em1 : 0.0f;
+        up.x = actp ? up.x : 0.0f;
+        up.y = actp ? up.y : 0.0f;
+        um.x = actm ? um.x : 0.0f;
+        um.y = actm ? um.y : 0.0f;
+        c = actp ? (actm ? -2.0f : -1.0f) : (actm ? -1.0f : 0.0f);
     }
-    const float fp0 = MASKED && !actp ? 0.0f : ep0, fp1 = MASKED && !actp ? 0.0f : ep1;
     if (B == 0) {
-        G0 = fma(ps.fa[K], (double)(fp0 + em0), G0);
+        G0 = fma(ps.fa[K], (double)fmaf(c, ue.x, up.x + um.x), G0);
     } else if (A == 0) {
-        G1 = fma(ps.fb[K], (double)(fp1 + em1), G1);
+        G1 = fma(ps.fb[K], (double)fmaf(c, ue.y, up.y + um.y), G1);
     } else {
-        const double t = fmaf((float)A, fp0 + em0, (float)B * (fp1 + em1));
+        const float s0 = fmaf(c, ue.x, up.x + um.x), s1 = fmaf(c, ue.y, up.y + um.y);
+        const double t = fmaf((float)A, s0, (float)B * s1);
         G0 = fma(ps.fa[K], t, G0);
         G1 = fma(ps.fb[K], t, G1);
     }
@@ -474,10 +474,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     // component and direction (x-step of u_x, y-step of u_x, x-step of u_y,
     // y-step of u_y), as high words (out-of-domain nodes are TMA zero fill)
     unsigned mxx = 0, mxy = 0, myx = 0, myy = 0;
-    if (threadIdx.x < AX * NYB) {
+    // (ALLIN: every node of the apron lies in the domain -- no per-node bounds tests)
+    auto ubar_pass = [&](auto allin) {
+        constexpr bool ALLIN = decltype(allin)::value;
         const int x = threadIdx.x % AX, y0 = (threadIdx.x / AX) * UR;
-        const bool ca = (unsigned)(ax0 + x) <= (unsigned)nx;      // node column x in the domain
-        const bool cb = (unsigned)(ax0 + x + 1) <= (unsigned)nx;  // node column x + 1
+        const bool ca = ALLIN || (unsigned)(ax0 + x) <= (unsigned)nx;      // node column x in the domain
+        const bool cb = ALLIN || (unsigned)(ax0 + x + 1) <= (unsigned)nx;  // node column x + 1
         double2 hs[UR + 1];
         double2 ap = make_double2(0.0, 0.0), bp = ap;
         bool rp = false;
@@ -487,12 +489,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             const double2 a = nt[y * BX + x], b = nt[y * BX + x + 1];
             hs[i] = make_double2(a.x + b.x, a.y + b.y);
             if (SCREEN) {
-                const bool rw = (unsigned)(ay0 + y) <= (unsigned)ny;
+                const bool rw = ALLIN || (unsigned)(ay0 + y) <= (unsigned)ny;
                 if (rw && ca && cb) {
                     mxx = max(mxx, hi_abs(b.x - a.x));
                     myx = max(myx, hi_abs(b.y - a.y));
                 }
-                if (i > 0 && rw && rp) {
+                if (i > 0 && rw && (ALLIN || rp)) {
                     if (ca) {
                         mxy = max(mxy, hi_abs(a.x - ap.x));
                         myy = max(myy, hi_abs(a.y - ap.y));
@@ -520,6 +522,12 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                 if (!skip && y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
             }
         }
+    };
+    if (threadIdx.x < AX * NYB) {
+        if (SCREEN && ax0 >= 0 && ay0 >= 0 && ax0 + BX - 1 <= nx && ay0 + BY - 1 <= ny)
+            ubar_pass(std::true_type{});
+        else
+            ubar_pass(std::false_type{});
     }
     if (SCREEN) {
         mxx = __reduce_max_sync(0xffffffffu, mxx);
@@ -649,9 +657,15 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             }
         }
     }
+    const bool skip2 = red[4 * NW] != 0u;
+    unsigned long long nb = 0;
+    bool anyw = false;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) anyw |= anyc[r];
+    // (a clean tile without a candidate in the warp has no bond state to test or write)
+    if (!skip2 || __any_sync(0xffffffffu, anyw)) {
     int e[EPT];
     uint32_t m0[EPT], m[EPT];
-    const bool skip2 = red[4 * NW] != 0u;
 #pragma unroll
     for (int r = 0; r < EPT; ++r) {
         const int ej = j0 - 1 + gy0 + r;
@@ -660,7 +674,6 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         m0[r] = skip2 ? 0u : ma[q0 + r * AX];
         m[r] = m0[r];
     }
-    unsigned long long nb = 0;
     bool changed = false;
     if (DO_BREAK) {  // rare: exact per-bond thresholds for the flagged elements
 #pragma unroll
@@ -695,6 +708,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             changed |= m[r] != m0[r];
         }
     if (DO_BREAK && bf.tclean && changed) bf.tclean[(size_t)by * gridDim.x + blockIdx.x] = 0u;
+    }
     // the node update needs, per node, (G(x,y) + G(x+1,y)) + (G(x,y+1) + G(x+1,y+1)):
     // the horizontal pair sums come from the neighbour lane, the vertical partner
     // row from this thread's next row -- except for a band's last row, whose
@@ -717,16 +731,14 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     double2* rdo = reinterpret_cast<double2*>(bf.rd_out);
     double2* rv2 = reinterpret_cast<double2*>(d.rv);
     const double2* P2 = reinterpret_cast<const double2*>(d.P);
-#pragma unroll
-    for (int r = 0; r < EPT; ++r) {
+    // one node: a = (P - K u) / M, the corrector, the next predictor (the same expressions
+    // on both paths below, so they round identically)
+    auto node = [&](int r, double im, int fl, bool ws) {
         const int lx = lane, ly = gy0 + r;
-        if (lx >= ox || ly >= oy) continue;
         const size_t n = (size_t)(j0 + ly) * NX + i0 + lx;
         const double2 hn = r + 1 < EPT ? hsum[r + 1] : gt[warp * GX + lx];  // row ly + 1
         const double k0 = d.Nsh * (hsum[r].x + hn.x);
         const double k1 = d.Nsh * (hsum[r].y + hn.y);
-        const double im = ims[ly * IX + lx + (i0 - ie)];
-        const int fl = (int)(dbits(im) & 7);  // 1: x constrained, 2: y constrained, 4: loaded
         double2 p = make_double2(0.0, 0.0);
         if (fl & 4) {
             const double sc = bf.scale_dev ? bf.scale_dev[step] : scale;
@@ -744,13 +756,35 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
             if (fl & 1) v0 = d.bcvel[2 * n];
             if (fl & 2) v1 = d.bcvel[2 * n + 1];
         }
-        if (write_state) {
+        if (ws) {
             reinterpret_cast<double2*>(d.a)[n] = make_double2(a0, a1);
             reinterpret_cast<double2*>(d.v)[n] = make_double2(v0, v1);
             reinterpret_cast<double2*>(d.u)[n] = make_double2(u0, u1);
         }
         rv2[n] = make_double2(v0 + d.c_pred_v * a0, v1 + d.c_pred_v * a1);
         rdo[n] = make_double2(u0 + d.dt * v0 + d.c_pred_d * a0, u1 + d.dt * v1 + d.c_pred_d * a1);
+    };
+    // {1/M, flags} of the thread's nodes (lane 31 and row 31 are the apron: not owned)
+    double imv[EPT];
+    int flor = 0;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r) {
+        imv[r] = (lane < TX && gy0 + r < TY) ? ims[(gy0 + r) * IX + lane + (i0 - ie)] : 0.0;
+        flor |= (int)dbits(imv[r]);
+    }
+    if (ox == TX && oy == TY && !write_state && !__any_sync(0xffffffffu, (flor & 7) != 0)) {
+        // interior step of unconstrained, unloaded nodes (nearly every warp): straight-line
+        if (lane < TX) {
+#pragma unroll
+            for (int r = 0; r < EPT; ++r)
+                if (gy0 + r < TY) node(r, imv[r], 0, false);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+            if (lane >= ox || gy0 + r >= oy) continue;
+            node(r, imv[r], (int)(dbits(imv[r]) & 7), write_state != 0);
+        }
     }
 
     if (DO_BREAK) {  // per warp (no CTA barrier at the tail; breaks are rare)

@@ -364,6 +364,33 @@ void build_tile9_maps(pmts_pd* h) {
     make(&h->t9_im, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, h->d_imf, NXP, NY, imx, imy);
 }
 
+// elements of the tiles that stage and re-write their bond states in the next step
+// (every element without the clean-tile flags); the skip rule of k_tile9
+double tile9_staged_elements(pmts_pd* h) {
+    if (!h->tile9 || !h->t9_clean_on || !h->t9_clean_ready) return (double)h->E;
+    const int cols = tile9_cols(h->L), rows = tile9_rows(h->L), T = tile9_tile_rows();
+    std::vector<uint32_t> f((size_t)cols * rows);
+    download(f.data(), h->t9_clean, f.size(), h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+    const int nx = h->L.nx, ny = h->L.ny;
+    double staged = 0.0;
+    for (int by = 0; by < rows; ++by)
+        for (int bx = 0; bx < cols; ++bx) {
+            const int i0 = bx * T, j0 = by * T, ax0 = i0 - 1 - kFusedR, ay0 = j0 - 1 - kFusedR;
+            const bool interior = ax0 >= 0 && ay0 >= 0 && ax0 + kFusedAX <= nx &&
+                                  ay0 + T + 1 + kFusedR <= ny;
+            bool skip = false;
+            if (interior) {
+                const uint32_t* tf = f.data() + (size_t)by * cols + bx;
+                const uint32_t* tb = tf - cols;
+                skip = (tf[-1] & tf[0] & tf[1] & tb[-1] & tb[0] & tb[1]) != 0u;
+            }
+            if (!skip)
+                staged += (double)std::max(0, std::min(T, nx - i0)) * std::max(0, std::min(T, ny - j0));
+        }
+    return staged;
+}
+
 Tile9Maps tile9_maps(const pmts_pd* h) {
     Tile9Maps m;
     m.rd = h->t9_rd[h->d.rd == h->rd_buf[0] ? 0 : 1];
@@ -1364,7 +1391,10 @@ int pmts_pd_info_get(pmts_pd* h, pmts_pd_info* info) {
                 // rd in + out, rv in + out, 1/M, node flags, mask in + out
                 info->kernels_per_step = 1;
                 info->path = 2;
-                info->bytes_per_step = N * dim * 8.0 * 4 + N * 8.0 + N * 1.0 + E * 4.0 * 2;
+                // (node flags ride in 1/M; bond-state words only move on the tiles that
+                // stage them -- the clean tiles of pd_tile9.cu touch none)
+                info->bytes_per_step =
+                    N * dim * 8.0 * 4 + N * 8.0 + tile9_staged_elements(h) * 4.0 * 2;
                 info->bond_bytes_per_step = info->bytes_per_step;
             }
         }
