@@ -345,6 +345,12 @@ typedef struct {
                                     = H_FE as a direct sparse product, bitwise the unit
                                     columns, no n_lambda^2 scratch; 1 = the unit columns
                                     (unit_fe_column, mts.hpp:389-397) through the scratch */
+    int32_t pd_linear;           /* linear PD force of the homogeneous substeps (unit, link and
+                                    interface solves, mts.hpp:230-238, 398-420): 0 (default) =
+                                    on a 3D box lattice with the 122-offset stencil the tile
+                                    kernel of pd_mts_lat.cu (coefficients in stencil order,
+                                    ubar apron in shared memory), else the ELL form; 1 = the
+                                    ELL form everywhere (the two differ by rounding only) */
 } pmts_mts_desc;
 
 typedef struct {
@@ -383,6 +389,8 @@ typedef struct {
     /* non-matching meshes: elements [0, fe_mesh_elems) / nodes [0, fe_mesh_nodes) are
        the FE lattice, the rest the PD lattice; -1 on a conforming mesh */
     int32_t fe_mesh_elems, fe_mesh_nodes;
+    int32_t pd_linear_lattice;   /* 1: the homogeneous substeps' linear PD force runs on the
+                                    lattice tile kernel (pmts_mts_desc.pd_linear) */
 } pmts_mts_view;
 
 typedef struct {                 /* MacroReport (mts.hpp:41-63) */

@@ -28,6 +28,7 @@ SOURCES = [
     ("pd_setup.cu", ["-fmad=false"]),
     ("pmts_pd.cu", ["-fmad=false"]),
     ("pd_mts.cu", ["-fmad=false"]),
+    ("pd_mts_lat.cu", ["-fmad=false"]),
     ("pmts_mts.cu", ["-fmad=false"]),
 ]
 HOST_SOURCES = ["pmts_setup.cpp", "pmts_mts_setup.cpp"]

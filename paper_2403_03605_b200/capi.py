@@ -83,7 +83,7 @@ class MtsDesc(C.Structure):
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
                 ("track_energy", _I), ("device", _I), ("fe_spacing", _D),
                 ("interface_precond", _I), ("interface_recursion", _I), ("shard_world", _I),
-                ("shard_rank", _I), ("interface_h_fe", _I)]
+                ("shard_rank", _I), ("interface_h_fe", _I), ("pd_linear", _I)]
 
 
 class MtsShardView(C.Structure):
@@ -105,7 +105,8 @@ class MtsView(C.Structure):
                 ("pd_bc_vel", _P), ("cpl_fe_dof", _P), ("cpl_pd_dof", _P), ("pairs", _P),
                 ("pe_weight", _P), ("node_xyz", _P), ("elem_nodes", _P), ("node_alpha", _P),
                 ("cpl_fe_nnz", C.c_int64), ("cpl_fe_rowptr", _P), ("cpl_fe_col", _P),
-                ("cpl_fe_w", _P), ("fe_mesh_elems", _I), ("fe_mesh_nodes", _I)]
+                ("cpl_fe_w", _P), ("fe_mesh_elems", _I), ("fe_mesh_nodes", _I),
+                ("pd_linear_lattice", _I)]
 
 
 class MtsReport(C.Structure):

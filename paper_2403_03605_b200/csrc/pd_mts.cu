@@ -727,6 +727,11 @@ void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double*
     }
     check("pd_force_lin");
 }
+void pd_ubar(const DevPD& d, const double* x, double* ubar, cudaStream_t s) {
+    if (d.dim == 2) k_pd_ubar<2><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+    else k_pd_ubar<3><<<blocks(d.E), kT, 0, s>>>(d, x, ubar);
+    check("pd_ubar");
+}
 void family_transpose(const DevPD& d, int32_t* colT, double* coefT, cudaStream_t s) {
     const long long n = (long long)d.E * d.K;
     const int b = (int)((n + kT - 1) / kT);

@@ -76,6 +76,22 @@ void ratio(const double* num, const double* den, double* out, cudaStream_t s);
 void family_transpose(const DevPD& d, int32_t* colT, double* coefT, cudaStream_t s);
 void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, const double* x,
                     const uint32_t* mask, double* ubar, cudaStream_t s);
+// the same linear force on a 3D box lattice in lattice order (pd_mts_lat.cu): the
+// coefficients in stencil order, the snapshot's bond states as stencil bits
+struct LinLat {
+    int nx = 0, ny = 0, nz = 0;
+    double h = 0.0;
+    double* coefS = nullptr;     // [122 E]
+    uint32_t* maskS = nullptr;   // [4 E]
+    const int8_t* slot = nullptr;  // [7^3] offset -> stencil slot (-1: none), device
+};
+void lin_lat_slot_table(int8_t* table343);
+int lin_lat_stencil_size();
+bool lin_lat_build(const DevPD& d, const LinLat& L, cudaStream_t s);  // false: an entry off the stencil
+void lin_lat_mask(const DevPD& d, const LinLat& L, const uint32_t* mask, cudaStream_t s);
+void pd_force_lin_lat(const DevPD& d, const LinLat& L, const double* x, double* ubar,
+                      cudaStream_t s);
+void pd_ubar(const DevPD& d, const double* x, double* ubar, cudaStream_t s);
 void iface_jac_csr(int n, const int32_t* rp, const int32_t* ci, const double* hv, int m,
                    double dt_pd, const int32_t* cpd, const double* Mpd, double* jd,
                    cudaStream_t s);

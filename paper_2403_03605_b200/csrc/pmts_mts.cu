@@ -313,8 +313,12 @@ struct pmts_mts {
     unsigned* ticket = nullptr;   // their last-block counter
     double* part3 = nullptr;      // operator-fused p.Ap partials (one per row block)
     unsigned* ticket3 = nullptr;
-    int32_t* famT_col = nullptr;  // entry-major families (PMTS_MTS_NO_TRANSPOSE=1: none)
+    int32_t* famT_col = nullptr;  // entry-major families (none on the lattice path below)
     double* famT_coef = nullptr;
+    // 3D box lattice in lattice order with the 122-offset stencil: the linear force of the
+    // homogeneous substeps on the k_sync snapshot runs in pd_mts_lat.cu
+    bool lin_lat = false;
+    mtsk::LinLat lat;
     double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
     int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
     double* hfe_v = nullptr;
@@ -361,6 +365,11 @@ struct pmts_mts {
         CKM(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
         owned.push_back(p);
         return p;
+    }
+    void release(void* p) {
+        if (!p) return;
+        owned.erase(std::remove(owned.begin(), owned.end(), p), owned.end());
+        cudaFree(p);
     }
     template <class T>
     T* upload(const std::vector<T>& v) {
@@ -412,7 +421,15 @@ struct pmts_mts {
     // updates that mask (count into slot)
     // linear PD force (centroid form) on the entry-major families when built
     void force_lin(const double* x, const uint32_t* mask) {
-        mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, x, mask, pd_ubar, stream);
+        if (lin_lat && mask == mask_sync) mtsk::pd_force_lin_lat(pdv, lat, x, pd_ubar, stream);
+        else if (famT_col) mtsk::pd_force_lin_t(pdv, famT_col, famT_coef, x, mask, pd_ubar, stream);
+        else mtsk::pd_force_lin(pdv, x, mask, pd_ubar, stream);
+    }
+    // k_sync <- the live bond states (mts.hpp:98, 252), and its stencil-bit form
+    void snapshot_bonds() {
+        CKM(cudaMemcpyAsync(mask_sync, mask_live, sizeof(uint32_t) * mask_words,
+                            cudaMemcpyDeviceToDevice, stream));
+        if (lin_lat) mtsk::lin_lat_mask(pdv, lat, mask_sync, stream);
     }
 
     void pd_K(double* x, double* y, uint32_t* mask, bool do_break, int slot) {
@@ -1259,8 +1276,7 @@ pmts_mts_report pmts_mts::macro_step() {
     {
         const double t0 = now_s();
         if (unit_stale) {
-            CKM(cudaMemcpyAsync(mask_sync, mask_live, sizeof(uint32_t) * mask_words,
-                                cudaMemcpyDeviceToDevice, stream));
+            snapshot_bonds();
             h_valid = false;
             if (hpd_valid) {  // k_sync changed: the recursion from here on
                 hpd_valid = false;
@@ -1902,16 +1918,59 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         pd_internal_pair_weights(h->pd, h->pe_weight.data());
         h->pdv = pd_internal_dev(h->pd);
         h->mask_live = h->pdv.mask;
-        {  // entry-major families for the linear PD force (coalesced lanes)
+        h->mask_words = (size_t)h->pdv.W * h->pdv.E;
+        h->mask_sync = h->alloc<uint32_t>(h->mask_words);
+        if (dim == 3 && desc->pd_linear != 1 && h->pdv.K <= mtsk::lin_lat_stencil_size()) {
+            // the local PD elements as a box of the generated lattice in lattice order?
+            const double hh = desc->scenario->spacing;
+            const int E = int(lel.size());
+            double org[3] = {1e300, 1e300, 1e300};
+            for (int e = 0; e < E; ++e)
+                for (int c = 0; c < 3; ++c)
+                    org[c] = std::min(org[c], s.centroid[3 * (size_t)s.pd_active[lel[e]] + c]);
+            long long n[3] = {0, 0, 0};
+            std::vector<int> idx(3 * (size_t)E);
+            for (int e = 0; e < E; ++e)
+                for (int c = 0; c < 3; ++c) {
+                    const long long q = std::llround(
+                        (s.centroid[3 * (size_t)s.pd_active[lel[e]] + c] - org[c]) / hh);
+                    idx[3 * (size_t)e + c] = int(q);
+                    n[c] = std::max(n[c], q + 1);
+                }
+            bool box = hh > 0.0 && n[0] * n[1] * n[2] == E;
+            for (int e = 0; e < E && box; ++e)
+                box = ((long long)idx[3 * (size_t)e + 2] * n[1] + idx[3 * (size_t)e + 1]) * n[0] +
+                          idx[3 * (size_t)e] == e;
+            if (box) {
+                h->lat.nx = int(n[0]);
+                h->lat.ny = int(n[1]);
+                h->lat.nz = int(n[2]);
+                h->lat.h = hh;
+                int8_t table[343];
+                mtsk::lin_lat_slot_table(table);
+                int8_t* dslot = h->alloc<int8_t>(343);
+                CKM(cudaMemcpy(dslot, table, 343, cudaMemcpyHostToDevice));
+                h->lat.slot = dslot;
+                h->lat.coefS = h->alloc<double>((size_t)mtsk::lin_lat_stencil_size() * E);
+                h->lat.maskS = h->alloc<uint32_t>(4 * (size_t)E);
+                // (an entry outside the 122 offsets -- another horizon -- keeps the ELL form)
+                h->lin_lat = mtsk::lin_lat_build(h->pdv, h->lat, h->stream);
+                if (!h->lin_lat) {
+                    h->release(h->lat.coefS);
+                    h->release(h->lat.maskS);
+                    h->lat.coefS = nullptr;
+                    h->lat.maskS = nullptr;
+                }
+            }
+        }
+        if (!h->lin_lat) {  // entry-major families for the linear PD force (coalesced lanes)
             const size_t ek = (size_t)h->pdv.E * h->pdv.K;
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
             mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->stream);
         }
-        h->mask_words = (size_t)h->pdv.W * h->pdv.E;
-        h->mask_sync = h->alloc<uint32_t>(h->mask_words);
-        CKM(cudaMemcpy(h->mask_sync, h->mask_live, sizeof(uint32_t) * h->mask_words,
-                       cudaMemcpyDeviceToDevice));
+        h->snapshot_bonds();
+        CKM(cudaStreamSynchronize(h->stream));
 
         // ---- device arrays ----
         auto flags = [](int n, const std::vector<int32_t>& bc, const std::vector<double>& vel,
@@ -2141,6 +2200,7 @@ int pmts_mts_view_get(const pmts_mts* h, pmts_mts_view* v) {
         v->cpl_fe_w = s.cpl_fe_w.data();
         v->fe_mesh_elems = s.fe_mesh_elems;
         v->fe_mesh_nodes = s.fe_mesh_nodes;
+        v->pd_linear_lattice = h->lin_lat ? 1 : 0;
         v->pairs = h->pairs.data();
         v->pe_weight = h->pe_weight.data();
         v->node_xyz = s.nodes.data();

@@ -67,6 +67,8 @@ class MtsSolver:
         d.interface_recursion = 1 if run.get("interface_h_pd", "precompute") == "recursion" else 0
         # run.interface_h_fe = sparse (default) | unit_columns (explicit FE side)
         d.interface_h_fe = 1 if run.get("interface_h_fe", "sparse") == "unit_columns" else 0
+        # run.pd_linear = lattice (default: where the PD elements are a 3D box lattice) | ell
+        d.pd_linear = 1 if run.get("pd_linear", "lattice") == "ell" else 0
         if shard is not None:
             d.shard_rank, d.shard_world = int(shard[0]), int(shard[1])
         h = C.c_void_p()
@@ -131,6 +133,7 @@ class MtsSolver:
             "cpl_fe_col": _arr(v.cpl_fe_col, i32, v.cpl_fe_nnz),
             "cpl_fe_w": _arr(v.cpl_fe_w, f64, v.cpl_fe_nnz),
             "fe_mesh_elems": v.fe_mesh_elems, "fe_mesh_nodes": v.fe_mesh_nodes,
+            "pd_linear_lattice": bool(v.pd_linear_lattice),
         }
 
     # -- integration --------------------------------------------------------

@@ -39,3 +39,28 @@ def test_cfg5_twin_shards_bitwise():
     for w in ("fe", "pd"):
         for x, y in zip(one.state(w), grp.state(w)):
             assert np.array_equal(x, y)
+
+
+def test_lattice_linear_force_matches_ell():
+    """The homogeneous substeps' linear PD force on the lattice tile kernel (default on a
+    3D box lattice, pd_mts_lat.cu) is the ELL form's operator -- the same coefficients in
+    stencil order, xi = h o instead of centroid differences: the coupled run it drives
+    equals the ELL-driven one to rounding (multipliers, states, broken counts)."""
+    out = {}
+    for form in ("lattice", "ell"):
+        c = copy.deepcopy(cf.get("cfg5_mts_small"))
+        c.setdefault("run", {})["pd_linear"] = form
+        s = MtsSolver(c)
+        assert bool(s.view.pd_linear_lattice) == (form == "lattice")
+        s.initialize()
+        reps = s.macro_step(12)
+        out[form] = (reps, s.lam(), s.state("fe"), s.state("pd"))
+    a, b = out["lattice"], out["ell"]
+    assert [r["newly_broken"] for r in a[0]] == [r["newly_broken"] for r in b[0]]
+    assert all(abs(x["interface_iterations"] - y["interface_iterations"]) <= 1
+               for x, y in zip(a[0], b[0]))
+    assert max(r["continuity"] for r in a[0]) <= 1e-8
+    assert np.linalg.norm(a[1] - b[1]) <= 1e-7 * np.linalg.norm(b[1])
+    for w in (2, 3):
+        for x, y in zip(a[w], b[w]):
+            assert np.linalg.norm(x - y) <= 1e-8 * max(np.linalg.norm(y), 1e-300)
