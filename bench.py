@@ -585,7 +585,9 @@ def bench_cfg5_mts(steps: int, warmup: int) -> dict:
     setup = time.perf_counter() - t0
     free_b, total_b = torch.cuda.mem_get_info(0)
     reps = s.macro_step(warmup)
+    torch.cuda.profiler.start()  # (a range for `ncu --profile-from-start off`; no-op otherwise)
     ms = s.macro_step_timed(steps)
+    torch.cuda.profiler.stop()
     last = s.macro_step(1)[0]
     u = s.state("pd")[0]
     return {"metric": MTS_METRIC, "unit": MTS_UNIT, "value": steps / (ms * 1e-3),

@@ -351,6 +351,11 @@ typedef struct {
                                     kernel of pd_mts_lat.cu (coefficients in stencil order,
                                     ubar apron in shared memory), else the ELL form; 1 = the
                                     ELL form everywhere (the two differ by rounding only) */
+    int32_t pd_elem_products;    /* free PD substeps (free_solve_pd, mts.hpp:152-180): the
+                                    per-element node products Nsh u_a and their sum formed once
+                                    per force call instead of once per family entry (bitwise
+                                    the same force): 0 = from 2^18 PD elements on, 1 = always,
+                                    2 = never */
 } pmts_mts_desc;
 
 typedef struct {

@@ -83,7 +83,7 @@ class MtsDesc(C.Structure):
                 ("beta_fe", _D), ("interface_mode", _I), ("enforce_continuity", _I),
                 ("track_energy", _I), ("device", _I), ("fe_spacing", _D),
                 ("interface_precond", _I), ("interface_recursion", _I), ("shard_world", _I),
-                ("shard_rank", _I), ("interface_h_fe", _I), ("pd_linear", _I)]
+                ("shard_rank", _I), ("interface_h_fe", _I), ("pd_linear", _I), ("pd_elem_products", _I)]
 
 
 class MtsShardView(C.Structure):

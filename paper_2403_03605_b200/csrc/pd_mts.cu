@@ -365,6 +365,29 @@ __global__ void k_dense_matvec(int n, const double* A, const double* x, double* 
 // (pd_det.cu k_det_bond: eta from node displacements in the (i<j) orientation,
 // exact stretch, inclusive test) with a warp-tree sum instead of the ascending
 // serial sum -- small PD subdomains are latency-bound at one thread per element.
+// Per element the products q_a = Nsh x(node_a) the force kernel forms for every partner
+// (Q[e][a][c]) and their ascending sum S[e][c] -- the very expressions of k_pd_force_warp,
+// so reading them instead of gathering 2^dim nodes per family entry is bitwise the same.
+template <int DIM>
+__global__ void k_pd_elem_q(DevPD d, const double* __restrict__ x, double* __restrict__ Q,
+                            double* __restrict__ S) {
+    constexpr int NN = DIM == 2 ? 4 : 8;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= d.E) return;
+    double q[NN][DIM];
+    for (int a = 0; a < NN; ++a) {
+        const int node = d.conn[a * d.E + e];
+        for (int c = 0; c < DIM; ++c) q[a][c] = d.Nsh * x[(size_t)node * DIM + c];
+    }
+    for (int a = 0; a < NN; ++a)
+        for (int c = 0; c < DIM; ++c) Q[((size_t)e * NN + a) * DIM + c] = q[a][c];
+    for (int c = 0; c < DIM; ++c) {
+        double sacc = 0.0;
+        for (int a = 0; a < NN; ++a) sacc = sacc + q[a][c];
+        S[(size_t)e * DIM + c] = sacc;
+    }
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kT) k_pd_force_warp(DevPD d, const double* __restrict__ x,
                                                       uint32_t* __restrict__ mask, int do_break,
@@ -416,6 +439,89 @@ __global__ void __launch_bounds__(kT) k_pd_force_warp(DevPD d, const double* __r
                     for (int a = 0; a < NN; ++a) sacc = sacc - qp[a][c];
                     eta[c] = sacc;
                 }
+                for (int c = 0; c < 3; ++c) xi[c] = ce[c] - cp[c];
+            }
+            double dot = xi[0] * eta[0] + xi[1] * eta[1];
+            if constexpr (DIM == 3) dot = dot + xi[2] * eta[2];
+            const double t = d.coef[(size_t)k * E + e] * dot;
+            if (e > p) {
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] + t * xi[c];
+            } else {
+                for (int c = 0; c < DIM; ++c) G[c] = G[c] - t * xi[c];
+            }
+            if (do_break) {
+                const double xin = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+                double len2 = 0.0;
+                for (int c = 0; c < DIM; ++c) {
+                    const double v = xi[c] + eta[c];
+                    len2 = len2 + v * v;
+                }
+                const double len = sqrt(len2);
+                const double sv = len <= 0.0 ? -1.0 : (len - xin) / xin;
+                brk = sv >= d.s_crit;
+                if (brk && e < p && owns_elem(d, e)) ++nb;  // once per bond, by its owner
+            }
+        }
+        if (do_break) {
+            const unsigned bal = __ballot_sync(0xffffffffu, brk);
+            if (lane == 0 && bal) mask[(size_t)(k0 >> 5) * E + e] = word & ~bal;
+        }
+    }
+    for (int c = 0; c < DIM; ++c)
+        for (int o = 16; o > 0; o >>= 1) G[c] += __shfl_down_sync(0xffffffffu, G[c], o);
+    if (lane == 0)
+        for (int c = 0; c < DIM; ++c) d.G[(size_t)e * DIM + c] = G[c];
+    if (do_break) {
+        for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+        if (lane == 0 && nb) atomicAdd(cnt, (unsigned long long)nb);
+    }
+}
+
+// k_pd_force_warp for large subdomains, on the per-element node products of k_pd_elem_q:
+// the same expressions in the same order (eta of an entry with e < p is S_p - q_e0 - ...
+// - q_e7, with e > p it is S_e - q_p0 - ... - q_p7), so the force, the stretch test and the
+// bond states are bitwise those of k_pd_force_warp.  The element's own products sit in
+// shared memory and the partner's stream through two registers, so the kernel fits 64
+// registers and four blocks per SM -- the original holds both sets (149 registers, one
+// block per SM, 8 warps) and ran 150 ms per call at BASELINE cfg5, latency-bound.
+template <int DIM>
+__global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __restrict__ mask,
+                                                           int do_break, unsigned long long* cnt,
+                                                           const double* __restrict__ Q,
+                                                           const double* __restrict__ S) {
+    constexpr int NN = DIM == 2 ? 4 : 8, NQ = NN * DIM;
+    __shared__ double qes[kT / 32][NQ];
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (e >= d.E) return;
+    const int E = d.E;
+    double* qe = qes[threadIdx.x >> 5];
+    if (lane < NQ) qe[lane] = Q[(size_t)e * NQ + lane];
+    __syncwarp();
+    double Se[DIM];
+    for (int c = 0; c < DIM; ++c) Se[c] = S[(size_t)e * DIM + c];
+    const double ce[3] = {d.cen[e], d.cen[E + e], d.cen[2 * E + e]};
+    double G[DIM];
+    for (int c = 0; c < DIM; ++c) G[c] = 0.0;
+    unsigned nb = 0;
+    for (int k0 = 0; k0 < d.K; k0 += 32) {
+        const int k = k0 + lane;
+        const int p = k < d.K ? d.col[(size_t)k * E + e] : -1;
+        const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
+        const bool on = p >= 0 && ((word >> lane) & 1u);
+        bool brk = false;
+        if (on) {
+            double eta[DIM], xi[3];
+            const double cp[3] = {d.cen[p], d.cen[E + p], d.cen[2 * E + p]};
+            if (e < p) {
+                for (int c = 0; c < DIM; ++c) eta[c] = S[(size_t)p * DIM + c];
+                for (int a = 0; a < NN; ++a)
+                    for (int c = 0; c < DIM; ++c) eta[c] = eta[c] - qe[a * DIM + c];
+                for (int c = 0; c < 3; ++c) xi[c] = cp[c] - ce[c];
+            } else {
+                const double* qp = Q + (size_t)p * NQ;
+                for (int c = 0; c < DIM; ++c) eta[c] = Se[c];
+                for (int a = 0; a < NN; ++a)
+                    for (int c = 0; c < DIM; ++c) eta[c] = eta[c] - qp[a * DIM + c];
                 for (int c = 0; c < 3; ++c) xi[c] = ce[c] - cp[c];
             }
             double dot = xi[0] * eta[0] + xi[1] * eta[1];
@@ -710,10 +816,21 @@ __global__ void k_scatter_scaled(int n, const int32_t* idx, const double* w, dou
 }  // namespace
 
 void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
-                   unsigned long long* cnt, cudaStream_t s) {
+                   unsigned long long* cnt, cudaStream_t s, double* Q, double* S) {
     const int b = (int)(((long long)d.E * 32 + kT - 1) / kT);
-    if (d.dim == 2) k_pd_force_warp<2><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
-    else k_pd_force_warp<3><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
+    if (Q && S) {  // large subdomains: the per-element node products first (bitwise the same)
+        if (d.dim == 2) {
+            k_pd_elem_q<2><<<blocks(d.E), kT, 0, s>>>(d, x, Q, S);
+            k_pd_force_warp_q<2><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S);
+        } else {
+            k_pd_elem_q<3><<<blocks(d.E), kT, 0, s>>>(d, x, Q, S);
+            k_pd_force_warp_q<3><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S);
+        }
+    } else if (d.dim == 2) {
+        k_pd_force_warp<2><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
+    } else {
+        k_pd_force_warp<3><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);
+    }
     check("pd_force_warp");
 }
 void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double* ubar,

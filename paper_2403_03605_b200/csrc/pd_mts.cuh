@@ -11,8 +11,11 @@ namespace mtsk {
 // PD substep kernels of the integrator: warp-per-element K^PD x (optional bond
 // test into mask / cnt), node sum fused with the explicit solve, the predictor
 // fused with zeroing the load, and scaled multiplier rows.
+// Q / S (E x 2^dim x dim and E x dim scratch, or null): the per-element node products
+// computed once per call instead of per family entry -- bitwise the same force
 void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
-                   unsigned long long* cnt, cudaStream_t s);
+                   unsigned long long* cnt, cudaStream_t s, double* Q = nullptr,
+                   double* S = nullptr);
 // linear (no bond test) K^PD x via centroid displacements; ubar: E x dim scratch
 void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double* ubar,
                   cudaStream_t s);

@@ -98,8 +98,11 @@ __device__ __forceinline__ void entry(Ctx& c) {
     double dot = imul<O::di>(e0);
     dot = iaxpy<O::dj>(dot, e1);
     dot = iaxpy<O::dk>(dot, e2);
+    // the coefficient load does not depend on the bond state (absent entries hold 0), so
+    // the compiler can issue it far ahead of its use: the kernel lives on loads in flight
+    const double cf = __ldcs(c.coef + (size_t)K * c.E);
     const bool act = (c.m[K >> 5] >> (K & 31)) & 1u;
-    const double t = act ? c.coef[(size_t)K * c.E] * dot : 0.0;
+    const double t = act ? cf * dot : 0.0;
     c.gx = iaxpy<-O::di>(c.gx, t);
     c.gy = iaxpy<-O::dj>(c.gy, t);
     c.gz = iaxpy<-O::dk>(c.gz, t);

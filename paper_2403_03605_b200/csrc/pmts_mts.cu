@@ -319,6 +319,9 @@ struct pmts_mts {
     // homogeneous substeps on the k_sync snapshot runs in pd_mts_lat.cu
     bool lin_lat = false;
     mtsk::LinLat lat;
+    // free substeps on large PD subdomains: per-element node products, formed once per
+    // force call instead of once per family entry (pd_mts.cu k_pd_elem_q)
+    double *elem_q = nullptr, *elem_s = nullptr;
     double *lam_d = nullptr, *lam_tmp = nullptr, *gvec = nullptr;          // size nl
     int32_t *hfe_rp = nullptr, *hfe_ci = nullptr;                          // H_FE, CSR
     double* hfe_v = nullptr;
@@ -434,7 +437,7 @@ struct pmts_mts {
 
     void pd_K(double* x, double* y, uint32_t* mask, bool do_break, int slot) {
         halo(x);  // sharded: the halo dofs of x from their owners
-        mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream);
+        mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s);
         launch_node_force(pdv, y, stream);
     }
 
@@ -650,7 +653,7 @@ struct pmts_mts {
     void pd_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
                   uint32_t* mask, bool do_break, int slot, bool homog, const DState& out) {
         if (do_break || !homog)  // free substeps: the deterministic per-entry arithmetic
-            mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream);
+            mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s);
         else  // homogeneous linear substeps (unit, link, interface): centroid form
             force_lin(rdp, mask);
         mtsk::pd_node_explicit(pdv, ra, ra_scale, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
@@ -1968,6 +1971,11 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
             mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->stream);
+        }
+        if (desc->pd_elem_products == 1 ||
+            (desc->pd_elem_products == 0 && h->pdv.E >= (1 << 18))) {  // (small: launch-bound)
+            h->elem_q = h->alloc<double>((size_t)h->pdv.E * nn * dim);
+            h->elem_s = h->alloc<double>((size_t)h->pdv.E * dim);
         }
         h->snapshot_bonds();
         CKM(cudaStreamSynchronize(h->stream));

@@ -69,6 +69,8 @@ class MtsSolver:
         d.interface_h_fe = 1 if run.get("interface_h_fe", "sparse") == "unit_columns" else 0
         # run.pd_linear = lattice (default: where the PD elements are a 3D box lattice) | ell
         d.pd_linear = 1 if run.get("pd_linear", "lattice") == "ell" else 0
+        # run.pd_elem_products = auto (default) | on | off
+        d.pd_elem_products = {"auto": 0, "on": 1, "off": 2}[run.get("pd_elem_products", "auto")]
         if shard is not None:
             d.shard_rank, d.shard_world = int(shard[0]), int(shard[1])
         h = C.c_void_p()

@@ -64,3 +64,26 @@ def test_lattice_linear_force_matches_ell():
     for w in (2, 3):
         for x, y in zip(a[w], b[w]):
             assert np.linalg.norm(x - y) <= 1e-8 * max(np.linalg.norm(y), 1e-300)
+
+
+def test_element_products_are_bitwise():
+    """Free PD substeps with the per-element node products formed once per force call
+    (the default from 2^18 PD elements on) instead of once per family entry: the same
+    expressions, so reports, multipliers, states and bond states are bit for bit equal."""
+    out = {}
+    for form in ("on", "off"):
+        c = copy.deepcopy(cf.get("cfg5_mts_small"))
+        c.setdefault("run", {})["pd_elem_products"] = form
+        s = MtsSolver(c)
+        s.initialize()
+        reps = s.macro_step(12)
+        out[form] = (reps, s.lam(), s.state("fe"), s.state("pd"), s.intact())
+    a, b = out["on"], out["off"]
+    assert sum(r["newly_broken"] for r in a[0]) > 0
+    for x, y in zip(a[0], b[0]):
+        for f in ("newly_broken", "interface_iterations", "continuity", "lambda_fe", "lambda_pd"):
+            assert x[f] == y[f], f
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[4], b[4])
+    for w in (2, 3):
+        for x, y in zip(a[w], b[w]):
+            assert np.array_equal(x, y)
