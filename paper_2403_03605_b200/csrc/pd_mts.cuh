@@ -84,13 +84,15 @@ void pd_force_lin_t(const DevPD& d, const int32_t* colT, const double* coefT, co
 struct LinLat {
     int nx = 0, ny = 0, nz = 0;
     double h = 0.0;
-    double* coefS = nullptr;     // [122 E]
+    double* coefS = nullptr;     // [61 E]: the positive offsets' coefficients
     uint32_t* maskS = nullptr;   // [4 E]
     const int8_t* slot = nullptr;  // [7^3] offset -> stencil slot (-1: none), device
 };
 void lin_lat_slot_table(int8_t* table343);
 int lin_lat_stencil_size();
-bool lin_lat_build(const DevPD& d, const LinLat& L, cudaStream_t s);  // false: an entry off the stencil
+int lin_lat_coef_slots();
+bool lin_lat_build(const DevPD& d, const LinLat& L, cudaStream_t s);  // false: an entry off the
+                                                                     // stencil or an unsymmetric bond
 void lin_lat_mask(const DevPD& d, const LinLat& L, const uint32_t* mask, cudaStream_t s);
 void pd_force_lin_lat(const DevPD& d, const LinLat& L, const double* x, double* ubar,
                       cudaStream_t s);

@@ -11,8 +11,9 @@
 //     G_e = - sum_p coef_ep (xi . (ubar_p - ubar_e)) xi ,   coef_ep = (1 - alpha) V_e V_p c(|xi|)
 //
 // runs here with one element per thread over a 16 x 4 x 4 tile whose ubar apron sits in
-// shared memory: the per-entry coefficients are re-laid in STENCIL order
-// (coefS[s E + e]: one coalesced 8-byte stream per offset, absent entries 0), the bond
+// shared memory: the per-entry coefficients are re-laid in STENCIL order, each bond's once
+// (coefS[s E + e] for the 61 positive offsets: one coalesced 8-byte stream per offset,
+// absent entries 0; the upper element reads its partner's copy), the bond
 // states of the k_sync snapshot as 122 stencil bits per element, and xi = h o is the
 // nominal lattice vector (compile-time integers; the ELL form subtracts centroids, a
 // 1e-16-level difference).  The coefficients are the very values the ELL form
@@ -84,6 +85,7 @@ struct Ctx {
     const double* ua;
     const double* coef;  // coefS + e
     size_t E;
+    int nx, nxy;         // element-id strides of a y / z step
     int q0;
     double ex, ey, ez;
     uint32_t m[4];
@@ -98,10 +100,19 @@ __device__ __forceinline__ void entry(Ctx& c) {
     double dot = imul<O::di>(e0);
     dot = iaxpy<O::dj>(dot, e1);
     dot = iaxpy<O::dk>(dot, e2);
-    // the coefficient load does not depend on the bond state (absent entries hold 0), so
-    // the compiler can issue it far ahead of its use: the kernel lives on loads in flight
-    const double cf = __ldcs(c.coef + (size_t)K * c.E);
+    // A bond's coefficient is stored once, at its lower element under the positive
+    // offset (slot K - 61); the entry of the upper element reads it there (e + o is the
+    // partner, which exists whenever the bit is set).  The loads depend on nothing but the
+    // bond states read at kernel start, so the compiler can issue them far ahead of their
+    // use: the kernel lives on loads in flight.
     const bool act = (c.m[K >> 5] >> (K & 31)) & 1u;
+    double cf;
+    if constexpr (K >= S3 / 2) {
+        cf = c.coef[(size_t)(K - S3 / 2) * c.E];
+    } else {
+        const int lin = O::dk * c.nxy + O::dj * c.nx + O::di;
+        cf = act ? c.coef[(size_t)(S3 / 2 - 1 - K) * c.E + lin] : 0.0;
+    }
     const double t = act ? cf * dot : 0.0;
     c.gx = iaxpy<-O::di>(c.gx, t);
     c.gy = iaxpy<-O::dj>(c.gy, t);
@@ -135,8 +146,10 @@ __device__ __forceinline__ int slot_of(const LinLat& L, int e, int p) {
     return L.slot[((dk + 3) * 7 + dj + 3) * 7 + di + 3];
 }
 
-// coefS[s E + e] = the coefficient of the entry of e with offset s (coefS zeroed before)
-__global__ void k_lin_lat_build(DevPD d, LinLat L, int* err) {
+// pass 0: coefS[(s - 61) E + e] = the coefficient of the entry of e with the positive
+// offset s (coefS zeroed before); pass 1: every entry with a negative offset carries the
+// very bits stored at its partner under the opposite offset (the bond's one coefficient)
+__global__ void k_lin_lat_build(DevPD d, LinLat L, int pass, int* err) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // q = k E + e
     if (q >= (long long)d.K * d.E) return;
     const int e = (int)(q % d.E);
@@ -147,7 +160,13 @@ __global__ void k_lin_lat_build(DevPD d, LinLat L, int* err) {
         *err = 1;
         return;
     }
-    L.coefS[(size_t)s * d.E + e] = d.coef[q];
+    if (pass == 0) {
+        if (s >= S3 / 2) L.coefS[(size_t)(s - S3 / 2) * d.E + e] = d.coef[q];
+    } else if (s < S3 / 2) {
+        if (__double_as_longlong(L.coefS[(size_t)(S3 / 2 - 1 - s) * d.E + p]) !=
+            __double_as_longlong(d.coef[q]))
+            *err = 2;
+    }
 }
 
 // the ELL bond states (bit k of word k / 32) as stencil bits
@@ -197,6 +216,8 @@ k_pd_force_lin_lat(DevPD d, LinLat L, const double* __restrict__ ub) {
     c.ua = ua;
     c.coef = L.coefS + e;
     c.E = (size_t)d.E;
+    c.nx = L.nx;
+    c.nxy = L.nx * L.ny;
     c.q0 = 3 * (((tz + R) * AY + ty + R) * AX + tx + R);
     c.ex = ua[c.q0];
     c.ey = ua[c.q0 + 1];
@@ -225,14 +246,16 @@ void lin_lat_slot_table(int8_t* table343) {
         table343[((o.dk[s] + 3) * 7 + o.dj[s] + 3) * 7 + o.di[s] + 3] = (int8_t)s;
 }
 int lin_lat_stencil_size() { return S3; }
+int lin_lat_coef_slots() { return S3 / 2; }
 
 bool lin_lat_build(const DevPD& d, const LinLat& L, cudaStream_t s) {
     int* err = nullptr;
     if (cudaMalloc(&err, sizeof(int)) != cudaSuccess) throw std::runtime_error("CUDA: cudaMalloc");
     cudaMemsetAsync(err, 0, sizeof(int), s);
-    cudaMemsetAsync(L.coefS, 0, sizeof(double) * (size_t)S3 * d.E, s);
+    cudaMemsetAsync(L.coefS, 0, sizeof(double) * (size_t)(S3 / 2) * d.E, s);
     const long long n = (long long)d.K * d.E;
-    k_lin_lat_build<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, L, err);
+    for (int pass = 0; pass < 2; ++pass)
+        k_lin_lat_build<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, L, pass, err);
     check_last("lin_lat_build");
     int h = 0;
     cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s);

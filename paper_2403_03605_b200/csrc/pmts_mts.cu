@@ -1954,7 +1954,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
                 int8_t* dslot = h->alloc<int8_t>(343);
                 CKM(cudaMemcpy(dslot, table, 343, cudaMemcpyHostToDevice));
                 h->lat.slot = dslot;
-                h->lat.coefS = h->alloc<double>((size_t)mtsk::lin_lat_stencil_size() * E);
+                h->lat.coefS = h->alloc<double>((size_t)mtsk::lin_lat_coef_slots() * E);
                 h->lat.maskS = h->alloc<uint32_t>(4 * (size_t)E);
                 // (an entry outside the 122 offsets -- another horizon -- keeps the ELL form)
                 h->lin_lat = mtsk::lin_lat_build(h->pdv, h->lat, h->stream);

@@ -86,6 +86,33 @@ def main_mts(names=None):
         print(name, run)
 
 
+# system arrays of the full-size coupled fixture kept as sha256 only (tens of MB otherwise)
+FULL_HASHED = ("fe_k_val", "fe_mass", "fe_p_ext", "pd_mass", "pd_p_ext", "fe_dof", "pd_dof",
+               "pairs", "pe_weight")
+
+
+def main_mts_full(steps=3):
+    """BASELINE cfg2's conforming analog at full size (0.25 mm, n_lambda = 14,436) through
+    the reference's own coupled loop (~10 minutes of reference setup): end states, the
+    multipliers and the interface iteration counts, the assembled systems as sha256."""
+    out_dir = os.path.dirname(os.path.abspath(__file__))
+    text = cf.render_cfg(cf.get("cfg2"))
+    with tempfile.TemporaryDirectory() as tmp:
+        run = po.run_ref_mts(text, tmp, steps=steps)
+        d = po.load_ref_mts_dump(tmp)
+    arrays = {k: d[k] for k in ("fe_u", "fe_v", "pd_u", "pd_v", "lambda", "iterations")}
+    meta = {k: v for k, v in d.items() if not isinstance(v, np.ndarray)}
+    meta.update(scenario="cfg2", steps=steps, run=run,
+                sha256={k: hashlib.sha256(np.ascontiguousarray(d[k]).tobytes()).hexdigest()
+                        for k in FULL_HASHED})
+    np.savez_compressed(os.path.join(out_dir, "mts_cfg2_full.npz"), cfg=np.array(text),
+                        meta=np.array(json.dumps(meta)), **arrays)
+    print("mts_cfg2_full", run)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["mts_cfg2_full"]:
+        main_mts_full()
+        sys.exit(0)
     main([a for a in sys.argv[1:] if not a.startswith("mts")] or None)
     main_mts([a for a in sys.argv[1:] if a.startswith("mts")] or None)
