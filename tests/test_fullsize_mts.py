@@ -1,8 +1,15 @@
-"""Full-size coupled MTS parity against the reference's own coupled loop (opt-in:
-the reference needs ~9 minutes of setup at BASELINE cfg2's conforming analog --
-0.25 mm, n_lambda = 14436).  Enable with PMTS_FULLSIZE=1 on a GPU box
-(PMTS_FULLSIZE_MTS_STEPS macro steps, default 3); the result recorded in
-DESIGN.md came from exactly this test."""
+"""Full-size coupled MTS parity against the reference's own coupled loop at BASELINE
+cfg2's conforming analog (0.25 mm, n_lambda = 14436).
+
+* `test_cfg2_full_size_vs_reference_golden` (always on): against
+  tests/golden/mts_cfg2_full.npz -- the reference's end states, multipliers and interface
+  iteration counts after 3 macro steps, and the sha256 of its assembled systems, made
+  here by tests/golden/make_golden.py mts_cfg2_full (the reference needs ~10 minutes of
+  setup, so it does not run on the GPU box).
+* `test_cfg2_coupled_vs_reference` (opt-in, PMTS_FULLSIZE=1): runs the reference on the
+  GPU box itself (PMTS_FULLSIZE_MTS_STEPS macro steps, default 3)."""
+import hashlib
+import json
 import os
 import tempfile
 
@@ -13,11 +20,38 @@ from oracle import pyoracle as po
 from paper_2403_03605_b200 import configs as cf
 from paper_2403_03605_b200.mts import MtsSolver
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(os.environ.get("PMTS_FULLSIZE") != "1",
-                                 reason="full-size reference run is opt-in (PMTS_FULLSIZE=1)")]
+pytestmark = [pytest.mark.gpu]
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mts_cfg2_full.npz")
 
 
+def test_cfg2_full_size_vs_reference_golden():
+    g = np.load(GOLDEN, allow_pickle=False)
+    meta = json.loads(str(g["meta"]))
+    sc = cf.get("cfg2")
+    assert cf.render_cfg(sc) == str(g["cfg"])  # the scenario the reference ran
+    s = MtsSolver(sc)
+    sy = s.system()
+    for k, h in meta["sha256"].items():  # assembled systems, pairs, bond weights: bitwise
+        assert hashlib.sha256(np.ascontiguousarray(sy[k]).tobytes()).hexdigest() == h, k
+    s.initialize()
+    reps = s.macro_step(meta["steps"])
+    rel = {}
+    for w in ("fe", "pd"):
+        u, v, _ = s.state(w)
+        for x, k in ((u, "u"), (v, "v")):
+            r = g[f"{w}_{k}"]
+            rel[f"{w}_{k}"] = float(np.linalg.norm(x - r) / np.linalg.norm(r))
+    rel["lambda"] = float(np.linalg.norm(s.lam() - g["lambda"]) / np.linalg.norm(g["lambda"]))
+    iters = [r["interface_iterations"] for r in reps]
+    print(f"cfg2 full size, {meta['steps']} macro steps: device relL2 {rel}; iterations {iters} "
+          f"vs the reference's {list(g['iterations'])}")
+    assert max(rel.values()) <= 1e-8
+    assert all(abs(a - int(b)) <= 1 for a, b in zip(iters, g["iterations"]))
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("PMTS_FULLSIZE") != "1",
+                    reason="full-size reference run is opt-in (PMTS_FULLSIZE=1)")
 @pytest.mark.parametrize("name", [os.environ.get("PMTS_FULLSIZE_MTS", "cfg2")])
 def test_cfg2_coupled_vs_reference(name):
     steps = int(os.environ.get("PMTS_FULLSIZE_MTS_STEPS", "3"))
