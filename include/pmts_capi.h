@@ -23,7 +23,8 @@
 extern "C" {
 #endif
 
-#define PMTS_ABI_VERSION 1
+#define PMTS_ABI_VERSION 2  /* 2: pmts_mts_desc.pd_linear / pd_elem_products,
+                                  pmts_mts_view.pd_linear_lattice, PMTS_OPT_CLEAN_TILES */
 
 enum pmts_status {
     PMTS_OK = 0,

@@ -172,6 +172,7 @@ SIGNATURES = {
     "pmts_mts_comm_init": (C.c_int, [_P, _P]),
 }
 
+ABI_VERSION = 2  # include/pmts_capi.h PMTS_ABI_VERSION
 _lib = None
 
 
@@ -186,6 +187,9 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.pmts_abi_version() != ABI_VERSION:  # the structs below mirror that header
+            raise ImportError(f"{LIB_PATH}: ABI {L.pmts_abi_version()}, this binding is for "
+                              f"{ABI_VERSION}: rebuild (__graft_entry__.build())")
         _lib = L
     return _lib
 

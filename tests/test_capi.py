@@ -31,7 +31,7 @@ def test_library_exports_every_symbol():
 
 def test_abi_version_and_error_string():
     L = capi.lib()
-    assert L.pmts_abi_version() == 1
+    assert L.pmts_abi_version() == capi.ABI_VERSION == 2
     assert isinstance(L.pmts_last_error(), bytes)
 
 
