@@ -368,6 +368,11 @@ __global__ void k_dense_matvec(int n, const double* A, const double* x, double* 
 // Per element the products q_a = Nsh x(node_a) the force kernel forms for every partner
 // (Q[e][a][c]) and their ascending sum S[e][c] -- the very expressions of k_pd_force_warp,
 // so reading them instead of gathering 2^dim nodes per family entry is bitwise the same.
+// S is a 64-byte record per element, {centroid x, y, z, S_x, S_y, S_z, 0, 0}: the partner
+// data of an entry with e < p in two sectors and three 16-byte loads (the centroids' three
+// arrays and S were five sectors and six loads -- the kernel below is bound by the L1
+// load wavefronts of its gathers, ncu: 98 % of peak).
+constexpr int kRec = 8;
 template <int DIM>
 __global__ void k_pd_elem_q(DevPD d, const double* __restrict__ x, double* __restrict__ Q,
                             double* __restrict__ S) {
@@ -381,11 +386,14 @@ __global__ void k_pd_elem_q(DevPD d, const double* __restrict__ x, double* __res
     }
     for (int a = 0; a < NN; ++a)
         for (int c = 0; c < DIM; ++c) Q[((size_t)e * NN + a) * DIM + c] = q[a][c];
+    double rec[kRec] = {d.cen[e], d.cen[d.E + e], d.cen[2 * (size_t)d.E + e], 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int c = 0; c < DIM; ++c) {
         double sacc = 0.0;
         for (int a = 0; a < NN; ++a) sacc = sacc + q[a][c];
-        S[(size_t)e * DIM + c] = sacc;
+        rec[3 + c] = sacc;
     }
+    double2* out = reinterpret_cast<double2*>(S + (size_t)e * kRec);
+    for (int i = 0; i < kRec / 2; ++i) out[i] = make_double2(rec[2 * i], rec[2 * i + 1]);
 }
 
 template <int DIM>
@@ -498,8 +506,8 @@ __global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __
     if (lane < NQ) qe[lane] = Q[(size_t)e * NQ + lane];
     __syncwarp();
     double Se[DIM];
-    for (int c = 0; c < DIM; ++c) Se[c] = S[(size_t)e * DIM + c];
-    const double ce[3] = {d.cen[e], d.cen[E + e], d.cen[2 * E + e]};
+    for (int c = 0; c < DIM; ++c) Se[c] = S[(size_t)e * kRec + 3 + c];
+    const double ce[3] = {S[(size_t)e * kRec], S[(size_t)e * kRec + 1], S[(size_t)e * kRec + 2]};
     double G[DIM];
     for (int c = 0; c < DIM; ++c) G[c] = 0.0;
     unsigned nb = 0;
@@ -511,17 +519,27 @@ __global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __
         bool brk = false;
         if (on) {
             double eta[DIM], xi[3];
-            const double cp[3] = {d.cen[p], d.cen[E + p], d.cen[2 * E + p]};
+            const double2* rp = reinterpret_cast<const double2*>(S + (size_t)p * kRec);
+            const double2 r0 = rp[0], r1 = rp[1];  // cen x, y | cen z, S_x
+            const double cp[3] = {r0.x, r0.y, r1.x};
             if (e < p) {
-                for (int c = 0; c < DIM; ++c) eta[c] = S[(size_t)p * DIM + c];
+                const double2 r2 = rp[2];  // S_y, S_z
+                const double sp[3] = {r1.y, r2.x, r2.y};
+                for (int c = 0; c < DIM; ++c) eta[c] = sp[c];
                 for (int a = 0; a < NN; ++a)
                     for (int c = 0; c < DIM; ++c) eta[c] = eta[c] - qe[a * DIM + c];
                 for (int c = 0; c < 3; ++c) xi[c] = cp[c] - ce[c];
             } else {
-                const double* qp = Q + (size_t)p * NQ;
+                // the partner's products in 16-byte loads, subtracted in the same order
+                // (a ascending for every component)
+                const double2* qp = reinterpret_cast<const double2*>(Q + (size_t)p * NQ);
                 for (int c = 0; c < DIM; ++c) eta[c] = Se[c];
-                for (int a = 0; a < NN; ++a)
-                    for (int c = 0; c < DIM; ++c) eta[c] = eta[c] - qp[a * DIM + c];
+#pragma unroll
+                for (int i = 0; i < NQ / 2; ++i) {
+                    const double2 v = qp[i];
+                    eta[(2 * i) % DIM] = eta[(2 * i) % DIM] - v.x;
+                    eta[(2 * i + 1) % DIM] = eta[(2 * i + 1) % DIM] - v.y;
+                }
                 for (int c = 0; c < 3; ++c) xi[c] = ce[c] - cp[c];
             }
             double dot = xi[0] * eta[0] + xi[1] * eta[1];

@@ -11,7 +11,7 @@ namespace mtsk {
 // PD substep kernels of the integrator: warp-per-element K^PD x (optional bond
 // test into mask / cnt), node sum fused with the explicit solve, the predictor
 // fused with zeroing the load, and scaled multiplier rows.
-// Q / S (E x 2^dim x dim and E x dim scratch, or null): the per-element node products
+// Q / S (E x 2^dim x dim and E x 8 scratch, or null): the per-element node products
 // computed once per call instead of per family entry -- bitwise the same force
 void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
                    unsigned long long* cnt, cudaStream_t s, double* Q = nullptr,

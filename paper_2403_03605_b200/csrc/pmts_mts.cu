@@ -1975,7 +1975,7 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
         if (desc->pd_elem_products == 1 ||
             (desc->pd_elem_products == 0 && h->pdv.E >= (1 << 18))) {  // (small: launch-bound)
             h->elem_q = h->alloc<double>((size_t)h->pdv.E * nn * dim);
-            h->elem_s = h->alloc<double>((size_t)h->pdv.E * dim);
+            h->elem_s = h->alloc<double>((size_t)h->pdv.E * 8);  // 64-byte records
         }
         h->snapshot_bonds();
         CKM(cudaStreamSynchronize(h->stream));
