@@ -496,7 +496,9 @@ template <int DIM>
 __global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __restrict__ mask,
                                                            int do_break, unsigned long long* cnt,
                                                            const double* __restrict__ Q,
-                                                           const double* __restrict__ S) {
+                                                           const double* __restrict__ S,
+                                                           const int32_t* __restrict__ colT,
+                                                           const double* __restrict__ coefT) {
     constexpr int NN = DIM == 2 ? 4 : 8, NQ = NN * DIM;
     __shared__ double qes[kT / 32][NQ];
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -513,7 +515,8 @@ __global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __
     unsigned nb = 0;
     for (int k0 = 0; k0 < d.K; k0 += 32) {
         const int k = k0 + lane;
-        const int p = k < d.K ? d.col[(size_t)k * E + e] : -1;
+        // (entry-major copies when present: the lanes of a warp read one line, not 32)
+        const int p = k < d.K ? (colT ? colT[(size_t)e * d.K + k] : d.col[(size_t)k * E + e]) : -1;
         const uint32_t word = mask[(size_t)(k0 >> 5) * E + e];
         const bool on = p >= 0 && ((word >> lane) & 1u);
         bool brk = false;
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(kT, 4) k_pd_force_warp_q(DevPD d, uint32_t* __
             }
             double dot = xi[0] * eta[0] + xi[1] * eta[1];
             if constexpr (DIM == 3) dot = dot + xi[2] * eta[2];
-            const double t = d.coef[(size_t)k * E + e] * dot;
+            const double t = (coefT ? coefT[(size_t)e * d.K + k] : d.coef[(size_t)k * E + e]) * dot;
             if (e > p) {
                 for (int c = 0; c < DIM; ++c) G[c] = G[c] + t * xi[c];
             } else {
@@ -834,15 +837,16 @@ __global__ void k_scatter_scaled(int n, const int32_t* idx, const double* w, dou
 }  // namespace
 
 void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
-                   unsigned long long* cnt, cudaStream_t s, double* Q, double* S) {
+                   unsigned long long* cnt, cudaStream_t s, double* Q, double* S,
+                   const int32_t* colT, const double* coefT) {
     const int b = (int)(((long long)d.E * 32 + kT - 1) / kT);
     if (Q && S) {  // large subdomains: the per-element node products first (bitwise the same)
         if (d.dim == 2) {
             k_pd_elem_q<2><<<blocks(d.E), kT, 0, s>>>(d, x, Q, S);
-            k_pd_force_warp_q<2><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S);
+            k_pd_force_warp_q<2><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S, colT, coefT);
         } else {
             k_pd_elem_q<3><<<blocks(d.E), kT, 0, s>>>(d, x, Q, S);
-            k_pd_force_warp_q<3><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S);
+            k_pd_force_warp_q<3><<<b, kT, 0, s>>>(d, mask, do_break, cnt, Q, S, colT, coefT);
         }
     } else if (d.dim == 2) {
         k_pd_force_warp<2><<<b, kT, 0, s>>>(d, x, mask, do_break, cnt);

@@ -15,7 +15,8 @@ namespace mtsk {
 // computed once per call instead of per family entry -- bitwise the same force
 void pd_force_warp(const DevPD& d, const double* x, uint32_t* mask, int do_break,
                    unsigned long long* cnt, cudaStream_t s, double* Q = nullptr,
-                   double* S = nullptr);
+                   double* S = nullptr, const int32_t* colT = nullptr,
+                   const double* coefT = nullptr);  // colT / coefT: entry-major families
 // linear (no bond test) K^PD x via centroid displacements; ubar: E x dim scratch
 void pd_force_lin(const DevPD& d, const double* x, const uint32_t* mask, double* ubar,
                   cudaStream_t s);

@@ -437,7 +437,7 @@ struct pmts_mts {
 
     void pd_K(double* x, double* y, uint32_t* mask, bool do_break, int slot) {
         halo(x);  // sharded: the halo dofs of x from their owners
-        mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s);
+        mtsk::pd_force_warp(pdv, x, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s, famT_col, famT_coef);
         launch_node_force(pdv, y, stream);
     }
 
@@ -653,7 +653,7 @@ struct pmts_mts {
     void pd_solve(const double* ra, double ra_scale, const double* rvp, const double* rdp,
                   uint32_t* mask, bool do_break, int slot, bool homog, const DState& out) {
         if (do_break || !homog)  // free substeps: the deterministic per-entry arithmetic
-            mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s);
+            mtsk::pd_force_warp(pdv, rdp, mask, do_break ? 1 : 0, d_counts + slot, stream, elem_q, elem_s, famT_col, famT_coef);
         else  // homogeneous linear substeps (unit, link, interface): centroid form
             force_lin(rdp, mask);
         mtsk::pd_node_explicit(pdv, ra, ra_scale, pd_M, pd_cf, rvp, rdp, pd_nm.gdt, pd_nm.bdt2,
@@ -1966,14 +1966,17 @@ int pmts_mts_create(const pmts_mts_desc* desc, pmts_mts** out) {
                 }
             }
         }
-        if (!h->lin_lat) {  // entry-major families for the linear PD force (coalesced lanes)
+        const bool elemq = desc->pd_elem_products == 1 ||
+                           (desc->pd_elem_products == 0 && h->pdv.E >= (1 << 18));
+        // entry-major families (coalesced lanes): the ELL linear force, and the
+        // element-product force of the free substeps
+        if (!h->lin_lat || elemq) {
             const size_t ek = (size_t)h->pdv.E * h->pdv.K;
             h->famT_col = h->alloc<int32_t>(ek);
             h->famT_coef = h->alloc<double>(ek);
             mtsk::family_transpose(h->pdv, h->famT_col, h->famT_coef, h->stream);
         }
-        if (desc->pd_elem_products == 1 ||
-            (desc->pd_elem_products == 0 && h->pdv.E >= (1 << 18))) {  // (small: launch-bound)
+        if (elemq) {  // (small subdomains are launch-bound: one kernel)
             h->elem_q = h->alloc<double>((size_t)h->pdv.E * nn * dim);
             h->elem_s = h->alloc<double>((size_t)h->pdv.E * 8);  // 64-byte records
         }
