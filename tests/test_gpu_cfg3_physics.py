@@ -227,3 +227,22 @@ def test_cfg3_full_size_window_through_crack_initiation():
     assert ref.sum() > 10
     assert agreement(mine, ref) >= 0.999
     assert tip_d <= sc.delta and path <= sc.delta
+    # the fp32-position / fp64-accumulate variant over the same window, from the same state
+    del s
+    sf = _device(sc, capi.FAST_F32POS)
+    sf.set_state(*snaps[0])
+    sf.step(sc.scales(k0 + 1, B))
+    fu, fv, _ = sf.state()
+    print(f"[cfg3 full size, fp32 positions] relL2 u {_rel(fu, ou):.3e} v {_rel(fv, ov):.3e} "
+          f"at step {i - 1}")
+    assert _rel(fu, ou) <= F32_TOL and _rel(fv, ov) <= F32_TOL
+    sf.step(sc.scales(i, W))
+    mf = sf.intact() == 0
+    mmf = broken_midpoints(pairs, mf, sc.centroid)
+    print(f"[cfg3 full size, fp32 positions] step {i + W - 1}: broken {int(mf.sum())}, agreement "
+          f"{agreement(mf, ref):.6f}, tip distance "
+          f"{np.linalg.norm(crack_tip(mmf) - crack_tip(mr)) / sc.delta:.3f} delta, path "
+          f"{hausdorff(mmf, mr) / sc.delta:.3f} delta")
+    assert agreement(mf, ref) >= 0.999
+    assert np.linalg.norm(crack_tip(mmf) - crack_tip(mr)) <= sc.delta
+    assert hausdorff(mmf, mr) <= sc.delta
