@@ -603,7 +603,19 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
 #pragma unroll
         for (int r = 0; r < EPT; ++r) anyc[r] = (cand >> r) & 1u;
         bool none[EPT];
-        if (tile_full) {
+        // a warp of a tile with broken or absent bonds still takes the unmasked instance
+        // when every bond state its own rows read is full: the words of apron rows gy0 ..
+        // gy0 + EPT + 2 (its elements and the partners up to three rows below), all columns
+        // (fp64 cells only: the masked instance moves 2.4x the shared-memory bytes there --
+        // cfg3 36.9 -> 35.1 us; with 8-byte cells the test costs more than it saves)
+        bool wfull = tile_full;
+        if (!F32 && !tile_full) {
+            bool f = true;
+            for (int idx = lane; idx < (EPT + R) * AX; idx += 32)
+                f = f && (ma[gy0 * AX + idx] & kPos) == kPos;
+            wfull = __all_sync(0xffffffffu, f);
+        }
+        if (wfull) {
 #pragma unroll
             for (int sb = 0; sb < EPT; sb += 4)
                 pairs_blocked<false>(ub + q0 + sb * AX, ue + sb, G0 + sb, G1 + sb, none + sb, ps);
