@@ -216,20 +216,36 @@ __device__ __forceinline__ void pair_term(const V* ubq, const uint32_t* maq,
 // (A = 0), -2..5 (|A| = 1, 2, loaded per half of the rows to stay within 80
 // registers) or 0..3 (|A| = 3): 62 shared loads per thread instead of 112 --
 // the shared-memory pipe was the limiter (ncu: 67 % of peak)
-template <bool DO_BREAK, typename V>
+// MASKED: the same cell loads with the bond states applied per pair (the bond e -> e + o
+// under e's own word m0, the bond e - o -> e under the word of e - o, read from maq) --
+// the pairs of an element accumulate in the same order as in pair_terms, so this is
+// bitwise that instance at less than half its shared-memory traffic
+template <bool DO_BREAK, bool MASKED, typename V>
 __device__ __forceinline__ void pairs_blocked(const V* ubq, const V* ue, double* G0, double* G1,
-                                              bool* anyc, const PairStencil2D& ps) {
-    // one block of 4 consecutive rows of the thread (ubq, ue, G, anyc at its first row)
+                                              bool* anyc, const PairStencil2D& ps,
+                                              const uint32_t* maq = nullptr,
+                                              const uint32_t* m0 = nullptr) {
+    // one block of 4 consecutive rows of the thread (ubq, ue, G, anyc, maq, m0 at its first row)
     constexpr int EPT = 4;
+#define PMTS_PM(K, UP, UM, ROW)                                                              \
+    {                                                                                        \
+        bool ap_ = true, am_ = true;                                                         \
+        if (MASKED) {                                                                        \
+            const int bit_ = ps.pbit[K];                                                     \
+            ap_ = (m0[ROW] >> bit_) & 1u;                                                    \
+            am_ = (maq[(ROW)*AX - ps.off[K]] >> bit_) & 1u;                                  \
+        }                                                                                    \
+        pair_math<DO_BREAK, MASKED, K>(UP, UM, ue[ROW], ap_, am_, G0[ROW], G1[ROW], anyc[ROW], ps); \
+    }
     {  // A = 0: (0,1) (0,2) (0,3)
         V c[10];
 #pragma unroll
         for (int i = 0; i < 10; ++i) c[i] = (i >= 3 && i < 7) ? ue[i - 3] : ubq[(i - 3) * AX];
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
-            pair_math<DO_BREAK, false, 0>(c[r + 4], c[r + 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-            pair_math<DO_BREAK, false, 1>(c[r + 5], c[r + 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-            pair_math<DO_BREAK, false, 2>(c[r + 6], c[r], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+            PMTS_PM(0, c[r + 4], c[r + 2], r)
+            PMTS_PM(1, c[r + 5], c[r + 1], r)
+            PMTS_PM(2, c[r + 6], c[r], r)
         }
     }
 #pragma unroll
@@ -246,26 +262,26 @@ __device__ __forceinline__ void pairs_blocked(const V* ubq, const V* ue, double*
             for (int rr = 0; rr < 2; ++rr) {
                 const int r = 2 * half + rr, q = rr + 2;
                 if (g == 1) {
-                    pair_math<DO_BREAK, false, 3>(p[q], m[q], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 4>(p[q + 1], m[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 5>(m[q + 1], p[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 6>(p[q + 2], m[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 7>(m[q + 2], p[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    PMTS_PM(3, p[q], m[q], r)
+                    PMTS_PM(4, p[q + 1], m[q - 1], r)
+                    PMTS_PM(5, m[q + 1], p[q - 1], r)
+                    PMTS_PM(6, p[q + 2], m[q - 2], r)
+                    PMTS_PM(7, m[q + 2], p[q - 2], r)
                 } else {
-                    pair_math<DO_BREAK, false, 8>(p[q], m[q], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 9>(p[q + 1], m[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 10>(m[q + 1], p[q - 1], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 11>(p[q + 2], m[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
-                    pair_math<DO_BREAK, false, 12>(m[q + 2], p[q - 2], ue[r], true, true, G0[r], G1[r], anyc[r], ps);
+                    PMTS_PM(8, p[q], m[q], r)
+                    PMTS_PM(9, p[q + 1], m[q - 1], r)
+                    PMTS_PM(10, m[q + 1], p[q - 1], r)
+                    PMTS_PM(11, p[q + 2], m[q - 2], r)
+                    PMTS_PM(12, m[q + 2], p[q - 2], r)
                 }
             }
         }
     }
 #pragma unroll
     for (int r = 0; r < EPT; ++r)  // |A| = 3: (3,0)
-        pair_math<DO_BREAK, false, 13>(ubq[r * AX + 3], ubq[r * AX - 3], ue[r], true, true, G0[r],
-                                       G1[r], anyc[r], ps);
+        PMTS_PM(13, ubq[r * AX + 3], ubq[r * AX - 3], r)
 }
+#undef PMTS_PM
 
 template <bool DO_BREAK, bool MASKED, int K, typename V>
 __device__ __forceinline__ void pair_terms(const V* ubq, const uint32_t* maq,
@@ -618,12 +634,22 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         if (wfull) {
 #pragma unroll
             for (int sb = 0; sb < EPT; sb += 4)
-                pairs_blocked<false>(ub + q0 + sb * AX, ue + sb, G0 + sb, G1 + sb, none + sb, ps);
+                pairs_blocked<false, false>(ub + q0 + sb * AX, ue + sb, G0 + sb, G1 + sb, none + sb, ps);
         } else {
             uint32_t m0[EPT];
 #pragma unroll
             for (int r = 0; r < EPT; ++r) m0[r] = ma[q0 + r * AX];
-            pair_terms<false, true, 0>(ub + q0, ma + q0, ue, m0, G0, G1, none, ps);
+            // (the blocked loads with bond states fit the register budget with 8-byte cells
+            // only: fp64 spilled ~100 B and ran 37.3 instead of 35.1 us; fp32 positions
+            // 32.0 -> 31.7 us)
+            if constexpr (F32) {
+#pragma unroll
+                for (int sb = 0; sb < EPT; sb += 4)
+                    pairs_blocked<false, true>(ub + q0 + sb * AX, ue + sb, G0 + sb, G1 + sb,
+                                               none + sb, ps, ma + q0 + sb * AX, m0 + sb);
+            } else {
+                pair_terms<false, true, 0>(ub + q0, ma + q0, ue, m0, G0, G1, none, ps);
+            }
         }
     } else if (tile_full) {
 #pragma unroll
