@@ -34,6 +34,9 @@ def child(args):
     if v0.any():
         z = np.zeros(s.n_dof)
         s.set_state(z, v0, z)
+    for o in args.opt:
+        k, v = o.split("=")
+        s.set_option(int(k), int(v))
     s.initial_acceleration(sc.load_scale(0.0))
     s.step(sc.scales(1, args.warmup))
     step0 = args.warmup + 1
@@ -60,6 +63,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="pmts_pd_set_option ID=VALUE")
     ap.add_argument("variants", nargs="*")
     args = ap.parse_args()
     if args.child:
@@ -69,7 +73,7 @@ def main():
         env = dict(os.environ, PMTS_LIB_PATH=os.path.abspath(path))
         cmd = [sys.executable, os.path.abspath(__file__), "--child", "--workload", args.workload,
                "--mode", args.mode, "--steps", str(args.steps), "--warmup", str(args.warmup),
-               "--reps", str(args.reps)]
+               "--reps", str(args.reps)] + [x for o in args.opt for x in ("--opt", o)]
         p = subprocess.run(cmd, env=env, capture_output=True, text=True)
         line = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else p.stderr[-400:]
         print(name, line, flush=True)
