@@ -482,7 +482,7 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
         const bool ca = ALLIN || (unsigned)(ax0 + x) <= (unsigned)nx;      // node column x in the domain
         const bool cb = ALLIN || (unsigned)(ax0 + x + 1) <= (unsigned)nx;  // node column x + 1
         double2 hs[UR + 1];
-        double2 ap = make_double2(0.0, 0.0), bp = ap;
+        double2 ap = make_double2(0.0, 0.0);
         bool rp = false;
 #pragma unroll
         for (int i = 0; i <= UR; ++i) {
@@ -500,13 +500,8 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                         mxy = max(mxy, hi_abs(a.x - ap.x));
                         myy = max(myy, hi_abs(a.y - ap.y));
                     }
-                    if (x == AX - 1 && cb) {
-                        mxy = max(mxy, hi_abs(b.x - bp.x));
-                        myy = max(myy, hi_abs(b.y - bp.y));
-                    }
                 }
                 ap = a;
-                bp = b;
                 rp = rw;
             }
         }
@@ -520,15 +515,41 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                 else
                     ub[y * AX + x] = make_double2(d.Nsh * (hs[i].x + hs[i + 1].x),
                                                   d.Nsh * (hs[i].y + hs[i + 1].y));
-                if (!skip && y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
+            }
+        }
+        // (staging tiles only; a uniform branch instead of a predicate per row)
+        if (!skip) {
+#pragma unroll
+            for (int i = 0; i < UR; ++i) {
+                const int y = y0 + i;
+                if (y < MY) tile_full = tile_full && (ma[y * AX + x] & kPos) == kPos;
             }
         }
     };
+    // the y-steps of the apron's last node column (b of x = AX - 1) are taken by the threads
+    // the ubar pass leaves idle: inside the pass they were a divergent branch every warp paid
+    auto last_column = [&](auto allin) {
+        constexpr bool ALLIN = decltype(allin)::value;
+        constexpr int NI = NT - AX * NYB;
+        static_assert(NI >= 1, "idle threads for the last node column");
+        const bool cb = ALLIN || (unsigned)(ax0 + BX - 1) <= (unsigned)nx;
+        for (int p = threadIdx.x - AX * NYB; p < BY - 1; p += NI) {
+            const bool rw = ALLIN || ((unsigned)(ay0 + p) <= (unsigned)ny &&
+                                      (unsigned)(ay0 + p + 1) <= (unsigned)ny);
+            if (cb && rw) {
+                const double2 b0 = nt[p * BX + BX - 1], b1 = nt[(p + 1) * BX + BX - 1];
+                mxy = max(mxy, hi_abs(b1.x - b0.x));
+                myy = max(myy, hi_abs(b1.y - b0.y));
+            }
+        }
+    };
+    const bool allin = SCREEN && ax0 >= 0 && ay0 >= 0 && ax0 + BX - 1 <= nx && ay0 + BY - 1 <= ny;
     if (threadIdx.x < AX * NYB) {
-        if (SCREEN && ax0 >= 0 && ay0 >= 0 && ax0 + BX - 1 <= nx && ay0 + BY - 1 <= ny)
-            ubar_pass(std::true_type{});
-        else
-            ubar_pass(std::false_type{});
+        if (allin) ubar_pass(std::true_type{});
+        else ubar_pass(std::false_type{});
+    } else if (SCREEN) {
+        if (allin) last_column(std::true_type{});
+        else last_column(std::false_type{});
     }
     if (SCREEN) {
         mxx = __reduce_max_sync(0xffffffffu, mxx);
@@ -607,10 +628,10 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     bool anyc[EPT];
 #pragma unroll
     for (int r = 0; r < EPT; ++r) anyc[r] = false;
+    uint32_t cand = 0;  // bit r: row r has a break candidate
     if constexpr (PAIRS) {
         // candidate break tests first, on the tiles the screen could not prove cold
         // (rolled over the rows: the registers are free before the force pass)
-        uint32_t cand = 0;
         if (DO_BREAK && hot) {
 #pragma unroll 1
             for (int r = 0; r < EPT; ++r) {
@@ -621,8 +642,6 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
                 cand |= (ac ? 1u : 0u) << r;
             }
         }
-#pragma unroll
-        for (int r = 0; r < EPT; ++r) anyc[r] = (cand >> r) & 1u;
         bool none[EPT];
         // a warp of a tile with broken or absent bonds still takes the unmasked instance
         // when every bond state its own rows read is full: the words of apron rows gy0 ..
@@ -702,9 +721,11 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     }
     const bool skip2 = red[4 * NW] != 0u;
     unsigned long long nb = 0;
-    bool anyw = false;
+    if constexpr (!PAIRS) {
 #pragma unroll
-    for (int r = 0; r < EPT; ++r) anyw |= anyc[r];
+        for (int r = 0; r < EPT; ++r) cand |= (anyc[r] ? 1u : 0u) << r;
+    }
+    const bool anyw = cand != 0u;
     // (a clean tile without a candidate in the warp has no bond state to test or write)
     if (!skip2 || __any_sync(0xffffffffu, anyw)) {
     int e[EPT];
@@ -721,8 +742,9 @@ k_tile9(DevPD d, LatticeDev L, const __grid_constant__ Stencil2D st,
     if (DO_BREAK) {  // rare: exact per-bond thresholds for the flagged elements
 #pragma unroll
         for (int r = 0; r < EPT; ++r) {
-            if (skip2 && anyc[r]) m0[r] = m[r] = bf.mask_in[e[r]];  // (a clean tile staged nothing)
-            uint32_t c = anyc[r] ? (m0[r] & kPos) : 0u;
+            const bool ac = (cand >> r) & 1u;
+            if (skip2 && ac) m0[r] = m[r] = bf.mask_in[e[r]];  // (a clean tile staged nothing)
+            uint32_t c = ac ? (m0[r] & kPos) : 0u;
             while (c) {
                 const int k = __ffs(c) - 1;
                 c &= c - 1;
